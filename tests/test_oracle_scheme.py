@@ -1,0 +1,377 @@
+"""Scheme-level pins of the oracle: exact solutions, invariants and special cases (SURVEY.md s8(c) pins table).
+
+free-stream (bitwise), conservation across coarse/fine faces (1e-12, BJ north_star), SSP-RK3 temporal
+order, spatial order on a smooth wave, Sod vs the exact Riemann solution (O16), closed-form isentropic
+vortex (O17), mirror / transpose symmetry, ghost fill (O7), prolongation / restriction (O8, O9).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import workloads as W
+from tests import exact_riemann as ER
+
+
+def run_init(o, cfg, regrids=None):
+    """A28: set_state, then (levels-1) x [regrid -> set_state]."""
+    fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+    o.set_state(fn)
+    for _ in range(cfg["levels"] - 1 if regrids is None else regrids):
+        o.regrid()
+        o.set_state(fn)
+
+
+def rel_change(a, b, scale):
+    """|a-b| / (sum |U_k| dV) per component (O18); an identically-zero component uses the largest scale."""
+    scale = np.where(scale > 0, scale, scale.max())
+    return np.abs(a - b) / scale
+
+
+# ----------------------------------------------------------------------------- free stream
+@pytest.mark.parametrize("scheme,char", [("central4", 1), ("weno5", 1), ("weno5", 0)])
+@pytest.mark.parametrize("bcname", ["periodic", "mixed"])
+def test_free_stream_bitwise_on_amr_mesh(scheme, char, bcname):
+    """Uniform U on any valid tree and BC is preserved bitwise (identical face fluxes, zero MC slopes,
+    (4a)/4 = a restriction)."""
+    bc = ("periodic",) * 4 if bcname == "periodic" else ("transmissive", "transmissive", "reflective", "reflective")
+    state = (1.3, 0.4, -0.25, 0.9) if bcname == "periodic" else (1.3, 0.4, 0.0, 0.9)
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(32, 32), n=8, levels=3, bc=bc, scheme=scheme,
+               characteristic=char, div_order=4, ic="uniform", uniform_state=state)
+    o = orc.Oracle(cfg)
+    o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    o.regrid_with_requests([(0, 1, 1), (0, 2, 1), (0, 0, 3)])
+    o.regrid_with_requests([(1, 3, 3), (1, 2, 2)])
+    o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    before = o.get_state()
+    assert len({k[0] for k in before}) == 3
+    for _ in range(3):
+        o.step(cfl=0.5)
+    after = o.get_state()
+    for k in before:
+        assert np.array_equal(before[k], after[k]), k
+
+
+# ----------------------------------------------------------------------------- conservation
+def _totals_scale(o):
+    st = o.get_state()
+    tr = o.tree()
+    s = np.zeros(4)
+    for (l, P, Q, lf) in tr:
+        if lf:
+            dv = ((o.cfg["hi"][0] - o.cfg["lo"][0]) / (o.cfg["base"][0] << l)) * \
+                 ((o.cfg["hi"][1] - o.cfg["lo"][1]) / (o.cfg["base"][1] << l))
+            s += np.abs(st[(l, P, Q)]).sum(axis=(1, 2)) * dv
+    return s
+
+
+@pytest.mark.parametrize("scheme", ["central4", "weno5"])
+def test_conservation_periodic_uniform(scheme):
+    cfg = W.vortex(N=64, n=16, scheme=scheme)
+    o = orc.Oracle(cfg)
+    run_init(o, cfg)
+    t0, sc = o.totals(), _totals_scale(o)
+    for _ in range(10):
+        o.step(cfl=0.5)
+    assert np.all(rel_change(o.totals(), t0, sc) < 1e-12)
+
+
+@pytest.mark.parametrize("scheme", ["central4", "weno5"])
+def test_conservation_periodic_amr_with_regrid(scheme):
+    """BJ north_star: totals to 1e-12 relative across coarse/fine interfaces (reflux O12 + restriction O9),
+    including regrids (conservative prolongation O8)."""
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(32, 32), n=8, levels=3, bc=("periodic",) * 4,
+               scheme=scheme, characteristic=1, div_order=4, ic="blast", blast_width=0.08,
+               theta=0.02, coarsen_frac=0.25, weno_eps=1e-6, gamma=1.4)
+    o = orc.Oracle(cfg)
+    run_init(o, cfg)
+    assert len({l for (l, _, _, lf) in o.tree() if lf}) == 3
+    t0, sc = o.totals(), _totals_scale(o)
+    for s in range(1, 11):
+        o.step(cfl=0.4)
+        if s % 4 == 0:
+            o.regrid()
+    assert np.all(rel_change(o.totals(), t0, sc) < 1e-12), rel_change(o.totals(), t0, sc)
+
+
+def test_reflux_is_what_makes_amr_conservative():
+    """Reflux pin (O12): a 1D-like strip with one static refined patch and a smooth moving wave.  Without the
+    correction the coarse and fine sides would disagree by O(dt h^4) per stage at the two C/F faces; with it
+    the leaf totals telescope to rounding (<= 1e-13 relative)."""
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 0.25), base=(32, 8), n=8, levels=2, bc=("periodic",) * 4,
+               scheme="weno5", characteristic=1, div_order=4, ic="smooth", amp=0.3, u0=0.8, v0=0.0)
+    o = orc.Oracle(cfg)
+    o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    o.regrid_with_requests([(0, 1, 0)])
+    o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    t0, sc = o.totals(), _totals_scale(o)
+    for _ in range(5):
+        o.step(cfl=0.5)
+    assert np.all(rel_change(o.totals(), t0, sc) < 1e-13)
+
+
+# ----------------------------------------------------------------------------- temporal / spatial order
+def _wave_cfg(N, scheme, n=16, char=1):
+    return dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(N, N), n=n, levels=1, bc=("periodic",) * 4, scheme=scheme,
+                characteristic=char, div_order=4, ic="smooth", amp=0.2, u0=1.0, v0=0.5, gamma=1.4)
+
+
+def _density(o, cfg):
+    st = o.get_state()
+    N = cfg["base"][0]
+    n = cfg["n"]
+    R = np.zeros((N, N))
+    for (l, P, Q), U in st.items():
+        R[Q * n:(Q + 1) * n, P * n:(P + 1) * n] = U[0]
+    return R
+
+
+def test_ssprk3_temporal_order():
+    """spatial error frozen (fixed grid), halving dt cuts the error 8x (+-25 %)."""
+    cfg = _wave_cfg(32, "central4")
+    T = 0.1
+
+    def run(K):
+        o = orc.Oracle(cfg)
+        o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+        for _ in range(K):
+            o.step(dt=T / K)
+        return _density(o, cfg)
+
+    ref = run(640)
+    e = [np.abs(run(K) - ref).max() for K in (20, 40, 80)]
+    r1, r2 = e[0] / e[1], e[1] / e[2]
+    assert 6.0 < r1 < 10.0 and 6.0 < r2 < 10.0, (e, r1, r2)
+
+
+def _wave_error(N, scheme, char=1):
+    cfg = _wave_cfg(N, scheme, n=16, char=char)
+    o = orc.Oracle(cfg)
+    o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    T = 0.05
+    h = 1.0 / N
+    K = int(math.ceil(T / (0.5 * h ** (4.0 / 3.0))))
+    for _ in range(K):
+        o.step(dt=T / K)
+    R = _density(o, cfg)
+    x = (np.arange(N) + 0.5) * h
+    X, Y = np.meshgrid(x, x)
+    exact = 1.0 + 0.2 * np.sin(2 * np.pi * (X - 1.0 * T)) * np.cos(2 * np.pi * (Y - 0.5 * T))
+    return np.abs(R - exact).mean()
+
+
+@pytest.mark.parametrize("scheme,char,min_order", [("central4", 1, 3.5), ("weno5", 1, 3.0), ("weno5", 0, 3.0)])
+def test_spatial_order_smooth_wave(scheme, char, min_order):
+    """observed order on a smooth advected density wave: Central4 >= 3.5, WENO5 >= 3.0."""
+    e1 = _wave_error(32, scheme, char)
+    e2 = _wave_error(64, scheme, char)
+    order = math.log2(e1 / e2)
+    assert order >= min_order, (e1, e2, order)
+
+
+# ----------------------------------------------------------------------------- exact solutions
+@pytest.mark.slow
+def test_sod_against_exact_riemann_two_levels():
+    """BJ configs[0] with A21/A23 (strip embedding, n = 8 rows): L1(rho) on [0,1] at t = 0.2 vs O16."""
+    cfg = dict(W.sod(), base=(208, 8), n=8, hi=(1.04, 0.04))
+    o = orc.Oracle(cfg)
+    run_init(o, cfg)
+    t, step = 0.0, 0
+    while t < 0.2 - 1e-15:
+        lam = o.lam()
+        dt = min(0.5 / lam, 0.2 - t)
+        o.step(dt=dt)
+        t += dt
+        step += 1
+        if step % 4 == 0:
+            o.regrid()
+    # composite leaf density along x (all rows identical: y-fluxes cancel exactly)
+    xs, rho = [], []
+    for (l, P, Q, lf) in o.tree():
+        if lf and Q == 0:
+            U = o.get_patch((l, P, Q))
+            X, Y = W.cell_centres(cfg, l, P, Q)
+            assert np.all(U[0] == U[0][0:1, :])          # rows identical
+            xs.append(X[0]); rho.append(U[0][0])
+            dx = 0.005 / (1 << l)
+            xs[-1] = (xs[-1], dx)
+    err, length = 0.0, 0.0
+    for (X, dx), r in zip(xs, rho):
+        m = X < 1.0
+        ex, _, _ = ER.sample(1.0, 0.0, 1.0, 0.125, 0.0, 0.1, (X[m] - 0.5) / 0.2)
+        err += np.sum(np.abs(r[m] - ex)) * dx
+    assert err < 0.01, err
+    assert max(r.max() for r in rho) < 1.0 + 0.01 * 0.875
+    assert min(r.min() for r in rho) > 0.125 - 0.01 * 0.875
+
+
+def test_exact_riemann_star_state_matches_published():
+    import json
+    import os
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "sod_star_state.json")))
+    ps, us = ER.star_state(*d["left"], *d["right"])
+    assert round(ps, 5) == d["p_star"] and round(us, 5) == d["u_star"]
+    r, u, p = ER.sample(*d["left"], *d["right"], np.array([us - 1e-9, us + 1e-9]))
+    assert round(r[0], 5) == d["rho_star_left"] and round(r[1], 5) == d["rho_star_right"]
+
+
+def test_isentropic_vortex_closed_form():
+    """O17 / BJ configs[1] at reduced size: after 20 CFL-0.5 steps the density matches the advected closed form;
+    the error falls by >= 2^3.5 from 64^2 to 128^2 on the [0,20]^2 variant (A30)."""
+    errs = []
+    for N in (64, 128):
+        cfg = W.vortex(N=N, n=16, L=20.0)
+        o = orc.Oracle(cfg)
+        o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+        t = 0.0
+        h = 20.0 / N
+        dt = 0.1 * h
+        K = int(round(1.0 / dt))
+        for _ in range(K):
+            o.step(dt=1.0 / K)
+        R = _density(o, cfg)
+        x = (np.arange(N) + 0.5) * h
+        X, Y = np.meshgrid(x, x)
+        ex = W.vortex_prim(cfg, X, Y, t=1.0)[0]
+        errs.append(np.abs(R - ex).max())
+    assert errs[0] / errs[1] > 2 ** 3.5, errs
+    assert errs[1] < 2e-3
+
+
+# ----------------------------------------------------------------------------- symmetry
+def _quadrant_small(scheme="weno5"):
+    return W.quadrant(N=64, n=16, levels=2, seed=3, scheme=scheme, theta=0.1)
+
+
+def _mirror_cfg_fn(cfg, kind):
+    def fn(l, P, Q):
+        n = cfg["n"]
+        NPx = (cfg["base"][0] // n) << l
+        if kind == "x":
+            U = W.patch_state(cfg, l, NPx - 1 - P, Q)[:, :, ::-1].copy()
+            U[1] = -U[1]
+            return U
+        U = W.patch_state(cfg, l, Q, P).transpose(0, 2, 1)[[0, 2, 1, 3]].copy()
+        return U
+    return fn
+
+
+@pytest.mark.parametrize("kind", ["x", "transpose"])
+def test_quadrant_mirror_and_transpose_symmetry(kind):
+    """Mirror x -> 1-x with u -> -u (and the transpose x <-> y, u <-> v) of the quadrant IC gives the mirrored
+    result, with regrids (trees mirror too)."""
+    cfg = _quadrant_small()
+    a = orc.Oracle(cfg)
+    b = orc.Oracle(cfg)
+    fa = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+    fb = _mirror_cfg_fn(cfg, kind)
+    for o, f in ((a, fa), (b, fb)):
+        o.set_state(f); o.regrid(); o.set_state(f)
+    for s in range(1, 7):
+        a.step(cfl=0.5)
+        b.step(cfl=0.5)
+        if s % 4 == 0:
+            a.regrid(); b.regrid()
+    sa, sb = a.get_state(), b.get_state()
+    scale = np.array([np.abs(U[k]).max() for U in sa.values() for k in range(4)]).reshape(-1, 4).max(axis=0)
+    for (l, P, Q), U in sa.items():
+        NPx = (cfg["base"][0] // cfg["n"]) << l
+        if kind == "x":
+            V = sb[(l, NPx - 1 - P, Q)][:, :, ::-1].copy()
+            V[1] = -V[1]
+        else:
+            V = sb[(l, Q, P)].transpose(0, 2, 1)[[0, 2, 1, 3]]
+        for k in range(4):
+            assert np.abs(U[k] - V[k]).max() <= 1e-12 * scale[k], (kind, l, P, Q, k)
+
+
+# ----------------------------------------------------------------------------- ghost fill (O7)
+def test_ghost_periodic_same_level_matches_global_roll():
+    cfg = W.sweep(N=64, n=16, seed=11)
+    o = orc.Oracle(cfg)
+    U0 = W.level0_state(cfg)                      # [NPy][NPx][4][n][n]
+    o.set_state(lambda l, P, Q: U0[Q, P])
+    n, g = 16, 4
+    G = U0.transpose(2, 0, 3, 1, 4).reshape(4, 64, 64)   # [4][J][I]
+    for (P, Q) in [(0, 0), (3, 1), (2, 3)]:
+        t = o.ghost_tile((0, P, Q), g)
+        for k in range(4):
+            Jr = np.arange(Q * n - g, Q * n + n + g) % 64
+            Ir = np.arange(P * n - g, P * n + n + g) % 64
+            ref = G[k][np.ix_(Jr, Ir)]
+            body = np.s_[g:g + n]
+            assert np.array_equal(t[k][body, :], ref[body, :])
+            assert np.array_equal(t[k][:, body], ref[:, body])
+            assert np.all(np.isnan(t[k][:g, :g]))     # corners are not defined (A26)
+
+
+@pytest.mark.parametrize("bc", ["transmissive", "reflective"])
+def test_ghost_physical_boundaries(bc):
+    cfg = dict(W.sweep(N=32, n=16, seed=5), bc=(bc,) * 4)
+    o = orc.Oracle(cfg)
+    U0 = W.level0_state(cfg)
+    o.set_state(lambda l, P, Q: U0[Q, P])
+    g = 4
+    t = o.ghost_tile((0, 0, 0), g)
+    U = U0[0, 0]
+    for k in range(4):
+        west = t[k][g:g + 16, 0:g]
+        south = t[k][0:g, g:g + 16]
+        if bc == "transmissive":
+            assert np.array_equal(west, np.repeat(U[k][:, :1], g, axis=1))
+            assert np.array_equal(south, np.repeat(U[k][:1, :], g, axis=0))
+        else:
+            sx = -1.0 if k == 1 else 1.0
+            sy = -1.0 if k == 2 else 1.0
+            assert np.array_equal(west, sx * U[k][:, g - 1::-1])
+            assert np.array_equal(south, sy * U[k][g - 1::-1, :])
+
+
+def test_coarse_fine_ghost_and_prolongation_exact_on_linear_data():
+    """O8: MC picks the central slope on linear data, so prolonged values (C/F ghosts and new patches) equal
+    the linear function at fine centres; children's mean equals the parent; restrict(prolong) = identity."""
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(32, 32), n=8, levels=2, bc=("transmissive",) * 4,
+               scheme="weno5", ic="uniform")
+    o = orc.Oracle(cfg)
+    lin = lambda X, Y: np.stack([1.0 + 0.3 * X - 0.2 * Y, 0.1 + 0.5 * Y, 0.2 - 0.1 * X, 2.5 + 0.05 * X])  # noqa
+
+    def fn(l, P, Q):
+        X, Y = W.cell_centres(cfg, l, P, Q)
+        return lin(X, Y)
+
+    o.set_state(fn)
+    parent_before = o.get_patch((0, 1, 1))
+    o.regrid_with_requests([(0, 1, 1)])
+    for a in (0, 1):
+        for b in (0, 1):
+            k = (1, 2 + a, 2 + b)
+            X, Y = W.cell_centres(cfg, *k)
+            np.testing.assert_allclose(o.get_patch(k), lin(X, Y), rtol=1e-14, atol=1e-14)
+    np.testing.assert_allclose(o.get_patch((0, 1, 1)), parent_before, rtol=1e-15, atol=1e-15)
+    # C/F ghost strip of a fine leaf facing coarse leaves: west strip of (1,2,2) lies in root (0,0,1)
+    g = 4
+    t = o.ghost_tile((1, 2, 2), g)
+    h = 1.0 / 64
+    I = np.arange(2 * 8 - g, 2 * 8)
+    J = np.arange(2 * 8, 3 * 8)
+    Xg, Yg = np.meshgrid((I + 0.5) * h, (J + 0.5) * h)
+    np.testing.assert_allclose(t[:, g:g + 8, 0:g], lin(Xg, Yg), rtol=1e-14, atol=1e-14)
+
+
+def test_prolong_mean_and_restrict_round_trip_random():
+    cfg = dict(W.sweep(N=32, n=8, seed=9), bc=("periodic",) * 4, levels=2)
+    o = orc.Oracle(cfg)
+    U0 = W.level0_state(cfg)
+    o.set_state(lambda l, P, Q: U0[Q, P])
+    before = o.get_patch((0, 2, 1))
+    o.regrid_with_requests([(0, 2, 1)])
+    kids = {(a, b): o.get_patch((1, 4 + a, 2 + b)) for a in (0, 1) for b in (0, 1)}
+    fine = np.zeros((4, 16, 16))
+    for (a, b), U in kids.items():
+        fine[:, b * 8:(b + 1) * 8, a * 8:(a + 1) * 8] = U
+    mean = 0.25 * (fine[:, 0::2, 0::2] + fine[:, 0::2, 1::2] + fine[:, 1::2, 0::2] + fine[:, 1::2, 1::2])
+    coarse_region = np.zeros((4, 8, 8))
+    coarse_region[:] = before[:, :, :]
+    np.testing.assert_allclose(mean, coarse_region, rtol=1e-14, atol=1e-14)
+    np.testing.assert_allclose(o.get_patch((0, 2, 1)), before, rtol=1e-15, atol=1e-15)
