@@ -1,0 +1,296 @@
+"""B200-native AMR compressible-Euler hot path of arXiv 2508.05020 -- Python binding.
+
+Argument marshalling only: every step of the numerical path runs in the sm_100a
+kernels of ``libamr.so`` behind the C ABI declared in ``include/amr.h``.  There is
+no CPU fallback: importing works without a GPU (so the ABI can be inspected), but
+creating a mesh needs the CUDA library and a device and raises otherwise.
+PyTorch is used only for device memory (optional ``pool`` tensor), streams and
+process groups (NCCL unique-id broadcast).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libamr.so")
+
+AMR_OK, AMR_E_ARG, AMR_E_CONFIG, AMR_E_NONPHYSICAL, AMR_E_MESH, AMR_E_CAPACITY, AMR_E_CUDA, AMR_E_COMM, \
+    AMR_E_STATE = range(9)
+STATUS = {0: "AMR_OK", 1: "AMR_E_ARG", 2: "AMR_E_CONFIG", 3: "AMR_E_NONPHYSICAL", 4: "AMR_E_MESH",
+          5: "AMR_E_CAPACITY", 6: "AMR_E_CUDA", 7: "AMR_E_COMM", 8: "AMR_E_STATE"}
+BC = {"periodic": 0, "transmissive": 1, "reflective": 2}
+SCHEME = {"central4": 0, "weno5": 1}
+COARSEN = {"r2_exact": 0, "alg2_literal": 1}
+
+# every symbol include/amr.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ["amr_abi_version", "amr_default_config", "amr_query_pool_bytes", "amr_create", "amr_destroy",
+               "amr_set_state", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
+               "amr_regrid", "amr_regrid_with_flags", "amr_get_patch_tree", "amr_diagnostics",
+               "amr_set_kernel_timing", "amr_get_stats", "amr_reset_stats", "amr_last_error"]
+
+
+class amr_config(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("lo", C.c_double * 2), ("hi", C.c_double * 2),
+                ("base_cells", C.c_int32 * 2), ("patch_cells", C.c_int32), ("num_levels", C.c_int32),
+                ("ratio", C.c_int32), ("gamma", C.c_double), ("bc", C.c_int32 * 4), ("scheme", C.c_int32),
+                ("weno_characteristic", C.c_int32), ("div_order", C.c_int32), ("weno_eps", C.c_double),
+                ("refine_threshold", C.c_double), ("coarsen_fraction", C.c_double), ("coarsen_rule", C.c_int32),
+                ("max_patches", C.c_int32), ("pool", C.c_void_p), ("pool_bytes", C.c_uint64),
+                ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("world_size", C.c_int32),
+                ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("check_positivity", C.c_int32),
+                ("use_graphs", C.c_int32)]
+
+
+class amr_patch_desc(C.Structure):
+    _fields_ = [("level", C.c_int32), ("i", C.c_int32), ("j", C.c_int32), ("parent", C.c_int32),
+                ("child", C.c_int32 * 4), ("nbr", C.c_int32 * 8), ("owner", C.c_int32),
+                ("leaf", C.c_uint8), ("refine_req", C.c_uint8), ("coarsen_req", C.c_uint8),
+                ("ambiguous", C.c_uint8)]
+
+
+class amr_stats(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("stage_launches", C.c_int64), ("stage_ms", C.c_double),
+                ("stage_timed", C.c_int64), ("stage_cells", C.c_int64), ("stage_bytes", C.c_double),
+                ("steps", C.c_int64), ("leaf_cells", C.c_int64), ("leaves", C.c_int64), ("patches", C.c_int64),
+                ("proxies", C.c_int64)]
+
+
+_lib = None
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_I32 = C.POINTER(C.c_int32)
+_U8 = C.POINTER(C.c_uint8)
+
+
+def load(path: str = LIB_PATH):
+    """Load libamr.so (build it first with ``python -m paper_2508_05020_b200.build``); raises if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA library {path} is missing: run `python -m paper_2508_05020_b200.build` "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    L.amr_abi_version.restype = C.c_int32
+    L.amr_default_config.argtypes = [C.POINTER(amr_config)]
+    L.amr_query_pool_bytes.argtypes = [C.POINTER(amr_config), C.POINTER(C.c_uint64)]
+    L.amr_create.argtypes = [C.POINTER(amr_config), C.POINTER(_P)]
+    L.amr_destroy.argtypes = [_P]
+    L.amr_destroy.restype = None
+    L.amr_set_state.argtypes = [_P, C.c_int32, _I32, _D]
+    L.amr_get_state.argtypes = [_P, C.c_int32, _I32, _D]
+    L.amr_set_state_device.argtypes = [_P, C.c_int32, _I32, C.c_void_p]
+    L.amr_get_state_device.argtypes = [_P, C.c_int32, _I32, C.c_void_p]
+    L.amr_step.argtypes = [_P, C.c_double, C.c_double, _D]
+    L.amr_steps.argtypes = [_P, C.c_int32, C.c_double, C.c_double]
+    L.amr_sync.argtypes = [_P]
+    L.amr_get_flags.argtypes = [_P, C.c_int32, _D, _U8]
+    L.amr_regrid.argtypes = [_P, _I32, _I32]
+    L.amr_regrid_with_flags.argtypes = [_P, C.c_int32, _I32, _U8, _I32, _I32]
+    L.amr_get_patch_tree.argtypes = [_P, C.POINTER(amr_patch_desc), C.c_int32, _I32]
+    L.amr_diagnostics.argtypes = [_P, _D, _D]
+    L.amr_set_kernel_timing.argtypes = [_P, C.c_int32]
+    L.amr_get_stats.argtypes = [_P, C.POINTER(amr_stats)]
+    L.amr_reset_stats.argtypes = [_P]
+    L.amr_last_error.argtypes = [_P]
+    L.amr_last_error.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+class AmrError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def make_config(cfg: dict, **over) -> amr_config:
+    """Marshal a workload dict (see workloads/) into the ABI's amr_config."""
+    L = load()
+    c = amr_config()
+    L.amr_default_config(C.byref(c))
+    c.dim = int(cfg.get("dim", 2))
+    c.lo[0], c.lo[1] = cfg["lo"]
+    c.hi[0], c.hi[1] = cfg["hi"]
+    c.base_cells[0], c.base_cells[1] = cfg["base"]
+    c.patch_cells = cfg["n"]
+    c.num_levels = cfg["levels"]
+    c.ratio = 2
+    c.gamma = cfg.get("gamma", 1.4)
+    for e, b in enumerate(cfg["bc"]):
+        c.bc[e] = BC[b]
+    c.scheme = SCHEME[cfg["scheme"]]
+    c.weno_characteristic = int(cfg.get("characteristic", 1))
+    c.div_order = int(cfg.get("div_order", 4))
+    c.weno_eps = cfg.get("weno_eps", 1e-6)
+    c.refine_threshold = cfg.get("theta", 0.1)
+    c.coarsen_fraction = cfg.get("coarsen_frac", 0.25)
+    c.coarsen_rule = COARSEN[cfg.get("coarsen_rule", "r2_exact")]
+    roots = (cfg["base"][0] // cfg["n"]) * (cfg["base"][1] // cfg["n"])
+    full = sum(4 ** l for l in range(cfg["levels"]))          # every root refined to the finest level
+    c.max_patches = int(cfg.get("max_patches", max(16, roots * full)))
+    c.check_positivity = int(cfg.get("check_positivity", 1))
+    c.world_size = 1
+    c.rank = 0
+    c.device = -1
+    for k, v in over.items():
+        setattr(c, k, v)
+    return c
+
+
+class Mesh:
+    """One composite AMR mesh on one GPU (one rank), advanced by the CUDA path."""
+
+    def __init__(self, cfg: dict, stream=None, pool=None, **over):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2508_05020_b200.Mesh needs a CUDA device (no CPU fallback)")
+        self.L = load()
+        self.cfg = dict(cfg)
+        self.n = cfg["n"]
+        self._keep = []
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        if stream.cuda_stream == 0:
+            # the legacy default stream cannot be named through the ABI (NULL = library stream):
+            # give the mesh its own torch stream so events recorded on `mesh.stream` bracket its kernels
+            stream = torch.cuda.Stream()
+        self.stream = stream
+        over.setdefault("cuda_stream", stream.cuda_stream)
+        over.setdefault("device", torch.cuda.current_device())
+        c = make_config(cfg, **over)
+        if pool == "torch":
+            need = C.c_uint64()
+            self.L.amr_query_pool_bytes(C.byref(c), C.byref(need))
+            t = torch.empty(int(need.value), dtype=torch.uint8, device="cuda")
+            self._keep.append(t)
+            c.pool = t.data_ptr()
+            c.pool_bytes = need.value
+        self._c = c
+        h = _P()
+        rc = self.L.amr_create(C.byref(c), C.byref(h))
+        if rc != AMR_OK:
+            raise AmrError(rc, "amr_create failed (see stderr)")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.amr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _chk(self, rc):
+        if rc != AMR_OK:
+            raise AmrError(rc, self.L.amr_last_error(self.h).decode())
+
+    # ---- tree
+    def tree(self):
+        cnt = C.c_int32()
+        self.L.amr_get_patch_tree(self.h, None, 0, C.byref(cnt))
+        arr = (amr_patch_desc * max(1, cnt.value))()
+        self._chk(self.L.amr_get_patch_tree(self.h, arr, cnt.value, C.byref(cnt)))
+        return arr[:cnt.value]
+
+    def keys(self):
+        return [(d.level, d.i, d.j) for d in self.tree()]
+
+    def leaves(self):
+        return [(d.level, d.i, d.j) for d in self.tree() if d.leaf]
+
+    # ---- state
+    def set_state(self, fn=None, U=None):
+        """Set every patch from fn(l, P, Q) -> U[4][n][n], or from U[npatch][4][n][n] in tree order."""
+        tr = self.tree()
+        m = len(tr)
+        if U is None:
+            U = np.empty((m, 4, self.n, self.n))
+            for e, d in enumerate(tr):
+                U[e] = fn(d.level, d.i, d.j)
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        idx = np.arange(m, dtype=np.int32)
+        self._chk(self.L.amr_set_state(self.h, m, idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
+
+    def set_state_device(self, tensor):
+        """Set every patch (tree order) from a contiguous CUDA float64 tensor [npatch][4][n][n]."""
+        m = len(self.tree())
+        assert tensor.is_cuda and tensor.dtype.is_floating_point and tensor.is_contiguous()
+        assert tensor.numel() == m * 4 * self.n * self.n
+        idx = np.arange(m, dtype=np.int32)
+        self._chk(self.L.amr_set_state_device(self.h, m, idx.ctypes.data_as(_I32), tensor.data_ptr()))
+
+    def get_state_device(self, tensor):
+        m = len(self.tree())
+        assert tensor.is_cuda and tensor.is_contiguous() and tensor.numel() == m * 4 * self.n * self.n
+        idx = np.arange(m, dtype=np.int32)
+        self._chk(self.L.amr_get_state_device(self.h, m, idx.ctypes.data_as(_I32), tensor.data_ptr()))
+
+    def get_state(self, as_dict=True):
+        tr = self.tree()
+        m = len(tr)
+        U = np.empty((m, 4, self.n, self.n))
+        idx = np.arange(m, dtype=np.int32)
+        self._chk(self.L.amr_get_state(self.h, m, idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
+        if not as_dict:
+            return U
+        return {(d.level, d.i, d.j): U[e] for e, d in enumerate(tr)}
+
+    # ---- stepping
+    def step(self, dt=0.0, cfl=0.0, want_dt=True):
+        d = C.c_double()
+        self._chk(self.L.amr_step(self.h, float(dt), float(cfl), C.byref(d) if want_dt else None))
+        return d.value if want_dt else None
+
+    def steps(self, k, dt=0.0, cfl=0.0):
+        self._chk(self.L.amr_steps(self.h, int(k), float(dt), float(cfl)))
+
+    def sync(self):
+        self._chk(self.L.amr_sync(self.h))
+
+    # ---- AMR
+    def flags(self):
+        tr = self.tree()
+        m = len(tr)
+        me = np.zeros(m)
+        bits = np.zeros(m, np.uint8)
+        self._chk(self.L.amr_get_flags(self.h, m, me.ctypes.data_as(_D), bits.ctypes.data_as(_U8)))
+        return {(d.level, d.i, d.j): (float(me[e]), bool(bits[e] & 1), bool(bits[e] & 2), bool(bits[e] & 4))
+                for e, d in enumerate(tr)}
+
+    def regrid(self):
+        nr, nc = C.c_int32(), C.c_int32()
+        self._chk(self.L.amr_regrid(self.h, C.byref(nr), C.byref(nc)))
+        return nr.value, nc.value
+
+    def regrid_with_requests(self, refine_keys=(), coarsen_keys=()):
+        pos = {k: e for e, k in enumerate(self.keys())}
+        keys = sorted(set(refine_keys) | set(coarsen_keys))
+        rs, cs = set(refine_keys), set(coarsen_keys)
+        idx = np.array([pos[k] for k in keys], np.int32)
+        bits = np.array([(k in rs) | ((k in cs) << 1) for k in keys], np.uint8)
+        nr, nc = C.c_int32(), C.c_int32()
+        self._chk(self.L.amr_regrid_with_flags(self.h, len(keys), idx.ctypes.data_as(_I32),
+                                               bits.ctypes.data_as(_U8), C.byref(nr), C.byref(nc)))
+        return nr.value, nc.value
+
+    # ---- diagnostics
+    def diagnostics(self):
+        t = np.zeros(4)
+        lam = C.c_double()
+        self._chk(self.L.amr_diagnostics(self.h, t.ctypes.data_as(_D), C.byref(lam)))
+        return t, lam.value
+
+    def set_kernel_timing(self, on=True):
+        self._chk(self.L.amr_set_kernel_timing(self.h, int(on)))
+
+    def stats(self):
+        s = amr_stats()
+        self._chk(self.L.amr_get_stats(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in amr_stats._fields_}
+
+    def reset_stats(self):
+        self._chk(self.L.amr_reset_stats(self.h))

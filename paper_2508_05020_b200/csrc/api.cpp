@@ -1,0 +1,931 @@
+// api.cpp -- the C ABI of include/amr.h: context, host plan (descriptor build from
+// the patch tree), step driver, regrid, state I/O, diagnostics and statistics.
+// Every step of the numerical path runs in the kernels of kernels.cu; the host
+// only orders launches and builds the descriptor lists (PAPER.md s3, Fig. 2).
+#include "../../include/amr.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+
+using namespace amr;
+
+namespace {
+
+amr_status fail(amr_ctx* c, amr_status s, const std::string& m) {
+    if (c) {
+        c->err = m;
+        if (s == AMR_E_CUDA || s == AMR_E_COMM) c->sticky = s;
+    }
+    return s;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(c, AMR_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+amr_status check(amr_ctx* c) {
+    if (!c) return AMR_E_ARG;
+    if (c->sticky != AMR_OK) {
+        c->err = "context unusable after an earlier CUDA/NCCL error";
+        return AMR_E_STATE;
+    }
+    return AMR_OK;
+}
+
+amr_status validate_config(const amr_config* cfg, std::string& m) {
+    const amr_config& c = *cfg;
+    int n = c.patch_cells;
+    if (!(n == 8 || n == 16 || n == 32 || n == 64)) { m = "patch_cells must be 8, 16, 32 or 64"; return AMR_E_CONFIG; }
+    if (c.base_cells[0] <= 0 || c.base_cells[1] <= 0 || c.base_cells[0] % n || c.base_cells[1] % n) {
+        m = "base_cells must be positive multiples of patch_cells"; return AMR_E_CONFIG;
+    }
+    if (c.ratio != 2) { m = "refinement ratio must be 2 (quadtree)"; return AMR_E_CONFIG; }
+    if (c.num_levels < 1 || c.num_levels > kMaxLevels - 1) { m = "num_levels out of range"; return AMR_E_CONFIG; }
+    if ((int64_t)c.base_cells[0] << (c.num_levels - 1) >= (int64_t(1) << 30) ||
+        (int64_t)c.base_cells[1] << (c.num_levels - 1) >= (int64_t(1) << 30)) { m = "mesh too large"; return AMR_E_CONFIG; }
+    if (!(c.gamma > 1.0)) { m = "gamma must exceed 1"; return AMR_E_CONFIG; }
+    for (int s = 0; s < 4; ++s)
+        if (c.bc[s] < 0 || c.bc[s] > 2) { m = "bad boundary condition"; return AMR_E_CONFIG; }
+    for (int ax = 0; ax < 2; ++ax)
+        if ((c.bc[2 * ax] == AMR_BC_PERIODIC) != (c.bc[2 * ax + 1] == AMR_BC_PERIODIC)) {
+            m = "periodic boundary must be set on both sides of an axis"; return AMR_E_CONFIG;
+        }
+    if (c.scheme != AMR_CENTRAL4 && c.scheme != AMR_WENO5_RUSANOV) { m = "bad scheme"; return AMR_E_CONFIG; }
+    if (c.div_order != 2 && c.div_order != 4) { m = "div_order must be 2 or 4"; return AMR_E_CONFIG; }
+    if (!(c.hi[0] > c.lo[0]) || !(c.hi[1] > c.lo[1])) { m = "empty domain"; return AMR_E_CONFIG; }
+    if (c.dim != 1 && c.dim != 2) { m = "dim must be 1 or 2"; return AMR_E_CONFIG; }
+    if (c.dim == 1 && (c.base_cells[1] != n || c.bc[2] != AMR_BC_PERIODIC)) {
+        m = "dim 1 needs one periodic row of patches (strip embedding)"; return AMR_E_CONFIG;
+    }
+    if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) { m = "bad world_size / rank"; return AMR_E_CONFIG; }
+    if (c.world_size > 1 && !c.nccl_unique_id) { m = "world_size > 1 needs nccl_unique_id"; return AMR_E_CONFIG; }
+    if (c.refine_threshold < 0 || c.coarsen_fraction < 0) { m = "bad thresholds"; return AMR_E_CONFIG; }
+    if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
+    return AMR_OK;
+}
+
+// ------------------------------------------------------------------ plan
+amr_status build_plan(amr_ctx* c) {
+    PatchTree& t = c->tree;
+    const int L = c->cfg.num_levels;
+    c->canon = t.canonical();
+    c->canon_pos.assign(t.capacity, -1);
+    for (size_t e = 0; e < c->canon.size(); ++e) c->canon_pos[c->canon[e]] = (int)e;
+
+    // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos
+    c->leaf_ids.clear();
+    for (int id : c->canon)
+        if (t.is_leaf(id) && c->comm.owns(c, id)) c->leaf_ids.push_back(id);
+    std::stable_sort(c->leaf_ids.begin(), c->leaf_ids.end(), [&](int a, int b) {
+        if (t.lev[a] != t.lev[b]) return t.lev[a] < t.lev[b];
+        return morton(t.pi[a], t.pj[a]) < morton(t.pi[b], t.pj[b]);
+    });
+    c->leaf_pos.assign(t.capacity, -1);
+    for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
+
+    static const int dirs[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
+    c->leaves.clear();
+    c->ptasks.clear();
+    c->rtasks.clear();
+    for (int id : c->leaf_ids) {
+        LeafDesc d{};
+        d.slot = id;
+        d.level = t.lev[id];
+        d.cf = 0;
+        RefluxTask rt{};
+        rt.leaf = (int)c->leaves.size();
+        rt.slot = id;
+        rt.level = t.lev[id];
+        rt.mask = 0;
+        for (int s = 0; s < 4; ++s) {
+            int nb = t.neighbour(id, dirs[s][0], dirs[s][1]);
+            if (nb >= 0) {
+                d.side[s] = nb;
+                if (t.has_children(nb)) {
+                    d.cf |= 1 << s;
+                    rt.mask |= 1 << s;
+                    // the two children of nb adjacent to the shared face, ordered along it
+                    int cidx[2];
+                    if (s == kW) { cidx[0] = 1; cidx[1] = 3; }
+                    else if (s == kE) { cidx[0] = 0; cidx[1] = 2; }
+                    else if (s == kS) { cidx[0] = 2; cidx[1] = 3; }
+                    else { cidx[0] = 0; cidx[1] = 1; }
+                    for (int h = 0; h < 2; ++h) {
+                        int ch = t.child[4 * nb + cidx[h]];
+                        if (ch < 0 || !t.is_leaf(ch) || c->leaf_pos[ch] < 0) return fail(c, AMR_E_MESH, "reflux: fine side is not a local leaf");
+                        rt.fine[s][h] = c->leaf_pos[ch];
+                    }
+                }
+            } else {
+                ProxyTask p{};
+                p.proxy = (int)c->ptasks.size();
+                p.slot = id;
+                p.side = s;
+                p.level = t.lev[id];
+                p.P = t.pi[id];
+                p.Q = t.pj[id];
+                if (nb == -2) {
+                    p.kind = 0;
+                    for (int q = 0; q < 9; ++q) p.coarse[q] = -1;
+                } else {
+                    p.kind = 1;
+                    d.cf |= 1 << (4 + s);
+                    int par = t.parent[id];
+                    if (par < 0) return fail(c, AMR_E_MESH, "missing same-level neighbour of a root");
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
+                            if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
+                            p.coarse[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
+                        }
+                }
+                d.side[s] = -1 - p.proxy;
+                c->ptasks.push_back(p);
+            }
+        }
+        c->leaves.push_back(d);
+        if (rt.mask) c->rtasks.push_back(rt);
+    }
+    c->rlev.assign(L, {});
+    for (int id : c->canon) {
+        if (!t.has_children(id) || !c->comm.owns(c, id)) continue;
+        RestrictTask r{};
+        r.parent = id;
+        for (int q = 0; q < 4; ++q) r.child[q] = t.child[4 * id + q];
+        c->rlev[t.lev[id] + 1].push_back(r);
+    }
+    c->leaf_cells = (int64_t)c->leaf_ids.size() * c->n * c->n;
+
+    cudaStream_t s = c->stream;
+    CU(c->d_leaves.upload(c->leaves, s));
+    CU(c->d_ptasks.upload(c->ptasks, s));
+    CU(c->d_rtasks.upload(c->rtasks, s));
+    c->d_rlev.resize(L);
+    for (int l = 0; l < L; ++l) CU(c->d_rlev[l].upload(c->rlev[l], s));
+    CU(c->proxy.reserve(std::max<size_t>(1, c->ptasks.size()) * c->PS));
+    CU(c->freg.reserve(std::max<size_t>(1, c->leaves.size()) * 16 * c->n));
+    CU(c->d_maxeta.reserve(std::max<size_t>(1, c->leaves.size())));
+    CU(c->d_amb.reserve(std::max<size_t>(1, c->leaves.size())));
+    CU(c->d_partial.reserve(4 * std::max<size_t>(1, c->leaves.size())));
+    CU(cudaStreamSynchronize(s));   // host vectors may change after return
+
+    c->st.leaves = 0;
+    for (int id : c->canon) c->st.leaves += t.is_leaf(id);
+    c->st.patches = (int64_t)c->canon.size();
+    c->st.leaf_cells = c->leaf_cells;
+    c->st.proxies = (int64_t)c->ptasks.size();
+    c->lambda_valid = false;
+    return AMR_OK;
+}
+
+AuxArgs aux(amr_ctx* c, const double* Ur, double* Uw) {
+    AuxArgs a{};
+    a.U = Ur;
+    a.Uw = Uw;
+    a.proxy = c->proxy.p;
+    a.freg = c->freg.p;
+    a.dt = c->d_dt;
+    a.gamma = c->cfg.gamma;
+    a.theta = c->cfg.refine_threshold;
+    a.coarsen_fraction = c->cfg.coarsen_fraction;
+    a.lambda_bits = c->d_lambda;
+    a.err = c->d_err;
+    a.check = c->cfg.check_positivity;
+    a.geo = c->geo;
+    return a;
+}
+
+amr_status count_launch(amr_ctx* c, cudaError_t e, const char* what) {
+    if (e != cudaSuccess) return fail(c, AMR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    c->st.launches++;
+    return AMR_OK;
+}
+
+#define LAUNCH(expr, what)                                         \
+    do {                                                           \
+        amr_status s_ = count_launch(c, (expr), what);             \
+        if (s_ != AMR_OK) return s_;                               \
+    } while (0)
+
+// restriction of every non-leaf patch, finest level first (O9)
+amr_status restrict_all(amr_ctx* c, double* Ubuf) {
+    AuxArgs a = aux(c, Ubuf, Ubuf);
+    for (int l = c->cfg.num_levels - 1; l >= 1; --l)
+        if (!c->rlev[l].empty()) LAUNCH(launch_restrict(c->d_rlev[l].p, (int)c->rlev[l].size(), a, c->stream), "restrict");
+    return AMR_OK;
+}
+
+amr_status fill_ghosts(amr_ctx* c, const double* Ubuf) {
+    if (c->ptasks.empty()) return AMR_OK;
+    AuxArgs a = aux(c, Ubuf, nullptr);
+    LAUNCH(launch_ghost(c->d_ptasks.p, (int)c->ptasks.size(), c->g, a, c->stream), "ghost");
+    return AMR_OK;
+}
+
+amr_status seed_lambda(amr_ctx* c) {
+    CU(cudaMemsetAsync(c->d_lambda, 0, sizeof(unsigned long long), c->stream));
+    amr_status s = c->comm.exchange_halos(c, c->U[c->un]);
+    if (s != AMR_OK) return s;
+    AuxArgs a = aux(c, c->U[c->un], nullptr);
+    LAUNCH(launch_lambda(c->d_leaves.p, (int)c->leaves.size(), a, c->stream), "lambda");
+    s = c->comm.allreduce_max_u64(c, c->d_lambda);
+    if (s != AMR_OK) return s;
+    c->lambda_valid = true;
+    return AMR_OK;
+}
+
+cudaEvent_t take_event(amr_ctx* c) {
+    if (c->ev_free.empty()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    cudaEvent_t e = c->ev_free.back();
+    c->ev_free.pop_back();
+    return e;
+}
+
+amr_status harvest_events(amr_ctx* c) {
+    if (c->ev_pending.empty()) return AMR_OK;
+    CU(cudaStreamSynchronize(c->stream));
+    for (size_t k = 0; k + 1 < c->ev_pending.size(); k += 2) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, c->ev_pending[k], c->ev_pending[k + 1]));
+        c->st.stage_ms += ms;
+        c->st.stage_timed++;
+        c->st.stage_cells += c->ev_cells[k / 2];
+        c->st.stage_bytes += c->ev_bytes[k / 2];
+        c->ev_free.push_back(c->ev_pending[k]);
+        c->ev_free.push_back(c->ev_pending[k + 1]);
+    }
+    c->ev_pending.clear();
+    c->ev_cells.clear();
+    c->ev_bytes.clear();
+    return AMR_OK;
+}
+
+// one SSP-RK3 step, queued on the stream without host synchronisation
+amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
+    if (!c->lambda_valid && !(dt > 0.0)) {
+        amr_status s = seed_lambda(c);
+        if (s != AMR_OK) return s;
+    }
+    LAUNCH(launch_dt(c->d_dt, c->d_lambda, c->d_err, dt, cfl, c->stream), "dt");
+    const int A = (c->un + 1) % 3, B = (c->un + 2) % 3;
+    const double as[3] = {0.0, 0.75, 1.0 / 3.0};
+    const double bs[3] = {1.0, 0.25, 2.0 / 3.0};
+    for (int s = 1; s <= 3; ++s) {
+        double* Uin = s == 1 ? c->U[c->un] : (s == 2 ? c->U[A] : c->U[B]);
+        double* Uout = s == 2 ? c->U[B] : c->U[A];
+        amr_status cs = c->comm.exchange_halos(c, Uin);
+        if (cs != AMR_OK) return cs;
+        cs = fill_ghosts(c, Uin);
+        if (cs != AMR_OK) return cs;
+        StageArgs a{};
+        a.leaves = c->d_leaves.p;
+        a.nleaves = (int)c->leaves.size();
+        a.tiles = c->n > 32 ? c->n / 32 : 1;
+        a.Uin = Uin;
+        a.Un = c->U[c->un];
+        a.Uout = Uout;
+        a.proxy = c->proxy.p;
+        a.freg = c->freg.p;
+        a.dt = c->d_dt;
+        a.a = as[s - 1];
+        a.b = bs[s - 1];
+        a.stage = s;
+        a.div_order = c->cfg.div_order;
+        a.characteristic = c->cfg.weno_characteristic;
+        a.check = c->cfg.check_positivity;
+        a.want_lambda = s == 3;
+        a.gamma = c->cfg.gamma;
+        a.eps = c->cfg.weno_eps;
+        a.lambda_bits = c->d_lambda;
+        a.err = c->d_err;
+        a.geo = c->geo;
+        int scheme = c->cfg.scheme == AMR_CENTRAL4 ? 0 : (c->cfg.weno_characteristic ? 1 : 2);
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (c->timing && a.nleaves > 0) {
+            e0 = take_event(c);
+            e1 = take_event(c);
+            CU(cudaEventRecord(e0, c->stream));
+        }
+        LAUNCH(launch_stage(scheme, a, c->stream), "stage");
+        c->st.stage_launches++;
+        if (e1) {
+            CU(cudaEventRecord(e1, c->stream));
+            c->ev_pending.push_back(e0);
+            c->ev_pending.push_back(e1);
+            c->ev_cells.push_back(c->leaf_cells);
+            c->ev_bytes.push_back((double)c->leaf_cells * (s == 1 ? 64.0 : 96.0));
+        }
+        cs = c->comm.exchange_fluxes(c);
+        if (cs != AMR_OK) return cs;
+        if (!c->rtasks.empty()) {
+            AuxArgs x = aux(c, Uout, Uout);
+            x.b = bs[s - 1];
+            x.stage = s;
+            x.want_lambda = s == 3;
+            LAUNCH(launch_reflux(c->d_rtasks.p, (int)c->rtasks.size(), x, c->stream), "reflux");
+        }
+        cs = restrict_all(c, Uout);
+        if (cs != AMR_OK) return cs;
+    }
+    amr_status cs = c->comm.allreduce_max_u64(c, c->d_lambda);
+    if (cs != AMR_OK) return cs;
+    c->un = A;
+    c->st.steps++;
+    c->lambda_valid = true;   // stage 3 (and the reflux) accumulated Lambda of U^(n+1)
+    if (c->timing && c->ev_pending.size() > 4096) return harvest_events(c);
+    return AMR_OK;
+}
+
+// read {err, dt}; on a device-reported error roll back to the pre-step buffer
+amr_status finish_step(amr_ctx* c, int prev_un, double* dt_used) {
+    int32_t* he = (int32_t*)c->h_pinned;
+    double* hdt = (double*)((char*)c->h_pinned + 16);
+    CU(cudaMemcpyAsync(he, c->d_err, 16, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(hdt, c->d_dt, 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    amr_status s = c->comm.agree_error(c, he);
+    if (s != AMR_OK) return s;
+    if (he[0] != 0) {
+        int32_t e0 = he[0], slot = he[1], stage = he[2], cell = he[3];
+        CU(cudaMemsetAsync(c->d_err, 0, 16, c->stream));
+        if (prev_un >= 0) {
+            c->un = prev_un;
+            c->st.steps--;
+        }
+        c->lambda_valid = false;
+        char b[256];
+        if (e0 == 2) std::snprintf(b, sizeof b, "non-positive or non-finite time step (wave speed)");
+        else if (slot >= 0 && slot < c->tree.capacity && c->tree.alive[slot])
+            std::snprintf(b, sizeof b, "non-physical state at stage %d, patch (level %d, i %d, j %d), cell %d", stage,
+                          c->tree.lev[slot], c->tree.pi[slot], c->tree.pj[slot], cell);
+        else std::snprintf(b, sizeof b, "non-physical state at stage %d", stage);
+        return fail(c, AMR_E_NONPHYSICAL, b);
+    }
+    c->last_dt = *hdt;
+    if (dt_used) *dt_used = *hdt;
+    return AMR_OK;
+}
+
+// flags on the current state (ghost-filled U^n): per-leaf max eta and ambiguity
+amr_status evaluate_flags(amr_ctx* c) {
+    double* Un = c->U[c->un];
+    amr_status s = c->comm.exchange_halos(c, Un);
+    if (s != AMR_OK) return s;
+    s = fill_ghosts(c, Un);
+    if (s != AMR_OK) return s;
+    AuxArgs a = aux(c, Un, nullptr);
+    LAUNCH(launch_flags(c->d_leaves.p, (int)c->leaves.size(), a, c->d_maxeta.p, c->d_amb.p, c->stream), "flags");
+    std::vector<double> me(c->leaves.size());
+    std::vector<int32_t> am(c->leaves.size());
+    if (!me.empty()) {
+        CU(cudaMemcpyAsync(me.data(), c->d_maxeta.p, me.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(am.data(), c->d_amb.p, am.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    PatchTree& t = c->tree;
+    std::vector<double> eta(t.capacity, std::nan(""));
+    std::vector<uint8_t> amb(t.capacity, 0);
+    for (size_t e = 0; e < c->leaf_ids.size(); ++e) { eta[c->leaf_ids[e]] = me[e]; amb[c->leaf_ids[e]] = (uint8_t)am[e]; }
+    s = c->comm.allgather_flags(c, eta, amb);
+    if (s != AMR_OK) return s;
+    c->fl_eta.assign(t.capacity, std::nan(""));
+    c->fl_ref.assign(t.capacity, 0);
+    c->fl_crs.assign(t.capacity, 0);
+    c->fl_amb.assign(t.capacity, 0);
+    const double th = c->cfg.refine_threshold, tc = th * c->cfg.coarsen_fraction;
+    for (int id : c->canon) {
+        if (t.is_leaf(id)) {
+            c->fl_eta[id] = eta[id];
+            c->fl_amb[id] = amb[id];
+            c->fl_ref[id] = t.lev[id] < c->cfg.num_levels - 1 && eta[id] > th;
+        } else {
+            bool all_leaves = true;
+            double m = 0.0;
+            uint8_t a = 0;
+            for (int q = 0; q < 4; ++q) {
+                int ch = t.child[4 * id + q];
+                if (!t.is_leaf(ch)) { all_leaves = false; break; }
+                if (!(eta[ch] <= m)) m = eta[ch];
+                a |= amb[ch];
+            }
+            if (all_leaves) {
+                c->fl_eta[id] = m;
+                c->fl_amb[id] = a;
+                c->fl_crs[id] = m < tc;
+            }
+        }
+    }
+    return AMR_OK;
+}
+
+// refinement pass, coarsening pass, validation, new-patch prolongation, restriction
+amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::vector<uint8_t>& crs, int32_t* nr,
+                        int32_t* nc) {
+    PatchTree nt = c->tree;
+    std::string m;
+    for (int id : c->canon) {
+        if (!ref[id] || !nt.is_leaf(id) || nt.lev[id] >= c->cfg.num_levels - 1) continue;
+        if (!nt.refine(id, m)) {
+            amr_status s = m.find("capacity") != std::string::npos ? AMR_E_CAPACITY : AMR_E_MESH;
+            return fail(c, s, "regrid: " + m + " (mesh unchanged)");
+        }
+    }
+    for (int l = c->cfg.num_levels - 2; l >= 0; --l)
+        for (int id : c->canon) {
+            if (nt.lev[id] != l || !crs[id] || !nt.alive[id]) continue;
+            if (nt.coarsen_allowed(id)) nt.delete_children(id);
+        }
+    if (!nt.validate(m)) return fail(c, AMR_E_MESH, "regrid produced an invalid mesh: " + m);
+    int n_new = 0, n_del = 0;
+    std::vector<std::vector<ProlongTask>> pro(c->cfg.num_levels);
+    for (int id = 0; id < nt.capacity; ++id) {
+        if (nt.alive[id] && !c->tree.alive[id]) {
+            ++n_new;
+            ProlongTask p{};
+            p.slot = id;
+            p.level = nt.lev[id];
+            p.P = nt.pi[id];
+            p.Q = nt.pj[id];
+            int par = nt.parent[id];
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int q = (dx == 0 && dy == 0) ? par : nt.neighbour(par, dx, dy);
+                    if (q == -1) return fail(c, AMR_E_MESH, "prolongation: coarse neighbourhood incomplete");
+                    p.coarse[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
+                }
+            pro[p.level].push_back(p);
+        }
+        if (c->tree.alive[id] && !nt.alive[id]) ++n_del;
+    }
+    c->tree = nt;
+    amr_status s = build_plan(c);
+    if (s != AMR_OK) return s;
+    double* Un = c->U[c->un];
+    for (int l = 1; l < c->cfg.num_levels; ++l) {
+        if (pro[l].empty()) continue;
+        s = c->comm.exchange_coarse(c, Un, l);
+        if (s != AMR_OK) return s;
+        CU(c->d_prolong.upload(pro[l], c->stream));
+        AuxArgs a = aux(c, Un, Un);
+        LAUNCH(launch_prolong(c->d_prolong.p, (int)pro[l].size(), a, c->stream), "prolong");
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    s = restrict_all(c, Un);
+    if (s != AMR_OK) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    c->lambda_valid = false;
+    c->fl_ref.assign(nt.capacity, 0);
+    c->fl_crs.assign(nt.capacity, 0);
+    c->fl_amb.assign(nt.capacity, 0);
+    c->fl_eta.assign(nt.capacity, std::nan(""));
+    if (nr) *nr = n_new;
+    if (nc) *nc = n_del;
+    return AMR_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int32_t amr_abi_version(void) { return AMR_ABI_VERSION; }
+
+amr_status amr_default_config(amr_config* cfg) {
+    if (!cfg) return AMR_E_ARG;
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->dim = 2;
+    cfg->lo[0] = cfg->lo[1] = 0.0;
+    cfg->hi[0] = cfg->hi[1] = 1.0;
+    cfg->base_cells[0] = cfg->base_cells[1] = 64;
+    cfg->patch_cells = 16;
+    cfg->num_levels = 1;
+    cfg->ratio = 2;
+    cfg->gamma = 1.4;
+    for (int s = 0; s < 4; ++s) cfg->bc[s] = AMR_BC_PERIODIC;
+    cfg->scheme = AMR_CENTRAL4;
+    cfg->weno_characteristic = 1;
+    cfg->div_order = 4;
+    cfg->weno_eps = 1e-6;
+    cfg->refine_threshold = 0.1;
+    cfg->coarsen_fraction = 0.25;
+    cfg->coarsen_rule = AMR_COARSEN_R2_EXACT;
+    cfg->max_patches = 4096;
+    cfg->device = -1;
+    cfg->world_size = 1;
+    cfg->rank = 0;
+    cfg->check_positivity = 1;
+    cfg->use_graphs = 0;
+    return AMR_OK;
+}
+
+amr_status amr_query_pool_bytes(const amr_config* cfg, uint64_t* bytes) {
+    if (!cfg || !bytes) return AMR_E_ARG;
+    *bytes = 3ull * (uint64_t)cfg->max_patches * 4ull * (uint64_t)cfg->patch_cells * cfg->patch_cells * 8ull;
+    return AMR_OK;
+}
+
+amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
+    if (!cfg || !out) return AMR_E_ARG;
+    *out = nullptr;
+    std::string m;
+    amr_status vs = validate_config(cfg, m);
+    if (vs != AMR_OK) {
+        std::fprintf(stderr, "amr_create: %s\n", m.c_str());
+        return vs;
+    }
+    std::unique_ptr<amr_ctx> h(new amr_ctx());
+    amr_ctx* c = h.get();
+    c->cfg = *cfg;
+    c->n = cfg->patch_cells;
+    c->PS = 4ull * c->n * c->n;
+    const int npx = cfg->base_cells[0] / c->n, npy = cfg->base_cells[1] / c->n;
+    if ((int64_t)npx * npy > cfg->max_patches) {
+        std::fprintf(stderr, "amr_create: %d roots exceed max_patches %d\n", npx * npy, cfg->max_patches);
+        return AMR_E_CAPACITY;
+    }
+    if (cfg->device >= 0) CU(cudaSetDevice(cfg->device));
+    c->tree.init(npx, npy, cfg->num_levels, cfg->bc[0] == AMR_BC_PERIODIC, cfg->bc[2] == AMR_BC_PERIODIC,
+                 cfg->max_patches, cfg->coarsen_rule);
+    Geometry& G = c->geo;
+    G.n = c->n;
+    for (int s = 0; s < 4; ++s) G.bc[s] = cfg->bc[s];
+    for (int l = 0; l < kMaxLevels; ++l) {
+        G.nc[0][l] = l < cfg->num_levels ? cfg->base_cells[0] << l : 0;
+        G.nc[1][l] = l < cfg->num_levels ? cfg->base_cells[1] << l : 0;
+        // O1: dx_l = (hi - lo) / (N * 2^l)
+        G.dx[l] = (cfg->hi[0] - cfg->lo[0]) / ((double)cfg->base_cells[0] * (double)(1 << std::min(l, 30)));
+        G.dy[l] = (cfg->hi[1] - cfg->lo[1]) / ((double)cfg->base_cells[1] * (double)(1 << std::min(l, 30)));
+        G.inv_dx[l] = 1.0 / G.dx[l];
+        G.inv_dy[l] = 1.0 / G.dy[l];
+    }
+    if (cfg->cuda_stream) c->stream = (cudaStream_t)cfg->cuda_stream;
+    else {
+        CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    uint64_t need = 0;
+    amr_query_pool_bytes(cfg, &need);
+    char* base = nullptr;
+    if (cfg->pool) {
+        if (cfg->pool_bytes < need) {
+            std::fprintf(stderr, "amr_create: pool too small (%llu < %llu bytes)\n", (unsigned long long)cfg->pool_bytes,
+                         (unsigned long long)need);
+            return AMR_E_ARG;
+        }
+        base = (char*)cfg->pool;
+    } else {
+        CU(cudaMalloc(&c->own_pool, need));
+        base = (char*)c->own_pool;
+    }
+    for (int b = 0; b < 3; ++b) c->U[b] = (double*)(base + (size_t)b * (need / 3));
+    CU(cudaMemsetAsync(base, 0, need, c->stream));
+    CU(cudaMalloc(&c->d_dt, 8));
+    CU(cudaMalloc(&c->d_lambda, 8));
+    CU(cudaMalloc(&c->d_tmp, 8));
+    CU(cudaMalloc(&c->d_err, 16));
+    CU(cudaMemsetAsync(c->d_err, 0, 16, c->stream));
+    CU(cudaMallocHost(&c->h_pinned, 64));
+    amr_status s = c->comm.init(c);
+    if (s != AMR_OK) {
+        std::fprintf(stderr, "amr_create: %s\n", c->err.c_str());
+        return s;
+    }
+    s = build_plan(c);
+    if (s != AMR_OK) {
+        std::fprintf(stderr, "amr_create: %s\n", c->err.c_str());
+        return s;
+    }
+    *out = h.release();
+    return AMR_OK;
+}
+
+void amr_destroy(amr_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    c->comm.finalize(c);
+    c->d_leaves.release(); c->d_ptasks.release(); c->d_rtasks.release(); c->d_prolong.release();
+    for (auto& d : c->d_rlev) d.release();
+    c->proxy.release(); c->freg.release(); c->staging.release(); c->d_maxeta.release(); c->d_partial.release();
+    c->d_slots.release(); c->d_amb.release();
+    if (c->own_pool) cudaFree(c->own_pool);
+    cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    for (auto e : c->ev_free) cudaEventDestroy(e);
+    for (auto e : c->ev_pending) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+static amr_status select_local(amr_ctx* c, int32_t npatch, const int32_t* tree_index, std::vector<int32_t>& slots,
+                               std::vector<int32_t>& which) {
+    slots.clear();
+    which.clear();
+    for (int k = 0; k < npatch; ++k) {
+        int ti = tree_index[k];
+        if (ti < 0 || ti >= (int)c->canon.size()) return fail(c, AMR_E_ARG, "tree_index out of range");
+        int id = c->canon[ti];
+        if (!c->comm.owns(c, id)) continue;
+        slots.push_back(id);
+        which.push_back(k);
+    }
+    return AMR_OK;
+}
+
+amr_status amr_set_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, const double* U) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (npatch < 0 || (npatch > 0 && (!tree_index || !U))) return fail(c, AMR_E_ARG, "set_state: bad arguments");
+    std::vector<int32_t> slots, which;
+    s = select_local(c, npatch, tree_index, slots, which);
+    if (s != AMR_OK) return s;
+    const size_t PS = c->PS;
+    const size_t chunk = 8192;   // patches per staging round
+    for (size_t b = 0; b < slots.size(); b += chunk) {
+        size_t m = std::min(chunk, slots.size() - b);
+        CU(c->staging.reserve(m * PS));
+        CU(c->d_slots.reserve(m));
+        bool contiguous = true;
+        for (size_t k = 1; k < m; ++k) contiguous &= which[b + k] == which[b] + (int)k;
+        if (contiguous) {
+            CU(cudaMemcpyAsync(c->staging.p, U + (size_t)which[b] * PS, m * PS * 8, cudaMemcpyHostToDevice, c->stream));
+        } else {
+            for (size_t k = 0; k < m; ++k)
+                CU(cudaMemcpyAsync(c->staging.p + k * PS, U + (size_t)which[b + k] * PS, PS * 8, cudaMemcpyHostToDevice,
+                                   c->stream));
+        }
+        CU(cudaMemcpyAsync(c->d_slots.p, slots.data() + b, m * 4, cudaMemcpyHostToDevice, c->stream));
+        LAUNCH(launch_scatter(c->staging.p, c->d_slots.p, (int)m, c->U[c->un], c->n, c->stream), "scatter");
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    s = c->comm.exchange_children(c, c->U[c->un]);
+    if (s != AMR_OK) return s;
+    s = restrict_all(c, c->U[c->un]);
+    if (s != AMR_OK) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    c->lambda_valid = false;
+    return AMR_OK;
+}
+
+amr_status amr_set_state_device(amr_ctx* c, int32_t npatch, const int32_t* tree_index, const double* dU) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (npatch < 0 || (npatch > 0 && (!tree_index || !dU))) return fail(c, AMR_E_ARG, "set_state_device: bad arguments");
+    std::vector<int32_t> slots, which;
+    s = select_local(c, npatch, tree_index, slots, which);
+    if (s != AMR_OK) return s;
+    const size_t PS = c->PS;
+    std::vector<int32_t> src_slots(slots.size());
+    // scatter row k of dU (packed) into its slot: a packed index list per chunk
+    const size_t chunk = 1 << 20;
+    for (size_t b = 0; b < slots.size(); b += chunk) {
+        size_t m = std::min(chunk, slots.size() - b);
+        bool contiguous = true;
+        for (size_t k = 1; k < m; ++k) contiguous &= which[b + k] == which[b] + (int)k;
+        if (!contiguous) return fail(c, AMR_E_ARG, "set_state_device: tree_index rows of local patches must be contiguous");
+        CU(c->d_slots.reserve(m));
+        CU(cudaMemcpyAsync(c->d_slots.p, slots.data() + b, m * 4, cudaMemcpyHostToDevice, c->stream));
+        LAUNCH(launch_scatter(dU + (size_t)which[b] * PS, c->d_slots.p, (int)m, c->U[c->un], c->n, c->stream), "scatter");
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    s = c->comm.exchange_children(c, c->U[c->un]);
+    if (s != AMR_OK) return s;
+    s = restrict_all(c, c->U[c->un]);
+    if (s != AMR_OK) return s;
+    c->lambda_valid = false;
+    return AMR_OK;
+}
+
+amr_status amr_get_state_device(amr_ctx* c, int32_t npatch, const int32_t* tree_index, double* dU_out) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (npatch < 0 || (npatch > 0 && (!tree_index || !dU_out))) return fail(c, AMR_E_ARG, "get_state_device: bad arguments");
+    std::vector<int32_t> slots, which;
+    s = select_local(c, npatch, tree_index, slots, which);
+    if (s != AMR_OK) return s;
+    for (size_t k = 1; k < which.size(); ++k)
+        if (which[k] != which[0] + (int)k) return fail(c, AMR_E_ARG, "get_state_device: local rows must be contiguous");
+    if (slots.empty()) return AMR_OK;
+    CU(c->d_slots.reserve(slots.size()));
+    CU(cudaMemcpyAsync(c->d_slots.p, slots.data(), slots.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    LAUNCH(launch_gather(c->U[c->un], c->d_slots.p, (int)slots.size(), dU_out + (size_t)which[0] * c->PS, c->n, c->stream),
+           "gather");
+    CU(cudaStreamSynchronize(c->stream));
+    return AMR_OK;
+}
+
+amr_status amr_get_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, double* U_out) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (npatch < 0 || (npatch > 0 && (!tree_index || !U_out))) return fail(c, AMR_E_ARG, "get_state: bad arguments");
+    std::vector<int32_t> slots, which;
+    s = select_local(c, npatch, tree_index, slots, which);
+    if (s != AMR_OK) return s;
+    const size_t PS = c->PS;
+    const size_t chunk = 8192;
+    std::vector<double> host;
+    for (size_t b = 0; b < slots.size(); b += chunk) {
+        size_t m = std::min(chunk, slots.size() - b);
+        CU(c->staging.reserve(m * PS));
+        CU(c->d_slots.reserve(m));
+        CU(cudaMemcpyAsync(c->d_slots.p, slots.data() + b, m * 4, cudaMemcpyHostToDevice, c->stream));
+        LAUNCH(launch_gather(c->U[c->un], c->d_slots.p, (int)m, c->staging.p, c->n, c->stream), "gather");
+        bool contiguous = true;
+        for (size_t k = 1; k < m; ++k) contiguous &= which[b + k] == which[b] + (int)k;
+        if (contiguous) {
+            CU(cudaMemcpyAsync(U_out + (size_t)which[b] * PS, c->staging.p, m * PS * 8, cudaMemcpyDeviceToHost, c->stream));
+        } else {
+            for (size_t k = 0; k < m; ++k)
+                CU(cudaMemcpyAsync(U_out + (size_t)which[b + k] * PS, c->staging.p + k * PS, PS * 8,
+                                   cudaMemcpyDeviceToHost, c->stream));
+        }
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    return AMR_OK;
+}
+
+amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (!(dt > 0.0) && !(cfl > 0.0)) return fail(c, AMR_E_ARG, "step: need dt > 0 or cfl > 0");
+    int prev = c->un;
+    s = enqueue_step(c, dt, cfl);
+    if (s != AMR_OK) return s;
+    if (c->cfg.check_positivity || dt_used) return finish_step(c, prev, dt_used);
+    return AMR_OK;
+}
+
+amr_status amr_steps(amr_ctx* c, int32_t nsteps, double dt, double cfl) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (nsteps < 0 || (!(dt > 0.0) && !(cfl > 0.0))) return fail(c, AMR_E_ARG, "steps: bad arguments");
+    for (int k = 0; k < nsteps; ++k) {
+        s = enqueue_step(c, dt, cfl);
+        if (s != AMR_OK) return s;
+    }
+    return AMR_OK;
+}
+
+amr_status amr_sync(amr_ctx* c) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    s = harvest_events(c);
+    if (s != AMR_OK) return s;
+    return finish_step(c, -1, nullptr);
+}
+
+amr_status amr_get_flags(amr_ctx* c, int32_t cap, double* maxeta, uint8_t* bits) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (cap < (int)c->canon.size() || !maxeta || !bits) return fail(c, AMR_E_ARG, "get_flags: capacity");
+    s = evaluate_flags(c);
+    if (s != AMR_OK) return s;
+    for (size_t e = 0; e < c->canon.size(); ++e) {
+        int id = c->canon[e];
+        maxeta[e] = c->fl_eta[id];
+        bits[e] = (uint8_t)(c->fl_ref[id] | (c->fl_crs[id] << 1) | (c->fl_amb[id] << 2));
+    }
+    return AMR_OK;
+}
+
+amr_status amr_regrid(amr_ctx* c, int32_t* n_refined, int32_t* n_coarsened) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    s = evaluate_flags(c);
+    if (s != AMR_OK) return s;
+    std::vector<uint8_t> ref = c->fl_ref, crs = c->fl_crs;
+    return apply_regrid(c, ref, crs, n_refined, n_coarsened);
+}
+
+amr_status amr_regrid_with_flags(amr_ctx* c, int32_t n, const int32_t* tree_index, const uint8_t* bits,
+                                 int32_t* n_refined, int32_t* n_coarsened) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (n < 0 || (n > 0 && (!tree_index || !bits))) return fail(c, AMR_E_ARG, "regrid_with_flags: bad arguments");
+    std::vector<uint8_t> ref(c->tree.capacity, 0), crs(c->tree.capacity, 0);
+    for (int k = 0; k < n; ++k) {
+        int ti = tree_index[k];
+        if (ti < 0 || ti >= (int)c->canon.size()) return fail(c, AMR_E_ARG, "regrid_with_flags: tree_index");
+        ref[c->canon[ti]] = bits[k] & 1;
+        crs[c->canon[ti]] = (bits[k] >> 1) & 1;
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    return apply_regrid(c, ref, crs, n_refined, n_coarsened);
+}
+
+amr_status amr_get_patch_tree(amr_ctx* c, amr_patch_desc* out, int32_t cap, int32_t* count) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (!count) return fail(c, AMR_E_ARG, "get_patch_tree: count is NULL");
+    *count = (int32_t)c->canon.size();
+    if (!out || cap < *count) return fail(c, AMR_E_ARG, "get_patch_tree: capacity smaller than the patch count");
+    const PatchTree& t = c->tree;
+    static const int moore[8][2] = {{0, 1}, {1, 0}, {0, -1}, {-1, 0}, {1, 1}, {1, -1}, {-1, -1}, {-1, 1}};
+    auto tix = [&](int id) { return id >= 0 ? c->canon_pos[id] : -1; };
+    for (size_t e = 0; e < c->canon.size(); ++e) {
+        int id = c->canon[e];
+        amr_patch_desc& d = out[e];
+        d.level = t.lev[id];
+        d.i = t.pi[id];
+        d.j = t.pj[id];
+        d.parent = tix(t.parent[id]);
+        for (int q = 0; q < 4; ++q) d.child[q] = tix(t.child[4 * id + q]);
+        for (int q = 0; q < 8; ++q) {
+            int nb = t.neighbour(id, moore[q][0], moore[q][1]);
+            d.nbr[q] = nb >= 0 ? tix(nb) : -1;
+        }
+        d.owner = c->comm.owner_of(c, id);
+        d.leaf = t.is_leaf(id);
+        d.refine_req = id < (int)c->fl_ref.size() ? c->fl_ref[id] : 0;
+        d.coarsen_req = id < (int)c->fl_crs.size() ? c->fl_crs[id] : 0;
+        d.ambiguous = id < (int)c->fl_amb.size() ? c->fl_amb[id] : 0;
+    }
+    return AMR_OK;
+}
+
+amr_status amr_diagnostics(amr_ctx* c, double totals[4], double* lambda_max) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    AuxArgs a = aux(c, c->U[c->un], nullptr);
+    if (totals) {
+        LAUNCH(launch_totals(c->d_leaves.p, (int)c->leaves.size(), a, c->d_partial.p, c->stream), "totals");
+        std::vector<double> part(4 * c->leaves.size());
+        if (!part.empty())
+            CU(cudaMemcpyAsync(part.data(), c->d_partial.p, part.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        // combine in canonical order (deterministic), long double accumulation
+        std::vector<int32_t> order(c->leaves.size());
+        for (size_t e = 0; e < order.size(); ++e) order[e] = (int32_t)e;
+        std::sort(order.begin(), order.end(),
+                  [&](int x, int y) { return c->canon_pos[c->leaf_ids[x]] < c->canon_pos[c->leaf_ids[y]]; });
+        long double acc[4] = {0, 0, 0, 0};
+        for (int e : order)
+            for (int k = 0; k < 4; ++k) acc[k] += part[4 * (size_t)e + k];
+        double loc[4];
+        for (int k = 0; k < 4; ++k) loc[k] = (double)acc[k];
+        s = c->comm.allreduce_sum4(c, loc);
+        if (s != AMR_OK) return s;
+        for (int k = 0; k < 4; ++k) totals[k] = loc[k];
+    }
+    if (lambda_max) {
+        AuxArgs b = a;
+        b.lambda_bits = c->d_tmp;
+        CU(cudaMemsetAsync(c->d_tmp, 0, 8, c->stream));
+        LAUNCH(launch_lambda(c->d_leaves.p, (int)c->leaves.size(), b, c->stream), "lambda");
+        s = c->comm.allreduce_max_u64(c, c->d_tmp);
+        if (s != AMR_OK) return s;
+        unsigned long long bits = 0;
+        CU(cudaMemcpyAsync(&bits, c->d_tmp, 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        std::memcpy(lambda_max, &bits, 8);
+    }
+    return AMR_OK;
+}
+
+amr_status amr_set_kernel_timing(amr_ctx* c, int32_t enable) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    c->timing = enable != 0;
+    return AMR_OK;
+}
+
+amr_status amr_get_stats(amr_ctx* c, amr_stats* out) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (!out) return fail(c, AMR_E_ARG, "get_stats: NULL");
+    s = harvest_events(c);
+    if (s != AMR_OK) return s;
+    *out = c->st;
+    return AMR_OK;
+}
+
+amr_status amr_reset_stats(amr_ctx* c) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    s = harvest_events(c);
+    if (s != AMR_OK) return s;
+    amr_stats keep = c->st;
+    std::memset(&c->st, 0, sizeof c->st);
+    c->st.leaf_cells = keep.leaf_cells;
+    c->st.leaves = keep.leaves;
+    c->st.patches = keep.patches;
+    c->st.proxies = keep.proxies;
+    return AMR_OK;
+}
+
+const char* amr_last_error(const amr_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+}  // extern "C"

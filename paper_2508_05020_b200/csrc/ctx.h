@@ -1,0 +1,106 @@
+// ctx.h -- the library context behind the opaque amr_ctx handle (include/amr.h).
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/amr.h"
+#include "comm.h"
+#include "device.h"
+#include "tree.h"
+
+namespace amr {
+
+template <class T>
+struct DevArray {
+    T* p = nullptr;
+    size_t cap = 0, count = 0;
+    cudaError_t upload(const std::vector<T>& v, cudaStream_t s) {
+        count = v.size();
+        if (v.size() > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = std::max<size_t>(v.size(), 16);
+            cudaError_t e = cudaMalloc(&p, cap * sizeof(T));
+            if (e != cudaSuccess) { cap = 0; return e; }
+        }
+        if (v.empty()) return cudaSuccess;
+        return cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+    }
+    cudaError_t reserve(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = std::max<size_t>(n, 16);
+        cudaError_t e = cudaMalloc(&p, cap * sizeof(T));
+        if (e != cudaSuccess) cap = 0;
+        return e;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; cap = count = 0; }
+};
+
+inline uint64_t morton(uint32_t x, uint32_t y) {
+    uint64_t r = 0;
+    for (int b = 0; b < 32; ++b) r |= (uint64_t((x >> b) & 1u) << (2 * b)) | (uint64_t((y >> b) & 1u) << (2 * b + 1));
+    return r;
+}
+
+}  // namespace amr
+
+using namespace amr;
+
+struct amr_ctx {
+    amr_config cfg{};
+    PatchTree tree;
+    int n = 0, g = 4;
+    Geometry geo{};
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double* U[3] = {nullptr, nullptr, nullptr};
+    void* own_pool = nullptr;
+    int un = 0;
+    size_t PS = 0;   // doubles per slot
+
+    // plan (rebuilt after every mesh change)
+    std::vector<int32_t> canon, canon_pos;      // canonical order; id -> tree index
+    std::vector<int32_t> leaf_ids;               // launch order
+    std::vector<int32_t> leaf_pos;               // id -> leaf index or -1
+    std::vector<LeafDesc> leaves;
+    std::vector<ProxyTask> ptasks;
+    std::vector<RefluxTask> rtasks;
+    std::vector<std::vector<RestrictTask>> rlev;  // rlev[l]: parents at level l-1 of level-l children
+    DevArray<LeafDesc> d_leaves;
+    DevArray<ProxyTask> d_ptasks;
+    DevArray<RefluxTask> d_rtasks;
+    std::vector<DevArray<RestrictTask>> d_rlev;
+    DevArray<ProlongTask> d_prolong;
+    DevArray<double> proxy, freg, staging, d_maxeta, d_partial;
+    DevArray<int32_t> d_slots, d_amb;
+    int64_t leaf_cells = 0;
+
+    // device scalars: dt, lambda bits, err[4]
+    double* d_dt = nullptr;
+    unsigned long long* d_lambda = nullptr;
+    int32_t* d_err = nullptr;
+    unsigned long long* d_tmp = nullptr;
+    void* h_pinned = nullptr;   // {int32 err[4]; double dt}
+    bool lambda_valid = false;
+    double last_dt = 0.0;
+
+    // flags of the last evaluation, per id
+    std::vector<uint8_t> fl_ref, fl_crs, fl_amb;
+    std::vector<double> fl_eta;
+
+    // stats / timing
+    amr_stats st{};
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_free, ev_pending;   // pairs (start, stop)
+    std::vector<int64_t> ev_cells;
+    std::vector<double> ev_bytes;
+
+    Comm comm;
+    std::string err;
+    amr_status sticky = AMR_OK;
+};
+

@@ -1,0 +1,133 @@
+// device.h -- plain-old-data descriptors shared by the host planner (api.cpp) and
+// the sm_100a kernels (kernels.cu), plus the kernel launchers.
+//
+// HBM layout: three RK state buffers U[buf][slot][var][j][i] (fp64 SoA,
+// 4 n^2 doubles per slot, var = rho, rho u, rho v, rho e); a proxy buffer of
+// patch-shaped ghost strips P[proxy][var][j][i] for leaf sides that have no
+// same-level neighbour (coarse/fine or physical boundary); flux registers
+// F[leaf][side][var][n] holding F-hat on coarse/fine sides.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace amr {
+
+constexpr int kMaxLevels = 16;
+
+enum Side { kW = 0, kE = 1, kS = 2, kN = 3 };
+
+// One leaf patch in launch order.  side[s] >= 0: slot of the same-level
+// neighbour (read from the stage input buffer); side[s] < 0: proxy -1-side[s].
+struct LeafDesc {
+    int32_t slot;
+    int32_t level;
+    int32_t side[4];
+    int32_t cf;        // bits 0-3: side is the COARSE side of a C/F face; bits 4-7: FINE side
+    int32_t pad;
+};
+
+// Fill one proxy strip (the g columns / rows of a virtual neighbour that touch the leaf).
+struct ProxyTask {
+    int32_t proxy;     // proxy index
+    int32_t slot;      // the leaf's own slot (physical BC source)
+    int32_t side;      // Side of the leaf the strip lies on
+    int32_t kind;      // 0 physical boundary, 1 coarse/fine prolongation
+    int32_t level;     // leaf level l
+    int32_t P, Q;      // leaf patch position at level l
+    int32_t coarse[9]; // slots of the parent's 3x3 level-(l-1) neighbourhood [(dy+1)*3+(dx+1)], -1 outside
+};
+
+// Flux correction of one coarse leaf (O12): for each C/F side the two fine leaves
+// across it (leaf indices into the flux registers), ordered along the side.
+struct RefluxTask {
+    int32_t leaf;      // index of the coarse leaf in the leaf list (its flux registers)
+    int32_t slot;
+    int32_t level;
+    int32_t mask;      // sides that are coarse sides of a C/F face
+    int32_t fine[4][2];
+};
+
+// Restriction parent <- 4 children (O9); child c = a + 2b.
+struct RestrictTask {
+    int32_t parent;
+    int32_t child[4];
+};
+
+// New patch initialised from its parent by prolongation (O8).
+struct ProlongTask {
+    int32_t slot;
+    int32_t level;     // level of the new patch
+    int32_t P, Q;
+    int32_t coarse[9]; // parent's 3x3 neighbourhood at level-1 (centre = parent)
+};
+
+struct Geometry {
+    int32_t n;                     // patch cells
+    int32_t nc[2][kMaxLevels];     // cells per axis per level
+    int32_t bc[4];                 // x-lo, x-hi, y-lo, y-hi
+    double inv_dx[kMaxLevels], inv_dy[kMaxLevels];
+    double dx[kMaxLevels], dy[kMaxLevels];
+};
+
+struct StageArgs {
+    const LeafDesc* leaves;
+    int32_t nleaves;
+    int32_t tiles;             // tiles per side of a patch (n / T)
+    const double* Uin;         // stage input U^(s-1)
+    const double* Un;          // U^n
+    double* Uout;              // U^(s)
+    const double* proxy;
+    double* freg;              // flux registers
+    const double* dt;          // device scalar
+    double a, b;               // U^(s) = a U^n + b (U^(s-1) + dt L)
+    int32_t stage;             // 1, 2, 3
+    int32_t div_order;
+    int32_t characteristic;
+    int32_t check;             // positivity check
+    int32_t want_lambda;       // accumulate Lambda (stage 3)
+    double gamma, eps;
+    unsigned long long* lambda_bits;
+    int32_t* err;              // [0] flag, [1] slot, [2] stage, [3] cell
+    Geometry geo;
+};
+
+struct AuxArgs {
+    const double* U;           // state read (ghost source / restriction source ...)
+    double* Uw;                // state written
+    double* proxy;
+    const double* freg;
+    const double* dt;
+    double b;                  // RK weight of the stage for the reflux
+    int32_t stage;
+    int32_t check;
+    int32_t want_lambda;
+    double gamma;
+    double theta, coarsen_fraction;
+    unsigned long long* lambda_bits;
+    int32_t* err;
+    Geometry geo;
+};
+
+// launchers (kernels.cu); each returns the CUDA error of the launch
+cudaError_t launch_stage(int scheme, const StageArgs& a, cudaStream_t s);
+cudaError_t launch_ghost(const ProxyTask* tasks, int ntasks, int g, const AuxArgs& a, cudaStream_t s);
+cudaError_t launch_reflux(const RefluxTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s);
+cudaError_t launch_restrict(const RestrictTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s);
+cudaError_t launch_prolong(const ProlongTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s);
+cudaError_t launch_lambda(const LeafDesc* leaves, int nleaves, const AuxArgs& a, cudaStream_t s);
+cudaError_t launch_dt(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed, double cfl,
+                      cudaStream_t s);
+cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* maxeta, int32_t* amb,
+                         cudaStream_t s);
+cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* partial, cudaStream_t s);
+
+// patch-granular copies between a packed [npatch][4][n][n] buffer and the pool slots
+cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int n, cudaStream_t s);
+cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int n, cudaStream_t s);
+
+// bytes of dynamic shared memory the stage kernel needs (for occupancy queries)
+size_t stage_smem_bytes(int scheme, int n);
+
+}  // namespace amr

@@ -1,0 +1,824 @@
+// kernels.cu -- sm_100a kernels of the AMR compressible-Euler hot path.
+//
+// The fused stage kernel is the GPU analogue of the paper's task fusion:
+// one launch over the leaf-patch list does, per patch tile, the halo gather
+// (same-level neighbours read in place, proxies for C/F and physical sides),
+// cons->prim (Eq. 4-7), reconstruction (Eq. 8 Central4 or WENO5-JS),
+// the face flux (central, or Rusanov Eq. 11-12), the flux divergence (Eq. 9 in
+// flux form), the SSP-RK3 combination (Fig. 9 ssprk3Stage), the positivity
+// check, flux registers for the coarse/fine correction and, at stage 3, the
+// per-patch max wave speed (warp shuffles + one atomic per warp).
+// Auxiliary kernels: ghost/proxy fill (O7/O8), reflux (O12), restriction (O9),
+// prolongation of new patches (O8), flags (O6), Lambda, totals (O18).
+// Readings and rewrites (A41: single-division WENO weights, reciprocal dx,
+// FMA contraction) are listed in DESIGN.md.
+#include <cmath>
+
+#include "device.h"
+
+namespace amr {
+namespace {
+
+constexpr int kBcPeriodic = 0, kBcTransmissive = 1, kBcReflective = 2;
+
+__device__ __forceinline__ bool physical_state(double r, double m, double w, double E, double g) {
+    double u = m / r, v = w / r;
+    double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
+    return r > 0.0 && p > 0.0 && isfinite(r) && isfinite(m) && isfinite(w) && isfinite(E) && isfinite(u) &&
+           isfinite(v) && isfinite(p);
+}
+
+__device__ __forceinline__ double wave_speed(double r, double m, double w, double E, double g, double idx,
+                                             double idy) {
+    double ir = 1.0 / r;
+    double u = m * ir, v = w * ir;
+    double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
+    double c = sqrt(g * p * ir);
+    return (fabs(u) + c) * idx + (fabs(v) + c) * idy;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ void report_error(int32_t* err, int slot, int stage, int cell) {
+    if (atomicCAS(err, 0, 1) == 0) {
+        err[1] = slot;
+        err[2] = stage;
+        err[3] = cell;
+    }
+}
+
+// ---------------------------------------------------------------- reconstruction + flux
+// WENO5-JS point-value interpolation to the face between v2 and v3 (A2), with the
+// three nonlinear weights normalised through one division (A41):
+// alpha_k ~ d_k / s_k, s_k = (eps + beta_k)^2  =>  omega_k ~ d_k prod_{j != k} s_j.
+__device__ __forceinline__ double weno5(double v0, double v1, double v2, double v3, double v4, double eps) {
+    const double c13_12 = 13.0 / 12.0;
+    double q0 = (3.0 * v0 - 10.0 * v1 + 15.0 * v2) * 0.125;
+    double q1 = (-v1 + 6.0 * v2 + 3.0 * v3) * 0.125;
+    double q2 = (3.0 * v2 + 6.0 * v3 - v4) * 0.125;
+    double t0 = v0 - 2.0 * v1 + v2, u0 = v0 - 4.0 * v1 + 3.0 * v2;
+    double t1 = v1 - 2.0 * v2 + v3, u1 = v1 - v3;
+    double t2 = v2 - 2.0 * v3 + v4, u2 = 3.0 * v2 - 4.0 * v3 + v4;
+    double s0 = eps + (c13_12 * t0 * t0 + 0.25 * u0 * u0);
+    double s1 = eps + (c13_12 * t1 * t1 + 0.25 * u1 * u1);
+    double s2 = eps + (c13_12 * t2 * t2 + 0.25 * u2 * u2);
+    s0 *= s0; s1 *= s1; s2 *= s2;
+    double w0 = s1 * s2, w1 = 10.0 * (s0 * s2), w2 = 5.0 * (s0 * s1);
+    return (w0 * q0 + w1 * q1 + w2 * q2) / (w0 + w1 + w2);
+}
+
+// WENO5 + Rusanov flux at one face in the face-normal frame.  c[s][k], s = cells
+// i-2..i+3, k = (rho, normal momentum, tangential momentum, rho e).
+template <bool CHAR>
+__device__ __forceinline__ void weno_rusanov(const double (&c)[6][4], double g, double eps, double F[4]) {
+    const double gm1 = g - 1.0;
+    double wl[4], wr[4];
+    double u = 0.0, v = 0.0, cs = 0.0, q = 0.0, H = 0.0;
+    if (CHAR) {
+        // eigen-system at the arithmetic-mean primitive state of cells i, i+1 (A4)
+        double iL = 1.0 / c[2][0], iR = 1.0 / c[3][0];
+        double uL = c[2][1] * iL, vL = c[2][2] * iL;
+        double uR = c[3][1] * iR, vR = c[3][2] * iR;
+        double pL = gm1 * (c[2][3] - 0.5 * (c[2][1] * uL + c[2][2] * vL));
+        double pR = gm1 * (c[3][3] - 0.5 * (c[3][1] * uR + c[3][2] * vR));
+        double r = 0.5 * (c[2][0] + c[3][0]);
+        u = 0.5 * (uL + uR);
+        v = 0.5 * (vL + vR);
+        double p = 0.5 * (pL + pR);
+        double c2 = g * p / r;
+        cs = sqrt(c2);
+        double ic = 1.0 / cs;
+        q = 0.5 * (u * u + v * v);
+        H = c2 / gm1 + q;
+        double b1 = gm1 / c2;
+        double b2 = b1 * q;
+        // rows of L (O10): l1, l2, l3, l4
+        const double L0[4] = {0.5 * (b2 + u * ic), 0.5 * (-b1 * u - ic), 0.5 * (-b1 * v), 0.5 * b1};
+        const double L1[4] = {1.0 - b2, b1 * u, b1 * v, -b1};
+        const double L3[4] = {0.5 * (b2 - u * ic), 0.5 * (-b1 * u + ic), 0.5 * (-b1 * v), 0.5 * b1};
+        double w[6];
+#pragma unroll
+        for (int s = 0; s < 6; ++s) w[s] = L0[0] * c[s][0] + L0[1] * c[s][1] + L0[2] * c[s][2] + L0[3] * c[s][3];
+        wl[0] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
+        wr[0] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) w[s] = L1[0] * c[s][0] + L1[1] * c[s][1] + L1[2] * c[s][2] + L1[3] * c[s][3];
+        wl[1] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
+        wr[1] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) w[s] = -v * c[s][0] + c[s][2];
+        wl[2] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
+        wr[2] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) w[s] = L3[0] * c[s][0] + L3[1] * c[s][1] + L3[2] * c[s][2] + L3[3] * c[s][3];
+        wl[3] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
+        wr[3] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            wl[k] = weno5(c[0][k], c[1][k], c[2][k], c[3][k], c[4][k], eps);
+            wr[k] = weno5(c[5][k], c[4][k], c[3][k], c[2][k], c[1][k], eps);
+        }
+    }
+    double UL[4], UR[4];
+    if (CHAR) {
+        // U = R w, columns r1 = (1, u-c, v, H-uc), r2 = (1, u, v, q), r3 = (0,0,1,v), r4 = (1, u+c, v, H+uc)
+        UL[0] = wl[0] + wl[1] + wl[3];
+        UL[1] = (u - cs) * wl[0] + u * wl[1] + (u + cs) * wl[3];
+        UL[2] = v * wl[0] + v * wl[1] + wl[2] + v * wl[3];
+        UL[3] = (H - u * cs) * wl[0] + q * wl[1] + v * wl[2] + (H + u * cs) * wl[3];
+        UR[0] = wr[0] + wr[1] + wr[3];
+        UR[1] = (u - cs) * wr[0] + u * wr[1] + (u + cs) * wr[3];
+        UR[2] = v * wr[0] + v * wr[1] + wr[2] + v * wr[3];
+        UR[3] = (H - u * cs) * wr[0] + q * wr[1] + v * wr[2] + (H + u * cs) * wr[3];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { UL[k] = wl[k]; UR[k] = wr[k]; }
+    }
+    // Rusanov (Eq. 11) with S = max(c^R + |u^R|, c^L + |u^L|) (Eq. 12)
+    double irL = 1.0 / UL[0], irR = 1.0 / UR[0];
+    double unL = UL[1] * irL, utL = UL[2] * irL;
+    double unR = UR[1] * irR, utR = UR[2] * irR;
+    double pL = gm1 * (UL[3] - 0.5 * (UL[1] * unL + UL[2] * utL));
+    double pR = gm1 * (UR[3] - 0.5 * (UR[1] * unR + UR[2] * utR));
+    double sL = sqrt(g * pL * irL) + fabs(unL);
+    double sR = sqrt(g * pR * irR) + fabs(unR);
+    double S = fmax(sR, sL);
+    double FL0 = UL[1], FL1 = UL[1] * unL + pL, FL2 = UL[2] * unL, FL3 = (UL[3] + pL) * unL;
+    double FR0 = UR[1], FR1 = UR[1] * unR + pR, FR2 = UR[2] * unR, FR3 = (UR[3] + pR) * unR;
+    F[0] = 0.5 * (FR0 + FL0) - 0.5 * S * (UR[0] - UL[0]);
+    F[1] = 0.5 * (FR1 + FL1) - 0.5 * S * (UR[1] - UL[1]);
+    F[2] = 0.5 * (FR2 + FL2) - 0.5 * S * (UR[2] - UL[2]);
+    F[3] = 0.5 * (FR3 + FL3) - 0.5 * S * (UR[3] - UL[3]);
+}
+
+// Central4 edge flux: Eq. 8 weights (9/16, -1/16) applied edge-from-node
+// (A7) to (p, T = p/rho, u_n, u_t) of cells i-1..i+2; rho_e = p_e / T_e (A6).
+__device__ __forceinline__ void central4_flux(const double (&c)[4][4], double inv_gm1, double F[4]) {
+    double e[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e[k] = 0.5625 * (c[1][k] + c[2][k]) - 0.0625 * (c[0][k] + c[3][k]);
+    double pe = e[0], un = e[2], ut = e[3];
+    double re = pe / e[1];
+    double Ee = pe * inv_gm1 + 0.5 * re * (un * un + ut * ut);
+    double mn = re * un;
+    F[0] = mn;
+    F[1] = mn * un + pe;
+    F[2] = mn * ut;
+    F[3] = (Ee + pe) * un;
+}
+
+// ---------------------------------------------------------------- the fused stage kernel
+template <int SCHEME>
+struct Traits;
+template <>
+struct Traits<0> { static constexpr int G = 3; };   // Central4 + Eq. 9: cells i-3..i+3
+template <>
+struct Traits<1> { static constexpr int G = 4; };   // WENO5 + Eq. 9: cells i-4..i+4 (A8)
+template <>
+struct Traits<2> { static constexpr int G = 4; };
+
+template <int T>
+struct Block;
+template <>
+struct Block<8> { static constexpr int NT = 64; };
+template <>
+struct Block<16> { static constexpr int NT = 160; };
+template <>
+struct Block<32> { static constexpr int NT = 256; };
+
+template <int SCHEME, int T>
+constexpr size_t stage_smem() {
+    return sizeof(double) * (4 * (T + 2 * Traits<SCHEME>::G) * (T + 2 * Traits<SCHEME>::G) + 4 * T * (T + 3));
+}
+
+// SCHEME 0: Central4; 1: WENO5 characteristic; 2: WENO5 component-wise.
+template <int SCHEME, int T>
+__global__ void __launch_bounds__(Block<T>::NT) stage_kernel(const StageArgs a) {
+    constexpr int G = Traits<SCHEME>::G;
+    constexpr int NT = Block<T>::NT;
+    constexpr int W = T + 2 * G;       // tile row width in shared memory
+    constexpr int NF = T + 3;          // faces per row: m = -1 .. T+1 (face m = left of cell m)
+    constexpr int CPT = (T * T + NT - 1) / NT;
+    extern __shared__ double smem[];
+    double* sQ = smem;                 // [4][W][W]: conserved (WENO) / (p, T, u, v) (Central4)
+    double* sF = smem + 4 * W * W;     // [4][T][NF] x-fluxes, then [4][NF][T] y-fluxes
+
+    const int tid = threadIdx.x;
+    const int tiles2 = a.tiles * a.tiles;
+    const int leaf = blockIdx.x / tiles2;
+    const int tt = blockIdx.x - leaf * tiles2;
+    const int tx = tt % a.tiles, ty = tt / a.tiles;
+    const LeafDesc d = a.leaves[leaf];
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n;
+    const size_t PS = 4 * nn;
+    const double* own = a.Uin + (size_t)d.slot * PS;
+    const double* srcs[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        srcs[s] = d.side[s] >= 0 ? a.Uin + (size_t)d.side[s] * PS : a.proxy + (size_t)(-1 - d.side[s]) * PS;
+
+    // ---- halo gather: plus-shaped tile (corners are never read, A26)
+    constexpr int EBAND = T * W, ESTRIP = G * T, ETOT = EBAND + 2 * ESTRIP;
+    for (int e = tid; e < ETOT; e += NT) {
+        int i, j;
+        if (e < EBAND) { j = e / W; i = e - j * W - G; }
+        else if (e < EBAND + ESTRIP) { int f = e - EBAND; j = f / T - G; i = f - (j + G) * T; }
+        else { int f = e - EBAND - ESTRIP; j = f / T; i = f - j * T; j += T; }
+        int pi = tx * T + i, pj = ty * T + j;
+        const double* base = own;
+        if (pi < 0) { base = srcs[kW]; pi += n; }
+        else if (pi >= n) { base = srcs[kE]; pi -= n; }
+        else if (pj < 0) { base = srcs[kS]; pj += n; }
+        else if (pj >= n) { base = srcs[kN]; pj -= n; }
+        const double* q = base + (size_t)pj * n + pi;
+        int o = (j + G) * W + (i + G);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sQ[k * W * W + o] = __ldg(q + k * nn);
+    }
+    // U^n of the owned cells (stages 2, 3), issued early
+    double un[CPT][4];
+    if (a.stage > 1) {
+        const double* pn = a.Un + (size_t)d.slot * PS;
+#pragma unroll
+        for (int r = 0; r < CPT; ++r) {
+            int c = tid + r * NT;
+            if (c < T * T) {
+                int i = c % T, j = c / T;
+                size_t off = (size_t)(ty * T + j) * n + tx * T + i;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) un[r][k] = __ldg(pn + k * nn + off);
+            }
+        }
+    }
+    __syncthreads();
+
+    const double g = a.gamma;
+    const double inv_gm1 = 1.0 / (g - 1.0);
+    double up[CPT][4];   // U^(s-1) of the owned cells
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        int c = tid + r * NT;
+        if (c < T * T) {
+            int i = c % T, j = c / T;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) up[r][k] = sQ[k * W * W + (j + G) * W + i + G];
+        }
+    }
+    if (SCHEME == 0) {
+        __syncthreads();
+        // cons -> (p, T, u, v) in place (Eq. 4-6)
+        for (int e = tid; e < ETOT; e += NT) {
+            int i, j;
+            if (e < EBAND) { j = e / W; i = e - j * W - G; }
+            else if (e < EBAND + ESTRIP) { int f = e - EBAND; j = f / T - G; i = f - (j + G) * T; }
+            else { int f = e - EBAND - ESTRIP; j = f / T; i = f - j * T; j += T; }
+            int o = (j + G) * W + (i + G);
+            double r = sQ[o], m = sQ[W * W + o], w = sQ[2 * W * W + o], E = sQ[3 * W * W + o];
+            double ir = 1.0 / r;
+            double u = m * ir, v = w * ir;
+            double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
+            sQ[o] = p;
+            sQ[W * W + o] = p * ir;
+            sQ[2 * W * W + o] = u;
+            sQ[3 * W * W + o] = v;
+        }
+        __syncthreads();
+    }
+
+    const int lvl = d.level;
+    const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
+    const bool div4 = a.div_order == 4;
+    double acc[CPT][4];
+
+    // ---- x faces: face m (left of cell m), row j; cells m-3..m+2
+    for (int e = tid; e < T * NF; e += NT) {
+        int j = e / NF, m = e - j * NF - 1;
+        int o = (j + G) * W + (m + G);
+        double f[4];
+        if (SCHEME == 0) {
+            double c[4][4];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                int oo = o + s - 2;
+                c[s][0] = sQ[oo]; c[s][1] = sQ[W * W + oo]; c[s][2] = sQ[2 * W * W + oo]; c[s][3] = sQ[3 * W * W + oo];
+            }
+            central4_flux(c, inv_gm1, f);
+        } else {
+            double c[6][4];
+#pragma unroll
+            for (int s = 0; s < 6; ++s) {
+                int oo = o + s - 3;
+                c[s][0] = sQ[oo]; c[s][1] = sQ[W * W + oo]; c[s][2] = sQ[2 * W * W + oo]; c[s][3] = sQ[3 * W * W + oo];
+            }
+            weno_rusanov<SCHEME == 1>(c, g, a.eps, f);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sF[(k * T + j) * NF + m + 1] = f[k];
+    }
+    __syncthreads();
+    const int leaf_tiles_x_lo = tx == 0, leaf_tiles_x_hi = tx == a.tiles - 1;
+    const int leaf_tiles_y_lo = ty == 0, leaf_tiles_y_hi = ty == a.tiles - 1;
+    const int store_mask = (d.cf | (d.cf >> 4)) & 15;
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        int c = tid + r * NT;
+        if (c < T * T) {
+            int i = c % T, j = c / T;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double* fr = sF + (k * T + j) * NF + i + 1;   // fr[0] = f at face i
+                double fl = fr[0], fh = fr[1];
+                double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-1] + fh) : fl;
+                double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2]) : fh;
+                acc[r][k] = -(Fh - Fl) * idx;
+                if (i == 0 && leaf_tiles_x_lo && (store_mask & 1))
+                    a.freg[(((size_t)leaf * 4 + kW) * 4 + k) * n + ty * T + j] = Fl;
+                if (i == T - 1 && leaf_tiles_x_hi && (store_mask & 2))
+                    a.freg[(((size_t)leaf * 4 + kE) * 4 + k) * n + ty * T + j] = Fh;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- y faces: face m (below cell m), column i; rotated frame (rho, w, m, E)
+    for (int e = tid; e < T * NF; e += NT) {
+        int m = e / T - 1, i = e - (m + 1) * T;
+        int o = (m + G) * W + (i + G);
+        double f[4];
+        if (SCHEME == 0) {
+            double c[4][4];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                int oo = o + (s - 2) * W;
+                c[s][0] = sQ[oo]; c[s][1] = sQ[W * W + oo]; c[s][2] = sQ[3 * W * W + oo]; c[s][3] = sQ[2 * W * W + oo];
+            }
+            central4_flux(c, inv_gm1, f);
+        } else {
+            double c[6][4];
+#pragma unroll
+            for (int s = 0; s < 6; ++s) {
+                int oo = o + (s - 3) * W;
+                c[s][0] = sQ[oo]; c[s][1] = sQ[2 * W * W + oo]; c[s][2] = sQ[W * W + oo]; c[s][3] = sQ[3 * W * W + oo];
+            }
+            weno_rusanov<SCHEME == 1>(c, g, a.eps, f);
+        }
+        sF[(0 * NF + m + 1) * T + i] = f[0];
+        sF[(1 * NF + m + 1) * T + i] = f[2];
+        sF[(2 * NF + m + 1) * T + i] = f[1];
+        sF[(3 * NF + m + 1) * T + i] = f[3];
+    }
+    __syncthreads();
+
+    // ---- divergence (y), RK combination, checks, Lambda
+    const double dt = *a.dt;
+    const int coarse_mask = d.cf & 15;
+    unsigned long long lam = 0ull;
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        int c = tid + r * NT;
+        if (c < T * T) {
+            int i = c % T, j = c / T;
+            double o4[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double* fr = sF + (k * NF + j + 1) * T + i;   // fr[0] = f at face j
+                double fl = fr[0], fh = fr[T];
+                double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-T] + fh) : fl;
+                double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2 * T]) : fh;
+                double L = acc[r][k] - (Fh - Fl) * idy;
+                if (j == 0 && leaf_tiles_y_lo && (store_mask & 4))
+                    a.freg[(((size_t)leaf * 4 + kS) * 4 + k) * n + tx * T + i] = Fl;
+                if (j == T - 1 && leaf_tiles_y_hi && (store_mask & 8))
+                    a.freg[(((size_t)leaf * 4 + kN) * 4 + k) * n + tx * T + i] = Fh;
+                double v = up[r][k] + dt * L;
+                if (a.stage > 1) v = a.a * un[r][k] + a.b * v;
+                o4[k] = v;
+            }
+            size_t off = (size_t)(ty * T + j) * n + tx * T + i;
+            double* po = a.Uout + (size_t)d.slot * PS + off;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) po[k * nn] = o4[k];
+            // cells on an edge that is the coarse side of a C/F face are finished by the reflux kernel
+            bool edge_cf = ((coarse_mask & 1) && leaf_tiles_x_lo && i == 0) ||
+                           ((coarse_mask & 2) && leaf_tiles_x_hi && i == T - 1) ||
+                           ((coarse_mask & 4) && leaf_tiles_y_lo && j == 0) ||
+                           ((coarse_mask & 8) && leaf_tiles_y_hi && j == T - 1);
+            if (!edge_cf) {
+                if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], g))
+                    report_error(a.err, d.slot, a.stage, (int)off);
+                if (a.want_lambda) {
+                    double s = wave_speed(o4[0], o4[1], o4[2], o4[3], g, idx, idy);
+                    unsigned long long b = (unsigned long long)__double_as_longlong(s);
+                    lam = b > lam ? b : lam;
+                }
+            }
+        }
+    }
+    if (a.want_lambda) {
+        lam = warp_max_u64(lam);
+        if ((tid & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
+    }
+}
+
+template <int SCHEME, int T>
+cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t s) {
+    constexpr size_t smem = stage_smem<SCHEME, T>();
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(stage_kernel<SCHEME, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    unsigned blocks = (unsigned)a.nleaves * a.tiles * a.tiles;
+    if (blocks == 0) return cudaSuccess;
+    stage_kernel<SCHEME, T><<<blocks, Block<T>::NT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int SCHEME>
+cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
+    int T = a.geo.n / a.tiles;
+    if (T == 8) return launch_stage_t<SCHEME, 8>(a, s);
+    if (T == 16) return launch_stage_t<SCHEME, 16>(a, s);
+    if (T == 32) return launch_stage_t<SCHEME, 32>(a, s);
+    return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------- coarse values for prolongation (O8)
+// Value of component k of coarse cell (rx, ry) given relative to the parent patch
+// (level l-1, position Pp, Qp); out-of-domain cells follow the BC rule (O7).
+__device__ __forceinline__ double coarse_value(const double* U, const int32_t* coarse, int n, int lc, int Pp, int Qp,
+                                               int rx, int ry, int k, const Geometry& geo) {
+    double sgn = 1.0;
+    int Ig = Pp * n + rx, Jg = Qp * n + ry;
+    const int NX = geo.nc[0][lc], NY = geo.nc[1][lc];
+    if (Ig < 0 && geo.bc[0] != kBcPeriodic) {
+        if (geo.bc[0] == kBcTransmissive) Ig = 0; else { Ig = -1 - Ig; if (k == 1) sgn = -1.0; }
+    } else if (Ig >= NX && geo.bc[1] != kBcPeriodic) {
+        if (geo.bc[1] == kBcTransmissive) Ig = NX - 1; else { Ig = 2 * NX - 1 - Ig; if (k == 1) sgn = -1.0; }
+    }
+    if (Jg < 0 && geo.bc[2] != kBcPeriodic) {
+        if (geo.bc[2] == kBcTransmissive) Jg = 0; else { Jg = -1 - Jg; if (k == 2) sgn = -1.0; }
+    } else if (Jg >= NY && geo.bc[3] != kBcPeriodic) {
+        if (geo.bc[3] == kBcTransmissive) Jg = NY - 1; else { Jg = 2 * NY - 1 - Jg; if (k == 2) sgn = -1.0; }
+    }
+    rx = Ig - Pp * n;
+    ry = Jg - Qp * n;
+    int bx = rx < 0 ? -1 : (rx >= n ? 1 : 0);
+    int by = ry < 0 ? -1 : (ry >= n ? 1 : 0);
+    int slot = coarse[(by + 1) * 3 + (bx + 1)];
+    int lx = rx - bx * n, ly = ry - by * n;
+    return sgn * U[(size_t)slot * 4 * n * n + (size_t)k * n * n + (size_t)ly * n + lx];
+}
+
+__device__ __forceinline__ double mc_limiter(double a, double b) {
+    if (a * b <= 0.0) return 0.0;
+    double m = fmin(fmin(2.0 * fabs(a), 2.0 * fabs(b)), fabs(a + b) * 0.5);
+    return a > 0.0 ? m : -m;
+}
+
+// O8 for fine cell (I, J) (global at level l, may be unwrapped by one patch)
+__device__ __forceinline__ double prolong_value(const double* U, const int32_t* coarse, int n, int l, int P, int Q,
+                                                int I, int J, int k, const Geometry& geo) {
+    int Pp = P >> 1, Qp = Q >> 1;
+    int Ic = I >> 1, Jc = J >> 1;   // arithmetic shift = floor division by 2
+    int ax = I & 1, by = J & 1;
+    int rx = Ic - Pp * n, ry = Jc - Qp * n;
+    double V = coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry, k, geo);
+    double sx = mc_limiter(V - coarse_value(U, coarse, n, l - 1, Pp, Qp, rx - 1, ry, k, geo),
+                           coarse_value(U, coarse, n, l - 1, Pp, Qp, rx + 1, ry, k, geo) - V);
+    double sy = mc_limiter(V - coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry - 1, k, geo),
+                           coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry + 1, k, geo) - V);
+    double t = V + ((2 * ax - 1) * 0.25) * sx;
+    return t + ((2 * by - 1) * 0.25) * sy;
+}
+
+// ---------------------------------------------------------------- ghost / proxy fill (O7, O8)
+__global__ void ghost_kernel(const ProxyTask* __restrict__ tasks, int ntasks, int g, const AuxArgs a) {
+    const int n = a.geo.n;
+    const int per = g * n;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)ntasks * per) return;
+    const int task = (int)(t / per), e = (int)(t - (long long)task * per);
+    const ProxyTask pt = tasks[task];
+    const int along = e % n, depth = e / n;
+    int li, lj;   // ghost cell, patch-local
+    switch (pt.side) {
+        case kW: li = depth - g; lj = along; break;
+        case kE: li = n + depth; lj = along; break;
+        case kS: li = along; lj = depth - g; break;
+        default: li = along; lj = n + depth; break;
+    }
+    const int pli = pt.side == kW ? li + n : (pt.side == kE ? li - n : li);
+    const int plj = pt.side == kS ? lj + n : (pt.side == kN ? lj - n : lj);
+    const size_t nn = (size_t)n * n;
+    double* dst = a.proxy + (size_t)pt.proxy * 4 * nn + (size_t)plj * n + pli;
+    if (pt.kind == 0) {
+        // physical boundary: source is an interior cell of the leaf itself (A25)
+        int bc = a.geo.bc[pt.side];
+        int si = li, sj = lj;
+        double sx = 1.0, sy = 1.0;
+        if (pt.side == kW) { si = bc == kBcTransmissive ? 0 : -1 - li; if (bc == kBcReflective) sx = -1.0; }
+        if (pt.side == kE) { si = bc == kBcTransmissive ? n - 1 : 2 * n - 1 - li; if (bc == kBcReflective) sx = -1.0; }
+        if (pt.side == kS) { sj = bc == kBcTransmissive ? 0 : -1 - lj; if (bc == kBcReflective) sy = -1.0; }
+        if (pt.side == kN) { sj = bc == kBcTransmissive ? n - 1 : 2 * n - 1 - lj; if (bc == kBcReflective) sy = -1.0; }
+        const double* src = a.U + (size_t)pt.slot * 4 * nn + (size_t)sj * n + si;
+        dst[0] = src[0];
+        dst[nn] = sx * src[nn];
+        dst[2 * nn] = sy * src[2 * nn];
+        dst[3 * nn] = src[3 * nn];
+    } else {
+        const int I = pt.P * n + li, J = pt.Q * n + lj;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            dst[k * nn] = prolong_value(a.U, pt.coarse, n, pt.level, pt.P, pt.Q, I, J, k, a.geo);
+    }
+}
+
+// ---------------------------------------------------------------- prolongation of new patches (O8)
+__global__ void prolong_kernel(const ProlongTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)ntasks * (long long)nn) return;
+    const int task = (int)(t / (long long)nn), e = (int)(t - (long long)task * nn);
+    const ProlongTask pt = tasks[task];
+    const int li = e % n, lj = e / n;
+    const int I = pt.P * n + li, J = pt.Q * n + lj;
+    double* dst = a.Uw + (size_t)pt.slot * 4 * nn + e;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[k * nn] = prolong_value(a.U, pt.coarse, n, pt.level, pt.P, pt.Q, I, J, k, a.geo);
+}
+
+// ---------------------------------------------------------------- restriction (O9)
+__global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)ntasks * (long long)nn) return;
+    const int task = (int)(t / (long long)nn), e = (int)(t - (long long)task * nn);
+    const RestrictTask rt = tasks[task];
+    const int i = e % n, j = e / n;
+    const int ca = (2 * i) / n, cb = (2 * j) / n;
+    const int fi = 2 * i - ca * n, fj = 2 * j - cb * n;
+    const double* f = a.Uw + (size_t)rt.child[ca + 2 * cb] * 4 * nn + (size_t)fj * n + fi;
+    double* dst = a.Uw + (size_t)rt.parent * 4 * nn + e;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double* fk = f + k * nn;
+        dst[k * nn] = ((fk[0] + fk[1]) + (fk[n] + fk[n + 1])) * 0.25;
+    }
+}
+
+// ---------------------------------------------------------------- flux correction (O12)
+__global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)ntasks * 4 * n) return;
+    const int task = (int)(t / (4 * n)), e = (int)(t - (long long)task * 4 * n);
+    const RefluxTask rt = tasks[task];
+    int i, j;
+    if (e < n) { i = 0; j = e; }
+    else if (e < 2 * n) { i = n - 1; j = e - n; }
+    else if (e < 3 * n) { i = e - 2 * n; j = 0; if (i == 0 || i == n - 1) return; }
+    else { i = e - 3 * n; j = n - 1; if (i == 0 || i == n - 1) return; }
+    int touch = (i == 0 ? 1 : 0) | (i == n - 1 ? 2 : 0) | (j == 0 ? 4 : 0) | (j == n - 1 ? 8 : 0);
+    int act = touch & rt.mask;
+    if (!act) return;
+    const double coef = a.b * (*a.dt);
+    double* U = a.Uw + (size_t)rt.slot * 4 * nn + (size_t)j * n + i;
+    double u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = U[k * nn];
+    const int l = rt.level;
+    // fixed order: x-low, x-high, y-low, y-high (bitwise rank invariance, O12)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        if (!(act & (1 << s))) continue;
+        const int along = s < 2 ? j : i;
+        const int opp = s ^ 1;
+        const double ih = s < 2 ? a.geo.inv_dx[l] : a.geo.inv_dy[l];
+        const double sigma = (s & 1) ? 1.0 : -1.0;
+        const int f0 = 2 * along, fl = f0 / n, fp = f0 - fl * n;
+        const int fleaf = rt.fine[s][fl];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            double Fc = a.freg[(((size_t)rt.leaf * 4 + s) * 4 + k) * n + along];
+            const double* ff = a.freg + (((size_t)fleaf * 4 + opp) * 4 + k) * n + fp;
+            double delta = Fc - 0.5 * (ff[0] + ff[1]);
+            u[k] += coef * sigma * delta * ih;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) U[k * nn] = u[k];
+    if (a.check && !physical_state(u[0], u[1], u[2], u[3], a.gamma)) report_error(a.err, rt.slot, a.stage, j * n + i);
+    if (a.want_lambda) {
+        double sp = wave_speed(u[0], u[1], u[2], u[3], a.gamma, a.geo.inv_dx[l], a.geo.inv_dy[l]);
+        atomicMax(a.lambda_bits, (unsigned long long)__double_as_longlong(sp));
+    }
+}
+
+// ---------------------------------------------------------------- Lambda (O13) over leaves
+__global__ void lambda_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs a) {
+    const LeafDesc d = leaves[blockIdx.x];
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n;
+    const double* U = a.U + (size_t)d.slot * 4 * nn;
+    unsigned long long lam = 0ull;
+    for (int e = threadIdx.x; e < (int)nn; e += blockDim.x) {
+        double s = wave_speed(U[e], U[nn + e], U[2 * nn + e], U[3 * nn + e], a.gamma, a.geo.inv_dx[d.level],
+                              a.geo.inv_dy[d.level]);
+        unsigned long long b = (unsigned long long)__double_as_longlong(s);
+        lam = b > lam ? b : lam;
+    }
+    lam = warp_max_u64(lam);
+    if ((threadIdx.x & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
+}
+
+__global__ void dt_kernel(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed, double cfl) {
+    double lam = __longlong_as_double((long long)*lambda_bits);
+    double d = dt_fixed > 0.0 ? dt_fixed : cfl / lam;
+    if (!(d > 0.0) || !isfinite(d)) {
+        if (atomicCAS(err, 0, 2) == 0) { err[1] = -1; err[2] = 0; err[3] = -1; }
+    }
+    *dt = d;
+    *lambda_bits = 0ull;
+}
+
+// ---------------------------------------------------------------- flags (O6)
+__global__ void flags_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs a, double* maxeta, int32_t* amb) {
+    const LeafDesc d = leaves[blockIdx.x];
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n, PS = 4 * nn;
+    const double* own = a.U + (size_t)d.slot * PS;
+    const double dx = a.geo.dx[d.level], dy = a.geo.dy[d.level];
+    const double th = a.theta, tc = a.theta * a.coarsen_fraction;
+    auto rho = [&](int i, int j) -> double {
+        const double* b = own;
+        if (i < 0) { int s = d.side[kW]; b = s >= 0 ? a.U + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS; i += n; }
+        else if (i >= n) { int s = d.side[kE]; b = s >= 0 ? a.U + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS; i -= n; }
+        else if (j < 0) { int s = d.side[kS]; b = s >= 0 ? a.U + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS; j += n; }
+        else if (j >= n) { int s = d.side[kN]; b = s >= 0 ? a.U + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS; j -= n; }
+        return b[(size_t)j * n + i];
+    };
+    unsigned long long m = 0ull;
+    int am = 0;
+    for (int e = threadIdx.x; e < (int)nn; e += blockDim.x) {
+        int i = e % n, j = e / n;
+        double gx = (rho(i + 1, j) - rho(i - 1, j)) / (2.0 * dx);
+        double gy = (rho(i, j + 1) - rho(i, j - 1)) / (2.0 * dy);
+        double eta = dx * sqrt(gx * gx + gy * gy) / rho(i, j);
+        unsigned long long b = (unsigned long long)__double_as_longlong(eta);
+        m = b > m ? b : m;
+        if (fabs(eta - th) <= 1e-9 * th || fabs(eta - tc) <= 1e-9 * tc) am = 1;
+    }
+    m = warp_max_u64(m);
+    am = __any_sync(0xffffffffu, am);
+    __shared__ unsigned long long sm[32];
+    __shared__ int sa[32];
+    if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = m; sa[threadIdx.x >> 5] = am; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long r = 0;
+        int ra = 0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) { r = sm[w] > r ? sm[w] : r; ra |= sa[w]; }
+        maxeta[blockIdx.x] = __longlong_as_double((long long)r);
+        amb[blockIdx.x] = ra;
+    }
+}
+
+// ---------------------------------------------------------------- totals (O18), fixed-order per-leaf sums
+__global__ void totals_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs a, double* partial) {
+    const LeafDesc d = leaves[blockIdx.x];
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n;
+    const double* U = a.U + (size_t)d.slot * 4 * nn;
+    __shared__ double s[4][256];
+    for (int k = 0; k < 4; ++k) {
+        double acc = 0.0;
+        for (int e = threadIdx.x; e < (int)nn; e += 256) acc += U[k * nn + e];
+        s[k][threadIdx.x] = acc;
+    }
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w)
+            for (int k = 0; k < 4; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double dv = a.geo.dx[d.level] * a.geo.dy[d.level];
+        for (int k = 0; k < 4; ++k) partial[4 * (size_t)blockIdx.x + k] = s[k][0] * dv;
+    }
+}
+
+// ---------------------------------------------------------------- packed <-> pool copies
+__global__ void scatter_kernel(const double* __restrict__ packed, const int32_t* __restrict__ slots, long long total,
+                               int ps, double* __restrict__ U, int to_pool) {
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long p = t / ps, e = t - p * ps;
+        size_t pool = (size_t)slots[p] * ps + e;
+        if (to_pool) U[pool] = packed[t];
+        else const_cast<double*>(packed)[t] = U[pool];
+    }
+}
+
+inline unsigned grid_for(long long work, int block) { return (unsigned)((work + block - 1) / block); }
+
+}  // namespace
+
+cudaError_t launch_stage(int scheme, const StageArgs& a, cudaStream_t s) {
+    if (scheme == 0) return launch_stage_s<0>(a, s);
+    if (scheme == 1) return launch_stage_s<1>(a, s);
+    return launch_stage_s<2>(a, s);
+}
+
+size_t stage_smem_bytes(int scheme, int n) {
+    int T = n > 32 ? 32 : n;
+    if (scheme == 0) return T == 8 ? stage_smem<0, 8>() : (T == 16 ? stage_smem<0, 16>() : stage_smem<0, 32>());
+    return T == 8 ? stage_smem<1, 8>() : (T == 16 ? stage_smem<1, 16>() : stage_smem<1, 32>());
+}
+
+cudaError_t launch_ghost(const ProxyTask* tasks, int ntasks, int g, const AuxArgs& a, cudaStream_t s) {
+    if (ntasks <= 0) return cudaSuccess;
+    long long work = (long long)ntasks * g * a.geo.n;
+    ghost_kernel<<<grid_for(work, 256), 256, 0, s>>>(tasks, ntasks, g, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reflux(const RefluxTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s) {
+    if (ntasks <= 0) return cudaSuccess;
+    long long work = (long long)ntasks * 4 * a.geo.n;
+    reflux_kernel<<<grid_for(work, 128), 128, 0, s>>>(tasks, ntasks, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_restrict(const RestrictTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s) {
+    if (ntasks <= 0) return cudaSuccess;
+    long long work = (long long)ntasks * a.geo.n * a.geo.n;
+    restrict_kernel<<<grid_for(work, 256), 256, 0, s>>>(tasks, ntasks, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prolong(const ProlongTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s) {
+    if (ntasks <= 0) return cudaSuccess;
+    long long work = (long long)ntasks * a.geo.n * a.geo.n;
+    prolong_kernel<<<grid_for(work, 256), 256, 0, s>>>(tasks, ntasks, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lambda(const LeafDesc* leaves, int nleaves, const AuxArgs& a, cudaStream_t s) {
+    if (nleaves <= 0) return cudaSuccess;
+    lambda_kernel<<<nleaves, 256, 0, s>>>(leaves, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed, double cfl,
+                      cudaStream_t s) {
+    dt_kernel<<<1, 1, 0, s>>>(dt, lambda_bits, err, dt_fixed, cfl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* maxeta, int32_t* amb,
+                         cudaStream_t s) {
+    if (nleaves <= 0) return cudaSuccess;
+    flags_kernel<<<nleaves, 256, 0, s>>>(leaves, a, maxeta, amb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int n, cudaStream_t s) {
+    if (npatch <= 0) return cudaSuccess;
+    long long total = (long long)npatch * 4 * n * n;
+    unsigned blocks = grid_for(total, 256);
+    if (blocks > 148u * 64u) blocks = 148u * 64u;
+    scatter_kernel<<<blocks, 256, 0, s>>>(packed, slots, total, 4 * n * n, U, 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int n, cudaStream_t s) {
+    if (npatch <= 0) return cudaSuccess;
+    long long total = (long long)npatch * 4 * n * n;
+    unsigned blocks = grid_for(total, 256);
+    if (blocks > 148u * 64u) blocks = 148u * 64u;
+    scatter_kernel<<<blocks, 256, 0, s>>>(packed, slots, total, 4 * n * n, const_cast<double*>(U), 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* partial, cudaStream_t s) {
+    if (nleaves <= 0) return cudaSuccess;
+    totals_kernel<<<nleaves, 256, 0, s>>>(leaves, a, partial);
+    return cudaGetLastError();
+}
+
+}  // namespace amr

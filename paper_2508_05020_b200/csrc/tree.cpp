@@ -1,0 +1,165 @@
+// tree.cpp -- see tree.h.  Citations: PAPER.md (P:Lnn), DESIGN.md s3 readings.
+#include "tree.h"
+
+#include <algorithm>
+#include <functional>
+
+namespace amr {
+
+namespace {
+// Fig. 2 nbr order: N, E, S, W, NE, SE, SW, NW
+const int kMoore[8][2] = {{0, 1}, {1, 0}, {0, -1}, {-1, 0}, {1, 1}, {1, -1}, {-1, -1}, {-1, 1}};
+inline int pmod(int a, int b) { int r = a % b; return r < 0 ? r + b : r; }
+}  // namespace
+
+void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, int rule) {
+    np0[0] = npx; np0[1] = npy; levels = nlev;
+    periodic[0] = perx; periodic[1] = pery;
+    capacity = cap; coarsen_rule = rule;
+    lev.assign(cap, -1); pi.assign(cap, 0); pj.assign(cap, 0); parent.assign(cap, -1);
+    child.assign(4 * (size_t)cap, -1); alive.assign(cap, 0);
+    n_alive = 0;
+    index_.clear();
+    index_.reserve((size_t)npx * npy * 2);
+    free_.clear();
+    for (int s = cap - 1; s >= 0; --s) free_.push_back(s);
+    std::make_heap(free_.begin(), free_.end(), std::greater<int32_t>());
+    // R1: the permanent root scaffold, created row by row
+    for (int j = 0; j < npy; ++j)
+        for (int i = 0; i < npx; ++i) alloc(0, i, j);
+}
+
+int PatchTree::alloc(int l, int i, int j) {
+    std::pop_heap(free_.begin(), free_.end(), std::greater<int32_t>());
+    int id = free_.back();
+    free_.pop_back();
+    lev[id] = l; pi[id] = i; pj[id] = j; parent[id] = -1; alive[id] = 1;
+    for (int c = 0; c < 4; ++c) child[4 * id + c] = -1;
+    index_[key(l, i, j)] = id;
+    ++n_alive;
+    return id;
+}
+
+void PatchTree::release(int id) {
+    index_.erase(key(lev[id], pi[id], pj[id]));
+    alive[id] = 0; lev[id] = -1; parent[id] = -1;
+    for (int c = 0; c < 4; ++c) child[4 * id + c] = -1;
+    free_.push_back(id);
+    std::push_heap(free_.begin(), free_.end(), std::greater<int32_t>());
+    --n_alive;
+}
+
+bool PatchTree::wrap(int l, int& i, int& j) const {
+    int nx = npatch(0, l), ny = npatch(1, l);
+    if (i < 0 || i >= nx) { if (!periodic[0]) return false; i = pmod(i, nx); }
+    if (j < 0 || j >= ny) { if (!periodic[1]) return false; j = pmod(j, ny); }
+    return true;
+}
+
+int PatchTree::find(int l, int i, int j) const {
+    if (l < 0 || l >= levels || !wrap(l, i, j)) return -1;
+    auto it = index_.find(key(l, i, j));
+    return it == index_.end() ? -1 : it->second;
+}
+
+int PatchTree::neighbour(int id, int dx, int dy) const {
+    int l = lev[id], i = pi[id] + dx, j = pj[id] + dy;
+    if (!wrap(l, i, j)) return -2;
+    auto it = index_.find(key(l, i, j));
+    return it == index_.end() ? -1 : it->second;
+}
+
+// Alg. 1 RefinePatch: before creating p's children make every
+// Moore position of p active, refining the corresponding neighbour of p's
+// parent (which exists by R2) recursively.
+bool PatchTree::refine(int id, std::string& err) {
+    if (has_children(id)) return true;
+    int l = lev[id];
+    if (l + 1 >= levels) { err = "refine beyond the finest level"; return false; }
+    for (int d = 0; d < 8; ++d) {
+        int q = neighbour(id, kMoore[d][0], kMoore[d][1]);
+        if (q != -1) continue;          // exists, or outside the domain (ghost patch)
+        int i = pi[id] + kMoore[d][0], j = pj[id] + kMoore[d][1];
+        wrap(l, i, j);
+        int r = find(l - 1, i >> 1, j >> 1);
+        if (l == 0 || r < 0) { err = "R2 violated: no coarse support for refinement"; return false; }
+        if (!refine(r, err)) return false;
+    }
+    if ((int)free_.size() < 4) { err = "slot capacity exceeded"; return false; }
+    for (int c = 0; c < 4; ++c) {
+        int a = c & 1, b = c >> 1;
+        int k = alloc(l + 1, 2 * pi[id] + a, 2 * pj[id] + b);
+        parent[k] = id;
+        child[4 * id + c] = k;
+    }
+    return true;
+}
+
+// IsCoarseningAllowed (Alg. 2) -- rule 1 literal; rule 0 the prose
+// condition of P:L259 (A16): children are leaves and none of them serves as a
+// Moore neighbour of a level-(l+1) patch that has children.
+bool PatchTree::coarsen_allowed(int id) const {
+    if (!has_children(id)) return false;
+    for (int c = 0; c < 4; ++c)
+        if (has_children(child[4 * id + c])) return false;
+    if (coarsen_rule == 1) {
+        if (lev[id] == 0) return false;
+        for (int d = 0; d < 8; ++d) {
+            int q = neighbour(id, kMoore[d][0], kMoore[d][1]);
+            if (q >= 0 && has_children(q)) return false;
+        }
+        return true;
+    }
+    for (int c = 0; c < 4; ++c) {
+        int k = child[4 * id + c];
+        for (int d = 0; d < 8; ++d) {
+            int q = neighbour(k, kMoore[d][0], kMoore[d][1]);
+            if (q >= 0 && parent[q] != id && has_children(q)) return false;
+        }
+    }
+    return true;
+}
+
+void PatchTree::delete_children(int id) {
+    for (int c = 0; c < 4; ++c) {
+        int k = child[4 * id + c];
+        if (k >= 0) release(k);
+        child[4 * id + c] = -1;
+    }
+}
+
+bool PatchTree::validate(std::string& err) const {
+    for (int j = 0; j < np0[1]; ++j)
+        for (int i = 0; i < np0[0]; ++i)
+            if (find(0, i, j) < 0) { err = "R1 violated: root missing"; return false; }
+    for (int id = 0; id < capacity; ++id) {
+        if (!alive[id]) continue;
+        if (lev[id] > 0) {
+            int p = parent[id];
+            if (p < 0 || !alive[p]) { err = "orphan patch"; return false; }
+        }
+        int nc = 0;
+        for (int c = 0; c < 4; ++c) nc += child[4 * id + c] >= 0;
+        if (nc != 0 && nc != 4) { err = "children not all-or-none"; return false; }
+        if (nc == 4) {
+            for (int d = 0; d < 8; ++d)
+                if (neighbour(id, kMoore[d][0], kMoore[d][1]) == -1) { err = "R2 violated"; return false; }
+        }
+    }
+    return true;
+}
+
+std::vector<int32_t> PatchTree::canonical() const {
+    std::vector<int32_t> ids;
+    ids.reserve(n_alive);
+    for (int id = 0; id < capacity; ++id)
+        if (alive[id]) ids.push_back(id);
+    std::sort(ids.begin(), ids.end(), [&](int a, int b) {
+        if (lev[a] != lev[b]) return lev[a] < lev[b];
+        if (pj[a] != pj[b]) return pj[a] < pj[b];
+        return pi[a] < pi[b];
+    });
+    return ids;
+}
+
+}  // namespace amr

@@ -1,0 +1,102 @@
+"""CPU checks of the C-ABI library: it builds for sm_100a, loads, exports every symbol include/amr.h
+declares, and rejects invalid configurations before touching a device (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_2508_05020_b200 as amr
+from paper_2508_05020_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return amr.load()
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "amr.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(amr_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_and_binding_agree():
+    assert declared_symbols() == sorted(amr.ABI_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+
+
+def test_struct_sizes_match_header(lib):
+    # amr_default_config writes sizeof(amr_config) bytes: a Python struct that is too small would be overrun
+    buf = (C.c_uint8 * (C.sizeof(amr.amr_config) + 64))()
+    for e in range(len(buf)):
+        buf[e] = 0xAB
+    assert lib.amr_default_config(C.cast(buf, C.POINTER(amr.amr_config))) == 0
+    tail = bytes(buf[C.sizeof(amr.amr_config):])
+    assert tail == b"\xab" * 64
+    c = C.cast(buf, C.POINTER(amr.amr_config)).contents
+    assert c.dim == 2 and c.ratio == 2 and c.gamma == 1.4 and c.div_order == 4 and c.weno_eps == 1e-6
+    assert lib.amr_abi_version() == 1
+
+
+def _cfg(lib, **kw):
+    c = amr.amr_config()
+    lib.amr_default_config(C.byref(c))
+    for k, v in kw.items():
+        if isinstance(v, (list, tuple)):
+            arr = getattr(c, k)
+            for e, x in enumerate(v):
+                arr[e] = x
+        else:
+            setattr(c, k, v)
+    return c
+
+
+@pytest.mark.parametrize("kw", [
+    dict(patch_cells=12),
+    dict(base_cells=(60, 64)),
+    dict(ratio=3),
+    dict(num_levels=0),
+    dict(bc=(0, 1, 0, 0)),
+    dict(scheme=7),
+    dict(div_order=3),
+    dict(gamma=1.0),
+    dict(dim=1, base_cells=(64, 32)),
+    dict(world_size=2, rank=0),
+    dict(world_size=1, rank=1),
+    dict(hi=(0.0, 1.0)),
+])
+def test_invalid_config_rejected_without_device(lib, kw):
+    c = _cfg(lib, **kw)
+    h = C.c_void_p()
+    rc = lib.amr_create(C.byref(c), C.byref(h))
+    assert rc in (amr.AMR_E_CONFIG, amr.AMR_E_ARG) and not h.value
+
+
+def test_null_arguments(lib):
+    assert lib.amr_default_config(None) == amr.AMR_E_ARG
+    h = C.c_void_p()
+    assert lib.amr_create(None, C.byref(h)) == amr.AMR_E_ARG
+    assert lib.amr_step(None, 0.1, 0.0, None) == amr.AMR_E_ARG
+    assert lib.amr_last_error(None) == b"null context"
+
+
+def test_pool_bytes(lib):
+    c = _cfg(lib, patch_cells=32, max_patches=100)
+    b = C.c_uint64()
+    assert lib.amr_query_pool_bytes(C.byref(c), C.byref(b)) == 0
+    assert b.value == 3 * 100 * 4 * 32 * 32 * 8
+
+
+def test_sass_is_sm100a(lib):
+    """The library carries sm_100a SASS for the fused stage kernel."""
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", amr.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout

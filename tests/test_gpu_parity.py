@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle, element by element (1e-11, O18), trees and
+flags in lockstep (A32).  Sizes span several tiles/patches with ragged level structure; full-size configs are
+checked on sampled patches (test_gpu_fullsize.py)."""
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2508_05020_b200 as amr
+import workloads as W
+from tests.parity import parity_error, run_pair
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+def test_vortex_central4_uniform(n):
+    """BJ configs[1] scaled to 128^2 (256^2 for n = 64 so there are several patches): 10 CFL-0.5 steps."""
+    N = 256 if n == 64 else 128
+    run_pair(W.vortex(N=N, n=n), steps=10, cfl=0.5)
+
+
+@pytest.mark.parametrize("char", [1, 0])
+def test_vortex_weno_uniform(char):
+    run_pair(W.vortex(N=128, n=32, scheme="weno5", characteristic=char), steps=10, cfl=0.5)
+
+
+@pytest.mark.parametrize("div", [2, 4])
+@pytest.mark.parametrize("scheme", ["central4", "weno5"])
+def test_divergence_orders(scheme, div):
+    run_pair(W.vortex(N=64, n=16, scheme=scheme, div_order=div), steps=5, cfl=0.4)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_quadrant_amr_lockstep(seed):
+    """BJ configs[2] at 64^2 base, 3 levels, 16^2 patches, transmissive, WENO5-char, regrid every 4 steps."""
+    cfg = W.quadrant(N=64, n=16, levels=3, seed=seed)
+    stats = {}
+    o, g, e = run_pair(cfg, steps=10, cfl=0.5, regrid_every=4, stats=stats)
+    levels = {k[0] for k in g.leaves()}
+    assert len(levels) >= 2
+
+
+def test_sod_strip_two_levels():
+    """BJ configs[0] (A21/A23): 13 roots of 16^2, transmissive x, periodic y (dim = 1 strip), 2 levels."""
+    cfg = dict(W.sod(), dim=1)
+    run_pair(cfg, steps=10, cfl=0.5, regrid_every=4)
+
+
+def test_shock_bubble_reflective_amr():
+    """BJ configs[3] at 128x64 base, 3 levels: reflective walls (mirror + negated normal momentum)."""
+    cfg = W.shock_bubble(Nx=128, Ny=64, n=16, levels=3)
+    run_pair(cfg, steps=10, cfl=0.5, regrid_every=4)
+
+
+def test_blast_periodic_amr_component_weno():
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(64, 64), n=8, levels=3, bc=("periodic",) * 4,
+               scheme="weno5", characteristic=0, div_order=4, ic="blast", blast_width=0.08, theta=0.02,
+               coarsen_frac=0.25, weno_eps=1e-6, gamma=1.4, cfl=0.4)
+    run_pair(cfg, steps=10, regrid_every=4, check_each=True)
+
+
+def test_free_stream_bitwise_gpu_amr():
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(32, 32), n=8, levels=3,
+               bc=("transmissive", "transmissive", "reflective", "reflective"), scheme="weno5", characteristic=1,
+               div_order=4, ic="uniform", uniform_state=(1.3, 0.4, 0.0, 0.9))
+    g = amr.Mesh(cfg)
+    g.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    g.regrid_with_requests([(0, 1, 1), (0, 2, 1), (0, 0, 3)])
+    g.regrid_with_requests([(1, 3, 3), (1, 2, 2)])
+    g.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    before = g.get_state()
+    for _ in range(3):
+        g.step(cfl=0.5)
+    after = g.get_state()
+    for k in before:
+        assert np.array_equal(before[k], after[k]), k
+
+
+def test_conservation_gpu_periodic_amr():
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(64, 64), n=16, levels=3, bc=("periodic",) * 4,
+               scheme="weno5", characteristic=1, div_order=4, ic="blast", blast_width=0.08, theta=0.02,
+               coarsen_frac=0.25, weno_eps=1e-6, gamma=1.4)
+    g = amr.Mesh(cfg)
+    fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+    g.set_state(fn)
+    for _ in range(2):
+        g.regrid()
+        g.set_state(fn)
+    t0, _ = g.diagnostics()
+    st = g.get_state()
+    scale = sum(np.abs(U).sum(axis=(1, 2)) * (1.0 / (64 << l)) ** 2 for (l, P, Q), U in st.items()
+                if (l, P, Q) in set(g.leaves()))
+    for s in range(1, 11):
+        g.step(cfl=0.4)
+        if s % 4 == 0:
+            g.regrid()
+    t1, _ = g.diagnostics()
+    assert np.all(np.abs(t1 - t0) <= 1e-12 * scale), (t1 - t0) / scale
+
+
+@pytest.mark.parametrize("scheme", ["central4", "weno5"])
+def test_patch_size_invariance_bitwise(scheme):
+    """on a uniform periodic mesh the decomposition is invisible: n = 8/16/32/64 give bitwise-equal states."""
+    res = {}
+    for n in (8, 16, 32, 64):
+        cfg = W.sweep(N=128, n=n, scheme=scheme, seed=3)
+        cfg["ic"] = "smooth"
+        g = amr.Mesh(cfg)
+        U0 = W.level0_state(cfg)
+        g.set_state(U=U0.reshape(-1, 4, n, n))
+        for _ in range(3):
+            g.step(dt=1e-5)
+        U = g.get_state(as_dict=False).reshape(128 // n, 128 // n, 4, n, n).transpose(2, 0, 3, 1, 4).reshape(4, 128, 128)
+        res[n] = U
+    for n in (16, 32, 64):
+        assert np.array_equal(res[8], res[n]), n
+
+
+def test_single_root_periodic_self_neighbour():
+    """a 1x1 periodic scaffold is its own neighbour in all 8 directions."""
+    cfg = W.vortex(N=32, n=32, L=10.0)
+    g = amr.Mesh(cfg)
+    d = g.tree()[0]
+    assert list(d.nbr) == [0] * 8
+    run_pair(cfg, steps=3, cfl=0.5)
+
+
+def test_nonphysical_step_not_committed():
+    cfg = W.sweep(N=64, n=16, scheme="central4", seed=5)
+    g = amr.Mesh(cfg)
+    U0 = W.level0_state(cfg).reshape(-1, 4, 16, 16).copy()
+    U0[5, 0, 3, 3] = -1.0            # negative density
+    g.set_state(U=U0)
+    before = g.get_state(as_dict=False)
+    with pytest.raises(amr.AmrError) as ei:
+        g.step(dt=1e-4)
+    assert ei.value.code == amr.AMR_E_NONPHYSICAL
+    assert "stage" in str(ei.value)
+    assert np.array_equal(before, g.get_state(as_dict=False))
+
+
+def test_capacity_error_leaves_mesh_unchanged():
+    cfg = dict(W.quadrant(N=64, n=16, levels=3), max_patches=20)
+    g = amr.Mesh(cfg)
+    g.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    keys = g.keys()
+    with pytest.raises(amr.AmrError) as ei:
+        g.regrid_with_requests([(0, 1, 1), (0, 2, 2)])
+    assert ei.value.code == amr.AMR_E_CAPACITY
+    assert g.keys() == keys
+    g.step(cfl=0.5)
+
+
+def test_tree_matches_oracle_after_random_requests():
+    cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(32, 32), n=8, levels=4, bc=("periodic",) * 4,
+               scheme="central4", ic="uniform")
+    rng = np.random.default_rng(0)
+    o = orc.Oracle(cfg)
+    g = amr.Mesh(cfg)
+    fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+    o.set_state(fn)
+    g.set_state(fn)
+    for it in range(30):
+        tr = o.tree()
+        leaves = [(l, P, Q) for (l, P, Q, lf) in tr if lf and l < 3]
+        parents = [(l, P, Q) for (l, P, Q, lf) in tr if not lf]
+        ref = [leaves[i] for i in rng.choice(len(leaves), size=min(3, len(leaves)), replace=False)]
+        crs = [parents[i] for i in rng.choice(len(parents), size=min(2, len(parents)), replace=False)] if parents else []
+        assert o.regrid_with_requests(ref, crs) == g.regrid_with_requests(ref, crs)
+        assert [(l, P, Q) for (l, P, Q, _) in o.tree()] == g.keys()
+    e, _ = parity_error(o.get_state(), g.get_state())
+    assert e == 0.0
