@@ -74,70 +74,78 @@ __device__ __forceinline__ double weno5(double v0, double v1, double v2, double 
     return (w0 * q0 + w1 * q1 + w2 * q2) / (w0 + w1 + w2);
 }
 
-// WENO5 + Rusanov flux at one face in the face-normal frame.  c[s][k], s = cells
-// i-2..i+3, k = (rho, normal momentum, tangential momentum, rho e).
+// WENO5 + Rusanov flux at one face in the face-normal frame (O10).
+// q points at component 0 of cell i-2 (the first of the 6 stencil cells) in shared memory;
+// cs = cell stride along the face normal, plane = component stride, kn / kt = components of
+// the normal / tangential momentum.  Each characteristic field re-reads its 6 x 4 stencil from
+// shared memory (keeps the live register set small; shared-memory bandwidth is not the limit).
 template <bool CHAR>
-__device__ __forceinline__ void weno_rusanov(const double (&c)[6][4], double g, double eps, double F[4]) {
+__device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int cs, int plane, int kn, int kt, double g,
+                                             double eps, double F[4]) {
     const double gm1 = g - 1.0;
+#define QV(s, k) q[(k) * plane + (s) * cs]
     double wl[4], wr[4];
-    double u = 0.0, v = 0.0, cs = 0.0, q = 0.0, H = 0.0;
+    double u = 0.0, v = 0.0, c = 0.0, qk = 0.0, H = 0.0;
     if (CHAR) {
         // eigen-system at the arithmetic-mean primitive state of cells i, i+1 (A4)
-        double iL = 1.0 / c[2][0], iR = 1.0 / c[3][0];
-        double uL = c[2][1] * iL, vL = c[2][2] * iL;
-        double uR = c[3][1] * iR, vR = c[3][2] * iR;
-        double pL = gm1 * (c[2][3] - 0.5 * (c[2][1] * uL + c[2][2] * vL));
-        double pR = gm1 * (c[3][3] - 0.5 * (c[3][1] * uR + c[3][2] * vR));
-        double r = 0.5 * (c[2][0] + c[3][0]);
+        double rL = QV(2, 0), rR = QV(3, 0);
+        double iL = 1.0 / rL, iR = 1.0 / rR;
+        double uL = QV(2, kn) * iL, vL = QV(2, kt) * iL;
+        double uR = QV(3, kn) * iR, vR = QV(3, kt) * iR;
+        double pL = gm1 * (QV(2, 3) - 0.5 * (QV(2, kn) * uL + QV(2, kt) * vL));
+        double pR = gm1 * (QV(3, 3) - 0.5 * (QV(3, kn) * uR + QV(3, kt) * vR));
+        double r = 0.5 * (rL + rR);
         u = 0.5 * (uL + uR);
         v = 0.5 * (vL + vR);
         double p = 0.5 * (pL + pR);
         double c2 = g * p / r;
-        cs = sqrt(c2);
-        double ic = 1.0 / cs;
-        q = 0.5 * (u * u + v * v);
-        H = c2 / gm1 + q;
+        c = sqrt(c2);
+        double ic = 1.0 / c;
+        qk = 0.5 * (u * u + v * v);
+        H = c2 / gm1 + qk;
         double b1 = gm1 / c2;
-        double b2 = b1 * q;
-        // rows of L (O10): l1, l2, l3, l4
-        const double L0[4] = {0.5 * (b2 + u * ic), 0.5 * (-b1 * u - ic), 0.5 * (-b1 * v), 0.5 * b1};
-        const double L1[4] = {1.0 - b2, b1 * u, b1 * v, -b1};
-        const double L3[4] = {0.5 * (b2 - u * ic), 0.5 * (-b1 * u + ic), 0.5 * (-b1 * v), 0.5 * b1};
+        double b2 = b1 * qk;
+        // rows of L (O10): l1 = 1/2 (b2 + u/c, -b1 u - 1/c, -b1 v, b1), l2, l3 = (-v, 0, 1, 0), l4
+        const double h1 = 0.5 * (b2 + u * ic), h2 = 0.5 * (-b1 * u - ic), h3 = 0.5 * (-b1 * v), h4 = 0.5 * b1;
+        const double m1 = 1.0 - b2, m2 = b1 * u, m3 = b1 * v, m4 = -b1;
+        const double k1 = 0.5 * (b2 - u * ic), k2 = 0.5 * (-b1 * u + ic);
         double w[6];
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = L0[0] * c[s][0] + L0[1] * c[s][1] + L0[2] * c[s][2] + L0[3] * c[s][3];
+        for (int s = 0; s < 6; ++s) w[s] = h1 * QV(s, 0) + h2 * QV(s, kn) + h3 * QV(s, kt) + h4 * QV(s, 3);
         wl[0] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
         wr[0] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = L1[0] * c[s][0] + L1[1] * c[s][1] + L1[2] * c[s][2] + L1[3] * c[s][3];
+        for (int s = 0; s < 6; ++s) w[s] = m1 * QV(s, 0) + m2 * QV(s, kn) + m3 * QV(s, kt) + m4 * QV(s, 3);
         wl[1] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
         wr[1] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = -v * c[s][0] + c[s][2];
+        for (int s = 0; s < 6; ++s) w[s] = -v * QV(s, 0) + QV(s, kt);
         wl[2] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
         wr[2] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = L3[0] * c[s][0] + L3[1] * c[s][1] + L3[2] * c[s][2] + L3[3] * c[s][3];
+        for (int s = 0; s < 6; ++s) w[s] = k1 * QV(s, 0) + k2 * QV(s, kn) + h3 * QV(s, kt) + h4 * QV(s, 3);
         wl[3] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
         wr[3] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
     } else {
+        const int kk[4] = {0, kn, kt, 3};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            wl[k] = weno5(c[0][k], c[1][k], c[2][k], c[3][k], c[4][k], eps);
-            wr[k] = weno5(c[5][k], c[4][k], c[3][k], c[2][k], c[1][k], eps);
+            wl[k] = weno5(QV(0, kk[k]), QV(1, kk[k]), QV(2, kk[k]), QV(3, kk[k]), QV(4, kk[k]), eps);
+            wr[k] = weno5(QV(5, kk[k]), QV(4, kk[k]), QV(3, kk[k]), QV(2, kk[k]), QV(1, kk[k]), eps);
         }
     }
+#undef QV
     double UL[4], UR[4];
     if (CHAR) {
         // U = R w, columns r1 = (1, u-c, v, H-uc), r2 = (1, u, v, q), r3 = (0,0,1,v), r4 = (1, u+c, v, H+uc)
         UL[0] = wl[0] + wl[1] + wl[3];
-        UL[1] = (u - cs) * wl[0] + u * wl[1] + (u + cs) * wl[3];
+        UL[1] = (u - c) * wl[0] + u * wl[1] + (u + c) * wl[3];
         UL[2] = v * wl[0] + v * wl[1] + wl[2] + v * wl[3];
-        UL[3] = (H - u * cs) * wl[0] + q * wl[1] + v * wl[2] + (H + u * cs) * wl[3];
+        UL[3] = (H - u * c) * wl[0] + qk * wl[1] + v * wl[2] + (H + u * c) * wl[3];
         UR[0] = wr[0] + wr[1] + wr[3];
-        UR[1] = (u - cs) * wr[0] + u * wr[1] + (u + cs) * wr[3];
+        UR[1] = (u - c) * wr[0] + u * wr[1] + (u + c) * wr[3];
         UR[2] = v * wr[0] + v * wr[1] + wr[2] + v * wr[3];
-        UR[3] = (H - u * cs) * wr[0] + q * wr[1] + v * wr[2] + (H + u * cs) * wr[3];
+        UR[3] = (H - u * c) * wr[0] + qk * wr[1] + v * wr[2] + (H + u * c) * wr[3];
     } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) { UL[k] = wl[k]; UR[k] = wr[k]; }
@@ -151,22 +159,24 @@ __device__ __forceinline__ void weno_rusanov(const double (&c)[6][4], double g, 
     double sL = sqrt(g * pL * irL) + fabs(unL);
     double sR = sqrt(g * pR * irR) + fabs(unR);
     double S = fmax(sR, sL);
-    double FL0 = UL[1], FL1 = UL[1] * unL + pL, FL2 = UL[2] * unL, FL3 = (UL[3] + pL) * unL;
-    double FR0 = UR[1], FR1 = UR[1] * unR + pR, FR2 = UR[2] * unR, FR3 = (UR[3] + pR) * unR;
-    F[0] = 0.5 * (FR0 + FL0) - 0.5 * S * (UR[0] - UL[0]);
-    F[1] = 0.5 * (FR1 + FL1) - 0.5 * S * (UR[1] - UL[1]);
-    F[2] = 0.5 * (FR2 + FL2) - 0.5 * S * (UR[2] - UL[2]);
-    F[3] = 0.5 * (FR3 + FL3) - 0.5 * S * (UR[3] - UL[3]);
+    F[0] = 0.5 * (UR[1] + UL[1]) - 0.5 * S * (UR[0] - UL[0]);
+    F[1] = 0.5 * ((UR[1] * unR + pR) + (UL[1] * unL + pL)) - 0.5 * S * (UR[1] - UL[1]);
+    F[2] = 0.5 * (UR[2] * unR + UL[2] * unL) - 0.5 * S * (UR[2] - UL[2]);
+    F[3] = 0.5 * ((UR[3] + pR) * unR + (UL[3] + pL) * unL) - 0.5 * S * (UR[3] - UL[3]);
 }
 
-// Central4 edge flux: Eq. 8 weights (9/16, -1/16) applied edge-from-node
-// (A7) to (p, T = p/rho, u_n, u_t) of cells i-1..i+2; rho_e = p_e / T_e (A6).
-__device__ __forceinline__ void central4_flux(const double (&c)[4][4], double inv_gm1, double F[4]) {
-    double e[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) e[k] = 0.5625 * (c[1][k] + c[2][k]) - 0.0625 * (c[0][k] + c[3][k]);
-    double pe = e[0], un = e[2], ut = e[3];
-    double re = pe / e[1];
+// Central4 edge flux: Eq. 8 weights (9/16, -1/16) applied edge-from-node (A7)
+// to (p, T = p/rho, u_n, u_t) of cells i-1..i+2; rho_e = p_e / T_e (A6).
+// q points at component 0 (p) of cell i-1 in shared memory (components p, T, u, v).
+__device__ __forceinline__ void central4_flux(const double* __restrict__ q, int cs, int plane, int kn, int kt,
+                                              double inv_gm1, double F[4]) {
+#define QV(s, k) q[(k) * plane + (s) * cs]
+    double pe = 0.5625 * (QV(1, 0) + QV(2, 0)) - 0.0625 * (QV(0, 0) + QV(3, 0));
+    double Te = 0.5625 * (QV(1, 1) + QV(2, 1)) - 0.0625 * (QV(0, 1) + QV(3, 1));
+    double un = 0.5625 * (QV(1, kn) + QV(2, kn)) - 0.0625 * (QV(0, kn) + QV(3, kn));
+    double ut = 0.5625 * (QV(1, kt) + QV(2, kt)) - 0.0625 * (QV(0, kt) + QV(3, kt));
+#undef QV
+    double re = pe / Te;
     double Ee = pe * inv_gm1 + 0.5 * re * (un * un + ut * ut);
     double mn = re * un;
     F[0] = mn;
@@ -176,40 +186,42 @@ __device__ __forceinline__ void central4_flux(const double (&c)[4][4], double in
 }
 
 // ---------------------------------------------------------------- the fused stage kernel
-template <int SCHEME>
-struct Traits;
-template <>
-struct Traits<0> { static constexpr int G = 3; };   // Central4 + Eq. 9: cells i-3..i+3
-template <>
-struct Traits<1> { static constexpr int G = 4; };   // WENO5 + Eq. 9: cells i-4..i+4 (A8)
-template <>
-struct Traits<2> { static constexpr int G = 4; };
+constexpr int kGL = 4;   // ghost width loaded into shared memory (16-byte aligned strips, A8)
 
 template <int T>
 struct Block;
 template <>
-struct Block<8> { static constexpr int NT = 64; };
+struct Block<8> { static constexpr int NT = 64; static constexpr int MINB = 8; };
 template <>
-struct Block<16> { static constexpr int NT = 160; };
+struct Block<16> { static constexpr int NT = 128; static constexpr int MINB = 4; };
 template <>
-struct Block<32> { static constexpr int NT = 256; };
+struct Block<32> { static constexpr int NT = 256; static constexpr int MINB = 2; };
 
 template <int SCHEME, int T>
 constexpr size_t stage_smem() {
-    return sizeof(double) * (4 * (T + 2 * Traits<SCHEME>::G) * (T + 2 * Traits<SCHEME>::G) + 4 * T * (T + 3));
+    return sizeof(double) * (4 * (T + 2 * kGL) * (T + 2 * kGL) + 4 * T * (T + 3));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
 // SCHEME 0: Central4; 1: WENO5 characteristic; 2: WENO5 component-wise.
+// One CTA per T x T tile of a leaf patch (T = n, or 32 for n = 64).
 template <int SCHEME, int T>
-__global__ void __launch_bounds__(Block<T>::NT) stage_kernel(const StageArgs a) {
-    constexpr int G = Traits<SCHEME>::G;
+__global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(const StageArgs a) {
+    constexpr int G = kGL;
     constexpr int NT = Block<T>::NT;
-    constexpr int W = T + 2 * G;       // tile row width in shared memory
+    constexpr int W = T + 2 * G;       // tile row width in shared memory (doubles)
+    constexpr int PL = W * W;          // one component plane
     constexpr int NF = T + 3;          // faces per row: m = -1 .. T+1 (face m = left of cell m)
     constexpr int CPT = (T * T + NT - 1) / NT;
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
     double* sQ = smem;                 // [4][W][W]: conserved (WENO) / (p, T, u, v) (Central4)
-    double* sF = smem + 4 * W * W;     // [4][T][NF] x-fluxes, then [4][NF][T] y-fluxes
+    double* sF = smem + 4 * PL;        // [4][T][NF] x-fluxes, then [4][NF][T] y-fluxes
 
     const int tid = threadIdx.x;
     const int tiles2 = a.tiles * a.tiles;
@@ -221,75 +233,50 @@ __global__ void __launch_bounds__(Block<T>::NT) stage_kernel(const StageArgs a) 
     const size_t nn = (size_t)n * n;
     const size_t PS = 4 * nn;
     const double* own = a.Uin + (size_t)d.slot * PS;
-    const double* srcs[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-        srcs[s] = d.side[s] >= 0 ? a.Uin + (size_t)d.side[s] * PS : a.proxy + (size_t)(-1 - d.side[s]) * PS;
 
-    // ---- halo gather: plus-shaped tile (corners are never read, A26)
-    constexpr int EBAND = T * W, ESTRIP = G * T, ETOT = EBAND + 2 * ESTRIP;
-    for (int e = tid; e < ETOT; e += NT) {
-        int i, j;
-        if (e < EBAND) { j = e / W; i = e - j * W - G; }
-        else if (e < EBAND + ESTRIP) { int f = e - EBAND; j = f / T - G; i = f - (j + G) * T; }
-        else { int f = e - EBAND - ESTRIP; j = f / T; i = f - j * T; j += T; }
-        int pi = tx * T + i, pj = ty * T + j;
-        const double* base = own;
-        if (pi < 0) { base = srcs[kW]; pi += n; }
-        else if (pi >= n) { base = srcs[kE]; pi -= n; }
-        else if (pj < 0) { base = srcs[kS]; pj += n; }
-        else if (pj >= n) { base = srcs[kN]; pj -= n; }
-        const double* q = base + (size_t)pj * n + pi;
-        int o = (j + G) * W + (i + G);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sQ[k * W * W + o] = __ldg(q + k * nn);
-    }
-    // U^n of the owned cells (stages 2, 3), issued early
-    double un[CPT][4];
-    if (a.stage > 1) {
-        const double* pn = a.Un + (size_t)d.slot * PS;
-#pragma unroll
-        for (int r = 0; r < CPT; ++r) {
-            int c = tid + r * NT;
-            if (c < T * T) {
-                int i = c % T, j = c / T;
-                size_t off = (size_t)(ty * T + j) * n + tx * T + i;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) un[r][k] = __ldg(pn + k * nn + off);
-            }
+    // ---- halo gather (a1): plus-shaped tile, 16-byte cp.async (corners are never read, A26)
+    {
+        constexpr int CR = W / 2, CB = T * CR, CS = G * T / 2, CV = CB + 2 * CS;
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sQ);
+        for (int e = tid; e < 4 * CV; e += NT) {
+            int k = e / CV, f = e - k * CV, i, j;
+            if (f < CB) { j = f / CR; i = 2 * (f - j * CR) - G; }
+            else if (f < CB + CS) { int h = f - CB; j = h / (T / 2) - G; i = 2 * (h - (j + G) * (T / 2)); }
+            else { int h = f - CB - CS; j = h / (T / 2); i = 2 * (h - j * (T / 2)); j += T; }
+            int pi = tx * T + i, pj = ty * T + j;
+            int s = 0;
+            bool halo = true;
+            if (pi < 0) { s = d.side[kW]; pi += n; }
+            else if (pi >= n) { s = d.side[kE]; pi -= n; }
+            else if (pj < 0) { s = d.side[kS]; pj += n; }
+            else if (pj >= n) { s = d.side[kN]; pj -= n; }
+            else halo = false;
+            const double* base = !halo ? own : (s >= 0 ? a.Uin + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS);
+            cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + (i + G)) * 8), base + k * nn + (size_t)pj * n + pi);
         }
+        cp_async_wait_all();
     }
     __syncthreads();
 
     const double g = a.gamma;
     const double inv_gm1 = 1.0 / (g - 1.0);
-    double up[CPT][4];   // U^(s-1) of the owned cells
-#pragma unroll
-    for (int r = 0; r < CPT; ++r) {
-        int c = tid + r * NT;
-        if (c < T * T) {
-            int i = c % T, j = c / T;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) up[r][k] = sQ[k * W * W + (j + G) * W + i + G];
-        }
-    }
     if (SCHEME == 0) {
-        __syncthreads();
-        // cons -> (p, T, u, v) in place (Eq. 4-6)
-        for (int e = tid; e < ETOT; e += NT) {
+        // cons -> (p, T, u, v) in place (Eq. 4-6) over the plus-shaped tile
+        constexpr int EB = T * W, ES = G * T, ET = EB + 2 * ES;
+        for (int e = tid; e < ET; e += NT) {
             int i, j;
-            if (e < EBAND) { j = e / W; i = e - j * W - G; }
-            else if (e < EBAND + ESTRIP) { int f = e - EBAND; j = f / T - G; i = f - (j + G) * T; }
-            else { int f = e - EBAND - ESTRIP; j = f / T; i = f - j * T; j += T; }
+            if (e < EB) { j = e / W; i = e - j * W - G; }
+            else if (e < EB + ES) { int f = e - EB; j = f / T - G; i = f - (j + G) * T; }
+            else { int f = e - EB - ES; j = f / T; i = f - j * T; j += T; }
             int o = (j + G) * W + (i + G);
-            double r = sQ[o], m = sQ[W * W + o], w = sQ[2 * W * W + o], E = sQ[3 * W * W + o];
+            double r = sQ[o], m = sQ[PL + o], w = sQ[2 * PL + o], E = sQ[3 * PL + o];
             double ir = 1.0 / r;
             double u = m * ir, v = w * ir;
             double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
             sQ[o] = p;
-            sQ[W * W + o] = p * ir;
-            sQ[2 * W * W + o] = u;
-            sQ[3 * W * W + o] = v;
+            sQ[PL + o] = p * ir;
+            sQ[2 * PL + o] = u;
+            sQ[3 * PL + o] = v;
         }
         __syncthreads();
     }
@@ -297,37 +284,22 @@ __global__ void __launch_bounds__(Block<T>::NT) stage_kernel(const StageArgs a) 
     const int lvl = d.level;
     const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
     const bool div4 = a.div_order == 4;
-    double acc[CPT][4];
+    const int x_lo = tx == 0, x_hi = tx == a.tiles - 1, y_lo = ty == 0, y_hi = ty == a.tiles - 1;
+    const int store_mask = (d.cf | (d.cf >> 4)) & 15;
 
-    // ---- x faces: face m (left of cell m), row j; cells m-3..m+2
+    // ---- x faces (a4-a6): face m (left of cell m), row j
     for (int e = tid; e < T * NF; e += NT) {
         int j = e / NF, m = e - j * NF - 1;
         int o = (j + G) * W + (m + G);
         double f[4];
-        if (SCHEME == 0) {
-            double c[4][4];
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                int oo = o + s - 2;
-                c[s][0] = sQ[oo]; c[s][1] = sQ[W * W + oo]; c[s][2] = sQ[2 * W * W + oo]; c[s][3] = sQ[3 * W * W + oo];
-            }
-            central4_flux(c, inv_gm1, f);
-        } else {
-            double c[6][4];
-#pragma unroll
-            for (int s = 0; s < 6; ++s) {
-                int oo = o + s - 3;
-                c[s][0] = sQ[oo]; c[s][1] = sQ[W * W + oo]; c[s][2] = sQ[2 * W * W + oo]; c[s][3] = sQ[3 * W * W + oo];
-            }
-            weno_rusanov<SCHEME == 1>(c, g, a.eps, f);
-        }
+        if (SCHEME == 0) central4_flux(sQ + o - 2, 1, PL, 2, 3, inv_gm1, f);
+        else weno_rusanov<SCHEME == 1>(sQ + o - 3, 1, PL, 1, 2, g, a.eps, f);
 #pragma unroll
         for (int k = 0; k < 4; ++k) sF[(k * T + j) * NF + m + 1] = f[k];
     }
     __syncthreads();
-    const int leaf_tiles_x_lo = tx == 0, leaf_tiles_x_hi = tx == a.tiles - 1;
-    const int leaf_tiles_y_lo = ty == 0, leaf_tiles_y_hi = ty == a.tiles - 1;
-    const int store_mask = (d.cf | (d.cf >> 4)) & 15;
+    // ---- x divergence (a7, Eq. 9 flux form) into registers
+    double acc[CPT][4];
 #pragma unroll
     for (int r = 0; r < CPT; ++r) {
         int c = tid + r * NT;
@@ -340,37 +312,22 @@ __global__ void __launch_bounds__(Block<T>::NT) stage_kernel(const StageArgs a) 
                 double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-1] + fh) : fl;
                 double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2]) : fh;
                 acc[r][k] = -(Fh - Fl) * idx;
-                if (i == 0 && leaf_tiles_x_lo && (store_mask & 1))
+                if (i == 0 && x_lo && (store_mask & 1))
                     a.freg[(((size_t)leaf * 4 + kW) * 4 + k) * n + ty * T + j] = Fl;
-                if (i == T - 1 && leaf_tiles_x_hi && (store_mask & 2))
+                if (i == T - 1 && x_hi && (store_mask & 2))
                     a.freg[(((size_t)leaf * 4 + kE) * 4 + k) * n + ty * T + j] = Fh;
             }
         }
     }
     __syncthreads();
 
-    // ---- y faces: face m (below cell m), column i; rotated frame (rho, w, m, E)
+    // ---- y faces: face m (below cell m), column i; normal momentum is component 2
     for (int e = tid; e < T * NF; e += NT) {
         int m = e / T - 1, i = e - (m + 1) * T;
         int o = (m + G) * W + (i + G);
         double f[4];
-        if (SCHEME == 0) {
-            double c[4][4];
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                int oo = o + (s - 2) * W;
-                c[s][0] = sQ[oo]; c[s][1] = sQ[W * W + oo]; c[s][2] = sQ[3 * W * W + oo]; c[s][3] = sQ[2 * W * W + oo];
-            }
-            central4_flux(c, inv_gm1, f);
-        } else {
-            double c[6][4];
-#pragma unroll
-            for (int s = 0; s < 6; ++s) {
-                int oo = o + (s - 3) * W;
-                c[s][0] = sQ[oo]; c[s][1] = sQ[2 * W * W + oo]; c[s][2] = sQ[W * W + oo]; c[s][3] = sQ[3 * W * W + oo];
-            }
-            weno_rusanov<SCHEME == 1>(c, g, a.eps, f);
-        }
+        if (SCHEME == 0) central4_flux(sQ + o - 2 * W, W, PL, 3, 2, inv_gm1, f);
+        else weno_rusanov<SCHEME == 1>(sQ + o - 3 * W, W, PL, 2, 1, g, a.eps, f);
         sF[(0 * NF + m + 1) * T + i] = f[0];
         sF[(1 * NF + m + 1) * T + i] = f[2];
         sF[(2 * NF + m + 1) * T + i] = f[1];
@@ -378,15 +335,19 @@ __global__ void __launch_bounds__(Block<T>::NT) stage_kernel(const StageArgs a) 
     }
     __syncthreads();
 
-    // ---- divergence (y), RK combination, checks, Lambda
+    // ---- y divergence, SSP-RK3 combination (a8), checks, Lambda (a9)
     const double dt = *a.dt;
     const int coarse_mask = d.cf & 15;
+    const double* pin = a.Uin + (size_t)d.slot * PS;
+    const double* pn = a.Un + (size_t)d.slot * PS;
+    double* po = a.Uout + (size_t)d.slot * PS;
     unsigned long long lam = 0ull;
 #pragma unroll
     for (int r = 0; r < CPT; ++r) {
         int c = tid + r * NT;
         if (c < T * T) {
             int i = c % T, j = c / T;
+            size_t off = (size_t)(ty * T + j) * n + tx * T + i;
             double o4[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -395,23 +356,19 @@ __global__ void __launch_bounds__(Block<T>::NT) stage_kernel(const StageArgs a) 
                 double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-T] + fh) : fl;
                 double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2 * T]) : fh;
                 double L = acc[r][k] - (Fh - Fl) * idy;
-                if (j == 0 && leaf_tiles_y_lo && (store_mask & 4))
+                if (j == 0 && y_lo && (store_mask & 4))
                     a.freg[(((size_t)leaf * 4 + kS) * 4 + k) * n + tx * T + i] = Fl;
-                if (j == T - 1 && leaf_tiles_y_hi && (store_mask & 8))
+                if (j == T - 1 && y_hi && (store_mask & 8))
                     a.freg[(((size_t)leaf * 4 + kN) * 4 + k) * n + tx * T + i] = Fh;
-                double v = up[r][k] + dt * L;
-                if (a.stage > 1) v = a.a * un[r][k] + a.b * v;
+                double v = __ldg(pin + k * nn + off) + dt * L;
+                if (a.stage > 1) v = a.a * __ldg(pn + k * nn + off) + a.b * v;
                 o4[k] = v;
             }
-            size_t off = (size_t)(ty * T + j) * n + tx * T + i;
-            double* po = a.Uout + (size_t)d.slot * PS + off;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) po[k * nn] = o4[k];
+            for (int k = 0; k < 4; ++k) po[k * nn + off] = o4[k];
             // cells on an edge that is the coarse side of a C/F face are finished by the reflux kernel
-            bool edge_cf = ((coarse_mask & 1) && leaf_tiles_x_lo && i == 0) ||
-                           ((coarse_mask & 2) && leaf_tiles_x_hi && i == T - 1) ||
-                           ((coarse_mask & 4) && leaf_tiles_y_lo && j == 0) ||
-                           ((coarse_mask & 8) && leaf_tiles_y_hi && j == T - 1);
+            bool edge_cf = ((coarse_mask & 1) && x_lo && i == 0) || ((coarse_mask & 2) && x_hi && i == T - 1) ||
+                           ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1);
             if (!edge_cf) {
                 if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], g))
                     report_error(a.err, d.slot, a.stage, (int)off);
