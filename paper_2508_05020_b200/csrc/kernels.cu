@@ -402,9 +402,288 @@ cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- Central4 fused stage kernel
+// Specialised for the HBM-bound shock-free scheme (Eq. 8/9): warp-per-row 16-byte cp.async gather,
+// in-place cons->prim, sliding-window face fluxes (each thread computes R consecutive faces of one
+// row / column with a rolling 4-cell register window) and sliding-window divergences (each thread owns
+// CPT cells of one column), so that every cell is loaded from shared memory a handful of times.
+__device__ __forceinline__ double fast_rcp(double x) {
+    // MUFU.RCP64H seed + two Newton steps (<= 1 ulp; A41)
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+template <int T>
+struct C4Cfg;
+template <>
+struct C4Cfg<32> { static constexpr int NT = 256, SEG = 7, R = 5, MINB = 2; };
+template <>
+struct C4Cfg<16> { static constexpr int NT = 128, SEG = 8, R = 3, MINB = 4; };
+template <>
+struct C4Cfg<8> { static constexpr int NT = 64, SEG = 8, R = 2, MINB = 8; };
+
+// Central4 edge flux from a rolling window c[0..3] = cells i-1..i+2 of (p, T, un, ut).
+__device__ __forceinline__ void c4_face(const double (&p)[4], const double (&Tt)[4], const double (&un)[4],
+                                        const double (&ut)[4], double inv_gm1, double F[4]) {
+    double pe = 0.5625 * (p[1] + p[2]) - 0.0625 * (p[0] + p[3]);
+    double Te = 0.5625 * (Tt[1] + Tt[2]) - 0.0625 * (Tt[0] + Tt[3]);
+    double ue = 0.5625 * (un[1] + un[2]) - 0.0625 * (un[0] + un[3]);
+    double ve = 0.5625 * (ut[1] + ut[2]) - 0.0625 * (ut[0] + ut[3]);
+    double re = pe * fast_rcp(Te);
+    double Ee = pe * inv_gm1 + 0.5 * re * (ue * ue + ve * ve);
+    double mn = re * ue;
+    F[0] = mn;
+    F[1] = mn * ue + pe;
+    F[2] = mn * ve;
+    F[3] = (Ee + pe) * ue;
+}
+
+template <int T>
+__global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(const StageArgs a) {
+    constexpr int G = kGL;
+    constexpr int NT = C4Cfg<T>::NT, SEG = C4Cfg<T>::SEG, R = C4Cfg<T>::R;
+    constexpr int NW = NT / 32;
+    constexpr int W = T + 2 * G;
+    constexpr int PL = W * W;
+    constexpr int NF = T + 3;                // faces m = -1 .. T+1
+    constexpr int CPT = T * T / NT;          // cells per thread (one column strip)
+    static_assert(SEG * R >= NF, "face segments must cover the row");
+    static_assert(T * SEG <= NT, "one thread per face segment");
+    extern __shared__ __align__(16) double smem[];
+    double* sQ = smem;                       // [4][W][W] conserved, then (p, T, u, v)
+    double* sF = smem + 4 * PL;              // [4][T][NF] x-fluxes, then [4][NF][T] y-fluxes
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tiles2 = a.tiles * a.tiles;
+    const int leaf = blockIdx.x / tiles2;
+    const int tt = blockIdx.x - leaf * tiles2;
+    const int tx = tt % a.tiles, ty = tt / a.tiles;
+    const LeafDesc d = a.leaves[leaf];
+    const int n = a.geo.n;
+    const size_t nn = (size_t)n * n;
+    const size_t PS = 4 * nn;
+    const double* own = a.Uin + (size_t)d.slot * PS;
+    const double* src[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        src[s] = d.side[s] >= 0 ? a.Uin + (size_t)d.side[s] * PS : a.proxy + (size_t)(-1 - d.side[s]) * PS;
+
+    // ---- (a1) halo gather: one warp per (component, row); lanes move 16-byte chunks
+    {
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sQ);
+        constexpr int CR = W / 2;            // chunks per band row
+        for (int task = warp; task < 4 * T; task += NW) {
+            const int k = task / T, j = task - k * T;
+            const int pj = ty * T + j;
+            if (lane < CR) {
+                int pi = tx * T + 2 * lane - G;
+                const double* b = own;
+                if (pi < 0) { b = src[kW]; pi += n; }
+                else if (pi >= n) { b = src[kE]; pi -= n; }
+                cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + 2 * lane) * 8), b + k * nn + (size_t)pj * n + pi);
+            }
+        }
+        for (int task = warp; task < 4 * 2 * G; task += NW) {
+            const int k = task / (2 * G), r = task - k * (2 * G);
+            const int j = r < G ? r - G : T + (r - G);
+            int pj = ty * T + j;
+            const double* b = own;
+            if (pj < 0) { b = src[kS]; pj += n; }
+            else if (pj >= n) { b = src[kN]; pj -= n; }
+            if (lane < T / 2) {
+                const int pi = tx * T + 2 * lane;
+                cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + G + 2 * lane) * 8), b + k * nn + (size_t)pj * n + pi);
+            }
+        }
+        cp_async_wait_all();
+    }
+    __syncthreads();
+
+    const double g = a.gamma, gm1 = g - 1.0;
+    const double inv_gm1 = 1.0 / gm1;
+    // ---- (a3) cons -> (p, T, u, v) in place: band rows then strip rows, lanes along the row
+    for (int task = warp; task < T + 2 * G; task += NW) {
+        const int j = task < T ? task : (task - T < G ? task - T - G : task - G);
+        const int i0 = task < T ? -G : 0, len = task < T ? W : T;
+        for (int c = lane; c < len; c += 32) {
+            const int o = (j + G) * W + (i0 + c + G);
+            double r = sQ[o], m = sQ[PL + o], w = sQ[2 * PL + o], E = sQ[3 * PL + o];
+            double ir = fast_rcp(r);
+            double u = m * ir, v = w * ir;
+            double p = gm1 * (E - 0.5 * (m * u + w * v));
+            sQ[o] = p;
+            sQ[PL + o] = p * ir;
+            sQ[2 * PL + o] = u;
+            sQ[3 * PL + o] = v;
+        }
+    }
+    __syncthreads();
+
+    const int lvl = d.level;
+    const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
+    const bool div4 = a.div_order == 4;
+    const int x_lo = tx == 0, x_hi = tx == a.tiles - 1, y_lo = ty == 0, y_hi = ty == a.tiles - 1;
+    const int store_mask = (d.cf | (d.cf >> 4)) & 15;
+    const double c13 = 13.0 / 12.0, c24 = 1.0 / 24.0;
+
+    // ---- (a4-a6) x faces: thread (row j, segment s) computes faces m0 .. m0+R-1
+    if (tid < T * SEG && (tid % SEG) * R - 1 <= T + 1) {
+        const int j = tid / SEG, s = tid - j * SEG;
+        const int m0 = s * R - 1;
+        const double* q = sQ + (j + G) * W + G;   // q[i] = cell i of row j
+        double p[4], Tt[4], un[4], ut[4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int i = m0 - 2 + c;
+            p[c + 1] = q[i]; Tt[c + 1] = q[PL + i]; un[c + 1] = q[2 * PL + i]; ut[c + 1] = q[3 * PL + i];
+        }
+#pragma unroll
+        for (int f = 0; f < R; ++f) {
+            const int m = m0 + f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un[c] = un[c + 1]; ut[c] = ut[c + 1]; }
+            if (m <= T + 1) {
+                const int i = m + 1;
+                p[3] = q[i]; Tt[3] = q[PL + i]; un[3] = q[2 * PL + i]; ut[3] = q[3 * PL + i];
+                double F[4];
+                c4_face(p, Tt, un, ut, inv_gm1, F);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sF[(k * T + j) * NF + m + 1] = F[k];
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- (a7) x divergence (Eq. 9 flux form): thread owns column i, rows j0 .. j0+CPT-1
+    const int ci = tid % T, cj0 = (tid / T) * CPT;
+    double acc[CPT][4];
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        const int j = cj0 + r;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double* fr = sF + (k * T + j) * NF + ci + 1;   // fr[0] = f at face ci
+            double fl = fr[0], fh = fr[1];
+            double Fl = div4 ? c13 * fl - c24 * (fr[-1] + fh) : fl;
+            double Fh = div4 ? c13 * fh - c24 * (fl + fr[2]) : fh;
+            acc[r][k] = -(Fh - Fl) * idx;
+            if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)leaf * 4 + kW) * 4 + k) * n + ty * T + j] = Fl;
+            if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)leaf * 4 + kE) * 4 + k) * n + ty * T + j] = Fh;
+        }
+    }
+    __syncthreads();
+
+    // ---- y faces: thread (column i, segment s), rolling window along j; normal velocity = v
+    if (tid < T * SEG && (tid / T) * R - 1 <= T + 1) {
+        const int i = tid % T, s = tid / T;
+        const int m0 = s * R - 1;
+        const double* q = sQ + G * W + (i + G);   // q[j * W] = cell (i, j)
+        double p[4], Tt[4], un[4], ut[4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int o = (m0 - 2 + c) * W;
+            p[c + 1] = q[o]; Tt[c + 1] = q[PL + o]; un[c + 1] = q[3 * PL + o]; ut[c + 1] = q[2 * PL + o];
+        }
+#pragma unroll
+        for (int f = 0; f < R; ++f) {
+            const int m = m0 + f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un[c] = un[c + 1]; ut[c] = ut[c + 1]; }
+            if (m <= T + 1) {
+                const int o = (m + 1) * W;
+                p[3] = q[o]; Tt[3] = q[PL + o]; un[3] = q[3 * PL + o]; ut[3] = q[2 * PL + o];
+                double F[4];
+                c4_face(p, Tt, un, ut, inv_gm1, F);
+                sF[(0 * NF + m + 1) * T + i] = F[0];
+                sF[(1 * NF + m + 1) * T + i] = F[2];
+                sF[(2 * NF + m + 1) * T + i] = F[1];
+                sF[(3 * NF + m + 1) * T + i] = F[3];
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- y divergence (sliding along the owned column), SSP-RK3 (a8), checks, Lambda (a9)
+    const double dt = *a.dt;
+    const int coarse_mask = d.cf & 15;
+    const size_t base_off = (size_t)(ty * T + cj0) * n + tx * T + ci;
+    const double* pin = a.Uin + (size_t)d.slot * PS + base_off;
+    const double* pn = a.Un + (size_t)d.slot * PS + base_off;
+    double* po = a.Uout + (size_t)d.slot * PS + base_off;
+    double out[CPT][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double* fc = sF + (k * NF + cj0 + 1) * T + ci;   // fc[r*T] = f at face cj0 + r
+        double fm1 = fc[-T], f0 = fc[0], f1 = fc[T];
+        double Flo = div4 ? c13 * f0 - c24 * (fm1 + f1) : f0;
+        if (cj0 == 0 && y_lo && (store_mask & 4)) a.freg[(((size_t)leaf * 4 + kS) * 4 + k) * n + tx * T + ci] = Flo;
+#pragma unroll
+        for (int r = 0; r < CPT; ++r) {
+            double f2 = fc[(r + 2) * T];
+            double Fhi = div4 ? c13 * f1 - c24 * (f0 + f2) : f1;
+            double L = acc[r][k] - (Fhi - Flo) * idy;
+            double v = __ldg(pin + k * nn + (size_t)r * n) + dt * L;
+            if (a.stage > 1) v = a.a * __ldg(pn + k * nn + (size_t)r * n) + a.b * v;
+            out[r][k] = v;
+            if (r == CPT - 1 && cj0 + r == T - 1 && y_hi && (store_mask & 8))
+                a.freg[(((size_t)leaf * 4 + kN) * 4 + k) * n + tx * T + ci] = Fhi;
+            Flo = Fhi;
+            f0 = f1;
+            f1 = f2;
+        }
+    }
+    unsigned long long lam = 0ull;
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        const int j = cj0 + r;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) po[k * nn + (size_t)r * n] = out[r][k];
+        bool edge_cf = ((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
+                       ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1);
+        if (!edge_cf) {
+            if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
+                report_error(a.err, d.slot, a.stage, (int)((ty * T + j) * n + tx * T + ci));
+            if (a.want_lambda) {
+                double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                unsigned long long b = (unsigned long long)__double_as_longlong(sp);
+                lam = b > lam ? b : lam;
+            }
+        }
+    }
+    if (a.want_lambda) {
+        lam = warp_max_u64(lam);
+        if (lane == 0 && lam) atomicMax(a.lambda_bits, lam);
+    }
+}
+
+template <int T>
+cudaError_t launch_c4_t(const StageArgs& a, cudaStream_t s) {
+    constexpr size_t smem = stage_smem<0, T>();
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(stage_c4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    unsigned blocks = (unsigned)a.nleaves * a.tiles * a.tiles;
+    if (blocks == 0) return cudaSuccess;
+    stage_c4_kernel<T><<<blocks, C4Cfg<T>::NT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int SCHEME>
 cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
     int T = a.geo.n / a.tiles;
+    if (SCHEME == 0) {
+        if (T == 8) return launch_c4_t<8>(a, s);
+        if (T == 16) return launch_c4_t<16>(a, s);
+        if (T == 32) return launch_c4_t<32>(a, s);
+        return cudaErrorInvalidValue;
+    }
     if (T == 8) return launch_stage_t<SCHEME, 8>(a, s);
     if (T == 16) return launch_stage_t<SCHEME, 16>(a, s);
     if (T == 32) return launch_stage_t<SCHEME, 32>(a, s);
