@@ -442,8 +442,11 @@ __device__ __forceinline__ void c4_face(const double (&p)[4], const double (&Tt)
     F[3] = (Ee + pe) * ue;
 }
 
-template <int T>
-__global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(const StageArgs a) {
+template <int N>
+__global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 32 : N)>::MINB)
+    stage_c4_kernel(const StageArgs a) {
+    constexpr int T = N > 32 ? 32 : N;       // tile edge
+    constexpr int TILES = N / T;             // tiles per patch edge
     constexpr int G = kGL;
     constexpr int NT = C4Cfg<T>::NT, SEG = C4Cfg<T>::SEG, R = C4Cfg<T>::R;
     constexpr int NW = NT / 32;
@@ -451,6 +454,9 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
     constexpr int PL = W * W;
     constexpr int NF = T + 3;                // faces m = -1 .. T+1
     constexpr int CPT = T * T / NT;          // cells per thread (one column strip)
+    constexpr int NN = N * N;
+    constexpr int PS = 4 * NN;
+    constexpr bool EXACT = SEG * R == NF;    // no face-segment guard needed
     static_assert(SEG * R >= NF, "face segments must cover the row");
     static_assert(T * SEG <= NT, "one thread per face segment");
     extern __shared__ __align__(16) double smem[];
@@ -458,14 +464,10 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
     double* sF = smem + 4 * PL;              // [4][T][NF] x-fluxes, then [4][NF][T] y-fluxes
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tiles2 = a.tiles * a.tiles;
-    const int leaf = blockIdx.x / tiles2;
-    const int tt = blockIdx.x - leaf * tiles2;
-    const int tx = tt % a.tiles, ty = tt / a.tiles;
+    const int leaf = TILES == 1 ? blockIdx.x : blockIdx.x / (TILES * TILES);
+    const int tt = TILES == 1 ? 0 : blockIdx.x - leaf * (TILES * TILES);
+    const int tx = tt % TILES, ty = tt / TILES;
     const LeafDesc d = a.leaves[leaf];
-    const int n = a.geo.n;
-    const size_t nn = (size_t)n * n;
-    const size_t PS = 4 * nn;
     const double* own = a.Uin + (size_t)d.slot * PS;
     const double* src[4];
 #pragma unroll
@@ -482,9 +484,9 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
             if (lane < CR) {
                 int pi = tx * T + 2 * lane - G;
                 const double* b = own;
-                if (pi < 0) { b = src[kW]; pi += n; }
-                else if (pi >= n) { b = src[kE]; pi -= n; }
-                cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + 2 * lane) * 8), b + k * nn + (size_t)pj * n + pi);
+                if (pi < 0) { b = src[kW]; pi += N; }
+                else if (pi >= N) { b = src[kE]; pi -= N; }
+                cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + 2 * lane) * 8), b + k * NN + pj * N + pi);
             }
         }
         for (int task = warp; task < 4 * 2 * G; task += NW) {
@@ -492,12 +494,10 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
             const int j = r < G ? r - G : T + (r - G);
             int pj = ty * T + j;
             const double* b = own;
-            if (pj < 0) { b = src[kS]; pj += n; }
-            else if (pj >= n) { b = src[kN]; pj -= n; }
-            if (lane < T / 2) {
-                const int pi = tx * T + 2 * lane;
-                cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + G + 2 * lane) * 8), b + k * nn + (size_t)pj * n + pi);
-            }
+            if (pj < 0) { b = src[kS]; pj += N; }
+            else if (pj >= N) { b = src[kN]; pj -= N; }
+            if (lane < T / 2)
+                cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + G + 2 * lane) * 8), b + k * NN + pj * N + tx * T + 2 * lane);
         }
         cp_async_wait_all();
     }
@@ -509,16 +509,16 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
     for (int task = warp; task < T + 2 * G; task += NW) {
         const int j = task < T ? task : (task - T < G ? task - T - G : task - G);
         const int i0 = task < T ? -G : 0, len = task < T ? W : T;
+        double* q = sQ + (j + G) * W + i0 + G;
         for (int c = lane; c < len; c += 32) {
-            const int o = (j + G) * W + (i0 + c + G);
-            double r = sQ[o], m = sQ[PL + o], w = sQ[2 * PL + o], E = sQ[3 * PL + o];
+            double r = q[c], m = q[PL + c], w = q[2 * PL + c], E = q[3 * PL + c];
             double ir = fast_rcp(r);
             double u = m * ir, v = w * ir;
             double p = gm1 * (E - 0.5 * (m * u + w * v));
-            sQ[o] = p;
-            sQ[PL + o] = p * ir;
-            sQ[2 * PL + o] = u;
-            sQ[3 * PL + o] = v;
+            q[c] = p;
+            q[PL + c] = p * ir;
+            q[2 * PL + c] = u;
+            q[3 * PL + c] = v;
         }
     }
     __syncthreads();
@@ -526,82 +526,79 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
     const int lvl = d.level;
     const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
     const bool div4 = a.div_order == 4;
-    const int x_lo = tx == 0, x_hi = tx == a.tiles - 1, y_lo = ty == 0, y_hi = ty == a.tiles - 1;
+    const bool x_lo = tx == 0, x_hi = tx == TILES - 1, y_lo = ty == 0, y_hi = ty == TILES - 1;
     const int store_mask = (d.cf | (d.cf >> 4)) & 15;
     const double c13 = 13.0 / 12.0, c24 = 1.0 / 24.0;
 
     // ---- (a4-a6) x faces: thread (row j, segment s) computes faces m0 .. m0+R-1
-    if (tid < T * SEG && (tid % SEG) * R - 1 <= T + 1) {
+    if (tid < T * SEG && (EXACT || (tid % SEG) * R - 1 <= T + 1)) {
         const int j = tid / SEG, s = tid - j * SEG;
         const int m0 = s * R - 1;
-        const double* q = sQ + (j + G) * W + G;   // q[i] = cell i of row j
+        const double* q = sQ + (j + G) * W + G + m0;   // q[c] = cell m0 + c of row j
+        double* fo = sF + j * NF + m0 + 1;              // fo[k*T*NF + f] = flux at face m0 + f
         double p[4], Tt[4], un[4], ut[4];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int i = m0 - 2 + c;
-            p[c + 1] = q[i]; Tt[c + 1] = q[PL + i]; un[c + 1] = q[2 * PL + i]; ut[c + 1] = q[3 * PL + i];
-        }
+        for (int c = 0; c < 3; ++c) { p[c + 1] = q[c - 2]; Tt[c + 1] = q[PL + c - 2]; un[c + 1] = q[2 * PL + c - 2]; ut[c + 1] = q[3 * PL + c - 2]; }
 #pragma unroll
         for (int f = 0; f < R; ++f) {
-            const int m = m0 + f;
 #pragma unroll
             for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un[c] = un[c + 1]; ut[c] = ut[c + 1]; }
-            if (m <= T + 1) {
-                const int i = m + 1;
-                p[3] = q[i]; Tt[3] = q[PL + i]; un[3] = q[2 * PL + i]; ut[3] = q[3 * PL + i];
+            if (EXACT || m0 + f <= T + 1) {
+                p[3] = q[f + 1]; Tt[3] = q[PL + f + 1]; un[3] = q[2 * PL + f + 1]; ut[3] = q[3 * PL + f + 1];
                 double F[4];
                 c4_face(p, Tt, un, ut, inv_gm1, F);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) sF[(k * T + j) * NF + m + 1] = F[k];
+                for (int k = 0; k < 4; ++k) fo[k * T * NF + f] = F[k];
             }
         }
     }
     __syncthreads();
 
-    // ---- (a7) x divergence (Eq. 9 flux form): thread owns column i, rows j0 .. j0+CPT-1
+    // ---- (a7) x divergence (Eq. 9 flux form): thread owns column ci, rows cj0 .. cj0+CPT-1
     const int ci = tid % T, cj0 = (tid / T) * CPT;
     double acc[CPT][4];
 #pragma unroll
     for (int r = 0; r < CPT; ++r) {
-        const int j = cj0 + r;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const double* fr = sF + (k * T + j) * NF + ci + 1;   // fr[0] = f at face ci
+            const double* fr = sF + (k * T + cj0 + r) * NF + ci + 1;   // fr[0] = f at face ci
             double fl = fr[0], fh = fr[1];
             double Fl = div4 ? c13 * fl - c24 * (fr[-1] + fh) : fl;
             double Fh = div4 ? c13 * fh - c24 * (fl + fr[2]) : fh;
             acc[r][k] = -(Fh - Fl) * idx;
-            if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)leaf * 4 + kW) * 4 + k) * n + ty * T + j] = Fl;
-            if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)leaf * 4 + kE) * 4 + k) * n + ty * T + j] = Fh;
+            if (store_mask) {
+                if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)leaf * 4 + kW) * 4 + k) * N + ty * T + cj0 + r] = Fl;
+                if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)leaf * 4 + kE) * 4 + k) * N + ty * T + cj0 + r] = Fh;
+            }
         }
     }
     __syncthreads();
 
     // ---- y faces: thread (column i, segment s), rolling window along j; normal velocity = v
-    if (tid < T * SEG && (tid / T) * R - 1 <= T + 1) {
+    if (tid < T * SEG && (EXACT || (tid / T) * R - 1 <= T + 1)) {
         const int i = tid % T, s = tid / T;
         const int m0 = s * R - 1;
-        const double* q = sQ + G * W + (i + G);   // q[j * W] = cell (i, j)
+        const double* q = sQ + (m0 + G) * W + (i + G);   // q[c*W] = cell (i, m0 + c)
+        double* fo = sF + (m0 + 1) * T + i;               // fo[k*NF*T + f*T] = flux at face m0 + f
         double p[4], Tt[4], un[4], ut[4];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const int o = (m0 - 2 + c) * W;
+            const int o = (c - 2) * W;
             p[c + 1] = q[o]; Tt[c + 1] = q[PL + o]; un[c + 1] = q[3 * PL + o]; ut[c + 1] = q[2 * PL + o];
         }
 #pragma unroll
         for (int f = 0; f < R; ++f) {
-            const int m = m0 + f;
 #pragma unroll
             for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un[c] = un[c + 1]; ut[c] = ut[c + 1]; }
-            if (m <= T + 1) {
-                const int o = (m + 1) * W;
+            if (EXACT || m0 + f <= T + 1) {
+                const int o = (f + 1) * W;
                 p[3] = q[o]; Tt[3] = q[PL + o]; un[3] = q[3 * PL + o]; ut[3] = q[2 * PL + o];
                 double F[4];
                 c4_face(p, Tt, un, ut, inv_gm1, F);
-                sF[(0 * NF + m + 1) * T + i] = F[0];
-                sF[(1 * NF + m + 1) * T + i] = F[2];
-                sF[(2 * NF + m + 1) * T + i] = F[1];
-                sF[(3 * NF + m + 1) * T + i] = F[3];
+                fo[0 * NF * T + f * T] = F[0];
+                fo[1 * NF * T + f * T] = F[2];
+                fo[2 * NF * T + f * T] = F[1];
+                fo[3 * NF * T + f * T] = F[3];
             }
         }
     }
@@ -610,27 +607,30 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
     // ---- y divergence (sliding along the owned column), SSP-RK3 (a8), checks, Lambda (a9)
     const double dt = *a.dt;
     const int coarse_mask = d.cf & 15;
-    const size_t base_off = (size_t)(ty * T + cj0) * n + tx * T + ci;
+    const int base_off = (ty * T + cj0) * N + tx * T + ci;
     const double* pin = a.Uin + (size_t)d.slot * PS + base_off;
     const double* pn = a.Un + (size_t)d.slot * PS + base_off;
     double* po = a.Uout + (size_t)d.slot * PS + base_off;
+    const bool rk_un = a.stage > 1;
+    const double ca = a.a, cb = a.b;
     double out[CPT][4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const double* fc = sF + (k * NF + cj0 + 1) * T + ci;   // fc[r*T] = f at face cj0 + r
         double fm1 = fc[-T], f0 = fc[0], f1 = fc[T];
         double Flo = div4 ? c13 * f0 - c24 * (fm1 + f1) : f0;
-        if (cj0 == 0 && y_lo && (store_mask & 4)) a.freg[(((size_t)leaf * 4 + kS) * 4 + k) * n + tx * T + ci] = Flo;
+        if (store_mask && cj0 == 0 && y_lo && (store_mask & 4))
+            a.freg[(((size_t)leaf * 4 + kS) * 4 + k) * N + tx * T + ci] = Flo;
 #pragma unroll
         for (int r = 0; r < CPT; ++r) {
             double f2 = fc[(r + 2) * T];
             double Fhi = div4 ? c13 * f1 - c24 * (f0 + f2) : f1;
             double L = acc[r][k] - (Fhi - Flo) * idy;
-            double v = __ldg(pin + k * nn + (size_t)r * n) + dt * L;
-            if (a.stage > 1) v = a.a * __ldg(pn + k * nn + (size_t)r * n) + a.b * v;
+            double v = __ldg(pin + k * NN + r * N) + dt * L;
+            if (rk_un) v = ca * __ldg(pn + k * NN + r * N) + cb * v;
             out[r][k] = v;
-            if (r == CPT - 1 && cj0 + r == T - 1 && y_hi && (store_mask & 8))
-                a.freg[(((size_t)leaf * 4 + kN) * 4 + k) * n + tx * T + ci] = Fhi;
+            if (store_mask && r == CPT - 1 && cj0 + r == T - 1 && y_hi && (store_mask & 8))
+                a.freg[(((size_t)leaf * 4 + kN) * 4 + k) * N + tx * T + ci] = Fhi;
             Flo = Fhi;
             f0 = f1;
             f1 = f2;
@@ -641,12 +641,12 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
     for (int r = 0; r < CPT; ++r) {
         const int j = cj0 + r;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) po[k * nn + (size_t)r * n] = out[r][k];
-        bool edge_cf = ((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
-                       ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1);
+        for (int k = 0; k < 4; ++k) po[k * NN + r * N] = out[r][k];
+        bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
+                                       ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
         if (!edge_cf) {
             if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
-                report_error(a.err, d.slot, a.stage, (int)((ty * T + j) * n + tx * T + ci));
+                report_error(a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + ci);
             if (a.want_lambda) {
                 double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
                 unsigned long long b = (unsigned long long)__double_as_longlong(sp);
@@ -660,18 +660,19 @@ __global__ void __launch_bounds__(C4Cfg<T>::NT, C4Cfg<T>::MINB) stage_c4_kernel(
     }
 }
 
-template <int T>
+template <int N>
 cudaError_t launch_c4_t(const StageArgs& a, cudaStream_t s) {
+    constexpr int T = N > 32 ? 32 : N;
     constexpr size_t smem = stage_smem<0, T>();
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(stage_c4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(stage_c4_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    unsigned blocks = (unsigned)a.nleaves * a.tiles * a.tiles;
+    unsigned blocks = (unsigned)a.nleaves * (N / T) * (N / T);
     if (blocks == 0) return cudaSuccess;
-    stage_c4_kernel<T><<<blocks, C4Cfg<T>::NT, smem, s>>>(a);
+    stage_c4_kernel<N><<<blocks, C4Cfg<T>::NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -679,10 +680,13 @@ template <int SCHEME>
 cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
     int T = a.geo.n / a.tiles;
     if (SCHEME == 0) {
-        if (T == 8) return launch_c4_t<8>(a, s);
-        if (T == 16) return launch_c4_t<16>(a, s);
-        if (T == 32) return launch_c4_t<32>(a, s);
-        return cudaErrorInvalidValue;
+        switch (a.geo.n) {
+            case 8: return launch_c4_t<8>(a, s);
+            case 16: return launch_c4_t<16>(a, s);
+            case 32: return launch_c4_t<32>(a, s);
+            case 64: return launch_c4_t<64>(a, s);
+            default: return cudaErrorInvalidValue;
+        }
     }
     if (T == 8) return launch_stage_t<SCHEME, 8>(a, s);
     if (T == 16) return launch_stage_t<SCHEME, 16>(a, s);
