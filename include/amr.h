@@ -83,6 +83,9 @@ typedef struct {
     const void* nccl_unique_id;   /* 128-byte ncclUniqueId broadcast by the caller (world_size > 1) */
     int32_t check_positivity;     /* 1: amr_step checks rho, p > 0 and finiteness (default)  */
     int32_t use_graphs;           /* 1: capture one step as a CUDA graph and replay it        */
+    int32_t comm_backend;         /* world_size > 1: 0 NCCL (nccl_unique_id = ncclUniqueId); 1 in-process
+                                     loopback of virtual ranks on one GPU, one host thread each
+                                     (test-only; nccl_unique_id = 128-byte group key string)   */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none
@@ -187,6 +190,11 @@ amr_status amr_diagnostics(amr_ctx* ctx, double totals[4], double* lambda_max);
 amr_status amr_set_kernel_timing(amr_ctx* ctx, int32_t enable);
 amr_status amr_get_stats(amr_ctx* ctx, amr_stats* out);
 amr_status amr_reset_stats(amr_ctx* ctx);
+
+/* Fill out128 with a fresh ncclUniqueId (rank 0; the caller broadcasts it, e.g. through a torch
+ * process group).  Loads torch's libnccl.so.2 (or $AMR_NCCL_LIB) at run time.  AMR_E_COMM if NCCL is
+ * unavailable. */
+amr_status amr_nccl_unique_id(void* out128);
 
 /* Message of the last failing call on ctx (valid until the next call); ctx may be NULL. */
 const char* amr_last_error(const amr_ctx* ctx);

@@ -1,0 +1,34 @@
+/*
+ * amr_debug.h -- host-only planning entry points of libamr.so (TEST-ONLY; no CUDA call is made).
+ *
+ * They expose the multi-rank plan the library computes from the replicated patch tree
+ * (SURVEY.md s8(e)): the root-tree Morton partition and the per-peer exchange lists, so the N > 1
+ * host logic can be checked on CPU (world-size-2 gloo tests) without a GPU.
+ * Indices are canonical tree indices ((level, j, i) order, as amr_get_patch_tree).
+ */
+#ifndef PAPER_2508_05020_AMR_DEBUG_H
+#define PAPER_2508_05020_AMR_DEBUG_H
+#include "amr.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct amr_plan amr_plan;
+
+/* Root scaffold of cfg (validated as amr_create; the device fields are ignored). */
+amr_status amr_plan_create(const amr_config* cfg, amr_plan** out);
+void amr_plan_destroy(amr_plan* p);
+/* Apply refine (bit 1) / coarsen (bit 2) requests exactly as amr_regrid_with_flags does to the tree. */
+amr_status amr_plan_regrid(amr_plan* p, int32_t n, const int32_t* tree_index, const uint8_t* bits);
+/* Patch metadata in canonical order (owner = rank under a world_size partition). */
+amr_status amr_plan_tree(amr_plan* p, int32_t world_size, amr_patch_desc* out, int32_t cap, int32_t* count);
+/* Exchange lists of `rank`: kind 0 halo (per stage), 1 flux registers.  counts_*[world] per peer;
+ * the index arrays hold the peers' lists back to back (capacity cap each). */
+amr_status amr_plan_exchange(amr_plan* p, int32_t world_size, int32_t rank, int32_t kind, int32_t* send_counts,
+                             int32_t* send_index, int32_t* recv_counts, int32_t* recv_index, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -29,7 +29,8 @@ COARSEN = {"r2_exact": 0, "alg2_literal": 1}
 ABI_SYMBOLS = ["amr_abi_version", "amr_default_config", "amr_query_pool_bytes", "amr_create", "amr_destroy",
                "amr_set_state", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
                "amr_regrid", "amr_regrid_with_flags", "amr_get_patch_tree", "amr_diagnostics",
-               "amr_set_kernel_timing", "amr_get_stats", "amr_reset_stats", "amr_last_error"]
+               "amr_set_kernel_timing", "amr_get_stats", "amr_reset_stats", "amr_nccl_unique_id",
+               "amr_last_error"]
 
 
 class amr_config(C.Structure):
@@ -41,7 +42,7 @@ class amr_config(C.Structure):
                 ("max_patches", C.c_int32), ("pool", C.c_void_p), ("pool_bytes", C.c_uint64),
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("world_size", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("check_positivity", C.c_int32),
-                ("use_graphs", C.c_int32)]
+                ("use_graphs", C.c_int32), ("comm_backend", C.c_int32)]
 
 
 class amr_patch_desc(C.Structure):
@@ -97,8 +98,18 @@ def load(path: str = LIB_PATH):
     L.amr_reset_stats.argtypes = [_P]
     L.amr_last_error.argtypes = [_P]
     L.amr_last_error.restype = C.c_char_p
+    L.amr_nccl_unique_id.argtypes = [C.c_void_p]
     _lib = L
     return L
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (call on rank 0, broadcast to the others)."""
+    buf = C.create_string_buffer(128)
+    rc = load().amr_nccl_unique_id(buf)
+    if rc != AMR_OK:
+        raise AmrError(rc, "amr_nccl_unique_id failed (is torch's NCCL loadable?)")
+    return buf.raw
 
 
 class AmrError(RuntimeError):
@@ -144,7 +155,11 @@ def make_config(cfg: dict, **over) -> amr_config:
 class Mesh:
     """One composite AMR mesh on one GPU (one rank), advanced by the CUDA path."""
 
-    def __init__(self, cfg: dict, stream=None, pool=None, **over):
+    def __init__(self, cfg: dict, stream=None, pool=None, world_size=1, rank=0, comm_backend=0, comm_id=None,
+                 **over):
+        """world_size > 1: comm_backend 0 (NCCL; comm_id = 128-byte ncclUniqueId from nccl_unique_id(),
+        broadcast by the caller) or 1 (in-process loopback, one host thread per virtual rank; comm_id =
+        group key)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2508_05020_b200.Mesh needs a CUDA device (no CPU fallback)")
@@ -152,6 +167,13 @@ class Mesh:
         self.cfg = dict(cfg)
         self.n = cfg["n"]
         self._keep = []
+        self.world_size, self.rank = world_size, rank
+        if world_size > 1:
+            key = comm_id if isinstance(comm_id, (bytes, bytearray)) else str(comm_id).encode()
+            buf = C.create_string_buffer(bytes(key).ljust(128, b"\0")[:128], 128)
+            self._keep.append(buf)
+            over.update(world_size=world_size, rank=rank, comm_backend=comm_backend,
+                        nccl_unique_id=C.cast(buf, C.c_void_p).value)
         if stream is None:
             stream = torch.cuda.current_stream()
         if stream.cuda_stream == 0:

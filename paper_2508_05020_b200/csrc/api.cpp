@@ -121,8 +121,8 @@ amr_status build_plan(amr_ctx* c) {
                     else { cidx[0] = 0; cidx[1] = 1; }
                     for (int h = 0; h < 2; ++h) {
                         int ch = t.child[4 * nb + cidx[h]];
-                        if (ch < 0 || !t.is_leaf(ch) || c->leaf_pos[ch] < 0) return fail(c, AMR_E_MESH, "reflux: fine side is not a local leaf");
-                        rt.fine[s][h] = c->leaf_pos[ch];
+                        if (ch < 0 || !t.is_leaf(ch)) return fail(c, AMR_E_MESH, "reflux: fine side is not a leaf");
+                        rt.fine[s][h] = ch;
                     }
                 }
             } else {
@@ -172,7 +172,7 @@ amr_status build_plan(amr_ctx* c) {
     c->d_rlev.resize(L);
     for (int l = 0; l < L; ++l) CU(c->d_rlev[l].upload(c->rlev[l], s));
     CU(c->proxy.reserve(std::max<size_t>(1, c->ptasks.size()) * c->PS));
-    CU(c->freg.reserve(std::max<size_t>(1, c->leaves.size()) * 16 * c->n));
+    CU(c->freg.reserve((size_t)t.capacity * 16 * c->n));   // indexed by slot (remote fine leaves arrive by exchange)
     CU(c->d_maxeta.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_amb.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_partial.reserve(4 * std::max<size_t>(1, c->leaves.size())));
@@ -184,6 +184,7 @@ amr_status build_plan(amr_ctx* c) {
     c->st.leaf_cells = c->leaf_cells;
     c->st.proxies = (int64_t)c->ptasks.size();
     c->lambda_valid = false;
+    c->comm.replan(t);
     return AMR_OK;
 }
 
@@ -353,11 +354,11 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
 amr_status finish_step(amr_ctx* c, int prev_un, double* dt_used) {
     int32_t* he = (int32_t*)c->h_pinned;
     double* hdt = (double*)((char*)c->h_pinned + 16);
+    amr_status cs = c->comm.allreduce_max_i32(c, c->d_err, 1);   // every rank sees an error anywhere
+    if (cs != AMR_OK) return cs;
     CU(cudaMemcpyAsync(he, c->d_err, 16, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaMemcpyAsync(hdt, c->d_dt, 8, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
-    amr_status s = c->comm.agree_error(c, he);
-    if (s != AMR_OK) return s;
     if (he[0] != 0) {
         int32_t e0 = he[0], slot = he[1], stage = he[2], cell = he[3];
         CU(cudaMemsetAsync(c->d_err, 0, 16, c->stream));
@@ -450,34 +451,49 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
         }
     if (!nt.validate(m)) return fail(c, AMR_E_MESH, "regrid produced an invalid mesh: " + m);
     int n_new = 0, n_del = 0;
+    const int W = c->comm.world, R = c->comm.rank;
+    // ownership of the new tree under the OLD partition (roots never change): the old owner of a
+    // root prolongs the new patches of that root, since it holds their parents' data
+    std::vector<int32_t> old_owner(nt.capacity, -1);
+    std::vector<uint8_t> is_new(nt.capacity, 0);
+    for (int id = 0; id < nt.capacity; ++id) {
+        if (!nt.alive[id]) continue;
+        int l = nt.lev[id];
+        int root = nt.find(0, nt.pi[id] >> l, nt.pj[id] >> l);
+        old_owner[id] = W == 1 ? 0 : c->comm.owner[root];
+        if (!c->tree.alive[id]) { is_new[id] = 1; ++n_new; }
+    }
+    for (int id = 0; id < nt.capacity; ++id)
+        if (c->tree.alive[id] && !nt.alive[id]) ++n_del;
     std::vector<std::vector<ProlongTask>> pro(c->cfg.num_levels);
     for (int id = 0; id < nt.capacity; ++id) {
-        if (nt.alive[id] && !c->tree.alive[id]) {
-            ++n_new;
-            ProlongTask p{};
-            p.slot = id;
-            p.level = nt.lev[id];
-            p.P = nt.pi[id];
-            p.Q = nt.pj[id];
-            int par = nt.parent[id];
-            for (int dy = -1; dy <= 1; ++dy)
-                for (int dx = -1; dx <= 1; ++dx) {
-                    int q = (dx == 0 && dy == 0) ? par : nt.neighbour(par, dx, dy);
-                    if (q == -1) return fail(c, AMR_E_MESH, "prolongation: coarse neighbourhood incomplete");
-                    p.coarse[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
-                }
-            pro[p.level].push_back(p);
-        }
-        if (c->tree.alive[id] && !nt.alive[id]) ++n_del;
+        if (!is_new[id] || old_owner[id] != (W == 1 ? 0 : R)) continue;
+        ProlongTask p{};
+        p.slot = id;
+        p.level = nt.lev[id];
+        p.P = nt.pi[id];
+        p.Q = nt.pj[id];
+        int par = nt.parent[id];
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                int q = (dx == 0 && dy == 0) ? par : nt.neighbour(par, dx, dy);
+                if (q == -1) return fail(c, AMR_E_MESH, "prolongation: coarse neighbourhood incomplete");
+                p.coarse[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
+            }
+        pro[p.level].push_back(p);
     }
     c->tree = nt;
+    if (W > 1) c->comm.owner = old_owner;
     amr_status s = build_plan(c);
     if (s != AMR_OK) return s;
     double* Un = c->U[c->un];
     for (int l = 1; l < c->cfg.num_levels; ++l) {
+        if (W > 1) {
+            ExchangeLists xl = plan_coarse(nt, is_new, l, old_owner, W, R);
+            s = c->comm.exchange_lists(c, xl, Un, (int)c->PS, "coarse exchange");
+            if (s != AMR_OK) return s;
+        }
         if (pro[l].empty()) continue;
-        s = c->comm.exchange_coarse(c, Un, l);
-        if (s != AMR_OK) return s;
         CU(c->d_prolong.upload(pro[l], c->stream));
         AuxArgs a = aux(c, Un, Un);
         LAUNCH(launch_prolong(c->d_prolong.p, (int)pro[l].size(), a, c->stream), "prolong");
@@ -485,6 +501,16 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     }
     s = restrict_all(c, Un);
     if (s != AMR_OK) return s;
+    if (W > 1) {
+        // repartition the new tree and migrate every patch whose owner changed
+        std::vector<int32_t> new_owner = partition_owners(nt, W);
+        ExchangeLists mig = plan_migration(nt, old_owner, new_owner, W, R);
+        s = c->comm.exchange_lists(c, mig, Un, (int)c->PS, "migration");
+        if (s != AMR_OK) return s;
+        c->comm.owner = new_owner;
+        s = build_plan(c);
+        if (s != AMR_OK) return s;
+    }
     CU(cudaStreamSynchronize(c->stream));
     c->lambda_valid = false;
     c->fl_ref.assign(nt.capacity, 0);
@@ -667,7 +693,7 @@ amr_status amr_set_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, 
                                    c->stream));
         }
         CU(cudaMemcpyAsync(c->d_slots.p, slots.data() + b, m * 4, cudaMemcpyHostToDevice, c->stream));
-        LAUNCH(launch_scatter(c->staging.p, c->d_slots.p, (int)m, c->U[c->un], c->n, c->stream), "scatter");
+        LAUNCH(launch_scatter(c->staging.p, c->d_slots.p, (int)m, c->U[c->un], (int)PS, c->stream), "scatter");
         CU(cudaStreamSynchronize(c->stream));
     }
     s = c->comm.exchange_children(c, c->U[c->un]);
@@ -697,7 +723,7 @@ amr_status amr_set_state_device(amr_ctx* c, int32_t npatch, const int32_t* tree_
         if (!contiguous) return fail(c, AMR_E_ARG, "set_state_device: tree_index rows of local patches must be contiguous");
         CU(c->d_slots.reserve(m));
         CU(cudaMemcpyAsync(c->d_slots.p, slots.data() + b, m * 4, cudaMemcpyHostToDevice, c->stream));
-        LAUNCH(launch_scatter(dU + (size_t)which[b] * PS, c->d_slots.p, (int)m, c->U[c->un], c->n, c->stream), "scatter");
+        LAUNCH(launch_scatter(dU + (size_t)which[b] * PS, c->d_slots.p, (int)m, c->U[c->un], (int)PS, c->stream), "scatter");
         CU(cudaStreamSynchronize(c->stream));
     }
     s = c->comm.exchange_children(c, c->U[c->un]);
@@ -720,8 +746,8 @@ amr_status amr_get_state_device(amr_ctx* c, int32_t npatch, const int32_t* tree_
     if (slots.empty()) return AMR_OK;
     CU(c->d_slots.reserve(slots.size()));
     CU(cudaMemcpyAsync(c->d_slots.p, slots.data(), slots.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    LAUNCH(launch_gather(c->U[c->un], c->d_slots.p, (int)slots.size(), dU_out + (size_t)which[0] * c->PS, c->n, c->stream),
-           "gather");
+    LAUNCH(launch_gather(c->U[c->un], c->d_slots.p, (int)slots.size(), dU_out + (size_t)which[0] * c->PS, (int)c->PS,
+                         c->stream), "gather");
     CU(cudaStreamSynchronize(c->stream));
     return AMR_OK;
 }
@@ -741,7 +767,7 @@ amr_status amr_get_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, 
         CU(c->staging.reserve(m * PS));
         CU(c->d_slots.reserve(m));
         CU(cudaMemcpyAsync(c->d_slots.p, slots.data() + b, m * 4, cudaMemcpyHostToDevice, c->stream));
-        LAUNCH(launch_gather(c->U[c->un], c->d_slots.p, (int)m, c->staging.p, c->n, c->stream), "gather");
+        LAUNCH(launch_gather(c->U[c->un], c->d_slots.p, (int)m, c->staging.p, (int)PS, c->stream), "gather");
         bool contiguous = true;
         for (size_t k = 1; k < m; ++k) contiguous &= which[b + k] == which[b] + (int)k;
         if (contiguous) {

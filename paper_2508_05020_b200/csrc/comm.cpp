@@ -1,27 +1,513 @@
-// comm.cpp -- see comm.h.
+// comm.cpp -- see comm.h.  Host planning (pure functions), the NCCL and loopback transports, and
+// the exchange / collective hooks called by the step driver (api.cpp).
 #include "comm.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
 
 #include "ctx.h"
 
+#ifdef AMR_HAVE_NCCL_H
+#include <nccl.h>
+#endif
+
 namespace amr {
+
+// =====================================================================================  planning
+namespace {
+const int kSideDir[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
+
+ExchangeLists from_needs(const std::vector<std::map<int, std::set<int32_t>>>& need, int world, int rank) {
+    // need[o][p] = slots owned by p that rank o needs
+    ExchangeLists L;
+    L.reset(world);
+    for (int p = 0; p < world; ++p) {
+        auto it = need[rank].find(p);
+        if (it != need[rank].end()) L.recv[p].assign(it->second.begin(), it->second.end());
+    }
+    for (int o = 0; o < world; ++o) {
+        auto it = need[o].find(rank);
+        if (it != need[o].end()) L.send[o].assign(it->second.begin(), it->second.end());
+    }
+    return L;
+}
+}  // namespace
+
+std::vector<int32_t> partition_owners(const PatchTree& t, int world) {
+    std::vector<int32_t> owner(t.capacity, -1);
+    if (world <= 1) {
+        for (int id = 0; id < t.capacity; ++id)
+            if (t.alive[id]) owner[id] = 0;
+        return owner;
+    }
+    const int npx = t.np0[0], npy = t.np0[1];
+    std::vector<int64_t> weight((size_t)npx * npy, 0);
+    for (int id = 0; id < t.capacity; ++id) {
+        if (!t.is_leaf(id)) continue;
+        int l = t.lev[id];
+        weight[(size_t)(t.pj[id] >> l) * npx + (t.pi[id] >> l)] += 1;
+    }
+    std::vector<int32_t> roots((size_t)npx * npy);
+    for (size_t r = 0; r < roots.size(); ++r) roots[r] = (int32_t)r;
+    std::stable_sort(roots.begin(), roots.end(), [&](int a, int b) {
+        return morton((uint32_t)(a % npx), (uint32_t)(a / npx)) < morton((uint32_t)(b % npx), (uint32_t)(b / npx));
+    });
+    int64_t total = 0;
+    for (auto w : weight) total += w;
+    std::vector<int32_t> root_rank((size_t)npx * npy, 0);
+    int64_t prefix = 0;
+    for (int r : roots) {
+        int64_t w = weight[r];
+        int64_t k = ((2 * prefix + w) * (int64_t)world) / (2 * std::max<int64_t>(total, 1));
+        root_rank[r] = (int32_t)std::min<int64_t>(k, world - 1);
+        prefix += w;
+    }
+    for (int id = 0; id < t.capacity; ++id) {
+        if (!t.alive[id]) continue;
+        int l = t.lev[id];
+        owner[id] = root_rank[(size_t)(t.pj[id] >> l) * npx + (t.pi[id] >> l)];
+    }
+    return owner;
+}
+
+void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out) {
+    out.clear();
+    for (int s = 0; s < 4; ++s) {
+        int nb = t.neighbour(id, kSideDir[s][0], kSideDir[s][1]);
+        if (nb >= 0) {
+            out.push_back(nb);
+        } else if (nb == -1) {
+            int par = t.parent[id];
+            if (par < 0) continue;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
+                    if (q >= 0) out.push_back(q);
+                }
+        }
+    }
+}
+
+ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank) {
+    std::vector<std::map<int, std::set<int32_t>>> need(world);
+    std::vector<int32_t> src;
+    for (int id = 0; id < t.capacity; ++id) {
+        if (!t.is_leaf(id)) continue;
+        int o = owner[id];
+        halo_sources(t, id, src);
+        for (int q : src)
+            if (owner[q] != o) need[o][owner[q]].insert(q);
+    }
+    return from_needs(need, world, rank);
+}
+
+ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank) {
+    static const int cidx[4][2] = {{1, 3}, {0, 2}, {2, 3}, {0, 1}};
+    std::vector<std::map<int, std::set<int32_t>>> need(world);
+    for (int id = 0; id < t.capacity; ++id) {
+        if (!t.is_leaf(id)) continue;
+        for (int s = 0; s < 4; ++s) {
+            int nb = t.neighbour(id, kSideDir[s][0], kSideDir[s][1]);
+            if (nb < 0 || !t.has_children(nb)) continue;
+            for (int h = 0; h < 2; ++h) {
+                int f = t.child[4 * nb + cidx[s][h]];
+                if (owner[f] != owner[id]) need[owner[id]][owner[f]].insert(f);
+            }
+        }
+    }
+    return from_needs(need, world, rank);
+}
+
+ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_new, int level,
+                          const std::vector<int32_t>& owner, int world, int rank) {
+    std::vector<std::map<int, std::set<int32_t>>> need(world);
+    for (int id = 0; id < nt.capacity; ++id) {
+        if (!nt.alive[id] || !is_new[id] || nt.lev[id] != level) continue;
+        int o = owner[id], par = nt.parent[id];
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                int q = (dx == 0 && dy == 0) ? par : nt.neighbour(par, dx, dy);
+                if (q >= 0 && owner[q] != o) need[o][owner[q]].insert(q);
+            }
+    }
+    return from_needs(need, world, rank);
+}
+
+ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& old_owner,
+                             const std::vector<int32_t>& new_owner, int world, int rank) {
+    std::vector<std::map<int, std::set<int32_t>>> need(world);
+    for (int id = 0; id < nt.capacity; ++id)
+        if (nt.alive[id] && old_owner[id] != new_owner[id]) need[new_owner[id]][old_owner[id]].insert(id);
+    return from_needs(need, world, rank);
+}
+
+// =====================================================================================  transports
+struct Xfer {
+    int peer;
+    void* buf;
+    size_t bytes;
+};
+
+struct Transport {
+    virtual ~Transport() {}
+    virtual std::string p2p(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) = 0;
+    // in-place allreduce on a device buffer; kind 0: max u64, 1: max f64, 2: sum f64, 3: max i32
+    virtual std::string allreduce(void* d, size_t count, int kind, cudaStream_t s) = 0;
+};
+
+// ---- NCCL (torch's libnccl.so.2, resolved at run time)
+#ifdef AMR_HAVE_NCCL_H
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool load(std::string& err) {
+        if (h) return true;
+        const char* env = getenv("AMR_NCCL_LIB");
+        const char* names[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
+        for (const char* nm : names) {
+            h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) { err = "cannot dlopen libnccl.so.2 (import torch first or set AMR_NCCL_LIB)"; return false; }
+#define SYM(f, name) f = reinterpret_cast<decltype(f)>(dlsym(h, name)); if (!f) { err = std::string("missing NCCL symbol ") + name; return false; }
+        SYM(CommInitRank, "ncclCommInitRank");
+        SYM(CommDestroy, "ncclCommDestroy");
+        SYM(GetUniqueId, "ncclGetUniqueId");
+        SYM(Send, "ncclSend");
+        SYM(Recv, "ncclRecv");
+        SYM(GroupStart, "ncclGroupStart");
+        SYM(GroupEnd, "ncclGroupEnd");
+        SYM(AllReduce, "ncclAllReduce");
+        SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+        return true;
+    }
+};
+NcclApi& nccl_api() {
+    static NcclApi api;
+    return api;
+}
+
+struct NcclTransport : Transport {
+    ncclComm_t comm = nullptr;
+    std::string err(ncclResult_t r) { return std::string("NCCL: ") + nccl_api().GetErrorString(r); }
+    std::string p2p(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
+        NcclApi& A = nccl_api();
+        ncclResult_t r = A.GroupStart();
+        if (r != ncclSuccess) return err(r);
+        for (auto& x : sends)
+            if (x.bytes && (r = A.Send(x.buf, x.bytes, ncclChar, x.peer, comm, s)) != ncclSuccess) return err(r);
+        for (auto& x : recvs)
+            if (x.bytes && (r = A.Recv(x.buf, x.bytes, ncclChar, x.peer, comm, s)) != ncclSuccess) return err(r);
+        r = A.GroupEnd();
+        return r == ncclSuccess ? std::string() : err(r);
+    }
+    std::string allreduce(void* d, size_t count, int kind, cudaStream_t s) override {
+        ncclDataType_t t = kind == 0 ? ncclUint64 : (kind == 3 ? ncclInt32 : ncclFloat64);
+        ncclRedOp_t op = kind == 2 ? ncclSum : ncclMax;
+        ncclResult_t r = nccl_api().AllReduce(d, d, count, t, op, comm, s);
+        return r == ncclSuccess ? std::string() : err(r);
+    }
+    ~NcclTransport() override {
+        if (comm) nccl_api().CommDestroy(comm);
+    }
+};
+#endif
+
+// ---- loopback: virtual ranks = host threads of one process on one GPU (test-only)
+struct LoopGroup {
+    int world = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    long gen = 0;
+    std::vector<std::vector<Xfer>> sends;
+    std::vector<cudaEvent_t> ready, done;
+    std::vector<void*> bufs;
+    int users = 0;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        long g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+std::mutex g_loop_mu;
+std::map<std::string, std::shared_ptr<LoopGroup>> g_loops;
+
+struct LoopTransport : Transport {
+    std::shared_ptr<LoopGroup> G;
+    std::string key;
+    int rank = 0;
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+    std::vector<unsigned char> host;
+    std::string p2p(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
+        cudaEventRecord(ev_ready, s);
+        G->sends[rank] = sends;
+        G->ready[rank] = ev_ready;
+        G->barrier();
+        for (auto& rv : recvs) {
+            if (!rv.bytes) continue;
+            const Xfer* match = nullptr;
+            for (auto& sx : G->sends[rv.peer])
+                if (sx.peer == rank) { match = &sx; break; }
+            if (!match || match->bytes != rv.bytes) return "loopback: unmatched receive";
+            cudaStreamWaitEvent(s, G->ready[rv.peer], 0);
+            cudaError_t e = cudaMemcpyAsync(rv.buf, match->buf, rv.bytes, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return cudaGetErrorString(e);
+        }
+        cudaEventRecord(ev_done, s);
+        G->done[rank] = ev_done;
+        G->barrier();
+        for (auto& sx : sends)
+            if (sx.bytes) cudaStreamWaitEvent(s, G->done[sx.peer], 0);
+        G->barrier();
+        return std::string();
+    }
+    std::string allreduce(void* d, size_t count, int kind, cudaStream_t s) override {
+        size_t esz = kind == 3 ? 4 : 8;
+        size_t bytes = count * esz;
+        cudaStreamSynchronize(s);
+        G->bufs[rank] = d;
+        G->barrier();
+        std::vector<unsigned char> acc(bytes), tmp(bytes);
+        for (int q = 0; q < G->world; ++q) {
+            if (cudaMemcpy(q == 0 ? acc.data() : tmp.data(), G->bufs[q], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return "loopback allreduce copy failed";
+            if (q == 0) continue;
+            for (size_t e = 0; e < count; ++e) {
+                if (kind == 0) {
+                    uint64_t a, b; std::memcpy(&a, &acc[e * 8], 8); std::memcpy(&b, &tmp[e * 8], 8);
+                    a = std::max(a, b); std::memcpy(&acc[e * 8], &a, 8);
+                } else if (kind == 1 || kind == 2) {
+                    double a, b; std::memcpy(&a, &acc[e * 8], 8); std::memcpy(&b, &tmp[e * 8], 8);
+                    a = kind == 1 ? (b > a ? b : a) : a + b; std::memcpy(&acc[e * 8], &a, 8);
+                } else {
+                    int32_t a, b; std::memcpy(&a, &acc[e * 4], 4); std::memcpy(&b, &tmp[e * 4], 4);
+                    a = std::max(a, b); std::memcpy(&acc[e * 4], &a, 4);
+                }
+            }
+        }
+        G->barrier();   // everyone has read every buffer
+        if (cudaMemcpy(d, acc.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return "loopback allreduce write failed";
+        G->barrier();
+        return std::string();
+    }
+    ~LoopTransport() override {
+        if (ev_ready) cudaEventDestroy(ev_ready);
+        if (ev_done) cudaEventDestroy(ev_done);
+        std::lock_guard<std::mutex> lk(g_loop_mu);
+        if (G && --G->users == 0) g_loops.erase(key);
+    }
+};
+
+// =====================================================================================  Comm
+Comm::Comm() = default;
+Comm::~Comm() = default;
 
 amr_status Comm::init(amr_ctx* c) {
     world = c->cfg.world_size;
     rank = c->cfg.rank;
-    if (world != 1) {
-        c->err = "world_size > 1 is not built into this library yet";
-        return AMR_E_CONFIG;
+    owner = partition_owners(c->tree, world);
+    if (world == 1) return AMR_OK;
+    if (c->cfg.comm_backend == 1) {
+        auto* T = new LoopTransport();
+        T->rank = rank;
+        T->key.assign((const char*)c->cfg.nccl_unique_id, strnlen((const char*)c->cfg.nccl_unique_id, 128));
+        {
+            std::lock_guard<std::mutex> lk(g_loop_mu);
+            auto& G = g_loops[T->key];
+            if (!G) {
+                G = std::make_shared<LoopGroup>();
+                G->world = world;
+                G->sends.resize(world);
+                G->ready.resize(world);
+                G->done.resize(world);
+                G->bufs.resize(world);
+            }
+            if (G->world != world) { delete T; c->err = "loopback group size mismatch"; return AMR_E_CONFIG; }
+            G->users++;
+            T->G = G;
+        }
+        cudaEventCreateWithFlags(&T->ev_ready, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&T->ev_done, cudaEventDisableTiming);
+        tr.reset(T);
+        T->G->barrier();   // all virtual ranks created
+        return AMR_OK;
+    }
+#ifdef AMR_HAVE_NCCL_H
+    std::string e;
+    if (!nccl_api().load(e)) { c->err = e; return AMR_E_COMM; }
+    auto* T = new NcclTransport();
+    ncclUniqueId id;
+    std::memcpy(&id, c->cfg.nccl_unique_id, sizeof id);
+    ncclResult_t r = nccl_api().CommInitRank(&T->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        c->err = std::string("ncclCommInitRank: ") + nccl_api().GetErrorString(r);
+        delete T;
+        return AMR_E_COMM;
+    }
+    tr.reset(T);
+    return AMR_OK;
+#else
+    c->err = "library built without nccl.h";
+    return AMR_E_COMM;
+#endif
+}
+
+void Comm::finalize(amr_ctx*) { tr.reset(); }
+
+void Comm::repartition(const PatchTree& t) { owner = partition_owners(t, world); }
+
+void Comm::replan(const PatchTree& t) {
+    if (world == 1) return;
+    halo = plan_halo(t, owner, world, rank);
+    flux = plan_flux(t, owner, world, rank);
+}
+
+amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per, const char* what) {
+    if (world == 1) return AMR_OK;
+    size_t ns = L.nsend(), nr = L.nrecv();
+    std::vector<int32_t> sidx, ridx;
+    sidx.reserve(ns);
+    ridx.reserve(nr);
+    for (auto& v : L.send) sidx.insert(sidx.end(), v.begin(), v.end());
+    for (auto& v : L.recv) ridx.insert(ridx.end(), v.begin(), v.end());
+    cudaStream_t s = c->stream;
+    if (c->x_sidx.upload(sidx, s) != cudaSuccess || c->x_ridx.upload(ridx, s) != cudaSuccess ||
+        c->x_send.reserve(std::max<size_t>(1, ns * per)) != cudaSuccess ||
+        c->x_recv.reserve(std::max<size_t>(1, nr * per)) != cudaSuccess) {
+        c->err = std::string(what) + ": exchange buffers";
+        c->sticky = AMR_E_CUDA;
+        return AMR_E_CUDA;
+    }
+    if (ns && launch_gather(U, c->x_sidx.p, (int)ns, c->x_send.p, per, s) != cudaSuccess) {
+        c->err = std::string(what) + ": pack";
+        c->sticky = AMR_E_CUDA;
+        return AMR_E_CUDA;
+    }
+    std::vector<Xfer> sends, recvs;
+    size_t so = 0, ro = 0;
+    for (int p = 0; p < world; ++p) {
+        if (!L.send[p].empty()) sends.push_back({p, c->x_send.p + so * per, L.send[p].size() * per * sizeof(double)});
+        if (!L.recv[p].empty()) recvs.push_back({p, c->x_recv.p + ro * per, L.recv[p].size() * per * sizeof(double)});
+        so += L.send[p].size();
+        ro += L.recv[p].size();
+    }
+    std::string e = tr->p2p(sends, recvs, s);
+    if (!e.empty()) {
+        c->err = std::string(what) + ": " + e;
+        c->sticky = AMR_E_COMM;
+        return AMR_E_COMM;
+    }
+    bytes_sent += (int64_t)(ns * per * sizeof(double));
+    if (nr && launch_scatter(c->x_recv.p, c->x_ridx.p, (int)nr, U, per, s) != cudaSuccess) {
+        c->err = std::string(what) + ": unpack";
+        c->sticky = AMR_E_CUDA;
+        return AMR_E_CUDA;
+    }
+    c->st.launches += (ns ? 1 : 0) + (nr ? 1 : 0);
+    return AMR_OK;
+}
+
+amr_status Comm::exchange_halos(amr_ctx* c, double* U) {
+    return exchange_lists(c, halo, U, (int)c->PS, "halo exchange");
+}
+
+amr_status Comm::exchange_fluxes(amr_ctx* c) {
+    return exchange_lists(c, flux, c->freg.p, 16 * c->n, "flux-register exchange");
+}
+
+amr_status Comm::allreduce_max_u64(amr_ctx* c, unsigned long long* d) {
+    if (world == 1) return AMR_OK;
+    std::string e = tr->allreduce(d, 1, 0, c->stream);
+    if (!e.empty()) { c->err = e; c->sticky = AMR_E_COMM; return AMR_E_COMM; }
+    return AMR_OK;
+}
+
+amr_status Comm::allreduce_max_i32(amr_ctx* c, int32_t* d, int n) {
+    if (world == 1) return AMR_OK;
+    std::string e = tr->allreduce(d, n, 3, c->stream);
+    if (!e.empty()) { c->err = e; c->sticky = AMR_E_COMM; return AMR_E_COMM; }
+    return AMR_OK;
+}
+
+amr_status Comm::allreduce_sum4(amr_ctx* c, double* h4) {
+    if (world == 1) return AMR_OK;
+    if (c->x_send.reserve(4) != cudaSuccess) { c->sticky = AMR_E_CUDA; return AMR_E_CUDA; }
+    cudaMemcpyAsync(c->x_send.p, h4, 32, cudaMemcpyHostToDevice, c->stream);
+    std::string e = tr->allreduce(c->x_send.p, 4, 2, c->stream);
+    if (!e.empty()) { c->err = e; c->sticky = AMR_E_COMM; return AMR_E_COMM; }
+    cudaMemcpyAsync(h4, c->x_send.p, 32, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    return AMR_OK;
+}
+
+amr_status Comm::allgather_flags(amr_ctx* c, std::vector<double>& eta, std::vector<uint8_t>& amb) {
+    if (world == 1) return AMR_OK;
+    size_t m = eta.size();
+    std::vector<double> e2(m);
+    std::vector<int32_t> a2(m);
+    for (size_t k = 0; k < m; ++k) {
+        e2[k] = (eta[k] >= 0.0) ? eta[k] : -1.0;   // non-owned (NaN) -> -1 loses every max
+        a2[k] = amb[k];
+    }
+    if (c->x_send.reserve(std::max<size_t>(1, m)) != cudaSuccess ||
+        c->x_recv.reserve(std::max<size_t>(1, (m + 1) / 2)) != cudaSuccess) {
+        c->sticky = AMR_E_CUDA;
+        return AMR_E_CUDA;
+    }
+    cudaMemcpyAsync(c->x_send.p, e2.data(), m * 8, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(c->x_recv.p, a2.data(), m * 4, cudaMemcpyHostToDevice, c->stream);
+    std::string e = tr->allreduce(c->x_send.p, m, 1, c->stream);
+    if (e.empty()) e = tr->allreduce(c->x_recv.p, m, 3, c->stream);
+    if (!e.empty()) { c->err = e; c->sticky = AMR_E_COMM; return AMR_E_COMM; }
+    cudaMemcpyAsync(e2.data(), c->x_send.p, m * 8, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(a2.data(), c->x_recv.p, m * 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    for (size_t k = 0; k < m; ++k) {
+        eta[k] = e2[k] >= 0.0 ? e2[k] : std::nan("");
+        amb[k] = (uint8_t)a2[k];
     }
     return AMR_OK;
 }
-void Comm::finalize(amr_ctx*) {}
-amr_status Comm::exchange_halos(amr_ctx*, double*) { return AMR_OK; }
-amr_status Comm::exchange_fluxes(amr_ctx*) { return AMR_OK; }
-amr_status Comm::exchange_coarse(amr_ctx*, double*, int) { return AMR_OK; }
-amr_status Comm::exchange_children(amr_ctx*, double*) { return AMR_OK; }
-amr_status Comm::allreduce_max_u64(amr_ctx*, unsigned long long*) { return AMR_OK; }
-amr_status Comm::allreduce_sum4(amr_ctx*, double*) { return AMR_OK; }
-amr_status Comm::allgather_flags(amr_ctx*, std::vector<double>&, std::vector<uint8_t>&) { return AMR_OK; }
+
 amr_status Comm::agree_error(amr_ctx*, int32_t*) { return AMR_OK; }
 
 }  // namespace amr
+
+// ====================================================================================  C ABI pieces
+extern "C" amr_status amr_nccl_unique_id(void* out128) {
+    if (!out128) return AMR_E_ARG;
+#ifdef AMR_HAVE_NCCL_H
+    std::string e;
+    if (!amr::nccl_api().load(e)) return AMR_E_COMM;
+    ncclUniqueId id;
+    if (amr::nccl_api().GetUniqueId(&id) != ncclSuccess) return AMR_E_COMM;
+    std::memcpy(out128, &id, sizeof id);
+    return AMR_OK;
+#else
+    return AMR_E_COMM;
+#endif
+}

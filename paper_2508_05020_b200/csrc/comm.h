@@ -1,29 +1,70 @@
-// comm.h -- multi-GPU plumbing of one node: ownership of patches and the data
-// exchanges a rank needs each stage.  World size 1 makes every
-// hook a no-op.
+// comm.h -- multi-GPU plumbing of one node.
+//
+// Every rank holds the same (replicated) patch tree and the same global slot numbering.  Patches
+// are owned by root tree: roots in Morton order, weighted by their leaf count, are cut into
+// world_size contiguous chunks, and every patch belongs to the owner of its root, so restriction
+// is always local.  Each rank advances its own leaves; the data its kernels read from patches
+// owned elsewhere (same-level face neighbours, the coarse 3x3 neighbourhood of C/F ghost strips,
+// fine flux registers of a C/F face, the coarse sources of new patches) is copied into the same
+// global slots of the local pool by grouped point-to-point exchanges; Lambda is a max-allreduce.
+// Transports: NCCL (one process per GPU, torch's libnccl.so.2 loaded with dlopen) or an
+// in-process loopback (virtual ranks as host threads on one GPU; test-only).
 #pragma once
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "../../include/amr.h"
+#include "tree.h"
 
 struct amr_ctx;
 
 namespace amr {
 
+// per-peer slot lists (sorted); send[r]: my slots that rank r needs; recv[r]: slots owned by r I need
+struct ExchangeLists {
+    std::vector<std::vector<int32_t>> send, recv;
+    void reset(int world) { send.assign(world, {}); recv.assign(world, {}); }
+    size_t nsend() const { size_t s = 0; for (auto& v : send) s += v.size(); return s; }
+    size_t nrecv() const { size_t s = 0; for (auto& v : recv) s += v.size(); return s; }
+};
+
+// ---- pure host planning (no CUDA): testable on CPU
+std::vector<int32_t> partition_owners(const PatchTree& t, int world);
+// slots read by the stage / flags / ghost kernels of leaf `id` that may live on another rank
+void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out);
+ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
+ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
+// coarse sources of new level-l patches prolonged by the (old) owner of their root
+ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_new, int level,
+                          const std::vector<int32_t>& owner, int world, int rank);
+ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& old_owner,
+                             const std::vector<int32_t>& new_owner, int world, int rank);
+
+struct Transport;
+
 struct Comm {
     int world = 1, rank = 0;
-    void* nccl = nullptr;              // ncclComm_t
-    std::vector<int32_t> owner;        // per slot (patch id), -1 free
+    std::unique_ptr<Transport> tr;
+    std::vector<int32_t> owner;        // per slot (patch id); -1 for free slots
+    ExchangeLists halo, flux;
+    int64_t bytes_sent = 0;
+
+    Comm();
+    ~Comm();
     amr_status init(amr_ctx* c);
     void finalize(amr_ctx* c);
-    bool owns(const amr_ctx* c, int id) const { return world == 1 || owner[id] == rank; }
-    int owner_of(const amr_ctx* c, int id) const { return world == 1 ? 0 : owner[id]; }
-    amr_status exchange_halos(amr_ctx* c, double* U);         // remote data read by local leaves / proxies
-    amr_status exchange_fluxes(amr_ctx* c);                   // remote fine flux registers for reflux
-    amr_status exchange_coarse(amr_ctx* c, double* U, int l); // remote coarse patches for new-patch prolongation
-    amr_status exchange_children(amr_ctx* c, double* U);      // remote children for restriction (none: root-tree ownership)
+    bool owns(const amr_ctx*, int id) const { return world == 1 || owner[id] == rank; }
+    int owner_of(const amr_ctx*, int id) const { return world == 1 ? 0 : owner[id]; }
+    void repartition(const PatchTree& t);      // owner <- partition_owners(t)
+    void replan(const PatchTree& t);           // halo / flux lists for the current owner
+
+    amr_status exchange_halos(amr_ctx* c, double* U);
+    amr_status exchange_fluxes(amr_ctx* c);
+    amr_status exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per_slot, const char* what);
+    amr_status exchange_children(amr_ctx*, double*) { return AMR_OK; }   // root-tree ownership: local
     amr_status allreduce_max_u64(amr_ctx* c, unsigned long long* d);
+    amr_status allreduce_max_i32(amr_ctx* c, int32_t* d, int n);
     amr_status allreduce_sum4(amr_ctx* c, double* h4);
     amr_status allgather_flags(amr_ctx* c, std::vector<double>& eta, std::vector<uint8_t>& amb);
     amr_status agree_error(amr_ctx* c, int32_t* h_err4);

@@ -77,6 +77,8 @@ struct amr_ctx {
     DevArray<ProlongTask> d_prolong;
     DevArray<double> proxy, freg, staging, d_maxeta, d_partial;
     DevArray<int32_t> d_slots, d_amb;
+    DevArray<int32_t> x_sidx, x_ridx;             // multi-rank exchange slot lists
+    DevArray<double> x_send, x_recv;              // multi-rank exchange buffers
     int64_t leaf_cells = 0;
 
     // device scalars: dt, lambda bits, err[4]

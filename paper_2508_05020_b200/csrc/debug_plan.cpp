@@ -1,0 +1,124 @@
+// debug_plan.cpp -- host-only planning API (include/amr_debug.h) for CPU tests of the multi-rank
+// logic.  Uses the same PatchTree, partition and exchange planning as the device path; never calls CUDA.
+#include "../../include/amr_debug.h"
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "tree.h"
+
+struct amr_plan {
+    amr::PatchTree tree;
+    int levels = 1;
+};
+
+namespace {
+std::vector<int32_t> canon_pos_of(const amr::PatchTree& t, std::vector<int32_t>& canon) {
+    canon = t.canonical();
+    std::vector<int32_t> pos(t.capacity, -1);
+    for (size_t e = 0; e < canon.size(); ++e) pos[canon[e]] = (int32_t)e;
+    return pos;
+}
+}  // namespace
+
+extern "C" {
+
+amr_status amr_plan_create(const amr_config* cfg, amr_plan** out) {
+    if (!cfg || !out) return AMR_E_ARG;
+    const amr_config& c = *cfg;
+    int n = c.patch_cells;
+    if (!(n == 8 || n == 16 || n == 32 || n == 64) || c.base_cells[0] % n || c.base_cells[1] % n || c.ratio != 2 ||
+        c.num_levels < 1 || c.max_patches < 1)
+        return AMR_E_CONFIG;
+    int npx = c.base_cells[0] / n, npy = c.base_cells[1] / n;
+    if ((int64_t)npx * npy > c.max_patches) return AMR_E_CAPACITY;
+    amr_plan* p = new amr_plan();
+    p->levels = c.num_levels;
+    p->tree.init(npx, npy, c.num_levels, c.bc[0] == AMR_BC_PERIODIC, c.bc[2] == AMR_BC_PERIODIC, c.max_patches,
+                 c.coarsen_rule);
+    *out = p;
+    return AMR_OK;
+}
+
+void amr_plan_destroy(amr_plan* p) { delete p; }
+
+amr_status amr_plan_regrid(amr_plan* p, int32_t n, const int32_t* tree_index, const uint8_t* bits) {
+    if (!p || n < 0 || (n && (!tree_index || !bits))) return AMR_E_ARG;
+    std::vector<int32_t> canon;
+    canon_pos_of(p->tree, canon);
+    std::vector<uint8_t> ref(p->tree.capacity, 0), crs(p->tree.capacity, 0);
+    for (int k = 0; k < n; ++k) {
+        if (tree_index[k] < 0 || tree_index[k] >= (int)canon.size()) return AMR_E_ARG;
+        ref[canon[tree_index[k]]] = bits[k] & 1;
+        crs[canon[tree_index[k]]] = (bits[k] >> 1) & 1;
+    }
+    amr::PatchTree nt = p->tree;
+    std::string m;
+    for (int id : canon) {
+        if (!ref[id] || !nt.is_leaf(id) || nt.lev[id] >= p->levels - 1) continue;
+        if (!nt.refine(id, m)) return m.find("capacity") != std::string::npos ? AMR_E_CAPACITY : AMR_E_MESH;
+    }
+    for (int l = p->levels - 2; l >= 0; --l)
+        for (int id : canon)
+            if (nt.lev[id] == l && crs[id] && nt.alive[id] && nt.coarsen_allowed(id)) nt.delete_children(id);
+    if (!nt.validate(m)) return AMR_E_MESH;
+    p->tree = nt;
+    return AMR_OK;
+}
+
+amr_status amr_plan_tree(amr_plan* p, int32_t world, amr_patch_desc* out, int32_t cap, int32_t* count) {
+    if (!p || !count || world < 1) return AMR_E_ARG;
+    std::vector<int32_t> canon;
+    std::vector<int32_t> pos = canon_pos_of(p->tree, canon);
+    *count = (int32_t)canon.size();
+    if (!out || cap < *count) return AMR_E_ARG;
+    std::vector<int32_t> owner = amr::partition_owners(p->tree, world);
+    static const int moore[8][2] = {{0, 1}, {1, 0}, {0, -1}, {-1, 0}, {1, 1}, {1, -1}, {-1, -1}, {-1, 1}};
+    const amr::PatchTree& t = p->tree;
+    for (size_t e = 0; e < canon.size(); ++e) {
+        int id = canon[e];
+        amr_patch_desc& d = out[e];
+        d.level = t.lev[id];
+        d.i = t.pi[id];
+        d.j = t.pj[id];
+        d.parent = t.parent[id] >= 0 ? pos[t.parent[id]] : -1;
+        for (int q = 0; q < 4; ++q) d.child[q] = t.child[4 * id + q] >= 0 ? pos[t.child[4 * id + q]] : -1;
+        for (int q = 0; q < 8; ++q) {
+            int nb = t.neighbour(id, moore[q][0], moore[q][1]);
+            d.nbr[q] = nb >= 0 ? pos[nb] : -1;
+        }
+        d.owner = owner[id];
+        d.leaf = t.is_leaf(id);
+        d.refine_req = d.coarsen_req = d.ambiguous = 0;
+    }
+    return AMR_OK;
+}
+
+amr_status amr_plan_exchange(amr_plan* p, int32_t world, int32_t rank, int32_t kind, int32_t* send_counts,
+                             int32_t* send_index, int32_t* recv_counts, int32_t* recv_index, int32_t cap) {
+    if (!p || world < 1 || rank < 0 || rank >= world || !send_counts || !recv_counts || !send_index || !recv_index)
+        return AMR_E_ARG;
+    std::vector<int32_t> canon;
+    std::vector<int32_t> pos = canon_pos_of(p->tree, canon);
+    std::vector<int32_t> owner = amr::partition_owners(p->tree, world);
+    amr::ExchangeLists L = kind == 0 ? amr::plan_halo(p->tree, owner, world, rank)
+                                     : amr::plan_flux(p->tree, owner, world, rank);
+    int ns = 0, nr = 0;
+    for (int q = 0; q < world; ++q) {
+        send_counts[q] = (int32_t)L.send[q].size();
+        recv_counts[q] = (int32_t)L.recv[q].size();
+        for (int s : L.send[q]) {
+            if (ns >= cap) return AMR_E_ARG;
+            send_index[ns++] = pos[s];
+        }
+        for (int s : L.recv[q]) {
+            if (nr >= cap) return AMR_E_ARG;
+            recv_index[nr++] = pos[s];
+        }
+    }
+    return AMR_OK;
+}
+
+}  // extern "C"

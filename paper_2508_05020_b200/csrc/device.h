@@ -5,7 +5,7 @@
 // 4 n^2 doubles per slot, var = rho, rho u, rho v, rho e); a proxy buffer of
 // patch-shaped ghost strips P[proxy][var][j][i] for leaf sides that have no
 // same-level neighbour (coarse/fine or physical boundary); flux registers
-// F[leaf][side][var][n] holding F-hat on coarse/fine sides.
+// F[slot][side][var][n] holding F-hat on coarse/fine sides.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -42,11 +42,11 @@ struct ProxyTask {
 // Flux correction of one coarse leaf (O12): for each C/F side the two fine leaves
 // across it (leaf indices into the flux registers), ordered along the side.
 struct RefluxTask {
-    int32_t leaf;      // index of the coarse leaf in the leaf list (its flux registers)
-    int32_t slot;
+    int32_t leaf;      // index of the coarse leaf in the leaf list
+    int32_t slot;      // its slot (flux registers are indexed by slot)
     int32_t level;
     int32_t mask;      // sides that are coarse sides of a C/F face
-    int32_t fine[4][2];
+    int32_t fine[4][2];   // slots of the two fine leaves across each C/F side
 };
 
 // Restriction parent <- 4 children (O9); child c = a + 2b.
@@ -123,9 +123,10 @@ cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, 
                          cudaStream_t s);
 cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* partial, cudaStream_t s);
 
-// patch-granular copies between a packed [npatch][4][n][n] buffer and the pool slots
-cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int n, cudaStream_t s);
-cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int n, cudaStream_t s);
+// slot-granular copies between a packed [npatch][per] buffer and per-slot arrays (state: per = 4 n^2;
+// flux registers: per = 16 n)
+cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int per, cudaStream_t s);
+cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int per, cudaStream_t s);
 
 // bytes of dynamic shared memory the stage kernel needs (for occupancy queries)
 size_t stage_smem_bytes(int scheme, int n);

@@ -313,9 +313,9 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
                 double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2]) : fh;
                 acc[r][k] = -(Fh - Fl) * idx;
                 if (i == 0 && x_lo && (store_mask & 1))
-                    a.freg[(((size_t)leaf * 4 + kW) * 4 + k) * n + ty * T + j] = Fl;
+                    a.freg[(((size_t)d.slot * 4 + kW) * 4 + k) * n + ty * T + j] = Fl;
                 if (i == T - 1 && x_hi && (store_mask & 2))
-                    a.freg[(((size_t)leaf * 4 + kE) * 4 + k) * n + ty * T + j] = Fh;
+                    a.freg[(((size_t)d.slot * 4 + kE) * 4 + k) * n + ty * T + j] = Fh;
             }
         }
     }
@@ -357,9 +357,9 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
                 double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2 * T]) : fh;
                 double L = acc[r][k] - (Fh - Fl) * idy;
                 if (j == 0 && y_lo && (store_mask & 4))
-                    a.freg[(((size_t)leaf * 4 + kS) * 4 + k) * n + tx * T + i] = Fl;
+                    a.freg[(((size_t)d.slot * 4 + kS) * 4 + k) * n + tx * T + i] = Fl;
                 if (j == T - 1 && y_hi && (store_mask & 8))
-                    a.freg[(((size_t)leaf * 4 + kN) * 4 + k) * n + tx * T + i] = Fh;
+                    a.freg[(((size_t)d.slot * 4 + kN) * 4 + k) * n + tx * T + i] = Fh;
                 double v = __ldg(pin + k * nn + off) + dt * L;
                 if (a.stage > 1) v = a.a * __ldg(pn + k * nn + off) + a.b * v;
                 o4[k] = v;
@@ -567,8 +567,8 @@ __global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 
             double Fh = div4 ? c13 * fh - c24 * (fl + fr[2]) : fh;
             acc[r][k] = -(Fh - Fl) * idx;
             if (store_mask) {
-                if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)leaf * 4 + kW) * 4 + k) * N + ty * T + cj0 + r] = Fl;
-                if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)leaf * 4 + kE) * 4 + k) * N + ty * T + cj0 + r] = Fh;
+                if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + k) * N + ty * T + cj0 + r] = Fl;
+                if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + k) * N + ty * T + cj0 + r] = Fh;
             }
         }
     }
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 
         double fm1 = fc[-T], f0 = fc[0], f1 = fc[T];
         double Flo = div4 ? c13 * f0 - c24 * (fm1 + f1) : f0;
         if (store_mask && cj0 == 0 && y_lo && (store_mask & 4))
-            a.freg[(((size_t)leaf * 4 + kS) * 4 + k) * N + tx * T + ci] = Flo;
+            a.freg[(((size_t)d.slot * 4 + kS) * 4 + k) * N + tx * T + ci] = Flo;
 #pragma unroll
         for (int r = 0; r < CPT; ++r) {
             double f2 = fc[(r + 2) * T];
@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 
             if (rk_un) v = ca * __ldg(pn + k * NN + r * N) + cb * v;
             out[r][k] = v;
             if (store_mask && r == CPT - 1 && cj0 + r == T - 1 && y_hi && (store_mask & 8))
-                a.freg[(((size_t)leaf * 4 + kN) * 4 + k) * N + tx * T + ci] = Fhi;
+                a.freg[(((size_t)d.slot * 4 + kN) * 4 + k) * N + tx * T + ci] = Fhi;
             Flo = Fhi;
             f0 = f1;
             f1 = f2;
@@ -854,7 +854,7 @@ __global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, 
         const int fleaf = rt.fine[s][fl];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            double Fc = a.freg[(((size_t)rt.leaf * 4 + s) * 4 + k) * n + along];
+            double Fc = a.freg[(((size_t)rt.slot * 4 + s) * 4 + k) * n + along];
             const double* ff = a.freg + (((size_t)fleaf * 4 + opp) * 4 + k) * n + fp;
             double delta = Fc - 0.5 * (ff[0] + ff[1]);
             u[k] += coef * sigma * delta * ih;
@@ -1037,21 +1037,21 @@ cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int n, cudaStream_t s) {
+cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int per, cudaStream_t s) {
     if (npatch <= 0) return cudaSuccess;
-    long long total = (long long)npatch * 4 * n * n;
+    long long total = (long long)npatch * per;
     unsigned blocks = grid_for(total, 256);
     if (blocks > 148u * 64u) blocks = 148u * 64u;
-    scatter_kernel<<<blocks, 256, 0, s>>>(packed, slots, total, 4 * n * n, U, 1);
+    scatter_kernel<<<blocks, 256, 0, s>>>(packed, slots, total, per, U, 1);
     return cudaGetLastError();
 }
 
-cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int n, cudaStream_t s) {
+cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int per, cudaStream_t s) {
     if (npatch <= 0) return cudaSuccess;
-    long long total = (long long)npatch * 4 * n * n;
+    long long total = (long long)npatch * per;
     unsigned blocks = grid_for(total, 256);
     if (blocks > 148u * 64u) blocks = 148u * 64u;
-    scatter_kernel<<<blocks, 256, 0, s>>>(packed, slots, total, 4 * n * n, const_cast<double*>(U), 0);
+    scatter_kernel<<<blocks, 256, 0, s>>>(packed, slots, total, per, const_cast<double*>(U), 0);
     return cudaGetLastError();
 }
 

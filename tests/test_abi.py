@@ -18,8 +18,8 @@ def lib():
     return amr.load()
 
 
-def declared_symbols():
-    txt = open(os.path.join(ROOT, "include", "amr.h")).read()
+def declared_symbols(header="amr.h"):
+    txt = open(os.path.join(ROOT, "include", header)).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(amr_[a-z_0-9]+)\s*\(", txt)))
 
@@ -28,8 +28,11 @@ def test_header_and_binding_agree():
     assert declared_symbols() == sorted(amr.ABI_SYMBOLS)
 
 
-def test_library_exports_every_declared_symbol(lib):
-    for s in declared_symbols():
+@pytest.mark.parametrize("header", ["amr.h", "amr_debug.h"])
+def test_library_exports_every_declared_symbol(lib, header):
+    syms = declared_symbols(header)
+    assert syms
+    for s in syms:
         assert hasattr(lib, s), s
 
 

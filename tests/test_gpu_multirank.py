@@ -1,0 +1,96 @@
+"""Multi-rank data path on ONE GPU: W virtual ranks (host threads, comm_backend = in-process loopback) run the
+same mesh as one rank; the final states must be BITWISE identical (SURVEY.md s8(e) rank invariance) and
+agree with the oracle.  This exercises ownership, halo / flux-register / coarse-source exchanges, the
+Lambda and flag collectives and patch migration at regrid with the real kernels; only the transport (NCCL vs
+device-to-device copies) differs from the one-process-per-GPU path.  The virtual ranks never spin on each
+other: every cross-rank dependency is a CUDA event between their streams."""
+import threading
+import uuid
+
+import numpy as np
+import pytest
+
+import paper_2508_05020_b200 as amr
+import workloads as W
+from tests.parity import parity_error
+
+pytestmark = pytest.mark.gpu
+
+
+def run_single(cfg, steps, regrid_every):
+    g = amr.Mesh(cfg)
+    fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+    g.set_state(fn)
+    for _ in range(cfg["levels"] - 1):
+        g.regrid()
+        g.set_state(fn)
+    dts = []
+    for s in range(1, steps + 1):
+        dts.append(g.step(cfl=cfg.get("cfl", 0.5)))
+        if regrid_every and s % regrid_every == 0:
+            g.regrid()
+    return g.get_state(), g.keys(), dts
+
+
+def run_multi(cfg, world, steps, regrid_every):
+    key = uuid.uuid4().hex[:16]
+    out = [None] * world
+    err = []
+
+    def worker(r):
+        try:
+            import torch
+            torch.cuda.set_device(0)
+            g = amr.Mesh(cfg, world_size=world, rank=r, comm_backend=1, comm_id=key)
+            fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+            g.set_state(fn)
+            for _ in range(cfg["levels"] - 1):
+                g.regrid()
+                g.set_state(fn)
+            dts = []
+            for s in range(1, steps + 1):
+                dts.append(g.step(cfl=cfg.get("cfl", 0.5)))
+                if regrid_every and s % regrid_every == 0:
+                    g.regrid()
+            tree = g.tree()
+            st = g.get_state()
+            owned = {(d.level, d.i, d.j) for d in tree if d.owner == r}
+            out[r] = ({k: v for k, v in st.items() if k in owned}, g.keys(), dts,
+                      {d.owner for d in tree}, g.stats())
+            g.close()
+        except Exception as e:   # surfaced below
+            err.append((r, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not err, err
+    return out
+
+
+CASES = {
+    "uniform_periodic_c4": (W.sweep(N=128, n=16, scheme="central4", seed=3, ic="smooth"), 4, None),
+    "quadrant_amr_weno": (W.quadrant(N=64, n=16, levels=3, seed=2), 8, 4),
+    "shock_bubble_reflective": (W.shock_bubble(Nx=128, Ny=64, n=16, levels=3), 8, 4),
+}
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", list(CASES))
+def test_virtual_ranks_bitwise_equal_single_rank(case, world):
+    cfg, steps, regrid = CASES[case]
+    ref_state, ref_keys, ref_dts = run_single(cfg, steps, regrid)
+    res = run_multi(cfg, world, steps, regrid)
+    merged = {}
+    for r, (st, keys, dts, owners, stats) in enumerate(res):
+        assert keys == ref_keys, f"rank {r}: tree differs"
+        assert dts == ref_dts, f"rank {r}: dt sequence differs"
+        assert owners == set(range(world)), f"rank {r}: not every rank owns patches"
+        merged.update(st)
+    assert set(merged) == set(ref_state)
+    for k, U in ref_state.items():
+        assert np.array_equal(U, merged[k]), (case, world, k)
+    e, _ = parity_error(ref_state, merged)
+    assert e == 0.0
