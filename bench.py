@@ -2,15 +2,18 @@
 """Benchmark of the B200 AMR compressible-Euler hot path (BASELINE.json metric:
 "Euler cell-updates/sec per RK stage at 1/2/4/8 B200; achieved HBM GB/s vs peak").
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload sweep|vortex|quadrant]
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload sweep|vortex]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
-Default workload: BASELINE.json configs[4] (uniform-patch throughput sweep) at 4096^2 cells per GPU
-(weak scaling, D5w), 32^2 patches, periodic, per-cell noise states from SplitMix64 seed 7, Central4
-(Eq. 8/9) with SSP-RK3; dt fixed from step 0 (CFL 0.3).  A step = one full SSP-RK3 step (3 fused stage
-launches plus the step's dt/Lambda work).  Before every timed step U^n is restored from a pristine copy
-(a 537 MB device-to-device write that also flushes the 126 MB L2; outside the timed intervals), so every
-timed step starts from the same positive state.  One JSON line is printed by rank 0.
-Multi-GPU (torchrun): each rank owns a 4096^2 slab of a periodic (4096 N) x 4096 domain... see DESIGN.md s6.
+Headline workload: BASELINE.json configs[4] (uniform-patch throughput sweep) at 4096^2 cells PER GPU (weak
+scaling: a 4096 x 4096N periodic domain, rank r owning one 4096^2 square through the Morton
+root partition), 32^2 patches, per-cell noise states from SplitMix64 seed 7, Central4 (Eq. 8/9) + SSP-RK3,
+dt fixed from step 0 (CFL 0.3).  A step = one full SSP-RK3 step through amr_steps (3 fused stage launches,
+the dt/Lambda work and, for N > 1, 3 halo exchanges and the Lambda allreduce over NCCL).  Before every
+timed step U^n is restored from a pristine device copy (537 MB per GPU, untimed; it also flushes the 126 MB
+L2), so every timed step starts from the same positive state.  Rank 0 prints one JSON line with the
+WENO5-characteristic stage throughput and the 3-level quadrant AMR step (BASELINE configs[2], regrid every
+4 steps) as extra keys.
 """
 from __future__ import annotations
 
@@ -30,13 +33,24 @@ import numpy as np  # noqa: E402
 
 import workloads as W  # noqa: E402
 
+BYTES_PER_CELL_STAGE = (64.0 + 96.0 + 96.0) / 3.0   # U^n (+U^(s-1)) read, U^(s) written, fp64
+
 
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("hbm_gbs", 6650.0), "measured"
-    return 6650.0, "fallback"
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def fp64_peak():
+    """Sustained DFMA TFLOP/s measured by scripts/dfma_peak on this pool (profiles/dfma_peak.json), else the
+    guide's unit-count estimate 148 SM x 64 DFMA/clk x 2 flops x 1.965 GHz."""
+    p = os.path.join(ROOT, "profiles", "dfma_peak.json")
+    if os.path.exists(p):
+        return json.load(open(p))["fp64_dfma_tflops"], "measured (profiles/dfma_peak.json)"
+    return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SM x 64 DFMA/clk x 2 x 1.965 GHz)"
 
 
 class Clocks:
@@ -61,7 +75,7 @@ class Clocks:
                     self.samples.append(f)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -82,69 +96,24 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def workload(args, world):
-    if args.workload == "sweep":
-        # D5w: 4096^2 cells per GPU, slabs stacked in y (weak scaling)
-        cfg = W.sweep(N=args.N, n=args.n, scheme=args.scheme, Ny=args.N * world, seed=7)
-        cfg["characteristic"] = args.characteristic
-        cfg["check_positivity"] = 0
-        name = (f"BASELINE configs[4] uniform-patch sweep, {args.N}x{args.N * world} cells "
-                f"({args.N}^2 per GPU), {args.n}^2 patches, periodic, noise seed 7")
-    elif args.workload == "vortex":
-        cfg = W.vortex(N=1024, n=32)
-        name = "BASELINE configs[1] isentropic vortex 1024^2, 32^2 patches"
-    else:
-        raise SystemExit(f"unknown workload {args.workload}")
+def sweep_cfg(args, world, scheme, characteristic=1):
+    cfg = W.sweep(N=args.N, n=args.n, scheme=scheme, Ny=args.N * world, seed=7)
+    cfg["characteristic"] = characteristic
+    cfg["check_positivity"] = 0
+    name = (f"BASELINE configs[4] uniform-patch sweep: {args.N}x{args.N * world} cells ({args.N}^2 per GPU, "
+            f"D5w weak scaling), {args.n}^2 patches, periodic, noise seed 7")
     return cfg, name
 
 
-def algorithmic_bytes_per_cell_stage():
-    # stage 1 reads U^n (32 B) + writes 32 B; stages 2-3 read U^(s-1), U^n, write: 96 B
-    return (64.0 + 96.0 + 96.0) / 3.0
-
-
-def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, on a bounded sample of the same workload."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+# --------------------------------------------------------------------------------------- reference arm
+def oracle_rate(cfg, cfl, seconds, max_steps=50, size=256):
+    """The CPU oracle as it stands on a size^2 periodic piece of the same field (same per-cell work)."""
     import oracle as orc
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    cfg, name = workload(args, 1)
-    # bounded sample: a 256^2 periodic piece of the same noise field (same per-cell work), K steps
-    sub = dict(cfg, base=(256, 256), hi=(256 / 4096.0, 256 / 4096.0))
+    sub = dict(cfg, base=(size, size), hi=(size / 4096.0, size / 4096.0))
     o = orc.Oracle(sub)
     U0 = W.level0_state(sub)
     o.set_state(lambda l, P, Q: U0[Q, P])
-    lam = o.lam()
-    dt = args.cfl / lam
-    t0 = time.perf_counter()
-    steps = max(1, min(args.steps, 3))
-    for _ in range(steps):
-        o.set_state(lambda l, P, Q: U0[Q, P])
-        try:
-            o.step(dt=dt)
-        except Exception:
-            pass
-    el = time.perf_counter() - t0
-    v = 256 * 256 * 3 * steps / el
-    line = {"impl": "reference", "metric": "Euler cell-updates/sec per RK stage", "value": v,
-            "unit": "cell-updates/s", "n_gpus": world, "steps": steps, "warmup": 0, "ms_per_step": el / steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": name, "scheme": args.scheme},
-            "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
-                             "sample": f"256^2 periodic piece of the same noise field, {steps} SSP-RK3 steps"},
-            "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def cpu_baseline(args, cfg):
-    import oracle as orc
-    sub = dict(cfg, base=(256, 256), hi=(256 / 4096.0, 256 / 4096.0))
-    o = orc.Oracle(sub)
-    U0 = W.level0_state(sub)
-    o.set_state(lambda l, P, Q: U0[Q, P])
-    dt = args.cfl / o.lam()
+    dt = cfl / o.lam()
     t0 = time.perf_counter()
     k = 0
     while True:
@@ -154,11 +123,191 @@ def cpu_baseline(args, cfg):
         except Exception:
             pass
         k += 1
-        if time.perf_counter() - t0 > args.cpu_seconds or k >= 50:
+        if time.perf_counter() - t0 > seconds or k >= max_steps:
             break
     el = time.perf_counter() - t0
-    return {"value": 256 * 256 * 3 * k / el, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
-            "sample": f"256^2 periodic piece of the same noise field, {k} SSP-RK3 steps, single thread"}
+    return size * size * 3 * k / el, k, el
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, timed on the host cores, on the same workload's per-cell work."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg, name = sweep_cfg(args, 1, args.scheme)
+    v, k, el = oracle_rate(cfg, args.cfl, seconds=max(5.0, 4.0 * args.steps), max_steps=max(3, 3 * args.steps))
+    sample = f"256^2 periodic piece of the same noise field, {k} SSP-RK3 steps, single thread"
+    line = {"impl": "reference", "metric": "Euler cell-updates/sec per RK stage", "value": v,
+            "unit": "cell-updates/s", "n_gpus": world, "steps": k, "warmup": 0, "ms_per_step": el / k * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "scheme": args.scheme},
+            "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------- our arm
+class Ctx:
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        from paper_2508_05020_b200 import build as B
+        if self.rank == 0:
+            B.build()
+        self.barrier()
+        import paper_2508_05020_b200 as amr
+        self.amr = amr
+        self.stream = torch.cuda.Stream()   # the library launches here; CUDA events are recorded here
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], device="cuda", dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([float(x)], device="cuda", dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def mesh(self, cfg):
+        kw = {}
+        if self.world > 1:
+            ids = [self.amr.nccl_unique_id() if self.rank == 0 else None]
+            self.dist.broadcast_object_list(ids, src=0)
+            kw = dict(world_size=self.world, rank=self.rank, comm_backend=0, comm_id=ids[0])
+        return self.amr.Mesh(cfg, stream=self.stream, **kw)
+
+
+def measure_sweep(X, args, cfg, steps, warmup, do_e2e):
+    torch = X.torch
+    mesh = X.mesh(cfg)
+    n = cfg["n"]
+    npx = cfg["base"][0] // n
+    own = mesh.owned()
+    q0, q1 = int(own[0]) // npx, int(own[-1]) // npx + 1
+    assert np.array_equal(own, np.arange(q0 * npx, q1 * npx)), "expected one slab of patch rows per rank"
+    U0 = W.level0_state(cfg, rows=(q0, q1)).reshape(-1, 4, n, n)
+    mesh.set_state(U=U0, indices=own)
+    _, lam = mesh.diagnostics()
+    dt = args.cfl / lam
+    U0d = torch.from_numpy(U0).cuda()
+    pinned = torch.from_numpy(U0).pin_memory()
+    torch.cuda.synchronize()
+
+    def restore():   # untimed: pristine device copy -> U^n (537 MB / GPU; also flushes the L2)
+        mesh.set_state_device(U0d, indices=own)
+
+    for _ in range(warmup):
+        restore()
+        mesh.steps(1, dt=dt)
+    torch.cuda.synchronize()
+    mesh.reset_stats()
+    mesh.set_kernel_timing(True)
+    times = []
+    X.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with Clocks(X.local) as clk:
+        for _ in range(steps):
+            restore()
+            X.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(X.stream)
+            mesh.steps(1, dt=dt)
+            e1.record(X.stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    X.barrier()
+    wall = time.perf_counter() - wall0
+    st = mesh.stats()
+    mesh.set_kernel_timing(False)
+    ms = X.max_over_ranks(sum(times))
+    cells = X.sum_over_ranks(st["leaf_cells"])
+    value = cells * 3 * steps / (ms / 1e3)
+    stage_avg_ms = st["stage_ms"] / max(1, st["stage_timed"])
+    bytes_per_launch = st["stage_bytes"] / max(1, st["stage_timed"])
+    achieved = bytes_per_launch / (stage_avg_ms / 1e3) / 1e9
+    res = {"value": value, "ms_per_step": ms / steps, "wall_s": wall, "stats": st, "clocks": clk.summary(),
+           "stage_share": st["stage_ms"] / sum(times) if times else None, "achieved_gbs": achieved,
+           "stage_avg_ms": stage_avg_ms, "cells_per_launch": st["stage_cells"] / max(1, st["stage_timed"]),
+           "gpu_launches": st["launches"]}
+    if do_e2e:
+        # end to end through the public API with host buffers: the state uploaded from pinned host memory,
+        # K steps each reading dt_used back (D2H), the final state downloaded -- all inside the timed region.
+        out = np.empty_like(U0)
+        torch.cuda.synchronize()
+        X.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(X.stream)
+        mesh.set_state(U=pinned.numpy(), indices=own)
+        for _ in range(steps):
+            mesh.step(dt=dt, want_dt=True)
+        out[:] = mesh.get_state(as_dict=False, indices=own)
+        e1.record(X.stream)
+        e1.synchronize()
+        ems = X.max_over_ranks(e0.elapsed_time(e1))
+        sb = U0.nbytes
+        res["e2e"] = {"value": cells * 3 * steps / (ems / 1e3), "unit": "cell-updates/s",
+                      "h2d_bytes_per_step": sb / steps, "d2h_bytes_per_step": sb / steps + 8,
+                      "includes": "amr_set_state from pinned host, K x amr_step(dt, &dt_used), amr_get_state"}
+    mesh.close()
+    return res
+
+
+def measure_quadrant(X, args):
+    """BASELINE configs[2]: quadrant Riemann problem, 512^2 base, 3 levels, WENO5-char, regrid every 4 steps.
+    Timed: K steps including the regrids (flags, Alg. 1/2, prolongation, migration) inside the region."""
+    torch = X.torch
+    cfg = W.quadrant(N=512, n=16, levels=3, seed=1)
+    mesh = X.mesh(cfg)
+    fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+    mesh.set_state(fn)
+    for _ in range(cfg["levels"] - 1):
+        mesh.regrid()
+        mesh.set_state(fn)
+    for s in range(2):
+        mesh.step(cfl=0.5)
+    torch.cuda.synchronize()
+    X.barrier()
+    steps = 8
+    leaf_cells = 0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(X.stream)
+    for s in range(1, steps + 1):
+        leaf_cells += mesh.stats()["leaf_cells"]
+        mesh.step(cfl=0.5, want_dt=False)
+        if s % 4 == 0:
+            mesh.regrid()
+    e1.record(X.stream)
+    e1.synchronize()
+    ms = X.max_over_ranks(e0.elapsed_time(e1))
+    cells = X.sum_over_ranks(leaf_cells)
+    st = mesh.stats()
+    mesh.close()
+    return {"value": cells * 3 / (ms / 1e3), "ms_per_step": ms / steps, "leaves": st["leaves"],
+            "patches": st["patches"], "leaf_cells_last": st["leaf_cells"],
+            "workload": "BASELINE configs[2] quadrant AMR, 512^2 base, 3 levels, 16^2 patches, WENO5-char, "
+                        "8 CFL-0.5 steps with 2 regrids inside the timed region"}
 
 
 def main():
@@ -167,160 +316,70 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "vortex"])
     ap.add_argument("--scheme", default="central4", choices=["central4", "weno5"])
     ap.add_argument("--characteristic", type=int, default=1)
     ap.add_argument("--N", type=int, default=4096)
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--cfl", type=float, default=0.3)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weno", action="store_true")
+    ap.add_argument("--no-amr", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
-    import torch
-    import torch.distributed as dist
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    from paper_2508_05020_b200 import build as B
-    if rank == 0:
-        B.build()
-    if world > 1:
-        dist.barrier()
-    import paper_2508_05020_b200 as amr
-
-    cfg, name = workload(args, world)
-    stream = torch.cuda.Stream()   # the library launches on this stream; CUDA events are recorded on it
-    hbm_peak, peak_kind = peaks()
-
-    def measure(scheme, characteristic, steps, warmup, do_e2e):
-        c = dict(cfg, scheme=scheme, characteristic=characteristic)
-        mesh = amr.Mesh(c, stream=stream, **({} if world == 1 else {}))
-        n = c["n"]
-        U0h = W.level0_state(c).reshape(-1, 4, n, n)
-        npatch = U0h.shape[0]
-        mesh.set_state(U=U0h)
-        pristine = mesh.get_state(as_dict=False)
-        # device copy of the pristine state for restores between timed steps
-        idx = np.arange(npatch, dtype=np.int32)
-        _, lam = mesh.diagnostics()
-        dt = args.cfl / lam
-        U0d = torch.from_numpy(pristine).cuda()
-        host_pinned = torch.from_numpy(pristine).pin_memory()
-        torch.cuda.synchronize()
-
-        def restore():
-            # untimed: pristine device copy -> U^n (537 MB device-to-device; also flushes the 126 MB L2)
-            mesh.set_state_device(U0d)
-
-        for _ in range(warmup):
-            restore()
-            mesh.step(dt=dt, want_dt=False)
-        torch.cuda.synchronize()
-        mesh.reset_stats()
-        mesh.set_kernel_timing(True)
-        times = []
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        wall0 = time.perf_counter()
-        with Clocks(local) as clk:
-            for _ in range(steps):
-                restore()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                mesh.steps(1, dt=dt)
-                e1.record(stream)
-                e1.synchronize()
-                times.append(e0.elapsed_time(e1))
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - wall0
-        if world > 1:
-            dist.barrier()
-        st = mesh.stats()
-        mesh.set_kernel_timing(False)
-        ms = sum(times)
-        if world > 1:
-            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        cells = st["leaf_cells"] * world
-        value = cells * 3 * steps / (ms / 1e3)
-        # roofline of the dominant kernel (the fused stage kernel), CUDA events on the launch stream
-        stage_avg_ms = st["stage_ms"] / max(1, st["stage_timed"])
-        bytes_per_launch = st["stage_bytes"] / max(1, st["stage_timed"])
-        achieved = bytes_per_launch / (stage_avg_ms / 1e3) / 1e9
-        res = {"value": value, "ms_per_step": ms / steps, "wall_s": wall, "stats": st, "clocks": clk.summary(),
-               "stage_share": st["stage_ms"] / ms if ms > 0 else None,
-               "roofline": {"bound": "hbm" if scheme == "central4" else "alu", "achieved": achieved,
-                            "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
-                            "peak_kind": peak_kind,
-                            "kernel": "stage_kernel (fused reconstruction+flux+divergence+RK)",
-                            "algorithmic_bytes_per_cell_stage": algorithmic_bytes_per_cell_stage(),
-                            "avg_launch_ms": stage_avg_ms},
-               "gpu_launches": st["launches"]}
-        if do_e2e:
-            # end to end through the public API with host buffers: upload the state from pinned host memory,
-            # K steps each reading dt_used back (D2H), download the final state -- all inside the timed region.
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            out = np.empty_like(pristine)
-            e0.record(stream)
-            mesh.set_state(U=host_pinned.numpy())
-            for _ in range(steps):
-                mesh.step(dt=dt, want_dt=True)
-            mesh.L.amr_get_state(mesh.h, npatch, idx.ctypes.data_as(amr._I32), out.ctypes.data_as(amr._D))
-            e1.record(stream)
-            e1.synchronize()
-            ems = e0.elapsed_time(e1)
-            if world > 1:
-                t = torch.tensor([ems], device="cuda", dtype=torch.float64)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ems = float(t.item())
-            sb = pristine.nbytes
-            res["e2e"] = {"value": cells * 3 * steps / (ems / 1e3), "unit": "cell-updates/s",
-                          "h2d_bytes_per_step": sb / steps, "d2h_bytes_per_step": sb / steps + 8}
-        mesh.close()
-        del U0d
-        return res
-
-    main_res = measure(args.scheme, args.characteristic, args.steps, args.warmup, True)
+    X = Ctx()
+    hbm_peak, hbm_kind = peaks()
+    cfg, name = sweep_cfg(args, X.world, args.scheme, args.characteristic)
+    main_res = measure_sweep(X, args, cfg, args.steps, args.warmup, True)
     extra = {}
     if not args.no_weno and args.scheme == "central4":
-        wr = measure("weno5", 1, max(3, args.steps // 2), 2, False)
-        extra["weno5_char"] = {"value": wr["value"], "ms_per_step": wr["ms_per_step"], "roofline": wr["roofline"],
-                               "positivity": "not held (noise input; see DESIGN.md s6)"}
-    if rank == 0:
+        wcfg, _ = sweep_cfg(args, X.world, "weno5", 1)
+        wr = measure_sweep(X, args, wcfg, max(3, args.steps // 2), 2, False)
+        fpk, fpk_kind = fp64_peak()
+        extra["weno5_char"] = {
+            "value": wr["value"], "unit": "cell-updates/s", "ms_per_step": wr["ms_per_step"],
+            "roofline": {"bound": "alu", "achieved_hbm_gbs": wr["achieved_gbs"], "hbm_frac": wr["achieved_gbs"] / hbm_peak,
+                         "stage_avg_ms": wr["stage_avg_ms"], "fp64_peak_tflops": fpk, "fp64_peak_kind": fpk_kind,
+                         "note": "fp64 pipe utilisation from ncu in profiles/; DESIGN.md s5"},
+            "positivity": "not held: WENO5-char reconstruction of white noise yields a few non-physical face "
+                          "states (DESIGN.md s6); throughput config only"}
+    if not args.no_amr:
+        extra["quadrant_amr"] = measure_quadrant(X, args)
+    if X.rank == 0:
+        rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
+              "frac": main_res["achieved_gbs"] / hbm_peak, "traffic": None, "peak_kind": hbm_kind,
+              "kernel": "stage_c4_kernel (fused halo gather + cons->prim + Central4 flux + Eq. 9 divergence + "
+                        "SSP-RK3 update)",
+              "algorithmic_bytes_per_cell_stage": BYTES_PER_CELL_STAGE,
+              "cells_per_launch": main_res["cells_per_launch"], "avg_launch_ms": main_res["stage_avg_ms"]}
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            t = json.load(open(tf))
+            rf["traffic"] = t.get("central4_bytes_per_launch")
+            rf["traffic_note"] = t.get("note")
         line = {"metric": "Euler cell-updates/sec per RK stage", "value": main_res["value"], "unit": "cell-updates/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
+                "n_gpus": X.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
+                "data": "synthetic (SplitMix64 noise, BASELINE configs[4] distributions)",
                 "config": {"workload": name, "scheme": args.scheme, "patch": args.n, "cfl_fixed_dt": args.cfl,
-                           "parallelism": f"patch-partition x{world}" if world > 1 else "single GPU",
-                           "l2": "inputs (3 x 537 MB buffers) larger than L2; U^n restored from a pristine copy "
-                                 "between timed steps (untimed, also flushes L2)",
-                           "positivity": "held for every timed step (check disabled in the timed region)"},
-                "roofline": main_res["roofline"], "e2e": main_res.get("e2e"),
-                "clocks": main_res["clocks"], "gpu_launches": main_res["gpu_launches"],
-                "stage_kernel_share": main_res["stage_share"]}
+                           "parallelism": f"Morton root partition x{X.world}, NCCL halo exchange" if X.world > 1
+                           else "single GPU",
+                           "l2": "inputs larger than L2 (3 x 537 MB buffers per GPU); U^n restored from a pristine "
+                                 "device copy between timed steps (untimed; also flushes L2)",
+                           "positivity": "held for every timed step (each starts from the pristine state)"},
+                "roofline": rf, "e2e": main_res["e2e"], "clocks": main_res["clocks"],
+                "gpu_launches": main_res["gpu_launches"], "stage_kernel_share": main_res["stage_share"]}
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args, cfg)
+            v, k, el = oracle_rate(cfg, args.cfl, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+                                    "sample": f"256^2 periodic piece of the same noise field, {k} SSP-RK3 steps "
+                                              f"({el:.1f} s), single thread"}
         line.update(extra)
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if X.world > 1:
+        X.dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -225,41 +225,48 @@ class Mesh:
         return [(d.level, d.i, d.j) for d in self.tree() if d.leaf]
 
     # ---- state
-    def set_state(self, fn=None, U=None):
-        """Set every patch from fn(l, P, Q) -> U[4][n][n], or from U[npatch][4][n][n] in tree order."""
+    def owned(self):
+        """Tree indices of the patches this rank owns (all of them on one rank)."""
+        return np.array([e for e, d in enumerate(self.tree()) if d.owner == self.rank], np.int32)
+
+    def set_state(self, fn=None, U=None, indices=None):
+        """Set patches from fn(l, P, Q) -> U[4][n][n] (only the patches this rank owns are evaluated), or from
+        U[k][4][n][n] for tree indices `indices` (default: every patch, tree order)."""
         tr = self.tree()
-        m = len(tr)
         if U is None:
-            U = np.empty((m, 4, self.n, self.n))
-            for e, d in enumerate(tr):
+            indices = self.owned() if indices is None else np.asarray(indices, np.int32)
+            U = np.empty((len(indices), 4, self.n, self.n))
+            for e, ti in enumerate(indices):
+                d = tr[ti]
                 U[e] = fn(d.level, d.i, d.j)
+        if indices is None:
+            indices = np.arange(len(tr), dtype=np.int32)
+        idx = np.ascontiguousarray(indices, dtype=np.int32)
         U = np.ascontiguousarray(U, dtype=np.float64)
-        idx = np.arange(m, dtype=np.int32)
-        self._chk(self.L.amr_set_state(self.h, m, idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
+        assert U.shape[0] == len(idx)
+        self._chk(self.L.amr_set_state(self.h, len(idx), idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
 
-    def set_state_device(self, tensor):
-        """Set every patch (tree order) from a contiguous CUDA float64 tensor [npatch][4][n][n]."""
-        m = len(self.tree())
+    def set_state_device(self, tensor, indices=None):
+        """Set patches (default: every patch, tree order) from a contiguous CUDA float64 tensor [k][4][n][n]."""
+        idx = np.arange(len(self.tree()), dtype=np.int32) if indices is None else np.asarray(indices, np.int32)
         assert tensor.is_cuda and tensor.dtype.is_floating_point and tensor.is_contiguous()
-        assert tensor.numel() == m * 4 * self.n * self.n
-        idx = np.arange(m, dtype=np.int32)
-        self._chk(self.L.amr_set_state_device(self.h, m, idx.ctypes.data_as(_I32), tensor.data_ptr()))
+        assert tensor.numel() == len(idx) * 4 * self.n * self.n
+        self._chk(self.L.amr_set_state_device(self.h, len(idx), idx.ctypes.data_as(_I32), tensor.data_ptr()))
 
-    def get_state_device(self, tensor):
-        m = len(self.tree())
-        assert tensor.is_cuda and tensor.is_contiguous() and tensor.numel() == m * 4 * self.n * self.n
-        idx = np.arange(m, dtype=np.int32)
-        self._chk(self.L.amr_get_state_device(self.h, m, idx.ctypes.data_as(_I32), tensor.data_ptr()))
+    def get_state_device(self, tensor, indices=None):
+        idx = np.arange(len(self.tree()), dtype=np.int32) if indices is None else np.asarray(indices, np.int32)
+        assert tensor.is_cuda and tensor.is_contiguous() and tensor.numel() == len(idx) * 4 * self.n * self.n
+        self._chk(self.L.amr_get_state_device(self.h, len(idx), idx.ctypes.data_as(_I32), tensor.data_ptr()))
 
-    def get_state(self, as_dict=True):
+    def get_state(self, as_dict=True, indices=None):
+        """State of patches `indices` (default all; on several ranks only owned patches are filled)."""
         tr = self.tree()
-        m = len(tr)
-        U = np.empty((m, 4, self.n, self.n))
-        idx = np.arange(m, dtype=np.int32)
-        self._chk(self.L.amr_get_state(self.h, m, idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
+        idx = np.arange(len(tr), dtype=np.int32) if indices is None else np.ascontiguousarray(indices, np.int32)
+        U = np.empty((len(idx), 4, self.n, self.n))
+        self._chk(self.L.amr_get_state(self.h, len(idx), idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
         if not as_dict:
             return U
-        return {(d.level, d.i, d.j): U[e] for e, d in enumerate(tr)}
+        return {(tr[ti].level, tr[ti].i, tr[ti].j): U[e] for e, ti in enumerate(idx)}
 
     # ---- stepping
     def step(self, dt=0.0, cfl=0.0, want_dt=True):

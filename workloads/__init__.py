@@ -210,14 +210,16 @@ def patch_state(cfg, l, P, Q):
     return np.ascontiguousarray(to_conserved(rho, u, v, p, cfg.get("gamma", GAMMA)))
 
 
-def level0_state(cfg):
-    """All level-0 patches at once: array [NPy][NPx][4][n][n] (used for the big uniform sweeps)."""
+def level0_state(cfg, rows=None):
+    """Level-0 patches at once: array [NPy][NPx][4][n][n] (big uniform sweeps); rows = (Q0, Q1) restricts
+    to patch rows Q0 <= Q < Q1 (one rank's slab)."""
     n = cfg["n"]
     Nx, Ny = cfg["base"]
     dx = (cfg["hi"][0] - cfg["lo"][0]) / Nx
     dy = (cfg["hi"][1] - cfg["lo"][1]) / Ny
     I = np.arange(Nx)
-    J = np.arange(Ny)
+    J = np.arange(Ny) if rows is None else np.arange(rows[0] * n, rows[1] * n)
+    Ny = len(J)
     x = cfg["lo"][0] + (I + 0.5) * dx
     y = cfg["lo"][1] + (J + 0.5) * dy
     X, Y = np.meshgrid(x, y)
