@@ -42,7 +42,7 @@ class amr_config(C.Structure):
                 ("max_patches", C.c_int32), ("pool", C.c_void_p), ("pool_bytes", C.c_uint64),
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("world_size", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("check_positivity", C.c_int32),
-                ("use_graphs", C.c_int32), ("comm_backend", C.c_int32)]
+                ("use_graphs", C.c_int32), ("comm_backend", C.c_int32), ("stage_kernel", C.c_int32)]
 
 
 class amr_patch_desc(C.Structure):
@@ -144,6 +144,7 @@ def make_config(cfg: dict, **over) -> amr_config:
     full = sum(4 ** l for l in range(cfg["levels"]))          # every root refined to the finest level
     c.max_patches = int(cfg.get("max_patches", max(16, roots * full)))
     c.check_positivity = int(cfg.get("check_positivity", 1))
+    c.stage_kernel = int(cfg.get("stage_kernel", 0))
     c.world_size = 1
     c.rank = 0
     c.device = -1

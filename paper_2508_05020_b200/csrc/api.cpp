@@ -70,6 +70,7 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.world_size > 1 && !c.nccl_unique_id) { m = "world_size > 1 needs nccl_unique_id"; return AMR_E_CONFIG; }
     if (c.refine_threshold < 0 || c.coarsen_fraction < 0) { m = "bad thresholds"; return AMR_E_CONFIG; }
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
+    if (c.stage_kernel != 0 && c.stage_kernel != 1) { m = "stage_kernel must be 0 or 1"; return AMR_E_CONFIG; }
     return AMR_OK;
 }
 
@@ -312,6 +313,9 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
         a.eps = c->cfg.weno_eps;
         a.lambda_bits = c->d_lambda;
         a.err = c->d_err;
+        a.nslots = c->cfg.max_patches;
+        a.nproxy = (int32_t)(c->proxy.cap / c->PS);
+        a.variant = c->cfg.stage_kernel;
         a.geo = c->geo;
         int scheme = c->cfg.scheme == AMR_CENTRAL4 ? 0 : (c->cfg.weno_characteristic ? 1 : 2);
         cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -554,6 +558,7 @@ amr_status amr_default_config(amr_config* cfg) {
     cfg->rank = 0;
     cfg->check_positivity = 1;
     cfg->use_graphs = 0;
+    cfg->stage_kernel = 0;
     return AMR_OK;
 }
 

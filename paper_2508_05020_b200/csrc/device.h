@@ -90,6 +90,9 @@ struct StageArgs {
     double gamma, eps;
     unsigned long long* lambda_bits;
     int32_t* err;              // [0] flag, [1] slot, [2] stage, [3] cell
+    int32_t nslots;            // slots in each RK buffer (TMA tensor-map extent)
+    int32_t nproxy;            // proxy patches allocated (TMA tensor-map extent)
+    int32_t variant;           // amr_config.stage_kernel: 0 best, 1 one-CTA-per-tile smem gather
     Geometry geo;
 };
 

@@ -14,6 +14,8 @@
 // FMA contraction) are listed in DESIGN.md.
 #include <cmath>
 
+#include <cuda.h>
+
 #include "device.h"
 
 namespace amr {
@@ -676,10 +678,351 @@ cudaError_t launch_c4_t(const StageArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- Central4 persistent TMA-pipelined stage kernel
+// One CTA of 512 threads per SM walks the 32 x 32 tiles of the leaf list (tile t, t + grid, ...).  Each tile's
+// conserved values -- the interior box and the four 4-wide side strips of the plus-shaped halo (corners are never
+// read, A26) -- arrive by five 3D TMA box loads (cp.async.bulk.tensor, pool viewed as [slot*4 + var][j][i]) into
+// one of two landing buffers, completing on an mbarrier; the loads of tile t + grid are issued as soon as tile t's
+// landing data has been converted, so HBM streams while the CTA computes.  Per tile:
+//   cons -> (p, T, u, v) into a padded plane (row stride 41 doubles: conflict-free row-wise and column-wise);
+//   x faces (warps 0-6: lane = row, warp = 5-face segment) and y faces (warps 8-14: lane = column) concurrently,
+//   each a sliding 4-cell register window, into separate flux planes;
+//   Eq. 9 divergence + SSP-RK3 (a8) per cell (lane = column, warp = row pair), with U^(s-1) from the landing
+//   buffer and U^n prefetched into registers at the start of the tile; streaming stores; Lambda (a9) reduced
+//   once per CTA.
+struct C4Maps {
+    CUtensorMap in_int;   // stage input, box {32, 32, 4}
+    CUtensorMap in_we;    // stage input, box {4, 32, 4}
+    CUtensorMap in_sn;    // stage input, box {32, 4, 4}
+    CUtensorMap px_we;    // proxy buffer, box {4, 32, 4}
+    CUtensorMap px_sn;    // proxy buffer, box {32, 4, 4}
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(mb), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t mb) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mb)
+        : "memory");
+}
+
+constexpr int kTmaThreads = 512;
+constexpr int kTmaT = 32;                                  // tile edge
+constexpr int kTmaWP = 41;                                 // prim plane row stride (odd: conflict-free)
+constexpr int kTmaPL = (kTmaT + 2 * kGL) * kTmaWP;         // prim plane (40 rows)
+constexpr int kTmaNF = kTmaT + 3;                          // faces per row: m = -1 .. T+1
+constexpr int kLandI = 0, kLandW = 4 * kTmaT * kTmaT, kLandE = kLandW + 4 * kTmaT * kGL,
+              kLandS = kLandE + 4 * kTmaT * kGL, kLandN = kLandS + 4 * kGL * kTmaT,
+              kLandSz = kLandN + 4 * kGL * kTmaT;          // doubles per landing buffer (49152 B)
+constexpr size_t kTmaSmem = sizeof(double) * (2 * kLandSz + 4 * kTmaPL + 2 * 4 * kTmaT * kTmaNF) + 16 + 128;
+
+template <int N>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    stage_c4_tma_kernel(const StageArgs a, const __grid_constant__ C4Maps maps, const int ntiles) {
+    constexpr int T = kTmaT, G = kGL, TILES = N / T, TT = TILES * TILES;
+    constexpr int NN = N * N, PS = 4 * NN;
+    constexpr int WP = kTmaWP, PL = kTmaPL, NF = kTmaNF;
+    constexpr int R = 5;                     // faces per sliding segment; 7 segments cover the 35 faces
+    static_assert(7 * R == NF, "segments must cover the row");
+    extern __shared__ unsigned char smem_raw[];
+    double* const land = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    double* const prim = land + 2 * kLandSz;     // [4][40][41] (p, T, u, v); cell (i, j) at (j+G)*WP + i+G
+    double* const fx = prim + 4 * PL;            // [4][T][NF]  x-face fluxes, face m at m+1
+    double* const fy = fx + 4 * T * NF;          // [4][NF][T]  y-face fluxes
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(fy + 4 * NF * T);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double g = a.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
+    const double c13 = 13.0 / 12.0, c24 = 1.0 / 24.0;
+    const bool div4 = a.div_order == 4;
+    const bool rk_un = a.stage > 1;
+    const double ca = a.a, cb = a.b;
+    const double dt = *a.dt;
+
+    auto issue = [&](int t, int b) {   // one thread: arm the barrier, five box loads
+        const int leaf = TILES == 1 ? t : t / TT;
+        const int tt = TILES == 1 ? 0 : t - leaf * TT;
+        const int tx = tt % TILES, ty = tt / TILES;
+        const LeafDesc d = a.leaves[leaf];
+        const uint32_t mb = smem_u32(&mbar[b]);
+        const uint32_t dst = smem_u32(land + b * kLandSz);
+        mbar_expect_tx(mb, kLandSz * 8);
+        tma_load3(dst + kLandI * 8, &maps.in_int, tx * T, ty * T, 4 * d.slot, mb);
+        // side strips: from the own patch inside a 64^2 patch, else from the neighbour (slot or proxy)
+        const CUtensorMap* mw = &maps.in_we;
+        int i0 = tx * T - G, z = 4 * d.slot;
+        if (tx == 0) { i0 = N - G; const int s = d.side[kW]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); mw = &maps.px_we; } }
+        tma_load3(dst + kLandW * 8, mw, i0, ty * T, z, mb);
+        mw = &maps.in_we; i0 = tx * T + T; z = 4 * d.slot;
+        if (tx == TILES - 1) { i0 = 0; const int s = d.side[kE]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); mw = &maps.px_we; } }
+        tma_load3(dst + kLandE * 8, mw, i0, ty * T, z, mb);
+        const CUtensorMap* ms = &maps.in_sn;
+        int j0 = ty * T - G; z = 4 * d.slot;
+        if (ty == 0) { j0 = N - G; const int s = d.side[kS]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); ms = &maps.px_sn; } }
+        tma_load3(dst + kLandS * 8, ms, tx * T, j0, z, mb);
+        ms = &maps.in_sn; j0 = ty * T + T; z = 4 * d.slot;
+        if (ty == TILES - 1) { j0 = 0; const int s = d.side[kN]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); ms = &maps.px_sn; } }
+        tma_load3(dst + kLandN * 8, ms, tx * T, j0, z, mb);
+    };
+
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_int)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_we)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_sn)) : "memory");
+        mbar_init(smem_u32(&mbar[0]), 1);
+        mbar_init(smem_u32(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+
+    const int ci = lane, cj0 = 2 * warp;         // epilogue / interior cells: column ci, rows cj0, cj0 + 1
+    unsigned long long lam = 0ull;
+    int k = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int b = k & 1;
+        const int leaf = TILES == 1 ? t : t / TT;
+        const int tt = TILES == 1 ? 0 : t - leaf * TT;
+        const int tx = tt % TILES, ty = tt / TILES;
+        const LeafDesc d = a.leaves[leaf];
+        const int base_off = (ty * T + cj0) * N + tx * T + ci;
+        double un[2][4] = {};
+        if (rk_un) {
+            const double* pn = a.Un + (size_t)d.slot * PS + base_off;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) un[r][q] = __ldg(pn + q * NN + r * N);
+        }
+        const double* L = land + b * kLandSz;
+        mbar_wait(smem_u32(&mbar[b]), (uint32_t)((k >> 1) & 1));
+
+        // ---- (a3) cons -> (p, T, u, v): interior cells (ci, cj0 + r), then one side-strip cell per thread
+        auto c2p = [&](double r, double m, double w, double E, int o) {
+            const double ir = fast_rcp(r);
+            const double u = m * ir, v = w * ir;
+            const double p = gm1 * (E - 0.5 * (m * u + w * v));
+            prim[o] = p;
+            prim[PL + o] = p * ir;
+            prim[2 * PL + o] = u;
+            prim[3 * PL + o] = v;
+        };
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const double* s = L + kLandI + (cj0 + r) * T + ci;
+            c2p(s[0], s[T * T], s[2 * T * T], s[3 * T * T], (cj0 + r + G) * WP + ci + G);
+        }
+        {
+            const int wg = warp >> 2, e = ((warp & 3) << 5) + lane;   // 128 cells per strip
+            int off, i, j;
+            if (wg < 2) { j = e >> 2; const int c = e & 3; off = (wg == 0 ? kLandW : kLandE) + e; i = wg == 0 ? c - G : T + c; }
+            else { const int rr = e >> 5; i = e & 31; off = (wg == 2 ? kLandS : kLandN) + e; j = wg == 2 ? rr - G : T + rr; }
+            const double* s = L + off;
+            c2p(s[0], s[G * T], s[2 * G * T], s[3 * G * T], (j + G) * WP + i + G);   // strip plane = 4 x 32
+        }
+        __syncthreads();   // (A) prim ready; everyone is past the previous tile's epilogue
+        if (tid == 0 && t + (int)gridDim.x < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t + gridDim.x, b ^ 1);
+        }
+
+        // ---- (a4-a6) faces: warps 0-6 x (lane = row), warps 8-14 y (lane = column)
+        if (warp < 7) {
+            const int j = lane, m0 = warp * R - 1;
+            const double* q = prim + (j + G) * WP + G + m0;    // q[c] = cell m0 + c of row j
+            double* fo = fx + j * NF + m0 + 1;
+            double p[4], Tt[4], uu[4], vv[4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) { p[c + 1] = q[c - 2]; Tt[c + 1] = q[PL + c - 2]; uu[c + 1] = q[2 * PL + c - 2]; vv[c + 1] = q[3 * PL + c - 2]; }
+#pragma unroll
+            for (int f = 0; f < R; ++f) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; uu[c] = uu[c + 1]; vv[c] = vv[c + 1]; }
+                p[3] = q[f + 1]; Tt[3] = q[PL + f + 1]; uu[3] = q[2 * PL + f + 1]; vv[3] = q[3 * PL + f + 1];
+                double F[4];
+                c4_face(p, Tt, uu, vv, inv_gm1, F);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) fo[kk * T * NF + f] = F[kk];
+            }
+        } else if (warp >= 8 && warp < 15) {
+            const int i = lane, m0 = (warp - 8) * R - 1;
+            const double* q = prim + (m0 + G) * WP + i + G;    // q[c*WP] = cell (i, m0 + c)
+            double* fo = fy + (m0 + 1) * T + i;
+            double p[4], Tt[4], un_[4], ut[4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int o = (c - 2) * WP;
+                p[c + 1] = q[o]; Tt[c + 1] = q[PL + o]; un_[c + 1] = q[3 * PL + o]; ut[c + 1] = q[2 * PL + o];
+            }
+#pragma unroll
+            for (int f = 0; f < R; ++f) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un_[c] = un_[c + 1]; ut[c] = ut[c + 1]; }
+                const int o = (f + 1) * WP;
+                p[3] = q[o]; Tt[3] = q[PL + o]; un_[3] = q[3 * PL + o]; ut[3] = q[2 * PL + o];
+                double F[4];
+                c4_face(p, Tt, un_, ut, inv_gm1, F);
+                fo[0 * NF * T + f * T] = F[0];
+                fo[1 * NF * T + f * T] = F[2];
+                fo[2 * NF * T + f * T] = F[1];
+                fo[3 * NF * T + f * T] = F[3];
+            }
+        }
+        __syncthreads();   // (B) fluxes ready
+
+        // ---- (a7) Eq. 9 divergence, (a8) SSP-RK3, checks, Lambda (a9)
+        const int lvl = d.level;
+        const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
+        const bool x_lo = tx == 0, x_hi = tx == TILES - 1, y_lo = ty == 0, y_hi = ty == TILES - 1;
+        const int store_mask = (d.cf | (d.cf >> 4)) & 15;
+        const int coarse_mask = d.cf & 15;
+        double out[2][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double Lx[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const double* fr = fx + (q * T + cj0 + r) * NF + ci + 1;   // fr[0] = f at face ci
+                const double fl = fr[0], fh = fr[1];
+                const double Fl = div4 ? c13 * fl - c24 * (fr[-1] + fh) : fl;
+                const double Fh = div4 ? c13 * fh - c24 * (fl + fr[2]) : fh;
+                Lx[r] = -(Fh - Fl) * idx;
+                if (store_mask) {
+                    if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + cj0 + r] = Fl;
+                    if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + cj0 + r] = Fh;
+                }
+            }
+            const double* fc = fy + (q * NF + cj0 + 1) * T + ci;          // fc[r*T] = f at face cj0 + r
+            const double f_1 = fc[-T], f0 = fc[0], f1 = fc[T], f2 = fc[2 * T], f3 = fc[3 * T];
+            const double F0 = div4 ? c13 * f0 - c24 * (f_1 + f1) : f0;
+            const double F1 = div4 ? c13 * f1 - c24 * (f0 + f2) : f1;
+            const double F2 = div4 ? c13 * f2 - c24 * (f1 + f3) : f2;
+            if (store_mask) {
+                if (cj0 == 0 && y_lo && (store_mask & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + q) * N + tx * T + ci] = F0;
+                if (cj0 + 1 == T - 1 && y_hi && (store_mask & 8)) a.freg[(((size_t)d.slot * 4 + kN) * 4 + q) * N + tx * T + ci] = F2;
+            }
+            const double Ly0 = Lx[0] - (F1 - F0) * idy;
+            const double Ly1 = Lx[1] - (F2 - F1) * idy;
+            const double* uin = L + kLandI + q * T * T + cj0 * T + ci;
+            double v0 = uin[0] + dt * Ly0, v1 = uin[T] + dt * Ly1;
+            if (rk_un) { v0 = ca * un[0][q] + cb * v0; v1 = ca * un[1][q] + cb * v1; }
+            out[0][q] = v0;
+            out[1][q] = v1;
+        }
+        double* po = a.Uout + (size_t)d.slot * PS + base_off;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) __stcs(po + q * NN + r * N, out[r][q]);
+            const int j = cj0 + r;
+            const bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
+                                                 ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
+            if (!edge_cf) {
+                if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
+                    report_error(a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + ci);
+                if (a.want_lambda) {
+                    const double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                    const unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
+                    lam = bits > lam ? bits : lam;
+                }
+            }
+        }
+    }
+    if (a.want_lambda) {
+        lam = warp_max_u64(lam);
+        if (lane == 0 && lam) atomicMax(a.lambda_bits, lam);
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 3D view [z = slot*4 + var][j][i] of a pool of `npatch` n x n patches
+bool encode_pool_map(CUtensorMap* m, const double* base, int n, int npatch, int bx, int by) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || !base || npatch < 1) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)npatch * 4};
+    const cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)n * n * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 4};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n < 1) n = 1;
+    }
+    return n;
+}
+
+template <int N>
+cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(stage_c4_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kTmaSmem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int ntiles = a.nleaves * (N / kTmaT) * (N / kTmaT);
+    if (ntiles == 0) return cudaSuccess;
+    C4Maps m;
+    const double* px = a.proxy ? a.proxy : a.Uin;   // no proxies: never dereferenced, any valid map will do
+    const int npx = a.proxy && a.nproxy > 0 ? a.nproxy : a.nslots;
+    if (!encode_pool_map(&m.in_int, a.Uin, N, a.nslots, kTmaT, kTmaT) ||
+        !encode_pool_map(&m.in_we, a.Uin, N, a.nslots, kGL, kTmaT) ||
+        !encode_pool_map(&m.in_sn, a.Uin, N, a.nslots, kTmaT, kGL) ||
+        !encode_pool_map(&m.px_we, px, N, npx, kGL, kTmaT) ||
+        !encode_pool_map(&m.px_sn, px, N, npx, kTmaT, kGL))
+        return cudaErrorInvalidValue;
+    const int grid = ntiles < sm_count() ? ntiles : sm_count();
+    stage_c4_tma_kernel<N><<<grid, kTmaThreads, kTmaSmem, s>>>(a, m, ntiles);
+    return cudaGetLastError();
+}
+
 template <int SCHEME>
 cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
     int T = a.geo.n / a.tiles;
     if (SCHEME == 0) {
+        if (a.variant == 0 && a.geo.n == 32) return launch_c4_tma_t<32>(a, s);
+        if (a.variant == 0 && a.geo.n == 64) return launch_c4_tma_t<64>(a, s);
         switch (a.geo.n) {
             case 8: return launch_c4_t<8>(a, s);
             case 16: return launch_c4_t<16>(a, s);
