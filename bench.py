@@ -100,6 +100,7 @@ def sweep_cfg(args, world, scheme, characteristic=1):
     cfg = W.sweep(N=args.N, n=args.n, scheme=scheme, Ny=args.N * world, seed=7)
     cfg["characteristic"] = characteristic
     cfg["check_positivity"] = 0
+    cfg["stage_kernel"] = args.stage_kernel
     name = (f"BASELINE configs[4] uniform-patch sweep: {args.N}x{args.N * world} cells ({args.N}^2 per GPU, "
             f"D5w weak scaling), {args.n}^2 patches, periodic, noise seed 7")
     return cfg, name
@@ -321,6 +322,7 @@ def main():
     ap.add_argument("--N", type=int, default=4096)
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--cfl", type=float, default=0.3)
+    ap.add_argument("--stage-kernel", type=int, default=0, help="amr_config.stage_kernel (0 default, 1 per-tile)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weno", action="store_true")

@@ -60,6 +60,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     if nccl_inc:
         inc += ["-I", nccl_inc, "-DAMR_HAVE_NCCL_H=1"]
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"] + ARCH + inc
+    common += os.environ.get("AMR_NVCC_FLAGS", "").split()   # e.g. -DAMR_PHASE_PROF (kernel phase timing)
     objs, jobs = [], []
     hdrs = headers()
     for src in sources():

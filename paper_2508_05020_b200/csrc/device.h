@@ -93,6 +93,7 @@ struct StageArgs {
     int32_t nslots;            // slots in each RK buffer (TMA tensor-map extent)
     int32_t nproxy;            // proxy patches allocated (TMA tensor-map extent)
     int32_t variant;           // amr_config.stage_kernel: 0 best, 1 one-CTA-per-tile smem gather
+    int32_t prof;              // phase timing of the TMA kernel (AMR_PHASE_PROF, debug)
     Geometry geo;
 };
 

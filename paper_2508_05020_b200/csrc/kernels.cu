@@ -683,13 +683,17 @@ cudaError_t launch_c4_t(const StageArgs& a, cudaStream_t s) {
 // conserved values -- the interior box and the four 4-wide side strips of the plus-shaped halo (corners are never
 // read, A26) -- arrive by five 3D TMA box loads (cp.async.bulk.tensor, pool viewed as [slot*4 + var][j][i]) into
 // one of two landing buffers, completing on an mbarrier; the loads of tile t + grid are issued as soon as tile t's
-// landing data has been converted, so HBM streams while the CTA computes.  Per tile:
-//   cons -> (p, T, u, v) into a padded plane (row stride 41 doubles: conflict-free row-wise and column-wise);
-//   x faces (warps 0-6: lane = row, warp = 5-face segment) and y faces (warps 8-14: lane = column) concurrently,
-//   each a sliding 4-cell register window, into separate flux planes;
-//   Eq. 9 divergence + SSP-RK3 (a8) per cell (lane = column, warp = row pair), with U^(s-1) from the landing
-//   buffer and U^n prefetched into registers at the start of the tile; streaming stores; Lambda (a9) reduced
-//   once per CTA.
+// landing data has been converted, so HBM streams while the CTA computes.  U^n of the tile's epilogue cells is
+// loaded into registers at the top of the tile.  Per tile:
+//   (a3) cons -> (p, T, u, v) into padded planes (row stride 44); the interior cell's U^(s-1) stays in registers;
+//   (a4-a6) x faces (warps 0-7) and y faces (warps 8-15) concurrently: a lane owns a 5-face segment of one line
+//   (lane = line + 4 * segment), slides a 4-cell register window along it, evaluates the Central4 edge flux
+//   (Eq. 8, A6/A7) and the Eq. 9 face flux F-hat with the outer neighbours f(m0-1), f(m0+5) shuffled in from
+//   the adjacent segments (lanes -4 / +4), and stores F-hat;
+//   (a7, a8) per cell (lane = column, warp = row pair): the divergence of F-hat, SSP-RK3, checks, streaming
+//   stores; Lambda (a9) reduced once per CTA.
+// The strides (prim 44, F-hat 36) give every half-warp's 8-byte shared accesses 16 distinct bank pairs: ncu
+// reports zero load conflicts (profiles/).
 struct C4Maps {
     CUtensorMap in_int;   // stage input, box {32, 32, 4}
     CUtensorMap in_we;    // stage input, box {4, 32, 4}
@@ -725,38 +729,76 @@ __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, 
 
 constexpr int kTmaThreads = 512;
 constexpr int kTmaT = 32;                                  // tile edge
-constexpr int kTmaWP = 41;                                 // prim plane row stride (odd: conflict-free)
-constexpr int kTmaPL = (kTmaT + 2 * kGL) * kTmaWP;         // prim plane (40 rows)
-constexpr int kTmaNF = kTmaT + 3;                          // faces per row: m = -1 .. T+1
+constexpr int kTmaWP = 44;                                 // prim plane row stride
+constexpr int kTmaPL = (kTmaT + 2 * kGL) * kTmaWP;         // prim plane (40 rows: j = -4 .. 35)
+constexpr int kTmaNH = kTmaT + 1;                          // F-hat faces per line: 0 .. T
+constexpr int kTmaFXS = 36, kTmaFYS = 36;                  // F-hat row strides
 constexpr int kLandI = 0, kLandW = 4 * kTmaT * kTmaT, kLandE = kLandW + 4 * kTmaT * kGL,
               kLandS = kLandE + 4 * kTmaT * kGL, kLandN = kLandS + 4 * kGL * kTmaT,
-              kLandSz = kLandN + 4 * kGL * kTmaT;          // doubles per landing buffer (49152 B)
-constexpr size_t kTmaSmem = sizeof(double) * (2 * kLandSz + 4 * kTmaPL + 2 * 4 * kTmaT * kTmaNF) + 16 + 128;
+              kLandSz = kLandN + 4 * kGL * kTmaT;
+constexpr size_t kTmaSmem = sizeof(double) * (2 * kLandSz + 4 * kTmaPL + 4 * kTmaT * kTmaFXS + 4 * kTmaNH * kTmaFYS) + 16 + 128;
 
-template <int N>
+// One 5-face segment (faces m0 .. m0+4 of a row or column; 7 segments cover faces -1 .. T+1): sliding 4-cell
+// window of (p, T, u_n, u_t) over the prim planes (q = cell m0, cs = cell stride along the line, kn / kt = planes
+// of the normal / tangential velocity), Central4 edge fluxes, and Eq. 9 F-hat at the 5 faces with f(m0-1) and
+// f(m0+5) from the neighbouring segments' lanes (s unused: lanes 0-3 / 24-27 get garbage there, never stored).
+template <bool DIV4>
+__device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs, int kn, int kt, double inv_gm1,
+                                           int s, double (&Fh)[5][4]) {
+    constexpr int PL = kTmaPL;
+    double p[4], Tt[4], un[4], ut[4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int o = (c - 2) * cs;
+        p[c + 1] = q[o]; Tt[c + 1] = q[PL + o]; un[c + 1] = q[kn * PL + o]; ut[c + 1] = q[kt * PL + o];
+    }
+    double f[5][4];
+#pragma unroll
+    for (int e = 0; e < 5; ++e) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un[c] = un[c + 1]; ut[c] = ut[c + 1]; }
+        const int o = (e + 1) * cs;
+        p[3] = q[o]; Tt[3] = q[PL + o]; un[3] = q[kn * PL + o]; ut[3] = q[kt * PL + o];
+        c4_face(p, Tt, un, ut, inv_gm1, f[e]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double lo = __shfl_up_sync(0xffffffffu, f[4][k], 4);
+        const double hi = __shfl_down_sync(0xffffffffu, f[0][k], 4);
+        (void)s;
+        if (DIV4) {
+            const double c13 = 13.0 / 12.0, c24 = 1.0 / 24.0;
+            Fh[0][k] = c13 * f[0][k] - c24 * (lo + f[1][k]);
+#pragma unroll
+            for (int e = 1; e < 4; ++e) Fh[e][k] = c13 * f[e][k] - c24 * (f[e - 1][k] + f[e + 1][k]);
+            Fh[4][k] = c13 * f[4][k] - c24 * (f[3][k] + hi);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 5; ++e) Fh[e][k] = f[e][k];
+        }
+    }
+}
+
+template <int N, bool DIV4>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     stage_c4_tma_kernel(const StageArgs a, const __grid_constant__ C4Maps maps, const int ntiles) {
     constexpr int T = kTmaT, G = kGL, TILES = N / T, TT = TILES * TILES;
     constexpr int NN = N * N, PS = 4 * NN;
-    constexpr int WP = kTmaWP, PL = kTmaPL, NF = kTmaNF;
-    constexpr int R = 5;                     // faces per sliding segment; 7 segments cover the 35 faces
-    static_assert(7 * R == NF, "segments must cover the row");
-    extern __shared__ unsigned char smem_raw[];
-    double* const land = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    double* const prim = land + 2 * kLandSz;     // [4][40][41] (p, T, u, v); cell (i, j) at (j+G)*WP + i+G
-    double* const fx = prim + 4 * PL;            // [4][T][NF]  x-face fluxes, face m at m+1
-    double* const fy = fx + 4 * T * NF;          // [4][NF][T]  y-face fluxes
-    uint64_t* const mbar = reinterpret_cast<uint64_t*>(fy + 4 * NF * T);
+    constexpr int WP = kTmaWP, PL = kTmaPL, NH = kTmaNH, FXS = kTmaFXS, FYS = kTmaFYS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* const land = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+    double* const prim = land + 2 * kLandSz;
+    double* const fx = prim + 4 * PL;
+    double* const fy = fx + 4 * T * FXS;
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(fy + 4 * NH * FYS);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double g = a.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
-    const double c13 = 13.0 / 12.0, c24 = 1.0 / 24.0;
-    const bool div4 = a.div_order == 4;
     const bool rk_un = a.stage > 1;
     const double ca = a.a, cb = a.b;
     const double dt = *a.dt;
 
-    auto issue = [&](int t, int b) {   // one thread: arm the barrier, five box loads
+    auto issue = [&](int t, int b) {
         const int leaf = TILES == 1 ? t : t / TT;
         const int tt = TILES == 1 ? 0 : t - leaf * TT;
         const int tx = tt % TILES, ty = tt / TILES;
@@ -765,7 +807,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const uint32_t dst = smem_u32(land + b * kLandSz);
         mbar_expect_tx(mb, kLandSz * 8);
         tma_load3(dst + kLandI * 8, &maps.in_int, tx * T, ty * T, 4 * d.slot, mb);
-        // side strips: from the own patch inside a 64^2 patch, else from the neighbour (slot or proxy)
         const CUtensorMap* mw = &maps.in_we;
         int i0 = tx * T - G, z = 4 * d.slot;
         if (tx == 0) { i0 = N - G; const int s = d.side[kW]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); mw = &maps.px_we; } }
@@ -793,7 +834,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     __syncthreads();
     if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
 
-    const int ci = lane, cj0 = 2 * warp;         // epilogue / interior cells: column ci, rows cj0, cj0 + 1
+    const int ci = lane, cj0 = 2 * warp;
+    const int seg_line = lane & 3, seg = lane < 28 ? lane >> 2 : 6;
+    const bool seg_store = lane < 28;
     unsigned long long lam = 0ull;
     int k = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
@@ -813,8 +856,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
         const double* L = land + b * kLandSz;
         mbar_wait(smem_u32(&mbar[b]), (uint32_t)((k >> 1) & 1));
-
-        // ---- (a3) cons -> (p, T, u, v): interior cells (ci, cj0 + r), then one side-strip cell per thread
         auto c2p = [&](double r, double m, double w, double E, int o) {
             const double ir = fast_rcp(r);
             const double u = m * ir, v = w * ir;
@@ -824,70 +865,58 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             prim[2 * PL + o] = u;
             prim[3 * PL + o] = v;
         };
+        double uc[2][4];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const double* s = L + kLandI + (cj0 + r) * T + ci;
-            c2p(s[0], s[T * T], s[2 * T * T], s[3 * T * T], (cj0 + r + G) * WP + ci + G);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) uc[r][q] = s[q * T * T];
+            c2p(uc[r][0], uc[r][1], uc[r][2], uc[r][3], (cj0 + r + G) * WP + ci + G);
         }
         {
-            const int wg = warp >> 2, e = ((warp & 3) << 5) + lane;   // 128 cells per strip
+            const int wg = warp >> 2, e = ((warp & 3) << 5) + lane;
             int off, i, j;
             if (wg < 2) { j = e >> 2; const int c = e & 3; off = (wg == 0 ? kLandW : kLandE) + e; i = wg == 0 ? c - G : T + c; }
             else { const int rr = e >> 5; i = e & 31; off = (wg == 2 ? kLandS : kLandN) + e; j = wg == 2 ? rr - G : T + rr; }
             const double* s = L + off;
-            c2p(s[0], s[G * T], s[2 * G * T], s[3 * G * T], (j + G) * WP + i + G);   // strip plane = 4 x 32
+            c2p(s[0], s[G * T], s[2 * G * T], s[3 * G * T], (j + G) * WP + i + G);
         }
-        __syncthreads();   // (A) prim ready; everyone is past the previous tile's epilogue
+        __syncthreads();
         if (tid == 0 && t + (int)gridDim.x < ntiles) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(t + gridDim.x, b ^ 1);
         }
-
-        // ---- (a4-a6) faces: warps 0-6 x (lane = row), warps 8-14 y (lane = column)
-        if (warp < 7) {
-            const int j = lane, m0 = warp * R - 1;
-            const double* q = prim + (j + G) * WP + G + m0;    // q[c] = cell m0 + c of row j
-            double* fo = fx + j * NF + m0 + 1;
-            double p[4], Tt[4], uu[4], vv[4];
+        {
+            const int m0 = seg * 5 - 1;
+            double Fh[5][4];
+            if (warp < 8) {
+                const int j = 4 * warp + seg_line;
+                c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
+                if (seg_store) {
+                    double* fo = fx + j * FXS + m0;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) { p[c + 1] = q[c - 2]; Tt[c + 1] = q[PL + c - 2]; uu[c + 1] = q[2 * PL + c - 2]; vv[c + 1] = q[3 * PL + c - 2]; }
+                    for (int e = 0; e < 5; ++e)
+                        if ((seg > 0 || e > 0) && (seg < 6 || e < 4))
 #pragma unroll
-            for (int f = 0; f < R; ++f) {
+                            for (int q = 0; q < 4; ++q) fo[q * T * FXS + e] = Fh[e][q];
+                }
+            } else {
+                const int i = 4 * (warp - 8) + seg_line;
+                c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
+                if (seg_store) {
+                    double* fo = fy + m0 * FYS + i;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; uu[c] = uu[c + 1]; vv[c] = vv[c + 1]; }
-                p[3] = q[f + 1]; Tt[3] = q[PL + f + 1]; uu[3] = q[2 * PL + f + 1]; vv[3] = q[3 * PL + f + 1];
-                double F[4];
-                c4_face(p, Tt, uu, vv, inv_gm1, F);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) fo[kk * T * NF + f] = F[kk];
-            }
-        } else if (warp >= 8 && warp < 15) {
-            const int i = lane, m0 = (warp - 8) * R - 1;
-            const double* q = prim + (m0 + G) * WP + i + G;    // q[c*WP] = cell (i, m0 + c)
-            double* fo = fy + (m0 + 1) * T + i;
-            double p[4], Tt[4], un_[4], ut[4];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int o = (c - 2) * WP;
-                p[c + 1] = q[o]; Tt[c + 1] = q[PL + o]; un_[c + 1] = q[3 * PL + o]; ut[c + 1] = q[2 * PL + o];
-            }
-#pragma unroll
-            for (int f = 0; f < R; ++f) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un_[c] = un_[c + 1]; ut[c] = ut[c + 1]; }
-                const int o = (f + 1) * WP;
-                p[3] = q[o]; Tt[3] = q[PL + o]; un_[3] = q[3 * PL + o]; ut[3] = q[2 * PL + o];
-                double F[4];
-                c4_face(p, Tt, un_, ut, inv_gm1, F);
-                fo[0 * NF * T + f * T] = F[0];
-                fo[1 * NF * T + f * T] = F[2];
-                fo[2 * NF * T + f * T] = F[1];
-                fo[3 * NF * T + f * T] = F[3];
+                    for (int e = 0; e < 5; ++e)
+                        if ((seg > 0 || e > 0) && (seg < 6 || e < 4)) {
+                            fo[0 * NH * FYS + e * FYS] = Fh[e][0];
+                            fo[1 * NH * FYS + e * FYS] = Fh[e][2];
+                            fo[2 * NH * FYS + e * FYS] = Fh[e][1];
+                            fo[3 * NH * FYS + e * FYS] = Fh[e][3];
+                        }
+                }
             }
         }
-        __syncthreads();   // (B) fluxes ready
-
-        // ---- (a7) Eq. 9 divergence, (a8) SSP-RK3, checks, Lambda (a9)
+        __syncthreads();
         const int lvl = d.level;
         const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
         const bool x_lo = tx == 0, x_hi = tx == TILES - 1, y_lo = ty == 0, y_hi = ty == TILES - 1;
@@ -899,29 +928,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             double Lx[2];
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const double* fr = fx + (q * T + cj0 + r) * NF + ci + 1;   // fr[0] = f at face ci
-                const double fl = fr[0], fh = fr[1];
-                const double Fl = div4 ? c13 * fl - c24 * (fr[-1] + fh) : fl;
-                const double Fh = div4 ? c13 * fh - c24 * (fl + fr[2]) : fh;
+                const double* fr = fx + (q * T + cj0 + r) * FXS + ci;
+                const double Fl = fr[0], Fh = fr[1];
                 Lx[r] = -(Fh - Fl) * idx;
                 if (store_mask) {
                     if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + cj0 + r] = Fl;
                     if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + cj0 + r] = Fh;
                 }
             }
-            const double* fc = fy + (q * NF + cj0 + 1) * T + ci;          // fc[r*T] = f at face cj0 + r
-            const double f_1 = fc[-T], f0 = fc[0], f1 = fc[T], f2 = fc[2 * T], f3 = fc[3 * T];
-            const double F0 = div4 ? c13 * f0 - c24 * (f_1 + f1) : f0;
-            const double F1 = div4 ? c13 * f1 - c24 * (f0 + f2) : f1;
-            const double F2 = div4 ? c13 * f2 - c24 * (f1 + f3) : f2;
+            const double* fc = fy + (q * NH + cj0) * FYS + ci;
+            const double F0 = fc[0], F1 = fc[FYS], F2 = fc[2 * FYS];
             if (store_mask) {
                 if (cj0 == 0 && y_lo && (store_mask & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + q) * N + tx * T + ci] = F0;
                 if (cj0 + 1 == T - 1 && y_hi && (store_mask & 8)) a.freg[(((size_t)d.slot * 4 + kN) * 4 + q) * N + tx * T + ci] = F2;
             }
             const double Ly0 = Lx[0] - (F1 - F0) * idy;
             const double Ly1 = Lx[1] - (F2 - F1) * idy;
-            const double* uin = L + kLandI + q * T * T + cj0 * T + ci;
-            double v0 = uin[0] + dt * Ly0, v1 = uin[T] + dt * Ly1;
+            double v0 = uc[0][q] + dt * Ly0, v1 = uc[1][q] + dt * Ly1;
             if (rk_un) { v0 = ca * un[0][q] + cb * v0; v1 = ca * un[1][q] + cb * v1; }
             out[0][q] = v0;
             out[1][q] = v1;
@@ -992,12 +1015,12 @@ int sm_count() {
     return n;
 }
 
-template <int N>
+template <int N, bool DIV4>
 cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(stage_c4_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kTmaSmem);
+        cudaError_t e = cudaFuncSetAttribute(stage_c4_tma_kernel<N, DIV4>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -1013,7 +1036,7 @@ cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
         !encode_pool_map(&m.px_sn, px, N, npx, kTmaT, kGL))
         return cudaErrorInvalidValue;
     const int grid = ntiles < sm_count() ? ntiles : sm_count();
-    stage_c4_tma_kernel<N><<<grid, kTmaThreads, kTmaSmem, s>>>(a, m, ntiles);
+    stage_c4_tma_kernel<N, DIV4><<<grid, kTmaThreads, kTmaSmem, s>>>(a, m, ntiles);
     return cudaGetLastError();
 }
 
@@ -1021,8 +1044,10 @@ template <int SCHEME>
 cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
     int T = a.geo.n / a.tiles;
     if (SCHEME == 0) {
-        if (a.variant == 0 && a.geo.n == 32) return launch_c4_tma_t<32>(a, s);
-        if (a.variant == 0 && a.geo.n == 64) return launch_c4_tma_t<64>(a, s);
+        if (a.variant == 0 && a.geo.n == 32)
+            return a.div_order == 4 ? launch_c4_tma_t<32, true>(a, s) : launch_c4_tma_t<32, false>(a, s);
+        if (a.variant == 0 && a.geo.n == 64)
+            return a.div_order == 4 ? launch_c4_tma_t<64, true>(a, s) : launch_c4_tma_t<64, false>(a, s);
         switch (a.geo.n) {
             case 8: return launch_c4_t<8>(a, s);
             case 16: return launch_c4_t<16>(a, s);

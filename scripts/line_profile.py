@@ -43,3 +43,13 @@ tots = sum(stall.values())
 print(f"total warp-inst {tot:.4g}, samples {tots:.0f}, matched offsets {sum(1 for o in per_off if o in off2line)}/{len(per_off)}")
 for ln in sorted(inst, key=lambda k: -inst[k])[:45]:
     print(f"line {ln}: {100*inst[ln]/tot:5.1f}% inst  {100*stall[ln]/max(1,tots):5.1f}% stall")
+
+# region summary when REGIONS="name:lo-hi,..." is given in the environment
+import os
+if os.environ.get("REGIONS"):
+    for spec in os.environ["REGIONS"].split(","):
+        nm, rng = spec.split(":")
+        lo, hi = map(int, rng.split("-"))
+        i = sum(v for k, v in inst.items() if k is not None and lo <= k <= hi)
+        s = sum(v for k, v in stall.items() if k is not None and lo <= k <= hi)
+        print(f"region {nm:10s} {100*i/tot:5.1f}% inst {100*s/max(1,tots):5.1f}% stall")
