@@ -56,6 +56,30 @@ __device__ __forceinline__ void report_error(int32_t* err, int slot, int stage, 
     }
 }
 
+// ---------------------------------------------------------------- fast fp64 reciprocal / square root (A41)
+// Branch-free replacements for IEEE division and sqrt on the hot path (no slow-path calls): MUFU seed + Newton
+// steps, <= 1 ulp for the positive normal arguments the scheme produces (rho, c^2, p, WENO weight sums); a
+// non-physical argument (<= 0, NaN) yields NaN or inf, which the positivity check reports.
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double fast_sqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    // two Newton steps on 1/sqrt(x), then one on sqrt(x) itself
+    double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    double s = x * y;
+    double r = fma(-s, s, x);
+    return fma(r, 0.5 * y, s);
+}
+
 // ---------------------------------------------------------------- reconstruction + flux
 // WENO5-JS point-value interpolation to the face between v2 and v3 (A2), with the
 // three nonlinear weights normalised through one division (A41):
@@ -73,7 +97,7 @@ __device__ __forceinline__ double weno5(double v0, double v1, double v2, double 
     double s2 = eps + (c13_12 * t2 * t2 + 0.25 * u2 * u2);
     s0 *= s0; s1 *= s1; s2 *= s2;
     double w0 = s1 * s2, w1 = 10.0 * (s0 * s2), w2 = 5.0 * (s0 * s1);
-    return (w0 * q0 + w1 * q1 + w2 * q2) / (w0 + w1 + w2);
+    return (w0 * q0 + w1 * q1 + w2 * q2) * fast_rcp(w0 + w1 + w2);
 }
 
 // WENO5 + Rusanov flux at one face in the face-normal frame (O10).
@@ -91,7 +115,7 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
     if (CHAR) {
         // eigen-system at the arithmetic-mean primitive state of cells i, i+1 (A4)
         double rL = QV(2, 0), rR = QV(3, 0);
-        double iL = 1.0 / rL, iR = 1.0 / rR;
+        double iL = fast_rcp(rL), iR = fast_rcp(rR);
         double uL = QV(2, kn) * iL, vL = QV(2, kt) * iL;
         double uR = QV(3, kn) * iR, vR = QV(3, kt) * iR;
         double pL = gm1 * (QV(2, 3) - 0.5 * (QV(2, kn) * uL + QV(2, kt) * vL));
@@ -100,12 +124,12 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         u = 0.5 * (uL + uR);
         v = 0.5 * (vL + vR);
         double p = 0.5 * (pL + pR);
-        double c2 = g * p / r;
-        c = sqrt(c2);
-        double ic = 1.0 / c;
+        double c2 = g * p * fast_rcp(r);
+        c = fast_sqrt(c2);
+        double ic = fast_rcp(c);
         qk = 0.5 * (u * u + v * v);
         H = c2 / gm1 + qk;
-        double b1 = gm1 / c2;
+        double b1 = gm1 * (ic * ic);
         double b2 = b1 * qk;
         // rows of L (O10): l1 = 1/2 (b2 + u/c, -b1 u - 1/c, -b1 v, b1), l2, l3 = (-v, 0, 1, 0), l4
         const double h1 = 0.5 * (b2 + u * ic), h2 = 0.5 * (-b1 * u - ic), h3 = 0.5 * (-b1 * v), h4 = 0.5 * b1;
@@ -153,13 +177,13 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         for (int k = 0; k < 4; ++k) { UL[k] = wl[k]; UR[k] = wr[k]; }
     }
     // Rusanov (Eq. 11) with S = max(c^R + |u^R|, c^L + |u^L|) (Eq. 12)
-    double irL = 1.0 / UL[0], irR = 1.0 / UR[0];
+    double irL = fast_rcp(UL[0]), irR = fast_rcp(UR[0]);
     double unL = UL[1] * irL, utL = UL[2] * irL;
     double unR = UR[1] * irR, utR = UR[2] * irR;
     double pL = gm1 * (UL[3] - 0.5 * (UL[1] * unL + UL[2] * utL));
     double pR = gm1 * (UR[3] - 0.5 * (UR[1] * unR + UR[2] * utR));
-    double sL = sqrt(g * pL * irL) + fabs(unL);
-    double sR = sqrt(g * pR * irR) + fabs(unR);
+    double sL = fast_sqrt(g * pL * irL) + fabs(unL);
+    double sR = fast_sqrt(g * pR * irR) + fabs(unR);
     double S = fmax(sR, sL);
     F[0] = 0.5 * (UR[1] + UL[1]) - 0.5 * S * (UR[0] - UL[0]);
     F[1] = 0.5 * ((UR[1] * unR + pR) + (UL[1] * unL + pL)) - 0.5 * S * (UR[1] - UL[1]);
@@ -409,15 +433,6 @@ cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t s) {
 // in-place cons->prim, sliding-window face fluxes (each thread computes R consecutive faces of one
 // row / column with a rolling 4-cell register window) and sliding-window divergences (each thread owns
 // CPT cells of one column), so that every cell is loaded from shared memory a handful of times.
-__device__ __forceinline__ double fast_rcp(double x) {
-    // MUFU.RCP64H seed + two Newton steps (<= 1 ulp; A41)
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
-}
 
 template <int T>
 struct C4Cfg;
