@@ -274,11 +274,12 @@ def measure_sweep(X, args, cfg, steps, warmup, do_e2e):
     return res
 
 
-def measure_quadrant(X, args):
+def measure_quadrant(X, args, use_graphs=0):
     """BASELINE configs[2]: quadrant Riemann problem, 512^2 base, 3 levels, WENO5-char, regrid every 4 steps.
-    Timed: K steps including the regrids (flags, Alg. 1/2, prolongation, migration) inside the region."""
+    Timed: K steps including the regrids (flags, Alg. 1/2, prolongation, migration) inside the region.
+    use_graphs = 1: each step is a CUDA-graph replay (re-captured after each regrid)."""
     torch = X.torch
-    cfg = W.quadrant(N=512, n=16, levels=3, seed=1)
+    cfg = dict(W.quadrant(N=512, n=16, levels=3, seed=1), use_graphs=use_graphs if X.world == 1 else 0)
     mesh = X.mesh(cfg)
     fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
     mesh.set_state(fn)
@@ -349,6 +350,9 @@ def main():
                           "states (DESIGN.md s6); throughput config only"}
     if not args.no_amr:
         extra["quadrant_amr"] = measure_quadrant(X, args)
+        if X.world == 1:
+            q = measure_quadrant(X, args, use_graphs=1)
+            extra["quadrant_amr"]["graphs"] = {"value": q["value"], "ms_per_step": q["ms_per_step"]}
     if X.rank == 0:
         rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
               "frac": main_res["achieved_gbs"] / hbm_peak, "traffic": None, "peak_kind": hbm_kind,

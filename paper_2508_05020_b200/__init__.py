@@ -145,6 +145,7 @@ def make_config(cfg: dict, **over) -> amr_config:
     c.max_patches = int(cfg.get("max_patches", max(16, roots * full)))
     c.check_positivity = int(cfg.get("check_positivity", 1))
     c.stage_kernel = int(cfg.get("stage_kernel", 0))
+    c.use_graphs = int(cfg.get("use_graphs", 0))
     c.world_size = 1
     c.rank = 0
     c.device = -1

@@ -185,6 +185,7 @@ amr_status build_plan(amr_ctx* c) {
     c->st.leaf_cells = c->leaf_cells;
     c->st.proxies = (int64_t)c->ptasks.size();
     c->lambda_valid = false;
+    c->plan_version++;
     c->comm.replan(t);
     return AMR_OK;
 }
@@ -281,7 +282,8 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
         amr_status s = seed_lambda(c);
         if (s != AMR_OK) return s;
     }
-    LAUNCH(launch_dt(c->d_dt, c->d_lambda, c->d_err, dt, cfl, c->stream), "dt");
+    if (c->capturing) LAUNCH(launch_dt_dev(c->d_dt, c->d_lambda, c->d_err, c->d_dtp, c->stream), "dt");
+    else LAUNCH(launch_dt(c->d_dt, c->d_lambda, c->d_err, dt, cfl, c->stream), "dt");
     const int A = (c->un + 1) % 3, B = (c->un + 2) % 3;
     const double as[3] = {0.0, 0.75, 1.0 / 3.0};
     const double bs[3] = {1.0, 0.25, 2.0 / 3.0};
@@ -627,6 +629,7 @@ amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
     CU(cudaMalloc(&c->d_lambda, 8));
     CU(cudaMalloc(&c->d_tmp, 8));
     CU(cudaMalloc(&c->d_err, 16));
+    CU(cudaMalloc(&c->d_dtp, 16));
     CU(cudaMemsetAsync(c->d_err, 0, 16, c->stream));
     CU(cudaMallocHost(&c->h_pinned, 64));
     amr_status s = c->comm.init(c);
@@ -652,7 +655,8 @@ void amr_destroy(amr_ctx* c) {
     c->proxy.release(); c->freg.release(); c->staging.release(); c->d_maxeta.release(); c->d_partial.release();
     c->d_slots.release(); c->d_amb.release();
     if (c->own_pool) cudaFree(c->own_pool);
-    cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp);
+    cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp); cudaFree(c->d_dtp);
+    for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     for (auto e : c->ev_free) cudaEventDestroy(e);
     for (auto e : c->ev_pending) cudaEventDestroy(e);
@@ -787,12 +791,56 @@ amr_status amr_get_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, 
     return AMR_OK;
 }
 
+// One step as a CUDA graph replay (use_graphs, one rank, kernel timing off): the launch sequence of
+// enqueue_step is captured once per position of U^n in the buffer rotation and per plan, and replayed with the
+// step's (dt, cfl) written to device memory first.  Host bookkeeping is the same as enqueue_step's.
+amr_status enqueue_step_graph(amr_ctx* c, double dt, double cfl) {
+    if (!c->lambda_valid && !(dt > 0.0)) {
+        amr_status s = seed_lambda(c);
+        if (s != AMR_OK) return s;
+    }
+    const int u = c->un;
+    if (!c->gexec[u] || c->gver[u] != c->plan_version) {
+        if (c->gexec[u]) { cudaGraphExecDestroy(c->gexec[u]); c->gexec[u] = nullptr; }
+        const int64_t l0 = c->st.launches, sl0 = c->st.stage_launches, st0 = c->st.steps;
+        const bool lv = c->lambda_valid;
+        cudaGraph_t g = nullptr;
+        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        c->capturing = true;
+        amr_status s = enqueue_step(c, dt, cfl);
+        c->capturing = false;
+        cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        c->glaunches[u] = c->st.launches - l0;
+        c->st.launches = l0;
+        c->st.stage_launches = sl0;
+        c->st.steps = st0;
+        c->un = u;
+        c->lambda_valid = lv;
+        if (s != AMR_OK) { if (g) cudaGraphDestroy(g); return s; }
+        if (e != cudaSuccess) return fail(c, AMR_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&c->gexec[u], g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(c, AMR_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        c->gver[u] = c->plan_version;
+    }
+    LAUNCH(launch_set2(c->d_dtp, dt, cfl, c->stream), "dt params");
+    CU(cudaGraphLaunch(c->gexec[u], c->stream));
+    c->st.launches += c->glaunches[u];
+    c->st.stage_launches += 3;
+    c->un = (u + 1) % 3;
+    c->st.steps++;
+    c->lambda_valid = true;
+    return AMR_OK;
+}
+
+bool use_graph(const amr_ctx* c) { return c->cfg.use_graphs && c->cfg.world_size == 1 && !c->timing; }
+
 amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     if (!(dt > 0.0) && !(cfl > 0.0)) return fail(c, AMR_E_ARG, "step: need dt > 0 or cfl > 0");
     int prev = c->un;
-    s = enqueue_step(c, dt, cfl);
+    s = use_graph(c) ? enqueue_step_graph(c, dt, cfl) : enqueue_step(c, dt, cfl);
     if (s != AMR_OK) return s;
     if (c->cfg.check_positivity || dt_used) return finish_step(c, prev, dt_used);
     return AMR_OK;
@@ -803,7 +851,7 @@ amr_status amr_steps(amr_ctx* c, int32_t nsteps, double dt, double cfl) {
     if (s != AMR_OK) return s;
     if (nsteps < 0 || (!(dt > 0.0) && !(cfl > 0.0))) return fail(c, AMR_E_ARG, "steps: bad arguments");
     for (int k = 0; k < nsteps; ++k) {
-        s = enqueue_step(c, dt, cfl);
+        s = use_graph(c) ? enqueue_step_graph(c, dt, cfl) : enqueue_step(c, dt, cfl);
         if (s != AMR_OK) return s;
     }
     return AMR_OK;

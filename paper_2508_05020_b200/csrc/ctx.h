@@ -101,6 +101,15 @@ struct amr_ctx {
     std::vector<int64_t> ev_cells;
     std::vector<double> ev_bytes;
 
+    // CUDA graphs of one step (use_graphs, single rank): one per position of U^n in the buffer rotation,
+    // re-captured when the plan changes
+    uint64_t plan_version = 0;
+    bool capturing = false;
+    cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
+    uint64_t gver[3] = {0, 0, 0};
+    int64_t glaunches[3] = {0, 0, 0};
+    double* d_dtp = nullptr;   // (dt_fixed, cfl) of a replayed step
+
     Comm comm;
     std::string err;
     amr_status sticky = AMR_OK;

@@ -123,6 +123,9 @@ cudaError_t launch_prolong(const ProlongTask* tasks, int ntasks, const AuxArgs& 
 cudaError_t launch_lambda(const LeafDesc* leaves, int nleaves, const AuxArgs& a, cudaStream_t s);
 cudaError_t launch_dt(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed, double cfl,
                       cudaStream_t s);
+cudaError_t launch_dt_dev(double* dt, unsigned long long* lambda_bits, int32_t* err, const double* params,
+                          cudaStream_t s);
+cudaError_t launch_set2(double* p, double a, double b, cudaStream_t s);
 cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* maxeta, int32_t* amb,
                          cudaStream_t s);
 cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* partial, cudaStream_t s);

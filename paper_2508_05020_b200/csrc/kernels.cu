@@ -1269,7 +1269,13 @@ __global__ void lambda_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs
     if ((threadIdx.x & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
 }
 
-__global__ void dt_kernel(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed, double cfl) {
+__global__ void set2_kernel(double* p, double a, double b) {
+    p[0] = a;
+    p[1] = b;
+}
+
+__device__ __forceinline__ void dt_kernel_body(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed,
+                                               double cfl) {
     double lam = __longlong_as_double((long long)*lambda_bits);
     double d = dt_fixed > 0.0 ? dt_fixed : cfl / lam;
     if (!(d > 0.0) || !isfinite(d)) {
@@ -1277,6 +1283,15 @@ __global__ void dt_kernel(double* dt, unsigned long long* lambda_bits, int32_t* 
     }
     *dt = d;
     *lambda_bits = 0ull;
+}
+
+__global__ void dt_kernel(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed, double cfl) {
+    dt_kernel_body(dt, lambda_bits, err, dt_fixed, cfl);
+}
+
+// dt of a graph-replayed step: (dt_fixed, cfl) read from device memory written by set2_kernel before the replay
+__global__ void dt_dev_kernel(double* dt, unsigned long long* lambda_bits, int32_t* err, const double* params) {
+    dt_kernel_body(dt, lambda_bits, err, params[0], params[1]);
 }
 
 // ---------------------------------------------------------------- flags (O6)
@@ -1404,6 +1419,17 @@ cudaError_t launch_prolong(const ProlongTask* tasks, int ntasks, const AuxArgs& 
 cudaError_t launch_lambda(const LeafDesc* leaves, int nleaves, const AuxArgs& a, cudaStream_t s) {
     if (nleaves <= 0) return cudaSuccess;
     lambda_kernel<<<nleaves, 256, 0, s>>>(leaves, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_dev(double* dt, unsigned long long* lambda_bits, int32_t* err, const double* params,
+                          cudaStream_t s) {
+    dt_dev_kernel<<<1, 1, 0, s>>>(dt, lambda_bits, err, params);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set2(double* p, double a, double b, cudaStream_t s) {
+    set2_kernel<<<1, 1, 0, s>>>(p, a, b);
     return cudaGetLastError();
 }
 

@@ -209,3 +209,32 @@ def test_stage_kernel_variants_agree(n, div):
         res.append(g.get_state(as_dict=False))
     scale = np.abs(res[1]).max(axis=(0, 2, 3), keepdims=True)
     assert np.max(np.abs(res[0] - res[1]) / scale) <= 1e-13
+
+
+@pytest.mark.parametrize("case", ["quadrant_amr", "vortex_c4"])
+def test_cuda_graph_replay_bitwise(case):
+    """use_graphs = 1 replays one captured step per RK-buffer position (re-captured after each regrid): states,
+    dt and trees bitwise equal to the stream-launched path, for CFL and fixed-dt steps."""
+    if case == "quadrant_amr":
+        base = W.quadrant(N=64, n=16, levels=3, seed=2)
+    else:
+        base = W.vortex(N=128, n=32)
+    runs = []
+    for graphs in (0, 1):
+        cfg = dict(base, use_graphs=graphs)
+        g = amr.Mesh(cfg)
+        fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+        g.set_state(fn)
+        for _ in range(cfg["levels"] - 1):
+            g.regrid()
+            g.set_state(fn)
+        dts = []
+        for s in range(1, 9):
+            dts.append(g.step(cfl=0.5) if s % 3 else g.step(dt=1e-4))
+            if s % 4 == 0:
+                g.regrid()
+        runs.append((g.get_state(), dts, g.keys()))
+    (s0, d0, k0), (s1, d1, k1) = runs
+    assert k0 == k1 and d0 == d1
+    for key in s0:
+        assert np.array_equal(s0[key], s1[key]), key
