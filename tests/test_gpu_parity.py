@@ -238,3 +238,32 @@ def test_cuda_graph_replay_bitwise(case):
     assert k0 == k1 and d0 == d1
     for key in s0:
         assert np.array_equal(s0[key], s1[key]), key
+
+
+@pytest.mark.parametrize("scheme", ["central4", "weno5"])
+def test_implosion_parity(scheme):
+    """NEXT #2, Eq. 13 at 128^2 (32^2 patches, periodic, CFL 0.45): oracle parity over 10 steps."""
+    run_pair(W.implosion(N=128, n=32, scheme=scheme), steps=10, cfl=0.45)
+
+
+@pytest.mark.parametrize("scheme", ["central4", "weno5"])
+def test_implosion_fullsize_symmetry(scheme):
+    """Eq. 13 at the paper's 1024^2: after 20 CFL-0.45 steps the GPU state keeps the x <-> y and mirror
+    symmetries of the IC (a property that holds at any size) and conserves the totals."""
+    cfg = W.implosion(N=1024, n=32, scheme=scheme)
+    g = amr.Mesh(cfg)
+    g.set_state(U=W.level0_state(cfg).reshape(-1, 4, 32, 32))
+    t0, _ = g.diagnostics()
+    for _ in range(20):
+        g.step(cfl=0.45)
+    t1, _ = g.diagnostics()
+    U = g.get_state(as_dict=False).reshape(32, 32, 4, 32, 32).transpose(2, 0, 3, 1, 4).reshape(4, 1024, 1024)
+    scale = np.abs(U).reshape(4, -1).max(axis=1)
+    T = U.transpose(0, 2, 1)[[0, 2, 1, 3]]
+    M = U[:, :, ::-1].copy()
+    M[1] = -M[1]
+    for k in range(4):
+        assert np.abs(U[k] - T[k]).max() <= 1e-12 * scale[k], ("transpose", k)
+        assert np.abs(U[k] - M[k]).max() <= 1e-12 * scale[k], ("mirror", k)
+    vol = np.abs(U).reshape(4, -1).sum(axis=1) * (0.6 / 1024) ** 2
+    assert np.all(np.abs(t1 - t0) <= 1e-12 * vol)

@@ -375,3 +375,33 @@ def test_prolong_mean_and_restrict_round_trip_random():
     coarse_region[:] = before[:, :, :]
     np.testing.assert_allclose(mean, coarse_region, rtol=1e-14, atol=1e-14)
     np.testing.assert_allclose(o.get_patch((0, 2, 1)), before, rtol=1e-15, atol=1e-15)
+
+
+# ----------------------------------------------------------------------------- implosion (Eq. 13), NEXT #2
+@pytest.mark.parametrize("scheme", ["central4", "weno5"])
+def test_implosion_symmetries_and_conservation(scheme):
+    """Eq. 13: the diamond IC on the periodic square (-0.3, 0.3)^2 is invariant under x <-> y
+    (with u <-> v) and under x -> -x (with u -> -u); the scheme preserves both and conserves mass,
+    momentum and energy to rounding."""
+    cfg = W.implosion(N=64, n=16, scheme=scheme)
+    o = orc.Oracle(cfg)
+    o.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    t0 = o.totals()
+    for _ in range(12):
+        o.step(cfl=0.45)
+    t1 = o.totals()
+    st = o.get_state()
+    n, NP = cfg["n"], 64 // cfg["n"]
+    G = np.zeros((4, 64, 64))
+    for (l, P, Q), U in st.items():
+        G[:, Q * n:(Q + 1) * n, P * n:(P + 1) * n] = U
+    scale = np.abs(G).reshape(4, -1).max(axis=1)
+    T = G.transpose(0, 2, 1)[[0, 2, 1, 3]]
+    M = G[:, :, ::-1].copy()
+    M[1] = -M[1]
+    for k in range(4):
+        assert np.abs(G[k] - T[k]).max() <= 1e-12 * scale[k], ("transpose", k)
+        assert np.abs(G[k] - M[k]).max() <= 1e-12 * scale[k], ("mirror", k)
+    assert np.abs(G[1]).max() > 1e-3 * scale[0]        # the flow has started
+    vol = np.abs(G).reshape(4, -1).sum(axis=1) * (0.6 / 64) ** 2
+    assert np.all(np.abs(t1 - t0) <= 1e-12 * vol), (t1 - t0) / vol

@@ -151,9 +151,19 @@ def ic_shock_bubble(cfg, X, Y, **_):
     return rho, u, np.zeros_like(X), p
 
 
-def ic_implosion(cfg, X, Y, **_):
-    """Eq. 13: (rho,p) = (0.125,0.140) where |x|+|y| < 0.15, else (1,1); at rest."""
-    inside = np.abs(X) + np.abs(Y) < 0.15
+def ic_implosion(cfg, X, Y, l=0, I=None, J=None, **_):
+    """Eq. 13: (rho,p) = (0.125,0.140) where |x|+|y| < 0.15, else (1,1); at rest.  On the centred
+    domain the cell-centre coordinates are evaluated from the cell index as |2I+1-N| h/2 so that mirrored cells get
+    bit-identical |x| (cells with |x|+|y| exactly 0.15 exist at every N = 64 k and must not be decided by the
+    rounding of lo + (I+1/2) h)."""
+    lo, hi = cfg["lo"], cfg["hi"]
+    if I is not None and J is not None and lo[0] == -hi[0] and lo[1] == -hi[1]:
+        Nx, Ny = cfg["base"][0] << l, cfg["base"][1] << l
+        ax = np.abs(2 * np.asarray(I, dtype=np.int64) + 1 - Nx) * (0.5 * (hi[0] - lo[0]) / Nx)
+        ay = np.abs(2 * np.asarray(J, dtype=np.int64) + 1 - Ny) * (0.5 * (hi[1] - lo[1]) / Ny)
+        inside = ax + ay < 0.15
+    else:
+        inside = np.abs(X) + np.abs(Y) < 0.15
     rho = np.where(inside, 0.125, 1.0)
     p = np.where(inside, 0.140, 1.0)
     z = np.zeros_like(X)
