@@ -88,8 +88,10 @@ typedef struct {
     int32_t comm_backend;         /* world_size > 1: 0 NCCL (nccl_unique_id = ncclUniqueId); 1 in-process
                                      loopback of virtual ranks on one GPU, one host thread each
                                      (test-only; nccl_unique_id = 128-byte group key string)   */
-    int32_t stage_kernel;         /* fused stage kernel variant: 0 default (Central4 with n >= 32: persistent
-                                     TMA-pipelined kernel), 1 one CTA per tile with a cp.async halo gather */
+    int32_t stage_kernel;         /* stage kernel organisation (NEXT #1 fusion study): 0 default (Central4 with
+                                     n >= 32: persistent TMA-pipelined fused kernel, else 1); 1 fused, one CTA per
+                                     tile with a cp.async halo gather; 2 unfused: four kernels per stage with the
+                                     primitives and face fluxes through HBM; 3 one launch of kernel 1 per leaf */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none

@@ -70,7 +70,7 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.world_size > 1 && !c.nccl_unique_id) { m = "world_size > 1 needs nccl_unique_id"; return AMR_E_CONFIG; }
     if (c.refine_threshold < 0 || c.coarsen_fraction < 0) { m = "bad thresholds"; return AMR_E_CONFIG; }
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
-    if (c.stage_kernel != 0 && c.stage_kernel != 1) { m = "stage_kernel must be 0 or 1"; return AMR_E_CONFIG; }
+    if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }
     return AMR_OK;
 }
 
@@ -318,6 +318,10 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
         a.nslots = c->cfg.max_patches;
         a.nproxy = (int32_t)(c->proxy.cap / c->PS);
         a.variant = c->cfg.stage_kernel;
+        if (a.variant == 2) {
+            CU(c->unf_scratch.reserve(unfused_scratch_doubles(c->n, std::max(1, a.nleaves))));
+            a.scratch = c->unf_scratch.p;
+        }
         a.geo = c->geo;
         int scheme = c->cfg.scheme == AMR_CENTRAL4 ? 0 : (c->cfg.weno_characteristic ? 1 : 2);
         cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -327,6 +331,7 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
             CU(cudaEventRecord(e0, c->stream));
         }
         LAUNCH(launch_stage(scheme, a, c->stream), "stage");
+        c->st.launches += stage_launches_per_stage(a.variant, a.nleaves) - 1;
         c->st.stage_launches++;
         if (e1) {
             CU(cudaEventRecord(e1, c->stream));
@@ -653,6 +658,7 @@ void amr_destroy(amr_ctx* c) {
     c->d_leaves.release(); c->d_ptasks.release(); c->d_rtasks.release(); c->d_prolong.release();
     for (auto& d : c->d_rlev) d.release();
     c->proxy.release(); c->freg.release(); c->staging.release(); c->d_maxeta.release(); c->d_partial.release();
+    c->unf_scratch.release();
     c->d_slots.release(); c->d_amb.release();
     if (c->own_pool) cudaFree(c->own_pool);
     cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp); cudaFree(c->d_dtp);

@@ -75,7 +75,7 @@ struct amr_ctx {
     DevArray<RefluxTask> d_rtasks;
     std::vector<DevArray<RestrictTask>> d_rlev;
     DevArray<ProlongTask> d_prolong;
-    DevArray<double> proxy, freg, staging, d_maxeta, d_partial;
+    DevArray<double> proxy, freg, staging, d_maxeta, d_partial, unf_scratch;
     DevArray<int32_t> d_slots, d_amb;
     DevArray<int32_t> x_sidx, x_ridx;             // multi-rank exchange slot lists
     DevArray<double> x_send, x_recv;              // multi-rank exchange buffers

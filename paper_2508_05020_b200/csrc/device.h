@@ -92,7 +92,8 @@ struct StageArgs {
     int32_t* err;              // [0] flag, [1] slot, [2] stage, [3] cell
     int32_t nslots;            // slots in each RK buffer (TMA tensor-map extent)
     int32_t nproxy;            // proxy patches allocated (TMA tensor-map extent)
-    int32_t variant;           // amr_config.stage_kernel: 0 best, 1 one-CTA-per-tile smem gather
+    int32_t variant;           // amr_config.stage_kernel: 0 best, 1 per-tile fused, 2 unfused, 3 per-patch launches
+    double* scratch;           // variant 2: intermediate fields (unfused_scratch_doubles)
     int32_t prof;              // phase timing of the TMA kernel (AMR_PHASE_PROF, debug)
     Geometry geo;
 };
@@ -134,6 +135,10 @@ cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a,
 // flux registers: per = 16 n)
 cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int per, cudaStream_t s);
 cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int per, cudaStream_t s);
+
+// unfused stage (variant 2): scratch doubles for nleaves patches; kernel launches per stage of a variant
+size_t unfused_scratch_doubles(int n, int nleaves);
+int stage_launches_per_stage(int variant, int nleaves);
 
 // bytes of dynamic shared memory the stage kernel needs (for occupancy queries)
 size_t stage_smem_bytes(int scheme, int n);

@@ -1055,6 +1055,147 @@ cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- unfused stage (NEXT #1 fusion study)
+// The GPU analogue of the paper's unfused task graph (Fig. 9 ssprk3Stage as its own task): four
+// kernels per stage over the leaf list, with the intermediate fields round-tripping through HBM:
+//   unf_prim:  halo gather + cons->prim (Central4: p, T, u, v; WENO: conserved copy) into padded tiles
+//   unf_xflux / unf_yflux: face fluxes (the fused kernel's reconstruction + Riemann flux) into face arrays
+//   unf_rk:    Eq. 9 F-hat, divergence, SSP-RK3, checks, Lambda, flux registers (ssprk3Stage)
+// Same device functions and arithmetic as the fused kernels; scratch layout per leaf: W [4][n+8][n+8],
+// fx [4][n][n+3], fy [4][n+3][n] (face m at m+1).
+constexpr int kUnfG = kGL;
+
+__global__ void unf_prim_kernel(const StageArgs a, int scheme) {
+    const int n = a.geo.n, Wd = n + 2 * kUnfG;
+    const long long per = (long long)Wd * Wd;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)a.nleaves * per) return;
+    const int leaf = (int)(t / per), e = (int)(t - (long long)leaf * per);
+    const int jj = e / Wd, ii = e - jj * Wd;
+    int i = ii - kUnfG, j = jj - kUnfG;
+    const bool xin = i >= 0 && i < n, yin = j >= 0 && j < n;
+    if (!xin && !yin) return;                       // corner blocks are never read (A26)
+    const LeafDesc d = a.leaves[leaf];
+    const size_t nn = (size_t)n * n, PS = 4 * nn;
+    int s = d.slot;
+    bool own = true;
+    if (i < 0) { s = d.side[kW]; i += n; own = false; }
+    else if (i >= n) { s = d.side[kE]; i -= n; own = false; }
+    else if (j < 0) { s = d.side[kS]; j += n; own = false; }
+    else if (j >= n) { s = d.side[kN]; j -= n; own = false; }
+    const double* b = (own || s >= 0) ? a.Uin + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS;
+    const size_t o = (size_t)j * n + i;
+    const double r = b[o], m = b[nn + o], w = b[2 * nn + o], E = b[3 * nn + o];
+    double* W = a.scratch + (size_t)leaf * 4 * per + e;
+    if (scheme == 0) {
+        const double ir = fast_rcp(r);
+        const double u = m * ir, v = w * ir;
+        const double p = (a.gamma - 1.0) * (E - 0.5 * (m * u + w * v));
+        W[0] = p; W[per] = p * ir; W[2 * per] = u; W[3 * per] = v;
+    } else {
+        W[0] = r; W[per] = m; W[2 * per] = w; W[3 * per] = E;
+    }
+}
+
+template <int SCHEME, int DIR>
+__global__ void unf_flux_kernel(const StageArgs a) {
+    const int n = a.geo.n, Wd = n + 2 * kUnfG, NF = n + 3;
+    const long long per = (long long)Wd * Wd, fper = 4LL * n * NF;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)a.nleaves * n * NF) return;
+    const int leaf = (int)(t / ((long long)n * NF)), e = (int)(t - (long long)leaf * n * NF);
+    const double* W = a.scratch + (size_t)leaf * 4 * per;
+    double* f = a.scratch + (size_t)a.nleaves * 4 * per + (size_t)(2 * leaf + DIR) * fper;
+    double F[4];
+    const double g = a.gamma, inv_gm1 = 1.0 / (g - 1.0);
+    if (DIR == 0) {   // x faces: row j, face m = -1 .. n+1 (left of cell m)
+        const int j = e / NF, m = e - j * NF - 1;
+        const int o = (j + kUnfG) * Wd + m + kUnfG;
+        if (SCHEME == 0) central4_flux(W + o - 2, 1, (int)per, 2, 3, inv_gm1, F);
+        else weno_rusanov<SCHEME == 1>(W + o - 3, 1, (int)per, 1, 2, g, a.eps, F);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[((size_t)k * n + j) * NF + m + 1] = F[k];
+    } else {          // y faces: column i, face m (below cell m); components stored in U order
+        const int m = e / n - 1, i = e - (m + 1) * n;
+        const int o = (m + kUnfG) * Wd + i + kUnfG;
+        if (SCHEME == 0) central4_flux(W + o - 2 * Wd, Wd, (int)per, 3, 2, inv_gm1, F);
+        else weno_rusanov<SCHEME == 1>(W + o - 3 * Wd, Wd, (int)per, 2, 1, g, a.eps, F);
+        f[((size_t)0 * NF + m + 1) * n + i] = F[0];
+        f[((size_t)1 * NF + m + 1) * n + i] = F[2];
+        f[((size_t)2 * NF + m + 1) * n + i] = F[1];
+        f[((size_t)3 * NF + m + 1) * n + i] = F[3];
+    }
+}
+
+__global__ void unf_rk_kernel(const StageArgs a) {
+    const int n = a.geo.n, Wd = n + 2 * kUnfG, NF = n + 3;
+    const long long per = (long long)Wd * Wd, fper = 4LL * n * NF;
+    const size_t nn = (size_t)n * n, PS = 4 * nn;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)a.nleaves * (long long)nn) return;
+    const int leaf = (int)(t / (long long)nn), c = (int)(t - (long long)leaf * nn);
+    const int i = c % n, j = c / n;
+    const LeafDesc d = a.leaves[leaf];
+    const double* fx = a.scratch + (size_t)a.nleaves * 4 * per + (size_t)(2 * leaf) * fper;
+    const double* fy = fx + fper;
+    const double idx = a.geo.inv_dx[d.level], idy = a.geo.inv_dy[d.level];
+    const bool div4 = a.div_order == 4;
+    const int store_mask = (d.cf | (d.cf >> 4)) & 15, coarse_mask = d.cf & 15;
+    const double c13 = 13.0 / 12.0, c24 = 1.0 / 24.0;
+    const double dt = *a.dt;
+    double o4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double* fr = fx + ((size_t)k * n + j) * NF + i + 1;   // fr[0] = f at face i
+        const double fl = fr[0], fh = fr[1];
+        const double Fl = div4 ? c13 * fl - c24 * (fr[-1] + fh) : fl;
+        const double Fh = div4 ? c13 * fh - c24 * (fl + fr[2]) : fh;
+        const double* fc = fy + ((size_t)k * NF + j + 1) * n + i;   // fc[0] = f at face j
+        const double gl = fc[0], gh = fc[n];
+        const double Gl = div4 ? c13 * gl - c24 * (fc[-n] + gh) : gl;
+        const double Gh = div4 ? c13 * gh - c24 * (gl + fc[2 * n]) : gh;
+        if (store_mask) {
+            if (i == 0 && (store_mask & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + k) * n + j] = Fl;
+            if (i == n - 1 && (store_mask & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + k) * n + j] = Fh;
+            if (j == 0 && (store_mask & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + k) * n + i] = Gl;
+            if (j == n - 1 && (store_mask & 8)) a.freg[(((size_t)d.slot * 4 + kN) * 4 + k) * n + i] = Gh;
+        }
+        const double L = -(Fh - Fl) * idx - (Gh - Gl) * idy;
+        double v = a.Uin[(size_t)d.slot * PS + k * nn + c] + dt * L;
+        if (a.stage > 1) v = a.a * a.Un[(size_t)d.slot * PS + k * nn + c] + a.b * v;
+        o4[k] = v;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a.Uout[(size_t)d.slot * PS + k * nn + c] = o4[k];
+    const bool edge_cf = ((coarse_mask & 1) && i == 0) || ((coarse_mask & 2) && i == n - 1) ||
+                         ((coarse_mask & 4) && j == 0) || ((coarse_mask & 8) && j == n - 1);
+    unsigned long long lam = 0ull;
+    if (!edge_cf) {
+        if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], a.gamma)) report_error(a.err, d.slot, a.stage, c);
+        if (a.want_lambda)
+            lam = (unsigned long long)__double_as_longlong(wave_speed(o4[0], o4[1], o4[2], o4[3], a.gamma, idx, idy));
+    }
+    if (a.want_lambda) {
+        lam = warp_max_u64(lam);
+        if ((threadIdx.x & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
+    }
+}
+
+template <int SCHEME>
+cudaError_t launch_unfused(const StageArgs& a, cudaStream_t s) {
+    if (a.nleaves == 0) return cudaSuccess;
+    if (!a.scratch) return cudaErrorInvalidValue;
+    const int n = a.geo.n, Wd = n + 2 * kUnfG;
+    const long long w = (long long)a.nleaves * Wd * Wd, f = (long long)a.nleaves * n * (n + 3),
+                    c = (long long)a.nleaves * n * n;
+    unf_prim_kernel<<<(unsigned)((w + 255) / 256), 256, 0, s>>>(a, SCHEME);
+    unf_flux_kernel<SCHEME, 0><<<(unsigned)((f + 127) / 128), 128, 0, s>>>(a);
+    unf_flux_kernel<SCHEME, 1><<<(unsigned)((f + 127) / 128), 128, 0, s>>>(a);
+    unf_rk_kernel<<<(unsigned)((c + 255) / 256), 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int SCHEME>
 cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
     int T = a.geo.n / a.tiles;
@@ -1377,9 +1518,31 @@ inline unsigned grid_for(long long work, int block) { return (unsigned)((work + 
 }  // namespace
 
 cudaError_t launch_stage(int scheme, const StageArgs& a, cudaStream_t s) {
+    if (a.variant == 2)   // unfused: four kernels per stage
+        return scheme == 0 ? launch_unfused<0>(a, s) : (scheme == 1 ? launch_unfused<1>(a, s) : launch_unfused<2>(a, s));
+    if (a.variant == 3) {   // one launch of the per-tile fused kernel per leaf patch
+        StageArgs b = a;
+        b.variant = 1;
+        b.nleaves = 1;
+        for (int l = 0; l < a.nleaves; ++l) {
+            b.leaves = a.leaves + l;
+            cudaError_t e = launch_stage(scheme, b, s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     if (scheme == 0) return launch_stage_s<0>(a, s);
     if (scheme == 1) return launch_stage_s<1>(a, s);
     return launch_stage_s<2>(a, s);
+}
+
+size_t unfused_scratch_doubles(int n, int nleaves) {
+    const size_t Wd = (size_t)n + 2 * kUnfG;
+    return (size_t)nleaves * (4 * Wd * Wd + 2 * 4 * (size_t)n * (n + 3));
+}
+
+int stage_launches_per_stage(int variant, int nleaves) {
+    return variant == 2 ? 4 : (variant == 3 ? nleaves : 1);
 }
 
 size_t stage_smem_bytes(int scheme, int n) {

@@ -181,11 +181,12 @@ def test_tree_matches_oracle_after_random_requests():
     assert e == 0.0
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("n", [32, 64])
 def test_central4_amr_walls(n, variant):
     """Central4 on a 2-level mesh with C/F faces (proxies, flux registers, reflux) and transmissive / reflective
-    walls, for both fused stage kernels: 0 = persistent TMA-pipelined (n >= 32), 1 = one CTA per tile."""
+    walls, for every stage-kernel organisation: 0 = persistent TMA-pipelined (n >= 32), 1 = one CTA per tile,
+    2 = unfused (four kernels, intermediates through HBM), 3 = one launch per leaf patch."""
     N = 128 if n == 32 else 256
     cfg = W.vortex(N=N, n=n, levels=2, theta=0.01 if n == 32 else 0.02, stage_kernel=variant,
                    bc=("transmissive", "transmissive", "reflective", "reflective"))
@@ -267,3 +268,11 @@ def test_implosion_fullsize_symmetry(scheme):
         assert np.abs(U[k] - M[k]).max() <= 1e-12 * scale[k], ("mirror", k)
     vol = np.abs(U).reshape(4, -1).sum(axis=1) * (0.6 / 1024) ** 2
     assert np.all(np.abs(t1 - t0) <= 1e-12 * vol)
+
+
+@pytest.mark.parametrize("variant", [2, 3])
+@pytest.mark.parametrize("char", [1, 0])
+def test_weno_amr_unfused_and_per_patch(variant, char):
+    """The NEXT #1 organisations on the WENO5 path with AMR (quadrant, 3 levels, regrids): oracle parity."""
+    cfg = W.quadrant(N=64, n=16, levels=3, seed=1, stage_kernel=variant, characteristic=char)
+    run_pair(cfg, steps=6, cfl=0.5, regrid_every=3)
