@@ -184,6 +184,8 @@ amr_status build_plan(amr_ctx* c) {
     c->st.patches = (int64_t)c->canon.size();
     c->st.leaf_cells = c->leaf_cells;
     c->st.proxies = (int64_t)c->ptasks.size();
+    if (c->cfg.stage_kernel == 2)
+        CU(c->unf_scratch.reserve(unfused_scratch_doubles(c->n, std::max<int>(1, (int)c->leaves.size()))));
     c->lambda_valid = false;
     c->plan_version++;
     c->comm.replan(t);
@@ -318,10 +320,7 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
         a.nslots = c->cfg.max_patches;
         a.nproxy = (int32_t)(c->proxy.cap / c->PS);
         a.variant = c->cfg.stage_kernel;
-        if (a.variant == 2) {
-            CU(c->unf_scratch.reserve(unfused_scratch_doubles(c->n, std::max(1, a.nleaves))));
-            a.scratch = c->unf_scratch.p;
-        }
+        a.scratch = c->unf_scratch.p;   // variant 2: reserved by build_plan (no allocation inside a graph capture)
         a.geo = c->geo;
         int scheme = c->cfg.scheme == AMR_CENTRAL4 ? 0 : (c->cfg.weno_characteristic ? 1 : 2);
         cudaEvent_t e0 = nullptr, e1 = nullptr;
