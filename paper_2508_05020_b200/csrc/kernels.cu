@@ -13,6 +13,8 @@
 // Readings and rewrites (A41: single-division WENO weights, reciprocal dx,
 // FMA contraction) are listed in DESIGN.md.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include <cuda.h>
 
@@ -715,9 +717,35 @@ struct C4Maps {
     CUtensorMap in_sn;    // stage input, box {32, 4, 4}
     CUtensorMap px_we;    // proxy buffer, box {4, 32, 4}
     CUtensorMap px_sn;    // proxy buffer, box {32, 4, 4}
+    CUtensorMap un_int;   // U^n, box {32, 32, 4}
+    CUtensorMap out_int;  // U^(s), box {32, 32, 4} (TMA store)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tma_prefetch3(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap* map, int c0, int c1, int c2, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(src) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// LeafDesc load the compiler may not sink towards its use (issued one tile ahead on purpose)
+__device__ __forceinline__ LeafDesc load_desc_early(const LeafDesc* p) {
+    static_assert(sizeof(LeafDesc) == 32, "LeafDesc is two 16-byte words");
+    int4 a, b;
+    asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p));
+    asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(reinterpret_cast<const char*>(p) + 16));
+    LeafDesc d;
+    d.slot = a.x; d.level = a.y; d.side[0] = a.z; d.side[1] = a.w;
+    d.side[2] = b.x; d.side[3] = b.y; d.cf = b.z; d.pad = b.w;
+    return d;
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_init(uint32_t mb, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
@@ -743,23 +771,33 @@ __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, 
 }
 
 constexpr int kTmaThreads = 512;
+// optional phase timing (build with AMR_NVCC_FLAGS=-DAMR_PHASE_PROF, run with AMR_PHASE_PROF=1): per-warp
+// cycle counts of the kernel phases, printed per launch by the launcher
+#ifdef AMR_PHASE_PROF
+__device__ unsigned long long g_phase[16][8];
+#define PH_MARK(slot) do { if (prof) { long long _c = clock64(); ph_acc[slot] += _c - ph_t; ph_t = _c; } } while (0)
+#else
+#define PH_MARK(slot) do { } while (0)
+#endif
 constexpr int kTmaT = 32;                                  // tile edge
 constexpr int kTmaWP = 44;                                 // prim plane row stride
 constexpr int kTmaPL = (kTmaT + 2 * kGL) * kTmaWP;         // prim plane (40 rows: j = -4 .. 35)
 constexpr int kTmaNH = kTmaT + 1;                          // F-hat faces per line: 0 .. T
-constexpr int kTmaFXS = 36, kTmaFYS = 36;                  // F-hat row strides
+constexpr int kTmaFXS = 36, kTmaFYS = 36;                  // row strides of the Lx / Ly planes (equal)
 constexpr int kLandI = 0, kLandW = 4 * kTmaT * kTmaT, kLandE = kLandW + 4 * kTmaT * kGL,
               kLandS = kLandE + 4 * kTmaT * kGL, kLandN = kLandS + 4 * kGL * kTmaT,
               kLandSz = kLandN + 4 * kGL * kTmaT;
-constexpr size_t kTmaSmem = sizeof(double) * (2 * kLandSz + 4 * kTmaPL + 4 * kTmaT * kTmaFXS + 4 * kTmaNH * kTmaFYS) + 16 + 128;
+constexpr size_t kTmaSmem =
+    sizeof(double) * (2 * kLandSz + 4 * kTmaPL + 4 * kTmaT * kTmaFXS + 4 * kTmaT * kTmaFYS) + 32 + 64 + 128;
 
 // One 5-face segment (faces m0 .. m0+4 of a row or column; 7 segments cover faces -1 .. T+1): sliding 4-cell
 // window of (p, T, u_n, u_t) over the prim planes (q = cell m0, cs = cell stride along the line, kn / kt = planes
 // of the normal / tangential velocity), Central4 edge fluxes, and Eq. 9 F-hat at the 5 faces with f(m0-1) and
-// f(m0+5) from the neighbouring segments' lanes (s unused: lanes 0-3 / 24-27 get garbage there, never stored).
+// f(m0+5) from the neighbouring segments' lanes, plus F-hat(m0+5) from the next segment (s unused: the values
+// shuffled in across the line ends are garbage and never used).
 template <bool DIV4>
 __device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs, int kn, int kt, double inv_gm1,
-                                           int s, double (&Fh)[5][4]) {
+                                           int s, double (&Fh)[6][4]) {
     constexpr int PL = kTmaPL;
     double p[4], Tt[4], un[4], ut[4];
 #pragma unroll
@@ -791,6 +829,7 @@ __device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs,
 #pragma unroll
             for (int e = 0; e < 5; ++e) Fh[e][k] = f[e][k];
         }
+        Fh[5][k] = __shfl_down_sync(0xffffffffu, Fh[0][k], 4);   // F-hat(m0+5): the next segment's first face
     }
 }
 
@@ -803,21 +842,26 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* const land = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     double* const prim = land + 2 * kLandSz;
-    double* const fx = prim + 4 * PL;
-    double* const fy = fx + 4 * T * FXS;
-    uint64_t* const mbar = reinterpret_cast<uint64_t*>(fy + 4 * NH * FYS);
+    double* const dUx = prim + 4 * PL;           // [4][T][FXS] Lx = -dF-hat_x/dx of cell (i, j) at j*FXS + i
+    double* const dUy = dUx + 4 * T * FXS;       // [4][T][FYS] Ly = -dF-hat_y/dy (components in U order)
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(dUy + 4 * T * FYS);   // [4]
+    LeafDesc* const sDesc = reinterpret_cast<LeafDesc*>(mbar + 4);          // [2] descriptors of tiles k, k+1
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double g = a.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
     const bool rk_un = a.stage > 1;
     const double ca = a.a, cb = a.b;
     const double dt = *a.dt;
+#ifdef AMR_PHASE_PROF
+    const bool prof = a.prof;
+    long long ph_t = clock64();
+    long long ph_acc[8] = {};
+#endif
 
-    auto issue = [&](int t, int b) {
+    auto issue = [&](int t, int b, const LeafDesc& d) {
         const int leaf = TILES == 1 ? t : t / TT;
         const int tt = TILES == 1 ? 0 : t - leaf * TT;
         const int tx = tt % TILES, ty = tt / TILES;
-        const LeafDesc d = a.leaves[leaf];
         const uint32_t mb = smem_u32(&mbar[b]);
         const uint32_t dst = smem_u32(land + b * kLandSz);
         mbar_expect_tx(mb, kLandSz * 8);
@@ -842,12 +886,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_int)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_we)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_sn)) : "memory");
-        mbar_init(smem_u32(&mbar[0]), 1);
-        mbar_init(smem_u32(&mbar[1]), 1);
+        for (int q = 0; q < 4; ++q) mbar_init(smem_u32(&mbar[q]), 1);   // [0,1] landing, [2,3] U^n
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    // tile descriptors travel global -> shared by cp.async one tile ahead (no register round trip: a warp-uniform
+    // load would otherwise be waited for at once to fill uniform registers)
+    auto desc_ptr = [&](int t) { return a.leaves + (TILES == 1 ? t : t / TT); };
+    LeafDesc dn{};
+    if ((int)blockIdx.x < ntiles) {
+        dn = *desc_ptr(blockIdx.x);
+        if (tid == 0) {
+            issue(blockIdx.x, 0, dn);
+            if (rk_un) tma_prefetch3(&maps.un_int, 0, 0, 4 * dn.slot);   // (tile offsets added below for N = 64)
+        }
+    }
 
     const int ci = lane, cj0 = 2 * warp;
     const int seg_line = lane & 3, seg = lane < 28 ? lane >> 2 : 6;
@@ -859,18 +912,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const int leaf = TILES == 1 ? t : t / TT;
         const int tt = TILES == 1 ? 0 : t - leaf * TT;
         const int tx = tt % TILES, ty = tt / TILES;
-        const LeafDesc d = a.leaves[leaf];
-        const int base_off = (ty * T + cj0) * N + tx * T + ci;
-        double un[2][4] = {};
-        if (rk_un) {
-            const double* pn = a.Un + (size_t)d.slot * PS + base_off;
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) un[r][q] = __ldg(pn + q * NN + r * N);
+        const LeafDesc d = k == 0 ? dn : sDesc[b];
+        if (tid == 32 && t + (int)gridDim.x < ntiles) {
+            const uint32_t dst = smem_u32(&sDesc[b ^ 1]);
+            const LeafDesc* src = desc_ptr(t + gridDim.x);
+            cp_async16(dst, src);
+            cp_async16(dst + 16, reinterpret_cast<const char*>(src) + 16);
         }
+        const int base_off = (ty * T + cj0) * N + tx * T + ci;
         const double* L = land + b * kLandSz;
+        PH_MARK(0);
         mbar_wait(smem_u32(&mbar[b]), (uint32_t)((k >> 1) & 1));
+        PH_MARK(1);
         auto c2p = [&](double r, double m, double w, double E, int o) {
             const double ir = fast_rcp(r);
             const double u = m * ir, v = w * ir;
@@ -896,79 +949,110 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const double* s = L + off;
             c2p(s[0], s[G * T], s[2 * G * T], s[3 * G * T], (j + G) * WP + i + G);
         }
+        if (tid == 32) cp_async_wait_all();      // descriptor of tile k+1 in sDesc[b^1] before (A)
+        PH_MARK(2);
         __syncthreads();
-        if (tid == 0 && t + (int)gridDim.x < ntiles) {
+        PH_MARK(3);
+        if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(t + gridDim.x, b ^ 1);
+            bulk_wait_read0();                   // the store of tile k-1 has read landing[b^1]
+            if (t + (int)gridDim.x < ntiles) {
+                const LeafDesc dn = sDesc[b ^ 1];
+                issue(t + gridDim.x, b ^ 1, dn);
+                if (rk_un) {                     // U^n of tile k+1 towards L2
+                    const int t2 = t + gridDim.x, tt2 = TILES == 1 ? 0 : t2 % TT;
+                    tma_prefetch3(&maps.un_int, (tt2 % TILES) * T, (tt2 / TILES) * T, 4 * dn.slot);
+                }
+            }
+            if (rk_un) {                         // U^n of tile k into the converted landing[b] interior
+                const uint32_t mb = smem_u32(&mbar[2 + b]);
+                mbar_expect_tx(mb, 4 * T * T * 8);
+                tma_load3(smem_u32(land + b * kLandSz + kLandI), &maps.un_int, tx * T, ty * T, 4 * d.slot, mb);
+            }
         }
+        PH_MARK(4);
         {
+            // faces, Eq. 9 F-hat and the divergence of the segment's own cells m0 .. m0+4 (within [0, T))
             const int m0 = seg * 5 - 1;
-            double Fh[5][4];
+            const int lvl = d.level;
+            double Fh[6][4];
             if (warp < 8) {
                 const int j = 4 * warp + seg_line;
+                const double idx = a.geo.inv_dx[lvl];
                 c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
                 if (seg_store) {
-                    double* fo = fx + j * FXS + m0;
 #pragma unroll
                     for (int e = 0; e < 5; ++e)
-                        if ((seg > 0 || e > 0) && (seg < 6 || e < 4))
+                        if (m0 + e >= 0 && m0 + e < T)
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) fo[q * T * FXS + e] = Fh[e][q];
+                            for (int q = 0; q < 4; ++q) dUx[(q * T + j) * FXS + m0 + e] = -(Fh[e + 1][q] - Fh[e][q]) * idx;
+                    const int sm = (d.cf | (d.cf >> 4)) & 15;
+                    if (sm & 3) {   // flux registers of coarse/fine x sides: F-hat at faces 0 and T
+#pragma unroll
+                        for (int e = 0; e < 5; ++e)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (m0 + e == 0 && tx == 0 && (sm & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + j] = Fh[e][q];
+                                if (m0 + e == T && tx == TILES - 1 && (sm & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + j] = Fh[e][q];
+                            }
+                    }
                 }
             } else {
                 const int i = 4 * (warp - 8) + seg_line;
+                const double idy = a.geo.inv_dy[lvl];
                 c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
                 if (seg_store) {
-                    double* fo = fy + m0 * FYS + i;
 #pragma unroll
                     for (int e = 0; e < 5; ++e)
-                        if ((seg > 0 || e > 0) && (seg < 6 || e < 4)) {
-                            fo[0 * NH * FYS + e * FYS] = Fh[e][0];
-                            fo[1 * NH * FYS + e * FYS] = Fh[e][2];
-                            fo[2 * NH * FYS + e * FYS] = Fh[e][1];
-                            fo[3 * NH * FYS + e * FYS] = Fh[e][3];
+                        if (m0 + e >= 0 && m0 + e < T) {
+                            double* o = dUy + (m0 + e) * FYS + i;
+                            o[0 * T * FYS] = -(Fh[e + 1][0] - Fh[e][0]) * idy;
+                            o[1 * T * FYS] = -(Fh[e + 1][2] - Fh[e][2]) * idy;
+                            o[2 * T * FYS] = -(Fh[e + 1][1] - Fh[e][1]) * idy;
+                            o[3 * T * FYS] = -(Fh[e + 1][3] - Fh[e][3]) * idy;
                         }
+                    const int sm = (d.cf | (d.cf >> 4)) & 15;
+                    if (sm & 12) {
+#pragma unroll
+                        for (int e = 0; e < 5; ++e) {
+                            const double Fu[4] = {Fh[e][0], Fh[e][2], Fh[e][1], Fh[e][3]};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (m0 + e == 0 && ty == 0 && (sm & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + q) * N + tx * T + i] = Fu[q];
+                                if (m0 + e == T && ty == TILES - 1 && (sm & 8)) a.freg[(((size_t)d.slot * 4 + kN) * 4 + q) * N + tx * T + i] = Fu[q];
+                            }
+                        }
+                    }
                 }
             }
         }
+        PH_MARK(5);
         __syncthreads();
+        PH_MARK(6);
         const int lvl = d.level;
         const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
         const bool x_lo = tx == 0, x_hi = tx == TILES - 1, y_lo = ty == 0, y_hi = ty == TILES - 1;
-        const int store_mask = (d.cf | (d.cf >> 4)) & 15;
         const int coarse_mask = d.cf & 15;
+        // U^n (TMA, landed in landing[b]) in, U^(s) out through the same slots, then one TMA store per tile
+        double* const sU = land + b * kLandSz + kLandI;
+        if (rk_un) mbar_wait(smem_u32(&mbar[2 + b]), (uint32_t)((k >> 1) & 1));
         double out[2][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            double Lx[2];
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const double* fr = fx + (q * T + cj0 + r) * FXS + ci;
-                const double Fl = fr[0], Fh = fr[1];
-                Lx[r] = -(Fh - Fl) * idx;
-                if (store_mask) {
-                    if (ci == 0 && x_lo && (store_mask & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + cj0 + r] = Fl;
-                    if (ci == T - 1 && x_hi && (store_mask & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + cj0 + r] = Fh;
-                }
+                const int o = (q * T + cj0 + r) * FXS + ci;   // FXS == FYS
+                const double L = dUx[o] + dUy[o];
+                double v = uc[r][q] + dt * L;
+                double* su = sU + (q * T + cj0 + r) * T + ci;
+                if (rk_un) v = ca * *su + cb * v;
+                out[r][q] = v;
+                *su = v;
             }
-            const double* fc = fy + (q * NH + cj0) * FYS + ci;
-            const double F0 = fc[0], F1 = fc[FYS], F2 = fc[2 * FYS];
-            if (store_mask) {
-                if (cj0 == 0 && y_lo && (store_mask & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + q) * N + tx * T + ci] = F0;
-                if (cj0 + 1 == T - 1 && y_hi && (store_mask & 8)) a.freg[(((size_t)d.slot * 4 + kN) * 4 + q) * N + tx * T + ci] = F2;
-            }
-            const double Ly0 = Lx[0] - (F1 - F0) * idy;
-            const double Ly1 = Lx[1] - (F2 - F1) * idy;
-            double v0 = uc[0][q] + dt * Ly0, v1 = uc[1][q] + dt * Ly1;
-            if (rk_un) { v0 = ca * un[0][q] + cb * v0; v1 = ca * un[1][q] + cb * v1; }
-            out[0][q] = v0;
-            out[1][q] = v1;
         }
-        double* po = a.Uout + (size_t)d.slot * PS + base_off;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) __stcs(po + q * NN + r * N, out[r][q]);
             const int j = cj0 + r;
             const bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
                                                  ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
@@ -982,11 +1066,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 }
             }
         }
+        __syncthreads();   // (C) U^(s) of the tile complete in shared memory
+        if (tid == 0) tma_store3(&maps.out_int, tx * T, ty * T, 4 * d.slot, smem_u32(sU));
+        PH_MARK(7);
     }
+    if (tid == 0) bulk_wait0();
     if (a.want_lambda) {
         lam = warp_max_u64(lam);
         if (lane == 0 && lam) atomicMax(a.lambda_bits, lam);
     }
+#ifdef AMR_PHASE_PROF
+    if (prof && lane == 0)
+        for (int p = 0; p < 8; ++p) atomicAdd(&g_phase[warp][p], (unsigned long long)ph_acc[p]);
+#endif
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
@@ -1048,10 +1140,35 @@ cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
         !encode_pool_map(&m.in_we, a.Uin, N, a.nslots, kGL, kTmaT) ||
         !encode_pool_map(&m.in_sn, a.Uin, N, a.nslots, kTmaT, kGL) ||
         !encode_pool_map(&m.px_we, px, N, npx, kGL, kTmaT) ||
-        !encode_pool_map(&m.px_sn, px, N, npx, kTmaT, kGL))
+        !encode_pool_map(&m.px_sn, px, N, npx, kTmaT, kGL) ||
+        !encode_pool_map(&m.un_int, a.Un, N, a.nslots, kTmaT, kTmaT) ||
+        !encode_pool_map(&m.out_int, a.Uout, N, a.nslots, kTmaT, kTmaT))
         return cudaErrorInvalidValue;
     const int grid = ntiles < sm_count() ? ntiles : sm_count();
+#ifdef AMR_PHASE_PROF
+    static const bool prof = getenv("AMR_PHASE_PROF") != nullptr;
+    StageArgs ap = a;
+    ap.prof = prof ? 1 : 0;
+    if (prof) {
+        static unsigned long long zero[16][8] = {};
+        cudaMemcpyToSymbolAsync(g_phase, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s);
+    }
+    stage_c4_tma_kernel<N, DIV4><<<grid, kTmaThreads, kTmaSmem, s>>>(ap, m, ntiles);
+    if (prof) {
+        unsigned long long h[16][8];
+        cudaMemcpyFromSymbolAsync(h, g_phase, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const double per = (double)grid * ((ntiles + grid - 1) / grid);
+        fprintf(stderr, "stage %d phase cycles per tile [top, mbar, c2p, waitA, issue, faces, waitB, epi]:\n", a.stage);
+        for (int w = 0; w < 16; w += 5) {
+            fprintf(stderr, "  w%02d", w);
+            for (int p = 0; p < 8; ++p) fprintf(stderr, " %6.0f", h[w][p] / per);
+            fprintf(stderr, "\n");
+        }
+    }
+#else
     stage_c4_tma_kernel<N, DIV4><<<grid, kTmaThreads, kTmaSmem, s>>>(a, m, ntiles);
+#endif
     return cudaGetLastError();
 }
 
