@@ -25,39 +25,6 @@ namespace {
 
 constexpr int kBcPeriodic = 0, kBcTransmissive = 1, kBcReflective = 2;
 
-__device__ __forceinline__ bool physical_state(double r, double m, double w, double E, double g) {
-    double u = m / r, v = w / r;
-    double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
-    return r > 0.0 && p > 0.0 && isfinite(r) && isfinite(m) && isfinite(w) && isfinite(E) && isfinite(u) &&
-           isfinite(v) && isfinite(p);
-}
-
-__device__ __forceinline__ double wave_speed(double r, double m, double w, double E, double g, double idx,
-                                             double idy) {
-    double ir = 1.0 / r;
-    double u = m * ir, v = w * ir;
-    double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
-    double c = sqrt(g * p * ir);
-    return (fabs(u) + c) * idx + (fabs(v) + c) * idy;
-}
-
-__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = w > v ? w : v;
-    }
-    return v;
-}
-
-__device__ __forceinline__ void report_error(int32_t* err, int slot, int stage, int cell) {
-    if (atomicCAS(err, 0, 1) == 0) {
-        err[1] = slot;
-        err[2] = stage;
-        err[3] = cell;
-    }
-}
-
 // ---------------------------------------------------------------- fast fp64 reciprocal / square root (A41)
 // Branch-free replacements for IEEE division and sqrt on the hot path (no slow-path calls): MUFU seed + Newton
 // steps, <= 1 ulp for the positive normal arguments the scheme produces (rho, c^2, p, WENO weight sums); a
@@ -80,6 +47,39 @@ __device__ __forceinline__ double fast_sqrt(double x) {
     double s = x * y;
     double r = fma(-s, s, x);
     return fma(r, 0.5 * y, s);
+}
+
+__device__ __forceinline__ bool physical_state(double r, double m, double w, double E, double g) {
+    double u = m / r, v = w / r;
+    double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
+    return r > 0.0 && p > 0.0 && isfinite(r) && isfinite(m) && isfinite(w) && isfinite(E) && isfinite(u) &&
+           isfinite(v) && isfinite(p);
+}
+
+__device__ __forceinline__ double wave_speed(double r, double m, double w, double E, double g, double idx,
+                                             double idy) {
+    double ir = fast_rcp(r);
+    double u = m * ir, v = w * ir;
+    double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
+    double c = fast_sqrt(g * p * ir);
+    return (fabs(u) + c) * idx + (fabs(v) + c) * idy;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ void report_error(int32_t* err, int slot, int stage, int cell) {
+    if (atomicCAS(err, 0, 1) == 0) {
+        err[1] = slot;
+        err[2] = stage;
+        err[3] = cell;
+    }
 }
 
 // ---------------------------------------------------------------- reconstruction + flux
