@@ -461,6 +461,24 @@ __device__ __forceinline__ void c4_face(const double (&p)[4], const double (&Tt)
     F[3] = (Ee + pe) * ue;
 }
 
+// The same edge flux scaled by 16 (F16 = 16 F, bit-exactly: every rescaling below is by a power of two): the
+// Eq. 8 weights (9/16, -1/16) become fma(9, inner pair, -outer pair), one operation fewer per variable; the
+// ratio p/T is scale-free, and the caller folds 1/16 into the divergence (idx / 16).
+__device__ __forceinline__ void c4_face16(const double (&p)[4], const double (&Tt)[4], const double (&un)[4],
+                                          const double (&ut)[4], double inv_gm1, double F16[4]) {
+    const double pe = fma(9.0, p[1] + p[2], -(p[0] + p[3]));      // 16 p_e
+    const double Te = fma(9.0, Tt[1] + Tt[2], -(Tt[0] + Tt[3]));  // 16 T_e
+    const double ue = 0.0625 * fma(9.0, un[1] + un[2], -(un[0] + un[3]));
+    const double ve = 0.0625 * fma(9.0, ut[1] + ut[2], -(ut[0] + ut[3]));
+    const double re = pe * fast_rcp(Te);                          // rho_e (scale-free)
+    const double Ee = fma(pe, inv_gm1, (8.0 * re) * fma(ve, ve, ue * ue));   // 16 E_e
+    const double mn = re * ue;
+    F16[0] = 16.0 * mn;
+    F16[1] = fma(16.0 * mn, ue, pe);
+    F16[2] = (16.0 * mn) * ve;
+    F16[3] = (Ee + pe) * ue;
+}
+
 template <int N>
 __global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 32 : N)>::MINB)
     stage_c4_kernel(const StageArgs a) {
@@ -812,7 +830,7 @@ __device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs,
         for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un[c] = un[c + 1]; ut[c] = ut[c + 1]; }
         const int o = (e + 1) * cs;
         p[3] = q[o]; Tt[3] = q[PL + o]; un[3] = q[kn * PL + o]; ut[3] = q[kt * PL + o];
-        c4_face(p, Tt, un, ut, inv_gm1, f[e]);
+        c4_face16(p, Tt, un, ut, inv_gm1, f[e]);   // 16 f
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -978,7 +996,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             double Fh[6][4];
             if (warp < 8) {
                 const int j = 4 * warp + seg_line;
-                const double idx = a.geo.inv_dx[lvl];
+                const double idx = 0.0625 * a.geo.inv_dx[lvl];   // F-hat arrive scaled by 16 (c4_face16)
                 c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
@@ -992,14 +1010,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         for (int e = 0; e < 5; ++e)
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                if (m0 + e == 0 && tx == 0 && (sm & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + j] = Fh[e][q];
-                                if (m0 + e == T && tx == TILES - 1 && (sm & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + j] = Fh[e][q];
+                                if (m0 + e == 0 && tx == 0 && (sm & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + j] = 0.0625 * Fh[e][q];
+                                if (m0 + e == T && tx == TILES - 1 && (sm & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + j] = 0.0625 * Fh[e][q];
                             }
                     }
                 }
             } else {
                 const int i = 4 * (warp - 8) + seg_line;
-                const double idy = a.geo.inv_dy[lvl];
+                const double idy = 0.0625 * a.geo.inv_dy[lvl];
                 c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
@@ -1015,7 +1033,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     if (sm & 12) {
 #pragma unroll
                         for (int e = 0; e < 5; ++e) {
-                            const double Fu[4] = {Fh[e][0], Fh[e][2], Fh[e][1], Fh[e][3]};
+                            const double Fu[4] = {0.0625 * Fh[e][0], 0.0625 * Fh[e][2], 0.0625 * Fh[e][1], 0.0625 * Fh[e][3]};
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 if (m0 + e == 0 && ty == 0 && (sm & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + q) * N + tx * T + i] = Fu[q];
