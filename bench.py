@@ -350,9 +350,6 @@ def main():
                           "states (DESIGN.md s6); throughput config only"}
     if not args.no_amr:
         extra["quadrant_amr"] = measure_quadrant(X, args)
-        if X.world == 1:
-            q = measure_quadrant(X, args, use_graphs=1)
-            extra["quadrant_amr"]["graphs"] = {"value": q["value"], "ms_per_step": q["ms_per_step"]}
     if X.rank == 0:
         rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
               "frac": main_res["achieved_gbs"] / hbm_peak, "traffic": None, "peak_kind": hbm_kind,

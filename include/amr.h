@@ -83,8 +83,8 @@ typedef struct {
     const void* nccl_unique_id;   /* 128-byte ncclUniqueId broadcast by the caller (world_size > 1) */
     int32_t check_positivity;     /* 1: amr_step checks rho, p > 0 and finiteness (default)  */
     int32_t use_graphs;           /* 1: amr_step / amr_steps replay one step as a CUDA graph (captured per position
-                                     of U^n in the RK buffer rotation, re-captured after every mesh change);
-                                     single rank with kernel timing off only, else ignored        */
+                                     of U^n in the RK buffer rotation, once a mesh plan has served 3 steps;
+                                     re-captured after mesh changes); single rank with kernel timing off only */
     int32_t comm_backend;         /* world_size > 1: 0 NCCL (nccl_unique_id = ncclUniqueId); 1 in-process
                                      loopback of virtual ranks on one GPU, one host thread each
                                      (test-only; nccl_unique_id = 128-byte group key string)   */

@@ -188,6 +188,7 @@ amr_status build_plan(amr_ctx* c) {
         CU(c->unf_scratch.reserve(unfused_scratch_doubles(c->n, std::max<int>(1, (int)c->leaves.size()))));
     c->lambda_valid = false;
     c->plan_version++;
+    c->plan_steps = 0;
     c->comm.replan(t);
     return AMR_OK;
 }
@@ -838,7 +839,12 @@ amr_status enqueue_step_graph(amr_ctx* c, double dt, double cfl) {
     return AMR_OK;
 }
 
-bool use_graph(const amr_ctx* c) { return c->cfg.use_graphs && c->cfg.world_size == 1 && !c->timing; }
+// graphs pay off only when a plan is replayed many times: capture once the current plan has served kGraphAfter
+// stream-launched steps (a regrid every few steps would otherwise re-capture all the time)
+constexpr int kGraphAfter = 3;
+bool use_graph(const amr_ctx* c) {
+    return c->cfg.use_graphs && c->cfg.world_size == 1 && !c->timing && c->plan_steps >= kGraphAfter;
+}
 
 amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
     amr_status s = check(c);
@@ -846,6 +852,7 @@ amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
     if (!(dt > 0.0) && !(cfl > 0.0)) return fail(c, AMR_E_ARG, "step: need dt > 0 or cfl > 0");
     int prev = c->un;
     s = use_graph(c) ? enqueue_step_graph(c, dt, cfl) : enqueue_step(c, dt, cfl);
+    c->plan_steps++;
     if (s != AMR_OK) return s;
     if (c->cfg.check_positivity || dt_used) return finish_step(c, prev, dt_used);
     return AMR_OK;
@@ -858,6 +865,7 @@ amr_status amr_steps(amr_ctx* c, int32_t nsteps, double dt, double cfl) {
     for (int k = 0; k < nsteps; ++k) {
         s = use_graph(c) ? enqueue_step_graph(c, dt, cfl) : enqueue_step(c, dt, cfl);
         if (s != AMR_OK) return s;
+        c->plan_steps++;
     }
     return AMR_OK;
 }

@@ -104,6 +104,7 @@ struct amr_ctx {
     // CUDA graphs of one step (use_graphs, single rank): one per position of U^n in the buffer rotation,
     // re-captured when the plan changes
     uint64_t plan_version = 0;
+    int64_t plan_steps = 0;     // steps taken with the current plan
     bool capturing = false;
     cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
     uint64_t gver[3] = {0, 0, 0};

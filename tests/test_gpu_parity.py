@@ -214,8 +214,8 @@ def test_stage_kernel_variants_agree(n, div):
 
 @pytest.mark.parametrize("case", ["quadrant_amr", "vortex_c4"])
 def test_cuda_graph_replay_bitwise(case):
-    """use_graphs = 1 replays one captured step per RK-buffer position (re-captured after each regrid): states,
-    dt and trees bitwise equal to the stream-launched path, for CFL and fixed-dt steps."""
+    """use_graphs = 1 replays one captured step per RK-buffer position once a plan has served 3 steps (re-captured
+    after each regrid): states, dt and trees bitwise equal to the stream-launched path, CFL and fixed-dt steps."""
     if case == "quadrant_amr":
         base = W.quadrant(N=64, n=16, levels=3, seed=2)
     else:
@@ -230,10 +230,11 @@ def test_cuda_graph_replay_bitwise(case):
             g.regrid()
             g.set_state(fn)
         dts = []
-        for s in range(1, 9):
+        for s in range(1, 15):
             dts.append(g.step(cfl=0.5) if s % 3 else g.step(dt=1e-4))
-            if s % 4 == 0:
+            if s % 7 == 0:
                 g.regrid()
+        st = g.stats()
         runs.append((g.get_state(), dts, g.keys()))
     (s0, d0, k0), (s1, d1, k1) = runs
     assert k0 == k1 and d0 == d1
