@@ -53,6 +53,13 @@ def fp64_peak():
     return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SM x 64 DFMA/clk x 2 x 1.965 GHz)"
 
 
+def fp64_work(kernel):
+    """fp64 SASS work per leaf cell-stage of a stage kernel, counted by ncu (profiles/r1c_fp64_work.json)."""
+    p = os.path.join(ROOT, "profiles", "r1c_fp64_work.json")
+    d = json.load(open(p)) if os.path.exists(p) else {}
+    return d.get(kernel, {"fp64_thread_inst_per_cell_stage": float("nan"), "flops_per_cell_stage": float("nan")})
+
+
 class Clocks:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
 
@@ -341,11 +348,19 @@ def main():
         wcfg, _ = sweep_cfg(args, X.world, "weno5", 1)
         wr = measure_sweep(X, args, wcfg, max(3, args.steps // 2), 2, False)
         fpk, fpk_kind = fp64_peak()
+        work = fp64_work("weno5_char")
+        rate = wr["cells_per_launch"] / (wr["stage_avg_ms"] / 1e3)          # cell-stages/s of the stage kernel
+        inst_peak = 148 * 64 * 1.965e9 / 1e12                                  # T fp64 thread-inst/s (unit counts)
         extra["weno5_char"] = {
             "value": wr["value"], "unit": "cell-updates/s", "ms_per_step": wr["ms_per_step"],
-            "roofline": {"bound": "alu", "achieved_hbm_gbs": wr["achieved_gbs"], "hbm_frac": wr["achieved_gbs"] / hbm_peak,
-                         "stage_avg_ms": wr["stage_avg_ms"], "fp64_peak_tflops": fpk, "fp64_peak_kind": fpk_kind,
-                         "note": "fp64 pipe utilisation from ncu in profiles/; DESIGN.md s5"},
+            "roofline": {"bound": "alu", "unit": "T fp64 inst/s",
+                         "achieved": work["fp64_thread_inst_per_cell_stage"] * rate / 1e12, "peak": inst_peak,
+                         "frac": work["fp64_thread_inst_per_cell_stage"] * rate / 1e12 / inst_peak,
+                         "peak_kind": "derived: 148 SM x 64 fp64 lanes x 1.965 GHz (DADD/DMUL/DFMA issue one each)",
+                         "achieved_tflops": work["flops_per_cell_stage"] * rate / 1e12, "fp64_peak_tflops": fpk,
+                         "fp64_peak_kind": fpk_kind, "work_per_cell_stage": work,
+                         "achieved_hbm_gbs": wr["achieved_gbs"], "hbm_frac": wr["achieved_gbs"] / hbm_peak,
+                         "stage_avg_ms": wr["stage_avg_ms"]},
             "positivity": "not held: WENO5-char reconstruction of white noise yields a few non-physical face "
                           "states (DESIGN.md s6); throughput config only"}
     if not args.no_amr:
