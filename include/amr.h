@@ -140,6 +140,14 @@ void amr_destroy(amr_ctx* ctx);
  * ignored.  AMR_E_ARG: bad index. */
 amr_status amr_set_state(amr_ctx* ctx, int32_t npatch, const int32_t* tree_index, const double* U);
 
+/* Initial-condition callback: fill U [4][ncell] (conserved, var-major) at the ncell points (x[c], y[c]). */
+typedef void (*amr_ic_fn)(int32_t ncell, const double* x, const double* y, double* U, void* user);
+
+/* Sample every locally owned active patch (leaves and covered patches) at its cell centres through `fn`
+ * (one call per patch, ncell = n^2 points in [j][i] order), then restrict as amr_set_state does (A33 point
+ * values).  `user` is passed through.  AMR_E_ARG: fn is NULL. */
+amr_status amr_set_state_fn(amr_ctx* ctx, amr_ic_fn fn, void* user);
+
 /* As amr_set_state, with U a DEVICE pointer (e.g. a torch CUDA tensor) on the ctx's device. */
 amr_status amr_set_state_device(amr_ctx* ctx, int32_t npatch, const int32_t* tree_index, const double* dU);
 

@@ -27,7 +27,7 @@ COARSEN = {"r2_exact": 0, "alg2_literal": 1}
 
 # every symbol include/amr.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["amr_abi_version", "amr_default_config", "amr_query_pool_bytes", "amr_create", "amr_destroy",
-               "amr_set_state", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
+               "amr_set_state", "amr_set_state_fn", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
                "amr_regrid", "amr_regrid_with_flags", "amr_get_patch_tree", "amr_diagnostics",
                "amr_set_kernel_timing", "amr_get_stats", "amr_reset_stats", "amr_nccl_unique_id",
                "amr_last_error"]
@@ -61,6 +61,7 @@ class amr_stats(C.Structure):
 
 _lib = None
 _P = C.c_void_p
+IC_FN = C.CFUNCTYPE(None, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
 _D = C.POINTER(C.c_double)
 _I32 = C.POINTER(C.c_int32)
 _U8 = C.POINTER(C.c_uint8)
@@ -82,6 +83,7 @@ def load(path: str = LIB_PATH):
     L.amr_destroy.argtypes = [_P]
     L.amr_destroy.restype = None
     L.amr_set_state.argtypes = [_P, C.c_int32, _I32, _D]
+    L.amr_set_state_fn.argtypes = [_P, IC_FN, C.c_void_p]
     L.amr_get_state.argtypes = [_P, C.c_int32, _I32, _D]
     L.amr_set_state_device.argtypes = [_P, C.c_int32, _I32, C.c_void_p]
     L.amr_get_state_device.argtypes = [_P, C.c_int32, _I32, C.c_void_p]
@@ -247,6 +249,17 @@ class Mesh:
         U = np.ascontiguousarray(U, dtype=np.float64)
         assert U.shape[0] == len(idx)
         self._chk(self.L.amr_set_state(self.h, len(idx), idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
+
+    def set_state_points(self, fn):
+        """Set every owned patch through the C callback amr_set_state_fn: fn(x, y) -> (rho, rho u, rho v, rho e)
+        arrays at the given cell centres (x, y: 1D float64 arrays of one patch's n^2 points)."""
+        def cb(ncell, x, y, U, _user):
+            xs = np.ctypeslib.as_array(x, shape=(ncell,))
+            ys = np.ctypeslib.as_array(y, shape=(ncell,))
+            out = np.ctypeslib.as_array(U, shape=(4 * ncell,))
+            out[:] = np.asarray(fn(xs, ys), dtype=np.float64).reshape(-1)
+        c_cb = IC_FN(cb)   # kept alive for the duration of the call
+        self._chk(self.L.amr_set_state_fn(self.h, c_cb, None))
 
     def set_state_device(self, tensor, indices=None):
         """Set patches (default: every patch, tree order) from a contiguous CUDA float64 tensor [k][4][n][n]."""

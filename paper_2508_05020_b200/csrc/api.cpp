@@ -685,6 +685,32 @@ static amr_status select_local(amr_ctx* c, int32_t npatch, const int32_t* tree_i
     return AMR_OK;
 }
 
+amr_status amr_set_state_fn(amr_ctx* c, amr_ic_fn fn, void* user) {
+    amr_status s = check(c);
+    if (s != AMR_OK) return s;
+    if (!fn) return fail(c, AMR_E_ARG, "set_state_fn: null callback");
+    // every locally owned active patch (leaves and covered patches), sampled at its cell centres (A33)
+    const PatchTree& t = c->tree;
+    const int n = c->n;
+    const size_t PS = c->PS, nn = (size_t)n * n;
+    std::vector<int32_t> idx;
+    for (size_t e = 0; e < c->canon.size(); ++e)
+        if (c->comm.owns(c, c->canon[e])) idx.push_back((int32_t)e);
+    std::vector<double> U(idx.size() * PS), x(nn), y(nn);
+    for (size_t k = 0; k < idx.size(); ++k) {
+        const int id = c->canon[idx[k]];
+        const int l = t.lev[id];
+        const double dx = c->geo.dx[l], dy = c->geo.dy[l];
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+                x[(size_t)j * n + i] = c->cfg.lo[0] + ((double)t.pi[id] * n + i + 0.5) * dx;
+                y[(size_t)j * n + i] = c->cfg.lo[1] + ((double)t.pj[id] * n + j + 0.5) * dy;
+            }
+        fn((int32_t)nn, x.data(), y.data(), U.data() + k * PS, user);
+    }
+    return amr_set_state(c, (int32_t)idx.size(), idx.data(), U.data());
+}
+
 amr_status amr_set_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, const double* U) {
     amr_status s = check(c);
     if (s != AMR_OK) return s;

@@ -277,3 +277,29 @@ def test_weno_amr_unfused_and_per_patch(variant, char):
     """The NEXT #1 organisations on the WENO5 path with AMR (quadrant, 3 levels, regrids): oracle parity."""
     cfg = W.quadrant(N=64, n=16, levels=3, seed=1, stage_kernel=variant, characteristic=char)
     run_pair(cfg, steps=6, cfl=0.5, regrid_every=3)
+
+
+def test_set_state_fn_matches_patch_arrays():
+    """amr_set_state_fn samples the IC at cell centres (A33) through a C callback; on a 3-level mesh it equals
+    set_state with the same IC evaluated per patch in numpy (workloads.patch_state)."""
+    cfg = W.quadrant(N=64, n=16, levels=3, seed=2, ic="vortex", vortex_centre=(0.5, 0.5), hi=(1.0, 1.0))
+    cfg["vortex_beta"] = 5.0
+    g1 = amr.Mesh(cfg)
+    fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
+    g1.set_state(fn)
+    g1.regrid_with_requests([(0, 1, 1), (0, 2, 2)])
+    g1.regrid_with_requests([(1, 3, 3)])
+    g2 = amr.Mesh(cfg)
+    g2.set_state(fn)
+    g2.regrid_with_requests([(0, 1, 1), (0, 2, 2)])
+    g2.regrid_with_requests([(1, 3, 3)])
+    g1.set_state(fn)
+
+    def pts(x, y):
+        rho, u, v, p = W.vortex_prim(cfg, x, y)
+        return W.to_conserved(rho, u, v, p, cfg["gamma"])
+    g2.set_state_points(pts)
+    s1, s2 = g1.get_state(), g2.get_state()
+    assert set(s1) == set(s2)
+    for k in s1:
+        np.testing.assert_allclose(s2[k], s1[k], rtol=0, atol=1e-14 * np.abs(s1[k]).max())
