@@ -1,0 +1,132 @@
+"""Full-size GPU parity: BASELINE.json configs at their stated sizes, run through the C ABI in the launch
+configuration bench.py times (persistent TMA Central4 kernel for 32^2 / 64^2 patches, WENO5-char stage kernel),
+checked against the oracle to 1e-11 (O18 / A31 metric, tests/parity.py).
+
+- configs[4] sweep, 4096^2 noise field (bench's headline workload): one SSP-RK3 step with bench's fixed dt
+  (CFL 0.3 of Lambda(U^0)), sampled patches compared with the oracle run on the patch's 3 x 3 neighbourhood cut
+  from the same field as a periodic 3n x 3n block.  The block's wrap contaminates a band growing 4 cells per stage
+  from its edge (12 cells after one step), so the centre patch is exact.  Corner patches cover the domain wrap.
+- configs[1] vortex, 1024^2 Central4: the whole oracle mesh, 10 CFL-0.5 steps.  WENO5-char: sampled blocks.
+- configs[2] quadrant, 512^2 base, 3 levels, WENO5-char: lockstep with regrids (A32), 6 steps.
+- configs[3] shock-bubble, 2048 x 1024 base, 4 levels, reflective walls: init protocol (A28) + 2 steps lockstep.
+"""
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2508_05020_b200 as amr
+import workloads as W
+from tests.parity import parity_error, run_pair
+
+pytestmark = pytest.mark.gpu
+
+
+def block_oracle(cfg, P, Q, dt, steps=1):
+    """Oracle result for patch (P, Q) of a 1-level periodic cfg after `steps` fixed-dt steps, computed on its
+    periodic 3 x 3 patch neighbourhood."""
+    n = cfg["n"]
+    NPx, NPy = cfg["base"][0] // n, cfg["base"][1] // n
+    dx = (cfg["hi"][0] - cfg["lo"][0]) / cfg["base"][0]
+    dy = (cfg["hi"][1] - cfg["lo"][1]) / cfg["base"][1]
+    sub = dict(cfg, base=(3 * n, 3 * n), lo=(0.0, 0.0), hi=(3 * n * dx, 3 * n * dy), levels=1,
+               bc=("periodic",) * 4)
+    o = orc.Oracle(sub)
+    o.set_state(lambda l, p, q: W.patch_state(cfg, 0, (P - 1 + p) % NPx, (Q - 1 + q) % NPy))
+    for _ in range(steps):
+        o.step(dt=dt)
+    return o.get_patch((0, 1, 1))
+
+
+def sampled_parity(cfg, samples, steps=1, cfl=0.3):
+    n = cfg["n"]
+    NPx = cfg["base"][0] // n
+    g = amr.Mesh(cfg)
+    g.set_state(U=W.level0_state(cfg).reshape(-1, 4, n, n))
+    _, lam = g.diagnostics()
+    dt = cfl / lam
+    for _ in range(steps):
+        g.step(dt=dt)
+    keys = [(0, P, Q) for (P, Q) in samples]
+    idx = np.array([Q * NPx + P for (P, Q) in samples], np.int32)   # tree order of a 1-level mesh is (Q, P)
+    Ug = g.get_state(as_dict=False, indices=idx)
+    so = {k: block_oracle(cfg, k[1], k[2], dt, steps) for k in keys}
+    sg = {k: Ug[e] for e, k in enumerate(keys)}
+    e, rel = parity_error(so, sg)
+    assert e <= 1e-11, (e, rel)
+    return e
+
+
+def _samples(NPx, NPy, k=6, seed=0):
+    rng = np.random.default_rng(seed)
+    s = {(0, 0), (NPx - 1, NPy - 1), (0, NPy - 1)}
+    while len(s) < k:
+        s.add((int(rng.integers(NPx)), int(rng.integers(NPy))))
+    return sorted(s)
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_sweep_4096_central4_sampled(n):
+    """configs[4] at 4096^2 with bench's kernel (stage_c4_tma_kernel), check off as in bench."""
+    cfg = W.sweep(N=4096, n=n, scheme="central4", seed=7)
+    cfg["check_positivity"] = 0
+    sampled_parity(cfg, _samples(4096 // n, 4096 // n))
+
+
+def test_vortex_1024_central4_full_oracle():
+    """configs[1]: 1024^2 periodic vortex, 32^2 patches, 10 CFL-0.5 steps, the whole mesh against the oracle."""
+    run_pair(W.vortex(N=1024, n=32), steps=10, cfl=0.5)
+
+
+def test_vortex_1024_weno_sampled():
+    """configs[1] WENO5-char variant: one step, sampled 3 x 3 blocks."""
+    cfg = W.vortex(N=1024, n=32, scheme="weno5", characteristic=1)
+    sampled_parity(cfg, _samples(32, 32, k=5, seed=1), cfl=0.5)
+
+
+def test_quadrant_512_three_levels_lockstep():
+    """configs[2] at full size: 512^2 base, 3 levels, 16^2 patches, WENO5-char, regrids in lockstep (A32)."""
+    stats = {}
+    o, g, e = run_pair(W.quadrant(N=512, n=16, levels=3, seed=1), steps=6, cfl=0.5, regrid_every=3, stats=stats)
+    assert len({k[0] for k in g.leaves()}) == 3
+
+
+def test_shock_bubble_full_size_lockstep():
+    """configs[3] at full size: 2048 x 1024 base, 4 levels, reflective walls, init protocol + 2 steps."""
+    o, g, e = run_pair(W.shock_bubble(), steps=2, cfl=0.5)
+    assert len({k[0] for k in g.leaves()}) == 4
+
+
+@pytest.mark.parametrize("n", [8, 64])
+def test_sweep_16384_maximum_size_tiling_invariance(n):
+    """configs[4] maximum size, 16384^2 (4.19 M patches at n = 8): the 4096^2 noise field tiled 4 x 4 is a valid
+    periodic state of the big domain, and the scheme is translation invariant, so one step on 16384^2 must equal
+    the 4096^2 step tiled, bit for bit (the 4096^2 step is itself oracle-checked above).  Same dt on both."""
+    import torch
+    small = W.sweep(N=4096, n=n, scheme="central4", seed=7)
+    small["check_positivity"] = 0
+    big = W.sweep(N=16384, n=n, scheme="central4", seed=7)
+    big.update(check_positivity=0, hi=(4.0, 4.0))          # same dx as the 4096^2 domain on [0, 1]^2
+    NP = 4096 // n
+    U0 = torch.from_numpy(W.level0_state(small)).cuda()    # [NP][NP][4][n][n]
+    gs = amr.Mesh(small)
+    gs.set_state_device(U0.reshape(-1, 4, n, n))
+    _, lam = gs.diagnostics()
+    dt = 0.3 / lam
+    gs.step(dt=dt)
+    Us = torch.empty_like(U0.reshape(-1, 4, n, n))
+    gs.get_state_device(Us)
+    gs.close()
+    gb = amr.Mesh(big)
+    gb.set_state_device(U0.repeat(4, 4, 1, 1, 1).reshape(-1, 4, n, n))
+    del U0
+    _, lam_b = gb.diagnostics()
+    assert lam_b == lam
+    gb.step(dt=dt)
+    Ub = torch.empty((16 * NP * NP, 4, n, n), dtype=torch.float64, device="cuda")
+    gb.get_state_device(Ub)
+    gb.close()
+    Ub = Ub.view(4, NP, 4, NP, 4, n, n)
+    Us = Us.view(NP, NP, 4, n, n)
+    for a in range(4):
+        for b in range(4):
+            assert torch.equal(Ub[a, :, b], Us), (a, b)
