@@ -281,6 +281,48 @@ def measure_sweep(X, args, cfg, steps, warmup, do_e2e):
     return res
 
 
+def measure_sweep_table(X, args, hbm_peak):
+    """BASELINE configs[4] as stated: totals 4096^2, 8192^2, 16384^2 x patches 8/16/32/64 (Central4, one GPU).
+    The 4096^2 noise field of each patch size is generated once and tiled periodically on the device for the
+    larger totals (a valid periodic state with the same statistics); per configuration the fused stage kernel's
+    CUDA-event time over 3 steps after 1 warm-up step, each step from the pristine state."""
+    torch = X.torch
+    rows = []
+    for n in (8, 16, 32, 64):
+        small = W.sweep(N=4096, n=n, scheme="central4", seed=7)
+        U0 = torch.from_numpy(W.level0_state(small)).cuda()
+        for N in (4096, 8192, 16384):
+            r = N // 4096
+            cfg = W.sweep(N=N, n=n, scheme="central4", seed=7)
+            cfg.update(check_positivity=0, stage_kernel=args.stage_kernel)
+            mesh = X.mesh(cfg)
+            Ut = U0.repeat(r, r, 1, 1, 1).reshape(-1, 4, n, n).contiguous()
+            torch.cuda.synchronize()   # Ut is written on torch's stream; the library reads it on its own
+            idx = np.arange(Ut.shape[0], dtype=np.int32)
+            mesh.set_state_device(Ut, indices=idx)
+            _, lam = mesh.diagnostics()
+            dt = args.cfl / lam
+            mesh.steps(1, dt=dt)
+            mesh.reset_stats()
+            mesh.set_kernel_timing(True)
+            for _ in range(3):
+                mesh.set_state_device(Ut, indices=idx)
+                mesh.steps(1, dt=dt)
+            torch.cuda.synchronize()
+            st = mesh.stats()
+            mesh.set_kernel_timing(False)
+            mesh.close()
+            del Ut
+            ms = st["stage_ms"] / max(1, st["stage_timed"])
+            cells = st["stage_cells"] / max(1, st["stage_timed"])
+            gbs = st["stage_bytes"] / max(1, st["stage_timed"]) / (ms / 1e3) / 1e9
+            rows.append({"N": N, "n": n, "stage_ms": ms, "cell_updates_per_s": cells / (ms / 1e3),
+                         "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak})
+        del U0
+        torch.cuda.empty_cache()
+    return rows
+
+
 def measure_quadrant(X, args, use_graphs=0):
     """BASELINE configs[2]: quadrant Riemann problem, 512^2 base, 3 levels, WENO5-char, regrid every 4 steps.
     Timed: K steps including the regrids (flags, Alg. 1/2, prolongation, migration) inside the region.
@@ -335,6 +377,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weno", action="store_true")
     ap.add_argument("--no-amr", action="store_true")
+    ap.add_argument("--sweep-table", action="store_true", help="add the configs[4] size x patch-size table")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -365,6 +408,9 @@ def main():
                           "states (DESIGN.md s6); throughput config only"}
     if not args.no_amr:
         extra["quadrant_amr"] = measure_quadrant(X, args)
+    if args.sweep_table and X.world == 1:
+        extra["sweep_table"] = {"workload": "BASELINE configs[4]: Central4 stage kernel per total size and patch size",
+                                "rows": measure_sweep_table(X, args, hbm_peak)}
     if X.rank == 0:
         rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
               "frac": main_res["achieved_gbs"] / hbm_peak, "traffic": None, "peak_kind": hbm_kind,
