@@ -1,3 +1,4 @@
+#include <chrono>
 // api.cpp -- the C ABI of include/amr.h: context, host plan (descriptor build from
 // the patch tree), step driver, regrid, state I/O, diagnostics and statistics.
 // Every step of the numerical path runs in the kernels of kernels.cu; the host
@@ -75,23 +76,43 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
 }
 
 // ------------------------------------------------------------------ plan
+// host-side regrid phase timing (AMR_REGRID_PROF=1 in the environment; stderr)
+struct PhaseClock {
+    bool on = getenv("AMR_REGRID_PROF") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  [regrid] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 amr_status build_plan(amr_ctx* c) {
+    PhaseClock clk;
     PatchTree& t = c->tree;
     const int L = c->cfg.num_levels;
+    // id -> position maps sized once; the previous plan's entries are cleared instead of refilling all slots
+    if ((int)c->canon_pos.size() != t.capacity) c->canon_pos.assign(t.capacity, -1);
+    else for (int id : c->canon) c->canon_pos[id] = -1;
+    if ((int)c->leaf_pos.size() != t.capacity) c->leaf_pos.assign(t.capacity, -1);
+    else for (int id : c->leaf_ids) c->leaf_pos[id] = -1;
     c->canon = t.canonical();
-    c->canon_pos.assign(t.capacity, -1);
     for (size_t e = 0; e < c->canon.size(); ++e) c->canon_pos[c->canon[e]] = (int)e;
 
     // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos
     c->leaf_ids.clear();
     for (int id : c->canon)
         if (t.is_leaf(id) && c->comm.owns(c, id)) c->leaf_ids.push_back(id);
-    std::stable_sort(c->leaf_ids.begin(), c->leaf_ids.end(), [&](int a, int b) {
-        if (t.lev[a] != t.lev[b]) return t.lev[a] < t.lev[b];
-        return morton(t.pi[a], t.pj[a]) < morton(t.pi[b], t.pj[b]);
-    });
-    c->leaf_pos.assign(t.capacity, -1);
+    {   // (level, Morton key) computed once per leaf, then one sort of (key, id) pairs
+        std::vector<std::pair<std::pair<int32_t, uint64_t>, int32_t>> kv;
+        kv.reserve(c->leaf_ids.size());
+        for (int id : c->leaf_ids) kv.push_back({{t.lev[id], morton(t.pi[id], t.pj[id])}, id});
+        std::sort(kv.begin(), kv.end());
+        for (size_t e = 0; e < kv.size(); ++e) c->leaf_ids[e] = kv[e].second;
+    }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
+    clk.mark("plan: canon + leaf order");
 
     static const int dirs[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
     c->leaves.clear();
@@ -165,6 +186,7 @@ amr_status build_plan(amr_ctx* c) {
         c->rlev[t.lev[id] + 1].push_back(r);
     }
     c->leaf_cells = (int64_t)c->leaf_ids.size() * c->n * c->n;
+    clk.mark("plan: descriptors");
 
     cudaStream_t s = c->stream;
     CU(c->d_leaves.upload(c->leaves, s));
@@ -178,6 +200,7 @@ amr_status build_plan(amr_ctx* c) {
     CU(c->d_amb.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_partial.reserve(4 * std::max<size_t>(1, c->leaves.size())));
     CU(cudaStreamSynchronize(s));   // host vectors may change after return
+    clk.mark("plan: uploads");
 
     c->st.leaves = 0;
     for (int id : c->canon) c->st.leaves += t.is_leaf(id);
@@ -408,15 +431,21 @@ amr_status evaluate_flags(amr_ctx* c) {
     }
     CU(cudaStreamSynchronize(c->stream));
     PatchTree& t = c->tree;
-    std::vector<double> eta(t.capacity, std::nan(""));
-    std::vector<uint8_t> amb(t.capacity, 0);
+    // per-id arrays sized once to the slot capacity; only the entries of active patches are (re)written and read
+    std::vector<double>& eta = c->fl_eta_raw;
+    std::vector<uint8_t>& amb = c->fl_amb_raw;
+    if ((int)eta.size() != t.capacity) { eta.assign(t.capacity, std::nan("")); amb.assign(t.capacity, 0); }
+    for (int id : c->canon) { eta[id] = std::nan(""); amb[id] = 0; }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) { eta[c->leaf_ids[e]] = me[e]; amb[c->leaf_ids[e]] = (uint8_t)am[e]; }
     s = c->comm.allgather_flags(c, eta, amb);
     if (s != AMR_OK) return s;
-    c->fl_eta.assign(t.capacity, std::nan(""));
-    c->fl_ref.assign(t.capacity, 0);
-    c->fl_crs.assign(t.capacity, 0);
-    c->fl_amb.assign(t.capacity, 0);
+    if ((int)c->fl_eta.size() != t.capacity) {
+        c->fl_eta.assign(t.capacity, std::nan(""));
+        c->fl_ref.assign(t.capacity, 0);
+        c->fl_crs.assign(t.capacity, 0);
+        c->fl_amb.assign(t.capacity, 0);
+    }
+    for (int id : c->canon) { c->fl_eta[id] = std::nan(""); c->fl_ref[id] = c->fl_crs[id] = c->fl_amb[id] = 0; }
     const double th = c->cfg.refine_threshold, tc = th * c->cfg.coarsen_fraction;
     for (int id : c->canon) {
         if (t.is_leaf(id)) {
@@ -446,11 +475,14 @@ amr_status evaluate_flags(amr_ctx* c) {
 // refinement pass, coarsening pass, validation, new-patch prolongation, restriction
 amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::vector<uint8_t>& crs, int32_t* nr,
                         int32_t* nc) {
-    PatchTree nt = c->tree;
+    PhaseClock clk;
+    PatchTree& nt = c->tree;   // modified in place inside a transaction (rolled back on any failure)
+    nt.begin_txn();
     std::string m;
     for (int id : c->canon) {
         if (!ref[id] || !nt.is_leaf(id) || nt.lev[id] >= c->cfg.num_levels - 1) continue;
         if (!nt.refine(id, m)) {
+            nt.rollback();
             amr_status s = m.find("capacity") != std::string::npos ? AMR_E_CAPACITY : AMR_E_MESH;
             return fail(c, s, "regrid: " + m + " (mesh unchanged)");
         }
@@ -460,25 +492,37 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
             if (nt.lev[id] != l || !crs[id] || !nt.alive[id]) continue;
             if (nt.coarsen_allowed(id)) nt.delete_children(id);
         }
-    if (!nt.validate(m)) return fail(c, AMR_E_MESH, "regrid produced an invalid mesh: " + m);
+    clk.mark("refine + coarsen");
+    if (!nt.validate(m)) {
+        nt.rollback();
+        return fail(c, AMR_E_MESH, "regrid produced an invalid mesh: " + m);
+    }
+    clk.mark("validate");
     int n_new = 0, n_del = 0;
     const int W = c->comm.world, R = c->comm.rank;
+    std::vector<uint8_t> is_new(nt.capacity, 0);
+    std::vector<int32_t> new_ids;
+    for (const auto& sn : nt.journal()) {   // created / deleted slots, from the transaction journal
+        if (nt.alive[sn.id] && !sn.alive) { is_new[sn.id] = 1; new_ids.push_back(sn.id); ++n_new; }
+        if (!nt.alive[sn.id] && sn.alive) ++n_del;
+    }
+    std::sort(new_ids.begin(), new_ids.end());
+    nt.commit();
     // ownership of the new tree under the OLD partition (roots never change): the old owner of a
     // root prolongs the new patches of that root, since it holds their parents' data
-    std::vector<int32_t> old_owner(nt.capacity, -1);
-    std::vector<uint8_t> is_new(nt.capacity, 0);
-    for (int id = 0; id < nt.capacity; ++id) {
-        if (!nt.alive[id]) continue;
-        int l = nt.lev[id];
-        int root = nt.find(0, nt.pi[id] >> l, nt.pj[id] >> l);
-        old_owner[id] = W == 1 ? 0 : c->comm.owner[root];
-        if (!c->tree.alive[id]) { is_new[id] = 1; ++n_new; }
+    std::vector<int32_t> old_owner;
+    if (W > 1) {
+        old_owner.assign(nt.capacity, -1);
+        for (int id = 0; id < nt.capacity; ++id) {
+            if (!nt.alive[id]) continue;
+            int l = nt.lev[id];
+            int root = nt.find(0, nt.pi[id] >> l, nt.pj[id] >> l);
+            old_owner[id] = c->comm.owner[root];
+        }
     }
-    for (int id = 0; id < nt.capacity; ++id)
-        if (c->tree.alive[id] && !nt.alive[id]) ++n_del;
     std::vector<std::vector<ProlongTask>> pro(c->cfg.num_levels);
-    for (int id = 0; id < nt.capacity; ++id) {
-        if (!is_new[id] || old_owner[id] != (W == 1 ? 0 : R)) continue;
+    for (int id : new_ids) {
+        if (W > 1 && old_owner[id] != R) continue;
         ProlongTask p{};
         p.slot = id;
         p.level = nt.lev[id];
@@ -493,10 +537,11 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
             }
         pro[p.level].push_back(p);
     }
-    c->tree = nt;
+    clk.mark("new patches / owners");
     if (W > 1) c->comm.owner = old_owner;
     amr_status s = build_plan(c);
     if (s != AMR_OK) return s;
+    clk.mark("build_plan");
     double* Un = c->U[c->un];
     for (int l = 1; l < c->cfg.num_levels; ++l) {
         if (W > 1) {
@@ -512,6 +557,7 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     }
     s = restrict_all(c, Un);
     if (s != AMR_OK) return s;
+    clk.mark("prolong + restrict");
     if (W > 1) {
         // repartition the new tree and migrate every patch whose owner changed
         std::vector<int32_t> new_owner = partition_owners(nt, W);
@@ -524,12 +570,11 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     }
     CU(cudaStreamSynchronize(c->stream));
     c->lambda_valid = false;
-    c->fl_ref.assign(nt.capacity, 0);
-    c->fl_crs.assign(nt.capacity, 0);
-    c->fl_amb.assign(nt.capacity, 0);
-    c->fl_eta.assign(nt.capacity, std::nan(""));
+    if ((int)c->fl_eta.size() == nt.capacity)   // no requests on the new mesh until the next flag evaluation
+        for (int id : c->canon) { c->fl_eta[id] = std::nan(""); c->fl_ref[id] = c->fl_crs[id] = c->fl_amb[id] = 0; }
     if (nr) *nr = n_new;
     if (nc) *nc = n_del;
+    clk.mark("finish");
     return AMR_OK;
 }
 
@@ -921,8 +966,10 @@ amr_status amr_get_flags(amr_ctx* c, int32_t cap, double* maxeta, uint8_t* bits)
 amr_status amr_regrid(amr_ctx* c, int32_t* n_refined, int32_t* n_coarsened) {
     amr_status s = check(c);
     if (s != AMR_OK) return s;
+    PhaseClock clk;
     s = evaluate_flags(c);
     if (s != AMR_OK) return s;
+    clk.mark("flags");
     std::vector<uint8_t> ref = c->fl_ref, crs = c->fl_crs;
     return apply_regrid(c, ref, crs, n_refined, n_coarsened);
 }

@@ -18,10 +18,10 @@ struct DevArray {
     size_t cap = 0, count = 0;
     cudaError_t upload(const std::vector<T>& v, cudaStream_t s) {
         count = v.size();
-        if (v.size() > cap) {
+        if (v.size() > cap) {   // grow with 50 % slack: regrids that add a few patches do not reallocate
             if (p) cudaFree(p);
             p = nullptr;
-            cap = std::max<size_t>(v.size(), 16);
+            cap = std::max<size_t>(v.size() + v.size() / 2, 16);
             cudaError_t e = cudaMalloc(&p, cap * sizeof(T));
             if (e != cudaSuccess) { cap = 0; return e; }
         }
@@ -40,11 +40,17 @@ struct DevArray {
     void release() { if (p) cudaFree(p); p = nullptr; cap = count = 0; }
 };
 
-inline uint64_t morton(uint32_t x, uint32_t y) {
-    uint64_t r = 0;
-    for (int b = 0; b < 32; ++b) r |= (uint64_t((x >> b) & 1u) << (2 * b)) | (uint64_t((y >> b) & 1u) << (2 * b + 1));
-    return r;
+// bit interleave x0 y0 x1 y1 ... (Morton / Z order) by magic-number spreading
+inline uint64_t spread_bits(uint32_t v) {
+    uint64_t x = v;
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
 }
+inline uint64_t morton(uint32_t x, uint32_t y) { return spread_bits(x) | (spread_bits(y) << 1); }
 
 }  // namespace amr
 
@@ -93,6 +99,8 @@ struct amr_ctx {
     // flags of the last evaluation, per id
     std::vector<uint8_t> fl_ref, fl_crs, fl_amb;
     std::vector<double> fl_eta;
+    std::vector<double> fl_eta_raw;    // per-leaf indicator gathered from the device (scratch)
+    std::vector<uint8_t> fl_amb_raw;
 
     // stats / timing
     amr_stats st{};

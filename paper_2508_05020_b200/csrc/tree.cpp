@@ -29,10 +29,49 @@ void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, 
         for (int i = 0; i < npx; ++i) alloc(0, i, j);
 }
 
+void PatchTree::touch(int id) {
+    if (!txn_ || touched_[id]) return;
+    touched_[id] = 1;
+    SlotSnap sn{id, lev[id], pi[id], pj[id], parent[id], {child[4 * id], child[4 * id + 1], child[4 * id + 2], child[4 * id + 3]},
+                alive[id]};
+    journal_.push_back(sn);
+}
+
+void PatchTree::begin_txn() {
+    journal_.clear();
+    if ((int)touched_.size() != capacity) touched_.assign(capacity, 0);
+    txn_ = true;
+}
+
+void PatchTree::commit() {
+    for (const auto& sn : journal_) touched_[sn.id] = 0;
+    txn_ = false;
+}
+
+void PatchTree::rollback() {
+    for (const auto& sn : journal_)
+        if (alive[sn.id]) { index_.erase(key(lev[sn.id], pi[sn.id], pj[sn.id])); --n_alive; }
+    for (auto it = journal_.rbegin(); it != journal_.rend(); ++it) {
+        const SlotSnap& sn = *it;
+        lev[sn.id] = sn.lev; pi[sn.id] = sn.pi; pj[sn.id] = sn.pj; parent[sn.id] = sn.parent; alive[sn.id] = sn.alive;
+        for (int c = 0; c < 4; ++c) child[4 * sn.id + c] = sn.child[c];
+    }
+    for (const auto& sn : journal_)
+        if (sn.alive) { index_[key(sn.lev, sn.pi, sn.pj)] = sn.id; ++n_alive; }
+    free_.clear();   // rare path: rebuild the free-slot heap
+    for (int s = 0; s < capacity; ++s)
+        if (!alive[s]) free_.push_back(s);
+    std::make_heap(free_.begin(), free_.end(), std::greater<int32_t>());
+    for (const auto& sn : journal_) touched_[sn.id] = 0;
+    journal_.clear();
+    txn_ = false;
+}
+
 int PatchTree::alloc(int l, int i, int j) {
     std::pop_heap(free_.begin(), free_.end(), std::greater<int32_t>());
     int id = free_.back();
     free_.pop_back();
+    touch(id);
     lev[id] = l; pi[id] = i; pj[id] = j; parent[id] = -1; alive[id] = 1;
     for (int c = 0; c < 4; ++c) child[4 * id + c] = -1;
     index_[key(l, i, j)] = id;
@@ -41,6 +80,7 @@ int PatchTree::alloc(int l, int i, int j) {
 }
 
 void PatchTree::release(int id) {
+    touch(id);
     index_.erase(key(lev[id], pi[id], pj[id]));
     alive[id] = 0; lev[id] = -1; parent[id] = -1;
     for (int c = 0; c < 4; ++c) child[4 * id + c] = -1;
@@ -86,6 +126,7 @@ bool PatchTree::refine(int id, std::string& err) {
         if (!refine(r, err)) return false;
     }
     if ((int)free_.size() < 4) { err = "slot capacity exceeded"; return false; }
+    touch(id);
     for (int c = 0; c < 4; ++c) {
         int a = c & 1, b = c >> 1;
         int k = alloc(l + 1, 2 * pi[id] + a, 2 * pj[id] + b);
@@ -121,6 +162,7 @@ bool PatchTree::coarsen_allowed(int id) const {
 }
 
 void PatchTree::delete_children(int id) {
+    touch(id);
     for (int c = 0; c < 4; ++c) {
         int k = child[4 * id + c];
         if (k >= 0) release(k);
@@ -132,8 +174,9 @@ bool PatchTree::validate(std::string& err) const {
     for (int j = 0; j < np0[1]; ++j)
         for (int i = 0; i < np0[0]; ++i)
             if (find(0, i, j) < 0) { err = "R1 violated: root missing"; return false; }
-    for (int id = 0; id < capacity; ++id) {
-        if (!alive[id]) continue;
+    for (const auto& kv : index_) {   // the active patches (O(active), not O(capacity))
+        const int id = kv.second;
+        if (!alive[id]) { err = "index refers to a free slot"; return false; }
         if (lev[id] > 0) {
             int p = parent[id];
             if (p < 0 || !alive[p]) { err = "orphan patch"; return false; }
@@ -150,15 +193,13 @@ bool PatchTree::validate(std::string& err) const {
 }
 
 std::vector<int32_t> PatchTree::canonical() const {
-    std::vector<int32_t> ids;
-    ids.reserve(n_alive);
+    std::vector<std::pair<uint64_t, int32_t>> kv;   // key (level, j, i) = the map key: one sort of pairs
+    kv.reserve(n_alive);
     for (int id = 0; id < capacity; ++id)
-        if (alive[id]) ids.push_back(id);
-    std::sort(ids.begin(), ids.end(), [&](int a, int b) {
-        if (lev[a] != lev[b]) return lev[a] < lev[b];
-        if (pj[a] != pj[b]) return pj[a] < pj[b];
-        return pi[a] < pi[b];
-    });
+        if (alive[id]) kv.push_back({key(lev[id], pi[id], pj[id]), id});
+    std::sort(kv.begin(), kv.end());
+    std::vector<int32_t> ids(kv.size());
+    for (size_t e = 0; e < kv.size(); ++e) ids[e] = kv[e].second;
     return ids;
 }
 

@@ -48,7 +48,23 @@ struct PatchTree {
     // ids of active patches in canonical order (level, j, i)
     std::vector<int32_t> canonical() const;
 
+    // Transactions (regrid is atomic): between begin_txn() and commit()/rollback() every modified slot
+    // is journaled once with its prior state, so a failed regrid is undone in O(changes) -- no copy of the
+    // capacity-sized arrays -- and the journal tells which slots were created or deleted.
+    struct SlotSnap {
+        int32_t id, lev, pi, pj, parent, child[4];
+        uint8_t alive;
+    };
+    void begin_txn();
+    void commit();
+    void rollback();
+    const std::vector<SlotSnap>& journal() const { return journal_; }
+
   private:
+    std::vector<SlotSnap> journal_;
+    std::vector<uint8_t> touched_;
+    bool txn_ = false;
+    void touch(int id);
     std::unordered_map<uint64_t, int32_t> index_;
     std::vector<int32_t> free_;   // min-heap of free slots
     int alloc(int l, int i, int j);
