@@ -327,8 +327,15 @@ def measure_quadrant(X, args, use_graphs=0):
     """BASELINE configs[2]: quadrant Riemann problem, 512^2 base, 3 levels, WENO5-char, regrid every 4 steps.
     Timed: K steps including the regrids (flags, Alg. 1/2, prolongation, migration) inside the region.
     use_graphs = 1: each step is a CUDA-graph replay (re-captured after each regrid)."""
-    torch = X.torch
     cfg = dict(W.quadrant(N=512, n=16, levels=3, seed=1), use_graphs=use_graphs if X.world == 1 else 0)
+    return measure_amr(X, cfg, "BASELINE configs[2] quadrant AMR, 512^2 base, 3 levels, 16^2 patches, WENO5-char, "
+                               "8 CFL-0.5 steps with 2 regrids inside the timed region")
+
+
+def measure_amr(X, cfg, workload):
+    """An AMR config: init protocol (A28), 2 untimed steps, then 8 CFL-0.5 steps with a regrid every 4 steps
+    inside the timed region (CUDA events on the library stream; the host regrid work is on the timeline)."""
+    torch = X.torch
     mesh = X.mesh(cfg)
     fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
     mesh.set_state(fn)
@@ -356,9 +363,7 @@ def measure_quadrant(X, args, use_graphs=0):
     st = mesh.stats()
     mesh.close()
     return {"value": cells * 3 / (ms / 1e3), "ms_per_step": ms / steps, "leaves": st["leaves"],
-            "patches": st["patches"], "leaf_cells_last": st["leaf_cells"],
-            "workload": "BASELINE configs[2] quadrant AMR, 512^2 base, 3 levels, 16^2 patches, WENO5-char, "
-                        "8 CFL-0.5 steps with 2 regrids inside the timed region"}
+            "patches": st["patches"], "leaf_cells_last": st["leaf_cells"], "workload": workload}
 
 
 def main():
@@ -408,6 +413,9 @@ def main():
                           "states (DESIGN.md s6); throughput config only"}
     if not args.no_amr:
         extra["quadrant_amr"] = measure_quadrant(X, args)
+        extra["shock_bubble_amr"] = measure_amr(
+            X, W.shock_bubble(), "BASELINE configs[3] shock-bubble AMR, 2048x1024 base, 4 levels, 16^2 patches, "
+                                 "WENO5-char, reflective walls, 8 CFL-0.5 steps with 2 regrids inside the timed region")
     if args.sweep_table and X.world == 1:
         extra["sweep_table"] = {"workload": "BASELINE configs[4]: Central4 stage kernel per total size and patch size",
                                 "rows": measure_sweep_table(X, args, hbm_peak)}
