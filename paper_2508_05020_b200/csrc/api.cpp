@@ -186,10 +186,35 @@ amr_status build_plan(amr_ctx* c) {
         c->rlev[t.lev[id] + 1].push_back(r);
     }
     c->leaf_cells = (int64_t)c->leaf_ids.size() * c->n * c->n;
+    // Central4 with n = 8, 16: complete aligned B x B blocks of same-level leaves (consecutive in level-Morton
+    // order, B = 32/n) form the 32 x 32 tiles of the TMA group kernel; the other leaves take the per-tile kernel
+    c->gleaves.clear();
+    c->singles.clear();
+    if (c->cfg.stage_kernel == 0 && c->cfg.scheme == AMR_CENTRAL4 && (c->n == 8 || c->n == 16)) {
+        const int B = 32 / c->n, K = B * B;
+        for (size_t e = 0; e < c->leaves.size();) {
+            const int id0 = c->leaf_ids[e];
+            bool ok = t.pi[id0] % B == 0 && t.pj[id0] % B == 0 && e + K <= c->leaves.size();
+            for (int m = 0; ok && m < K; ++m) {
+                const int id = c->leaf_ids[e + m];
+                const int mx = (m & 1) | ((m >> 1) & 2), my = ((m >> 1) & 1) | ((m >> 2) & 2);
+                ok = t.lev[id] == t.lev[id0] && t.pi[id] == t.pi[id0] + mx && t.pj[id] == t.pj[id0] + my;
+            }
+            if (ok) {
+                c->gleaves.insert(c->gleaves.end(), c->leaves.begin() + e, c->leaves.begin() + e + K);
+                e += K;
+            } else {
+                c->singles.push_back(c->leaves[e]);
+                e += 1;
+            }
+        }
+    }
     clk.mark("plan: descriptors");
 
     cudaStream_t s = c->stream;
     CU(c->d_leaves.upload(c->leaves, s));
+    CU(c->d_gleaves.upload(c->gleaves, s));
+    CU(c->d_singles.upload(c->singles, s));
     CU(c->d_ptasks.upload(c->ptasks, s));
     CU(c->d_rtasks.upload(c->rtasks, s));
     c->d_rlev.resize(L);
@@ -345,16 +370,23 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
         a.nproxy = (int32_t)(c->proxy.cap / c->PS);
         a.variant = c->cfg.stage_kernel;
         a.scratch = c->unf_scratch.p;   // variant 2: reserved by build_plan (no allocation inside a graph capture)
+        if (!c->gleaves.empty()) {      // Central4 n = 8, 16: block tiles, then the remaining single leaves
+            const int K = (32 / c->n) * (32 / c->n);
+            a.gleaves = c->d_gleaves.p;
+            a.ngroups = (int32_t)(c->gleaves.size() / K);
+            a.leaves = c->d_singles.p;
+            a.nleaves = (int32_t)c->singles.size();
+        }
         a.geo = c->geo;
         int scheme = c->cfg.scheme == AMR_CENTRAL4 ? 0 : (c->cfg.weno_characteristic ? 1 : 2);
         cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (c->timing && a.nleaves > 0) {
+        if (c->timing && !c->leaves.empty()) {
             e0 = take_event(c);
             e1 = take_event(c);
             CU(cudaEventRecord(e0, c->stream));
         }
         LAUNCH(launch_stage(scheme, a, c->stream), "stage");
-        c->st.launches += stage_launches_per_stage(a.variant, a.nleaves) - 1;
+        c->st.launches += stage_launches_per_stage(a.variant, a.nleaves) - 1 + (a.gleaves && a.nleaves > 0 ? 1 : 0);
         c->st.stage_launches++;
         if (e1) {
             CU(cudaEventRecord(e1, c->stream));
@@ -700,7 +732,7 @@ void amr_destroy(amr_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
     c->comm.finalize(c);
-    c->d_leaves.release(); c->d_ptasks.release(); c->d_rtasks.release(); c->d_prolong.release();
+    c->d_leaves.release(); c->d_gleaves.release(); c->d_singles.release(); c->d_ptasks.release(); c->d_rtasks.release(); c->d_prolong.release();
     for (auto& d : c->d_rlev) d.release();
     c->proxy.release(); c->freg.release(); c->staging.release(); c->d_maxeta.release(); c->d_partial.release();
     c->unf_scratch.release();

@@ -73,6 +73,8 @@ struct amr_ctx {
     std::vector<int32_t> leaf_ids;               // launch order
     std::vector<int32_t> leaf_pos;               // id -> leaf index or -1
     std::vector<LeafDesc> leaves;
+    std::vector<LeafDesc> gleaves, singles;        // Central4 n = 8, 16: 32 x 32 blocks of leaves / the rest
+    DevArray<LeafDesc> d_gleaves, d_singles;
     std::vector<ProxyTask> ptasks;
     std::vector<RefluxTask> rtasks;
     std::vector<std::vector<RestrictTask>> rlev;  // rlev[l]: parents at level l-1 of level-l children

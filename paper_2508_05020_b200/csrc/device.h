@@ -94,6 +94,8 @@ struct StageArgs {
     int32_t nproxy;            // proxy patches allocated (TMA tensor-map extent)
     int32_t variant;           // amr_config.stage_kernel: 0 best, 1 per-tile fused, 2 unfused, 3 per-patch launches
     double* scratch;           // variant 2: intermediate fields (unfused_scratch_doubles)
+    const LeafDesc* gleaves;   // n = 8, 16 Central4: members of 32 x 32 blocks [ngroups][(32/n)^2] (Morton order);
+    int32_t ngroups;           //   leaves / nleaves then list only the leaves outside complete blocks
     int32_t prof;              // phase timing of the TMA kernel (AMR_PHASE_PROF, debug)
     Geometry geo;
 };

@@ -812,6 +812,7 @@ constexpr int kLandI = 0, kLandW = 4 * kTmaT * kTmaT, kLandE = kLandW + 4 * kTma
               kLandSz = kLandN + 4 * kGL * kTmaT;
 constexpr size_t kTmaSmem =
     sizeof(double) * (2 * kLandSz + 4 * kTmaPL + 4 * kTmaT * kTmaFXS + 4 * kTmaT * kTmaFYS) + 32 + 64 + 128;
+constexpr size_t kTmaGroupSmem = kTmaSmem - 64 + 2 * 16 * 32;   // member descriptors [2][<=16]
 
 // One 5-face segment (faces m0 .. m0+4 of a row or column; 7 segments cover faces -1 .. T+1): sliding 4-cell
 // window of (p, T, u_n, u_t) over the prim planes (q = cell m0, cs = cell stride along the line, kn / kt = planes
@@ -1336,10 +1337,304 @@ cudaError_t launch_unfused(const StageArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- Central4 TMA kernel for small patches (groups)
+// For patch sizes N = 8, 16 a 32 x 32 tile is a B x B block (B = 32/N) of same-level leaves formed on the host
+// (consecutive leaves in level-Morton order: K = B^2 members, member m at block position demorton(m)); leaves
+// that do not complete a block go to the one-CTA-per-tile kernel.  The tile is then processed exactly like a
+// 32 x 32 patch tile of stage_c4_tma_kernel: the halo strips come from the members on the block edge, the
+// interior from K boxes; the TMA issue is spread over the lanes of warp 0 (K + 4B <= 32 boxes); U^n in and
+// U^(s) out by one box per member.  Landing layout: interior [K][4][N][N], W/E strips [B][4][N][4], S/N
+// strips [B][4][4][N].
+__device__ __forceinline__ int gm_x(int m) { return (m & 1) | ((m >> 1) & 2); }          // demorton, B <= 4
+__device__ __forceinline__ int gm_y(int m) { return ((m >> 1) & 1) | ((m >> 2) & 2); }
+__device__ __forceinline__ int gm_of(int x, int y) { return (x & 1) | ((y & 1) << 1) | ((x & 2) << 1) | ((y & 2) << 2); }
+
+template <int N, bool DIV4>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    stage_c4_group_kernel(const StageArgs a, const __grid_constant__ C4Maps maps, const int ntiles) {
+    constexpr int T = kTmaT, G = kGL, B = T / N, K = B * B;
+    constexpr int NN = N * N;
+    constexpr int WP = kTmaWP, PL = kTmaPL, FXS = kTmaFXS, FYS = kTmaFYS;
+    static_assert(K + 4 * B <= 32, "one TMA box per lane of warp 0");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* const land = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+    double* const prim = land + 2 * kLandSz;
+    double* const dUx = prim + 4 * PL;
+    double* const dUy = dUx + 4 * T * FXS;
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(dUy + 4 * T * FYS);   // [4]
+    LeafDesc* const sDesc = reinterpret_cast<LeafDesc*>(mbar + 4);          // [2][K] member descriptors
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double g = a.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
+    const bool rk_un = a.stage > 1;
+    const double ca = a.a, cb = a.b;
+    const double dt = *a.dt;
+    const int stride = gridDim.x;
+
+    // warp 0: arm the landing barrier, then one box per lane (interior of member `lane`, or one edge strip)
+    auto issue = [&](int b, const LeafDesc* D) {
+        const uint32_t mb = smem_u32(&mbar[b]);
+        const uint32_t dst = smem_u32(land + b * kLandSz);
+        if (lane == 0) mbar_expect_tx(mb, kLandSz * 8);
+        __syncwarp();
+        if (lane < K) {
+            tma_load3(dst + (kLandI + lane * 4 * NN) * 8, &maps.in_int, 0, 0, 4 * D[lane].slot, mb);
+        } else if (lane < K + 4 * B) {
+            const int e = lane - K, side = e / B, r = e - side * B;
+            const int m = side == kW ? gm_of(0, r) : side == kE ? gm_of(B - 1, r) : side == kS ? gm_of(r, 0) : gm_of(r, B - 1);
+            const int s = D[m].side[side];
+            const int z = s >= 0 ? 4 * s : 4 * (-1 - s);
+            if (side < 2) {
+                const CUtensorMap* mp = s >= 0 ? &maps.in_we : &maps.px_we;
+                tma_load3(dst + ((side == kW ? kLandW : kLandE) + r * 16 * N) * 8, mp, side == kW ? N - G : 0, 0, z, mb);
+            } else {
+                const CUtensorMap* mp = s >= 0 ? &maps.in_sn : &maps.px_sn;
+                tma_load3(dst + ((side == kS ? kLandS : kLandN) + r * 16 * N) * 8, mp, 0, side == kS ? N - G : 0, z, mb);
+            }
+        }
+    };
+    auto fetch_desc = [&](int t, int slotbuf) {   // warp 1: member descriptors of tile t -> sDesc[slotbuf]
+        if (lane < K) {
+            const uint32_t dst = smem_u32(&sDesc[slotbuf * K + lane]);
+            const LeafDesc* src = a.leaves + (size_t)t * K + lane;
+            cp_async16(dst, src);
+            cp_async16(dst + 16, reinterpret_cast<const char*>(src) + 16);
+        }
+    };
+
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_int)) : "memory");
+        for (int q = 0; q < 4; ++q) mbar_init(smem_u32(&mbar[q]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1 && (int)blockIdx.x < ntiles) { fetch_desc(blockIdx.x, 0); cp_async_wait_all(); }
+    __syncthreads();
+    if (warp == 0 && (int)blockIdx.x < ntiles) issue(0, sDesc);
+
+    const int seg_line = lane & 3, seg = lane < 28 ? lane >> 2 : 6;
+    const bool seg_store = lane < 28;
+    // interior / epilogue cells c = tid + 512 r: member m, in-member index w, tile position (ci[r], cj[r])
+    int cm[2], cw[2], ci[2], cj[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int c = tid + 512 * r;
+        cm[r] = c / NN;
+        cw[r] = c - cm[r] * NN;
+        ci[r] = gm_x(cm[r]) * N + cw[r] % N;
+        cj[r] = gm_y(cm[r]) * N + cw[r] / N;
+    }
+    unsigned long long lam = 0ull;
+    int k = 0;
+    for (int t = blockIdx.x; t < ntiles; t += stride, ++k) {
+        const int b = k & 1;
+        const LeafDesc* D = sDesc + b * K;
+        if (warp == 1 && t + stride < ntiles) fetch_desc(t + stride, b ^ 1);
+        const double* L = land + b * kLandSz;
+        mbar_wait(smem_u32(&mbar[b]), (uint32_t)((k >> 1) & 1));
+        auto c2p = [&](double r, double m, double w, double E, int o) {
+            const double ir = fast_rcp(r);
+            const double u = m * ir, v = w * ir;
+            const double p = gm1 * (E - 0.5 * (m * u + w * v));
+            prim[o] = p;
+            prim[PL + o] = p * ir;
+            prim[2 * PL + o] = u;
+            prim[3 * PL + o] = v;
+        };
+        double uc[2][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const double* s = L + kLandI + cm[r] * 4 * NN + cw[r];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) uc[r][q] = s[q * NN];
+            c2p(uc[r][0], uc[r][1], uc[r][2], uc[r][3], (cj[r] + G) * WP + ci[r] + G);
+        }
+        {
+            const int wg = warp >> 2, e = ((warp & 3) << 5) + lane;   // 0 W, 1 E, 2 S, 3 N; 128 cells each
+            int off, i, j;
+            if (wg < 2) {
+                j = e >> 2;
+                const int c = e & 3, r = j / N;
+                off = (wg == 0 ? kLandW : kLandE) + r * 16 * N + (j - r * N) * 4 + c;
+                i = wg == 0 ? c - G : T + c;
+            } else {
+                const int rr = e >> 5;
+                i = e & 31;
+                const int r = i / N;
+                off = (wg == 2 ? kLandS : kLandN) + r * 16 * N + rr * N + (i - r * N);
+                j = wg == 2 ? rr - G : T + rr;
+            }
+            const double* s = L + off;
+            c2p(s[0], s[4 * N], s[8 * N], s[12 * N], (j + G) * WP + i + G);   // strip plane = 4 N doubles
+        }
+        if (warp == 1) cp_async_wait_all();      // member descriptors of tile k+1 before (A)
+        __syncthreads();   // (A)
+        if (warp == 0) {
+            if (lane < K) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bulk_wait_read0();               // this lane's store of tile k-1 has read landing[b^1]
+            }
+            __syncwarp();
+            if (t + stride < ntiles) {
+                issue(b ^ 1, sDesc + (b ^ 1) * K);
+                if (rk_un && lane < K) tma_prefetch3(&maps.un_int, 0, 0, 4 * sDesc[(b ^ 1) * K + lane].slot);
+            }
+            if (rk_un) {                         // U^n of tile k into the converted landing[b] interior
+                const uint32_t mb = smem_u32(&mbar[2 + b]);
+                if (lane == 0) mbar_expect_tx(mb, 4 * T * T * 8);
+                __syncwarp();
+                if (lane < K)
+                    tma_load3(smem_u32(land + b * kLandSz + kLandI + lane * 4 * NN), &maps.un_int, 0, 0, 4 * D[lane].slot, mb);
+            }
+        }
+        {
+            const int m0 = seg * 5 - 1;
+            const int lvl = D[0].level;
+            double Fh[6][4];
+            if (warp < 8) {
+                const int j = 4 * warp + seg_line;
+                const double idx = 0.0625 * a.geo.inv_dx[lvl];
+                c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
+                if (seg_store) {
+#pragma unroll
+                    for (int e = 0; e < 5; ++e)
+                        if (m0 + e >= 0 && m0 + e < T)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) dUx[(q * T + j) * FXS + m0 + e] = -(Fh[e + 1][q] - Fh[e][q]) * idx;
+                    const int r = j / N;
+                    const LeafDesc& dw = D[gm_of(0, r)];
+                    const LeafDesc& de = D[gm_of(B - 1, r)];
+                    const int smw = (dw.cf | (dw.cf >> 4)) & 1, sme = (de.cf | (de.cf >> 4)) & 2;
+                    if (smw | sme) {   // flux registers of coarse/fine x sides on the block edge
+#pragma unroll
+                        for (int e = 0; e < 5; ++e)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (m0 + e == 0 && smw) a.freg[(((size_t)dw.slot * 4 + kW) * 4 + q) * N + j - r * N] = 0.0625 * Fh[e][q];
+                                if (m0 + e == T && sme) a.freg[(((size_t)de.slot * 4 + kE) * 4 + q) * N + j - r * N] = 0.0625 * Fh[e][q];
+                            }
+                    }
+                }
+            } else {
+                const int i = 4 * (warp - 8) + seg_line;
+                const double idy = 0.0625 * a.geo.inv_dy[lvl];
+                c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
+                if (seg_store) {
+#pragma unroll
+                    for (int e = 0; e < 5; ++e)
+                        if (m0 + e >= 0 && m0 + e < T) {
+                            double* o = dUy + (m0 + e) * FYS + i;
+                            o[0 * T * FYS] = -(Fh[e + 1][0] - Fh[e][0]) * idy;
+                            o[1 * T * FYS] = -(Fh[e + 1][2] - Fh[e][2]) * idy;
+                            o[2 * T * FYS] = -(Fh[e + 1][1] - Fh[e][1]) * idy;
+                            o[3 * T * FYS] = -(Fh[e + 1][3] - Fh[e][3]) * idy;
+                        }
+                    const int r = i / N;
+                    const LeafDesc& ds = D[gm_of(r, 0)];
+                    const LeafDesc& dn = D[gm_of(r, B - 1)];
+                    const int sms = (ds.cf | (ds.cf >> 4)) & 4, smn = (dn.cf | (dn.cf >> 4)) & 8;
+                    if (sms | smn) {
+#pragma unroll
+                        for (int e = 0; e < 5; ++e) {
+                            const double Fu[4] = {0.0625 * Fh[e][0], 0.0625 * Fh[e][2], 0.0625 * Fh[e][1], 0.0625 * Fh[e][3]};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (m0 + e == 0 && sms) a.freg[(((size_t)ds.slot * 4 + kS) * 4 + q) * N + i - r * N] = Fu[q];
+                                if (m0 + e == T && smn) a.freg[(((size_t)dn.slot * 4 + kN) * 4 + q) * N + i - r * N] = Fu[q];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();   // (B)
+        const int lvl = D[0].level;
+        const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
+        double* const sU = land + b * kLandSz + kLandI;
+        if (rk_un) mbar_wait(smem_u32(&mbar[2 + b]), (uint32_t)((k >> 1) & 1));
+        double out[2][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int o = (q * T + cj[r]) * FXS + ci[r];
+                const double Lr = dUx[o] + dUy[o];
+                double v = uc[r][q] + dt * Lr;
+                double* su = sU + cm[r] * 4 * NN + q * NN + cw[r];
+                if (rk_un) v = ca * *su + cb * v;
+                out[r][q] = v;
+                *su = v;
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const LeafDesc& dm = D[cm[r]];
+            const int cmask = dm.cf & 15, ii = cw[r] % N, jj = cw[r] / N;
+            const bool edge_cf = cmask && (((cmask & 1) && ii == 0) || ((cmask & 2) && ii == N - 1) ||
+                                           ((cmask & 4) && jj == 0) || ((cmask & 8) && jj == N - 1));
+            if (!edge_cf) {
+                if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
+                    report_error(a.err, dm.slot, a.stage, cw[r]);
+                if (a.want_lambda) {
+                    const double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                    const unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
+                    lam = bits > lam ? bits : lam;
+                }
+            }
+        }
+        __syncthreads();   // (C) U^(s) of the tile complete in shared memory
+        if (warp == 0 && lane < K) tma_store3(&maps.out_int, 0, 0, 4 * D[lane].slot, smem_u32(sU + lane * 4 * NN));
+    }
+    if (warp == 0 && lane < K) bulk_wait0();
+    if (a.want_lambda) {
+        lam = warp_max_u64(lam);
+        if (lane == 0 && lam) atomicMax(a.lambda_bits, lam);
+    }
+}
+
+template <int N, bool DIV4>
+cudaError_t launch_c4_group_t(const StageArgs& a, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(stage_c4_group_kernel<N, DIV4>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaGroupSmem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int ntiles = a.ngroups;
+    if (ntiles == 0) return cudaSuccess;
+    C4Maps m;
+    const double* px = a.proxy ? a.proxy : a.Uin;
+    const int npx = a.proxy && a.nproxy > 0 ? a.nproxy : a.nslots;
+    if (!encode_pool_map(&m.in_int, a.Uin, N, a.nslots, N, N) ||
+        !encode_pool_map(&m.in_we, a.Uin, N, a.nslots, kGL, N) ||
+        !encode_pool_map(&m.in_sn, a.Uin, N, a.nslots, N, kGL) ||
+        !encode_pool_map(&m.px_we, px, N, npx, kGL, N) ||
+        !encode_pool_map(&m.px_sn, px, N, npx, N, kGL) ||
+        !encode_pool_map(&m.un_int, a.Un, N, a.nslots, N, N) ||
+        !encode_pool_map(&m.out_int, a.Uout, N, a.nslots, N, N))
+        return cudaErrorInvalidValue;
+    StageArgs ag = a;
+    ag.leaves = a.gleaves;
+    const int grid = ntiles < sm_count() ? ntiles : sm_count();
+    stage_c4_group_kernel<N, DIV4><<<grid, kTmaThreads, kTmaGroupSmem, s>>>(ag, m, ntiles);
+    return cudaGetLastError();
+}
+
 template <int SCHEME>
 cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
     int T = a.geo.n / a.tiles;
     if (SCHEME == 0) {
+        if (a.variant == 0 && a.geo.n == 16 && a.gleaves) {
+            cudaError_t e = a.div_order == 4 ? launch_c4_group_t<16, true>(a, s) : launch_c4_group_t<16, false>(a, s);
+            if (e != cudaSuccess || a.nleaves == 0) return e;   // then the leaves outside complete blocks
+            return launch_c4_t<16>(a, s);
+        }
+        if (a.variant == 0 && a.geo.n == 8 && a.gleaves) {
+            cudaError_t e = a.div_order == 4 ? launch_c4_group_t<8, true>(a, s) : launch_c4_group_t<8, false>(a, s);
+            if (e != cudaSuccess || a.nleaves == 0) return e;
+            return launch_c4_t<8>(a, s);
+        }
         if (a.variant == 0 && a.geo.n == 32)
             return a.div_order == 4 ? launch_c4_tma_t<32, true>(a, s) : launch_c4_tma_t<32, false>(a, s);
         if (a.variant == 0 && a.geo.n == 64)

@@ -182,13 +182,14 @@ def test_tree_matches_oracle_after_random_requests():
 
 
 @pytest.mark.parametrize("variant", [0, 1, 2, 3])
-@pytest.mark.parametrize("n", [32, 64])
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
 def test_central4_amr_walls(n, variant):
     """Central4 on a 2-level mesh with C/F faces (proxies, flux registers, reflux) and transmissive / reflective
-    walls, for every stage-kernel organisation: 0 = persistent TMA-pipelined (n >= 32), 1 = one CTA per tile,
+    walls, for every stage-kernel organisation: 0 = persistent TMA-pipelined (n >= 32; n = 8, 16: 32 x 32 blocks
+    of leaves plus the per-tile kernel for leaves outside complete blocks), 1 = one CTA per tile,
     2 = unfused (four kernels, intermediates through HBM), 3 = one launch per leaf patch."""
-    N = 128 if n == 32 else 256
-    cfg = W.vortex(N=N, n=n, levels=2, theta=0.01 if n == 32 else 0.02, stage_kernel=variant,
+    N = 256 if n == 64 else 128
+    cfg = W.vortex(N=N, n=n, levels=2, theta=0.02 if n == 64 else 0.01, stage_kernel=variant,
                    bc=("transmissive", "transmissive", "reflective", "reflective"))
     o, g, e = run_pair(cfg, steps=10, cfl=0.5, regrid_every=4)
     assert len({k[0] for k in g.leaves()}) == 2
