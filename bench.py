@@ -382,7 +382,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weno", action="store_true")
     ap.add_argument("--no-amr", action="store_true")
-    ap.add_argument("--sweep-table", action="store_true", help="add the configs[4] size x patch-size table")
+    ap.add_argument("--no-sweep-table", action="store_true",
+                    help="skip the configs[4] size x patch-size table (single GPU only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -416,7 +417,7 @@ def main():
         extra["shock_bubble_amr"] = measure_amr(
             X, W.shock_bubble(), "BASELINE configs[3] shock-bubble AMR, 2048x1024 base, 4 levels, 16^2 patches, "
                                  "WENO5-char, reflective walls, 8 CFL-0.5 steps with 2 regrids inside the timed region")
-    if args.sweep_table and X.world == 1:
+    if not args.no_sweep_table and X.world == 1:
         extra["sweep_table"] = {"workload": "BASELINE configs[4]: Central4 stage kernel per total size and patch size",
                                 "rows": measure_sweep_table(X, args, hbm_peak)}
     if X.rank == 0:
