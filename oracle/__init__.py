@@ -65,6 +65,7 @@ def lib():
         L.orc_lambda.argtypes = [C.c_void_p, _D]
         L.orc_totals.argtypes = [C.c_void_p, _D]
         L.orc_step.argtypes = [C.c_void_p, C.c_double, C.c_double, _D]
+        L.orc_step_subcycled.argtypes = [C.c_void_p, C.c_double, C.c_double, _D]
         L.orc_flags.argtypes = [C.c_void_p, C.c_int, _D, _U8, _U8, _U8]
         L.orc_regrid_with_requests.argtypes = [C.c_void_p, C.c_int, _I, _I, _I, _U8, _U8, _I, _I]
         L.orc_regrid.argtypes = [C.c_void_p, _I, _I]
@@ -184,9 +185,11 @@ class Oracle:
         self._chk(lib().orc_totals(self.h, _dp(out)))
         return out
 
-    def step(self, dt=0.0, cfl=0.0):
+    def step(self, dt=0.0, cfl=0.0, subcycle=False):
+        """One step (O11); subcycle=True: one level-0 step with Berger-Colella time subcycling (NEXT #4)."""
         d = C.c_double()
-        self._chk(lib().orc_step(self.h, float(dt), float(cfl), C.byref(d)))
+        f = lib().orc_step_subcycled if subcycle else lib().orc_step
+        self._chk(f(self.h, float(dt), float(cfl), C.byref(d)))
         return d.value
 
     def flags(self):

@@ -658,6 +658,235 @@ void step(Oracle& o, double dt) {
     o.U.swap(prev);
 }
 
+/* ------------------------------------------------------------------ NEXT #4: Berger-Colella time subcycling
+ * Readings S1-S8 (SURVEY s8(f) NEXT #4, S:L441-445 -- the paper itself uses one global dt):
+ *  S1 level l advances with dt_l = dt_0 / 2^l: advance(l) takes one SSP-RK3 step of EVERY active level-l patch
+ *     (leaves and covered patches), then advance(l+1) twice, then refluxes the level-l leaves and restricts
+ *     level l+1 into the covered level-l patches;
+ *  S2 a level-l ghost with no same-level patch is the O8 prolongation of the level-(l-1) field taken linearly in
+ *     time, U_{l-1}(tau) = U_old + theta (U_new - U_old), theta = (tau - t_old) / dt_{l-1}, at the stage time tau
+ *     = t + c_s dt_l with the SSP-RK3 abscissae c = (0, 1, 1/2);
+ *  S3 flux registers accumulate the time integral of F-hat over a step with the SSP-RK3 quadrature weights
+ *     w = (1/6, 1/6, 2/3): coarse side sum_s w_s F_s, fine side sum over both substeps of (1/2) sum_s w_s F_s;
+ *  S4 reflux after the substeps: U += sigma dt_l / h (F_coarse - mean of the two fine faces), O12's sign and side
+ *     order;
+ *  S5 positivity is checked on the leaves after every stage of their level;
+ *  S6 dt_0 = CFL / max over leaf cells of ((|u|+c)/dx_l + (|v|+c)/dy_l) / 2^l (every level at CFL <= cfl). */
+const double SSP_C[3] = {0.0, 1.0, 0.5};
+const double SSP_W[3] = {1.0 / 6.0, 1.0 / 6.0, 2.0 / 3.0};
+
+/* S6 */
+double lambda_subcycled(const Oracle& o) {
+    int n = o.n();
+    double lam = 0.0;
+    for (auto& kv : o.tree) {
+        if (kv.second) continue;
+        const Key& p = kv.first;
+        const std::vector<double>& u = o.U.at(p);
+        double dx = o.h(0, p.l), dy = o.h(1, p.l);
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+                double Uc[4], W[4];
+                for (int k = 0; k < NV; ++k) Uc[k] = u[((size_t)k * n + j) * n + i];
+                cons2prim(o.c.gamma, Uc, W);
+                double cs = std::sqrt(o.c.gamma * W[3] / W[0]);
+                double s = ((std::fabs(W[1]) + cs) / dx + (std::fabs(W[2]) + cs) / dy) / (double)(1 << p.l);
+                if (!(s <= lam)) lam = s;
+            }
+    }
+    return lam;
+}
+
+/* C/F side classification of leaf p: 1 coarse side (same-level neighbour has children), 2 fine side (no
+ * same-level neighbour inside the domain), 0 otherwise */
+int cf_side(const Oracle& o, const Key& p, int side) {
+    int ax = side / 2, hi = side % 2;
+    int P = p.P + (ax == 0 ? (hi ? 1 : -1) : 0), Q = p.Q + (ax == 1 ? (hi ? 1 : -1) : 0);
+    if (!wrap_patch(o, p.l, P, Q)) return 0;
+    Key q{p.l, P, Q};
+    if (!o.active(q)) return 2;
+    return o.has_children(q) ? 1 : 0;
+}
+
+struct Subcycler {
+    Oracle& o;
+    std::vector<Field> old_state;                 /* per level: the level's patches at the start of its step */
+    std::vector<double> t_old, dt_lev;            /* per level: start time and length of its current step */
+    /* S3: per level, leaf -> [4 sides][NV][n] accumulated F-hat; accC: coarse sides over one step of the level,
+     * accF: fine sides over the two substeps of the level within one step of its parent level */
+    std::vector<std::map<Key, std::vector<double>>> accC, accF;
+
+    explicit Subcycler(Oracle& oo) : o(oo), old_state(oo.c.levels), t_old(oo.c.levels), dt_lev(oo.c.levels),
+                                     accC(oo.c.levels), accF(oo.c.levels) {}
+
+    std::vector<double>& reg(std::map<Key, std::vector<double>>& m, const Key& p) {
+        auto it = m.find(p);
+        if (it == m.end()) it = m.emplace(p, std::vector<double>((size_t)4 * NV * o.n(), 0.0)).first;
+        return it->second;
+    }
+
+    /* S3: F-hat on leaf p's C/F sides into its registers, with weight w (coarse side) or w/2 (fine side) */
+    void accumulate(const Key& p, const Fluxes& F, double w) {
+        int n = o.n();
+        for (int side = 0; side < 4; ++side) {
+            int kind = cf_side(o, p, side);
+            if (kind == 0) continue;
+            int ax = side / 2, hi = side % 2;
+            std::vector<double>& a = kind == 1 ? reg(accC[p.l], p) : reg(accF[p.l], p);
+            double wgt = kind == 1 ? w : 0.5 * w;
+            for (int k = 0; k < NV; ++k)
+                for (int t = 0; t < n; ++t) {
+                    double f = ax == 0 ? F.X[((size_t)k * n + t) * (n + 1) + (hi ? n : 0)]
+                                       : F.Y[((size_t)k * (n + 1) + (hi ? n : 0)) * n + t];
+                    a[((size_t)side * NV + k) * n + t] += wgt * f;
+                }
+        }
+    }
+
+    /* S1, S2, S5: one SSP-RK3 step of every active level-l patch from t0 with dt */
+    void step_level(int l, double t0, double dt) {
+        int n = o.n(), g = o.ghost_width();
+        const double a_s[3] = {0.0, 0.75, 1.0 / 3.0};
+        const double b_s[3] = {1.0, 0.25, 2.0 / 3.0};
+        Field Un;
+        for (auto& kv : o.tree)
+            if (kv.first.l == l) Un[kv.first] = o.U.at(kv.first);
+        old_state[l] = Un;
+        t_old[l] = t0;
+        dt_lev[l] = dt;
+        Field prev = Un;
+        for (int s = 0; s < 3; ++s) {
+            /* what a level-l tile reads: level l at this stage, level l-1 linearly in time (S2) */
+            Field view = prev;
+            if (l > 0) {
+                double theta = (t0 + SSP_C[s] * dt - t_old[l - 1]) / dt_lev[l - 1];
+                for (auto& kv : old_state[l - 1]) {
+                    const std::vector<double>& uo = kv.second;
+                    const std::vector<double>& un = o.U.at(kv.first);
+                    std::vector<double> u(uo.size());
+                    for (size_t e = 0; e < u.size(); ++e) u[e] = uo[e] + theta * (un[e] - uo[e]);
+                    view[kv.first] = u;
+                }
+            }
+            Field next = prev;
+            for (auto& kv : o.tree) {
+                const Key& p = kv.first;
+                if (p.l != l) continue;
+                std::vector<double> tile = build_tile(o, view, p, g);
+                std::vector<double> L;
+                Fluxes F;
+                spatial_operator(o, tile, l, L, F.X, F.Y);
+                std::vector<double>& out = next.at(p);
+                const std::vector<double>& un = Un.at(p);
+                const std::vector<double>& up = prev.at(p);
+                for (size_t e = 0; e < out.size(); ++e) {
+                    if (s == 0) out[e] = un[e] + dt * L[e];
+                    else out[e] = a_s[s] * un[e] + b_s[s] * (up[e] + dt * L[e]);
+                }
+                if (!kv.second) {   /* leaf: flux registers (S3), positivity (S5) */
+                    accumulate(p, F, SSP_W[s]);
+                    for (int e = 0; e < n * n; ++e) {
+                        double Uc[4] = {out[e], out[n * n + e], out[2 * n * n + e], out[3 * n * n + e]};
+                        if (!physical(Uc, o.c.gamma)) {
+                            char b[200];
+                            std::snprintf(b, sizeof b, "non-physical state at level %d stage %d, patch (P=%d,Q=%d), cell %d",
+                                          l, s + 1, p.P, p.Q, e);
+                            throw std::domain_error(b);
+                        }
+                    }
+                }
+            }
+            prev.swap(next);
+        }
+        for (auto& kv : prev) o.U[kv.first] = kv.second;
+    }
+
+    /* S4: the coarse leaves of level l against the fine registers of level l+1 (O12 sides, order, sign) */
+    void reflux_level(int l) {
+        int n = o.n();
+        double dt = dt_lev[l];
+        for (auto& kv : o.tree) {
+            const Key& p = kv.first;
+            if (p.l != l || kv.second) continue;
+            for (int side = 0; side < 4; ++side) {
+                if (cf_side(o, p, side) != 1) continue;
+                int ax = side / 2, hi = side % 2;
+                double h = o.h(ax, l);
+                double sigma = hi ? 1.0 : -1.0;
+                std::vector<double>& u = o.U.at(p);
+                const std::vector<double>& ac = reg(accC[l], p);
+                for (int t = 0; t < n; ++t) {
+                    int ci = ax == 0 ? (hi ? n - 1 : 0) : t;
+                    int cj = ax == 1 ? (hi ? n - 1 : 0) : t;
+                    int I = p.P * n + ci, J = p.Q * n + cj;
+                    for (int k = 0; k < NV; ++k) {
+                        double Fc = ac[((size_t)side * NV + k) * n + t];
+                        double Ff[2];
+                        for (int b = 0; b < 2; ++b) {
+                            int fI, fJ;
+                            if (ax == 0) { fI = hi ? 2 * I + 2 : 2 * I - 1; fJ = 2 * J + b; }
+                            else { fI = 2 * I + b; fJ = hi ? 2 * J + 2 : 2 * J - 1; }
+                            fI = posmod(fI, o.NC(0, l + 1));
+                            fJ = posmod(fJ, o.NC(1, l + 1));
+                            Key r{l + 1, fI / n, fJ / n};
+                            if (!o.active(r) || o.has_children(r)) fail("subcycle reflux: fine neighbour is not a leaf");
+                            int li = fI - r.P * n, lj = fJ - r.Q * n;
+                            const std::vector<double>& af = reg(accF[l + 1], r);
+                            Ff[b] = af[((size_t)(side ^ 1) * NV + k) * n + (ax == 0 ? lj : li)];
+                        }
+                        double delta = Fc - 0.5 * (Ff[0] + Ff[1]);
+                        u[((size_t)k * n + cj) * n + ci] += dt * sigma * delta / h;
+                    }
+                }
+            }
+        }
+    }
+
+    /* O9 for one level pair: level l+1 into the covered level-l patches, fixed order */
+    void restrict_level(int l) {
+        int n = o.n();
+        for (auto& kv : o.tree) {
+            const Key& p = kv.first;
+            if (p.l != l || !kv.second) continue;
+            std::vector<double>& up = o.U.at(p);
+            for (int k = 0; k < NV; ++k)
+                for (int j = 0; j < n; ++j)
+                    for (int i = 0; i < n; ++i) {
+                        int a = (2 * i) / n, b = (2 * j) / n;
+                        const std::vector<double>& uc = o.U.at(Key{l + 1, 2 * p.P + a, 2 * p.Q + b});
+                        int fi = 2 * i - a * n, fj = 2 * j - b * n;
+                        double f00 = uc[(k * n + fj) * n + fi], f10 = uc[(k * n + fj) * n + fi + 1];
+                        double f01 = uc[(k * n + fj + 1) * n + fi], f11 = uc[(k * n + fj + 1) * n + fi + 1];
+                        up[(k * n + j) * n + i] = ((f00 + f10) + (f01 + f11)) * 0.25;
+                    }
+        }
+    }
+
+    bool level_exists(int l) const {
+        if (l >= o.c.levels) return false;
+        for (auto& kv : o.tree)
+            if (kv.first.l == l) return true;
+        return false;
+    }
+
+    /* S1: step level l, then twice the next level, then reflux and restriction at the common time */
+    void advance(int l, double t0, double dt) {
+        accC[l].clear();
+        step_level(l, t0, dt);
+        if (!level_exists(l + 1)) return;
+        accF[l + 1].clear();
+        advance(l + 1, t0, 0.5 * dt);
+        advance(l + 1, t0 + 0.5 * dt, 0.5 * dt);
+        reflux_level(l);
+        restrict_level(l);
+    }
+};
+
+void step_subcycled(Oracle& o, double dt0) {
+    Subcycler sc(o);
+    sc.advance(0, 0.0, dt0);
+}
+
 /* O6: per-leaf refinement indicator eta = dx sqrt(gx^2 + gy^2) / rho (BJ configs[0], A19) */
 struct LeafFlag {
     double maxeta;
@@ -848,6 +1077,21 @@ int orc_step(void* h, double dt, double cfl, double* dt_used) {
             d = cfl / lam;   /* O13 */
         }
         step(o, d);
+        if (dt_used) *dt_used = d;
+    });
+}
+
+int orc_step_subcycled(void* h, double dt0, double cfl, double* dt_used) {
+    return guarded(h, [&] {
+        Oracle& o = *H(h);
+        double d = dt0;
+        if (!(d > 0.0)) {
+            if (!(cfl > 0.0)) fail("need dt > 0 or cfl > 0");
+            double lam = lambda_subcycled(o);
+            if (!(lam > 0.0) || !std::isfinite(lam)) throw std::domain_error("non-finite wave speed");
+            d = cfl / lam;   /* S6 */
+        }
+        step_subcycled(o, d);
         if (dt_used) *dt_used = d;
     });
 }

@@ -51,6 +51,9 @@ int orc_restrict_all(void* h);                         /* O9 */
 int orc_lambda(void* h, double* lam);                  /* O13 */
 int orc_totals(void* h, double* out4);                 /* O18 */
 int orc_step(void* h, double dt, double cfl, double* dt_used);   /* O11 */
+/* NEXT #4: one level-0 step of Berger-Colella time subcycling (dt_l = dt0 / 2^l, readings S1-S6 in oracle.cpp
+ * and DESIGN.md s3b); dt0 <= 0: dt0 = cfl / max over leaves of the level-0-normalised wave speed */
+int orc_step_subcycled(void* h, double dt0, double cfl, double* dt_used);
 
 /* flags (O6) for every active patch, canonical order */
 int orc_flags(void* h, int cap, double* maxeta, unsigned char* refine,
