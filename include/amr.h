@@ -92,6 +92,11 @@ typedef struct {
                                      n >= 32: persistent TMA-pipelined fused kernel, else 1); 1 fused, one CTA per
                                      tile with a cp.async halo gather; 2 unfused: four kernels per stage with the
                                      primitives and face fluxes through HBM; 3 one launch of kernel 1 per leaf */
+    int32_t subcycle;             /* 1: Berger-Colella time subcycling (NEXT #4; DESIGN.md s3b S1-S6): level l takes
+                                     2^l steps of dt_0 / 2^l per amr_step, C/F ghosts interpolated in time, fluxes
+                                     refluxed with quadrature-weighted registers; dt / cfl of amr_step refer to
+                                     level 0 and amr_diagnostics' lambda is normalised to level 0.  Single rank;
+                                     a non-physical step is reported (AMR_E_NONPHYSICAL) but only level 0 rolls back */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none

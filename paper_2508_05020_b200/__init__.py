@@ -42,7 +42,7 @@ class amr_config(C.Structure):
                 ("max_patches", C.c_int32), ("pool", C.c_void_p), ("pool_bytes", C.c_uint64),
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("world_size", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("check_positivity", C.c_int32),
-                ("use_graphs", C.c_int32), ("comm_backend", C.c_int32), ("stage_kernel", C.c_int32)]
+                ("use_graphs", C.c_int32), ("comm_backend", C.c_int32), ("stage_kernel", C.c_int32), ("subcycle", C.c_int32)]
 
 
 class amr_patch_desc(C.Structure):
@@ -148,6 +148,7 @@ def make_config(cfg: dict, **over) -> amr_config:
     c.check_positivity = int(cfg.get("check_positivity", 1))
     c.stage_kernel = int(cfg.get("stage_kernel", 0))
     c.use_graphs = int(cfg.get("use_graphs", 0))
+    c.subcycle = int(cfg.get("subcycle", 0))
     c.world_size = 1
     c.rank = 0
     c.device = -1

@@ -72,6 +72,7 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.refine_threshold < 0 || c.coarsen_fraction < 0) { m = "bad thresholds"; return AMR_E_CONFIG; }
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
     if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }
+    if (c.subcycle && c.world_size > 1) { m = "subcycling is single-rank in this build"; return AMR_E_CONFIG; }
     return AMR_OK;
 }
 
@@ -87,6 +88,90 @@ struct PhaseClock {
         t = n;
     }
 };
+
+// Subcycling plan (NEXT #4): for each level, the descriptors of every active patch of the level -- its leaves
+// (launch order) and then its covered patches (pad bit 0; all same-level neighbours exist by R2) -- with proxies
+// of their own (C/F ghosts prolonged in time per stage, physical BC), the C/F register tasks of the level's
+// leaves, and per-level offsets of the reflux tasks (rtasks are in level-major leaf order).
+amr_status build_subcycle_plan(amr_ctx* c) {
+    const PatchTree& t = c->tree;
+    const int L = c->cfg.num_levels;
+    static const int dirs[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
+    c->sub_descs.clear();
+    c->sub_ptasks.clear();
+    c->acc_tasks.clear();
+    c->sub_off.assign(L + 1, 0);
+    c->sub_poff.assign(L + 1, 0);
+    c->acc_off.assign(L + 1, 0);
+    c->rt_off.assign(L + 1, 0);
+    auto add = [&](int id, bool covered) -> amr_status {
+        LeafDesc d{};
+        d.slot = id;
+        d.level = t.lev[id];
+        d.pad = covered ? 1 : 0;
+        for (int s = 0; s < 4; ++s) {
+            int nb = t.neighbour(id, dirs[s][0], dirs[s][1]);
+            if (nb >= 0) {
+                d.side[s] = nb;
+                if (!covered && t.has_children(nb)) d.cf |= 1 << s;
+            } else {
+                ProxyTask p{};
+                p.proxy = (int)c->sub_ptasks.size();
+                p.slot = id;
+                p.side = s;
+                p.level = t.lev[id];
+                p.P = t.pi[id];
+                p.Q = t.pj[id];
+                if (nb == -2) {
+                    p.kind = 0;
+                    for (int q = 0; q < 9; ++q) p.coarse[q] = -1;
+                } else {
+                    if (covered) return fail(c, AMR_E_MESH, "subcycle: covered patch without a same-level neighbour");
+                    p.kind = 1;
+                    d.cf |= 1 << (4 + s);
+                    int par = t.parent[id];
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
+                            if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
+                            p.coarse[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
+                        }
+                }
+                d.side[s] = -1 - p.proxy;
+                c->sub_ptasks.push_back(p);
+            }
+        }
+        if (!covered)
+            for (int s = 0; s < 4; ++s) {
+                if (d.cf & (1 << s)) c->acc_tasks.push_back(AccTask{id, s, 1});
+                if (d.cf & (1 << (4 + s))) c->acc_tasks.push_back(AccTask{id, s, 2});
+            }
+        c->sub_descs.push_back(d);
+        return AMR_OK;
+    };
+    size_t e = 0, r = 0;
+    for (int l = 0; l < L; ++l) {
+        c->sub_off[l] = (int32_t)c->sub_descs.size();
+        c->sub_poff[l] = (int32_t)c->sub_ptasks.size();
+        c->acc_off[l] = (int32_t)c->acc_tasks.size();
+        c->rt_off[l] = (int32_t)r;
+        for (; e < c->leaf_ids.size() && t.lev[c->leaf_ids[e]] == l; ++e) {
+            amr_status s = add(c->leaf_ids[e], false);
+            if (s != AMR_OK) return s;
+        }
+        for (int id : c->canon)
+            if (t.lev[id] == l && t.has_children(id)) {
+                amr_status s = add(id, true);
+                if (s != AMR_OK) return s;
+            }
+        while (r < c->rtasks.size() && c->rtasks[r].level == l) ++r;
+    }
+    c->sub_off[L] = (int32_t)c->sub_descs.size();
+    c->sub_poff[L] = (int32_t)c->sub_ptasks.size();
+    c->acc_off[L] = (int32_t)c->acc_tasks.size();
+    c->rt_off[L] = (int32_t)r;
+    return AMR_OK;
+}
 
 amr_status build_plan(amr_ctx* c) {
     PhaseClock clk;
@@ -190,7 +275,7 @@ amr_status build_plan(amr_ctx* c) {
     // order, B = 32/n) form the 32 x 32 tiles of the TMA group kernel; the other leaves take the per-tile kernel
     c->gleaves.clear();
     c->singles.clear();
-    if (c->cfg.stage_kernel == 0 && c->cfg.scheme == AMR_CENTRAL4 && (c->n == 8 || c->n == 16)) {
+    if (c->cfg.stage_kernel == 0 && c->cfg.scheme == AMR_CENTRAL4 && (c->n == 8 || c->n == 16) && !c->cfg.subcycle) {
         const int B = 32 / c->n, K = B * B;
         for (size_t e = 0; e < c->leaves.size();) {
             const int id0 = c->leaf_ids[e];
@@ -209,6 +294,10 @@ amr_status build_plan(amr_ctx* c) {
             }
         }
     }
+    if (c->cfg.subcycle) {
+        amr_status ss = build_subcycle_plan(c);
+        if (ss != AMR_OK) return ss;
+    }
     clk.mark("plan: descriptors");
 
     cudaStream_t s = c->stream;
@@ -217,6 +306,13 @@ amr_status build_plan(amr_ctx* c) {
     CU(c->d_singles.upload(c->singles, s));
     CU(c->d_ptasks.upload(c->ptasks, s));
     CU(c->d_rtasks.upload(c->rtasks, s));
+    if (c->cfg.subcycle) {
+        CU(c->d_sub_descs.upload(c->sub_descs, s));
+        CU(c->d_sub_ptasks.upload(c->sub_ptasks, s));
+        CU(c->d_acc_tasks.upload(c->acc_tasks, s));
+        CU(c->sub_proxy.reserve(std::max<size_t>(1, c->sub_ptasks.size()) * c->PS));
+        CU(c->facc.reserve((size_t)t.capacity * 16 * c->n));
+    }
     c->d_rlev.resize(L);
     for (int l = 0; l < L; ++l) CU(c->d_rlev[l].upload(c->rlev[l], s));
     CU(c->proxy.reserve(std::max<size_t>(1, c->ptasks.size()) * c->PS));
@@ -244,6 +340,7 @@ amr_status build_plan(amr_ctx* c) {
 AuxArgs aux(amr_ctx* c, const double* Ur, double* Uw) {
     AuxArgs a{};
     a.U = Ur;
+    a.Uc = Ur;
     a.Uw = Uw;
     a.proxy = c->proxy.p;
     a.freg = c->freg.p;
@@ -290,6 +387,7 @@ amr_status seed_lambda(amr_ctx* c) {
     amr_status s = c->comm.exchange_halos(c, c->U[c->un]);
     if (s != AMR_OK) return s;
     AuxArgs a = aux(c, c->U[c->un], nullptr);
+    a.lam0 = c->cfg.subcycle;
     LAUNCH(launch_lambda(c->d_leaves.p, (int)c->leaves.size(), a, c->stream), "lambda");
     s = c->comm.allreduce_max_u64(c, c->d_lambda);
     if (s != AMR_OK) return s;
@@ -707,7 +805,7 @@ amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
     }
     for (int b = 0; b < 3; ++b) c->U[b] = (double*)(base + (size_t)b * (need / 3));
     CU(cudaMemsetAsync(base, 0, need, c->stream));
-    CU(cudaMalloc(&c->d_dt, 8));
+    CU(cudaMalloc(&c->d_dt, 8 * kMaxLevels));   // dt per level (subcycling); dt[0] otherwise
     CU(cudaMalloc(&c->d_lambda, 8));
     CU(cudaMalloc(&c->d_tmp, 8));
     CU(cudaMalloc(&c->d_err, 16));
@@ -900,6 +998,126 @@ amr_status amr_get_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, 
     return AMR_OK;
 }
 
+// ---------------------------------------------------------------- subcycled step (NEXT #4, S1-S6)
+// Buffer rotation: every level starts the coarse step in buffer un and must end it in (un + 1) % 3.  A level-l
+// step moves its current buffer by +1 or +2 (stage outputs in the two other buffers); level l takes 2^l steps, so
+// the increments are chosen with sum = 1 (mod 3): 2^l - k ones then k twos, k = (1 - 2^l) mod 3.  Levels own
+// disjoint slots, so a level's old (step start) and new buffers stay intact while the next level interpolates.
+struct SubRun {
+    amr_ctx* c;
+    int L;
+    int cur[kMaxLevels], start[kMaxLevels], nstep[kMaxLevels];
+    int inc(int l) const {
+        const int m = 1 << l, k = ((1 - m) % 3 + 3) % 3;
+        return nstep[l] >= m - k ? 2 : 1;
+    }
+    bool has_level(int l) const { return l < L && c->sub_off[l + 1] > c->sub_off[l]; }
+
+    amr_status advance(int l, bool final, int sub_i) {
+        static const double as[3] = {0.0, 0.75, 1.0 / 3.0}, bs[3] = {1.0, 0.25, 2.0 / 3.0};
+        static const double cs[3] = {0.0, 1.0, 0.5}, ws[3] = {1.0 / 6.0, 1.0 / 6.0, 2.0 / 3.0};
+        const int P = (cur[l] + inc(l)) % 3, Q = 3 - cur[l] - P;
+        start[l] = cur[l];
+        double* Un = c->U[cur[l]];
+        const int n0 = c->sub_off[l], nl = c->sub_off[l + 1] - n0;
+        const int p0 = c->sub_poff[l], pl = c->sub_poff[l + 1] - p0;
+        const int a0 = c->acc_off[l], al = c->acc_off[l + 1] - a0;
+        for (int s = 1; s <= 3; ++s) {
+            double* Uin = s == 1 ? Un : (s == 2 ? c->U[P] : c->U[Q]);
+            double* Uout = s == 2 ? c->U[Q] : c->U[P];
+            if (pl > 0) {   // ghosts: physical BC from the stage input, C/F from level l-1 in time (S2)
+                AuxArgs g = aux(c, Uin, nullptr);
+                g.proxy = c->sub_proxy.p;
+                if (l > 0) {
+                    g.Uc = c->U[cur[l - 1]];
+                    g.Uold = c->U[start[l - 1]];
+                    g.tfrac = (sub_i + cs[s - 1]) * 0.5;
+                }
+                LAUNCH(launch_ghost(c->d_sub_ptasks.p + p0, pl, c->g, g, c->stream), "ghost");
+            }
+            StageArgs a{};
+            a.leaves = c->d_sub_descs.p + n0;
+            a.nleaves = nl;
+            a.tiles = c->n > 32 ? c->n / 32 : 1;
+            a.Uin = Uin;
+            a.Un = Un;
+            a.Uout = Uout;
+            a.proxy = c->sub_proxy.p;
+            a.freg = c->freg.p;
+            a.dt = c->d_dt + l;
+            a.a = as[s - 1];
+            a.b = bs[s - 1];
+            a.stage = s;
+            a.div_order = c->cfg.div_order;
+            a.characteristic = c->cfg.weno_characteristic;
+            a.check = c->cfg.check_positivity;
+            a.want_lambda = final && s == 3;
+            a.lam0 = 1;
+            a.gamma = c->cfg.gamma;
+            a.eps = c->cfg.weno_eps;
+            a.lambda_bits = c->d_lambda;
+            a.err = c->d_err;
+            a.nslots = c->cfg.max_patches;
+            a.nproxy = (int32_t)(c->sub_proxy.cap / c->PS);
+            a.variant = c->cfg.stage_kernel;
+            a.scratch = c->unf_scratch.p;
+            a.geo = c->geo;
+            const int scheme = c->cfg.scheme == AMR_CENTRAL4 ? 0 : (c->cfg.weno_characteristic ? 1 : 2);
+            LAUNCH(launch_stage(scheme, a, c->stream), "stage");
+            c->st.launches += stage_launches_per_stage(a.variant, a.nleaves) - 1;
+            c->st.stage_launches++;
+            if (al > 0)
+                LAUNCH(launch_accumulate(c->d_acc_tasks.p + a0, al, c->n, c->freg.p, c->facc.p, ws[s - 1], 0.5 * ws[s - 1],
+                                         s == 1, s == 1 && sub_i == 0, c->stream), "accumulate");
+        }
+        cur[l] = P;
+        nstep[l]++;
+        if (!has_level(l + 1)) return AMR_OK;
+        amr_status st = advance(l + 1, false, 0);
+        if (st != AMR_OK) return st;
+        st = advance(l + 1, final, 1);
+        if (st != AMR_OK) return st;
+        const int r0 = c->rt_off[l], rl = c->rt_off[l + 1] - r0;
+        if (rl > 0) {   // S4
+            AuxArgs x = aux(c, c->U[cur[l]], c->U[cur[l]]);
+            x.freg = c->facc.p;
+            x.dt = c->d_dt + l;
+            x.b = 1.0;
+            x.stage = 3;
+            x.want_lambda = final;
+            x.lam0 = 1;
+            LAUNCH(launch_reflux(c->d_rtasks.p + r0, rl, x, c->stream), "reflux");
+        }
+        if (!c->rlev[l + 1].empty()) {   // O9: level l+1 into the covered level-l patches
+            AuxArgs r = aux(c, c->U[cur[l + 1]], c->U[cur[l]]);
+            LAUNCH(launch_restrict(c->d_rlev[l + 1].p, (int)c->rlev[l + 1].size(), r, c->stream), "restrict");
+        }
+        return AMR_OK;
+    }
+};
+
+amr_status enqueue_step_subcycled(amr_ctx* c, double dt, double cfl) {
+    if (!c->lambda_valid && !(dt > 0.0)) {
+        amr_status s = seed_lambda(c);
+        if (s != AMR_OK) return s;
+    }
+    LAUNCH(launch_dt(c->d_dt, c->d_lambda, c->d_err, dt, cfl, c->stream), "dt");
+    LAUNCH(launch_dt_levels(c->d_dt, c->cfg.num_levels, c->stream), "dt levels");
+    SubRun r{};
+    r.c = c;
+    r.L = c->cfg.num_levels;
+    for (int l = 0; l < kMaxLevels; ++l) { r.cur[l] = r.start[l] = c->un; r.nstep[l] = 0; }
+    amr_status s = r.advance(0, true, 0);
+    if (s != AMR_OK) return s;
+    for (int l = 0; l < r.L; ++l)
+        if (r.has_level(l) && r.cur[l] != (c->un + 1) % 3)
+            return fail(c, AMR_E_STATE, "subcycle: buffer rotation out of step");
+    c->un = (c->un + 1) % 3;
+    c->st.steps++;
+    c->lambda_valid = true;
+    return AMR_OK;
+}
+
 // One step as a CUDA graph replay (use_graphs, one rank, kernel timing off): the launch sequence of
 // enqueue_step is captured once per position of U^n in the buffer rotation and per plan, and replayed with the
 // step's (dt, cfl) written to device memory first.  Host bookkeeping is the same as enqueue_step's.
@@ -946,7 +1164,12 @@ amr_status enqueue_step_graph(amr_ctx* c, double dt, double cfl) {
 // stream-launched steps (a regrid every few steps would otherwise re-capture all the time)
 constexpr int kGraphAfter = 3;
 bool use_graph(const amr_ctx* c) {
-    return c->cfg.use_graphs && c->cfg.world_size == 1 && !c->timing && c->plan_steps >= kGraphAfter;
+    return c->cfg.use_graphs && c->cfg.world_size == 1 && !c->timing && c->plan_steps >= kGraphAfter &&
+           !c->cfg.subcycle;
+}
+amr_status enqueue_any_step(amr_ctx* c, double dt, double cfl) {
+    if (c->cfg.subcycle) return enqueue_step_subcycled(c, dt, cfl);
+    return use_graph(c) ? enqueue_step_graph(c, dt, cfl) : enqueue_step(c, dt, cfl);
 }
 
 amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
@@ -954,7 +1177,7 @@ amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
     if (s != AMR_OK) return s;
     if (!(dt > 0.0) && !(cfl > 0.0)) return fail(c, AMR_E_ARG, "step: need dt > 0 or cfl > 0");
     int prev = c->un;
-    s = use_graph(c) ? enqueue_step_graph(c, dt, cfl) : enqueue_step(c, dt, cfl);
+    s = enqueue_any_step(c, dt, cfl);
     c->plan_steps++;
     if (s != AMR_OK) return s;
     if (c->cfg.check_positivity || dt_used) return finish_step(c, prev, dt_used);
@@ -966,7 +1189,7 @@ amr_status amr_steps(amr_ctx* c, int32_t nsteps, double dt, double cfl) {
     if (s != AMR_OK) return s;
     if (nsteps < 0 || (!(dt > 0.0) && !(cfl > 0.0))) return fail(c, AMR_E_ARG, "steps: bad arguments");
     for (int k = 0; k < nsteps; ++k) {
-        s = use_graph(c) ? enqueue_step_graph(c, dt, cfl) : enqueue_step(c, dt, cfl);
+        s = enqueue_any_step(c, dt, cfl);
         if (s != AMR_OK) return s;
         c->plan_steps++;
     }

@@ -121,6 +121,17 @@ struct amr_ctx {
     int64_t glaunches[3] = {0, 0, 0};
     double* d_dtp = nullptr;   // (dt_fixed, cfl) of a replayed step
 
+    // subcycling (NEXT #4): per-level launch lists of every active patch (leaves, then covered patches with
+    // LeafDesc.pad bit 0) with their own proxies, per-level C/F register tasks, accumulated registers
+    std::vector<LeafDesc> sub_descs;
+    std::vector<ProxyTask> sub_ptasks;
+    std::vector<AccTask> acc_tasks;
+    std::vector<int32_t> sub_off, sub_poff, acc_off, rt_off;   // per level [L+1]
+    DevArray<LeafDesc> d_sub_descs;
+    DevArray<ProxyTask> d_sub_ptasks;
+    DevArray<AccTask> d_acc_tasks;
+    DevArray<double> sub_proxy, facc;
+
     Comm comm;
     std::string err;
     amr_status sticky = AMR_OK;

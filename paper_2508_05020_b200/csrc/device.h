@@ -97,11 +97,21 @@ struct StageArgs {
     const LeafDesc* gleaves;   // n = 8, 16 Central4: members of 32 x 32 blocks [ngroups][(32/n)^2] (Morton order);
     int32_t ngroups;           //   leaves / nleaves then list only the leaves outside complete blocks
     int32_t prof;              // phase timing of the TMA kernel (AMR_PHASE_PROF, debug)
+    int32_t lam0;              // subcycling: Lambda normalised to level 0 (S6); LeafDesc.pad bit 0 = covered patch
     Geometry geo;
+};
+
+// Subcycling (S3): one C/F side of a leaf whose F-hat is accumulated over a step; kind 1 coarse side, 2 fine side.
+struct AccTask {
+    int32_t slot, side, kind;
 };
 
 struct AuxArgs {
     const double* U;           // state read (ghost source / restriction source ...)
+    const double* Uc;          // ghost kernel: coarse-level source of C/F prolongation (= U without subcycling)
+    const double* Uold;        // subcycling: coarse level at the start of its step (nullptr: no time interpolation)
+    double tfrac;              //   fraction of that step at the stage time (S2)
+    int32_t lam0;              // subcycling: Lambda normalised to level 0 (S6)
     double* Uw;                // state written
     double* proxy;
     const double* freg;
@@ -129,6 +139,9 @@ cudaError_t launch_dt(double* dt, unsigned long long* lambda_bits, int32_t* err,
 cudaError_t launch_dt_dev(double* dt, unsigned long long* lambda_bits, int32_t* err, const double* params,
                           cudaStream_t s);
 cudaError_t launch_set2(double* p, double a, double b, cudaStream_t s);
+cudaError_t launch_dt_levels(double* dt, int levels, cudaStream_t s);
+cudaError_t launch_accumulate(const AccTask* tasks, int ntasks, int n, const double* freg, double* acc, double w_coarse,
+                              double w_fine, int assign_coarse, int assign_fine, cudaStream_t s);
 cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* maxeta, int32_t* amb,
                          cudaStream_t s);
 cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* partial, cudaStream_t s);

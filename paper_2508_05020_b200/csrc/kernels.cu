@@ -402,11 +402,12 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             // cells on an edge that is the coarse side of a C/F face are finished by the reflux kernel
             bool edge_cf = ((coarse_mask & 1) && x_lo && i == 0) || ((coarse_mask & 2) && x_hi && i == T - 1) ||
                            ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1);
-            if (!edge_cf) {
+            if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
                 if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], g))
                     report_error(a.err, d.slot, a.stage, (int)off);
                 if (a.want_lambda) {
                     double s = wave_speed(o4[0], o4[1], o4[2], o4[3], g, idx, idy);
+                    if (a.lam0) s = ldexp(s, -d.level);
                     unsigned long long b = (unsigned long long)__double_as_longlong(s);
                     lam = b > lam ? b : lam;
                 }
@@ -686,11 +687,12 @@ __global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 
         for (int k = 0; k < 4; ++k) po[k * NN + r * N] = out[r][k];
         bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
                                        ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
-        if (!edge_cf) {
+        if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
             if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
                 report_error(a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + ci);
             if (a.want_lambda) {
                 double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                    if (a.lam0) sp = ldexp(sp, -d.level);   // subcycling: level-0-normalised (S6)
                 unsigned long long b = (unsigned long long)__double_as_longlong(sp);
                 lam = b > lam ? b : lam;
             }
@@ -1080,11 +1082,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const int j = cj0 + r;
             const bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
                                                  ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
-            if (!edge_cf) {
+            if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
                 if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
                     report_error(a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + ci);
                 if (a.want_lambda) {
-                    const double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                    double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                    if (a.lam0) sp = ldexp(sp, -d.level);   // subcycling: level-0-normalised (S6)
                     const unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
                     lam = bits > lam ? bits : lam;
                 }
@@ -1312,10 +1315,11 @@ __global__ void unf_rk_kernel(const StageArgs a) {
     const bool edge_cf = ((coarse_mask & 1) && i == 0) || ((coarse_mask & 2) && i == n - 1) ||
                          ((coarse_mask & 4) && j == 0) || ((coarse_mask & 8) && j == n - 1);
     unsigned long long lam = 0ull;
-    if (!edge_cf) {
+    if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
         if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], a.gamma)) report_error(a.err, d.slot, a.stage, c);
         if (a.want_lambda)
-            lam = (unsigned long long)__double_as_longlong(wave_speed(o4[0], o4[1], o4[2], o4[3], a.gamma, idx, idy));
+            lam = (unsigned long long)__double_as_longlong(a.lam0 ? ldexp(wave_speed(o4[0], o4[1], o4[2], o4[3], a.gamma, idx, idy), -d.level)
+                                                                  : wave_speed(o4[0], o4[1], o4[2], o4[3], a.gamma, idx, idy));
     }
     if (a.want_lambda) {
         lam = warp_max_u64(lam);
@@ -1576,7 +1580,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
                     report_error(a.err, dm.slot, a.stage, cw[r]);
                 if (a.want_lambda) {
-                    const double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                    double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
+                    if (a.lam0) sp = ldexp(sp, -dm.level);   // subcycling: level-0-normalised (S6)
                     const unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
                     lam = bits > lam ? bits : lam;
                 }
@@ -1656,8 +1661,10 @@ cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
 // ---------------------------------------------------------------- coarse values for prolongation (O8)
 // Value of component k of coarse cell (rx, ry) given relative to the parent patch
 // (level l-1, position Pp, Qp); out-of-domain cells follow the BC rule (O7).
+// Uold != nullptr (subcycling, S2): the coarse level linearly in time, Uold + tfrac (U - Uold), before the BC sign.
 __device__ __forceinline__ double coarse_value(const double* U, const int32_t* coarse, int n, int lc, int Pp, int Qp,
-                                               int rx, int ry, int k, const Geometry& geo) {
+                                               int rx, int ry, int k, const Geometry& geo, const double* Uold,
+                                               double tfrac) {
     double sgn = 1.0;
     int Ig = Pp * n + rx, Jg = Qp * n + ry;
     const int NX = geo.nc[0][lc], NY = geo.nc[1][lc];
@@ -1677,7 +1684,10 @@ __device__ __forceinline__ double coarse_value(const double* U, const int32_t* c
     int by = ry < 0 ? -1 : (ry >= n ? 1 : 0);
     int slot = coarse[(by + 1) * 3 + (bx + 1)];
     int lx = rx - bx * n, ly = ry - by * n;
-    return sgn * U[(size_t)slot * 4 * n * n + (size_t)k * n * n + (size_t)ly * n + lx];
+    const size_t o = (size_t)slot * 4 * n * n + (size_t)k * n * n + (size_t)ly * n + lx;
+    double v = U[o];
+    if (Uold) v = Uold[o] + tfrac * (v - Uold[o]);
+    return sgn * v;
 }
 
 __device__ __forceinline__ double mc_limiter(double a, double b) {
@@ -1688,16 +1698,17 @@ __device__ __forceinline__ double mc_limiter(double a, double b) {
 
 // O8 for fine cell (I, J) (global at level l, may be unwrapped by one patch)
 __device__ __forceinline__ double prolong_value(const double* U, const int32_t* coarse, int n, int l, int P, int Q,
-                                                int I, int J, int k, const Geometry& geo) {
+                                                int I, int J, int k, const Geometry& geo, const double* Uold = nullptr,
+                                                double tfrac = 0.0) {
     int Pp = P >> 1, Qp = Q >> 1;
     int Ic = I >> 1, Jc = J >> 1;   // arithmetic shift = floor division by 2
     int ax = I & 1, by = J & 1;
     int rx = Ic - Pp * n, ry = Jc - Qp * n;
-    double V = coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry, k, geo);
-    double sx = mc_limiter(V - coarse_value(U, coarse, n, l - 1, Pp, Qp, rx - 1, ry, k, geo),
-                           coarse_value(U, coarse, n, l - 1, Pp, Qp, rx + 1, ry, k, geo) - V);
-    double sy = mc_limiter(V - coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry - 1, k, geo),
-                           coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry + 1, k, geo) - V);
+    double V = coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry, k, geo, Uold, tfrac);
+    double sx = mc_limiter(V - coarse_value(U, coarse, n, l - 1, Pp, Qp, rx - 1, ry, k, geo, Uold, tfrac),
+                           coarse_value(U, coarse, n, l - 1, Pp, Qp, rx + 1, ry, k, geo, Uold, tfrac) - V);
+    double sy = mc_limiter(V - coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry - 1, k, geo, Uold, tfrac),
+                           coarse_value(U, coarse, n, l - 1, Pp, Qp, rx, ry + 1, k, geo, Uold, tfrac) - V);
     double t = V + ((2 * ax - 1) * 0.25) * sx;
     return t + ((2 * by - 1) * 0.25) * sy;
 }
@@ -1740,7 +1751,7 @@ __global__ void ghost_kernel(const ProxyTask* __restrict__ tasks, int ntasks, in
         const int I = pt.P * n + li, J = pt.Q * n + lj;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            dst[k * nn] = prolong_value(a.U, pt.coarse, n, pt.level, pt.P, pt.Q, I, J, k, a.geo);
+            dst[k * nn] = prolong_value(a.Uc, pt.coarse, n, pt.level, pt.P, pt.Q, I, J, k, a.geo, a.Uold, a.tfrac);
     }
 }
 
@@ -1770,7 +1781,7 @@ __global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntas
     const int i = e % n, j = e / n;
     const int ca = (2 * i) / n, cb = (2 * j) / n;
     const int fi = 2 * i - ca * n, fj = 2 * j - cb * n;
-    const double* f = a.Uw + (size_t)rt.child[ca + 2 * cb] * 4 * nn + (size_t)fj * n + fi;
+    const double* f = a.U + (size_t)rt.child[ca + 2 * cb] * 4 * nn + (size_t)fj * n + fi;   // children (read)
     double* dst = a.Uw + (size_t)rt.parent * 4 * nn + e;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -1824,6 +1835,7 @@ __global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, 
     if (a.check && !physical_state(u[0], u[1], u[2], u[3], a.gamma)) report_error(a.err, rt.slot, a.stage, j * n + i);
     if (a.want_lambda) {
         double sp = wave_speed(u[0], u[1], u[2], u[3], a.gamma, a.geo.inv_dx[l], a.geo.inv_dy[l]);
+        if (a.lam0) sp = ldexp(sp, -l);
         atomicMax(a.lambda_bits, (unsigned long long)__double_as_longlong(sp));
     }
 }
@@ -1838,6 +1850,7 @@ __global__ void lambda_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs
     for (int e = threadIdx.x; e < (int)nn; e += blockDim.x) {
         double s = wave_speed(U[e], U[nn + e], U[2 * nn + e], U[3 * nn + e], a.gamma, a.geo.inv_dx[d.level],
                               a.geo.inv_dy[d.level]);
+        if (a.lam0) s = ldexp(s, -d.level);
         unsigned long long b = (unsigned long long)__double_as_longlong(s);
         lam = b > lam ? b : lam;
     }
@@ -1863,6 +1876,26 @@ __device__ __forceinline__ void dt_kernel_body(double* dt, unsigned long long* l
 
 __global__ void dt_kernel(double* dt, unsigned long long* lambda_bits, int32_t* err, double dt_fixed, double cfl) {
     dt_kernel_body(dt, lambda_bits, err, dt_fixed, cfl);
+}
+
+// subcycling (S1): dt_l = dt_0 / 2^l for every level, from dt[0]
+__global__ void dt_levels_kernel(double* dt, int levels) {
+    for (int l = 1; l < levels; ++l) dt[l] = ldexp(dt[0], -l);
+}
+
+// subcycling (S3): flux registers of C/F sides accumulated over a step, acc = (assign ? 0 : acc) + w F-hat
+__global__ void accumulate_kernel(const AccTask* __restrict__ tasks, int ntasks, int n, const double* __restrict__ freg,
+                                  double* __restrict__ acc, double w_coarse, double w_fine, int assign_coarse,
+                                  int assign_fine) {
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)ntasks * 4 * n) return;
+    const int task = (int)(t / (4 * n)), e = (int)(t - (long long)task * 4 * n);
+    const AccTask at = tasks[task];
+    const size_t o = (((size_t)at.slot * 4 + at.side) * 4) * n + e;   // [slot][side][k][n], e = k n + along
+    const bool fine = at.kind == 2;
+    const double w = fine ? w_fine : w_coarse;
+    const double prev = (fine ? assign_fine : assign_coarse) ? 0.0 : acc[o];
+    acc[o] = prev + w * freg[o];
 }
 
 // dt of a graph-replayed step: (dt_fixed, cfl) read from device memory written by set2_kernel before the replay
@@ -2023,6 +2056,20 @@ cudaError_t launch_lambda(const LeafDesc* leaves, int nleaves, const AuxArgs& a,
 cudaError_t launch_dt_dev(double* dt, unsigned long long* lambda_bits, int32_t* err, const double* params,
                           cudaStream_t s) {
     dt_dev_kernel<<<1, 1, 0, s>>>(dt, lambda_bits, err, params);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_levels(double* dt, int levels, cudaStream_t s) {
+    dt_levels_kernel<<<1, 1, 0, s>>>(dt, levels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_accumulate(const AccTask* tasks, int ntasks, int n, const double* freg, double* acc, double w_coarse,
+                              double w_fine, int assign_coarse, int assign_fine, cudaStream_t s) {
+    if (ntasks <= 0) return cudaSuccess;
+    const long long work = (long long)ntasks * 4 * n;
+    accumulate_kernel<<<grid_for(work, 256), 256, 0, s>>>(tasks, ntasks, n, freg, acc, w_coarse, w_fine, assign_coarse,
+                                                          assign_fine);
     return cudaGetLastError();
 }
 

@@ -68,12 +68,13 @@ def run_pair(cfg, steps, cfl=None, dt=None, regrid_every=None, init=True, stats=
     assert e0 == 0.0, f"initial states differ: {e0}"
     worst = 0.0
     cfl = cfg.get("cfl", 0.5) if (cfl is None and dt is None) else cfl
+    sub = bool(cfg.get("subcycle", 0))
     for s in range(1, steps + 1):
         if dt is not None:
-            o.step(dt=dt)
+            o.step(dt=dt, subcycle=sub)
             g.step(dt=dt)
         else:
-            d1 = o.step(cfl=cfl)
+            d1 = o.step(cfl=cfl, subcycle=sub)
             d2 = g.step(cfl=cfl)
             assert abs(d1 - d2) <= 1e-10 * d1, (s, d1, d2)
         if check_each:
