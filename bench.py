@@ -333,8 +333,9 @@ def measure_quadrant(X, args, use_graphs=0):
 
 
 def measure_amr(X, cfg, workload):
-    """An AMR config: init protocol (A28), 2 untimed steps, then 8 CFL-0.5 steps with a regrid every 4 steps
-    inside the timed region (CUDA events on the library stream; the host regrid work is on the timeline)."""
+    """An AMR config: init protocol (A28), 4 untimed steps with one regrid, then 8 CFL-0.5 steps with a regrid
+    every 4 steps inside the timed region (CUDA events on the library stream; the host regrid work is on the
+    timeline); also the simulated time advanced per second."""
     torch = X.torch
     mesh = X.mesh(cfg)
     fn = lambda l, P, Q: W.patch_state(cfg, l, P, Q)   # noqa: E731
@@ -342,8 +343,10 @@ def measure_amr(X, cfg, workload):
     for _ in range(cfg["levels"] - 1):
         mesh.regrid()
         mesh.set_state(fn)
-    for s in range(2):
+    for s in range(4):                 # warm-up incl. one regrid (first launches load the regrid kernels)
         mesh.step(cfl=0.5)
+        if s == 1:
+            mesh.regrid()
     torch.cuda.synchronize()
     X.barrier()
     steps = 8
@@ -351,9 +354,10 @@ def measure_amr(X, cfg, workload):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(X.stream)
+    sim_t = 0.0
     for s in range(1, steps + 1):
         leaf_cells += mesh.stats()["leaf_cells"]
-        mesh.step(cfl=0.5, want_dt=False)
+        sim_t += mesh.step(cfl=0.5, want_dt=True)
         if s % 4 == 0:
             mesh.regrid()
     e1.record(X.stream)
@@ -362,8 +366,12 @@ def measure_amr(X, cfg, workload):
     cells = X.sum_over_ranks(leaf_cells)
     st = mesh.stats()
     mesh.close()
-    return {"value": cells * 3 / (ms / 1e3), "ms_per_step": ms / steps, "leaves": st["leaves"],
-            "patches": st["patches"], "leaf_cells_last": st["leaf_cells"], "workload": workload}
+    out = {"value": cells * 3 / (ms / 1e3), "ms_per_step": ms / steps, "leaves": st["leaves"],
+           "patches": st["patches"], "leaf_cells_last": st["leaf_cells"], "workload": workload,
+           "simulated_time_per_s": sim_t / (ms / 1e3)}
+    if cfg.get("subcycle"):
+        out["value_note"] = "leaf cell-updates counted once per level-0 step (finer levels update 2^l times)"
+    return out
 
 
 def main():
@@ -417,6 +425,10 @@ def main():
         extra["shock_bubble_amr"] = measure_amr(
             X, W.shock_bubble(), "BASELINE configs[3] shock-bubble AMR, 2048x1024 base, 4 levels, 16^2 patches, "
                                  "WENO5-char, reflective walls, 8 CFL-0.5 steps with 2 regrids inside the timed region")
+        if X.world == 1:   # NEXT #4: the same problem with Berger-Colella subcycling (level-0 steps)
+            extra["shock_bubble_amr_subcycled"] = measure_amr(
+                X, dict(W.shock_bubble(), subcycle=1),
+                "configs[3] with time subcycling: 8 level-0 steps (each = 8 finest-level steps), 2 regrids")
     if not args.no_sweep_table and X.world == 1:
         extra["sweep_table"] = {"workload": "BASELINE configs[4]: Central4 stage kernel per total size and patch size",
                                 "rows": measure_sweep_table(X, args, hbm_peak)}
