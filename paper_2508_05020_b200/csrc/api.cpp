@@ -189,11 +189,12 @@ amr_status build_plan(amr_ctx* c) {
     c->leaf_ids.clear();
     for (int id : c->canon)
         if (t.is_leaf(id) && c->comm.owns(c, id)) c->leaf_ids.push_back(id);
-    {   // (level, Morton key) computed once per leaf, then one sort of (key, id) pairs
-        std::vector<std::pair<std::pair<int32_t, uint64_t>, int32_t>> kv;
+    {   // packed (level, Morton key) computed once per leaf, then one radix sort of (key, id) pairs
+        std::vector<std::pair<uint64_t, int32_t>> kv;
         kv.reserve(c->leaf_ids.size());
-        for (int id : c->leaf_ids) kv.push_back({{t.lev[id], morton(t.pi[id], t.pj[id])}, id});
-        std::sort(kv.begin(), kv.end());
+        for (int id : c->leaf_ids)   // level in the top 6 bits; Morton of 29-bit coordinates below
+            kv.push_back({(uint64_t(t.lev[id]) << 58) | morton(t.pi[id], t.pj[id]), id});
+        radix_sort_pairs(kv);
         for (size_t e = 0; e < kv.size(); ++e) c->leaf_ids[e] = kv[e].second;
     }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;

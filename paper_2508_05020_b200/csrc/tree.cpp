@@ -57,7 +57,7 @@ void PatchTree::rollback() {
         for (int c = 0; c < 4; ++c) child[4 * sn.id + c] = sn.child[c];
     }
     for (const auto& sn : journal_)
-        if (sn.alive) { index_[key(sn.lev, sn.pi, sn.pj)] = sn.id; ++n_alive; }
+        if (sn.alive) { index_.set(key(sn.lev, sn.pi, sn.pj), sn.id); ++n_alive; }
     free_.clear();   // rare path: rebuild the free-slot heap
     for (int s = 0; s < capacity; ++s)
         if (!alive[s]) free_.push_back(s);
@@ -74,7 +74,7 @@ int PatchTree::alloc(int l, int i, int j) {
     touch(id);
     lev[id] = l; pi[id] = i; pj[id] = j; parent[id] = -1; alive[id] = 1;
     for (int c = 0; c < 4; ++c) child[4 * id + c] = -1;
-    index_[key(l, i, j)] = id;
+    index_.set(key(l, i, j), id);
     ++n_alive;
     return id;
 }
@@ -98,15 +98,13 @@ bool PatchTree::wrap(int l, int& i, int& j) const {
 
 int PatchTree::find(int l, int i, int j) const {
     if (l < 0 || l >= levels || !wrap(l, i, j)) return -1;
-    auto it = index_.find(key(l, i, j));
-    return it == index_.end() ? -1 : it->second;
+    return index_.find(key(l, i, j));
 }
 
 int PatchTree::neighbour(int id, int dx, int dy) const {
     int l = lev[id], i = pi[id] + dx, j = pj[id] + dy;
     if (!wrap(l, i, j)) return -2;
-    auto it = index_.find(key(l, i, j));
-    return it == index_.end() ? -1 : it->second;
+    return index_.find(key(l, i, j));
 }
 
 // Alg. 1 RefinePatch: before creating p's children make every
@@ -174,8 +172,10 @@ bool PatchTree::validate(std::string& err) const {
     for (int j = 0; j < np0[1]; ++j)
         for (int i = 0; i < np0[0]; ++i)
             if (find(0, i, j) < 0) { err = "R1 violated: root missing"; return false; }
-    for (const auto& kv : index_) {   // the active patches (O(active), not O(capacity))
-        const int id = kv.second;
+    std::vector<int32_t> ids;   // the active patches (O(active), not O(capacity))
+    ids.reserve(index_.size());
+    index_.for_each([&](uint64_t, int32_t id) { ids.push_back(id); });
+    for (int id : ids) {
         if (!alive[id]) { err = "index refers to a free slot"; return false; }
         if (lev[id] > 0) {
             int p = parent[id];
@@ -195,9 +195,8 @@ bool PatchTree::validate(std::string& err) const {
 std::vector<int32_t> PatchTree::canonical() const {
     std::vector<std::pair<uint64_t, int32_t>> kv;   // key (level, j, i) = the map key: one sort of pairs
     kv.reserve(n_alive);
-    for (int id = 0; id < capacity; ++id)
-        if (alive[id]) kv.push_back({key(lev[id], pi[id], pj[id]), id});
-    std::sort(kv.begin(), kv.end());
+    index_.for_each([&](uint64_t k, int32_t id) { kv.push_back({k, id}); });
+    radix_sort_pairs(kv);
     std::vector<int32_t> ids(kv.size());
     for (size_t e = 0; e < kv.size(); ++e) ids[e] = kv[e].second;
     return ids;

@@ -6,12 +6,100 @@
 // and the coarsening pass of Alg. 2 / its prose condition.
 // Independent of oracle/ (no shared code).
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
 namespace amr {
+
+// Open-addressing hash map uint64 key -> int32 id (linear probing, backward-shift deletion): the patch index of the
+// tree.  Keys are never ~0ull (the empty marker); the table stays at most half full.
+class FlatIndex {
+  public:
+    void clear() { keys_.assign(keys_.size(), kEmpty); size_ = 0; }
+    void reserve(size_t n) {
+        size_t cap = 16;
+        while (cap < 2 * n) cap <<= 1;
+        if (cap > keys_.size()) rehash(cap);
+    }
+    int32_t find(uint64_t k) const {
+        if (keys_.empty()) return -1;
+        for (size_t i = hash(k) & mask(); ; i = (i + 1) & mask()) {
+            if (keys_[i] == k) return vals_[i];
+            if (keys_[i] == kEmpty) return -1;
+        }
+    }
+    void set(uint64_t k, int32_t v) {
+        if (2 * (size_ + 1) > keys_.size()) rehash(keys_.empty() ? 16 : 2 * keys_.size());
+        size_t i = hash(k) & mask();
+        while (keys_[i] != kEmpty && keys_[i] != k) i = (i + 1) & mask();
+        if (keys_[i] == kEmpty) ++size_;
+        keys_[i] = k;
+        vals_[i] = v;
+    }
+    void erase(uint64_t k) {
+        if (keys_.empty()) return;
+        size_t i = hash(k) & mask();
+        while (keys_[i] != k) {
+            if (keys_[i] == kEmpty) return;
+            i = (i + 1) & mask();
+        }
+        // backward-shift deletion keeps every probe chain contiguous
+        size_t j = i;
+        for (;;) {
+            j = (j + 1) & mask();
+            if (keys_[j] == kEmpty) break;
+            const size_t h = hash(keys_[j]) & mask();
+            const bool move = (j > i) ? (h <= i || h > j) : (h <= i && h > j);
+            if (move) { keys_[i] = keys_[j]; vals_[i] = vals_[j]; i = j; }
+        }
+        keys_[i] = kEmpty;
+        --size_;
+    }
+    size_t size() const { return size_; }
+    template <class F>
+    void for_each(F f) const {
+        for (size_t i = 0; i < keys_.size(); ++i)
+            if (keys_[i] != kEmpty) f(keys_[i], vals_[i]);
+    }
+
+  private:
+    static constexpr uint64_t kEmpty = ~0ull;
+    std::vector<uint64_t> keys_;
+    std::vector<int32_t> vals_;
+    size_t size_ = 0;
+    size_t mask() const { return keys_.size() - 1; }
+    static size_t hash(uint64_t k) { k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; return (size_t)k; }
+    void rehash(size_t cap) {
+        std::vector<uint64_t> ok;
+        std::vector<int32_t> ov;
+        ok.swap(keys_);
+        ov.swap(vals_);
+        keys_.assign(cap, kEmpty);
+        vals_.assign(cap, -1);
+        size_ = 0;
+        for (size_t i = 0; i < ok.size(); ++i)
+            if (ok[i] != kEmpty) set(ok[i], ov[i]);
+    }
+};
+
+// LSD radix sort of (key, id) pairs by key, 16-bit digits; a digit shared by every key is skipped.  Keys are
+// unique in every use (patch keys, level-Morton keys), so the order is the plain key order.
+inline void radix_sort_pairs(std::vector<std::pair<uint64_t, int32_t>>& v) {
+    std::vector<std::pair<uint64_t, int32_t>> tmp(v.size());
+    std::vector<uint32_t> cnt(65536);
+    for (int shift = 0; shift < 64; shift += 16) {
+        std::fill(cnt.begin(), cnt.end(), 0u);
+        for (const auto& e : v) ++cnt[(e.first >> shift) & 0xffff];
+        if (!v.empty() && cnt[(v[0].first >> shift) & 0xffff] == v.size()) continue;
+        uint32_t sum = 0;
+        for (auto& c : cnt) { const uint32_t x = c; c = sum; sum += x; }
+        for (const auto& e : v) tmp[cnt[(e.first >> shift) & 0xffff]++] = e;
+        v.swap(tmp);
+    }
+}
 
 struct PatchTree {
     // geometry
@@ -65,7 +153,7 @@ struct PatchTree {
     std::vector<uint8_t> touched_;
     bool txn_ = false;
     void touch(int id);
-    std::unordered_map<uint64_t, int32_t> index_;
+    FlatIndex index_;
     std::vector<int32_t> free_;   // min-heap of free slots
     int alloc(int l, int i, int j);
     void release(int id);
