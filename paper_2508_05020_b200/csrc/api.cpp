@@ -198,6 +198,15 @@ amr_status build_plan(amr_ctx* c) {
         for (size_t e = 0; e < kv.size(); ++e) c->leaf_ids[e] = kv[e].second;
     }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
+    c->sib.clear();   // owned parents whose 4 children are (owned) leaves: the coarsening candidates of a12
+    for (int id : c->canon) {
+        if (!t.has_children(id)) continue;
+        int q = 0;
+        while (q < 4 && c->leaf_pos[t.child[4 * id + q]] >= 0) ++q;
+        if (q < 4) continue;
+        c->sib.push_back(id);
+        for (q = 0; q < 4; ++q) c->sib.push_back(c->leaf_pos[t.child[4 * id + q]]);
+    }
     clk.mark("plan: canon + leaf order");
 
     static const int dirs[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
@@ -320,6 +329,9 @@ amr_status build_plan(amr_ctx* c) {
     CU(c->freg.reserve((size_t)t.capacity * 16 * c->n));   // indexed by slot (remote fine leaves arrive by exchange)
     CU(c->d_maxeta.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_amb.reserve(std::max<size_t>(1, c->leaves.size())));
+    CU(c->d_sib.upload(c->sib, c->stream));
+    CU(c->d_flist.reserve(2 * (c->leaves.size() + c->sib.size() / 5) + 2));
+    CU(c->d_fcount.reserve(1));
     CU(c->d_partial.reserve(4 * std::max<size_t>(1, c->leaves.size())));
     CU(cudaStreamSynchronize(s));   // host vectors may change after return
     clk.mark("plan: uploads");
@@ -603,6 +615,39 @@ amr_status evaluate_flags(amr_ctx* c) {
     return AMR_OK;
 }
 
+// Refine / coarsen requests of the current state with device-side compaction (single rank): the flag kernel's
+// per-leaf eta stays on the device and only the (slot, bits) list of actual requests comes back.  The requests
+// equal evaluate_flags' fl_ref / fl_crs (same comparisons on the same doubles); gpu test test_regrid_compact_*.
+amr_status flag_requests(amr_ctx* c, std::vector<uint8_t>& ref, std::vector<uint8_t>& crs) {
+    double* Un = c->U[c->un];
+    amr_status s = fill_ghosts(c, Un);
+    if (s != AMR_OK) return s;
+    AuxArgs a = aux(c, Un, nullptr);
+    const int nl = (int)c->leaves.size(), ns = (int)c->sib.size() / 5;
+    LAUNCH(launch_flags(c->d_leaves.p, nl, a, c->d_maxeta.p, c->d_amb.p, c->stream), "flags");
+    const double th = c->cfg.refine_threshold, tc = th * c->cfg.coarsen_fraction;
+    LAUNCH(launch_flags_compact(c->d_leaves.p, nl, c->d_sib.p, ns, c->d_maxeta.p, th, tc, c->cfg.num_levels - 1,
+                                c->d_flist.p, c->d_fcount.p, c->stream), "flags compact");
+    int32_t cnt = 0;
+    CU(cudaMemcpyAsync(&cnt, c->d_fcount.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (cnt < 0 || cnt > nl + ns) return fail(c, AMR_E_CUDA, "flags compact: bad request count");
+    std::vector<int32_t> lst(2 * (size_t)cnt);
+    if (cnt) {
+        CU(cudaMemcpyAsync(lst.data(), c->d_flist.p, lst.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    ref.assign(c->tree.capacity, 0);
+    crs.assign(c->tree.capacity, 0);
+    for (int32_t k = 0; k < cnt; ++k) {
+        const int id = lst[2 * k], b = lst[2 * k + 1];
+        if (id < 0 || id >= c->tree.capacity) return fail(c, AMR_E_CUDA, "flags compact: bad slot");
+        if (b & 1) ref[id] = 1;
+        if (b & 2) crs[id] = 1;
+    }
+    return AMR_OK;
+}
+
 // refinement pass, coarsening pass, validation, new-patch prolongation, restriction
 amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::vector<uint8_t>& crs, int32_t* nr,
                         int32_t* nc) {
@@ -835,7 +880,7 @@ void amr_destroy(amr_ctx* c) {
     for (auto& d : c->d_rlev) d.release();
     c->proxy.release(); c->freg.release(); c->staging.release(); c->d_maxeta.release(); c->d_partial.release();
     c->unf_scratch.release();
-    c->d_slots.release(); c->d_amb.release();
+    c->d_slots.release(); c->d_amb.release(); c->d_sib.release(); c->d_flist.release(); c->d_fcount.release();
     if (c->own_pool) cudaFree(c->own_pool);
     cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp); cudaFree(c->d_dtp);
     for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);
@@ -1223,10 +1268,17 @@ amr_status amr_regrid(amr_ctx* c, int32_t* n_refined, int32_t* n_coarsened) {
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     PhaseClock clk;
-    s = evaluate_flags(c);
-    if (s != AMR_OK) return s;
+    std::vector<uint8_t> ref, crs;
+    if (c->comm.world == 1) {
+        s = flag_requests(c, ref, crs);
+        if (s != AMR_OK) return s;
+    } else {   // ranks exchange full per-leaf flags (Comm::allgather_flags)
+        s = evaluate_flags(c);
+        if (s != AMR_OK) return s;
+        ref = c->fl_ref;
+        crs = c->fl_crs;
+    }
     clk.mark("flags");
-    std::vector<uint8_t> ref = c->fl_ref, crs = c->fl_crs;
     return apply_regrid(c, ref, crs, n_refined, n_coarsened);
 }
 

@@ -72,6 +72,7 @@ struct amr_ctx {
     std::vector<int32_t> canon, canon_pos;      // canonical order; id -> tree index
     std::vector<int32_t> leaf_ids;               // launch order
     std::vector<int32_t> leaf_pos;               // id -> leaf index or -1
+    std::vector<int32_t> sib;                    // sibling groups: parent id + its 4 leaf children's leaf indices
     std::vector<LeafDesc> leaves;
     std::vector<LeafDesc> gleaves, singles;        // Central4 n = 8, 16: 32 x 32 blocks of leaves / the rest
     DevArray<LeafDesc> d_gleaves, d_singles;
@@ -84,7 +85,7 @@ struct amr_ctx {
     std::vector<DevArray<RestrictTask>> d_rlev;
     DevArray<ProlongTask> d_prolong;
     DevArray<double> proxy, freg, staging, d_maxeta, d_partial, unf_scratch;
-    DevArray<int32_t> d_slots, d_amb;
+    DevArray<int32_t> d_slots, d_amb, d_sib, d_flist, d_fcount;
     DevArray<int32_t> x_sidx, x_ridx;             // multi-rank exchange slot lists
     DevArray<double> x_send, x_recv;              // multi-rank exchange buffers
     int64_t leaf_cells = 0;

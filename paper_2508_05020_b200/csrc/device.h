@@ -144,6 +144,10 @@ cudaError_t launch_accumulate(const AccTask* tasks, int ntasks, int n, const dou
                               double w_fine, int assign_coarse, int assign_fine, cudaStream_t s);
 cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* maxeta, int32_t* amb,
                          cudaStream_t s);
+// compact (slot, bits) list of the refine (bit 0) / coarsen (bit 1) requests; count is reset on the stream first
+cudaError_t launch_flags_compact(const LeafDesc* leaves, int nleaves, const int32_t* sib, int nsib,
+                                 const double* maxeta, double th, double tc, int top, int32_t* list, int32_t* count,
+                                 cudaStream_t s);
 cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* partial, cudaStream_t s);
 
 // slot-granular copies between a packed [npatch][per] buffer and per-slot arrays (state: per = 4 n^2;

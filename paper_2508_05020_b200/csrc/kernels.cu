@@ -2091,6 +2091,50 @@ cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, 
     return cudaGetLastError();
 }
 
+// Flag compaction: one thread per leaf and per sibling group (a parent whose 4 children are leaves);
+// the refine bit of a leaf, eta > theta below the finest level, and the coarsen bit of a sibling group,
+// max child eta < theta * coarsen_fraction (Alg. 2 / A15), are appended as (slot, bits) to a compact list with one
+// atomic per warp, so the host reads only the requests.  Same comparisons and NaN handling as the full host path.
+__global__ void flags_compact_kernel(const LeafDesc* __restrict__ leaves, int nleaves, const int32_t* __restrict__ sib,
+                                     int nsib, const double* __restrict__ maxeta, double th, double tc, int top,
+                                     int32_t* list, int32_t* count) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    int slot = -1, bits = 0;
+    if (k < nleaves) {
+        const double e = maxeta[k];
+        if (leaves[k].level < top && e > th) { slot = leaves[k].slot; bits = 1; }
+    } else if (k - nleaves < nsib) {
+        const int32_t* g = sib + 5 * (k - nleaves);
+        double m = 0.0;
+        for (int q = 0; q < 4; ++q) {
+            const double e = maxeta[g[1 + q]];
+            if (!(e <= m)) m = e;
+        }
+        if (m < tc) { slot = g[0]; bits = 2; }
+    }
+    const unsigned want = __ballot_sync(0xffffffffu, bits != 0);
+    if (!want) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(want) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count, __popc(want));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (bits) {
+        const int at = base + __popc(want & ((1u << lane) - 1u));
+        list[2 * at] = slot;
+        list[2 * at + 1] = bits;
+    }
+}
+
+cudaError_t launch_flags_compact(const LeafDesc* leaves, int nleaves, const int32_t* sib, int nsib,
+                                 const double* maxeta, double th, double tc, int top, int32_t* list, int32_t* count,
+                                 cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess || nleaves + nsib <= 0) return e;
+    flags_compact_kernel<<<grid_for((long long)nleaves + nsib, 256), 256, 0, s>>>(leaves, nleaves, sib, nsib, maxeta,
+                                                                                   th, tc, top, list, count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int per, cudaStream_t s) {
     if (npatch <= 0) return cudaSuccess;
     long long total = (long long)npatch * per;
