@@ -297,6 +297,9 @@ amr_status build_plan(amr_ctx* c) {
             }
             if (ok) {
                 c->gleaves.insert(c->gleaves.end(), c->leaves.begin() + e, c->leaves.begin() + e + K);
+                bool contig = true;   // members in consecutive slots: the block is one contiguous run of the pool
+                for (int m = 1; m < K; ++m) contig = contig && c->leaf_ids[e + m] == id0 + m;
+                if (contig) c->gleaves[c->gleaves.size() - K].pad |= 2;
                 e += K;
             } else {
                 c->singles.push_back(c->leaves[e]);

@@ -97,7 +97,8 @@ struct StageArgs {
     const LeafDesc* gleaves;   // n = 8, 16 Central4: members of 32 x 32 blocks [ngroups][(32/n)^2] (Morton order);
     int32_t ngroups;           //   leaves / nleaves then list only the leaves outside complete blocks
     int32_t prof;              // phase timing of the TMA kernel (AMR_PHASE_PROF, debug)
-    int32_t lam0;              // subcycling: Lambda normalised to level 0 (S6); LeafDesc.pad bit 0 = covered patch
+    int32_t lam0;              // subcycling: Lambda normalised to level 0 (S6); LeafDesc.pad bit 0 = covered patch;
+                               // group tiles: pad bit 1 of member 0 = members in consecutive slots
     Geometry geo;
 };
 

@@ -795,6 +795,25 @@ __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, 
         : "memory");
 }
 
+// 1D bulk copies (cp.async.bulk, no tensor map) for boxes that are one contiguous run of the pool: the whole
+// [4][n][n] patch of a 32^2 patch, or K consecutive slots of a group
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_prefetch(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+#ifdef AMR_NO_BULK1D
+constexpr bool kBulk1D = false;
+#else
+constexpr bool kBulk1D = true;
+#endif
+
 constexpr int kTmaThreads = 512;
 // optional phase timing (build with AMR_NVCC_FLAGS=-DAMR_PHASE_PROF, run with AMR_PHASE_PROF=1): per-warp
 // cycle counts of the kernel phases, printed per launch by the launcher
@@ -891,7 +910,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const uint32_t mb = smem_u32(&mbar[b]);
         const uint32_t dst = smem_u32(land + b * kLandSz);
         mbar_expect_tx(mb, kLandSz * 8);
-        tma_load3(dst + kLandI * 8, &maps.in_int, tx * T, ty * T, 4 * d.slot, mb);
+        if (kBulk1D && TILES == 1) bulk_load(dst + kLandI * 8, a.Uin + (size_t)d.slot * 4 * N * N, 4 * N * N * 8, mb);
+        else tma_load3(dst + kLandI * 8, &maps.in_int, tx * T, ty * T, 4 * d.slot, mb);
         const CUtensorMap* mw = &maps.in_we;
         int i0 = tx * T - G, z = 4 * d.slot;
         if (tx == 0) { i0 = N - G; const int s = d.side[kW]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); mw = &maps.px_we; } }
@@ -924,7 +944,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         dn = *desc_ptr(blockIdx.x);
         if (tid == 0) {
             issue(blockIdx.x, 0, dn);
-            if (rk_un) tma_prefetch3(&maps.un_int, 0, 0, 4 * dn.slot);   // (tile offsets added below for N = 64)
+            if (rk_un) {                     // (tile offsets added below for N = 64)
+                if (kBulk1D && TILES == 1) bulk_prefetch(a.Un + (size_t)dn.slot * 4 * N * N, 4 * N * N * 8);
+                else tma_prefetch3(&maps.un_int, 0, 0, 4 * dn.slot);
+            }
         }
     }
 
@@ -987,13 +1010,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 issue(t + gridDim.x, b ^ 1, dn);
                 if (rk_un) {                     // U^n of tile k+1 towards L2
                     const int t2 = t + gridDim.x, tt2 = TILES == 1 ? 0 : t2 % TT;
-                    tma_prefetch3(&maps.un_int, (tt2 % TILES) * T, (tt2 / TILES) * T, 4 * dn.slot);
+                    if (kBulk1D && TILES == 1) bulk_prefetch(a.Un + (size_t)dn.slot * 4 * N * N, 4 * N * N * 8);
+                    else tma_prefetch3(&maps.un_int, (tt2 % TILES) * T, (tt2 / TILES) * T, 4 * dn.slot);
                 }
             }
             if (rk_un) {                         // U^n of tile k into the converted landing[b] interior
                 const uint32_t mb = smem_u32(&mbar[2 + b]);
                 mbar_expect_tx(mb, 4 * T * T * 8);
-                tma_load3(smem_u32(land + b * kLandSz + kLandI), &maps.un_int, tx * T, ty * T, 4 * d.slot, mb);
+                if (kBulk1D && TILES == 1) bulk_load(smem_u32(land + b * kLandSz + kLandI), a.Un + (size_t)d.slot * 4 * N * N, 4 * N * N * 8, mb);
+                else tma_load3(smem_u32(land + b * kLandSz + kLandI), &maps.un_int, tx * T, ty * T, 4 * d.slot, mb);
             }
         }
         PH_MARK(4);
@@ -1094,7 +1119,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             }
         }
         __syncthreads();   // (C) U^(s) of the tile complete in shared memory
-        if (tid == 0) tma_store3(&maps.out_int, tx * T, ty * T, 4 * d.slot, smem_u32(sU));
+        if (tid == 0) {
+            if (kBulk1D && TILES == 1) bulk_store(a.Uout + (size_t)d.slot * 4 * N * N, smem_u32(sU), 4 * N * N * 8);
+            else tma_store3(&maps.out_int, tx * T, ty * T, 4 * d.slot, smem_u32(sU));
+        }
         PH_MARK(7);
     }
     if (tid == 0) bulk_wait0();
@@ -1374,6 +1402,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const double ca = a.a, cb = a.b;
     const double dt = *a.dt;
     const int stride = gridDim.x;
+#ifdef AMR_PHASE_PROF
+    const bool prof = a.prof;
+    long long ph_t = clock64();
+    long long ph_acc[8] = {};
+#endif
 
     // warp 0: arm the landing barrier, then one box per lane (interior of member `lane`, or one edge strip)
     auto issue = [&](int b, const LeafDesc* D) {
@@ -1382,7 +1415,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         if (lane == 0) mbar_expect_tx(mb, kLandSz * 8);
         __syncwarp();
         if (lane < K) {
-            tma_load3(dst + (kLandI + lane * 4 * NN) * 8, &maps.in_int, 0, 0, 4 * D[lane].slot, mb);
+            if (kBulk1D && (D[0].pad & 2)) {   // consecutive member slots: the K interiors are one pool run
+                if (lane == 0) bulk_load(dst + kLandI * 8, a.Uin + (size_t)D[0].slot * 4 * NN, K * 4 * NN * 8, mb);
+            } else {
+                tma_load3(dst + (kLandI + lane * 4 * NN) * 8, &maps.in_int, 0, 0, 4 * D[lane].slot, mb);
+            }
         } else if (lane < K + 4 * B) {
             const int e = lane - K, side = e / B, r = e - side * B;
             const int m = side == kW ? gm_of(0, r) : side == kE ? gm_of(B - 1, r) : side == kS ? gm_of(r, 0) : gm_of(r, B - 1);
@@ -1434,7 +1471,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const LeafDesc* D = sDesc + b * K;
         if (warp == 1 && t + stride < ntiles) fetch_desc(t + stride, b ^ 1);
         const double* L = land + b * kLandSz;
+        PH_MARK(0);
         mbar_wait(smem_u32(&mbar[b]), (uint32_t)((k >> 1) & 1));
+        PH_MARK(1);
         auto c2p = [&](double r, double m, double w, double E, int o) {
             const double ir = fast_rcp(r);
             const double u = m * ir, v = w * ir;
@@ -1471,7 +1510,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             c2p(s[0], s[4 * N], s[8 * N], s[12 * N], (j + G) * WP + i + G);   // strip plane = 4 N doubles
         }
         if (warp == 1) cp_async_wait_all();      // member descriptors of tile k+1 before (A)
+        PH_MARK(2);
         __syncthreads();   // (A)
+        PH_MARK(3);
         if (warp == 0) {
             if (lane < K) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1480,16 +1521,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             __syncwarp();
             if (t + stride < ntiles) {
                 issue(b ^ 1, sDesc + (b ^ 1) * K);
-                if (rk_un && lane < K) tma_prefetch3(&maps.un_int, 0, 0, 4 * sDesc[(b ^ 1) * K + lane].slot);
+                const LeafDesc* Dn = sDesc + (b ^ 1) * K;
+                if (rk_un && lane < K) {
+                    if (kBulk1D && (Dn[0].pad & 2)) { if (lane == 0) bulk_prefetch(a.Un + (size_t)Dn[0].slot * 4 * NN, K * 4 * NN * 8); }
+                    else tma_prefetch3(&maps.un_int, 0, 0, 4 * Dn[lane].slot);
+                }
             }
             if (rk_un) {                         // U^n of tile k into the converted landing[b] interior
                 const uint32_t mb = smem_u32(&mbar[2 + b]);
                 if (lane == 0) mbar_expect_tx(mb, 4 * T * T * 8);
                 __syncwarp();
-                if (lane < K)
+                if (kBulk1D && (D[0].pad & 2)) {
+                    if (lane == 0) bulk_load(smem_u32(land + b * kLandSz + kLandI), a.Un + (size_t)D[0].slot * 4 * NN, K * 4 * NN * 8, mb);
+                } else if (lane < K) {
                     tma_load3(smem_u32(land + b * kLandSz + kLandI + lane * 4 * NN), &maps.un_int, 0, 0, 4 * D[lane].slot, mb);
+                }
             }
         }
+        PH_MARK(4);
         {
             const int m0 = seg * 5 - 1;
             const int lvl = D[0].level;
@@ -1550,7 +1599,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 }
             }
         }
+        PH_MARK(5);
         __syncthreads();   // (B)
+        PH_MARK(6);
         const int lvl = D[0].level;
         const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
         double* const sU = land + b * kLandSz + kLandI;
@@ -1588,13 +1639,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             }
         }
         __syncthreads();   // (C) U^(s) of the tile complete in shared memory
-        if (warp == 0 && lane < K) tma_store3(&maps.out_int, 0, 0, 4 * D[lane].slot, smem_u32(sU + lane * 4 * NN));
+        if (warp == 0 && lane < K) {
+            if (kBulk1D && (D[0].pad & 2)) { if (lane == 0) bulk_store(a.Uout + (size_t)D[0].slot * 4 * NN, smem_u32(sU), K * 4 * NN * 8); }
+            else tma_store3(&maps.out_int, 0, 0, 4 * D[lane].slot, smem_u32(sU + lane * 4 * NN));
+        }
+        PH_MARK(7);
     }
     if (warp == 0 && lane < K) bulk_wait0();
     if (a.want_lambda) {
         lam = warp_max_u64(lam);
         if (lane == 0 && lam) atomicMax(a.lambda_bits, lam);
     }
+#ifdef AMR_PHASE_PROF
+    if (prof && lane == 0)
+        for (int p = 0; p < 8; ++p) atomicAdd(&g_phase[warp][p], (unsigned long long)ph_acc[p]);
+#endif
 }
 
 template <int N, bool DIV4>
@@ -1622,7 +1681,29 @@ cudaError_t launch_c4_group_t(const StageArgs& a, cudaStream_t s) {
     StageArgs ag = a;
     ag.leaves = a.gleaves;
     const int grid = ntiles < sm_count() ? ntiles : sm_count();
+#ifdef AMR_PHASE_PROF
+    static const bool prof = getenv("AMR_PHASE_PROF") != nullptr;
+    ag.prof = prof ? 1 : 0;
+    if (prof) {
+        static unsigned long long zero[16][8] = {};
+        cudaMemcpyToSymbolAsync(g_phase, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s);
+    }
     stage_c4_group_kernel<N, DIV4><<<grid, kTmaThreads, kTmaGroupSmem, s>>>(ag, m, ntiles);
+    if (prof) {
+        unsigned long long h[16][8];
+        cudaMemcpyFromSymbolAsync(h, g_phase, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const double per = (double)grid * ((ntiles + grid - 1) / grid);
+        fprintf(stderr, "group N=%d stage %d phase cycles per tile [top, mbar, c2p, waitA, issue, faces, waitB, epi]:\n", N, a.stage);
+        for (int w = 0; w < 16; w += 5) {
+            fprintf(stderr, "  w%02d", w);
+            for (int p = 0; p < 8; ++p) fprintf(stderr, " %6.0f", h[w][p] / per);
+            fprintf(stderr, "\n");
+        }
+    }
+#else
+    stage_c4_group_kernel<N, DIV4><<<grid, kTmaThreads, kTmaGroupSmem, s>>>(ag, m, ntiles);
+#endif
     return cudaGetLastError();
 }
 

@@ -10,6 +10,16 @@ namespace {
 // Fig. 2 nbr order: N, E, S, W, NE, SE, SW, NW
 const int kMoore[8][2] = {{0, 1}, {1, 0}, {0, -1}, {-1, 0}, {1, 1}, {1, -1}, {-1, -1}, {-1, 1}};
 inline int pmod(int a, int b) { int r = a % b; return r < 0 ? r + b : r; }
+uint64_t spread(uint32_t v) {
+    uint64_t x = v;
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+uint64_t morton_key(uint32_t x, uint32_t y) { return spread(x) | (spread(y) << 1); }
 }  // namespace
 
 void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, int rule) {
@@ -24,9 +34,14 @@ void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, 
     free_.clear();
     for (int s = cap - 1; s >= 0; --s) free_.push_back(s);
     std::make_heap(free_.begin(), free_.end(), std::greater<int32_t>());
-    // R1: the permanent root scaffold, created row by row
+    // R1: the permanent root scaffold, allocated in Morton order of (i, j) so that every aligned 2^k x 2^k block
+    // of roots occupies consecutive slots (the Central4 group kernel then moves a block with one bulk copy)
+    std::vector<std::pair<uint64_t, int32_t>> kv;
+    kv.reserve((size_t)npx * npy);
     for (int j = 0; j < npy; ++j)
-        for (int i = 0; i < npx; ++i) alloc(0, i, j);
+        for (int i = 0; i < npx; ++i) kv.push_back({morton_key(i, j), j * npx + i});
+    radix_sort_pairs(kv);
+    for (const auto& e : kv) alloc(0, e.second % npx, e.second / npx);
 }
 
 void PatchTree::touch(int id) {
