@@ -168,7 +168,7 @@ class Ctx:
         if self.world > 1:
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
         from paper_2508_05020_b200 import build as B
-        if self.rank == 0:
+        if self.rank == 0 and not os.path.exists(B.OUT):   # an existing library is used as built (flags kept)
             B.build()
         self.barrier()
         import paper_2508_05020_b200 as amr

@@ -61,6 +61,10 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         inc += ["-I", nccl_inc, "-DAMR_HAVE_NCCL_H=1"]
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"] + ARCH + inc
     common += os.environ.get("AMR_NVCC_FLAGS", "").split()   # e.g. -DAMR_PHASE_PROF (kernel phase timing)
+    stamp = os.path.join(BUILD, "flags.txt")   # objects built with other flags are stale
+    prev = open(stamp).read() if os.path.exists(stamp) else None
+    if prev != " ".join(common):
+        force = True
     objs, jobs = [], []
     hdrs = headers()
     for src in sources():
@@ -89,6 +93,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         cmd = [NVCC, "-shared", "-o", OUT + ".tmp"] + objs + ARCH + ["-cudart=static", "-ldl", "-lpthread"]
         subprocess.check_call(cmd)
         os.replace(OUT + ".tmp", OUT)
+    with open(stamp, "w") as f:
+        f.write(" ".join(common))
     return OUT
 
 
