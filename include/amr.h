@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define AMR_ABI_VERSION 1
+#define AMR_ABI_VERSION 2
 
 typedef struct amr_ctx amr_ctx;   /* opaque */
 
@@ -97,6 +97,14 @@ typedef struct {
                                      refluxed with quadrature-weighted registers; dt / cfl of amr_step refer to
                                      level 0 and amr_diagnostics' lambda is normalised to level 0.  Single rank;
                                      a non-physical step is reported (AMR_E_NONPHYSICAL) but only level 0 rolls back */
+    int32_t halo_mode;            /* world_size > 1, halo and flux-register exchanges (NEXT #3): 0 pack kernel +
+                                     transport point-to-point (NCCL send/recv, or loopback copies) + unpack kernel;
+                                     1 peer pull: at amr_create every rank maps every other rank's state pool (CUDA
+                                     IPC handles exchanged over NCCL; directly for loopback virtual ranks), and each
+                                     exchange is a stream-ordered cross-rank fence (a one-word NCCL allreduce, or
+                                     CUDA events between loopback streams) followed by ONE kernel that loads the
+                                     needed slots from the owners' pools over NVLink into the local pool.  Regrid
+                                     exchanges (coarse sources, migration, flags) use the transport in both modes */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none

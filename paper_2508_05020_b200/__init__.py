@@ -26,6 +26,7 @@ SCHEME = {"central4": 0, "weno5": 1}
 COARSEN = {"r2_exact": 0, "alg2_literal": 1}
 
 # every symbol include/amr.h declares (checked by tests/test_abi.py)
+ABI_VERSION = 2   # include/amr.h AMR_ABI_VERSION: the amr_config layout below
 ABI_SYMBOLS = ["amr_abi_version", "amr_default_config", "amr_query_pool_bytes", "amr_create", "amr_destroy",
                "amr_set_state", "amr_set_state_fn", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
                "amr_regrid", "amr_regrid_with_flags", "amr_get_patch_tree", "amr_diagnostics",
@@ -42,7 +43,8 @@ class amr_config(C.Structure):
                 ("max_patches", C.c_int32), ("pool", C.c_void_p), ("pool_bytes", C.c_uint64),
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("world_size", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("check_positivity", C.c_int32),
-                ("use_graphs", C.c_int32), ("comm_backend", C.c_int32), ("stage_kernel", C.c_int32), ("subcycle", C.c_int32)]
+                ("use_graphs", C.c_int32), ("comm_backend", C.c_int32), ("stage_kernel", C.c_int32), ("subcycle", C.c_int32),
+                ("halo_mode", C.c_int32)]
 
 
 class amr_patch_desc(C.Structure):
@@ -77,6 +79,8 @@ def load(path: str = LIB_PATH):
                            "(there is no CPU fallback)")
     L = C.CDLL(path)
     L.amr_abi_version.restype = C.c_int32
+    if L.amr_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{path}: ABI version {L.amr_abi_version()} != {ABI_VERSION} (rebuild the library)")
     L.amr_default_config.argtypes = [C.POINTER(amr_config)]
     L.amr_query_pool_bytes.argtypes = [C.POINTER(amr_config), C.POINTER(C.c_uint64)]
     L.amr_create.argtypes = [C.POINTER(amr_config), C.POINTER(_P)]
@@ -149,6 +153,7 @@ def make_config(cfg: dict, **over) -> amr_config:
     c.stage_kernel = int(cfg.get("stage_kernel", 0))
     c.use_graphs = int(cfg.get("use_graphs", 0))
     c.subcycle = int(cfg.get("subcycle", 0))
+    c.halo_mode = int(cfg.get("halo_mode", 0))
     c.world_size = 1
     c.rank = 0
     c.device = -1

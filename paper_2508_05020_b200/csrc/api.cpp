@@ -73,6 +73,7 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
     if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }
     if (c.subcycle && c.world_size > 1) { m = "subcycling is single-rank in this build"; return AMR_E_CONFIG; }
+    if (c.halo_mode != 0 && c.halo_mode != 1) { m = "halo_mode must be 0 or 1"; return AMR_E_CONFIG; }
     return AMR_OK;
 }
 
@@ -862,6 +863,7 @@ amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
     CU(cudaMemsetAsync(c->d_err, 0, 16, c->stream));
     CU(cudaMallocHost(&c->h_pinned, 64));
     amr_status s = c->comm.init(c);
+    if (s == AMR_OK && c->comm.world > 1 && c->comm.halo_mode == 1) s = c->comm.map_pool(c, base, need);
     if (s != AMR_OK) {
         std::fprintf(stderr, "amr_create: %s\n", c->err.c_str());
         return s;

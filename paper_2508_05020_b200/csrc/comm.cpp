@@ -161,6 +161,10 @@ struct Transport {
     virtual std::string p2p(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) = 0;
     // in-place allreduce on a device buffer; kind 0: max u64, 1: max f64, 2: sum f64, 3: max i32
     virtual std::string allreduce(void* d, size_t count, int kind, cudaStream_t s) = 0;
+    // halo_mode 1: map every rank's device buffer [base, base + bytes) into this process (out[rank] = base)
+    virtual std::string map_peers(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s) = 0;
+    // stream-ordered cross-rank fence: work queued after it on s runs after every rank's work queued before it
+    virtual std::string fence(cudaStream_t s) = 0;
 };
 
 // ---- NCCL (torch's libnccl.so.2, resolved at run time)
@@ -175,6 +179,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     bool load(std::string& err) {
         if (h) return true;
@@ -195,6 +200,7 @@ struct NcclApi {
         SYM(GroupEnd, "ncclGroupEnd");
         SYM(AllReduce, "ncclAllReduce");
         SYM(GetErrorString, "ncclGetErrorString");
+        SYM(CommUserRank, "ncclCommUserRank");
 #undef SYM
         return true;
     }
@@ -224,7 +230,60 @@ struct NcclTransport : Transport {
         ncclResult_t r = nccl_api().AllReduce(d, d, count, t, op, comm, s);
         return r == ncclSuccess ? std::string() : err(r);
     }
+    // peer mapping by CUDA IPC: each rank publishes (handle of the allocation holding base, offset of base in it);
+    // the W records are combined by a byte-wise sum allreduce (every record is zero except on its owner)
+    std::vector<void*> opened;
+    int32_t* d_fence = nullptr;
+    std::string map_peers(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s) override {
+        (void)bytes;
+        using RangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+        static RangeFn range = nullptr;
+        if (!range) {
+            void* p = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                return "cuMemGetAddressRange unavailable";
+            range = reinterpret_cast<RangeFn>(p);
+        }
+        unsigned long long alloc = 0;
+        size_t asz = 0;
+        if (range(&alloc, &asz, (unsigned long long)(uintptr_t)base) != 0) return "cuMemGetAddressRange failed";
+        struct Rec { cudaIpcMemHandle_t h; uint64_t off; };
+        int me = 0;
+        nccl_api().CommUserRank(comm, &me);
+        const int world = (int)out.size();
+        std::vector<Rec> recs(world);
+        std::memset(recs.data(), 0, recs.size() * sizeof(Rec));
+        if (cudaIpcGetMemHandle(&recs[me].h, (void*)(uintptr_t)alloc) != cudaSuccess) return "cudaIpcGetMemHandle failed";
+        recs[me].off = (uint64_t)((uintptr_t)base - alloc);
+        void* d = nullptr;
+        const size_t nb = recs.size() * sizeof(Rec);
+        if (cudaMalloc(&d, nb) != cudaSuccess) return "map_peers: cudaMalloc";
+        cudaMemcpyAsync(d, recs.data(), nb, cudaMemcpyHostToDevice, s);
+        ncclResult_t r = nccl_api().AllReduce(d, d, nb, ncclUint8, ncclSum, comm, s);
+        if (r != ncclSuccess) { cudaFree(d); return err(r); }
+        cudaMemcpyAsync(recs.data(), d, nb, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        cudaFree(d);
+        for (int q = 0; q < world; ++q) {
+            if (q == me) { out[q] = base; continue; }
+            void* p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, recs[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                return "cudaIpcOpenMemHandle failed";
+            opened.push_back(p);
+            out[q] = (char*)p + recs[q].off;
+        }
+        return std::string();
+    }
+    std::string fence(cudaStream_t s) override {   // a one-word allreduce completes only after every rank reached it
+        if (!d_fence && cudaMalloc(&d_fence, sizeof(int32_t)) != cudaSuccess) return "fence: cudaMalloc";
+        ncclResult_t r = nccl_api().AllReduce(d_fence, d_fence, 1, ncclInt32, ncclMax, comm, s);
+        return r == ncclSuccess ? std::string() : err(r);
+    }
     ~NcclTransport() override {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        if (d_fence) cudaFree(d_fence);
         if (comm) nccl_api().CommDestroy(comm);
     }
 };
@@ -314,6 +373,22 @@ struct LoopTransport : Transport {
         G->barrier();
         return std::string();
     }
+    std::string map_peers(void* base, size_t, std::vector<void*>& out, cudaStream_t) override {
+        G->bufs[rank] = base;   // virtual ranks share the process: their buffers are directly addressable
+        G->barrier();
+        for (int q = 0; q < G->world; ++q) out[q] = G->bufs[q];
+        G->barrier();
+        return std::string();
+    }
+    std::string fence(cudaStream_t s) override {   // CUDA events between the virtual ranks' streams (no spinning)
+        cudaEventRecord(ev_ready, s);
+        G->ready[rank] = ev_ready;
+        G->barrier();
+        for (int q = 0; q < G->world; ++q)
+            if (q != rank) cudaStreamWaitEvent(s, G->ready[q], 0);
+        G->barrier();
+        return std::string();
+    }
     ~LoopTransport() override {
         if (ev_ready) cudaEventDestroy(ev_ready);
         if (ev_done) cudaEventDestroy(ev_done);
@@ -329,6 +404,7 @@ Comm::~Comm() = default;
 amr_status Comm::init(amr_ctx* c) {
     world = c->cfg.world_size;
     rank = c->cfg.rank;
+    halo_mode = c->cfg.halo_mode;
     owner = partition_owners(c->tree, world);
     if (world == 1) return AMR_OK;
     if (c->cfg.comm_backend == 1) {
@@ -376,7 +452,14 @@ amr_status Comm::init(amr_ctx* c) {
 #endif
 }
 
-void Comm::finalize(amr_ctx*) { tr.reset(); }
+void Comm::finalize(amr_ctx*) {
+    for (PullList* P : {&pull_halo, &pull_flux})
+        if (P->slots) { cudaFree(P->slots); cudaFree(P->peers); P->slots = P->peers = nullptr; }
+    if (d_pool_bases) cudaFree(d_pool_bases);
+    if (d_freg_bases) cudaFree(d_freg_bases);
+    d_pool_bases = d_freg_bases = nullptr;
+    tr.reset();
+}
 
 void Comm::repartition(const PatchTree& t) { owner = partition_owners(t, world); }
 
@@ -384,6 +467,7 @@ void Comm::replan(const PatchTree& t) {
     if (world == 1) return;
     halo = plan_halo(t, owner, world, rank);
     flux = plan_flux(t, owner, world, rank);
+    ++lists_version;
 }
 
 amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per, const char* what) {
@@ -432,11 +516,64 @@ amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, i
 }
 
 amr_status Comm::exchange_halos(amr_ctx* c, double* U) {
+    if (world > 1 && halo_mode == 1) return peer_pull(c, halo, pull_halo, U, false, "halo pull");
     return exchange_lists(c, halo, U, (int)c->PS, "halo exchange");
 }
 
 amr_status Comm::exchange_fluxes(amr_ctx* c) {
+    if (world > 1 && halo_mode == 1) return peer_pull(c, flux, pull_flux, c->freg.p, true, "flux-register pull");
     return exchange_lists(c, flux, c->freg.p, 16 * c->n, "flux-register exchange");
+}
+
+amr_status Comm::map_pool(amr_ctx* c, void* base, size_t bytes) {
+    std::vector<void*> peers(world, nullptr);
+    std::string e = tr->map_peers(base, bytes, peers, c->stream);
+    if (!e.empty()) { c->err = "halo_mode 1: " + e; return AMR_E_COMM; }
+    if (!d_pool_bases && cudaMalloc(&d_pool_bases, world * sizeof(double*)) != cudaSuccess) return AMR_E_CUDA;
+    if (cudaMemcpy(d_pool_bases, peers.data(), world * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess)
+        return AMR_E_CUDA;
+    pool_base = base;
+    return AMR_OK;
+}
+
+// fence, then one pull kernel for every slot of L.recv (each from its owner's mapped buffer at the same offset);
+// the slot lists go to the device once per plan.  Every rank calls this at the same points (collective fence).
+amr_status Comm::peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, double* dst, bool freg, const char* what) {
+    auto bad = [&](amr_status st, const std::string& m) { c->err = std::string(what) + ": " + m; c->sticky = st; return st; };
+    if (freg && mapped_freg != c->freg.p) {   // (re)map the flux-register buffers (identical sizes on every rank)
+        std::vector<void*> peers(world, nullptr);
+        std::string e = tr->map_peers(c->freg.p, c->freg.cap * sizeof(double), peers, c->stream);
+        if (!e.empty()) return bad(AMR_E_COMM, e);
+        if (!d_freg_bases && cudaMalloc(&d_freg_bases, world * sizeof(double*)) != cudaSuccess) return bad(AMR_E_CUDA, "alloc");
+        if (cudaMemcpy(d_freg_bases, peers.data(), world * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bad(AMR_E_CUDA, "peer table");
+        mapped_freg = c->freg.p;
+    }
+    if (P.version != lists_version) {
+        std::vector<int32_t> sl, pe;
+        for (int p = 0; p < world; ++p)
+            for (int32_t id : L.recv[p]) { sl.push_back(id); pe.push_back(p); }
+        if (P.slots) { cudaFree(P.slots); cudaFree(P.peers); P.slots = P.peers = nullptr; }
+        P.n = (int)sl.size();
+        if (P.n) {
+            if (cudaMalloc(&P.slots, sl.size() * 4) != cudaSuccess || cudaMalloc(&P.peers, pe.size() * 4) != cudaSuccess)
+                return bad(AMR_E_CUDA, "lists");
+            cudaMemcpy(P.slots, sl.data(), sl.size() * 4, cudaMemcpyHostToDevice);
+            cudaMemcpy(P.peers, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice);
+        }
+        P.version = lists_version;
+    }
+    std::string e = tr->fence(c->stream);
+    if (!e.empty()) return bad(AMR_E_COMM, e);
+    const int per = freg ? 16 * c->n : (int)c->PS;
+    const size_t off = freg ? 0 : (size_t)(dst - (double*)pool_base);
+    if (P.n) {
+        if (launch_peer_pull(P.slots, P.peers, P.n, freg ? d_freg_bases : d_pool_bases, off, dst, per, c->stream) != cudaSuccess)
+            return bad(AMR_E_CUDA, "pull kernel");
+        c->st.launches += 1;
+        bytes_sent += (int64_t)P.n * per * (int64_t)sizeof(double);   // bytes moved into this rank
+    }
+    return AMR_OK;
 }
 
 amr_status Comm::allreduce_max_u64(amr_ctx* c, unsigned long long* d) {

@@ -48,7 +48,22 @@ struct Comm {
     std::unique_ptr<Transport> tr;
     std::vector<int32_t> owner;        // per slot (patch id); -1 for free slots
     ExchangeLists halo, flux;
+    uint64_t lists_version = 0;        // bumped by replan
     int64_t bytes_sent = 0;
+
+    // halo_mode 1 (NEXT #3): every rank's state pool and flux-register buffer mapped into this process; halo and
+    // flux exchanges become a stream-ordered cross-rank fence plus one peer_pull_kernel launch
+    int halo_mode = 0;
+    void* pool_base = nullptr;               // local pool (the 3 RK buffers)
+    const void* mapped_freg = nullptr;       // local flux-register buffer the peer table was built for
+    double** d_pool_bases = nullptr;         // device [world]: every rank's pool base as seen here
+    double** d_freg_bases = nullptr;
+    struct PullList {
+        uint64_t version = ~0ull;
+        int n = 0;
+        int32_t* slots = nullptr;            // device
+        int32_t* peers = nullptr;
+    } pull_halo, pull_flux;
 
     Comm();
     ~Comm();
@@ -63,6 +78,8 @@ struct Comm {
     amr_status exchange_fluxes(amr_ctx* c);
     amr_status exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per_slot, const char* what);
     amr_status exchange_children(amr_ctx*, double*) { return AMR_OK; }   // root-tree ownership: local
+    amr_status map_pool(amr_ctx* c, void* base, size_t bytes);   // collective (amr_create)
+    amr_status peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, double* dst, bool freg, const char* what);
     amr_status allreduce_max_u64(amr_ctx* c, unsigned long long* d);
     amr_status allreduce_max_i32(amr_ctx* c, int32_t* d, int n);
     amr_status allreduce_sum4(amr_ctx* c, double* h4);

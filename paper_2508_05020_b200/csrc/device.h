@@ -155,6 +155,9 @@ cudaError_t launch_totals(const LeafDesc* leaves, int nleaves, const AuxArgs& a,
 // flux registers: per = 16 n)
 cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int per, cudaStream_t s);
 cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, double* packed, int per, cudaStream_t s);
+// slots[k] of the local buffer dst <- the same slot of peer peers[k]'s buffer (bases[peer] + off), `per` doubles each
+cudaError_t launch_peer_pull(const int32_t* slots, const int32_t* peers, int n, const double* const* bases,
+                             size_t off, double* dst, int per, cudaStream_t s);
 
 // unfused stage (variant 2): scratch doubles for nleaves patches; kernel launches per stage of a variant
 size_t unfused_scratch_doubles(int n, int nleaves);

@@ -2216,6 +2216,27 @@ cudaError_t launch_flags_compact(const LeafDesc* leaves, int nleaves, const int3
     return cudaGetLastError();
 }
 
+// Peer pull (NEXT #3, halo_mode 1): one CTA per received slot loads the slot's `per` doubles straight from the
+// owning rank's pool, mapped into this process (NVLink peer memory; another virtual rank's buffer on one GPU), into
+// the same slot of the local buffer -- no pack / unpack kernels, no staging buffers, no transport call.  16-byte
+// vector loads (every slot region is a multiple of 16 bytes and 16-byte aligned).
+__global__ void peer_pull_kernel(const int32_t* __restrict__ slots, const int32_t* __restrict__ peers,
+                                 const double* const* __restrict__ bases, size_t off, double* __restrict__ dst, int per) {
+    const size_t slot = (size_t)slots[blockIdx.x];
+    const double2* src = reinterpret_cast<const double2*>(bases[peers[blockIdx.x]] + off + slot * per);
+    double2* out = reinterpret_cast<double2*>(dst + slot * per);
+    const int nv = per / 2;
+    for (int e = threadIdx.x; e < nv; e += blockDim.x) out[e] = src[e];
+}
+
+cudaError_t launch_peer_pull(const int32_t* slots, const int32_t* peers, int n, const double* const* bases,
+                             size_t off, double* dst, int per, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (per % 2) return cudaErrorInvalidValue;
+    peer_pull_kernel<<<n, 256, 0, s>>>(slots, peers, bases, off, dst, per);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int per, cudaStream_t s) {
     if (npatch <= 0) return cudaSuccess;
     long long total = (long long)npatch * per;

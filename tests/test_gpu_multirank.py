@@ -77,12 +77,14 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("halo_mode", [0, 1])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case", list(CASES))
-def test_virtual_ranks_bitwise_equal_single_rank(case, world):
+def test_virtual_ranks_bitwise_equal_single_rank(case, world, halo_mode):
+    """halo_mode 0: pack + transport copy + unpack; 1: peer pull (NEXT #3) from the other ranks' mapped pools."""
     cfg, steps, regrid = CASES[case]
     ref_state, ref_keys, ref_dts = run_single(cfg, steps, regrid)
-    res = run_multi(cfg, world, steps, regrid)
+    res = run_multi(dict(cfg, halo_mode=halo_mode), world, steps, regrid)
     merged = {}
     for r, (st, keys, dts, owners, stats) in enumerate(res):
         assert keys == ref_keys, f"rank {r}: tree differs"
@@ -94,3 +96,14 @@ def test_virtual_ranks_bitwise_equal_single_rank(case, world):
         assert np.array_equal(U, merged[k]), (case, world, k)
     e, _ = parity_error(ref_state, merged)
     assert e == 0.0
+
+
+def test_peer_pull_launches_one_kernel_per_exchange():
+    """halo_mode 1 replaces the pack and unpack kernels of every halo / flux exchange by one pull kernel: on the
+    same run it launches fewer kernels than halo_mode 0 and moves the same patch bytes."""
+    cfg, steps, regrid = CASES["quadrant_amr_weno"]
+    st = {}
+    for hm in (0, 1):
+        res = run_multi(dict(cfg, halo_mode=hm), 2, steps, regrid)
+        st[hm] = res[0][4]
+    assert st[1]["launches"] < st[0]["launches"], st
