@@ -387,8 +387,9 @@ def main():
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--cfl", type=float, default=0.3)
     ap.add_argument("--stage-kernel", type=int, default=0, help="amr_config.stage_kernel (0 default, 1 per-tile)")
-    ap.add_argument("--halo-mode", type=int, default=0, choices=[0, 1],
-                    help="N > 1 halo exchange: 0 pack + NCCL send/recv + unpack, 1 peer pull over CUDA IPC (NEXT #3)")
+    ap.add_argument("--halo-mode", type=int, default=0, choices=[0, 1, 2],
+                    help="N > 1 halo exchange: 0 pack + NCCL send/recv + unpack, 1 peer pull over CUDA IPC, "
+                         "2 remote face strips loaded by the stage kernel from the peers' pools (NEXT #3)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weno", action="store_true")
@@ -452,7 +453,7 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (SplitMix64 noise, BASELINE configs[4] distributions)",
                 "config": {"workload": name, "scheme": args.scheme, "patch": args.n, "cfl_fixed_dt": args.cfl,
-                           "parallelism": (f"Morton root partition x{X.world}, " + ("peer-pull halo (CUDA IPC, NVLink)" if args.halo_mode else "NCCL halo exchange")) if X.world > 1
+                           "parallelism": (f"Morton root partition x{X.world}, " + (["NCCL halo exchange", "peer-pull halo (CUDA IPC, NVLink)", "remote strips read by the stage kernel (CUDA IPC, NVLink)"][args.halo_mode])) if X.world > 1
                            else "single GPU",
                            "l2": "inputs larger than L2 (3 x 537 MB buffers per GPU); U^n restored from a pristine "
                                  "device copy between timed steps (untimed; also flushes L2)",

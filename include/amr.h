@@ -103,8 +103,13 @@ typedef struct {
                                      IPC handles exchanged over NCCL; directly for loopback virtual ranks), and each
                                      exchange is a stream-ordered cross-rank fence (a one-word NCCL allreduce, or
                                      CUDA events between loopback streams) followed by ONE kernel that loads the
-                                     needed slots from the owners' pools over NVLink into the local pool.  Regrid
-                                     exchanges (coarse sources, migration, flags) use the transport in both modes */
+                                     needed slots from the owners' pools over NVLink into the local pool;
+                                     2 (Central4 TMA kernel: central4, patch_cells >= 32, stage_kernel 0, <= 8 ranks)
+                                     as 1, but the stage kernel itself loads the 4-wide face strips of remote
+                                     neighbours by TMA from the owners' pools, so before a stage only the coarse
+                                     sources of C/F ghosts are pulled (the halo transfer overlaps the compute).
+                                     Regrid exchanges (coarse sources, migration, flags) use the transport in all
+                                     modes */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none

@@ -73,7 +73,12 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
     if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }
     if (c.subcycle && c.world_size > 1) { m = "subcycling is single-rank in this build"; return AMR_E_CONFIG; }
-    if (c.halo_mode != 0 && c.halo_mode != 1) { m = "halo_mode must be 0 or 1"; return AMR_E_CONFIG; }
+    if (c.halo_mode < 0 || c.halo_mode > 2) { m = "halo_mode must be 0, 1 or 2"; return AMR_E_CONFIG; }
+    if (c.halo_mode == 2 && c.world_size > 1 &&
+        (c.scheme != AMR_CENTRAL4 || c.patch_cells < 32 || c.stage_kernel != 0 || c.world_size > 8)) {
+        m = "halo_mode 2 needs the Central4 TMA kernel (central4, patch_cells >= 32, stage_kernel 0) and <= 8 ranks";
+        return AMR_E_CONFIG;
+    }
     return AMR_OK;
 }
 
@@ -228,6 +233,8 @@ amr_status build_plan(amr_ctx* c) {
             int nb = t.neighbour(id, dirs[s][0], dirs[s][1]);
             if (nb >= 0) {
                 d.side[s] = nb;
+                if (c->comm.world > 1 && c->comm.halo_mode == 2 && c->comm.owner[nb] != c->comm.rank)
+                    d.pad |= (16 << s) | (c->comm.owner[nb] << (8 + 3 * s));   // strip read from the owner's pool
                 if (t.has_children(nb)) {
                     d.cf |= 1 << s;
                     rt.mask |= 1 << s;
@@ -456,7 +463,7 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
     for (int s = 1; s <= 3; ++s) {
         double* Uin = s == 1 ? c->U[c->un] : (s == 2 ? c->U[A] : c->U[B]);
         double* Uout = s == 2 ? c->U[B] : c->U[A];
-        amr_status cs = c->comm.exchange_halos(c, Uin);
+        amr_status cs = c->comm.exchange_halos_stage(c, Uin);
         if (cs != AMR_OK) return cs;
         cs = fill_ghosts(c, Uin);
         if (cs != AMR_OK) return cs;
@@ -493,6 +500,11 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
             a.nleaves = (int32_t)c->singles.size();
         }
         a.geo = c->geo;
+        if (c->comm.world > 1 && c->comm.halo_mode == 2) {   // remote face strips: TMA straight from the owners' pools
+            a.npeers = c->comm.world;
+            const size_t off = (size_t)(Uin - (double*)c->comm.pool_base);
+            for (int q = 0; q < c->comm.world; ++q) a.peer_in[q] = c->comm.peer_pool[q] + off;
+        }
         int scheme = c->cfg.scheme == AMR_CENTRAL4 ? 0 : (c->cfg.weno_characteristic ? 1 : 2);
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (c->timing && !c->leaves.empty()) {
@@ -863,7 +875,7 @@ amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
     CU(cudaMemsetAsync(c->d_err, 0, 16, c->stream));
     CU(cudaMallocHost(&c->h_pinned, 64));
     amr_status s = c->comm.init(c);
-    if (s == AMR_OK && c->comm.world > 1 && c->comm.halo_mode == 1) s = c->comm.map_pool(c, base, need);
+    if (s == AMR_OK && c->comm.world > 1 && c->comm.halo_mode >= 1) s = c->comm.map_pool(c, base, need);
     if (s != AMR_OK) {
         std::fprintf(stderr, "amr_create: %s\n", c->err.c_str());
         return s;

@@ -78,12 +78,12 @@ std::vector<int32_t> partition_owners(const PatchTree& t, int world) {
     return owner;
 }
 
-void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out) {
+void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out, bool faces) {
     out.clear();
     for (int s = 0; s < 4; ++s) {
         int nb = t.neighbour(id, kSideDir[s][0], kSideDir[s][1]);
         if (nb >= 0) {
-            out.push_back(nb);
+            if (faces) out.push_back(nb);
         } else if (nb == -1) {
             int par = t.parent[id];
             if (par < 0) continue;
@@ -96,13 +96,13 @@ void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out) {
     }
 }
 
-ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank) {
+ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, bool faces) {
     std::vector<std::map<int, std::set<int32_t>>> need(world);
     std::vector<int32_t> src;
     for (int id = 0; id < t.capacity; ++id) {
         if (!t.is_leaf(id)) continue;
         int o = owner[id];
-        halo_sources(t, id, src);
+        halo_sources(t, id, src, faces);
         for (int q : src)
             if (owner[q] != o) need[o][owner[q]].insert(q);
     }
@@ -453,7 +453,7 @@ amr_status Comm::init(amr_ctx* c) {
 }
 
 void Comm::finalize(amr_ctx*) {
-    for (PullList* P : {&pull_halo, &pull_flux})
+    for (PullList* P : {&pull_halo, &pull_flux, &pull_halo_cf})
         if (P->slots) { cudaFree(P->slots); cudaFree(P->peers); P->slots = P->peers = nullptr; }
     if (d_pool_bases) cudaFree(d_pool_bases);
     if (d_freg_bases) cudaFree(d_freg_bases);
@@ -467,6 +467,7 @@ void Comm::replan(const PatchTree& t) {
     if (world == 1) return;
     halo = plan_halo(t, owner, world, rank);
     flux = plan_flux(t, owner, world, rank);
+    if (halo_mode == 2) halo_cf = plan_halo(t, owner, world, rank, false);
     ++lists_version;
 }
 
@@ -516,12 +517,17 @@ amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, i
 }
 
 amr_status Comm::exchange_halos(amr_ctx* c, double* U) {
-    if (world > 1 && halo_mode == 1) return peer_pull(c, halo, pull_halo, U, false, "halo pull");
+    if (world > 1 && halo_mode >= 1) return peer_pull(c, halo, pull_halo, U, false, "halo pull");
     return exchange_lists(c, halo, U, (int)c->PS, "halo exchange");
 }
 
+amr_status Comm::exchange_halos_stage(amr_ctx* c, double* U) {
+    if (world > 1 && halo_mode == 2) return peer_pull(c, halo_cf, pull_halo_cf, U, false, "C/F source pull");
+    return exchange_halos(c, U);
+}
+
 amr_status Comm::exchange_fluxes(amr_ctx* c) {
-    if (world > 1 && halo_mode == 1) return peer_pull(c, flux, pull_flux, c->freg.p, true, "flux-register pull");
+    if (world > 1 && halo_mode >= 1) return peer_pull(c, flux, pull_flux, c->freg.p, true, "flux-register pull");
     return exchange_lists(c, flux, c->freg.p, 16 * c->n, "flux-register exchange");
 }
 
@@ -533,6 +539,8 @@ amr_status Comm::map_pool(amr_ctx* c, void* base, size_t bytes) {
     if (cudaMemcpy(d_pool_bases, peers.data(), world * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess)
         return AMR_E_CUDA;
     pool_base = base;
+    peer_pool.assign(world, nullptr);
+    for (int q = 0; q < world; ++q) peer_pool[q] = (double*)peers[q];
     return AMR_OK;
 }
 

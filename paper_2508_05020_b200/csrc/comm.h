@@ -32,8 +32,9 @@ struct ExchangeLists {
 // ---- pure host planning (no CUDA): testable on CPU
 std::vector<int32_t> partition_owners(const PatchTree& t, int world);
 // slots read by the stage / flags / ghost kernels of leaf `id` that may live on another rank
-void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out);
-ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
+// (faces = false: only the coarse sources of C/F ghost strips -- halo_mode 2 reads face neighbours in the stage kernel)
+void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out, bool faces = true);
+ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, bool faces = true);
 ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
 // coarse sources of new level-l patches prolonged by the (old) owner of their root
 ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_new, int level,
@@ -47,7 +48,7 @@ struct Comm {
     int world = 1, rank = 0;
     std::unique_ptr<Transport> tr;
     std::vector<int32_t> owner;        // per slot (patch id); -1 for free slots
-    ExchangeLists halo, flux;
+    ExchangeLists halo, flux, halo_cf;
     uint64_t lists_version = 0;        // bumped by replan
     int64_t bytes_sent = 0;
 
@@ -58,12 +59,13 @@ struct Comm {
     const void* mapped_freg = nullptr;       // local flux-register buffer the peer table was built for
     double** d_pool_bases = nullptr;         // device [world]: every rank's pool base as seen here
     double** d_freg_bases = nullptr;
+    std::vector<double*> peer_pool;          // host copy of the peer pool bases (halo_mode 2 tensor maps)
     struct PullList {
         uint64_t version = ~0ull;
         int n = 0;
         int32_t* slots = nullptr;            // device
         int32_t* peers = nullptr;
-    } pull_halo, pull_flux;
+    } pull_halo, pull_flux, pull_halo_cf;
 
     Comm();
     ~Comm();
@@ -75,6 +77,8 @@ struct Comm {
     void replan(const PatchTree& t);           // halo / flux lists for the current owner
 
     amr_status exchange_halos(amr_ctx* c, double* U);
+    // before a stage kernel: halo_mode 2 pulls only the C/F coarse sources (face strips are read in the kernel)
+    amr_status exchange_halos_stage(amr_ctx* c, double* U);
     amr_status exchange_fluxes(amr_ctx* c);
     amr_status exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per_slot, const char* what);
     amr_status exchange_children(amr_ctx*, double*) { return AMR_OK; }   // root-tree ownership: local

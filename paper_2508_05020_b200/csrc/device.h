@@ -25,7 +25,8 @@ struct LeafDesc {
     int32_t level;
     int32_t side[4];
     int32_t cf;        // bits 0-3: side is the COARSE side of a C/F face; bits 4-7: FINE side
-    int32_t pad;
+    int32_t pad;       // bit 0 covered patch (subcycling); bit 1 group member slots consecutive; halo_mode 2:
+                       // bits 4-7 side neighbour owned by another rank, bits 8 + 3 s .. 10 + 3 s its rank
 };
 
 // Fill one proxy strip (the g columns / rows of a virtual neighbour that touch the leaf).
@@ -99,6 +100,8 @@ struct StageArgs {
     int32_t prof;              // phase timing of the TMA kernel (AMR_PHASE_PROF, debug)
     int32_t lam0;              // subcycling: Lambda normalised to level 0 (S6); LeafDesc.pad bit 0 = covered patch;
                                // group tiles: pad bit 1 of member 0 = members in consecutive slots
+    int32_t npeers;            // halo_mode 2: ranks whose pools are mapped (0 otherwise)
+    const double* peer_in[8];  //   rank q's U^(s-1) as mapped here (host-side: tensor-map bases of the strip loads)
     Geometry geo;
 };
 

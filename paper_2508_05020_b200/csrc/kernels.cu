@@ -744,6 +744,8 @@ struct C4Maps {
     CUtensorMap px_sn;    // proxy buffer, box {32, 4, 4}
     CUtensorMap un_int;   // U^n, box {32, 32, 4}
     CUtensorMap out_int;  // U^(s), box {32, 32, 4} (TMA store)
+    CUtensorMap peer_we[8];   // halo_mode 2: rank q's U^(s-1) mapped over NVLink, W/E strip boxes
+    CUtensorMap peer_sn[8];   //   S/N strip boxes
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -914,17 +916,36 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         else tma_load3(dst + kLandI * 8, &maps.in_int, tx * T, ty * T, 4 * d.slot, mb);
         const CUtensorMap* mw = &maps.in_we;
         int i0 = tx * T - G, z = 4 * d.slot;
-        if (tx == 0) { i0 = N - G; const int s = d.side[kW]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); mw = &maps.px_we; } }
+        // a patch-edge strip comes from the neighbour's slot -- in another rank's pool over NVLink when the
+        // neighbour is remote (halo_mode 2, LeafDesc.pad) -- or from the proxy of a C/F side
+        auto peer = [&](int side) { return (d.pad >> (8 + 3 * side)) & 7; };
+        if (tx == 0) {
+            i0 = N - G; const int s = d.side[kW];
+            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kW)) mw = &maps.peer_we[peer(kW)]; }
+            else { z = 4 * (-1 - s); mw = &maps.px_we; }
+        }
         tma_load3(dst + kLandW * 8, mw, i0, ty * T, z, mb);
         mw = &maps.in_we; i0 = tx * T + T; z = 4 * d.slot;
-        if (tx == TILES - 1) { i0 = 0; const int s = d.side[kE]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); mw = &maps.px_we; } }
+        if (tx == TILES - 1) {
+            i0 = 0; const int s = d.side[kE];
+            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kE)) mw = &maps.peer_we[peer(kE)]; }
+            else { z = 4 * (-1 - s); mw = &maps.px_we; }
+        }
         tma_load3(dst + kLandE * 8, mw, i0, ty * T, z, mb);
         const CUtensorMap* ms = &maps.in_sn;
         int j0 = ty * T - G; z = 4 * d.slot;
-        if (ty == 0) { j0 = N - G; const int s = d.side[kS]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); ms = &maps.px_sn; } }
+        if (ty == 0) {
+            j0 = N - G; const int s = d.side[kS];
+            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kS)) ms = &maps.peer_sn[peer(kS)]; }
+            else { z = 4 * (-1 - s); ms = &maps.px_sn; }
+        }
         tma_load3(dst + kLandS * 8, ms, tx * T, j0, z, mb);
         ms = &maps.in_sn; j0 = ty * T + T; z = 4 * d.slot;
-        if (ty == TILES - 1) { j0 = 0; const int s = d.side[kN]; if (s >= 0) z = 4 * s; else { z = 4 * (-1 - s); ms = &maps.px_sn; } }
+        if (ty == TILES - 1) {
+            j0 = 0; const int s = d.side[kN];
+            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kN)) ms = &maps.peer_sn[peer(kN)]; }
+            else { z = 4 * (-1 - s); ms = &maps.px_sn; }
+        }
         tma_load3(dst + kLandN * 8, ms, tx * T, j0, z, mb);
     };
 
@@ -1199,6 +1220,10 @@ cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
         !encode_pool_map(&m.un_int, a.Un, N, a.nslots, kTmaT, kTmaT) ||
         !encode_pool_map(&m.out_int, a.Uout, N, a.nslots, kTmaT, kTmaT))
         return cudaErrorInvalidValue;
+    for (int q = 0; q < a.npeers && q < 8; ++q)   // halo_mode 2: every rank's U^(s-1) as mapped in this process
+        if (!encode_pool_map(&m.peer_we[q], a.peer_in[q], N, a.nslots, kGL, kTmaT) ||
+            !encode_pool_map(&m.peer_sn[q], a.peer_in[q], N, a.nslots, kTmaT, kGL))
+            return cudaErrorInvalidValue;
     const int grid = ntiles < sm_count() ? ntiles : sm_count();
 #ifdef AMR_PHASE_PROF
     static const bool prof = getenv("AMR_PHASE_PROF") != nullptr;

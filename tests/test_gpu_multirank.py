@@ -71,18 +71,23 @@ def run_multi(cfg, world, steps, regrid_every):
 
 
 CASES = {
+    "uniform_periodic_c4_n32": (W.sweep(N=256, n=32, scheme="central4", seed=3, ic="smooth"), 4, None),
+    "implosion_c4_amr_n32": (W.implosion(N=256, n=32, scheme="central4", levels=2), 6, 3),
     "uniform_periodic_c4": (W.sweep(N=128, n=16, scheme="central4", seed=3, ic="smooth"), 4, None),
     "quadrant_amr_weno": (W.quadrant(N=64, n=16, levels=3, seed=2), 8, 4),
     "shock_bubble_reflective": (W.shock_bubble(Nx=128, Ny=64, n=16, levels=3), 8, 4),
 }
 
 
-@pytest.mark.parametrize("halo_mode", [0, 1])
+@pytest.mark.parametrize("halo_mode", [0, 1, 2])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case", list(CASES))
 def test_virtual_ranks_bitwise_equal_single_rank(case, world, halo_mode):
-    """halo_mode 0: pack + transport copy + unpack; 1: peer pull (NEXT #3) from the other ranks' mapped pools."""
+    """halo_mode 0: pack + transport copy + unpack; 1: peer pull (NEXT #3) from the other ranks' mapped pools;
+    2: the Central4 TMA stage kernel loads remote face strips from the owners' pools itself (n >= 32 only)."""
     cfg, steps, regrid = CASES[case]
+    if halo_mode == 2 and not (cfg["scheme"] == "central4" and cfg["n"] >= 32):
+        pytest.skip("halo_mode 2 is the Central4 TMA path")
     ref_state, ref_keys, ref_dts = run_single(cfg, steps, regrid)
     res = run_multi(dict(cfg, halo_mode=halo_mode), world, steps, regrid)
     merged = {}
