@@ -439,8 +439,9 @@ def main():
     if X.rank == 0:
         rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
               "frac": main_res["achieved_gbs"] / hbm_peak, "traffic": None, "peak_kind": hbm_kind,
-              "kernel": "stage_c4_kernel (fused halo gather + cons->prim + Central4 flux + Eq. 9 divergence + "
-                        "SSP-RK3 update)",
+              "kernel": ({8: "stage_c4_group_kernel<8>", 16: "stage_c4_group_kernel<16>"}.get(args.n, f"stage_c4_tma_kernel<{args.n}>")
+                         if args.scheme == "central4" and args.stage_kernel == 0 else "stage kernel variant %d" % args.stage_kernel)
+                        + " (TMA halo + cons->prim + Central4 flux + Eq. 9 divergence + SSP-RK3 update, one launch per stage)",
               "algorithmic_bytes_per_cell_stage": BYTES_PER_CELL_STAGE,
               "cells_per_launch": main_res["cells_per_launch"], "avg_launch_ms": main_res["stage_avg_ms"]}
         tf = os.path.join(ROOT, "profiles", "traffic.json")
