@@ -332,12 +332,12 @@ amr_status build_plan(amr_ctx* c) {
         CU(c->d_sub_ptasks.upload(c->sub_ptasks, s));
         CU(c->d_acc_tasks.upload(c->acc_tasks, s));
         CU(c->sub_proxy.reserve(std::max<size_t>(1, c->sub_ptasks.size()) * c->PS));
-        CU(c->facc.reserve((size_t)t.capacity * 16 * c->n));
+        CU(c->facc.reserve((size_t)t.capacity * 16 * c->n, false));
     }
     c->d_rlev.resize(L);
     for (int l = 0; l < L; ++l) CU(c->d_rlev[l].upload(c->rlev[l], s));
     CU(c->proxy.reserve(std::max<size_t>(1, c->ptasks.size()) * c->PS));
-    CU(c->freg.reserve((size_t)t.capacity * 16 * c->n));   // indexed by slot (remote fine leaves arrive by exchange)
+    CU(c->freg.reserve((size_t)t.capacity * 16 * c->n, false));   // indexed by slot (remote fine leaves arrive by exchange)
     CU(c->d_maxeta.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_amb.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_sib.upload(c->sib, c->stream));

@@ -28,11 +28,13 @@ struct DevArray {
         if (v.empty()) return cudaSuccess;
         return cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
     }
-    cudaError_t reserve(size_t n) {
+    // grows with 50 % slack (a proxy count growing by one must not re-allocate); slack = false for arrays sized
+    // by the fixed slot capacity
+    cudaError_t reserve(size_t n, bool slack = true) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFree(p);
         p = nullptr;
-        cap = std::max<size_t>(n, 16);
+        cap = std::max<size_t>(slack ? n + n / 2 : n, 16);
         cudaError_t e = cudaMalloc(&p, cap * sizeof(T));
         if (e != cudaSuccess) cap = 0;
         return e;
