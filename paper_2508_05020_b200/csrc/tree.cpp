@@ -118,6 +118,10 @@ int PatchTree::find(int l, int i, int j) const {
 
 int PatchTree::neighbour(int id, int dx, int dy) const {
     int l = lev[id], i = pi[id] + dx, j = pj[id] + dy;
+    if (l > 0) {   // a sibling (same parent; never across a wrap) comes from the parent's child links
+        const int a = (pi[id] & 1) + dx, b = (pj[id] & 1) + dy;
+        if (a >= 0 && a <= 1 && b >= 0 && b <= 1) return child[4 * parent[id] + a + 2 * b];
+    }
     if (!wrap(l, i, j)) return -2;
     return index_.find(key(l, i, j));
 }

@@ -85,18 +85,23 @@ class FlatIndex {
     }
 };
 
-// LSD radix sort of (key, id) pairs by key, 16-bit digits; a digit shared by every key is skipped.  Keys are
-// unique in every use (patch keys, level-Morton keys), so the order is the plain key order.
+// LSD radix sort of (key, id) pairs by key; a digit shared by every key is skipped.  Digits of 8 bits below 64 k
+// pairs (the 256 counters stay cheap to clear), 16 bits above.  Keys are unique in every use (patch keys,
+// level-Morton keys), so the order is the plain key order.
 inline void radix_sort_pairs(std::vector<std::pair<uint64_t, int32_t>>& v) {
+    const int bits = v.size() < 65536 ? 8 : 16;
+    const uint64_t mask = (1ull << bits) - 1;
     std::vector<std::pair<uint64_t, int32_t>> tmp(v.size());
-    std::vector<uint32_t> cnt(65536);
-    for (int shift = 0; shift < 64; shift += 16) {
+    std::vector<uint32_t> cnt(size_t(1) << bits);
+    uint64_t diff = 0;   // bits in which some key differs from the first: only those digits need a pass
+    for (const auto& e : v) diff |= e.first ^ v[0].first;
+    for (int shift = 0; shift < 64; shift += bits) {
+        if (!((diff >> shift) & mask)) continue;
         std::fill(cnt.begin(), cnt.end(), 0u);
-        for (const auto& e : v) ++cnt[(e.first >> shift) & 0xffff];
-        if (!v.empty() && cnt[(v[0].first >> shift) & 0xffff] == v.size()) continue;
+        for (const auto& e : v) ++cnt[(e.first >> shift) & mask];
         uint32_t sum = 0;
         for (auto& c : cnt) { const uint32_t x = c; c = sum; sum += x; }
-        for (const auto& e : v) tmp[cnt[(e.first >> shift) & 0xffff]++] = e;
+        for (const auto& e : v) tmp[cnt[(e.first >> shift) & mask]++] = e;
         v.swap(tmp);
     }
 }
