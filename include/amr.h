@@ -95,7 +95,8 @@ typedef struct {
     int32_t subcycle;             /* 1: Berger-Colella time subcycling (NEXT #4; DESIGN.md s3b S1-S6): level l takes
                                      2^l steps of dt_0 / 2^l per amr_step, C/F ghosts interpolated in time, fluxes
                                      refluxed with quadrature-weighted registers; dt / cfl of amr_step refer to
-                                     level 0 and amr_diagnostics' lambda is normalised to level 0.  Single rank;
+                                     level 0 and amr_diagnostics' lambda is normalised to level 0.  Any world_size
+                                     (per-level face / coarse-source / register exchanges);
                                      a non-physical step is reported (AMR_E_NONPHYSICAL) but only level 0 rolls back */
     int32_t halo_mode;            /* world_size > 1, halo and flux-register exchanges (NEXT #3): 0 pack kernel +
                                      transport point-to-point (NCCL send/recv, or loopback copies) + unpack kernel;

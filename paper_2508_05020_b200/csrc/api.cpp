@@ -72,7 +72,6 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.refine_threshold < 0 || c.coarsen_fraction < 0) { m = "bad thresholds"; return AMR_E_CONFIG; }
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
     if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }
-    if (c.subcycle && c.world_size > 1) { m = "subcycling is single-rank in this build"; return AMR_E_CONFIG; }
     if (c.halo_mode < 0 || c.halo_mode > 2) { m = "halo_mode must be 0, 1 or 2"; return AMR_E_CONFIG; }
     if (c.halo_mode == 2 && c.world_size > 1 &&
         (c.scheme != AMR_CENTRAL4 || c.patch_cells < 32 || c.stage_kernel != 0 || c.world_size > 8)) {
@@ -166,12 +165,14 @@ amr_status build_subcycle_plan(amr_ctx* c) {
             if (s != AMR_OK) return s;
         }
         for (int id : c->canon)
-            if (t.lev[id] == l && t.has_children(id)) {
+            if (t.lev[id] == l && t.has_children(id) && c->comm.owns(c, id)) {
                 amr_status s = add(id, true);
                 if (s != AMR_OK) return s;
             }
         while (r < c->rtasks.size() && c->rtasks[r].level == l) ++r;
     }
+    c->sub_levels = 0;
+    for (int id : c->canon) c->sub_levels = std::max(c->sub_levels, t.lev[id] + 1);
     c->sub_off[L] = (int32_t)c->sub_descs.size();
     c->sub_poff[L] = (int32_t)c->sub_ptasks.size();
     c->acc_off[L] = (int32_t)c->acc_tasks.size();
@@ -1074,7 +1075,12 @@ struct SubRun {
         const int m = 1 << l, k = ((1 - m) % 3 + 3) % 3;
         return nstep[l] >= m - k ? 2 : 1;
     }
-    bool has_level(int l) const { return l < L && c->sub_off[l + 1] > c->sub_off[l]; }
+    // a level takes part in the recursion when it exists anywhere in the replicated tree (every rank must make the
+    // same sequence of collective exchanges, whether or not it owns patches of the level)
+    bool has_level(int l) const { return l < L && l < c->sub_levels; }
+    amr_status xchg(const ExchangeLists& x, double* buf, int per, const char* what) {
+        return c->comm.world > 1 ? c->comm.exchange_lists(c, x, buf, per, what) : AMR_OK;
+    }
 
     amr_status advance(int l, bool final, int sub_i) {
         static const double as[3] = {0.0, 0.75, 1.0 / 3.0}, bs[3] = {1.0, 0.25, 2.0 / 3.0};
@@ -1088,6 +1094,9 @@ struct SubRun {
         for (int s = 1; s <= 3; ++s) {
             double* Uin = s == 1 ? Un : (s == 2 ? c->U[P] : c->U[Q]);
             double* Uout = s == 2 ? c->U[Q] : c->U[P];
+            amr_status xs = xchg(c->comm.sub.face.empty() ? ExchangeLists() : c->comm.sub.face[l], Uin, (int)c->PS,
+                                 "subcycle face halo");
+            if (xs != AMR_OK) return xs;
             if (pl > 0) {   // ghosts: physical BC from the stage input, C/F from level l-1 in time (S2)
                 AuxArgs g = aux(c, Uin, nullptr);
                 g.proxy = c->sub_proxy.p;
@@ -1136,11 +1145,20 @@ struct SubRun {
         cur[l] = P;
         nstep[l]++;
         if (!has_level(l + 1)) return AMR_OK;
+        if (c->comm.world > 1) {   // coarse sources of level l+1's C/F ghosts, at the start and the end of this step
+            amr_status xs = xchg(c->comm.sub.coarse[l + 1], c->U[cur[l]], (int)c->PS, "subcycle coarse sources (new)");
+            if (xs == AMR_OK) xs = xchg(c->comm.sub.coarse[l + 1], c->U[start[l]], (int)c->PS, "subcycle coarse sources (old)");
+            if (xs != AMR_OK) return xs;
+        }
         amr_status st = advance(l + 1, false, 0);
         if (st != AMR_OK) return st;
         st = advance(l + 1, final, 1);
         if (st != AMR_OK) return st;
         const int r0 = c->rt_off[l], rl = c->rt_off[l + 1] - r0;
+        if (c->comm.world > 1) {   // accumulated registers of remote fine leaves on this level's C/F faces
+            st = xchg(c->comm.sub.facc[l], c->facc.p, 16 * c->n, "subcycle flux registers");
+            if (st != AMR_OK) return st;
+        }
         if (rl > 0) {   // S4
             AuxArgs x = aux(c, c->U[cur[l]], c->U[cur[l]]);
             x.freg = c->facc.p;
@@ -1171,6 +1189,8 @@ amr_status enqueue_step_subcycled(amr_ctx* c, double dt, double cfl) {
     r.L = c->cfg.num_levels;
     for (int l = 0; l < kMaxLevels; ++l) { r.cur[l] = r.start[l] = c->un; r.nstep[l] = 0; }
     amr_status s = r.advance(0, true, 0);
+    if (s != AMR_OK) return s;
+    s = c->comm.allreduce_max_u64(c, c->d_lambda);   // Lambda of U^(n+1) over all ranks
     if (s != AMR_OK) return s;
     for (int l = 0; l < r.L; ++l)
         if (r.has_level(l) && r.cur[l] != (c->un + 1) % 3)

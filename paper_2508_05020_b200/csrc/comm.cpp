@@ -141,6 +141,48 @@ ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_ne
     return from_needs(need, world, rank);
 }
 
+SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank) {
+    static const int cidx[4][2] = {{1, 3}, {0, 2}, {2, 3}, {0, 1}};   // children of a W/E/S/N neighbour on the face
+    const int L = t.levels;
+    std::vector<std::vector<std::map<int, std::set<int32_t>>>> face(L), coarse(L), facc(L);
+    for (int l = 0; l < L; ++l) {
+        face[l].resize(world);
+        coarse[l].resize(world);
+        facc[l].resize(world);
+    }
+    for (int id = 0; id < t.capacity; ++id) {
+        if (!t.alive[id]) continue;   // every active patch is advanced (leaves, and covered patches)
+        const int l = t.lev[id], o = owner[id];
+        const bool leaf = t.is_leaf(id);
+        for (int s = 0; s < 4; ++s) {
+            const int nb = t.neighbour(id, kSideDir[s][0], kSideDir[s][1]);
+            if (nb >= 0) {
+                if (owner[nb] != o) face[l][o][owner[nb]].insert(nb);
+                if (leaf && t.has_children(nb))
+                    for (int h = 0; h < 2; ++h) {
+                        const int f = t.child[4 * nb + cidx[s][h]];
+                        if (f >= 0 && owner[f] != o) facc[l][o][owner[f]].insert(f);
+                    }
+            } else if (nb == -1 && leaf) {
+                const int par = t.parent[id];
+                if (par < 0) continue;
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
+                        if (q >= 0 && owner[q] != o) coarse[l][o][owner[q]].insert(q);
+                    }
+            }
+        }
+    }
+    SubLists out;
+    for (int l = 0; l < L; ++l) {
+        out.face.push_back(from_needs(face[l], world, rank));
+        out.coarse.push_back(from_needs(coarse[l], world, rank));
+        out.facc.push_back(from_needs(facc[l], world, rank));
+    }
+    return out;
+}
+
 ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& old_owner,
                              const std::vector<int32_t>& new_owner, int world, int rank) {
     std::vector<std::map<int, std::set<int32_t>>> need(world);
@@ -405,6 +447,7 @@ amr_status Comm::init(amr_ctx* c) {
     world = c->cfg.world_size;
     rank = c->cfg.rank;
     halo_mode = c->cfg.halo_mode;
+    subcycle = c->cfg.subcycle != 0;
     owner = partition_owners(c->tree, world);
     if (world == 1) return AMR_OK;
     if (c->cfg.comm_backend == 1) {
@@ -468,6 +511,7 @@ void Comm::replan(const PatchTree& t) {
     halo = plan_halo(t, owner, world, rank);
     flux = plan_flux(t, owner, world, rank);
     if (halo_mode == 2) halo_cf = plan_halo(t, owner, world, rank, false);
+    if (subcycle) sub = plan_subcycle(t, owner, world, rank);
     ++lists_version;
 }
 

@@ -39,6 +39,14 @@ ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, i
 // coarse sources of new level-l patches prolonged by the (old) owner of their root
 ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_new, int level,
                           const std::vector<int32_t>& owner, int world, int rank);
+// subcycling (NEXT #4) across ranks, per level l: the remote slots a level-l stage reads (same-level face
+// neighbours of every advanced level-l patch, leaves and covered ones), the remote coarse sources of the level's
+// C/F ghosts (read at two times: the coarse step's start and end buffers), and the remote fine leaves whose
+// accumulated registers the level-l reflux reads
+struct SubLists {
+    std::vector<ExchangeLists> face, coarse, facc;
+};
+SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
 ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& old_owner,
                              const std::vector<int32_t>& new_owner, int world, int rank);
 
@@ -49,6 +57,8 @@ struct Comm {
     std::unique_ptr<Transport> tr;
     std::vector<int32_t> owner;        // per slot (patch id); -1 for free slots
     ExchangeLists halo, flux, halo_cf;
+    bool subcycle = false;
+    SubLists sub;                      // subcycle: per-level lists (plan_subcycle)
     uint64_t lists_version = 0;        // bumped by replan
     int64_t bytes_sent = 0;
 

@@ -130,6 +130,7 @@ struct amr_ctx {
     std::vector<ProxyTask> sub_ptasks;
     std::vector<AccTask> acc_tasks;
     std::vector<int32_t> sub_off, sub_poff, acc_off, rt_off;   // per level [L+1]
+    int sub_levels = 0;                                        // levels present in the (replicated) tree
     DevArray<LeafDesc> d_sub_descs;
     DevArray<ProxyTask> d_sub_ptasks;
     DevArray<AccTask> d_acc_tasks;

@@ -76,6 +76,8 @@ CASES = {
     "uniform_periodic_c4": (W.sweep(N=128, n=16, scheme="central4", seed=3, ic="smooth"), 4, None),
     "quadrant_amr_weno": (W.quadrant(N=64, n=16, levels=3, seed=2), 8, 4),
     "shock_bubble_reflective": (W.shock_bubble(Nx=128, Ny=64, n=16, levels=3), 8, 4),
+    "shock_bubble_subcycled": (dict(W.shock_bubble(Nx=128, Ny=64, n=16, levels=3), subcycle=1), 4, 2),
+    "implosion_c4_subcycled_n32": (W.implosion(N=256, n=32, scheme="central4", levels=3, subcycle=1), 4, 2),
 }
 
 
