@@ -23,7 +23,9 @@ void amr_plan_destroy(amr_plan* p);
 amr_status amr_plan_regrid(amr_plan* p, int32_t n, const int32_t* tree_index, const uint8_t* bits);
 /* Patch metadata in canonical order (owner = rank under a world_size partition). */
 amr_status amr_plan_tree(amr_plan* p, int32_t world_size, amr_patch_desc* out, int32_t cap, int32_t* count);
-/* Exchange lists of `rank`: kind 0 halo (per stage), 1 flux registers.  counts_*[world] per peer;
+/* Exchange lists of `rank`: kind 0 halo (per stage), 1 flux registers; subcycling (plan_subcycle) for level l:
+ * kind 2 + 3 l face halo of a level-l stage, 3 + 3 l coarse sources of its C/F ghosts, 4 + 3 l accumulated
+ * registers of the fine leaves its reflux reads.  counts_*[world] per peer;
  * the index arrays hold the peers' lists back to back (capacity cap each). */
 amr_status amr_plan_exchange(amr_plan* p, int32_t world_size, int32_t rank, int32_t kind, int32_t* send_counts,
                              int32_t* send_index, int32_t* recv_counts, int32_t* recv_index, int32_t cap);

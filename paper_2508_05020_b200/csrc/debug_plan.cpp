@@ -103,8 +103,15 @@ amr_status amr_plan_exchange(amr_plan* p, int32_t world, int32_t rank, int32_t k
     std::vector<int32_t> canon;
     std::vector<int32_t> pos = canon_pos_of(p->tree, canon);
     std::vector<int32_t> owner = amr::partition_owners(p->tree, world);
-    amr::ExchangeLists L = kind == 0 ? amr::plan_halo(p->tree, owner, world, rank)
-                                     : amr::plan_flux(p->tree, owner, world, rank);
+    amr::ExchangeLists L;
+    if (kind == 0) L = amr::plan_halo(p->tree, owner, world, rank);
+    else if (kind == 1) L = amr::plan_flux(p->tree, owner, world, rank);
+    else {
+        const int l = (kind - 2) / 3, which = (kind - 2) % 3;
+        if (kind < 2 || l >= p->levels) return AMR_E_ARG;
+        amr::SubLists S = amr::plan_subcycle(p->tree, owner, world, rank);
+        L = which == 0 ? S.face[l] : (which == 1 ? S.coarse[l] : S.facc[l]);
+    }
     int ns = 0, nr = 0;
     for (int q = 0; q < world; ++q) {
         send_counts[q] = (int32_t)L.send[q].size();

@@ -109,6 +109,46 @@ def needed_sources(tree, rank, world_tree):
     return need
 
 
+def needed_subcycle(tree, rank, levels=3):
+    """Independent statement of the subcycled exchanges of `rank`: per level, remote same-level face
+    neighbours of every owned active patch, remote coarse sources of owned leaves' C/F sides, remote fine leaves
+    on owned leaves' coarse C/F sides."""
+    key = {(d.level, d.i, d.j): e for e, d in enumerate(tree)}
+    npx = {l: (128 // 8) << l for l in range(levels)}
+    npy = {l: (64 // 8) << l for l in range(levels)}
+    face, coarse, facc = ([set() for _ in range(levels)] for _ in range(3))
+
+    def pos(l, i, j):
+        i %= npx[l]
+        if j < 0 or j >= npy[l]:
+            return None
+        return key.get((l, i, j))
+
+    for d in tree:
+        if d.owner != rank:
+            continue
+        l = d.level
+        for dx, dy in SIDES:
+            q = pos(l, d.i + dx, d.j + dy)
+            if q is not None:
+                if tree[q].owner != rank:
+                    face[l].add(q)
+                if d.leaf and not tree[q].leaf:        # the two fine leaves of q along the shared face
+                    for k in range(2):
+                        fi = 2 * tree[q].i + (1 if dx == -1 else 0 if dx == 1 else k)
+                        fj = 2 * tree[q].j + (1 if dy == -1 else 0 if dy == 1 else k)
+                        f = key[(l + 1, fi, fj)]
+                        if tree[f].owner != rank:
+                            facc[l].add(f)
+            elif d.leaf and 0 <= d.j + dy < npy[l]:
+                for ddy in (-1, 0, 1):
+                    for ddx in (-1, 0, 1):
+                        c = pos(l - 1, d.i // 2 + ddx, d.j // 2 + ddy)
+                        if c is not None and tree[c].owner != rank:
+                            coarse[l].add(c)
+    return face, coarse, facc
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -118,7 +158,11 @@ def _worker(rank, world, port, q):
         tr = p.tree(world)
         halo = dict(zip(("send", "recv"), p.exchange(world, rank, 0)))
         flux = dict(zip(("send", "recv"), p.exchange(world, rank, 1)))
-        mine = {"rank": rank, "owner": [d.owner for d in tr], "halo": halo, "flux": flux,
+        sub = {k: [dict(zip(("send", "recv"), p.exchange(world, rank, 2 + 3 * l + w))) for l in range(3)]
+               for w, k in enumerate(("face", "coarse", "facc"))}
+        ns = needed_subcycle(tr, rank)
+        mine = {"rank": rank, "owner": [d.owner for d in tr], "halo": halo, "flux": flux, "sub": sub,
+                "sub_need": {k: [sorted(x) for x in v] for k, v in zip(("face", "coarse", "facc"), ns)},
                 "need": sorted(needed_sources(tr, rank, tr)),
                 "leaves": sum(1 for d in tr if d.leaf and d.owner == rank)}
         allv = [None] * world
@@ -200,3 +244,19 @@ def test_partition_weak_scaling_slabs():
         send, recv = p.exchange(world, 0, 0)
         # the square of rank 0 needs one row of 128 patches from each y-neighbour
         assert sum(len(v) for v in recv.values()) == 256   # two rows of 128 (periodic in y)
+
+
+@pytest.mark.parametrize("kind", ["face", "coarse", "facc"])
+def test_gloo_subcycle_lists_match_and_cover_every_remote_read(gathered, kind):
+    """Subcycling across ranks: per level, rank 0's sends are rank 1's receives and vice versa, and every
+    rank receives exactly the remote slots its level-l kernels read (independent statement above)."""
+    a, b = gathered
+    nonempty = 0
+    for l in range(3):
+        assert a["sub"][kind][l]["send"][1] == b["sub"][kind][l]["recv"][0]
+        assert b["sub"][kind][l]["send"][0] == a["sub"][kind][l]["recv"][1]
+        for r in gathered:
+            got = r["sub"][kind][l]["recv"][1 - r["rank"]]
+            assert sorted(got) == r["sub_need"][kind][l], (kind, l, r["rank"])
+            nonempty += len(got)
+    assert nonempty > 0, kind
