@@ -242,15 +242,15 @@ class Mesh:
     def set_state(self, fn=None, U=None, indices=None):
         """Set patches from fn(l, P, Q) -> U[4][n][n] (only the patches this rank owns are evaluated), or from
         U[k][4][n][n] for tree indices `indices` (default: every patch, tree order)."""
-        tr = self.tree()
         if U is None:
+            tr = self.tree()
             indices = self.owned() if indices is None else np.asarray(indices, np.int32)
             U = np.empty((len(indices), 4, self.n, self.n))
             for e, ti in enumerate(indices):
                 d = tr[ti]
                 U[e] = fn(d.level, d.i, d.j)
         if indices is None:
-            indices = np.arange(len(tr), dtype=np.int32)
+            indices = np.arange(len(self.tree()), dtype=np.int32)
         idx = np.ascontiguousarray(indices, dtype=np.int32)
         U = np.ascontiguousarray(U, dtype=np.float64)
         assert U.shape[0] == len(idx)
@@ -279,11 +279,17 @@ class Mesh:
         assert tensor.is_cuda and tensor.is_contiguous() and tensor.numel() == len(idx) * 4 * self.n * self.n
         self._chk(self.L.amr_get_state_device(self.h, len(idx), idx.ctypes.data_as(_I32), tensor.data_ptr()))
 
-    def get_state(self, as_dict=True, indices=None):
-        """State of patches `indices` (default all; on several ranks only owned patches are filled)."""
-        tr = self.tree()
+    def get_state(self, as_dict=True, indices=None, out=None):
+        """State of patches `indices` (default all; on several ranks only owned patches are filled).  `out`: a
+        preallocated C-contiguous float64 array [k][4][n][n] to fill (e.g. a pinned-memory view: the download
+        then runs at full PCIe rate, with no fresh pageable allocation)."""
+        tr = self.tree() if (as_dict or indices is None) else None
         idx = np.arange(len(tr), dtype=np.int32) if indices is None else np.ascontiguousarray(indices, np.int32)
-        U = np.empty((len(idx), 4, self.n, self.n))
+        if out is None:
+            U = np.empty((len(idx), 4, self.n, self.n))
+        else:
+            U = out
+            assert U.dtype == np.float64 and U.flags.c_contiguous and U.size == len(idx) * 4 * self.n * self.n
         self._chk(self.L.amr_get_state(self.h, len(idx), idx.ctypes.data_as(_I32), U.ctypes.data_as(_D)))
         if not as_dict:
             return U
