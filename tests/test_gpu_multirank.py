@@ -114,3 +114,21 @@ def test_peer_pull_launches_one_kernel_per_exchange():
         res = run_multi(dict(cfg, halo_mode=hm), 2, steps, regrid)
         st[hm] = res[0][4]
     assert st[1]["launches"] < st[0]["launches"], st
+
+
+@pytest.mark.parametrize("halo_mode", [0, 1, 2])
+def test_more_ranks_than_roots(halo_mode):
+    """Degenerate partition: 6 virtual ranks over 4 root patches -- two ranks own nothing and run every
+    collective with empty launch lists; the owned results are still bitwise those of one rank."""
+    cfg = W.sweep(N=64, n=32, scheme="central4", seed=5, ic="smooth")
+    ref_state, ref_keys, ref_dts = run_single(cfg, 3, None)
+    res = run_multi(dict(cfg, halo_mode=halo_mode), 6, 3, None)
+    merged = {}
+    owners = set()
+    for r, (st, keys, dts, own, stats) in enumerate(res):
+        assert keys == ref_keys and dts == ref_dts
+        owners |= {r} if st else set()
+        merged.update(st)
+    assert len(owners) == 4
+    for k, U in ref_state.items():
+        assert np.array_equal(U, merged[k]), k

@@ -304,3 +304,17 @@ def test_set_state_fn_matches_patch_arrays():
     assert set(s1) == set(s2)
     for k in s1:
         np.testing.assert_allclose(s2[k], s1[k], rtol=0, atol=1e-14 * np.abs(s1[k]).max())
+
+
+def test_empty_calls():
+    """Zero-patch state transfers and an empty request list are valid no-ops."""
+    cfg = W.quadrant(N=64, n=16, levels=2, seed=3)
+    g = amr.Mesh(cfg)
+    g.set_state(lambda l, P, Q: W.patch_state(cfg, l, P, Q))
+    before = g.get_state()
+    g.set_state(U=np.zeros((0, 4, 16, 16)), indices=np.zeros(0, np.int32))
+    assert g.get_state(as_dict=False, indices=np.zeros(0, np.int32)).shape == (0, 4, 16, 16)
+    assert g.regrid_with_requests([], []) == (0, 0)
+    after = g.get_state()
+    assert set(before) == set(after) and all(np.array_equal(before[k], after[k]) for k in before)
+    g.close()
