@@ -290,13 +290,15 @@ def measure_sweep_table(X, args, hbm_peak):
     CUDA-event time over 3 steps after 1 warm-up step, each step from the pristine state."""
     torch = X.torch
     rows = []
+    fpk_inst = 148 * 64 * 1.965e9
     for n in (8, 16, 32, 64):
         small = W.sweep(N=4096, n=n, scheme="central4", seed=7)
         U0 = torch.from_numpy(W.level0_state(small)).cuda()
-        for N in (4096, 8192, 16384):
+        runs = [(N, "central4", 1) for N in (4096, 8192, 16384)] + [(4096, "weno5", 1), (4096, "weno5", 0)]
+        for N, scheme, char in runs:
             r = N // 4096
-            cfg = W.sweep(N=N, n=n, scheme="central4", seed=7)
-            cfg.update(check_positivity=0, stage_kernel=args.stage_kernel)
+            cfg = W.sweep(N=N, n=n, scheme=scheme, seed=7)
+            cfg.update(check_positivity=0, stage_kernel=args.stage_kernel, characteristic=char)
             mesh = X.mesh(cfg)
             Ut = U0.repeat(r, r, 1, 1, 1).reshape(-1, 4, n, n).contiguous()
             torch.cuda.synchronize()   # Ut is written on torch's stream; the library reads it on its own
@@ -318,8 +320,11 @@ def measure_sweep_table(X, args, hbm_peak):
             ms = st["stage_ms"] / max(1, st["stage_timed"])
             cells = st["stage_cells"] / max(1, st["stage_timed"])
             gbs = st["stage_bytes"] / max(1, st["stage_timed"]) / (ms / 1e3) / 1e9
-            rows.append({"N": N, "n": n, "stage_ms": ms, "cell_updates_per_s": cells / (ms / 1e3),
-                         "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak})
+            row = {"N": N, "n": n, "scheme": scheme if scheme == "central4" else ("weno5_char" if char else "weno5_comp"),
+                   "stage_ms": ms, "cell_updates_per_s": cells / (ms / 1e3), "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak}
+            if scheme == "weno5" and char:   # fp64-issue bound: SASS instruction count of the WENO5-char kernel
+                row["fp64_issue_frac"] = fp64_work("weno5_char")["fp64_thread_inst_per_cell_stage"] * row["cell_updates_per_s"] / fpk_inst
+            rows.append(row)
         del U0
         torch.cuda.empty_cache()
     return rows
@@ -362,22 +367,27 @@ def measure_amr(X, cfg, workload, windows=3):
         X.barrier()
         e0.record(X.stream)
         sim_t = 0.0
+        rg = 0.0
         for s in range(1, steps + 1):
             leaf_cells += mesh.stats()["leaf_cells"]
             sim_t += mesh.step(cfl=0.5, want_dt=True)
             if s % 4 == 0:
+                t0 = time.perf_counter()   # host wall time of the regrid call (it synchronises the stream)
                 mesh.regrid()
+                rg += time.perf_counter() - t0
         e1.record(X.stream)
         e1.synchronize()
         ms = X.max_over_ranks(e0.elapsed_time(e1))
-        res.append((ms, X.sum_over_ranks(leaf_cells), sim_t))
+        res.append((ms, X.sum_over_ranks(leaf_cells), sim_t, X.max_over_ranks(rg * 1e3)))
     st = mesh.stats()
     mesh.close()
-    ms, cells, sim_t = sorted(res)[len(res) // 2]
+    ms, cells, sim_t, rg_ms = sorted(res)[len(res) // 2]
     out = {"value": cells * 3 / (ms / 1e3), "ms_per_step": ms / steps, "leaves": st["leaves"],
            "patches": st["patches"], "leaf_cells_last": st["leaf_cells"], "workload": workload,
            "simulated_time_per_s": sim_t / (ms / 1e3),
-           "windows_ms_per_step": [r[0] / steps for r in res], "reported": "median window"}
+           "windows_ms_per_step": [r[0] / steps for r in res], "reported": "median window",
+           "regrid_ms_per_call": rg_ms / (steps // 4),
+           "step_ms_without_regrid": (ms - rg_ms) / steps}
     if cfg.get("subcycle"):
         out["value_note"] = "leaf cell-updates counted once per level-0 step (finer levels update 2^l times)"
     return out
@@ -434,15 +444,19 @@ def main():
                           "states (DESIGN.md s6); throughput config only"}
     if not args.no_amr:
         extra["quadrant_amr"] = measure_quadrant(X, args)
+        G = X.world   # D4w: G mirrored copies of configs[3] stacked in y, one per GPU (weak scaling; G = 1: configs[3])
         extra["shock_bubble_amr"] = measure_amr(
-            X, W.shock_bubble(), "BASELINE configs[3] shock-bubble AMR, 2048x1024 base, 4 levels, 16^2 patches, "
-                                 "WENO5-char, reflective walls, 8 CFL-0.5 steps with 2 regrids inside the timed region")
+            X, W.shock_bubble(G=G), f"BASELINE configs[3] shock-bubble AMR{' (D4w weak scaling, %d copies)' % G if G > 1 else ''}, "
+                                    f"2048x{1024 * G} base, 4 levels, 16^2 patches, WENO5-char, reflective walls, 8 CFL-0.5 "
+                                    "steps with 2 regrids inside the timed region")
         if X.world == 1:   # NEXT #4: the same problem with Berger-Colella subcycling (level-0 steps)
             extra["shock_bubble_amr_subcycled"] = measure_amr(
                 X, dict(W.shock_bubble(), subcycle=1),
                 "configs[3] with time subcycling: 8 level-0 steps (each = 8 finest-level steps), 2 regrids")
     if not args.no_sweep_table and X.world == 1:
-        extra["sweep_table"] = {"workload": "BASELINE configs[4]: Central4 stage kernel per total size and patch size",
+        extra["sweep_table"] = {"workload": "BASELINE configs[4]: stage kernel per total size and patch size (Central4 at "
+                                            "4096^2..16384^2; WENO5 char / comp at 4096^2; fp64_issue_frac from the "
+                                            "n = 32 WENO5-char SASS count)",
                                 "rows": measure_sweep_table(X, args, hbm_peak)}
     if X.rank == 0:
         rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
