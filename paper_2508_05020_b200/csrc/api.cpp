@@ -294,7 +294,9 @@ amr_status build_plan(amr_ctx* c) {
     // order, B = 32/n) form the 32 x 32 tiles of the TMA group kernel; the other leaves take the per-tile kernel
     c->gleaves.clear();
     c->singles.clear();
-    if (c->cfg.stage_kernel == 0 && c->cfg.scheme == AMR_CENTRAL4 && (c->n == 8 || c->n == 16) && !c->cfg.subcycle) {
+    const bool group_c4 = c->cfg.scheme == AMR_CENTRAL4 && (c->n == 8 || c->n == 16);
+    const bool group_weno = c->cfg.scheme != AMR_CENTRAL4 && c->n == 8;   // n = 16 WENO: one CTA per patch (DESIGN s5)
+    if (c->cfg.stage_kernel == 0 && (group_c4 || group_weno) && !c->cfg.subcycle) {
         const int B = 32 / c->n, K = B * B;
         for (size_t e = 0; e < c->leaves.size();) {
             const int id0 = c->leaf_ids[e];

@@ -1750,6 +1750,168 @@ cudaError_t launch_c4_group_t(const StageArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- WENO5 stage kernel for 8^2 patches (groups)
+// n = 8 with WENO5: the 32 x 32 tiles of 4 x 4 same-level leaves of the Central4 group kernel (StageArgs.gleaves,
+// member m at block position demorton(m)), processed like one 32 x 32 tile of stage_kernel: one halo gather for
+// the block (members' interiors, outer strips from the edge members' neighbours), 32 x 35 faces per direction
+// instead of 16 x (8 x 11) -- the Eq. 9 stencil's extra faces and the halo are paid once per block -- and
+// per-member epilogue addressing.  Faces between members are same-level faces.  (For n = 16 the 2 x 2 blocks
+// measured slower on the AMR configs -- fewer, larger CTAs -- so n = 16 keeps one CTA per patch.)
+template <int SCHEME, int N>
+__global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_kernel(const StageArgs a) {
+    constexpr int T = 32, G = kGL, B = T / N, K = B * B, NN = N * N;
+    constexpr int NT = Block<T>::NT;
+    constexpr int W = T + 2 * G, PL = W * W, NF = T + 3;
+    constexpr int CPT = T * T / NT;
+    constexpr size_t PS = 4 * (size_t)NN;
+    extern __shared__ __align__(16) double smem[];
+    double* sQ = smem;                 // [4][W][W] conserved
+    double* sF = smem + 4 * PL;        // [4][T][NF] x-fluxes, then [4][NF][T] y-fluxes
+    __shared__ LeafDesc sD[K];
+
+    const int tid = threadIdx.x;
+    if (tid < K) sD[tid] = a.gleaves[(size_t)blockIdx.x * K + tid];
+    __syncthreads();
+    auto mem = [](int x, int y) { return (x & 1) | ((y & 1) << 1) | ((x & 2) << 1) | ((y & 2) << 2); };
+
+    // ---- halo gather (a1): plus-shaped block tile in 16-byte chunks; a chunk never straddles two members
+    {
+        constexpr int CR = W / 2, CB = T * CR, CS = G * T / 2, CV = CB + 2 * CS;
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sQ);
+        for (int e = tid; e < 4 * CV; e += NT) {
+            int kq = e / CV, f = e - kq * CV, i, j;
+            if (f < CB) { j = f / CR; i = 2 * (f - j * CR) - G; }
+            else if (f < CB + CS) { int h = f - CB; j = h / (T / 2) - G; i = 2 * (h - (j + G) * (T / 2)); }
+            else { int h = f - CB - CS; j = h / (T / 2); i = 2 * (h - j * (T / 2)); j += T; }
+            const int mx = i < 0 ? 0 : (i >= T ? B - 1 : i / N), my = j < 0 ? 0 : (j >= T ? B - 1 : j / N);
+            const LeafDesc& d = sD[mem(mx, my)];
+            int pi = i - mx * N, pj = j - my * N, sl = d.slot;
+            bool halo = true;
+            if (pi < 0) { sl = d.side[kW]; pi += N; }
+            else if (pi >= N) { sl = d.side[kE]; pi -= N; }
+            else if (pj < 0) { sl = d.side[kS]; pj += N; }
+            else if (pj >= N) { sl = d.side[kN]; pj -= N; }
+            else halo = false;
+            const double* base = !halo ? a.Uin + (size_t)sl * PS
+                                       : (sl >= 0 ? a.Uin + (size_t)sl * PS : a.proxy + (size_t)(-1 - sl) * PS);
+            cp_async16(sb + (uint32_t)((kq * PL + (j + G) * W + (i + G)) * 8), base + kq * NN + pj * N + pi);
+        }
+        cp_async_wait_all();
+    }
+    __syncthreads();
+
+    const double g = a.gamma;
+    const int lvl = sD[0].level;
+    const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
+    const bool div4 = a.div_order == 4;
+
+    // ---- x faces (a4-a6): face m (left of cell m), row j
+    for (int e = tid; e < T * NF; e += NT) {
+        int j = e / NF, m = e - j * NF - 1;
+        int o = (j + G) * W + (m + G);
+        double f[4];
+        weno_rusanov<SCHEME == 1>(sQ + o - 3, 1, PL, 1, 2, g, a.eps, f);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sF[(q * T + j) * NF + m + 1] = f[q];
+    }
+    __syncthreads();
+    double acc[CPT][4];
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        const int c = tid + r * NT, i = c % T, j = c / T;
+        const LeafDesc& dw = sD[mem(0, j / N)];
+        const LeafDesc& de = sD[mem(B - 1, j / N)];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double* fr = sF + (q * T + j) * NF + i + 1;
+            double fl = fr[0], fh = fr[1];
+            double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-1] + fh) : fl;
+            double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2]) : fh;
+            acc[r][q] = -(Fh - Fl) * idx;
+            if (i == 0 && ((dw.cf | (dw.cf >> 4)) & 1))   // flux registers of C/F sides on the block edge
+                a.freg[(((size_t)dw.slot * 4 + kW) * 4 + q) * N + j % N] = Fl;
+            if (i == T - 1 && ((de.cf | (de.cf >> 4)) & 2))
+                a.freg[(((size_t)de.slot * 4 + kE) * 4 + q) * N + j % N] = Fh;
+        }
+    }
+    __syncthreads();
+    // ---- y faces: face m (below cell m), column i; normal momentum is component 2
+    for (int e = tid; e < T * NF; e += NT) {
+        int m = e / T - 1, i = e - (m + 1) * T;
+        int o = (m + G) * W + (i + G);
+        double f[4];
+        weno_rusanov<SCHEME == 1>(sQ + o - 3 * W, W, PL, 2, 1, g, a.eps, f);
+        sF[(0 * NF + m + 1) * T + i] = f[0];
+        sF[(1 * NF + m + 1) * T + i] = f[2];
+        sF[(2 * NF + m + 1) * T + i] = f[1];
+        sF[(3 * NF + m + 1) * T + i] = f[3];
+    }
+    __syncthreads();
+
+    // ---- y divergence, SSP-RK3 combination (a8), checks, Lambda (a9), per member
+    const double dt = *a.dt;
+    unsigned long long lam = 0ull;
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        const int c = tid + r * NT, i = c % T, j = c / T;
+        const LeafDesc& dm = sD[mem(i / N, j / N)];
+        const LeafDesc& ds = sD[mem(i / N, 0)];
+        const LeafDesc& dn = sD[mem(i / N, B - 1)];
+        const int li = i % N, lj = j % N;
+        const size_t off = (size_t)lj * N + li;
+        const double* pin = a.Uin + (size_t)dm.slot * PS;
+        const double* pn = a.Un + (size_t)dm.slot * PS;
+        double* po = a.Uout + (size_t)dm.slot * PS;
+        double o4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double* fr = sF + (q * NF + j + 1) * T + i;
+            double fl = fr[0], fh = fr[T];
+            double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-T] + fh) : fl;
+            double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2 * T]) : fh;
+            double L = acc[r][q] - (Fh - Fl) * idy;
+            if (j == 0 && ((ds.cf | (ds.cf >> 4)) & 4)) a.freg[(((size_t)ds.slot * 4 + kS) * 4 + q) * N + li] = Fl;
+            if (j == T - 1 && ((dn.cf | (dn.cf >> 4)) & 8)) a.freg[(((size_t)dn.slot * 4 + kN) * 4 + q) * N + li] = Fh;
+            double v = __ldg(pin + q * NN + off) + dt * L;
+            if (a.stage > 1) v = a.a * __ldg(pn + q * NN + off) + a.b * v;
+            o4[q] = v;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) po[q * NN + off] = o4[q];
+        const int cm = dm.cf & 15;   // C/F coarse sides are block-edge sides (members are same-level neighbours)
+        const bool edge_cf = ((cm & 1) && li == 0) || ((cm & 2) && li == N - 1) || ((cm & 4) && lj == 0) ||
+                             ((cm & 8) && lj == N - 1);
+        if (!edge_cf) {
+            if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], g)) report_error(a.err, dm.slot, a.stage, (int)off);
+            if (a.want_lambda) {
+                double sp = wave_speed(o4[0], o4[1], o4[2], o4[3], g, idx, idy);
+                if (a.lam0) sp = ldexp(sp, -dm.level);
+                unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
+                lam = bits > lam ? bits : lam;
+            }
+        }
+    }
+    if (a.want_lambda) {
+        lam = warp_max_u64(lam);
+        if ((tid & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
+    }
+}
+
+template <int SCHEME, int N>
+cudaError_t launch_group_t(const StageArgs& a, cudaStream_t s) {
+    constexpr size_t smem = stage_smem<SCHEME, 32>();
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(stage_group_kernel<SCHEME, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    if (a.ngroups == 0) return cudaSuccess;
+    stage_group_kernel<SCHEME, N><<<a.ngroups, Block<32>::NT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int SCHEME>
 cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
     int T = a.geo.n / a.tiles;
@@ -1775,6 +1937,10 @@ cudaError_t launch_stage_s(const StageArgs& a, cudaStream_t s) {
             case 64: return launch_c4_t<64>(a, s);
             default: return cudaErrorInvalidValue;
         }
+    }
+    if (a.variant == 0 && a.gleaves && a.geo.n == 8) {   // WENO 4 x 4 block tiles, then the rest
+        cudaError_t e = launch_group_t<SCHEME, 8>(a, s);
+        if (e != cudaSuccess || a.nleaves == 0) return e;
     }
     if (T == 8) return launch_stage_t<SCHEME, 8>(a, s);
     if (T == 16) return launch_stage_t<SCHEME, 16>(a, s);
