@@ -474,14 +474,15 @@ __device__ __forceinline__ void c4_face16(const double (&p)[4], const double (&T
                                           const double (&ut)[4], double inv_gm1, double F16[4]) {
     const double pe = fma(9.0, p[1] + p[2], -(p[0] + p[3]));      // 16 p_e
     const double Te = fma(9.0, Tt[1] + Tt[2], -(Tt[0] + Tt[3]));  // 16 T_e
-    const double ue = 0.0625 * fma(9.0, un[1] + un[2], -(un[0] + un[3]));
+    const double U16 = fma(9.0, un[1] + un[2], -(un[0] + un[3]));   // 16 u_e
+    const double ue = 0.0625 * U16;
     const double ve = 0.0625 * fma(9.0, ut[1] + ut[2], -(ut[0] + ut[3]));
     const double re = pe * fast_rcp(Te);                          // rho_e (scale-free)
     const double Ee = fma(pe, inv_gm1, (8.0 * re) * fma(ve, ve, ue * ue));   // 16 E_e
-    const double mn = re * ue;
-    F16[0] = 16.0 * mn;
-    F16[1] = fma(16.0 * mn, ue, pe);
-    F16[2] = (16.0 * mn) * ve;
+    const double mn16 = re * U16;                                 // = 16 (re ue) exactly
+    F16[0] = mn16;
+    F16[1] = fma(mn16, ue, pe);
+    F16[2] = mn16 * ve;
     F16[3] = (Ee + pe) * ue;
 }
 
