@@ -38,7 +38,8 @@ class _Cfg(C.Structure):
     _fields_ = [("lo", C.c_double * 2), ("hi", C.c_double * 2), ("base", C.c_int * 2), ("n", C.c_int),
                 ("levels", C.c_int), ("gamma", C.c_double), ("bc", C.c_int * 4), ("scheme", C.c_int),
                 ("characteristic", C.c_int), ("div_order", C.c_int), ("weno_eps", C.c_double),
-                ("theta", C.c_double), ("coarsen_frac", C.c_double), ("coarsen_rule", C.c_int)]
+                ("theta", C.c_double), ("coarsen_frac", C.c_double), ("coarsen_rule", C.c_int),
+                ("check_positivity", C.c_int)]
 
 
 _lib = None
@@ -111,6 +112,7 @@ def make_cfg(cfg: dict) -> _Cfg:
     c.theta = cfg.get("theta", 0.1)
     c.coarsen_frac = cfg.get("coarsen_frac", 0.25)
     c.coarsen_rule = {"r2_exact": 0, "alg2_literal": 1}[cfg.get("coarsen_rule", "r2_exact")]
+    c.check_positivity = int(cfg.get("check_positivity", 1))
     return c
 
 

@@ -645,7 +645,7 @@ void step(Oracle& o, double dt) {
             const std::vector<double>& u = next.at(kv.first);
             for (int e = 0; e < n * n; ++e) {
                 double Uc[4] = {u[e], u[n * n + e], u[2 * n * n + e], u[3 * n * n + e]};
-                if (!physical(Uc, o.c.gamma)) {
+                if (o.c.check_positivity && !physical(Uc, o.c.gamma)) {
                     char b[200];
                     std::snprintf(b, sizeof b, "non-physical state at stage %d, patch (l=%d,P=%d,Q=%d), cell %d", s + 1,
                                   kv.first.l, kv.first.P, kv.first.Q, e);
@@ -787,7 +787,7 @@ struct Subcycler {
                     accumulate(p, F, SSP_W[s]);
                     for (int e = 0; e < n * n; ++e) {
                         double Uc[4] = {out[e], out[n * n + e], out[2 * n * n + e], out[3 * n * n + e]};
-                        if (!physical(Uc, o.c.gamma)) {
+                        if (o.c.check_positivity && !physical(Uc, o.c.gamma)) {
                             char b[200];
                             std::snprintf(b, sizeof b, "non-physical state at level %d stage %d, patch (P=%d,Q=%d), cell %d",
                                           l, s + 1, p.P, p.Q, e);

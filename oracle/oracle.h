@@ -33,6 +33,8 @@ typedef struct {
     double theta;          /* refinement threshold (BJ configs[0]: 0.1)        */
     double coarsen_frac;   /* coarsen when eta < theta*coarsen_frac (A20: 0.25) */
     int coarsen_rule;      /* 0 R2-exact prose rule, 1 Alg. 2 literal  */
+    int check_positivity;  /* 1: a non-physical leaf state after a stage is an error; 0: not checked
+                              (the white-noise sweep is a throughput config, not physics) */
 } orc_config;
 
 void*       orc_create(const orc_config* cfg);

@@ -181,6 +181,7 @@ amr_status build_subcycle_plan(amr_ctx* c) {
 }
 
 amr_status build_plan(amr_ctx* c) {
+    NvtxRange nv("build_plan");
     PhaseClock clk;
     PatchTree& t = c->tree;
     const int L = c->cfg.num_levels;
@@ -463,7 +464,9 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
     const int A = (c->un + 1) % 3, B = (c->un + 2) % 3;
     const double as[3] = {0.0, 0.75, 1.0 / 3.0};
     const double bs[3] = {1.0, 0.25, 2.0 / 3.0};
+    static const char* const kStageName[3] = {"stage 1", "stage 2", "stage 3"};
     for (int s = 1; s <= 3; ++s) {
+        NvtxRange nv(kStageName[s - 1]);
         double* Uin = s == 1 ? c->U[c->un] : (s == 2 ? c->U[A] : c->U[B]);
         double* Uout = s == 2 ? c->U[B] : c->U[A];
         amr_status cs = c->comm.exchange_halos_stage(c, Uin);
@@ -1258,6 +1261,7 @@ amr_status enqueue_any_step(amr_ctx* c, double dt, double cfl) {
 }
 
 amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
+    NvtxRange nv("amr_step");
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     if (!(dt > 0.0) && !(cfl > 0.0)) return fail(c, AMR_E_ARG, "step: need dt > 0 or cfl > 0");
@@ -1270,6 +1274,7 @@ amr_status amr_step(amr_ctx* c, double dt, double cfl, double* dt_used) {
 }
 
 amr_status amr_steps(amr_ctx* c, int32_t nsteps, double dt, double cfl) {
+    NvtxRange nv("amr_steps");
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     if (nsteps < 0 || (!(dt > 0.0) && !(cfl > 0.0))) return fail(c, AMR_E_ARG, "steps: bad arguments");
@@ -1304,6 +1309,7 @@ amr_status amr_get_flags(amr_ctx* c, int32_t cap, double* maxeta, uint8_t* bits)
 }
 
 amr_status amr_regrid(amr_ctx* c, int32_t* n_refined, int32_t* n_coarsened) {
+    NvtxRange nv("amr_regrid");
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     PhaseClock clk;

@@ -517,6 +517,7 @@ void Comm::replan(const PatchTree& t) {
 
 amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per, const char* what) {
     if (world == 1) return AMR_OK;
+    NvtxRange nv(what);
     size_t ns = L.nsend(), nr = L.nrecv();
     std::vector<int32_t> sidx, ridx;
     sidx.reserve(ns);
@@ -591,6 +592,7 @@ amr_status Comm::map_pool(amr_ctx* c, void* base, size_t bytes) {
 // fence, then one pull kernel for every slot of L.recv (each from its owner's mapped buffer at the same offset);
 // the slot lists go to the device once per plan.  Every rank calls this at the same points (collective fence).
 amr_status Comm::peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, double* dst, bool freg, const char* what) {
+    NvtxRange nv(what);
     auto bad = [&](amr_status st, const std::string& m) { c->err = std::string(what) + ": " + m; c->sticky = st; return st; };
     if (freg && mapped_freg != c->freg.p) {   // (re)map the flux-register buffers (identical sizes on every rank)
         std::vector<void*> peers(world, nullptr);

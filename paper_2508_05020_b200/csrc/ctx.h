@@ -58,6 +58,16 @@ inline uint64_t morton(uint32_t x, uint32_t y) { return spread_bits(x) | (spread
 
 using namespace amr;
 
+// NVTX ranges (header-only NVTX v3; free when no tool is attached): host-side enqueue timeline of steps, stages,
+// exchanges and regrid phases for nsys
+#include <nvtx3/nvToolsExt.h>
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct amr_ctx {
     amr_config cfg{};
     PatchTree tree;
