@@ -190,7 +190,9 @@ amr_status build_plan(amr_ctx* c) {
     else for (int id : c->canon) c->canon_pos[id] = -1;
     if ((int)c->leaf_pos.size() != t.capacity) c->leaf_pos.assign(t.capacity, -1);
     else for (int id : c->leaf_ids) c->leaf_pos[id] = -1;
+    clk.mark("plan: reset maps");
     c->canon = t.canonical();
+    clk.mark("plan: canonical");
     for (size_t e = 0; e < c->canon.size(); ++e) c->canon_pos[c->canon[e]] = (int)e;
 
     // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos
@@ -206,6 +208,7 @@ amr_status build_plan(amr_ctx* c) {
         for (size_t e = 0; e < kv.size(); ++e) c->leaf_ids[e] = kv[e].second;
     }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
+    clk.mark("plan: leaf order");
     c->sib.clear();   // owned parents whose 4 children are (owned) leaves: the coarsening candidates of a12
     for (int id : c->canon) {
         if (!t.has_children(id)) continue;
@@ -282,6 +285,7 @@ amr_status build_plan(amr_ctx* c) {
         c->leaves.push_back(d);
         if (rt.mask) c->rtasks.push_back(rt);
     }
+    clk.mark("plan: leaf descriptors");
     c->rlev.assign(L, {});
     for (int id : c->canon) {
         if (!t.has_children(id) || !c->comm.owns(c, id)) continue;

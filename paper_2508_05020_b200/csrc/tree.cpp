@@ -41,7 +41,8 @@ void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, 
     for (int j = 0; j < npy; ++j)
         for (int i = 0; i < npx; ++i) kv.push_back({morton_key(i, j), j * npx + i});
     radix_sort_pairs(kv);
-    for (const auto& e : kv) alloc(0, e.second % npx, e.second / npx);
+    root_.assign((size_t)npx * npy, -1);
+    for (const auto& e : kv) root_[e.second] = alloc(0, e.second % npx, e.second / npx);
 }
 
 void PatchTree::touch(int id) {
@@ -117,13 +118,19 @@ int PatchTree::find(int l, int i, int j) const {
 }
 
 int PatchTree::neighbour(int id, int dx, int dy) const {
-    int l = lev[id], i = pi[id] + dx, j = pj[id] + dy;
-    if (l > 0) {   // a sibling (same parent; never across a wrap) comes from the parent's child links
-        const int a = (pi[id] & 1) + dx, b = (pj[id] & 1) + dy;
-        if (a >= 0 && a <= 1 && b >= 0 && b <= 1) return child[4 * parent[id] + a + 2 * b];
+    const int l = lev[id];
+    if (l == 0) {
+        int i = pi[id] + dx, j = pj[id] + dy;
+        if (!wrap(0, i, j)) return -2;
+        return root_[(size_t)j * np0[0] + i];
     }
-    if (!wrap(l, i, j)) return -2;
-    return index_.find(key(l, i, j));
+    int a = (pi[id] & 1) + dx, b = (pj[id] & 1) + dy;   // position relative to the parent's children, -1 .. 2
+    if (a >= 0 && a <= 1 && b >= 0 && b <= 1) return child[4 * parent[id] + a + 2 * b];   // a sibling
+    const int DX = a < 0 ? -1 : (a > 1 ? 1 : 0), DY = b < 0 ? -1 : (b > 1 ? 1 : 0);
+    const int pn = neighbour(parent[id], DX, DY);      // same-level neighbour of the parent (recursion by level)
+    if (pn < 0) return pn;                              // outside the domain, or missing
+    if (!has_children(pn)) return -1;
+    return child[4 * pn + (a - 2 * DX) + 2 * (b - 2 * DY)];
 }
 
 // Alg. 1 RefinePatch: before creating p's children make every
@@ -189,8 +196,10 @@ void PatchTree::delete_children(int id) {
 
 bool PatchTree::validate(std::string& err) const {
     for (int j = 0; j < np0[1]; ++j)
-        for (int i = 0; i < np0[0]; ++i)
-            if (find(0, i, j) < 0) { err = "R1 violated: root missing"; return false; }
+        for (int i = 0; i < np0[0]; ++i) {   // R1: the root table's slots are alive roots at their position
+            const int r = root_[(size_t)j * np0[0] + i];
+            if (r < 0 || !alive[r] || lev[r] != 0 || pi[r] != i || pj[r] != j) { err = "R1 violated: root missing"; return false; }
+        }
     std::vector<int32_t> ids;   // the active patches (O(active), not O(capacity))
     ids.reserve(index_.size());
     index_.for_each([&](uint64_t, int32_t id) { ids.push_back(id); });

@@ -128,7 +128,9 @@ struct PatchTree {
     // wrap a level-l patch position; false when outside a non-periodic boundary
     bool wrap(int l, int& i, int& j) const;
     int find(int l, int i, int j) const;          // id or -1 (position wrapped first)
-    int neighbour(int id, int dx, int dy) const;  // id, -1 missing, -2 outside domain
+    // id, -1 missing, -2 outside domain (|dx|, |dy| <= 1): by the parent/child links -- a sibling, else the child of
+    // the parent's neighbour (roots from a table) -- with no hash probe
+    int neighbour(int id, int dx, int dy) const;
     bool has_children(int id) const { return child[4 * id] >= 0; }
     bool is_leaf(int id) const { return alive[id] && child[4 * id] < 0; }
 
@@ -159,6 +161,7 @@ struct PatchTree {
     bool txn_ = false;
     void touch(int id);
     FlatIndex index_;
+    std::vector<int32_t> root_;   // root (i, j) -> slot, row-major (R1: roots are permanent)
     std::vector<int32_t> free_;   // min-heap of free slots
     int alloc(int l, int i, int j);
     void release(int id);
