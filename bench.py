@@ -54,8 +54,8 @@ def fp64_peak():
 
 
 def fp64_work(kernel):
-    """fp64 SASS work per leaf cell-stage of a stage kernel, counted by ncu (profiles/r1e_fp64_work.json)."""
-    p = os.path.join(ROOT, "profiles", "r1e_fp64_work.json")
+    """fp64 SASS work per leaf cell-stage of a stage kernel, counted by ncu (profiles/r1f_fp64_work.json)."""
+    p = os.path.join(ROOT, "profiles", "r1f_fp64_work.json")
     d = json.load(open(p)) if os.path.exists(p) else {}
     return d.get(kernel, {"fp64_thread_inst_per_cell_stage": float("nan"), "flops_per_cell_stage": float("nan")})
 
