@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define AMR_ABI_VERSION 2
+#define AMR_ABI_VERSION 3
 
 typedef struct amr_ctx amr_ctx;   /* opaque */
 
@@ -57,6 +57,16 @@ typedef enum {
 typedef enum { AMR_BC_PERIODIC = 0, AMR_BC_TRANSMISSIVE = 1, AMR_BC_REFLECTIVE = 2 } amr_bc;
 typedef enum { AMR_CENTRAL4 = 0, AMR_WENO5_RUSANOV = 1 } amr_scheme;
 typedef enum { AMR_COARSEN_R2_EXACT = 0, AMR_COARSEN_ALG2_LITERAL = 1 } amr_coarsen_rule;
+
+/* comm_backend 2 (multi-process test transport): collectives supplied by the caller, e.g. over a torch gloo
+ * group.  allgather: every rank contributes `bytes` from `send`; `recv` receives world_size x bytes in rank order.
+ * barrier: returns once every rank has called it.  Both return 0 on success.  Lets several processes share ONE GPU
+ * (NCCL refuses that) so that the CUDA-IPC peer mapping of halo_mode 1 / 2 is exercised without a second GPU. */
+typedef struct {
+    int32_t (*allgather)(const void* send, uint64_t bytes, void* recv, void* user);
+    int32_t (*barrier)(void* user);
+    void* user;
+} amr_host_comm;
 
 typedef struct {
     int32_t dim;                  /* 2, or 1 for the strip embedding of 1D problems (A23)   */
@@ -87,7 +97,9 @@ typedef struct {
                                      re-captured after mesh changes); single rank with kernel timing off only */
     int32_t comm_backend;         /* world_size > 1: 0 NCCL (nccl_unique_id = ncclUniqueId); 1 in-process
                                      loopback of virtual ranks on one GPU, one host thread each
-                                     (test-only; nccl_unique_id = 128-byte group key string)   */
+                                     (test-only; nccl_unique_id = 128-byte group key string); 2 one process
+                                     per rank with caller-supplied host collectives (host_comm; test-only:
+                                     data through host memory, peer pools through CUDA IPC)      */
     int32_t stage_kernel;         /* stage kernel organisation (NEXT #1 fusion study): 0 default (Central4 with
                                      n >= 32: persistent TMA-pipelined fused kernel, else 1); 1 fused, one CTA per
                                      tile with a cp.async halo gather; 2 unfused: four kernels per stage with the
@@ -111,6 +123,7 @@ typedef struct {
                                      sources of C/F ghosts are pulled (the halo transfer overlaps the compute).
                                      Regrid exchanges (coarse sources, migration, flags) use the transport in all
                                      modes */
+    const amr_host_comm* host_comm;   /* comm_backend 2: the caller's collectives (kept alive until destroy) */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none

@@ -26,7 +26,7 @@ SCHEME = {"central4": 0, "weno5": 1}
 COARSEN = {"r2_exact": 0, "alg2_literal": 1}
 
 # every symbol include/amr.h declares (checked by tests/test_abi.py)
-ABI_VERSION = 2   # include/amr.h AMR_ABI_VERSION: the amr_config layout below
+ABI_VERSION = 3   # include/amr.h AMR_ABI_VERSION: the amr_config layout below
 ABI_SYMBOLS = ["amr_abi_version", "amr_default_config", "amr_query_pool_bytes", "amr_create", "amr_destroy",
                "amr_set_state", "amr_set_state_fn", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
                "amr_regrid", "amr_regrid_with_flags", "amr_get_patch_tree", "amr_diagnostics",
@@ -44,7 +44,44 @@ class amr_config(C.Structure):
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("world_size", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("check_positivity", C.c_int32),
                 ("use_graphs", C.c_int32), ("comm_backend", C.c_int32), ("stage_kernel", C.c_int32), ("subcycle", C.c_int32),
-                ("halo_mode", C.c_int32)]
+                ("halo_mode", C.c_int32), ("host_comm", C.c_void_p)]
+
+
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p)
+HOST_BARRIER = C.CFUNCTYPE(C.c_int32, C.c_void_p)
+
+
+class amr_host_comm(C.Structure):
+    _fields_ = [("allgather", HOST_ALLGATHER), ("barrier", HOST_BARRIER), ("user", C.c_void_p)]
+
+
+def gloo_host_comm():
+    """(allgather, barrier) over the default torch.distributed group (e.g. gloo) for comm_backend 2: several
+    processes, possibly on one GPU, exchange through host memory and map each other's pools with CUDA IPC."""
+    import torch
+    import torch.distributed as dist
+    ws = dist.get_world_size()
+
+    def allgather(send, nbytes, recv, _user):
+        try:
+            src = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send)).copy()
+            outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(ws)]
+            dist.all_gather(outs, torch.from_numpy(src))
+            dst = np.ctypeslib.as_array((C.c_uint8 * (nbytes * ws)).from_address(recv))
+            for q in range(ws):
+                dst[q * nbytes:(q + 1) * nbytes] = outs[q].numpy()
+            return 0
+        except Exception:   # noqa: BLE001 -- reported to the library as a failed collective
+            return 1
+
+    def barrier(_user):
+        try:
+            dist.barrier()
+            return 0
+        except Exception:   # noqa: BLE001
+            return 1
+
+    return allgather, barrier
 
 
 class amr_patch_desc(C.Structure):
@@ -168,8 +205,9 @@ class Mesh:
     def __init__(self, cfg: dict, stream=None, pool=None, world_size=1, rank=0, comm_backend=0, comm_id=None,
                  **over):
         """world_size > 1: comm_backend 0 (NCCL; comm_id = 128-byte ncclUniqueId from nccl_unique_id(),
-        broadcast by the caller) or 1 (in-process loopback, one host thread per virtual rank; comm_id =
-        group key)."""
+        broadcast by the caller), 1 (in-process loopback, one host thread per virtual rank; comm_id = group key)
+        or 2 (one process per rank with host collectives; comm_id = (allgather, barrier), default
+        gloo_host_comm() over torch.distributed)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2508_05020_b200.Mesh needs a CUDA device (no CPU fallback)")
@@ -178,7 +216,13 @@ class Mesh:
         self.n = cfg["n"]
         self._keep = []
         self.world_size, self.rank = world_size, rank
-        if world_size > 1:
+        if world_size > 1 and comm_backend == 2:   # host collectives (comm_id = (allgather, barrier) callables)
+            ag, bar = comm_id if comm_id is not None else gloo_host_comm()
+            hc = amr_host_comm(HOST_ALLGATHER(ag), HOST_BARRIER(bar), None)
+            self._keep.append(hc)
+            over.update(world_size=world_size, rank=rank, comm_backend=2,
+                        host_comm=C.cast(C.pointer(hc), C.c_void_p).value)
+        elif world_size > 1:
             key = comm_id if isinstance(comm_id, (bytes, bytearray)) else str(comm_id).encode()
             buf = C.create_string_buffer(bytes(key).ljust(128, b"\0")[:128], 128)
             self._keep.append(buf)

@@ -68,7 +68,12 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
         m = "dim 1 needs one periodic row of patches (strip embedding)"; return AMR_E_CONFIG;
     }
     if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) { m = "bad world_size / rank"; return AMR_E_CONFIG; }
-    if (c.world_size > 1 && !c.nccl_unique_id) { m = "world_size > 1 needs nccl_unique_id"; return AMR_E_CONFIG; }
+    if (c.comm_backend < 0 || c.comm_backend > 2) { m = "comm_backend must be 0, 1 or 2"; return AMR_E_CONFIG; }
+    if (c.world_size > 1 && c.comm_backend != 2 && !c.nccl_unique_id) {
+        m = "world_size > 1 needs nccl_unique_id";
+        return AMR_E_CONFIG;
+    }
+    if (c.world_size > 1 && c.comm_backend == 2 && !c.host_comm) { m = "comm_backend 2 needs host_comm"; return AMR_E_CONFIG; }
     if (c.refine_threshold < 0 || c.coarsen_fraction < 0) { m = "bad thresholds"; return AMR_E_CONFIG; }
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
     if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }

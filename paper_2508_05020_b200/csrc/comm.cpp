@@ -331,6 +331,107 @@ struct NcclTransport : Transport {
 };
 #endif
 
+// ---- host collectives (comm_backend 2, test-only): one process per rank, possibly several on one GPU; data moves
+// through host memory with the caller's allgather, peer pools are mapped with CUDA IPC exactly as over NCCL.
+struct HostTransport : Transport {
+    const amr_host_comm* hc = nullptr;
+    int world = 1, rank = 0;
+    std::vector<void*> opened;
+    std::string gather(const void* send, size_t bytes, void* recv) {
+        return hc->allgather(send, (uint64_t)bytes, recv, hc->user) == 0 ? std::string() : "host allgather failed";
+    }
+    std::string p2p(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
+        // every rank publishes its per-peer byte counts, then all its outgoing messages back to back
+        std::vector<uint64_t> mine(world, 0), counts((size_t)world * world);
+        for (auto& x : sends) mine[x.peer] = x.bytes;
+        std::string e = gather(mine.data(), world * 8, counts.data());
+        if (!e.empty()) return e;
+        uint64_t maxtot = 0;
+        for (int q = 0; q < world; ++q) {
+            uint64_t t = 0;
+            for (int p = 0; p < world; ++p) t += counts[(size_t)q * world + p];
+            maxtot = std::max(maxtot, t);
+        }
+        std::vector<unsigned char> out(std::max<uint64_t>(maxtot, 1), 0), all((size_t)world * std::max<uint64_t>(maxtot, 1));
+        cudaStreamSynchronize(s);
+        for (auto& x : sends) {
+            uint64_t off = 0;
+            for (int p = 0; p < x.peer; ++p) off += mine[p];
+            if (x.bytes && cudaMemcpy(out.data() + off, x.buf, x.bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return "host p2p: download";
+        }
+        e = gather(out.data(), out.size(), all.data());
+        if (!e.empty()) return e;
+        for (auto& rv : recvs) {
+            if (!rv.bytes) continue;
+            const uint64_t* cq = &counts[(size_t)rv.peer * world];
+            if (cq[rank] != rv.bytes) return "host p2p: unmatched receive";
+            uint64_t off = 0;
+            for (int p = 0; p < rank; ++p) off += cq[p];
+            if (cudaMemcpy(rv.buf, all.data() + (size_t)rv.peer * out.size() + off, rv.bytes, cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+                return "host p2p: upload";
+        }
+        return std::string();
+    }
+    std::string allreduce(void* d, size_t count, int kind, cudaStream_t s) override {
+        const size_t esz = kind == 3 ? 4 : 8, bytes = count * esz;
+        std::vector<unsigned char> mine(bytes), all(bytes * world);
+        cudaStreamSynchronize(s);
+        if (cudaMemcpy(mine.data(), d, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return "host allreduce: download";
+        std::string e = gather(mine.data(), bytes, all.data());
+        if (!e.empty()) return e;
+        for (size_t k = 0; k < count; ++k)
+            for (int q = 1; q < world; ++q) {
+                unsigned char* a = all.data() + k * esz;
+                const unsigned char* b = all.data() + (size_t)q * bytes + k * esz;
+                if (kind == 0) { uint64_t x, y; std::memcpy(&x, a, 8); std::memcpy(&y, b, 8); x = std::max(x, y); std::memcpy(a, &x, 8); }
+                else if (kind == 1 || kind == 2) {
+                    double x, y; std::memcpy(&x, a, 8); std::memcpy(&y, b, 8);
+                    x = kind == 1 ? (y > x ? y : x) : x + y; std::memcpy(a, &x, 8);
+                } else { int32_t x, y; std::memcpy(&x, a, 4); std::memcpy(&y, b, 4); x = std::max(x, y); std::memcpy(a, &x, 4); }
+            }
+        return cudaMemcpy(d, all.data(), bytes, cudaMemcpyHostToDevice) == cudaSuccess ? std::string() : "host allreduce: upload";
+    }
+    std::string map_peers(void* base, size_t, std::vector<void*>& out, cudaStream_t) override {
+        using RangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+        static RangeFn range = nullptr;
+        if (!range) {
+            void* p = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                return "cuMemGetAddressRange unavailable";
+            range = reinterpret_cast<RangeFn>(p);
+        }
+        unsigned long long alloc = 0;
+        size_t asz = 0;
+        if (range(&alloc, &asz, (unsigned long long)(uintptr_t)base) != 0) return "cuMemGetAddressRange failed";
+        struct Rec { cudaIpcMemHandle_t h; uint64_t off; } me{};
+        if (cudaIpcGetMemHandle(&me.h, (void*)(uintptr_t)alloc) != cudaSuccess) return "cudaIpcGetMemHandle failed";
+        me.off = (uint64_t)((uintptr_t)base - alloc);
+        std::vector<Rec> recs(world);
+        std::string e = gather(&me, sizeof me, recs.data());
+        if (!e.empty()) return e;
+        for (int q = 0; q < world; ++q) {
+            if (q == rank) { out[q] = base; continue; }
+            void* p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, recs[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                return "cudaIpcOpenMemHandle failed";
+            opened.push_back(p);
+            out[q] = (char*)p + recs[q].off;
+        }
+        return std::string();
+    }
+    std::string fence(cudaStream_t s) override {   // every rank's queued work done, then a host barrier
+        if (cudaStreamSynchronize(s) != cudaSuccess) return "fence: stream";
+        return hc->barrier(hc->user) == 0 ? std::string() : "host barrier failed";
+    }
+    ~HostTransport() override {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+    }
+};
+
 // ---- loopback: virtual ranks = host threads of one process on one GPU (test-only)
 struct LoopGroup {
     int world = 0;
@@ -450,6 +551,18 @@ amr_status Comm::init(amr_ctx* c) {
     subcycle = c->cfg.subcycle != 0;
     owner = partition_owners(c->tree, world);
     if (world == 1) return AMR_OK;
+    if (c->cfg.comm_backend == 2) {
+        if (!c->cfg.host_comm || !c->cfg.host_comm->allgather || !c->cfg.host_comm->barrier) {
+            c->err = "comm_backend 2 needs host_comm with allgather and barrier";
+            return AMR_E_CONFIG;
+        }
+        auto* T = new HostTransport();
+        T->hc = c->cfg.host_comm;
+        T->world = world;
+        T->rank = rank;
+        tr.reset(T);
+        return AMR_OK;
+    }
     if (c->cfg.comm_backend == 1) {
         auto* T = new LoopTransport();
         T->rank = rank;
