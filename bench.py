@@ -165,9 +165,17 @@ class Ctx:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(self.local)
+        # AMR_BENCH_HOST_COMM=1 (test only): every rank on GPU 0, a gloo process group and the library's host-
+        # collective transport (comm_backend 2, CUDA IPC peer pools) -- exercises the N > 1 bench logic on one GPU;
+        # its numbers are not multi-GPU numbers
+        self.host_comm = os.environ.get("AMR_BENCH_HOST_COMM", "0") == "1"
+        self.dev = 0 if self.host_comm else self.local
+        torch.cuda.set_device(self.dev)
         if self.world > 1:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.host_comm:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
         from paper_2508_05020_b200 import build as B
         if self.rank == 0 and not os.path.exists(B.OUT):   # an existing library is used as built (flags kept)
             B.build()
@@ -183,7 +191,7 @@ class Ctx:
     def max_over_ranks(self, x):
         if self.world == 1:
             return x
-        t = self.torch.tensor([x], device="cuda", dtype=self.torch.float64)
+        t = self.torch.tensor([x], device="cpu" if self.host_comm else "cuda", dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -193,13 +201,15 @@ class Ctx:
     def sum_over_ranks(self, x):
         if self.world == 1:
             return x
-        t = self.torch.tensor([float(x)], device="cuda", dtype=self.torch.float64)
+        t = self.torch.tensor([float(x)], device="cpu" if self.host_comm else "cuda", dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return float(t.item())
 
     def mesh(self, cfg):
         kw = {}
-        if self.world > 1:
+        if self.world > 1 and self.host_comm:
+            kw = dict(world_size=self.world, rank=self.rank, comm_backend=2)
+        elif self.world > 1:
             ids = [self.amr.nccl_unique_id() if self.rank == 0 else None]
             self.dist.broadcast_object_list(ids, src=0)
             kw = dict(world_size=self.world, rank=self.rank, comm_backend=0, comm_id=ids[0])
@@ -235,7 +245,7 @@ def measure_sweep(X, args, cfg, steps, warmup, do_e2e):
     X.barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
-    with Clocks(X.local) as clk:
+    with Clocks(X.dev) as clk:
         for _ in range(steps):
             restore()
             X.barrier()

@@ -18,6 +18,7 @@ CASES = {
     "uniform_c4_n32": (W.sweep(N=256, n=32, scheme="central4", seed=3, ic="smooth"), 3, None),
     "implosion_c4_amr_n32": (W.implosion(N=256, n=32, scheme="central4", levels=2), 4, 2),
     "quadrant_weno_amr": (W.quadrant(N=64, n=16, levels=3, seed=2), 6, 3),
+    "noise_c4_n32": (dict(W.sweep(N=256, n=32, scheme="central4", Ny=512, seed=7), check_positivity=0, cfl=0.3), 2, None),
 }
 
 
@@ -67,7 +68,8 @@ def _free_port():
 
 
 @pytest.mark.parametrize("name,halo_mode", [("uniform_c4_n32", 0), ("uniform_c4_n32", 1), ("uniform_c4_n32", 2),
-                                            ("implosion_c4_amr_n32", 2), ("quadrant_weno_amr", 1)])
+                                            ("implosion_c4_amr_n32", 2), ("quadrant_weno_amr", 1),
+                                            ("noise_c4_n32", 0), ("noise_c4_n32", 2)])
 def test_two_processes_bitwise_equal_single_rank(name, halo_mode):
     import torch.multiprocessing as mp
     import paper_2508_05020_b200 as amr
