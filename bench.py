@@ -501,7 +501,8 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (SplitMix64 noise, BASELINE configs[4] distributions)",
                 "config": {"workload": name, "scheme": args.scheme, "patch": args.n, "cfl_fixed_dt": args.cfl,
-                           "parallelism": (f"Morton root partition x{X.world}, " + (["NCCL halo exchange", "peer-pull halo (CUDA IPC, NVLink)", "remote strips read by the stage kernel (CUDA IPC, NVLink)"][args.halo_mode])) if X.world > 1
+                           "parallelism": (f"Morton root partition x{X.world}, " + (["NCCL halo exchange", "peer-pull halo (CUDA IPC, NVLink)", "remote strips read by the stage kernel (CUDA IPC, NVLink)"][args.halo_mode])
+                                            + (" -- TEST transport: host collectives, all ranks on GPU 0" if X.host_comm else "")) if X.world > 1
                            else "single GPU",
                            "l2": "inputs larger than L2 (3 x 537 MB buffers per GPU); U^n restored from a pristine "
                                  "device copy between timed steps (untimed; also flushes L2)",

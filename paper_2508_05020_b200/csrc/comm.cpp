@@ -191,6 +191,18 @@ ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& ol
     return from_needs(need, world, rank);
 }
 
+// Host <-> device copies ordered on the library stream s and completed on return.  A plain cudaMemcpy runs on the
+// legacy default stream, which does not order against the (non-blocking) library stream, and an H2D copy from
+// pageable memory may still be in flight when it returns: a later kernel on s could read the old bytes.
+inline cudaError_t h2d_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(s);
+}
+inline cudaError_t d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(s);
+}
+
 // =====================================================================================  transports
 struct Xfer {
     int peer;
@@ -357,7 +369,7 @@ struct HostTransport : Transport {
         for (auto& x : sends) {
             uint64_t off = 0;
             for (int p = 0; p < x.peer; ++p) off += mine[p];
-            if (x.bytes && cudaMemcpy(out.data() + off, x.buf, x.bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+            if (x.bytes && d2h_sync(out.data() + off, x.buf, x.bytes, s) != cudaSuccess)
                 return "host p2p: download";
         }
         e = gather(out.data(), out.size(), all.data());
@@ -368,8 +380,7 @@ struct HostTransport : Transport {
             if (cq[rank] != rv.bytes) return "host p2p: unmatched receive";
             uint64_t off = 0;
             for (int p = 0; p < rank; ++p) off += cq[p];
-            if (cudaMemcpy(rv.buf, all.data() + (size_t)rv.peer * out.size() + off, rv.bytes, cudaMemcpyHostToDevice) !=
-                cudaSuccess)
+            if (h2d_sync(rv.buf, all.data() + (size_t)rv.peer * out.size() + off, rv.bytes, s) != cudaSuccess)
                 return "host p2p: upload";
         }
         return std::string();
@@ -378,7 +389,7 @@ struct HostTransport : Transport {
         const size_t esz = kind == 3 ? 4 : 8, bytes = count * esz;
         std::vector<unsigned char> mine(bytes), all(bytes * world);
         cudaStreamSynchronize(s);
-        if (cudaMemcpy(mine.data(), d, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return "host allreduce: download";
+        if (d2h_sync(mine.data(), d, bytes, s) != cudaSuccess) return "host allreduce: download";
         std::string e = gather(mine.data(), bytes, all.data());
         if (!e.empty()) return e;
         for (size_t k = 0; k < count; ++k)
@@ -391,7 +402,7 @@ struct HostTransport : Transport {
                     x = kind == 1 ? (y > x ? y : x) : x + y; std::memcpy(a, &x, 8);
                 } else { int32_t x, y; std::memcpy(&x, a, 4); std::memcpy(&y, b, 4); x = std::max(x, y); std::memcpy(a, &x, 4); }
             }
-        return cudaMemcpy(d, all.data(), bytes, cudaMemcpyHostToDevice) == cudaSuccess ? std::string() : "host allreduce: upload";
+        return h2d_sync(d, all.data(), bytes, s) == cudaSuccess ? std::string() : "host allreduce: upload";
     }
     std::string map_peers(void* base, size_t, std::vector<void*>& out, cudaStream_t) override {
         using RangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
@@ -495,7 +506,7 @@ struct LoopTransport : Transport {
         G->barrier();
         std::vector<unsigned char> acc(bytes), tmp(bytes);
         for (int q = 0; q < G->world; ++q) {
-            if (cudaMemcpy(q == 0 ? acc.data() : tmp.data(), G->bufs[q], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+            if (d2h_sync(q == 0 ? acc.data() : tmp.data(), G->bufs[q], bytes, s) != cudaSuccess)
                 return "loopback allreduce copy failed";
             if (q == 0) continue;
             for (size_t e = 0; e < count; ++e) {
@@ -512,7 +523,7 @@ struct LoopTransport : Transport {
             }
         }
         G->barrier();   // everyone has read every buffer
-        if (cudaMemcpy(d, acc.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return "loopback allreduce write failed";
+        if (h2d_sync(d, acc.data(), bytes, s) != cudaSuccess) return "loopback allreduce write failed";
         G->barrier();
         return std::string();
     }
@@ -694,7 +705,7 @@ amr_status Comm::map_pool(amr_ctx* c, void* base, size_t bytes) {
     std::string e = tr->map_peers(base, bytes, peers, c->stream);
     if (!e.empty()) { c->err = "halo_mode 1: " + e; return AMR_E_COMM; }
     if (!d_pool_bases && cudaMalloc(&d_pool_bases, world * sizeof(double*)) != cudaSuccess) return AMR_E_CUDA;
-    if (cudaMemcpy(d_pool_bases, peers.data(), world * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess)
+    if (h2d_sync(d_pool_bases, peers.data(), world * sizeof(double*), c->stream) != cudaSuccess)
         return AMR_E_CUDA;
     pool_base = base;
     peer_pool.assign(world, nullptr);
@@ -712,7 +723,7 @@ amr_status Comm::peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, doub
         std::string e = tr->map_peers(c->freg.p, c->freg.cap * sizeof(double), peers, c->stream);
         if (!e.empty()) return bad(AMR_E_COMM, e);
         if (!d_freg_bases && cudaMalloc(&d_freg_bases, world * sizeof(double*)) != cudaSuccess) return bad(AMR_E_CUDA, "alloc");
-        if (cudaMemcpy(d_freg_bases, peers.data(), world * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess)
+        if (h2d_sync(d_freg_bases, peers.data(), world * sizeof(double*), c->stream) != cudaSuccess)
             return bad(AMR_E_CUDA, "peer table");
         mapped_freg = c->freg.p;
     }
@@ -725,8 +736,9 @@ amr_status Comm::peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, doub
         if (P.n) {
             if (cudaMalloc(&P.slots, sl.size() * 4) != cudaSuccess || cudaMalloc(&P.peers, pe.size() * 4) != cudaSuccess)
                 return bad(AMR_E_CUDA, "lists");
-            cudaMemcpy(P.slots, sl.data(), sl.size() * 4, cudaMemcpyHostToDevice);
-            cudaMemcpy(P.peers, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice);
+            if (h2d_sync(P.slots, sl.data(), sl.size() * 4, c->stream) != cudaSuccess ||
+                h2d_sync(P.peers, pe.data(), pe.size() * 4, c->stream) != cudaSuccess)
+                return bad(AMR_E_CUDA, "lists upload");
         }
         P.version = lists_version;
     }
