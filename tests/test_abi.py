@@ -75,6 +75,10 @@ def _cfg(lib, **kw):
     dict(world_size=2, rank=0),
     dict(world_size=1, rank=1),
     dict(hi=(0.0, 1.0)),
+    dict(halo_mode=3),
+    dict(comm_backend=3),
+    dict(world_size=2, rank=0, comm_backend=2),                      # host collectives missing
+    dict(world_size=2, rank=0, halo_mode=2, scheme=1, nccl_unique_id=1),   # halo_mode 2 is the Central4 TMA path
 ])
 def test_invalid_config_rejected_without_device(lib, kw):
     c = _cfg(lib, **kw)
