@@ -651,7 +651,9 @@ amr_status evaluate_flags(amr_ctx* c) {
 // equal evaluate_flags' fl_ref / fl_crs (same comparisons on the same doubles); gpu test test_regrid_compact_*.
 amr_status flag_requests(amr_ctx* c, std::vector<uint8_t>& ref, std::vector<uint8_t>& crs) {
     double* Un = c->U[c->un];
-    amr_status s = fill_ghosts(c, Un);
+    amr_status s = c->comm.exchange_halos(c, Un);   // the indicator reads neighbours (remote ones on N > 1)
+    if (s != AMR_OK) return s;
+    s = fill_ghosts(c, Un);
     if (s != AMR_OK) return s;
     AuxArgs a = aux(c, Un, nullptr);
     const int nl = (int)c->leaves.size(), ns = (int)c->sib.size() / 5;
@@ -668,6 +670,9 @@ amr_status flag_requests(amr_ctx* c, std::vector<uint8_t>& ref, std::vector<uint
         CU(cudaMemcpyAsync(lst.data(), c->d_flist.p, lst.size() * 4, cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
     }
+    s = c->comm.allgather_requests(c, lst);   // N > 1: every rank's owned requests, on every rank
+    if (s != AMR_OK) return s;
+    cnt = (int32_t)(lst.size() / 2);
     ref.assign(c->tree.capacity, 0);
     crs.assign(c->tree.capacity, 0);
     for (int32_t k = 0; k < cnt; ++k) {
@@ -1323,15 +1328,8 @@ amr_status amr_regrid(amr_ctx* c, int32_t* n_refined, int32_t* n_coarsened) {
     if (s != AMR_OK) return s;
     PhaseClock clk;
     std::vector<uint8_t> ref, crs;
-    if (c->comm.world == 1) {
-        s = flag_requests(c, ref, crs);
-        if (s != AMR_OK) return s;
-    } else {   // ranks exchange full per-leaf flags (Comm::allgather_flags)
-        s = evaluate_flags(c);
-        if (s != AMR_OK) return s;
-        ref = c->fl_ref;
-        crs = c->fl_crs;
-    }
+    s = flag_requests(c, ref, crs);   // device-compacted requests; on N > 1 the ranks' lists are exchanged
+    if (s != AMR_OK) return s;
     clk.mark("flags");
     return apply_regrid(c, ref, crs, n_refined, n_coarsened);
 }

@@ -809,6 +809,56 @@ amr_status Comm::allgather_flags(amr_ctx* c, std::vector<double>& eta, std::vect
     return AMR_OK;
 }
 
+amr_status Comm::allgather_requests(amr_ctx* c, std::vector<int32_t>& lst) {
+    if (world == 1) return AMR_OK;
+    auto bad = [&](amr_status st, const std::string& m) { c->err = "request exchange: " + m; c->sticky = st; return st; };
+    const int32_t mine = (int32_t)lst.size();
+    // device scratch: [world] counts out, [world] counts in, then the lists
+    if (c->x_send.reserve((size_t)world + lst.size() / 2 + 2) != cudaSuccess) return bad(AMR_E_CUDA, "alloc");
+    int32_t* dsend = reinterpret_cast<int32_t*>(c->x_send.p);
+    std::vector<int32_t> cnt_out(world, mine), cnt_in(world, 0);
+    if (c->x_recv.reserve((size_t)world) != cudaSuccess) return bad(AMR_E_CUDA, "alloc");
+    int32_t* drecv = reinterpret_cast<int32_t*>(c->x_recv.p);
+    if (h2d_sync(dsend, cnt_out.data(), world * 4, c->stream) != cudaSuccess) return bad(AMR_E_CUDA, "upload");
+    std::vector<Xfer> sends, recvs;
+    for (int p = 0; p < world; ++p)
+        if (p != rank) { sends.push_back({p, dsend + p, 4}); recvs.push_back({p, drecv + p, 4}); }
+    std::string e = tr->p2p(sends, recvs, c->stream);
+    if (!e.empty()) return bad(AMR_E_COMM, e);
+    if (d2h_sync(cnt_in.data(), drecv, world * 4, c->stream) != cudaSuccess) return bad(AMR_E_CUDA, "download");
+    cnt_in[rank] = mine;
+    size_t total = 0;
+    for (int p = 0; p < world; ++p) {
+        if (cnt_in[p] < 0 || cnt_in[p] % 2) return bad(AMR_E_COMM, "bad count");
+        total += (size_t)cnt_in[p];
+    }
+    if (c->x_send.reserve(std::max<size_t>(1, (size_t)mine / 2 + 1)) != cudaSuccess ||
+        c->x_recv.reserve(std::max<size_t>(1, total / 2 + 1)) != cudaSuccess)
+        return bad(AMR_E_CUDA, "alloc");
+    dsend = reinterpret_cast<int32_t*>(c->x_send.p);
+    drecv = reinterpret_cast<int32_t*>(c->x_recv.p);
+    if (mine && h2d_sync(dsend, lst.data(), (size_t)mine * 4, c->stream) != cudaSuccess) return bad(AMR_E_CUDA, "upload");
+    sends.clear();
+    recvs.clear();
+    size_t off = 0;
+    std::vector<size_t> at(world, 0);
+    for (int p = 0; p < world; ++p) {
+        at[p] = off;
+        if (p != rank) {
+            sends.push_back({p, dsend, (size_t)mine * 4});
+            recvs.push_back({p, drecv + off, (size_t)cnt_in[p] * 4});
+            off += (size_t)cnt_in[p];
+        }
+    }
+    e = tr->p2p(sends, recvs, c->stream);
+    if (!e.empty()) return bad(AMR_E_COMM, e);
+    std::vector<int32_t> got(off);
+    if (off && d2h_sync(got.data(), drecv, off * 4, c->stream) != cudaSuccess) return bad(AMR_E_CUDA, "download");
+    lst.insert(lst.end(), got.begin(), got.end());
+    bytes_sent += (int64_t)mine * 4 * (world - 1);
+    return AMR_OK;
+}
+
 amr_status Comm::agree_error(amr_ctx*, int32_t*) { return AMR_OK; }
 
 }  // namespace amr

@@ -98,6 +98,8 @@ struct Comm {
     amr_status allreduce_max_i32(amr_ctx* c, int32_t* d, int n);
     amr_status allreduce_sum4(amr_ctx* c, double* h4);
     amr_status allgather_flags(amr_ctx* c, std::vector<double>& eta, std::vector<uint8_t>& amb);
+    // regrid requests: every rank's compact (slot, bits) list appended to `lst` on every rank (p2p; O(requests))
+    amr_status allgather_requests(amr_ctx* c, std::vector<int32_t>& lst);
     amr_status agree_error(amr_ctx* c, int32_t* h_err4);
 };
 
