@@ -471,7 +471,9 @@ def main():
         extra["quadrant_amr"] = measure_quadrant(X, args)
         G = X.world   # D4w: G mirrored copies of configs[3] stacked in y, one per GPU (weak scaling; G = 1: configs[3])
         extra["shock_bubble_amr"] = measure_amr(
-            X, W.shock_bubble(G=G), f"BASELINE configs[3] shock-bubble AMR{' (D4w weak scaling, %d copies)' % G if G > 1 else ''}, "
+            # slot capacity 100 k per copy (the problem keeps ~16 k active patches per copy); the default (every root
+            # refined to the finest level, 5.6 M slots at G = 8) would take ~150 GB of pool per GPU
+            X, W.shock_bubble(G=G, max_patches=100_000 * G), f"BASELINE configs[3] shock-bubble AMR{' (D4w weak scaling, %d copies)' % G if G > 1 else ''}, "
                                     f"2048x{1024 * G} base, 4 levels, 16^2 patches, WENO5-char, reflective walls, 8 CFL-0.5 "
                                     "steps with 2 regrids inside the timed region")
         if X.world == 1:   # NEXT #4: the same problem with Berger-Colella subcycling (level-0 steps)
