@@ -515,7 +515,7 @@ def main():
                 "conservation_drift_per_step": main_res["conservation_drift_per_step"],
                 "positivity": main_res["positivity"]}
         if not args.no_cpu_baseline:
-            v, k, el = oracle_rate(cfg, args.cfl, args.cpu_seconds)
+            v, k, el = oracle_rate(cfg, args.cfl, args.cpu_seconds, max_steps=100000)
             line["cpu_baseline"] = {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
                                     "sample": f"256^2 periodic piece of the same noise field, {k} SSP-RK3 steps "
                                               f"({el:.1f} s), single thread"}
