@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const int tx = tt % TILES, ty = tt / TILES;
         const uint32_t mb = smem_u32(&mbar[b]);
         const uint32_t dst = smem_u32(land + b * kLandSz);
-        mbar_expect_tx(mb, kLandSz * 8);
+        mbar_expect_tx(mb, (kLandSz - 2 * 4 * T) * 8);   // S / N strips: 3 rows (row -4 / T+3 is never read)
         if (kBulk1DTile && TILES == 1) bulk_load(dst + kLandI * 8, a.Uin + (size_t)d.slot * 4 * N * N, 4 * N * N * 8, mb);
         else tma_load3(dst + kLandI * 8, &maps.in_int, tx * T, ty * T, 4 * d.slot, mb);
         const CUtensorMap* mw = &maps.in_we;
@@ -960,9 +960,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
         tma_load3(dst + kLandE * 8, mw, i0, ty * T, z, mb);
         const CUtensorMap* ms = &maps.in_sn;
-        int j0 = ty * T - G; z = 4 * d.slot;
+        int j0 = ty * T - (G - 1); z = 4 * d.slot;
         if (ty == 0) {
-            j0 = N - G; const int s = d.side[kS];
+            j0 = N - (G - 1); const int s = d.side[kS];
             if (s >= 0) { z = 4 * s; if (d.pad & (16 << kS)) ms = &maps.peer_sn[peer(kS)]; }
             else { z = 4 * (-1 - s); ms = &maps.px_sn; }
         }
@@ -1063,15 +1063,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 c2p(uc[r][0], uc[r][1], uc[r][2], uc[r][3], (cj0 + r + G) * WP + ci + G);
             }
         }
-        if (kC4Vec2 && kC4StripPairs) {   // strips: 256 adjacent cell pairs, one per lane 0-15 of every warp
-            if (lane < 16) {
-                const int P = warp * 16 + lane, wg = P >> 6, e = P & 63;
-                int off, i, j;
-                if (wg < 2) { j = e >> 1; const int c = (e & 1) * 2; off = (wg == 0 ? kLandW : kLandE) + j * G + c; i = wg == 0 ? c - G : T + c; }
-                else { const int rr = e >> 4; i = (e & 15) * 2; off = (wg == 2 ? kLandS : kLandN) + rr * T + i; j = wg == 2 ? rr - G : T + rr; }
+        static_assert(kC4Vec2 && kC4StripPairs, "the per-tile kernel converts cells in pairs");
+        {   // strips: W/E 2 x 64 and S/N (3 rows) 2 x 48 adjacent cell pairs, one per lane 0-15 of warps 0-13
+            const int P = warp * 16 + lane;
+            if (lane < 16 && P < 224) {
+                int off, i, j, ps;
+                if (P < 128) {
+                    const int wg = P >> 6, e = P & 63;
+                    j = e >> 1; const int c = (e & 1) * 2;
+                    off = (wg == 0 ? kLandW : kLandE) + j * G + c; i = wg == 0 ? c - G : T + c; ps = G * T;
+                } else {
+                    const int h = P - 128, wg = h >= 48, e = h - 48 * wg, rr = e >> 4;
+                    i = (e & 15) * 2;
+                    off = (wg == 0 ? kLandS : kLandN) + rr * T + i; j = wg == 0 ? rr - (G - 1) : T + rr; ps = (G - 1) * T;
+                }
                 double2 cv[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) cv[q] = *reinterpret_cast<const double2*>(L + off + q * G * T);
+                for (int q = 0; q < 4; ++q) cv[q] = *reinterpret_cast<const double2*>(L + off + q * ps);
                 double pr[4][2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -1086,13 +1094,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) *reinterpret_cast<double2*>(prim + q * PL + o) = make_double2(pr[q][0], pr[q][1]);
             }
-        } else {
-            const int wg = warp >> 2, e = ((warp & 3) << 5) + lane;
-            int off, i, j;
-            if (wg < 2) { j = e >> 2; const int c = e & 3; off = (wg == 0 ? kLandW : kLandE) + e; i = wg == 0 ? c - G : T + c; }
-            else { const int rr = e >> 5; i = e & 31; off = (wg == 2 ? kLandS : kLandN) + e; j = wg == 2 ? rr - G : T + rr; }
-            const double* s = L + off;
-            c2p(s[0], s[G * T], s[2 * G * T], s[3 * G * T], (j + G) * WP + i + G);
         }
         if (tid == 32) cp_async_wait_all();      // descriptor of tile k+1 in sDesc[dsn] before (A)
         PH_MARK(2);
@@ -1313,15 +1314,15 @@ cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
     const int npx = a.proxy && a.nproxy > 0 ? a.nproxy : a.nslots;
     if (!encode_pool_map(&m.in_int, a.Uin, N, a.nslots, kTmaT, kTmaT) ||
         !encode_pool_map(&m.in_we, a.Uin, N, a.nslots, kGL, kTmaT) ||
-        !encode_pool_map(&m.in_sn, a.Uin, N, a.nslots, kTmaT, kGL) ||
+        !encode_pool_map(&m.in_sn, a.Uin, N, a.nslots, kTmaT, kGL - 1) ||
         !encode_pool_map(&m.px_we, px, N, npx, kGL, kTmaT) ||
-        !encode_pool_map(&m.px_sn, px, N, npx, kTmaT, kGL) ||
+        !encode_pool_map(&m.px_sn, px, N, npx, kTmaT, kGL - 1) ||
         !encode_pool_map(&m.un_int, a.Un, N, a.nslots, kTmaT, kTmaT) ||
         !encode_pool_map(&m.out_int, a.Uout, N, a.nslots, kTmaT, kTmaT))
         return cudaErrorInvalidValue;
     for (int q = 0; q < a.npeers && q < 8; ++q)   // halo_mode 2: every rank's U^(s-1) as mapped in this process
         if (!encode_pool_map(&m.peer_we[q], a.peer_in[q], N, a.nslots, kGL, kTmaT) ||
-            !encode_pool_map(&m.peer_sn[q], a.peer_in[q], N, a.nslots, kTmaT, kGL))
+            !encode_pool_map(&m.peer_sn[q], a.peer_in[q], N, a.nslots, kTmaT, kGL - 1))
             return cudaErrorInvalidValue;
     const int grid = ntiles < sm_count() ? ntiles : sm_count();
 #ifdef AMR_PHASE_PROF
