@@ -1,3 +1,5 @@
+"""Conservation and rank invariance of one Central4 step on a 512 x 1024 noise field: single rank vs two loopback
+virtual ranks (totals drift and bitwise owned states).  python scripts/drift_check.py (GPU box)."""
 import threading, uuid, numpy as np, torch, sys
 sys.path.insert(0, '.')
 import paper_2508_05020_b200 as amr, workloads as W
