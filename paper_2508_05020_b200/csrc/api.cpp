@@ -205,7 +205,8 @@ amr_status build_plan(amr_ctx* c) {
     for (int id : c->canon)
         if (t.is_leaf(id) && c->comm.owns(c, id)) c->leaf_ids.push_back(id);
     {   // packed (level, Morton key) computed once per leaf, then one radix sort of (key, id) pairs
-        std::vector<std::pair<uint64_t, int32_t>> kv;
+        static thread_local std::vector<std::pair<uint64_t, int32_t>> kv;   // scratch kept across plans
+        kv.clear();
         kv.reserve(c->leaf_ids.size());
         for (int id : c->leaf_ids)   // level in the top 6 bits; Morton of 29-bit coordinates below
             kv.push_back({(uint64_t(t.lev[id]) << 58) | morton(t.pi[id], t.pj[id]), id});
@@ -673,13 +674,19 @@ amr_status flag_requests(amr_ctx* c, std::vector<uint8_t>& ref, std::vector<uint
     s = c->comm.allgather_requests(c, lst);   // N > 1: every rank's owned requests, on every rank
     if (s != AMR_OK) return s;
     cnt = (int32_t)(lst.size() / 2);
-    ref.assign(c->tree.capacity, 0);
-    crs.assign(c->tree.capacity, 0);
+    if ((int)ref.size() != c->tree.capacity) {
+        ref.assign(c->tree.capacity, 0);
+        crs.assign(c->tree.capacity, 0);
+        c->rq_set.clear();
+    }
+    for (int id : c->rq_set) ref[id] = crs[id] = 0;   // the previous regrid's requests
+    c->rq_set.clear();
     for (int32_t k = 0; k < cnt; ++k) {
         const int id = lst[2 * k], b = lst[2 * k + 1];
         if (id < 0 || id >= c->tree.capacity) return fail(c, AMR_E_CUDA, "flags compact: bad slot");
         if (b & 1) ref[id] = 1;
         if (b & 2) crs[id] = 1;
+        c->rq_set.push_back(id);
     }
     return AMR_OK;
 }
@@ -712,8 +719,11 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     clk.mark("validate");
     int n_new = 0, n_del = 0;
     const int W = c->comm.world, R = c->comm.rank;
-    std::vector<uint8_t> is_new(nt.capacity, 0);
-    std::vector<int32_t> new_ids;
+    std::vector<uint8_t>& is_new = c->rq_new;   // kept across regrids; the previous regrid's entries reset
+    if ((int)is_new.size() != nt.capacity) { is_new.assign(nt.capacity, 0); c->rq_new_ids.clear(); }
+    for (int id : c->rq_new_ids) is_new[id] = 0;
+    std::vector<int32_t>& new_ids = c->rq_new_ids;
+    new_ids.clear();
     for (const auto& sn : nt.journal()) {   // created / deleted slots, from the transaction journal
         if (nt.alive[sn.id] && !sn.alive) { is_new[sn.id] = 1; new_ids.push_back(sn.id); ++n_new; }
         if (!nt.alive[sn.id] && sn.alive) ++n_del;
@@ -1327,7 +1337,8 @@ amr_status amr_regrid(amr_ctx* c, int32_t* n_refined, int32_t* n_coarsened) {
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     PhaseClock clk;
-    std::vector<uint8_t> ref, crs;
+    std::vector<uint8_t>& ref = c->rq_ref;
+    std::vector<uint8_t>& crs = c->rq_crs;
     s = flag_requests(c, ref, crs);   // device-compacted requests; on N > 1 the ranks' lists are exchanged
     if (s != AMR_OK) return s;
     clk.mark("flags");

@@ -116,6 +116,9 @@ struct amr_ctx {
     std::vector<double> fl_eta;
     std::vector<double> fl_eta_raw;    // per-leaf indicator gathered from the device (scratch)
     std::vector<uint8_t> fl_amb_raw;
+    // regrid scratch kept across regrids (capacity-sized, reset entry by entry: no per-regrid allocation / fill)
+    std::vector<uint8_t> rq_ref, rq_crs, rq_new;
+    std::vector<int32_t> rq_set, rq_new_ids;
 
     // stats / timing
     amr_stats st{};

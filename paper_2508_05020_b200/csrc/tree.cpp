@@ -221,7 +221,8 @@ bool PatchTree::validate(std::string& err) const {
 }
 
 std::vector<int32_t> PatchTree::canonical() const {
-    std::vector<std::pair<uint64_t, int32_t>> kv;   // key (level, j, i) = the map key: one sort of pairs
+    static thread_local std::vector<std::pair<uint64_t, int32_t>> kv;   // key (level, j, i) = the map key
+    kv.clear();
     kv.reserve(n_alive);
     index_.for_each([&](uint64_t k, int32_t id) { kv.push_back({k, id}); });
     radix_sort_pairs(kv);

@@ -91,8 +91,11 @@ class FlatIndex {
 inline void radix_sort_pairs(std::vector<std::pair<uint64_t, int32_t>>& v) {
     const int bits = v.size() < 65536 ? 8 : 16;
     const uint64_t mask = (1ull << bits) - 1;
-    std::vector<std::pair<uint64_t, int32_t>> tmp(v.size());
-    std::vector<uint32_t> cnt(size_t(1) << bits);
+    // scratch kept across calls (per thread): a fresh 100 KB+ buffer is an mmap plus page faults on every regrid
+    static thread_local std::vector<std::pair<uint64_t, int32_t>> tmp;
+    static thread_local std::vector<uint32_t> cnt;
+    tmp.resize(v.size());
+    cnt.assign(size_t(1) << bits, 0u);
     uint64_t diff = 0;   // bits in which some key differs from the first: only those digits need a pass
     for (const auto& e : v) diff |= e.first ^ v[0].first;
     for (int shift = 0; shift < 64; shift += bits) {
