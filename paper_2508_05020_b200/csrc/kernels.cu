@@ -1565,9 +1565,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
     };
     auto fetch_desc = [&](int t, int slotbuf) {   // warp 1: member descriptors of tile t -> sDesc[slotbuf]
+        // the compiler predicates this copy in every warp; lanes that copy nothing keep one common address (ncu
+        // counted ~32 shared wavefronts per predicated-off warp instruction with lane-varying addresses; no time)
+        const int m = lane < K ? lane : 0;
+        const uint32_t dst = smem_u32(&sDesc[slotbuf * K + m]);
+        const LeafDesc* src = a.leaves + (size_t)t * K + m;
         if (lane < K) {
-            const uint32_t dst = smem_u32(&sDesc[slotbuf * K + lane]);
-            const LeafDesc* src = a.leaves + (size_t)t * K + lane;
             cp_async16(dst, src);
             cp_async16(dst + 16, reinterpret_cast<const char*>(src) + 16);
         }
