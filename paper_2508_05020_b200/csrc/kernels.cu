@@ -2249,49 +2249,59 @@ __global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntas
 __global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
     const int n = a.geo.n;
     const size_t nn = (size_t)n * n;
-    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (long long)ntasks * 4 * n) return;
-    const int task = (int)(t / (4 * n)), e = (int)(t - (long long)task * 4 * n);
-    const RefluxTask rt = tasks[task];
-    int i, j;
-    if (e < n) { i = 0; j = e; }
-    else if (e < 2 * n) { i = n - 1; j = e - n; }
-    else if (e < 3 * n) { i = e - 2 * n; j = 0; if (i == 0 || i == n - 1) return; }
-    else { i = e - 3 * n; j = n - 1; if (i == 0 || i == n - 1) return; }
-    int touch = (i == 0 ? 1 : 0) | (i == n - 1 ? 2 : 0) | (j == 0 ? 4 : 0) | (j == n - 1 ? 8 : 0);
-    int act = touch & rt.mask;
-    if (!act) return;
-    const double coef = a.b * (*a.dt);
-    double* U = a.Uw + (size_t)rt.slot * 4 * nn + (size_t)j * n + i;
-    double u[4];
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // every lane stays to the end: Lambda is warp-reduced before one atomic per warp
+    unsigned long long lam = 0ull;
+    int task = 0, i = 0, j = 0, act = 0;
+    if (t < (long long)ntasks * 4 * n) {
+        task = (int)(t / (4 * n));
+        const int e = (int)(t - (long long)task * 4 * n);
+        bool ok = true;
+        if (e < n) { i = 0; j = e; }
+        else if (e < 2 * n) { i = n - 1; j = e - n; }
+        else if (e < 3 * n) { i = e - 2 * n; j = 0; ok = i != 0 && i != n - 1; }
+        else { i = e - 3 * n; j = n - 1; ok = i != 0 && i != n - 1; }
+        const int touch = (i == 0 ? 1 : 0) | (i == n - 1 ? 2 : 0) | (j == 0 ? 4 : 0) | (j == n - 1 ? 8 : 0);
+        act = ok ? touch & tasks[task].mask : 0;
+    }
+    if (act) {
+        const RefluxTask rt = tasks[task];
+        const double coef = a.b * (*a.dt);
+        double* U = a.Uw + (size_t)rt.slot * 4 * nn + (size_t)j * n + i;
+        double u[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) u[k] = U[k * nn];
-    const int l = rt.level;
-    // fixed order: x-low, x-high, y-low, y-high (bitwise rank invariance, O12)
+        for (int k = 0; k < 4; ++k) u[k] = U[k * nn];
+        const int l = rt.level;
+        // fixed order: x-low, x-high, y-low, y-high (bitwise rank invariance, O12)
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        if (!(act & (1 << s))) continue;
-        const int along = s < 2 ? j : i;
-        const int opp = s ^ 1;
-        const double ih = s < 2 ? a.geo.inv_dx[l] : a.geo.inv_dy[l];
-        const double sigma = (s & 1) ? 1.0 : -1.0;
-        const int f0 = 2 * along, fl = f0 / n, fp = f0 - fl * n;
-        const int fleaf = rt.fine[s][fl];
+        for (int s = 0; s < 4; ++s) {
+            if (!(act & (1 << s))) continue;
+            const int along = s < 2 ? j : i;
+            const int opp = s ^ 1;
+            const double ih = s < 2 ? a.geo.inv_dx[l] : a.geo.inv_dy[l];
+            const double sigma = (s & 1) ? 1.0 : -1.0;
+            const int f0 = 2 * along, fl = f0 / n, fp = f0 - fl * n;
+            const int fleaf = rt.fine[s][fl];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            double Fc = a.freg[(((size_t)rt.slot * 4 + s) * 4 + k) * n + along];
-            const double* ff = a.freg + (((size_t)fleaf * 4 + opp) * 4 + k) * n + fp;
-            double delta = Fc - 0.5 * (ff[0] + ff[1]);
-            u[k] += coef * sigma * delta * ih;
+            for (int k = 0; k < 4; ++k) {
+                double Fc = a.freg[(((size_t)rt.slot * 4 + s) * 4 + k) * n + along];
+                const double* ff = a.freg + (((size_t)fleaf * 4 + opp) * 4 + k) * n + fp;
+                double delta = Fc - 0.5 * (ff[0] + ff[1]);
+                u[k] += coef * sigma * delta * ih;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) U[k * nn] = u[k];
+        if (a.check && !physical_state(u[0], u[1], u[2], u[3], a.gamma)) report_error(a.err, rt.slot, a.stage, j * n + i);
+        if (a.want_lambda) {
+            double sp = wave_speed(u[0], u[1], u[2], u[3], a.gamma, a.geo.inv_dx[l], a.geo.inv_dy[l]);
+            if (a.lam0) sp = ldexp(sp, -l);
+            lam = (unsigned long long)__double_as_longlong(sp);
         }
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) U[k * nn] = u[k];
-    if (a.check && !physical_state(u[0], u[1], u[2], u[3], a.gamma)) report_error(a.err, rt.slot, a.stage, j * n + i);
     if (a.want_lambda) {
-        double sp = wave_speed(u[0], u[1], u[2], u[3], a.gamma, a.geo.inv_dx[l], a.geo.inv_dy[l]);
-        if (a.lam0) sp = ldexp(sp, -l);
-        atomicMax(a.lambda_bits, (unsigned long long)__double_as_longlong(sp));
+        lam = warp_max_u64(lam);
+        if ((threadIdx.x & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
     }
 }
 
