@@ -191,7 +191,7 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
     double pR = gm1 * (UR[3] - 0.5 * (UR[1] * unR + UR[2] * utR));
     double sL = fast_sqrt(g * pL * irL) + fabs(unL);
     double sR = fast_sqrt(g * pR * irR) + fabs(unR);
-    double S = fmax(sR, sL);
+    double S = sR > sL ? sR : sL;   // as the oracle (O10): a NaN wave speed propagates instead of being dropped
     F[0] = 0.5 * (UR[1] + UL[1]) - 0.5 * S * (UR[0] - UL[0]);
     F[1] = 0.5 * ((UR[1] * unR + pR) + (UL[1] * unL + pL)) - 0.5 * S * (UR[1] - UL[1]);
     F[2] = 0.5 * (UR[2] * unR + UL[2] * unL) - 0.5 * S * (UR[2] - UL[2]);
@@ -2076,7 +2076,9 @@ __device__ __forceinline__ double coarse_value(const double* U, const int32_t* c
 
 __device__ __forceinline__ double mc_limiter(double a, double b) {
     if (a * b <= 0.0) return 0.0;
-    double m = fmin(fmin(2.0 * fabs(a), 2.0 * fabs(b)), fabs(a + b) * 0.5);
+    double m = fabs(a + b) * 0.5;   // min of the three by comparisons (fmin would drop a NaN; same values otherwise)
+    if (2.0 * fabs(a) < m) m = 2.0 * fabs(a);
+    if (2.0 * fabs(b) < m) m = 2.0 * fabs(b);
     return a > 0.0 ? m : -m;
 }
 

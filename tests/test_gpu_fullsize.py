@@ -3,9 +3,9 @@ configuration bench.py times (persistent TMA Central4 kernel for 32^2 / 64^2 pat
 checked against the oracle to 1e-11 (O18 / A31 metric, tests/parity.py).
 
 - configs[4] sweep, 4096^2 noise field (bench's headline workload): one SSP-RK3 step with bench's fixed dt
-  (CFL 0.3 of Lambda(U^0)), sampled patches compared with the oracle run on the patch's 3 x 3 neighbourhood cut
-  from the same field as a periodic 3n x 3n block.  The block's wrap contaminates a band growing 4 cells per stage
-  from its edge (12 cells after one step), so the centre patch is exact.  Corner patches cover the domain wrap.
+  (CFL 0.3 of Lambda(U^0)), sampled patches compared with the oracle run on the patch's neighbourhood cut from
+  the same field as a periodic block wide enough that the wrap's contamination (the scheme's reach per stage,
+  3 stages) cannot reach the centre patch.  Corner patches cover the domain wrap.
 - configs[1] vortex, 1024^2 Central4: the whole oracle mesh, 10 CFL-0.5 steps.  WENO5-char: sampled blocks.
 - configs[2] quadrant, 512^2 base, 3 levels, WENO5-char: lockstep with regrids (A32), 6 steps.
 - configs[3] shock-bubble, 2048 x 1024 base, 4 levels, reflective walls: init protocol (A28) + 2 steps lockstep.
@@ -23,21 +23,26 @@ pytestmark = pytest.mark.gpu
 
 def block_oracle(cfg, P, Q, dt, steps=1):
     """Oracle result for patch (P, Q) of a 1-level periodic cfg after `steps` fixed-dt steps, computed on its
-    periodic 3 x 3 patch neighbourhood."""
+    periodic (2r+1) x (2r+1) patch neighbourhood: the block's wrap contaminates a band growing by the scheme's
+    reach per stage (3 cells Central4, 4 cells WENO5 with Eq. 9) from its edge, so r patches of margin must cover
+    3 x reach x steps cells."""
     n = cfg["n"]
+    reach = 3 * steps * (4 if cfg["scheme"] == "weno5" else 3)
+    r = max(1, -(-reach // n))
+    b = 2 * r + 1
     NPx, NPy = cfg["base"][0] // n, cfg["base"][1] // n
     dx = (cfg["hi"][0] - cfg["lo"][0]) / cfg["base"][0]
     dy = (cfg["hi"][1] - cfg["lo"][1]) / cfg["base"][1]
-    sub = dict(cfg, base=(3 * n, 3 * n), lo=(0.0, 0.0), hi=(3 * n * dx, 3 * n * dy), levels=1,
+    sub = dict(cfg, base=(b * n, b * n), lo=(0.0, 0.0), hi=(b * n * dx, b * n * dy), levels=1,
                bc=("periodic",) * 4)
     o = orc.Oracle(sub)
-    o.set_state(lambda l, p, q: W.patch_state(cfg, 0, (P - 1 + p) % NPx, (Q - 1 + q) % NPy))
+    o.set_state(lambda l, p, q: W.patch_state(cfg, 0, (P - r + p) % NPx, (Q - r + q) % NPy))
     for _ in range(steps):
         o.step(dt=dt)
-    return o.get_patch((0, 1, 1))
+    return o.get_patch((0, r, r))
 
 
-def sampled_parity(cfg, samples, steps=1, cfl=0.3):
+def sampled_parity(cfg, samples, steps=1, cfl=0.3, nan_ok=False):
     n = cfg["n"]
     NPx = cfg["base"][0] // n
     g = amr.Mesh(cfg)
@@ -51,6 +56,11 @@ def sampled_parity(cfg, samples, steps=1, cfl=0.3):
     Ug = g.get_state(as_dict=False, indices=idx)
     so = {k: block_oracle(cfg, k[1], k[2], dt, steps) for k in keys}
     sg = {k: Ug[e] for e, k in enumerate(keys)}
+    if nan_ok:   # non-physical states (NaN) must sit in the same cells on both sides; the rest is compared
+        for k in keys:
+            assert np.array_equal(np.isnan(so[k]), np.isnan(sg[k])), k
+            so[k] = np.nan_to_num(so[k], nan=0.0)
+            sg[k] = np.nan_to_num(sg[k], nan=0.0)
     e, rel = parity_error(so, sg)
     assert e <= 1e-11, (e, rel)
     return e
@@ -64,12 +74,23 @@ def _samples(NPx, NPy, k=6, seed=0):
     return sorted(s)
 
 
-@pytest.mark.parametrize("n", [32, 64])
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
 def test_sweep_4096_central4_sampled(n):
-    """configs[4] at 4096^2 with bench's kernel (stage_c4_tma_kernel), check off as in bench."""
+    """configs[4] at 4096^2 with bench's kernels (group kernel n = 8, 16; TMA kernel n = 32, 64), check off as in
+    bench."""
     cfg = W.sweep(N=4096, n=n, scheme="central4", seed=7)
     cfg["check_positivity"] = 0
     sampled_parity(cfg, _samples(4096 // n, 4096 // n))
+
+
+@pytest.mark.parametrize("n,char", [(8, 1), (16, 1), (8, 0)])
+def test_sweep_4096_weno_sampled(n, char):
+    """configs[4] WENO5 rows of the sweep table at 4096^2 (n = 8: the 4 x 4 block-tile WENO kernel).  White noise
+    makes a few characteristic reconstructions non-physical (NaN through the eigen-system's sound speed): the NaN
+    cells must coincide with the oracle's."""
+    cfg = W.sweep(N=4096, n=n, scheme="weno5", seed=7)
+    cfg.update(check_positivity=0, characteristic=char)
+    sampled_parity(cfg, _samples(4096 // n, 4096 // n, k=4, seed=2), nan_ok=True)
 
 
 def test_sweep_4096_extreme_patch_matches_oracle():
