@@ -213,9 +213,12 @@ amr_status amr_sync(amr_ctx* ctx);
  * (|eta - threshold| <= 1e-9 relative).  cap >= number of active patches. */
 amr_status amr_get_flags(amr_ctx* ctx, int32_t cap, double* maxeta, uint8_t* bits);
 
-/* Regrid: flags, refinement pass (Alg. 1 with recursion), coarsening pass
- * (Alg. 2 / prose rule, finest level first), R1/R2 validation, prolongation of
- * new patches, restriction.  AMR_E_CAPACITY leaves the mesh unchanged. */
+/* Regrid: flags (evaluated and compacted on the device into a (slot, refine|coarsen) request list; on N > 1
+ * ranks the lists are exchanged, so the host handles O(requests), not O(patches)), refinement pass (Alg. 1 with
+ * recursion), coarsening pass (Alg. 2 / prose rule, finest level first), R1/R2 validation, prolongation of new
+ * patches, restriction, repartition and migration on N > 1.  The requests equal amr_get_flags' bits 1 and 2.
+ * *n_refined / *n_coarsened (may be NULL) receive the numbers of patches created / deleted.
+ * AMR_E_CAPACITY leaves the mesh unchanged. */
 amr_status amr_regrid(amr_ctx* ctx, int32_t* n_refined, int32_t* n_coarsened);
 
 /* Regrid with externally given requests (bits as in amr_get_flags, indexed by
