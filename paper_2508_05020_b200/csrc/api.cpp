@@ -208,8 +208,9 @@ amr_status build_plan(amr_ctx* c) {
         static thread_local std::vector<std::pair<uint64_t, int32_t>> kv;   // scratch kept across plans
         kv.clear();
         kv.reserve(c->leaf_ids.size());
-        for (int id : c->leaf_ids)   // level in the top 6 bits; Morton of 29-bit coordinates below
-            kv.push_back({(uint64_t(t.lev[id]) << 58) | morton(t.pi[id], t.pj[id]), id});
+        const int ms = t.morton_shift();   // level above the Morton key of the finest-level coordinate bits
+        for (int id : c->leaf_ids)
+            kv.push_back({(uint64_t(t.lev[id]) << ms) | morton(t.pi[id], t.pj[id]), id});
         radix_sort_pairs(kv);
         for (size_t e = 0; e < kv.size(); ++e) c->leaf_ids[e] = kv[e].second;
     }
@@ -230,6 +231,7 @@ amr_status build_plan(amr_ctx* c) {
     c->leaves.clear();
     c->ptasks.clear();
     c->rtasks.clear();
+    int cpar = -1, cnb[9];   // the last C/F parent's 3 x 3 neighbourhood
     for (int id : c->leaf_ids) {
         LeafDesc d{};
         d.slot = id;
@@ -277,12 +279,16 @@ amr_status build_plan(amr_ctx* c) {
                     d.cf |= 1 << (4 + s);
                     int par = t.parent[id];
                     if (par < 0) return fail(c, AMR_E_MESH, "missing same-level neighbour of a root");
-                    for (int dy = -1; dy <= 1; ++dy)
-                        for (int dx = -1; dx <= 1; ++dx) {
-                            int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
-                            if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
-                            p.coarse[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
-                        }
+                    if (par != cpar) {   // siblings are consecutive in Morton order: one 3 x 3 lookup per parent
+                        cpar = par;
+                        for (int dy = -1; dy <= 1; ++dy)
+                            for (int dx = -1; dx <= 1; ++dx) {
+                                int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
+                                if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
+                                cnb[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
+                            }
+                    }
+                    for (int q = 0; q < 9; ++q) p.coarse[q] = cnb[q];
                 }
                 d.side[s] = -1 - p.proxy;
                 c->ptasks.push_back(p);
@@ -692,13 +698,21 @@ amr_status flag_requests(amr_ctx* c, std::vector<uint8_t>& ref, std::vector<uint
 }
 
 // refinement pass, coarsening pass, validation, new-patch prolongation, restriction
-amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::vector<uint8_t>& crs, int32_t* nr,
-                        int32_t* nc) {
+amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::vector<uint8_t>& crs,
+                        const std::vector<int32_t>& req, int32_t* nr, int32_t* nc) {
     PhaseClock clk;
     PatchTree& nt = c->tree;   // modified in place inside a transaction (rolled back on any failure)
+    // the requested patches in canonical order: the passes below visit exactly the patches a walk over the whole
+    // canonical list would act on, in the same order, in O(requests log requests)
+    std::vector<std::pair<uint64_t, int32_t>>& order = c->rq_order;
+    order.clear();
+    for (int id : req) order.push_back({(uint64_t)c->canon_pos[id], id});
+    radix_sort_pairs(order);
+    order.erase(std::unique(order.begin(), order.end()), order.end());
     nt.begin_txn();
     std::string m;
-    for (int id : c->canon) {
+    for (const auto& o : order) {
+        const int id = o.second;
         if (!ref[id] || !nt.is_leaf(id) || nt.lev[id] >= c->cfg.num_levels - 1) continue;
         if (!nt.refine(id, m)) {
             nt.rollback();
@@ -707,12 +721,13 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
         }
     }
     for (int l = c->cfg.num_levels - 2; l >= 0; --l)
-        for (int id : c->canon) {
+        for (const auto& o : order) {
+            const int id = o.second;
             if (nt.lev[id] != l || !crs[id] || !nt.alive[id]) continue;
             if (nt.coarsen_allowed(id)) nt.delete_children(id);
         }
     clk.mark("refine + coarsen");
-    if (!nt.validate(m)) {
+    if (!nt.validate_txn(m)) {   // O(changes); amr_plan_regrid checks it against the full validate()
         nt.rollback();
         return fail(c, AMR_E_MESH, "regrid produced an invalid mesh: " + m);
     }
@@ -1342,7 +1357,7 @@ amr_status amr_regrid(amr_ctx* c, int32_t* n_refined, int32_t* n_coarsened) {
     s = flag_requests(c, ref, crs);   // device-compacted requests; on N > 1 the ranks' lists are exchanged
     if (s != AMR_OK) return s;
     clk.mark("flags");
-    return apply_regrid(c, ref, crs, n_refined, n_coarsened);
+    return apply_regrid(c, ref, crs, c->rq_set, n_refined, n_coarsened);
 }
 
 amr_status amr_regrid_with_flags(amr_ctx* c, int32_t n, const int32_t* tree_index, const uint8_t* bits,
@@ -1351,14 +1366,16 @@ amr_status amr_regrid_with_flags(amr_ctx* c, int32_t n, const int32_t* tree_inde
     if (s != AMR_OK) return s;
     if (n < 0 || (n > 0 && (!tree_index || !bits))) return fail(c, AMR_E_ARG, "regrid_with_flags: bad arguments");
     std::vector<uint8_t> ref(c->tree.capacity, 0), crs(c->tree.capacity, 0);
+    std::vector<int32_t> req(n);
     for (int k = 0; k < n; ++k) {
         int ti = tree_index[k];
         if (ti < 0 || ti >= (int)c->canon.size()) return fail(c, AMR_E_ARG, "regrid_with_flags: tree_index");
         ref[c->canon[ti]] = bits[k] & 1;
         crs[c->canon[ti]] = (bits[k] >> 1) & 1;
+        req[k] = c->canon[ti];
     }
     CU(cudaStreamSynchronize(c->stream));
-    return apply_regrid(c, ref, crs, n_refined, n_coarsened);
+    return apply_regrid(c, ref, crs, req, n_refined, n_coarsened);
 }
 
 amr_status amr_get_patch_tree(amr_ctx* c, amr_patch_desc* out, int32_t cap, int32_t* count) {

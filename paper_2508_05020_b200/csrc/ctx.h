@@ -119,6 +119,7 @@ struct amr_ctx {
     // regrid scratch kept across regrids (capacity-sized, reset entry by entry: no per-regrid allocation / fill)
     std::vector<uint8_t> rq_ref, rq_crs, rq_new;
     std::vector<int32_t> rq_set, rq_new_ids;
+    std::vector<std::pair<uint64_t, int32_t>> rq_order;   // requested slots by canonical position (apply_regrid)
 
     // stats / timing
     amr_stats st{};

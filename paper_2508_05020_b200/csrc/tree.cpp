@@ -26,8 +26,13 @@ void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, 
     np0[0] = npx; np0[1] = npy; levels = nlev;
     periodic[0] = perx; periodic[1] = pery;
     capacity = cap; coarsen_rule = rule;
+    for (int ax = 0; ax < 2; ++ax) {
+        kb[ax] = 0;
+        while ((int64_t(1) << kb[ax]) < (int64_t(ax ? npy : npx) << (nlev - 1))) ++kb[ax];
+    }
     lev.assign(cap, -1); pi.assign(cap, 0); pj.assign(cap, 0); parent.assign(cap, -1);
     child.assign(4 * (size_t)cap, -1); alive.assign(cap, 0);
+    node_.assign(cap, Node{-1, 0, 0, -1, {-1, -1, -1, -1}});
     n_alive = 0;
     index_.clear();
     index_.reserve((size_t)npx * npy * 2);
@@ -55,6 +60,7 @@ void PatchTree::touch(int id) {
 
 void PatchTree::begin_txn() {
     journal_.clear();
+    released_parent_ = false;
     if ((int)touched_.size() != capacity) touched_.assign(capacity, 0);
     txn_ = true;
 }
@@ -71,6 +77,7 @@ void PatchTree::rollback() {
         const SlotSnap& sn = *it;
         lev[sn.id] = sn.lev; pi[sn.id] = sn.pi; pj[sn.id] = sn.pj; parent[sn.id] = sn.parent; alive[sn.id] = sn.alive;
         for (int c = 0; c < 4; ++c) child[4 * sn.id + c] = sn.child[c];
+        sync(sn.id);
     }
     for (const auto& sn : journal_)
         if (sn.alive) { index_.set(key(sn.lev, sn.pi, sn.pj), sn.id); ++n_alive; }
@@ -90,6 +97,7 @@ int PatchTree::alloc(int l, int i, int j) {
     touch(id);
     lev[id] = l; pi[id] = i; pj[id] = j; parent[id] = -1; alive[id] = 1;
     for (int c = 0; c < 4; ++c) child[4 * id + c] = -1;
+    sync(id);
     index_.set(key(l, i, j), id);
     ++n_alive;
     return id;
@@ -97,9 +105,11 @@ int PatchTree::alloc(int l, int i, int j) {
 
 void PatchTree::release(int id) {
     touch(id);
+    if (child[4 * id] >= 0) released_parent_ = true;
     index_.erase(key(lev[id], pi[id], pj[id]));
     alive[id] = 0; lev[id] = -1; parent[id] = -1;
     for (int c = 0; c < 4; ++c) child[4 * id + c] = -1;
+    sync(id);
     free_.push_back(id);
     std::push_heap(free_.begin(), free_.end(), std::greater<int32_t>());
     --n_alive;
@@ -118,19 +128,20 @@ int PatchTree::find(int l, int i, int j) const {
 }
 
 int PatchTree::neighbour(int id, int dx, int dy) const {
-    const int l = lev[id];
-    if (l == 0) {
-        int i = pi[id] + dx, j = pj[id] + dy;
+    const Node& n = node_[id];
+    if (n.lev == 0) {
+        int i = n.pi + dx, j = n.pj + dy;
         if (!wrap(0, i, j)) return -2;
         return root_[(size_t)j * np0[0] + i];
     }
-    int a = (pi[id] & 1) + dx, b = (pj[id] & 1) + dy;   // position relative to the parent's children, -1 .. 2
-    if (a >= 0 && a <= 1 && b >= 0 && b <= 1) return child[4 * parent[id] + a + 2 * b];   // a sibling
+    int a = (n.pi & 1) + dx, b = (n.pj & 1) + dy;   // position relative to the parent's children, -1 .. 2
+    if (a >= 0 && a <= 1 && b >= 0 && b <= 1) return node_[n.parent].child[a + 2 * b];   // a sibling
     const int DX = a < 0 ? -1 : (a > 1 ? 1 : 0), DY = b < 0 ? -1 : (b > 1 ? 1 : 0);
-    const int pn = neighbour(parent[id], DX, DY);      // same-level neighbour of the parent (recursion by level)
+    const int pn = neighbour(n.parent, DX, DY);         // same-level neighbour of the parent (recursion by level)
     if (pn < 0) return pn;                              // outside the domain, or missing
-    if (!has_children(pn)) return -1;
-    return child[4 * pn + (a - 2 * DX) + 2 * (b - 2 * DY)];
+    const Node& p = node_[pn];
+    if (p.child[0] < 0) return -1;
+    return p.child[(a - 2 * DX) + 2 * (b - 2 * DY)];
 }
 
 // Alg. 1 RefinePatch: before creating p's children make every
@@ -156,7 +167,9 @@ bool PatchTree::refine(int id, std::string& err) {
         int k = alloc(l + 1, 2 * pi[id] + a, 2 * pj[id] + b);
         parent[k] = id;
         child[4 * id + c] = k;
+        sync(k);
     }
+    sync(id);
     return true;
 }
 
@@ -192,6 +205,7 @@ void PatchTree::delete_children(int id) {
         if (k >= 0) release(k);
         child[4 * id + c] = -1;
     }
+    sync(id);
 }
 
 bool PatchTree::validate(std::string& err) const {
@@ -200,10 +214,10 @@ bool PatchTree::validate(std::string& err) const {
             const int r = root_[(size_t)j * np0[0] + i];
             if (r < 0 || !alive[r] || lev[r] != 0 || pi[r] != i || pj[r] != j) { err = "R1 violated: root missing"; return false; }
         }
-    std::vector<int32_t> ids;   // the active patches (O(active), not O(capacity))
-    ids.reserve(index_.size());
-    index_.for_each([&](uint64_t, int32_t id) { ids.push_back(id); });
-    for (int id : ids) {
+    static thread_local std::vector<std::pair<uint64_t, int32_t>> kv;   // the active patches (O(active))
+    index_.dump(kv);
+    for (const auto& e : kv) {
+        const int id = e.second;
         if (!alive[id]) { err = "index refers to a free slot"; return false; }
         if (lev[id] > 0) {
             int p = parent[id];
@@ -220,11 +234,40 @@ bool PatchTree::validate(std::string& err) const {
     return true;
 }
 
+bool PatchTree::validate_txn(std::string& err) const {
+    if (released_parent_) { err = "orphan patch"; return false; }
+    auto r2 = [&](int id) {
+        for (int d = 0; d < 8; ++d)
+            if (neighbour(id, kMoore[d][0], kMoore[d][1]) == -1) return false;
+        return true;
+    };
+    for (const SlotSnap& sn : journal_) {
+        const int id = sn.id;
+        if (sn.alive && sn.lev == 0 && !(alive[id] && lev[id] == 0 && pi[id] == sn.pi && pj[id] == sn.pj)) {
+            err = "R1 violated: root missing";
+            return false;
+        }
+        if (alive[id]) {   // a created or modified patch: the per-patch checks of validate()
+            if (lev[id] > 0 && (parent[id] < 0 || !alive[parent[id]])) { err = "orphan patch"; return false; }
+            int nc = 0;
+            for (int c = 0; c < 4; ++c) nc += child[4 * id + c] >= 0;
+            if (nc != 0 && nc != 4) { err = "children not all-or-none"; return false; }
+            if (nc == 4 && !r2(id)) { err = "R2 violated"; return false; }
+        }
+        if (sn.alive && find(sn.lev, sn.pi, sn.pj) < 0) {   // a removed position: its refined Moore neighbours
+            for (int d = 0; d < 8; ++d) {
+                const int q = find(sn.lev, sn.pi + kMoore[d][0], sn.pj + kMoore[d][1]);
+                if (q >= 0 && has_children(q)) { err = "R2 violated"; return false; }
+            }
+        }
+    }
+    return true;
+}
+
 std::vector<int32_t> PatchTree::canonical() const {
     static thread_local std::vector<std::pair<uint64_t, int32_t>> kv;   // key (level, j, i) = the map key
-    kv.clear();
-    kv.reserve(n_alive);
-    index_.for_each([&](uint64_t k, int32_t id) { kv.push_back({k, id}); });
+    index_.dump(kv);
+    for (auto& e : kv) e.first = canon_key(e.first);
     radix_sort_pairs(kv);
     std::vector<int32_t> ids(kv.size());
     for (size_t e = 0; e < kv.size(); ++e) ids[e] = kv[e].second;

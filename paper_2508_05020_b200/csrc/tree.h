@@ -64,6 +64,16 @@ class FlatIndex {
         for (size_t i = 0; i < keys_.size(); ++i)
             if (keys_[i] != kEmpty) f(keys_[i], vals_[i]);
     }
+    // every (key, id) entry into out, in table order; branch-free (a half-full table defeats the branch predictor)
+    void dump(std::vector<std::pair<uint64_t, int32_t>>& out) const {
+        out.resize(size_ + 1);
+        size_t n = 0;
+        for (size_t i = 0; i < keys_.size(); ++i) {
+            out[n] = {keys_[i], vals_[i]};
+            n += keys_[i] != kEmpty;
+        }
+        out.resize(n);
+    }
 
   private:
     static constexpr uint64_t kEmpty = ~0ull;
@@ -85,21 +95,25 @@ class FlatIndex {
     }
 };
 
-// LSD radix sort of (key, id) pairs by key; a digit shared by every key is skipped.  Digits of 8 bits below 64 k
-// pairs (the 256 counters stay cheap to clear), 16 bits above.  Keys are unique in every use (patch keys,
-// level-Morton keys), so the order is the plain key order.
+// LSD radix sort of (key, id) pairs by key.  Only the bit span in which the keys differ is sorted, in the fewest
+// passes of digits of at most 8 bits (under 2 k pairs), 12 bits (under 64 k) or 16 bits, split evenly (a compact
+// 22-bit patch key takes two passes).  Keys are unique in every use (patch keys, level-Morton keys), so the order
+// is the plain key order.
 inline void radix_sort_pairs(std::vector<std::pair<uint64_t, int32_t>>& v) {
-    const int bits = v.size() < 65536 ? 8 : 16;
+    if (v.size() < 2) return;
+    uint64_t diff = 0;   // bits in which some key differs from the first: only that span needs passes
+    for (const auto& e : v) diff |= e.first ^ v[0].first;
+    if (!diff) return;
+    const int lo = __builtin_ctzll(diff), span = 64 - __builtin_clzll(diff) - lo;
+    const int maxb = v.size() < 2048 ? 8 : (v.size() < 65536 ? 12 : 16);
+    const int passes = (span + maxb - 1) / maxb, bits = (span + passes - 1) / passes;
     const uint64_t mask = (1ull << bits) - 1;
     // scratch kept across calls (per thread): a fresh 100 KB+ buffer is an mmap plus page faults on every regrid
     static thread_local std::vector<std::pair<uint64_t, int32_t>> tmp;
     static thread_local std::vector<uint32_t> cnt;
     tmp.resize(v.size());
-    cnt.assign(size_t(1) << bits, 0u);
-    uint64_t diff = 0;   // bits in which some key differs from the first: only those digits need a pass
-    for (const auto& e : v) diff |= e.first ^ v[0].first;
-    for (int shift = 0; shift < 64; shift += bits) {
-        if (!((diff >> shift) & mask)) continue;
+    cnt.resize(size_t(1) << bits);
+    for (int p = 0, shift = lo; p < passes; ++p, shift += bits) {
         std::fill(cnt.begin(), cnt.end(), 0u);
         for (const auto& e : v) ++cnt[(e.first >> shift) & mask];
         uint32_t sum = 0;
@@ -127,6 +141,13 @@ struct PatchTree {
     static uint64_t key(int l, int i, int j) {
         return (uint64_t(uint32_t(l)) << 56) | (uint64_t(uint32_t(j)) << 28) | uint64_t(uint32_t(i));
     }
+    // bits of a finest-level patch coordinate per axis: (level, j, i) and (level, Morton(i, j)) packed above
+    // kb[0] + kb[1] (resp. 2 max(kb)) bits sort in few radix passes
+    int kb[2] = {0, 0};
+    uint64_t canon_key(uint64_t k) const {   // key(l, i, j) -> same order, compact
+        return ((k >> 56) << (kb[0] + kb[1])) | (((k >> 28) & 0xFFFFFFFull) << kb[0]) | (k & 0xFFFFFFFull);
+    }
+    int morton_shift() const { return 2 * std::max(kb[0], kb[1]); }   // level above a Morton key of (i, j)
     int npatch(int ax, int l) const { return np0[ax] << l; }
     // wrap a level-l patch position; false when outside a non-periodic boundary
     bool wrap(int l, int& i, int& j) const;
@@ -134,8 +155,8 @@ struct PatchTree {
     // id, -1 missing, -2 outside domain (|dx|, |dy| <= 1): by the parent/child links -- a sibling, else the child of
     // the parent's neighbour (roots from a table) -- with no hash probe
     int neighbour(int id, int dx, int dy) const;
-    bool has_children(int id) const { return child[4 * id] >= 0; }
-    bool is_leaf(int id) const { return alive[id] && child[4 * id] < 0; }
+    bool has_children(int id) const { return node_[id].child[0] >= 0; }
+    bool is_leaf(int id) const { return node_[id].lev >= 0 && node_[id].child[0] < 0; }   // alive <=> lev >= 0
 
     // Alg. 1 on a copy-on-write basis; returns false (tree unchanged by caller's
     // transaction) on capacity overflow.
@@ -143,6 +164,10 @@ struct PatchTree {
     bool coarsen_allowed(int id) const;
     void delete_children(int id);
     bool validate(std::string& err) const;
+    // The same checks restricted to what the open transaction changed (journaled slots, the Moore neighbours of
+    // removed positions, released slots with children): equal to validate() when the tree was valid at
+    // begin_txn(), in O(changes).
+    bool validate_txn(std::string& err) const;
     // ids of active patches in canonical order (level, j, i)
     std::vector<int32_t> canonical() const;
 
@@ -162,8 +187,18 @@ struct PatchTree {
     std::vector<SlotSnap> journal_;
     std::vector<uint8_t> touched_;
     bool txn_ = false;
+    bool released_parent_ = false;   // a slot with children was released inside the transaction (orphans)
     void touch(int id);
     FlatIndex index_;
+    // packed copy of (lev, pi, pj, parent, child[4]) per slot, for neighbour(): one 32-byte line per node visited
+    // instead of five arrays (1.8x faster lookups); written only by sync(), after every change of a slot
+    struct Node {
+        int32_t lev, pi, pj, parent, child[4];
+    };
+    std::vector<Node> node_;
+    void sync(int id) {
+        node_[id] = Node{lev[id], pi[id], pj[id], parent[id], {child[4 * id], child[4 * id + 1], child[4 * id + 2], child[4 * id + 3]}};
+    }
     std::vector<int32_t> root_;   // root (i, j) -> slot, row-major (R1: roots are permanent)
     std::vector<int32_t> free_;   // min-heap of free slots
     int alloc(int l, int i, int j);

@@ -3,6 +3,8 @@ Moore neighbour link of amr_plan_tree -- computed from parent/child links and th
 equals a brute-force lookup of the neighbour's (level, i, j) among the active patches (periodic wrap in x, walls
 in y), and the links are symmetric; parent/child links match the positions.  Exercises R2 closure too (Alg. 1
 recursion creates the support the lookup relies on)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -43,3 +45,38 @@ def test_neighbour_links_match_brute_force(seed):
             if d.child[c] >= 0:
                 ch = tr[d.child[c]]
                 assert (ch.level, ch.i, ch.j) == (d.level + 1, 2 * d.i + (c & 1), 2 * d.j + (c >> 1))
+
+
+@pytest.mark.parametrize("rule", ["r2_exact", "alg2_literal"])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_incremental_validation_matches_full(rule, seed):
+    """The device path validates a regrid in O(changes) (PatchTree::validate_txn); amr_plan_regrid runs it beside
+    the full O(active) validate() and returns AMR_E_STATE (8) if they ever disagree.  Random mixed refine /
+    coarsen requests under both coarsening rules (the literal Alg. 2 rule can break R2 and must be rejected by
+    both); a rejected regrid leaves the tree unchanged."""
+    rng = np.random.default_rng(100 + seed)
+    levels = 4
+    p = Plan(dict(_cfg(levels), coarsen_rule=rule))
+    L = p.L
+    outcomes = {0: 0, 4: 0}
+    sizes = []
+    for it in range(14):
+        tr = p.tree(1)
+        sizes.append(len(tr))
+        if it < 10:   # grow with mixed requests, then coarsen everywhere coarsening is allowed
+            k = rng.integers(1, max(2, len(tr) // 3))
+            idx = rng.choice(len(tr), size=k, replace=False).astype(np.int32)
+            bits = rng.choice(np.array([1, 2, 2, 3], np.uint8), size=k)
+        else:
+            k = len(tr)
+            idx = np.arange(k, dtype=np.int32)
+            bits = np.full(k, 2, np.uint8)
+        rc = L.amr_plan_regrid(p.h, k, idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                               bits.ctypes.data_as(C.POINTER(C.c_uint8)))
+        assert rc in outcomes, rc
+        outcomes[rc] += 1
+        if rc:
+            assert [(d.level, d.i, d.j) for d in p.tree(1)] == [(d.level, d.i, d.j) for d in tr]
+    sizes.append(len(p.tree(1)))
+    assert outcomes[0] > 0
+    assert min(sizes[10:]) < sizes[10] and sizes[10] > sizes[0]   # grew, then shrank
