@@ -114,6 +114,7 @@ amr_status build_subcycle_plan(amr_ctx* c) {
     c->sub_poff.assign(L + 1, 0);
     c->acc_off.assign(L + 1, 0);
     c->rt_off.assign(L + 1, 0);
+    int cpar = -1, cnb[9];   // the last C/F parent's 3 x 3 neighbourhood
     auto add = [&](int id, bool covered) -> amr_status {
         LeafDesc d{};
         d.slot = id;
@@ -140,12 +141,16 @@ amr_status build_subcycle_plan(amr_ctx* c) {
                     p.kind = 1;
                     d.cf |= 1 << (4 + s);
                     int par = t.parent[id];
-                    for (int dy = -1; dy <= 1; ++dy)
-                        for (int dx = -1; dx <= 1; ++dx) {
-                            int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
-                            if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
-                            p.coarse[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
-                        }
+                    if (par != cpar) {   // siblings are consecutive (Morton leaf order): one lookup per parent
+                        cpar = par;
+                        for (int dy = -1; dy <= 1; ++dy)
+                            for (int dx = -1; dx <= 1; ++dx) {
+                                int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
+                                if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
+                                cnb[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
+                            }
+                    }
+                    for (int q = 0; q < 9; ++q) p.coarse[q] = cnb[q];
                 }
                 d.side[s] = -1 - p.proxy;
                 c->sub_ptasks.push_back(p);
