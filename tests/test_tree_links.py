@@ -27,6 +27,8 @@ def test_neighbour_links_match_brute_force(seed):
         pick = rng.choice(len(leaves), size=max(1, len(leaves) // 6), replace=False)
         p.refine([leaves[k] for k in pick])
     tr = p.tree(1)
+    order = [(d.level, d.j, d.i) for d in tr]   # canonical order (compact radix keys): (level, j, i), unique
+    assert order == sorted(set(order))
     key = {(d.level, d.i, d.j): e for e, d in enumerate(tr)}
     npx = {l: (64 // 8) << l for l in range(levels)}
     npy = {l: (48 // 8) << l for l in range(levels)}
@@ -78,5 +80,7 @@ def test_incremental_validation_matches_full(rule, seed):
         if rc:
             assert [(d.level, d.i, d.j) for d in p.tree(1)] == [(d.level, d.i, d.j) for d in tr]
     sizes.append(len(p.tree(1)))
+    order = [(d.level, d.j, d.i) for d in p.tree(1)]
+    assert order == sorted(set(order))
     assert outcomes[0] > 0
     assert min(sizes[10:]) < sizes[10] and sizes[10] > sizes[0]   # grew, then shrank
