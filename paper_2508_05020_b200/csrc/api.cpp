@@ -164,7 +164,7 @@ amr_status build_subcycle_plan(amr_ctx* c) {
         c->sub_descs.push_back(d);
         return AMR_OK;
     };
-    size_t e = 0, r = 0;
+    size_t e = 0, r = 0, cp = 0;
     for (int l = 0; l < L; ++l) {
         c->sub_off[l] = (int32_t)c->sub_descs.size();
         c->sub_poff[l] = (int32_t)c->sub_ptasks.size();
@@ -174,11 +174,13 @@ amr_status build_subcycle_plan(amr_ctx* c) {
             amr_status s = add(c->leaf_ids[e], false);
             if (s != AMR_OK) return s;
         }
-        for (int id : c->canon)
-            if (t.lev[id] == l && t.has_children(id) && c->comm.owns(c, id)) {
+        for (; cp < c->canon.size() && t.lev[c->canon[cp]] == l; ++cp) {   // canon is level-major: level l's run
+            const int id = c->canon[cp];
+            if (t.has_children(id) && c->comm.owns(c, id)) {
                 amr_status s = add(id, true);
                 if (s != AMR_OK) return s;
             }
+        }
         while (r < c->rtasks.size() && c->rtasks[r].level == l) ++r;
     }
     c->sub_levels = 0;
