@@ -27,7 +27,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with g++ (-O2 -ffp-contract=off, no fast-math)."""
     stale = not os.path.exists(_SO) or any(os.path.getmtime(s) > os.path.getmtime(_SO) for s in _SRC)
     if force or stale:
-        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-fopenmp",
                "-o", _SO + ".tmp", _SRC[0]]
         subprocess.check_call(cmd)
         os.replace(_SO + ".tmp", _SO)
@@ -39,7 +39,7 @@ class _Cfg(C.Structure):
                 ("levels", C.c_int), ("gamma", C.c_double), ("bc", C.c_int * 4), ("scheme", C.c_int),
                 ("characteristic", C.c_int), ("div_order", C.c_int), ("weno_eps", C.c_double),
                 ("theta", C.c_double), ("coarsen_frac", C.c_double), ("coarsen_rule", C.c_int),
-                ("check_positivity", C.c_int)]
+                ("check_positivity", C.c_int), ("reflux", C.c_int)]
 
 
 _lib = None
@@ -64,6 +64,10 @@ def lib():
         L.orc_get_patch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _D]
         L.orc_restrict_all.argtypes = [C.c_void_p]
         L.orc_lambda.argtypes = [C.c_void_p, _D]
+        L.orc_lambda_subcycled.argtypes = [C.c_void_p, _D]
+        L.orc_stage1.argtypes = [C.c_void_p, C.c_double]
+        L.orc_set_num_threads.argtypes = [C.c_int]
+        L.orc_get_max_threads.restype = C.c_int
         L.orc_totals.argtypes = [C.c_void_p, _D]
         L.orc_step.argtypes = [C.c_void_p, C.c_double, C.c_double, _D]
         L.orc_step_subcycled.argtypes = [C.c_void_p, C.c_double, C.c_double, _D]
@@ -113,6 +117,7 @@ def make_cfg(cfg: dict) -> _Cfg:
     c.coarsen_frac = cfg.get("coarsen_frac", 0.25)
     c.coarsen_rule = {"r2_exact": 0, "alg2_literal": 1}[cfg.get("coarsen_rule", "r2_exact")]
     c.check_positivity = int(cfg.get("check_positivity", 1))
+    c.reflux = int(cfg.get("oracle_reflux", 1))   # test-only no-reflux control (oracle side only)
     return c
 
 
@@ -181,6 +186,15 @@ class Oracle:
         v = C.c_double()
         self._chk(lib().orc_lambda(self.h, C.byref(v)))
         return v.value
+
+    def lam_subcycled(self):
+        v = C.c_double()
+        self._chk(lib().orc_lambda_subcycled(self.h, C.byref(v)))
+        return v.value
+
+    def stage1(self, dt):
+        """O11 stage 1 alone (forward Euler with reflux and restriction) -- for the reflux-placement pin."""
+        self._chk(lib().orc_stage1(self.h, float(dt)))
 
     def totals(self):
         out = np.zeros(4)
@@ -267,6 +281,15 @@ def eigen_x(WL, WR, gamma=1.4):
 def face_flux_x(cfg: dict, cells):
     c = make_cfg(cfg); cells = _f64(cells); assert cells.shape == (6, 4)
     F = np.empty(4); lib().orc_face_flux_x(C.byref(c), _dp(cells), _dp(F)); return F
+
+
+def set_num_threads(n: int):
+    """OpenMP threads of the oracle (over patches; results do not depend on it)."""
+    lib().orc_set_num_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().orc_get_max_threads())
 
 
 def mc(a, b):

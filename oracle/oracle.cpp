@@ -16,6 +16,7 @@
 #include "oracle.h"
 
 #include <cmath>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -23,6 +24,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace {
 
@@ -38,12 +42,35 @@ bool operator<(const Key& a, const Key& b) {
     if (a.Q != b.Q) return a.Q < b.Q;
     return a.P < b.P;
 }
-bool operator==(const Key& a, const Key& b) { return a.l == b.l && a.P == b.P && a.Q == b.Q; }
 
 /* O1: Moore directions in Fig. 2 nbr order: N, E, S, W, NE, SE, SW, NW. */
 const int MOORE[8][2] = {{0, 1}, {1, 0}, {0, -1}, {-1, 0}, {1, 1}, {1, -1}, {-1, -1}, {-1, 1}};
 
 void fail(const std::string& m) { throw std::runtime_error(m); }
+
+/* Deterministic parallelism over patches ("OpenMP over patches only"): f(e) for e in [0, n)
+ * writes only data owned by item e, so the result does not depend on the thread count or schedule.  An
+ * exception inside an item is re-thrown after the loop (the one of the lowest item, as a serial loop would). */
+template <class F>
+void par_for(long n, F f) {
+    long bad = n;
+    int kind = 0;
+    std::string msg;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long e = 0; e < n; ++e) {
+        try {
+            f(e);
+        } catch (const std::domain_error& x) {
+#pragma omp critical(orc_err)
+            if (e < bad) { bad = e; kind = 1; msg = x.what(); }
+        } catch (const std::exception& x) {
+#pragma omp critical(orc_err)
+            if (e < bad) { bad = e; kind = 2; msg = x.what(); }
+        }
+    }
+    if (kind == 1) throw std::domain_error(msg);
+    if (kind == 2) throw std::runtime_error(msg);
+}
 
 typedef std::map<Key, std::vector<double>> Field;   /* per patch U[4][n][n] */
 
@@ -70,7 +97,6 @@ struct Oracle {
     int ghost_width() const { return 4; }   /* A8: enough for every scheme */
 };
 
-int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 int posmod(int a, int b) { int r = a % b; return r < 0 ? r + b : r; }
 
 /* O1: wrap a patch position at level l; false when outside a non-periodic side. */
@@ -509,24 +535,27 @@ void validate(const Oracle& o) {
 
 /* ------------------------------------------------------------------ restriction / reflux */
 /* O9: 2x2 average in the fixed order ((a+b)+(c+d))*0.25, finest level first */
+void restrict_parent(const Oracle& o, Field& S, const Key& p) {
+    int n = o.n(), l = p.l + 1;
+    std::vector<double>& up = S.at(p);
+    for (int k = 0; k < NV; ++k)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+                int a = (2 * i) / n, b = (2 * j) / n;
+                const std::vector<double>& uc = S.at(Key{l, 2 * p.P + a, 2 * p.Q + b});
+                int fi = 2 * i - a * n, fj = 2 * j - b * n;
+                double f00 = uc[(k * n + fj) * n + fi], f10 = uc[(k * n + fj) * n + fi + 1];
+                double f01 = uc[(k * n + fj + 1) * n + fi], f11 = uc[(k * n + fj + 1) * n + fi + 1];
+                up[(k * n + j) * n + i] = ((f00 + f10) + (f01 + f11)) * 0.25;
+            }
+}
+
 void restrict_all(const Oracle& o, Field& S) {
-    int n = o.n();
     for (int l = o.c.levels - 1; l >= 1; --l) {
-        for (auto& kv : o.tree) {
-            const Key& p = kv.first;
-            if (p.l != l - 1 || !kv.second) continue;
-            std::vector<double>& up = S.at(p);
-            for (int k = 0; k < NV; ++k)
-                for (int j = 0; j < n; ++j)
-                    for (int i = 0; i < n; ++i) {
-                        int a = (2 * i) / n, b = (2 * j) / n;
-                        const std::vector<double>& uc = S.at(Key{l, 2 * p.P + a, 2 * p.Q + b});
-                        int fi = 2 * i - a * n, fj = 2 * j - b * n;
-                        double f00 = uc[(k * n + fj) * n + fi], f10 = uc[(k * n + fj) * n + fi + 1];
-                        double f01 = uc[(k * n + fj + 1) * n + fi], f11 = uc[(k * n + fj + 1) * n + fi + 1];
-                        up[(k * n + j) * n + i] = ((f00 + f10) + (f01 + f11)) * 0.25;
-                    }
-        }
+        std::vector<Key> parents;   /* level l-1 patches with children; each writes only its own data */
+        for (auto& kv : o.tree)
+            if (kv.first.l == l - 1 && kv.second) parents.push_back(kv.first);
+        par_for((long)parents.size(), [&](long e) { restrict_parent(o, S, parents[e]); });
     }
 }
 
@@ -590,15 +619,32 @@ bool physical(const double* U, double g) {
     return W[0] > 0.0 && W[3] > 0.0;
 }
 
-/* O13: Lambda = max over leaf cells of (|u|+c)/dx + (|v|+c)/dy */
-double lambda_max(const Oracle& o) {
+/* max that keeps a NaN: once any candidate is NaN the result is NaN (a non-physical cell makes the wave speed,
+ * hence dt, undefined -- O13 / S:L412 "errors: NonPositiveState"); otherwise the ordinary maximum */
+double nan_max(double a, double b) {
+    if (std::isnan(a) || std::isnan(b)) return std::nan("");
+    return b > a ? b : a;
+}
+
+std::vector<Key> leaf_keys(const Oracle& o) {
+    std::vector<Key> v;
+    for (auto& kv : o.tree)
+        if (!kv.second) v.push_back(kv.first);
+    return v;
+}
+
+/* O13 ("max over all leaf nodes of [(|u|+c)/dx + (|v|+c)/dy]; uses each patch's own level spacing"):
+ * Lambda = max over leaf cells of (|u|+c)/dx_l + (|v|+c)/dy_l.  norm_level = 1 divides each leaf's value by 2^l
+ * (subcycling reading S6).  The max is order-independent, so the per-patch maxima may be taken in parallel. */
+double lambda_of(const Oracle& o, bool norm_level) {
     int n = o.n();
-    double lam = 0.0;
-    for (auto& kv : o.tree) {
-        if (kv.second) continue;
-        const Key& p = kv.first;
+    std::vector<Key> lv = leaf_keys(o);
+    std::vector<double> pm(lv.size(), 0.0);
+    par_for((long)lv.size(), [&](long e) {
+        const Key& p = lv[e];
         const std::vector<double>& u = o.U.at(p);
         double dx = o.h(0, p.l), dy = o.h(1, p.l);
+        double lam = 0.0;
         for (int j = 0; j < n; ++j)
             for (int i = 0; i < n; ++i) {
                 double Uc[4], W[4];
@@ -606,55 +652,68 @@ double lambda_max(const Oracle& o) {
                 cons2prim(o.c.gamma, Uc, W);
                 double cs = std::sqrt(o.c.gamma * W[3] / W[0]);
                 double s = (std::fabs(W[1]) + cs) / dx + (std::fabs(W[2]) + cs) / dy;
-                if (!(s <= lam)) lam = s;   /* NaN propagates */
+                if (norm_level) s = s / (double)(1 << p.l);
+                lam = nan_max(lam, s);
             }
-    }
+        pm[e] = lam;
+    });
+    double lam = 0.0;
+    for (double v : pm) lam = nan_max(lam, v);
     return lam;
 }
 
-/* O11: one SSP-RK3 step (Shu-Osher form) on the whole composite mesh */
-void step(Oracle& o, double dt) {
+double lambda_max(const Oracle& o) { return lambda_of(o, false); }
+
+/* O11 stage s (0, 1, 2) of SSP-RK3 (Shu-Osher form S:L419): U^(s+1) from U^(s) = prev and U^n = Un on
+ * every leaf, then O12 reflux (skipped when the test-only switch c.reflux is 0: the no-reflux control), then O9
+ * restriction, then the positivity check of the leaves.  Leaves are independent within the stage. */
+void stage(Oracle& o, const Field& Un, Field& prev, int s, double dt) {
     int n = o.n(), g = o.ghost_width();
     const double a_s[3] = {0.0, 0.75, 1.0 / 3.0};
     const double b_s[3] = {1.0, 0.25, 2.0 / 3.0};
-    const Field& Un = o.U;
-    Field prev = o.U;
-    for (int s = 0; s < 3; ++s) {
-        Field next = prev;
-        std::map<Key, Fluxes> Fh;
-        for (auto& kv : o.tree) {
-            if (kv.second) continue;
-            const Key& p = kv.first;
-            std::vector<double> tile = build_tile(o, prev, p, g);
-            std::vector<double> L;
-            Fluxes F;
-            spatial_operator(o, tile, p.l, L, F.X, F.Y);
-            Fh[p] = F;
-            std::vector<double>& out = next.at(p);
-            const std::vector<double>& un = Un.at(p);
-            const std::vector<double>& up = prev.at(p);
-            for (size_t e = 0; e < out.size(); ++e) {
-                if (s == 0) out[e] = un[e] + dt * L[e];
-                else out[e] = a_s[s] * un[e] + b_s[s] * (up[e] + dt * L[e]);
-            }
+    std::vector<Key> lv = leaf_keys(o);
+    Field next = prev;
+    std::vector<Fluxes> F(lv.size());
+    par_for((long)lv.size(), [&](long e) {
+        const Key& p = lv[e];
+        std::vector<double> tile = build_tile(o, prev, p, g);
+        std::vector<double> L;
+        spatial_operator(o, tile, p.l, L, F[e].X, F[e].Y);
+        std::vector<double>& out = next.at(p);
+        const std::vector<double>& un = Un.at(p);
+        const std::vector<double>& up = prev.at(p);
+        for (size_t q = 0; q < out.size(); ++q) {
+            if (s == 0) out[q] = un[q] + dt * L[q];
+            else out[q] = a_s[s] * un[q] + b_s[s] * (up[q] + dt * L[q]);
         }
-        reflux(o, next, Fh, b_s[s] * dt);
-        restrict_all(o, next);
-        for (auto& kv : o.tree) {
-            if (kv.second) continue;
-            const std::vector<double>& u = next.at(kv.first);
-            for (int e = 0; e < n * n; ++e) {
-                double Uc[4] = {u[e], u[n * n + e], u[2 * n * n + e], u[3 * n * n + e]};
-                if (o.c.check_positivity && !physical(Uc, o.c.gamma)) {
-                    char b[200];
-                    std::snprintf(b, sizeof b, "non-physical state at stage %d, patch (l=%d,P=%d,Q=%d), cell %d", s + 1,
-                                  kv.first.l, kv.first.P, kv.first.Q, e);
-                    throw std::domain_error(b);
-                }
-            }
-        }
-        prev.swap(next);
+    });
+    std::map<Key, Fluxes> Fh;
+    for (size_t e = 0; e < lv.size(); ++e) {
+        Fluxes& d = Fh[lv[e]];
+        d.X.swap(F[e].X);
+        d.Y.swap(F[e].Y);
     }
+    if (o.c.reflux) reflux(o, next, Fh, b_s[s] * dt);
+    restrict_all(o, next);
+    for (const Key& p : lv) {
+        const std::vector<double>& u = next.at(p);
+        for (int q = 0; q < n * n; ++q) {
+            double Uc[4] = {u[q], u[n * n + q], u[2 * n * n + q], u[3 * n * n + q]};
+            if (o.c.check_positivity && !physical(Uc, o.c.gamma)) {
+                char b[200];
+                std::snprintf(b, sizeof b, "non-physical state at stage %d, patch (l=%d,P=%d,Q=%d), cell %d", s + 1,
+                              p.l, p.P, p.Q, q);
+                throw std::domain_error(b);
+            }
+        }
+    }
+    prev.swap(next);
+}
+
+/* O11: one SSP-RK3 step on the whole composite mesh; U^n is replaced only when all three stages succeed */
+void step(Oracle& o, double dt) {
+    Field prev = o.U;
+    for (int s = 0; s < 3; ++s) stage(o, o.U, prev, s, dt);
     o.U.swap(prev);
 }
 
@@ -676,26 +735,7 @@ const double SSP_C[3] = {0.0, 1.0, 0.5};
 const double SSP_W[3] = {1.0 / 6.0, 1.0 / 6.0, 2.0 / 3.0};
 
 /* S6 */
-double lambda_subcycled(const Oracle& o) {
-    int n = o.n();
-    double lam = 0.0;
-    for (auto& kv : o.tree) {
-        if (kv.second) continue;
-        const Key& p = kv.first;
-        const std::vector<double>& u = o.U.at(p);
-        double dx = o.h(0, p.l), dy = o.h(1, p.l);
-        for (int j = 0; j < n; ++j)
-            for (int i = 0; i < n; ++i) {
-                double Uc[4], W[4];
-                for (int k = 0; k < NV; ++k) Uc[k] = u[((size_t)k * n + j) * n + i];
-                cons2prim(o.c.gamma, Uc, W);
-                double cs = std::sqrt(o.c.gamma * W[3] / W[0]);
-                double s = ((std::fabs(W[1]) + cs) / dx + (std::fabs(W[2]) + cs) / dy) / (double)(1 << p.l);
-                if (!(s <= lam)) lam = s;
-            }
-    }
-    return lam;
-}
+double lambda_subcycled(const Oracle& o) { return lambda_of(o, true); }
 
 /* C/F side classification of leaf p: 1 coarse side (same-level neighbour has children), 2 fine side (no
  * same-level neighbour inside the domain), 0 otherwise */
@@ -769,30 +809,36 @@ struct Subcycler {
                 }
             }
             Field next = prev;
-            for (auto& kv : o.tree) {
-                const Key& p = kv.first;
-                if (p.l != l) continue;
+            std::vector<Key> pl;   /* every active level-l patch (S1); independent within the stage */
+            for (auto& kv : o.tree)
+                if (kv.first.l == l) pl.push_back(kv.first);
+            std::vector<Fluxes> F(pl.size());
+            par_for((long)pl.size(), [&](long e) {
+                const Key& p = pl[e];
                 std::vector<double> tile = build_tile(o, view, p, g);
                 std::vector<double> L;
-                Fluxes F;
-                spatial_operator(o, tile, l, L, F.X, F.Y);
+                spatial_operator(o, tile, l, L, F[e].X, F[e].Y);
                 std::vector<double>& out = next.at(p);
                 const std::vector<double>& un = Un.at(p);
                 const std::vector<double>& up = prev.at(p);
-                for (size_t e = 0; e < out.size(); ++e) {
-                    if (s == 0) out[e] = un[e] + dt * L[e];
-                    else out[e] = a_s[s] * un[e] + b_s[s] * (up[e] + dt * L[e]);
+                for (size_t q = 0; q < out.size(); ++q) {
+                    if (s == 0) out[q] = un[q] + dt * L[q];
+                    else out[q] = a_s[s] * un[q] + b_s[s] * (up[q] + dt * L[q]);
                 }
-                if (!kv.second) {   /* leaf: flux registers (S3), positivity (S5) */
-                    accumulate(p, F, SSP_W[s]);
-                    for (int e = 0; e < n * n; ++e) {
-                        double Uc[4] = {out[e], out[n * n + e], out[2 * n * n + e], out[3 * n * n + e]};
-                        if (o.c.check_positivity && !physical(Uc, o.c.gamma)) {
-                            char b[200];
-                            std::snprintf(b, sizeof b, "non-physical state at level %d stage %d, patch (P=%d,Q=%d), cell %d",
-                                          l, s + 1, p.P, p.Q, e);
-                            throw std::domain_error(b);
-                        }
+            });
+            for (size_t e = 0; e < pl.size(); ++e) {
+                const Key& p = pl[e];
+                if (o.has_children(p)) continue;
+                /* leaf: flux registers (S3), positivity (S5) */
+                accumulate(p, F[e], SSP_W[s]);
+                const std::vector<double>& out = next.at(p);
+                for (int q = 0; q < n * n; ++q) {
+                    double Uc[4] = {out[q], out[n * n + q], out[2 * n * n + q], out[3 * n * n + q]};
+                    if (o.c.check_positivity && !physical(Uc, o.c.gamma)) {
+                        char b[200];
+                        std::snprintf(b, sizeof b, "non-physical state at level %d stage %d, patch (P=%d,Q=%d), cell %d",
+                                      l, s + 1, p.P, p.Q, q);
+                        throw std::domain_error(b);
                     }
                 }
             }
@@ -893,12 +939,12 @@ struct LeafFlag {
     bool ambiguous;
 };
 std::map<Key, LeafFlag> leaf_flags(const Oracle& o) {
-    std::map<Key, LeafFlag> out;
     int n = o.n(), g = 1, w = n + 2;
     double th = o.c.theta, tc = o.c.theta * o.c.coarsen_frac;
-    for (auto& kv : o.tree) {
-        if (kv.second) continue;
-        const Key& p = kv.first;
+    std::vector<Key> lv = leaf_keys(o);
+    std::vector<LeafFlag> fl(lv.size());
+    par_for((long)lv.size(), [&](long e) {
+        const Key& p = lv[e];
         std::vector<double> t = build_tile(o, o.U, p, g);
         double dx = o.h(0, p.l), dy = o.h(1, p.l);
         LeafFlag f{0.0, false};
@@ -909,27 +955,35 @@ std::map<Key, LeafFlag> leaf_flags(const Oracle& o) {
                 double gy = (R(j + 1, i) - R(j - 1, i)) / (2.0 * dy);
                 double eta = dx * std::sqrt(gx * gx + gy * gy) / R(j, i);
                 if (!(eta <= f.maxeta)) f.maxeta = eta;
+                /* A32: within 1e-9 relative of either threshold */
                 if (std::fabs(eta - th) <= 1e-9 * th || std::fabs(eta - tc) <= 1e-9 * tc) f.ambiguous = true;
             }
-        out[p] = f;
-    }
+        fl[e] = f;
+    });
+    std::map<Key, LeafFlag> out;
+    for (size_t e = 0; e < lv.size(); ++e) out[lv[e]] = fl[e];
     return out;
 }
 
 /* O8 for whole new patches, then O9 -- the data half of a regrid */
 void regrid_apply(Oracle& o, const std::map<Key, char>& old_tree) {
     int n = o.n();
-    for (int l = 1; l < o.c.levels; ++l)
-        for (auto& kv : o.tree) {
-            const Key& p = kv.first;
-            if (p.l != l || old_tree.count(p)) continue;
+    for (int l = 1; l < o.c.levels; ++l) {
+        std::vector<Key> fresh;   /* new level-l patches; they read level l-1 only, so they are independent */
+        for (auto& kv : o.tree)
+            if (kv.first.l == l && !old_tree.count(kv.first)) fresh.push_back(kv.first);
+        std::vector<std::vector<double>> val(fresh.size());
+        par_for((long)fresh.size(), [&](long e) {
+            const Key& p = fresh[e];
             std::vector<double> u((size_t)NV * n * n);
             for (int k = 0; k < NV; ++k)
                 for (int j = 0; j < n; ++j)
                     for (int i = 0; i < n; ++i)
                         u[((size_t)k * n + j) * n + i] = prolong_value(o, o.U, l, p.P * n + i, p.Q * n + j, k);
-            o.U[p] = u;
-        }
+            val[e].swap(u);
+        });
+        for (size_t e = 0; e < fresh.size(); ++e) o.U[fresh[e]].swap(val[e]);
+    }
     for (auto it = o.U.begin(); it != o.U.end();) {
         if (!o.tree.count(it->first)) it = o.U.erase(it);
         else ++it;
@@ -1048,6 +1102,32 @@ int orc_get_patch(void* h, int l, int P, int Q, double* U) {
 int orc_restrict_all(void* h) { return guarded(h, [&] { restrict_all(*H(h), H(h)->U); }); }
 
 int orc_lambda(void* h, double* lam) { return guarded(h, [&] { *lam = lambda_max(*H(h)); }); }
+int orc_lambda_subcycled(void* h, double* lam) { return guarded(h, [&] { *lam = lambda_subcycled(*H(h)); }); }
+
+int orc_stage1(void* h, double dt) {
+    return guarded(h, [&] {
+        Oracle& o = *H(h);
+        Field prev = o.U;
+        stage(o, o.U, prev, 0, dt);
+        o.U.swap(prev);
+    });
+}
+
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
+int orc_get_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
 
 int orc_totals(void* h, double* out4) {
     /* O18: M_k = sum over leaf cells of U_k dx dy, accumulated in long double */

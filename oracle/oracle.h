@@ -35,6 +35,8 @@ typedef struct {
     int coarsen_rule;      /* 0 R2-exact prose rule, 1 Alg. 2 literal  */
     int check_positivity;  /* 1: a non-physical leaf state after a stage is an error; 0: not checked
                               (the white-noise sweep is a throughput config, not physics) */
+    int reflux;            /* 1: O12 flux correction at coarse/fine faces (default); 0: TEST-ONLY control that
+                              omits it (the pins show conservation then fails) */
 } orc_config;
 
 void*       orc_create(const orc_config* cfg);
@@ -50,9 +52,16 @@ int orc_validate(void* h);
 int orc_set_patch(void* h, int l, int P, int Q, const double* U);
 int orc_get_patch(void* h, int l, int P, int Q, double* U);
 int orc_restrict_all(void* h);                         /* O9 */
-int orc_lambda(void* h, double* lam);                  /* O13 */
+int orc_lambda(void* h, double* lam);                  /* O13; NaN if any leaf cell gives NaN */
+int orc_lambda_subcycled(void* h, double* lam);        /* S6: per-leaf value divided by 2^l */
 int orc_totals(void* h, double* out4);                 /* O18 */
 int orc_step(void* h, double dt, double cfl, double* dt_used);   /* O11 */
+/* O11 stage 1 alone (U <- U + dt L(U), reflux with b_1 = 1, restriction): the unit the reflux-placement pin
+ * takes apart */
+int orc_stage1(void* h, double dt);
+/* OpenMP over patches: results are independent of the thread count */
+void orc_set_num_threads(int n);
+int  orc_get_max_threads(void);
 /* NEXT #4: one level-0 step of Berger-Colella time subcycling (dt_l = dt0 / 2^l, readings S1-S6 in oracle.cpp
  * and DESIGN.md s3b); dt0 <= 0: dt0 = cfl / max over leaves of the level-0-normalised wave speed */
 int orc_step_subcycled(void* h, double dt0, double cfl, double* dt_used);
