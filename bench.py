@@ -115,43 +115,74 @@ def sweep_cfg(args, world, scheme, characteristic=1):
 
 
 # --------------------------------------------------------------------------------------- reference arm
-def oracle_rate(cfg, cfl, seconds, max_steps=50, size=256):
-    """The CPU oracle as it stands on a size^2 periodic piece of the same field (same per-cell work)."""
+def host_cpu():
+    """The host the oracle runs on: logical CPUs usable by this process and the lscpu model name."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = os.cpu_count()
+    return {"model": model, "logical_cpus": os.cpu_count(), "usable_cpus": usable}
+
+
+def oracle_rate(cfg, cfl, seconds, threads=1, size=256, max_steps=100000, min_steps=1):
+    """The CPU oracle as it stands (OpenMP over patches with `threads` threads; deterministic) on a size^2
+    periodic piece of the same field (the same per-cell work).  Every step starts from the pristine piece; the
+    restore (marshalling through ctypes) is outside the timed calls, so only amr-equivalent orc_step time counts.
+    Returns (cell-updates/s per RK stage, steps, seconds timed)."""
     import oracle as orc
+    orc.set_num_threads(threads)
     sub = dict(cfg, base=(size, size), hi=(size / 4096.0, size / 4096.0))
     o = orc.Oracle(sub)
     U0 = W.level0_state(sub)
     o.set_state(lambda l, P, Q: U0[Q, P])
     dt = cfl / o.lam()
-    t0 = time.perf_counter()
-    k = 0
-    while True:
+    el, k = 0.0, 0
+    while (el < seconds or k < min_steps) and k < max_steps:
         o.set_state(lambda l, P, Q: U0[Q, P])
-        try:
-            o.step(dt=dt)
-        except Exception:
-            pass
+        t0 = time.perf_counter()
+        o.step(dt=dt)                  # check_positivity is 0 for the sweep: never raises
+        el += time.perf_counter() - t0
         k += 1
-        if time.perf_counter() - t0 > seconds or k >= max_steps:
-            break
-    el = time.perf_counter() - t0
     return size * size * 3 * k / el, k, el
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle, timed on the host cores, on the same workload's per-cell work."""
+    """--impl reference: the CPU oracle (there is no installable reference implementation: the reference is a
+    paper), timed on all of the host's cores, on this arm's workload: K timed steps after W warm-up steps, each an
+    SSP-RK3 step of a 1024^2 periodic piece of the same noise field (the same per-cell work as the GPU's
+    4096^2-per-GPU step, a bounded sample of it).  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    cfg, name = sweep_cfg(args, 1, args.scheme)
-    v, k, el = oracle_rate(cfg, args.cfl, seconds=max(5.0, 4.0 * args.steps), max_steps=max(3, 3 * args.steps))
-    sample = f"256^2 periodic piece of the same noise field, {k} SSP-RK3 steps, single thread"
+    import oracle as orc
+    orc.build()
+    cpu = host_cpu()
+    threads = cpu["usable_cpus"] or 1
+    cfg, name = sweep_cfg(args, world, args.scheme)
+    size = 1024
+    oracle_rate(cfg, args.cfl, 0.0, threads=threads, size=size, max_steps=max(1, args.warmup), min_steps=args.warmup)
+    v, k, el = oracle_rate(cfg, args.cfl, 0.0, threads=threads, size=size, max_steps=args.steps,
+                           min_steps=args.steps)
+    sample = (f"{size}^2 periodic piece of the same noise field per step, {k} timed SSP-RK3 steps after "
+              f"{args.warmup} warm-up, OpenMP over patches with {threads} threads on {cpu['model']}")
     line = {"impl": "reference", "metric": "Euler cell-updates/sec per RK stage", "value": v,
-            "unit": "cell-updates/s", "n_gpus": world, "steps": k, "warmup": 0, "ms_per_step": el / k * 1e3,
+            "unit": "cell-updates/s", "n_gpus": world, "steps": k, "warmup": args.warmup,
+            "ms_per_step": el / k * 1e3,
+            "ms_per_step_note": f"one SSP-RK3 step of the {size}^2 sample",
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": name, "scheme": args.scheme},
-            "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "config": {"workload": name, "scheme": args.scheme, "patch": args.n, "cfl_fixed_dt": args.cfl},
+            "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": threads, "kind": "oracle",
+                             "sample": sample, "host": cpu},
             "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -177,7 +208,7 @@ class Ctx:
             else:
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
         from paper_2508_05020_b200 import build as B
-        if self.rank == 0 and not os.path.exists(B.OUT):   # an existing library is used as built (flags kept)
+        if self.rank == 0:   # the library of this source tree (an mtime no-op when it is fresh)
             B.build()
         self.barrier()
         import paper_2508_05020_b200 as amr
@@ -515,10 +546,17 @@ def main():
                 "conservation_drift_per_step": main_res["conservation_drift_per_step"],
                 "positivity": main_res["positivity"]}
         if not args.no_cpu_baseline:
-            v, k, el = oracle_rate(cfg, args.cfl, args.cpu_seconds, max_steps=100000)
-            line["cpu_baseline"] = {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
-                                    "sample": f"256^2 periodic piece of the same noise field, {k} SSP-RK3 steps "
-                                              f"({el:.1f} s), single thread"}
+            cpu = host_cpu()
+            nt = cpu["usable_cpus"] or 1
+            v1, k1, el1 = oracle_rate(cfg, args.cfl, args.cpu_seconds / 2, threads=1, size=256)
+            vn, kn, eln = oracle_rate(cfg, args.cfl, args.cpu_seconds / 2, threads=nt, size=1024)
+            line["cpu_baseline"] = {
+                "value": vn, "unit": "cell-updates/s", "cores": nt, "kind": "oracle",
+                "sample": f"1024^2 periodic piece of the same noise field, {kn} SSP-RK3 steps ({eln:.1f} s timed), "
+                          f"OpenMP over patches, {nt} threads",
+                "host": cpu,
+                "single_thread": {"value": v1, "cores": 1,
+                                  "sample": f"256^2 piece, {k1} steps ({el1:.1f} s timed), 1 thread"}}
         line.update(extra)
         print(json.dumps(line), flush=True)
     if X.world > 1:

@@ -69,14 +69,17 @@ def run_pair(cfg, steps, cfl=None, dt=None, regrid_every=None, init=True, stats=
     worst = 0.0
     cfl = cfg.get("cfl", 0.5) if (cfl is None and dt is None) else cfl
     sub = bool(cfg.get("subcycle", 0))
+    dts = stats.setdefault("dts", [])
     for s in range(1, steps + 1):
         if dt is not None:
             o.step(dt=dt, subcycle=sub)
             g.step(dt=dt)
+            dts.append(dt)
         else:
             d1 = o.step(cfl=cfl, subcycle=sub)
             d2 = g.step(cfl=cfl)
             assert abs(d1 - d2) <= 1e-10 * d1, (s, d1, d2)
+            dts.append(d2)
         if check_each:
             e, _ = parity_error(o.get_state(), g.get_state())
             worst = max(worst, e)

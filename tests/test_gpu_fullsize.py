@@ -7,8 +7,10 @@ checked against the oracle to 1e-11 (O18 / A31 metric, tests/parity.py).
   the same field as a periodic block wide enough that the wrap's contamination (the scheme's reach per stage,
   3 stages) cannot reach the centre patch.  Corner patches cover the domain wrap.
 - configs[1] vortex, 1024^2 Central4: the whole oracle mesh, 10 CFL-0.5 steps.  WENO5-char: sampled blocks.
-- configs[2] quadrant, 512^2 base, 3 levels, WENO5-char: lockstep with regrids (A32), 6 steps.
-- configs[3] shock-bubble, 2048 x 1024 base, 4 levels, reflective walls: init protocol (A28) + 2 steps lockstep.
+- configs[2] quadrant, 512^2 base, 3 levels, WENO5-char: init protocol (A28) + 10 CFL-0.5 steps, regrid every 4
+  (A34: two regrids inside the window), flags in lockstep (A32); also with time subcycling (NEXT #4).
+- configs[3] shock-bubble, 2048 x 1024 base, 4 levels, reflective walls: init protocol + 10 CFL-0.5 steps, regrid
+  every 4, lockstep.  (The oracle runs OpenMP over patches, deterministic, so these finish in minutes.)
 """
 import numpy as np
 import pytest
@@ -126,17 +128,31 @@ def test_vortex_1024_weno_sampled():
     sampled_parity(cfg, _samples(32, 32, k=5, seed=1), cfl=0.5)
 
 
-def test_quadrant_512_three_levels_lockstep():
-    """configs[2] at full size: 512^2 base, 3 levels, 16^2 patches, WENO5-char, regrids in lockstep (A32)."""
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_quadrant_512_three_levels_lockstep(seed):
+    """configs[2] at full size: 512^2 base, 3 levels, 16^2 patches, WENO5-char, 10 steps, regrid every 4 (A34),
+    seeds 1-3 (D3)."""
     stats = {}
-    o, g, e = run_pair(W.quadrant(N=512, n=16, levels=3, seed=1), steps=6, cfl=0.5, regrid_every=3, stats=stats)
+    o, g, e = run_pair(W.quadrant(N=512, n=16, levels=3, seed=seed), steps=10, cfl=0.5, regrid_every=4,
+                       stats=stats)
+    assert len({k[0] for k in g.leaves()}) == 3
+    assert len(stats["dts"]) == 10
+
+
+def test_quadrant_512_subcycled_lockstep():
+    """configs[2] at full size with Berger-Colella subcycling (NEXT #4): 10 level-0 steps, regrid every 4."""
+    cfg = dict(W.quadrant(N=512, n=16, levels=3, seed=1), subcycle=1)
+    o, g, e = run_pair(cfg, steps=10, cfl=0.5, regrid_every=4)
     assert len({k[0] for k in g.leaves()}) == 3
 
 
 def test_shock_bubble_full_size_lockstep():
-    """configs[3] at full size: 2048 x 1024 base, 4 levels, reflective walls, init protocol + 2 steps."""
-    o, g, e = run_pair(W.shock_bubble(), steps=2, cfl=0.5)
+    """configs[3] at full size: 2048 x 1024 base, 4 levels, reflective walls, init protocol + 10 steps, regrid
+    every 4 (two regrids inside the window, A34)."""
+    stats = {}
+    o, g, e = run_pair(W.shock_bubble(), steps=10, cfl=0.5, regrid_every=4, stats=stats)
     assert len({k[0] for k in g.leaves()}) == 4
+    assert len(stats["dts"]) == 10
 
 
 @pytest.mark.parametrize("n", [8, 64])

@@ -3,7 +3,7 @@
 exercises what the in-process loopback cannot: cudaIpcGetMemHandle / cudaIpcOpenMemHandle of another process's
 pool, the peer-pull kernel and the stage kernel's TMA loads reading IPC-mapped memory (halo_mode 1 / 2), and the
 cross-process fence (stream synchronise + host barrier; no kernel ever waits on another process).  The owned
-results must be bitwise those of one rank."""
+results must be bitwise those of one rank, which is itself run in lockstep with the oracle (1e-11)."""
 import os
 import socket
 
@@ -73,9 +73,12 @@ def _free_port():
 def test_two_processes_bitwise_equal_single_rank(name, halo_mode):
     import torch.multiprocessing as mp
     import paper_2508_05020_b200 as amr
+    from tests.parity import run_pair
     cfg, steps, regrid = CASES[name]
-    g = amr.Mesh(cfg)
-    ref_dts = _drive(g, cfg, steps, regrid)
+    stats = {}
+    o, g, e = run_pair(cfg, steps, cfl=cfg.get("cfl", 0.5), regrid_every=regrid, stats=stats)
+    assert e <= 1e-11
+    ref_dts = stats["dts"]
     ref, ref_keys = g.get_state(), g.keys()
     g.close()
     world = 2

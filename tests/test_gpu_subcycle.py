@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("char", [1, 0])
 def test_quadrant_three_levels(char):
     cfg = dict(W.quadrant(N=64, n=16, levels=3, seed=1, characteristic=char), subcycle=1)
-    o, g, e = run_pair(cfg, steps=6, cfl=0.5, regrid_every=3)
+    o, g, e = run_pair(cfg, steps=10, cfl=0.5, regrid_every=4)
     assert len({k[0] for k in g.leaves()}) == 3
 
 
@@ -25,7 +25,7 @@ def test_central4_two_levels_walls(n):
     N = 128
     cfg = dict(W.vortex(N=N, n=n, levels=2, theta=0.01, bc=("transmissive", "transmissive", "reflective",
                                                             "reflective")), subcycle=1)
-    o, g, e = run_pair(cfg, steps=6, cfl=0.5, regrid_every=3)
+    o, g, e = run_pair(cfg, steps=10, cfl=0.5, regrid_every=4)
     assert len({k[0] for k in g.leaves()}) == 2
 
 
@@ -33,12 +33,12 @@ def test_blast_periodic_three_levels_n8():
     cfg = dict(lo=(0.0, 0.0), hi=(1.0, 1.0), base=(64, 64), n=8, levels=3, bc=("periodic",) * 4,
                scheme="weno5", characteristic=1, div_order=4, ic="blast", blast_width=0.08, theta=0.02,
                coarsen_frac=0.25, weno_eps=1e-6, gamma=1.4, cfl=0.4, subcycle=1)
-    run_pair(cfg, steps=6, regrid_every=3, check_each=True)
+    run_pair(cfg, steps=10, regrid_every=4, check_each=True)
 
 
 def test_shock_bubble_subcycled():
     cfg = dict(W.shock_bubble(Nx=128, Ny=64, n=16, levels=3), subcycle=1)
-    run_pair(cfg, steps=6, cfl=0.5, regrid_every=3)
+    run_pair(cfg, steps=10, cfl=0.5, regrid_every=4)
 
 
 def test_single_level_is_the_global_step_bitwise():
