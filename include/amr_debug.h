@@ -1,5 +1,6 @@
 /*
- * amr_debug.h -- host-only planning entry points of libamr.so (TEST-ONLY; no CUDA call is made).
+ * amr_debug.h -- TEST-ONLY entry points of libamr.so: host-only planning calls (no CUDA call is made) and
+ * one self-test of the NCCL transport (the only call here that touches the GPU).
  *
  * They expose the multi-rank plan the library computes from the replicated patch tree
  * (SURVEY.md s8(e)): the root-tree Morton partition and the per-peer exchange lists, so the N > 1
@@ -29,6 +30,14 @@ amr_status amr_plan_tree(amr_plan* p, int32_t world_size, amr_patch_desc* out, i
  * the index arrays hold the peers' lists back to back (capacity cap each). */
 amr_status amr_plan_exchange(amr_plan* p, int32_t world_size, int32_t rank, int32_t kind, int32_t* send_counts,
                              int32_t* send_index, int32_t* recv_counts, int32_t* recv_index, int32_t cap);
+
+/* NCCL self-test (needs a GPU and torch's libnccl.so.2): a ONE-rank communicator from the 128-byte unique id
+ * (amr_nccl_unique_id) drives the data path's NCCL transport -- grouped send/recv to self (the halo / flux /
+ * migration exchange call pattern), the four allreduce kinds (Lambda max-u64, max-f64, sum-f64 totals, max-i32
+ * errors), the peer-table byte-sum allreduce and the one-word fence -- and checks the results (bytes received =
+ * bytes sent; 1-rank reductions are the identity).  Returns AMR_OK, AMR_E_COMM (message in msg, NUL-terminated,
+ * at most msg_cap bytes) or AMR_E_CUDA. */
+amr_status amr_debug_nccl_selftest(const void* nccl_unique_id, char* msg, int32_t msg_cap);
 
 #ifdef __cplusplus
 }

@@ -877,3 +877,72 @@ extern "C" amr_status amr_nccl_unique_id(void* out128) {
     return AMR_E_COMM;
 #endif
 }
+
+// ====================================================================================  test-only: NCCL self-test
+// Drives the NCCL transport of the data path (NcclTransport: grouped send/recv, the four allreduce kinds, the
+// peer-mapping exchange and the stream-ordered fence) on a ONE-rank communicator -- the only communicator a one-GPU
+// box can host -- so that every resolved NCCL entry point runs once: ncclCommInitRank, ncclCommUserRank,
+// ncclGroupStart/End, ncclSend/Recv (to self), ncclAllReduce (max u64 / max f64 / sum f64 / max i32 / byte sum),
+// ncclGetErrorString, ncclCommDestroy.  Results are checked: the received bytes equal the sent ones and a 1-rank
+// reduction is the identity.
+extern "C" amr_status amr_debug_nccl_selftest(const void* uid128, char* msg, int32_t msg_cap) {
+    auto say = [&](const std::string& m) {
+        if (msg && msg_cap > 0) {
+            std::strncpy(msg, m.c_str(), (size_t)msg_cap - 1);
+            msg[msg_cap - 1] = 0;
+        }
+    };
+    if (!uid128) return AMR_E_ARG;
+#ifdef AMR_HAVE_NCCL_H
+    std::string e;
+    if (!amr::nccl_api().load(e)) { say(e); return AMR_E_COMM; }
+    amr::NcclApi& A = amr::nccl_api();
+    auto T = std::make_unique<amr::NcclTransport>();
+    ncclUniqueId id;
+    std::memcpy(&id, uid128, sizeof id);
+    ncclResult_t r = A.CommInitRank(&T->comm, 1, id, 0);
+    if (r != ncclSuccess) { say(std::string("ncclCommInitRank: ") + A.GetErrorString(r)); return AMR_E_COMM; }
+    say(std::string("ok: ") + A.GetErrorString(ncclSuccess));
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) { say("stream"); return AMR_E_CUDA; }
+    const size_t n = 4096;
+    std::vector<double> h(n), back(n);
+    for (size_t i = 0; i < n; ++i) h[i] = std::ldexp((double)(i * 2654435761u % 1000003u), -7) - 3.0;
+    double *src = nullptr, *dst = nullptr;
+    amr_status st = AMR_OK;
+    auto fail = [&](amr_status code, const std::string& m) { say(m); st = code; };
+    if (cudaMalloc(&src, n * 8) != cudaSuccess || cudaMalloc(&dst, n * 8) != cudaSuccess) fail(AMR_E_CUDA, "malloc");
+    if (st == AMR_OK) {
+        amr::h2d_sync(src, h.data(), n * 8, s);
+        cudaMemsetAsync(dst, 0, n * 8, s);
+        // grouped send/recv to self, as exchange_lists issues them (one Xfer per peer)
+        std::string x = T->p2p({{0, src, n * 8}}, {{0, dst, n * 8}}, s);
+        if (!x.empty()) fail(AMR_E_COMM, x);
+        else if (amr::d2h_sync(back.data(), dst, n * 8, s) != cudaSuccess) fail(AMR_E_CUDA, "d2h");
+        else if (std::memcmp(back.data(), h.data(), n * 8) != 0) fail(AMR_E_COMM, "send/recv to self: data differ");
+    }
+    for (int kind = 0; kind < 4 && st == AMR_OK; ++kind) {   // 1-rank reductions: identity
+        std::string x = T->allreduce(src, kind == 3 ? 2 * n : n, kind, s);
+        if (!x.empty()) { fail(AMR_E_COMM, x); break; }
+        if (amr::d2h_sync(back.data(), src, n * 8, s) != cudaSuccess) { fail(AMR_E_CUDA, "d2h"); break; }
+        if (std::memcmp(back.data(), h.data(), n * 8) != 0) fail(AMR_E_COMM, "allreduce kind " + std::to_string(kind) + " changed data");
+    }
+    if (st == AMR_OK) {   // peer table (byte-sum allreduce of the IPC records) and the fence
+        std::vector<void*> peers(1, nullptr);
+        std::string x = T->map_peers(src, n * 8, peers, s);
+        if (!x.empty()) fail(AMR_E_COMM, x);
+        else if (peers[0] != (void*)src) fail(AMR_E_COMM, "map_peers: own base not returned");
+        else if (!(x = T->fence(s)).empty()) fail(AMR_E_COMM, x);
+        else if (cudaStreamSynchronize(s) != cudaSuccess) fail(AMR_E_CUDA, "sync");
+    }
+    cudaFree(src);
+    cudaFree(dst);
+    T.reset();   // ncclCommDestroy
+    cudaStreamDestroy(s);
+    return st;
+#else
+    (void)msg_cap;
+    say("library built without nccl.h");
+    return AMR_E_COMM;
+#endif
+}

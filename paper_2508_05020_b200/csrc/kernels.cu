@@ -230,9 +230,14 @@ struct Block<16> { static constexpr int NT = 128; static constexpr int MINB = 4;
 template <>
 struct Block<32> { static constexpr int NT = 256; static constexpr int MINB = 2; };
 
+// T <= 16: x and y face fluxes in separate planes, computed in ONE loop over both directions (at T = 16 the
+// 16 x 19 faces per direction fill 128 threads to 79 % per pass, 2 x 304 faces in one pass fill 95 %)
+template <int T>
+constexpr bool kCombFaces = T <= 16;
+
 template <int SCHEME, int T>
 constexpr size_t stage_smem() {
-    return sizeof(double) * (4 * (T + 2 * kGL) * (T + 2 * kGL) + 4 * T * (T + 3));
+    return sizeof(double) * (4 * (T + 2 * kGL) * (T + 2 * kGL) + (kCombFaces<T> ? 2 : 1) * 4 * T * (T + 3));
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
@@ -320,8 +325,9 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
     const int x_lo = tx == 0, x_hi = tx == a.tiles - 1, y_lo = ty == 0, y_hi = ty == a.tiles - 1;
     const int store_mask = (d.cf | (d.cf >> 4)) & 15;
 
-    // ---- x faces (a4-a6): face m (left of cell m), row j
-    for (int e = tid; e < T * NF; e += NT) {
+    constexpr bool COMB = kCombFaces<T>;
+    double* const sFy = COMB ? sF + 4 * T * NF : sF;   // y-face fluxes [4][NF][T]
+    auto x_face = [&](int e) {   // face m (left of cell m), row j
         int j = e / NF, m = e - j * NF - 1;
         int o = (j + G) * W + (m + G);
         double f[4];
@@ -329,6 +335,30 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
         else weno_rusanov<SCHEME == 1>(sQ + o - 3, 1, PL, 1, 2, g, a.eps, f);
 #pragma unroll
         for (int k = 0; k < 4; ++k) sF[(k * T + j) * NF + m + 1] = f[k];
+    };
+    auto y_face = [&](int e) {   // face m (below cell m), column i; normal momentum is component 2
+        int m = e / T - 1, i = e - (m + 1) * T;
+        int o = (m + G) * W + (i + G);
+        double f[4];
+        if (SCHEME == 0) central4_flux(sQ + o - 2 * W, W, PL, 3, 2, inv_gm1, f);
+        else weno_rusanov<SCHEME == 1>(sQ + o - 3 * W, W, PL, 2, 1, g, a.eps, f);
+        sFy[(0 * NF + m + 1) * T + i] = f[0];
+        sFy[(1 * NF + m + 1) * T + i] = f[2];
+        sFy[(2 * NF + m + 1) * T + i] = f[1];
+        sFy[(3 * NF + m + 1) * T + i] = f[3];
+    };
+    // ---- faces (a4-a6)
+    if (COMB) {   // both directions in one pass; the x range padded to whole warps (no warp straddles x / y)
+        constexpr int NX = T * NF, NXP = (NX + 31) / 32 * 32;
+        for (int e = tid; e < NXP + NX; e += NT) {
+            if (e < NXP) {
+                if (e < NX) x_face(e);
+            } else {
+                y_face(e - NXP);
+            }
+        }
+    } else {
+        for (int e = tid; e < T * NF; e += NT) x_face(e);
     }
     __syncthreads();
     // ---- x divergence (a7, Eq. 9 flux form) into registers
@@ -352,21 +382,11 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             }
         }
     }
-    __syncthreads();
-
-    // ---- y faces: face m (below cell m), column i; normal momentum is component 2
-    for (int e = tid; e < T * NF; e += NT) {
-        int m = e / T - 1, i = e - (m + 1) * T;
-        int o = (m + G) * W + (i + G);
-        double f[4];
-        if (SCHEME == 0) central4_flux(sQ + o - 2 * W, W, PL, 3, 2, inv_gm1, f);
-        else weno_rusanov<SCHEME == 1>(sQ + o - 3 * W, W, PL, 2, 1, g, a.eps, f);
-        sF[(0 * NF + m + 1) * T + i] = f[0];
-        sF[(1 * NF + m + 1) * T + i] = f[2];
-        sF[(2 * NF + m + 1) * T + i] = f[1];
-        sF[(3 * NF + m + 1) * T + i] = f[3];
+    if (!COMB) {   // y faces into the same plane once the x divergence has read it
+        __syncthreads();
+        for (int e = tid; e < T * NF; e += NT) y_face(e);
+        __syncthreads();
     }
-    __syncthreads();
 
     // ---- y divergence, SSP-RK3 combination (a8), checks, Lambda (a9)
     const double dt = *a.dt;
@@ -384,7 +404,7 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             double o4[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const double* fr = sF + (k * NF + j + 1) * T + i;   // fr[0] = f at face j
+                const double* fr = sFy + (k * NF + j + 1) * T + i;   // fr[0] = f at face j
                 double fl = fr[0], fh = fr[T];
                 double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-T] + fh) : fl;
                 double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2 * T]) : fh;
@@ -393,7 +413,8 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
                     a.freg[(((size_t)d.slot * 4 + kS) * 4 + k) * n + tx * T + i] = Fl;
                 if (j == T - 1 && y_hi && (store_mask & 8))
                     a.freg[(((size_t)d.slot * 4 + kN) * 4 + k) * n + tx * T + i] = Fh;
-                double v = __ldg(pin + k * nn + off) + dt * L;
+                // U^(s-1): the WENO tile holds it in shared memory (Central4 converted its tile to primitives)
+                double v = (SCHEME != 0 ? sQ[k * PL + (j + G) * W + (i + G)] : __ldg(pin + k * nn + off)) + dt * L;
                 if (a.stage > 1) v = a.a * __ldg(pn + k * nn + off) + a.b * v;
                 o4[k] = v;
             }

@@ -10,7 +10,7 @@ import paper_2508_05020_b200 as amr  # noqa: E402
 import workloads as W  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "sb"
-cfg = W.shock_bubble() if which == "sb" else W.quadrant(N=512, n=16, levels=3, seed=1)
+cfg = W.shock_bubble(max_patches=100_000) if which == "sb" else W.quadrant(N=512, n=16, levels=3, seed=1)
 if len(sys.argv) > 2:
     cfg["subcycle"] = int(sys.argv[2])
 g = amr.Mesh(cfg)
