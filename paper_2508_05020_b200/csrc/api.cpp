@@ -382,6 +382,7 @@ amr_status build_plan(amr_ctx* c) {
     if (c->cfg.stage_kernel == 2)
         CU(c->unf_scratch.reserve(unfused_scratch_doubles(c->n, std::max<int>(1, (int)c->leaves.size()))));
     c->lambda_valid = false;
+    c->ghost_valid = false;
     c->plan_version++;
     c->plan_steps = 0;
     c->comm.replan(t);
@@ -476,6 +477,13 @@ amr_status harvest_events(amr_ctx* c) {
     return AMR_OK;
 }
 
+// The work after a stage kernel as one cooperative post-stage launch (one rank: no flux / halo exchange sits
+// between reflux, restriction and the next ghost fill).  AMR_POST_FUSE=0 selects the separate launches (A/B).
+bool post_fused(const amr_ctx* c) {
+    static const bool on = [] { const char* e = getenv("AMR_POST_FUSE"); return !(e && e[0] == '0'); }();
+    return on && c->comm.world == 1;
+}
+
 // one SSP-RK3 step, queued on the stream without host synchronisation
 amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
     if (!c->lambda_valid && !(dt > 0.0)) {
@@ -485,6 +493,7 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
     if (c->capturing) LAUNCH(launch_dt_dev(c->d_dt, c->d_lambda, c->d_err, c->d_dtp, c->stream), "dt");
     else LAUNCH(launch_dt(c->d_dt, c->d_lambda, c->d_err, dt, cfl, c->stream), "dt");
     const int A = (c->un + 1) % 3, B = (c->un + 2) % 3;
+    const bool fused = post_fused(c);
     const double as[3] = {0.0, 0.75, 1.0 / 3.0};
     const double bs[3] = {1.0, 0.25, 2.0 / 3.0};
     static const char* const kStageName[3] = {"stage 1", "stage 2", "stage 3"};
@@ -492,10 +501,15 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
         NvtxRange nv(kStageName[s - 1]);
         double* Uin = s == 1 ? c->U[c->un] : (s == 2 ? c->U[A] : c->U[B]);
         double* Uout = s == 2 ? c->U[B] : c->U[A];
-        amr_status cs = c->comm.exchange_halos_stage(c, Uin);
-        if (cs != AMR_OK) return cs;
-        cs = fill_ghosts(c, Uin);
-        if (cs != AMR_OK) return cs;
+        amr_status cs = AMR_OK;
+        // one rank: the previous stage's post kernel filled the ghost strips of this stage's input; stage 1 fills
+        // them here unless the last step's stage 3 already did (and nothing has changed U^n or the plan since)
+        if (!fused || (s == 1 && !(c->ghost_valid && !c->capturing))) {
+            cs = c->comm.exchange_halos_stage(c, Uin);
+            if (cs != AMR_OK) return cs;
+            cs = fill_ghosts(c, Uin);
+            if (cs != AMR_OK) return cs;
+        }
         StageArgs a{};
         a.leaves = c->d_leaves.p;
         a.nleaves = (int)c->leaves.size();
@@ -551,18 +565,41 @@ amr_status enqueue_step(amr_ctx* c, double dt, double cfl) {
             c->ev_cells.push_back(c->leaf_cells);
             c->ev_bytes.push_back((double)c->leaf_cells * (s == 1 ? 64.0 : 96.0));
         }
-        cs = c->comm.exchange_fluxes(c);
-        if (cs != AMR_OK) return cs;
-        if (!c->rtasks.empty()) {
-            AuxArgs x = aux(c, Uout, Uout);
-            x.b = bs[s - 1];
-            x.stage = s;
-            x.want_lambda = s == 3;
-            LAUNCH(launch_reflux(c->d_rtasks.p, (int)c->rtasks.size(), x, c->stream), "reflux");
+        if (fused) {   // reflux + restriction + the next stage's ghost strips in one cooperative launch
+            PostArgs p{};
+            p.a = aux(c, Uout, Uout);
+            p.a.b = bs[s - 1];
+            p.a.stage = s;
+            p.a.want_lambda = s == 3;
+            p.rtasks = c->d_rtasks.p;
+            p.nr = (int32_t)c->rtasks.size();
+            p.levels = c->cfg.num_levels;
+            bool work = p.nr > 0;
+            for (int l = 1; l < p.levels; ++l) {
+                p.rl[l] = c->d_rlev[l].p;
+                p.nrl[l] = (int32_t)c->rlev[l].size();
+                work = work || p.nrl[l] > 0;
+            }
+            p.ptasks = c->d_ptasks.p;
+            p.np = (s < 3 || !c->capturing) ? (int32_t)c->ptasks.size() : 0;   // a graph refills at its stage 1
+            p.g = c->g;
+            work = work || p.np > 0;
+            if (work) LAUNCH(launch_post_stage(p, c->stream), "post stage");
+        } else {
+            cs = c->comm.exchange_fluxes(c);
+            if (cs != AMR_OK) return cs;
+            if (!c->rtasks.empty()) {
+                AuxArgs x = aux(c, Uout, Uout);
+                x.b = bs[s - 1];
+                x.stage = s;
+                x.want_lambda = s == 3;
+                LAUNCH(launch_reflux(c->d_rtasks.p, (int)c->rtasks.size(), x, c->stream), "reflux");
+            }
+            cs = restrict_all(c, Uout);
+            if (cs != AMR_OK) return cs;
         }
-        cs = restrict_all(c, Uout);
-        if (cs != AMR_OK) return cs;
     }
+    c->ghost_valid = fused && !c->capturing;   // the ghost strips of U^(n+1) are in the proxies
     amr_status cs = c->comm.allreduce_max_u64(c, c->d_lambda);
     if (cs != AMR_OK) return cs;
     c->un = A;
@@ -589,6 +626,7 @@ amr_status finish_step(amr_ctx* c, int prev_un, double* dt_used) {
             c->st.steps--;
         }
         c->lambda_valid = false;
+    c->ghost_valid = false;
         char b[256];
         if (e0 == 2) std::snprintf(b, sizeof b, "non-positive or non-finite time step (wave speed)");
         else if (slot >= 0 && slot < c->tree.capacity && c->tree.alive[slot])
@@ -814,6 +852,7 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     }
     CU(cudaStreamSynchronize(c->stream));
     c->lambda_valid = false;
+    c->ghost_valid = false;
     if ((int)c->fl_eta.size() == nt.capacity)   // no requests on the new mesh until the next flag evaluation
         for (int id : c->canon) { c->fl_eta[id] = std::nan(""); c->fl_ref[id] = c->fl_crs[id] = c->fl_amb[id] = 0; }
     if (nr) *nr = n_new;
@@ -1033,6 +1072,7 @@ amr_status amr_set_state(amr_ctx* c, int32_t npatch, const int32_t* tree_index, 
     if (s != AMR_OK) return s;
     CU(cudaStreamSynchronize(c->stream));
     c->lambda_valid = false;
+    c->ghost_valid = false;
     return AMR_OK;
 }
 
@@ -1062,6 +1102,7 @@ amr_status amr_set_state_device(amr_ctx* c, int32_t npatch, const int32_t* tree_
     s = restrict_all(c, c->U[c->un]);
     if (s != AMR_OK) return s;
     c->lambda_valid = false;
+    c->ghost_valid = false;
     return AMR_OK;
 }
 
@@ -1249,6 +1290,7 @@ amr_status enqueue_step_subcycled(amr_ctx* c, double dt, double cfl) {
     c->un = (c->un + 1) % 3;
     c->st.steps++;
     c->lambda_valid = true;
+    c->ghost_valid = false;
     return AMR_OK;
 }
 
@@ -1291,6 +1333,7 @@ amr_status enqueue_step_graph(amr_ctx* c, double dt, double cfl) {
     c->un = (u + 1) % 3;
     c->st.steps++;
     c->lambda_valid = true;
+    c->ghost_valid = false;   // the captured stage 3 does not refill (its stage 1 always does)
     return AMR_OK;
 }
 

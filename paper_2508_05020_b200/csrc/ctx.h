@@ -109,6 +109,7 @@ struct amr_ctx {
     unsigned long long* d_tmp = nullptr;
     void* h_pinned = nullptr;   // {int32 err[4]; double dt}
     bool lambda_valid = false;
+    bool ghost_valid = false;      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
     double last_dt = 0.0;
 
     // flags of the last evaluation, per id

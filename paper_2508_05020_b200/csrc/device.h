@@ -131,7 +131,22 @@ struct AuxArgs {
     Geometry geo;
 };
 
+// The work between two stage kernels (post_stage_kernel, one cooperative launch): reflux, restriction of every
+// level (finest first), then -- np > 0 -- the ghost strips of the next stage's input (= this stage's output).
+struct PostArgs {
+    AuxArgs a;                           // U = Uw = the stage output; b, stage, want_lambda of the stage
+    const RefluxTask* rtasks;
+    int32_t nr;
+    int32_t levels;
+    const RestrictTask* rl[kMaxLevels];  // rl[l]: level l restricted into level l - 1
+    int32_t nrl[kMaxLevels];
+    const ProxyTask* ptasks;
+    int32_t np;
+    int32_t g;
+};
+
 // launchers (kernels.cu); each returns the CUDA error of the launch
+cudaError_t launch_post_stage(const PostArgs& p, cudaStream_t s);
 cudaError_t launch_stage(int scheme, const StageArgs& a, cudaStream_t s);
 cudaError_t launch_ghost(const ProxyTask* tasks, int ntasks, int g, const AuxArgs& a, cudaStream_t s);
 cudaError_t launch_reflux(const RefluxTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s);

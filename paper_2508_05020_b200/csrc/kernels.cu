@@ -17,10 +17,14 @@
 #include <cstdlib>
 
 #include <cuda.h>
+#include <cooperative_groups.h>
+
+#include <algorithm>
 
 #include "device.h"
 
 namespace amr {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kBcPeriodic = 0, kBcTransmissive = 1, kBcReflective = 2;
@@ -2167,11 +2171,10 @@ __global__ void ghost_kernel(const ProxyTask* __restrict__ tasks, int ntasks, in
 // every fine ghost cell applies prolong_value's arithmetic to them -- bitwise the per-cell kernel's result with
 // ~16x fewer global reads (each coarse value was re-read by up to 20 fine cells x stencil points).
 constexpr int kGhostThreads = 128;
-__global__ void __launch_bounds__(kGhostThreads) ghost_tile_kernel(const ProxyTask* __restrict__ tasks, int g,
-                                                                  const AuxArgs a) {
-    extern __shared__ double cs[];   // [4][ry span][rx span]
+// One C/F or physical-boundary ghost strip, by a whole thread block (block-uniform pt; cs: shared staging of
+// 4 (g/2 + 2)(n/2 + 2) doubles).  Used by ghost_tile_kernel (one block per strip) and the fused post-stage kernel.
+__device__ __forceinline__ void ghost_strip(const ProxyTask& pt, int g, const AuxArgs& a, double* cs) {
     const int n = a.geo.n;
-    const ProxyTask pt = tasks[blockIdx.x];
     const size_t nn = (size_t)n * n;
     // ghost cells of the strip, patch-local (li, lj) ranges
     int li0, li1, lj0, lj1;
@@ -2249,11 +2252,10 @@ __global__ void prolong_kernel(const ProlongTask* __restrict__ tasks, int ntasks
 }
 
 // ---------------------------------------------------------------- restriction (O9)
-__global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
+// O9 for parent cell e of restriction task `task`: ((a + b) + (c + d)) * 0.25 of the 2 x 2 children cells
+__device__ __forceinline__ void restrict_cell(const RestrictTask* __restrict__ tasks, long long t, const AuxArgs& a) {
     const int n = a.geo.n;
     const size_t nn = (size_t)n * n;
-    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (long long)ntasks * (long long)nn) return;
     const int task = (int)(t / (long long)nn), e = (int)(t - (long long)task * nn);
     const RestrictTask rt = tasks[task];
     const int i = e % n, j = e / n;
@@ -2268,13 +2270,25 @@ __global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntas
     }
 }
 
+__global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)ntasks * a.geo.n * a.geo.n) return;
+    restrict_cell(tasks, t, a);
+}
+
+
 // ---------------------------------------------------------------- flux correction (O12)
-__global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
+__global__ void __launch_bounds__(kGhostThreads) ghost_tile_kernel(const ProxyTask* __restrict__ tasks, int g,
+                                                                  const AuxArgs a) {
+    extern __shared__ double cs[];   // [4][ry span][rx span]
+    ghost_strip(tasks[blockIdx.x], g, a, cs);
+}
+
+// O12 correction of one coarse boundary cell (work item t of 4 n per reflux task); Lambda (stage 3) into lam
+__device__ __forceinline__ void reflux_cell(const RefluxTask* __restrict__ tasks, int ntasks, long long t,
+                                            const AuxArgs& a, unsigned long long& lam) {
     const int n = a.geo.n;
     const size_t nn = (size_t)n * n;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    // every lane stays to the end: Lambda is warp-reduced before one atomic per warp
-    unsigned long long lam = 0ull;
     int task = 0, i = 0, j = 0, act = 0;
     if (t < (long long)ntasks * 4 * n) {
         task = (int)(t / (4 * n));
@@ -2319,12 +2333,50 @@ __global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, 
         if (a.want_lambda) {
             double sp = wave_speed(u[0], u[1], u[2], u[3], a.gamma, a.geo.inv_dx[l], a.geo.inv_dy[l]);
             if (a.lam0) sp = ldexp(sp, -l);
-            lam = (unsigned long long)__double_as_longlong(sp);
+            const unsigned long long b = (unsigned long long)__double_as_longlong(sp);
+            lam = b > lam ? b : lam;
         }
     }
+}
+
+__global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
+    // every lane stays to the end: Lambda is warp-reduced before one atomic per warp
+    unsigned long long lam = 0ull;
+    reflux_cell(tasks, ntasks, (long long)blockIdx.x * blockDim.x + threadIdx.x, a, lam);
     if (a.want_lambda) {
         lam = warp_max_u64(lam);
         if ((threadIdx.x & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
+    }
+}
+
+// The work between two stage kernels in ONE cooperative launch (instead of reflux + one restriction launch per
+// level + the next stage's ghost fill): O12 reflux of the coarse leaves; grid barrier; O9 restriction level by
+// level, finest first, a grid barrier after each; then the O7/O8 ghost strips of the next stage's input (this
+// stage's output).  The same per-cell arithmetic as the separate kernels, so the results are bitwise theirs.
+constexpr int kPostThreads = 256;
+__global__ void __launch_bounds__(kPostThreads) post_stage_kernel(const PostArgs p) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double cs[4 * (kGL / 2 + 2) * (64 / 2 + 2)];   // ghost staging (n <= 64, g = kGL)
+    const int n = p.a.geo.n;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    unsigned long long lam = 0ull;
+    const long long nre = (long long)p.nr * 4 * n;
+    for (long long t = tid; t < nre; t += nthr) reflux_cell(p.rtasks, p.nr, t, p.a, lam);
+    if (p.a.want_lambda) {
+        lam = warp_max_u64(lam);
+        if ((threadIdx.x & 31) == 0 && lam) atomicMax(p.a.lambda_bits, lam);
+    }
+    grid.sync();
+    for (int l = p.levels - 1; l >= 1; --l) {
+        if (p.nrl[l] == 0) continue;
+        const long long w = (long long)p.nrl[l] * n * n;
+        for (long long t = tid; t < w; t += nthr) restrict_cell(p.rl[l], t, p.a);
+        grid.sync();
+    }
+    for (int task = blockIdx.x; task < p.np; task += gridDim.x) {
+        ghost_strip(p.ptasks[task], p.g, p.a, cs);
+        __syncthreads();   // cs is reused by the block's next strip
     }
 }
 
@@ -2524,6 +2576,24 @@ cudaError_t launch_reflux(const RefluxTask* tasks, int ntasks, const AuxArgs& a,
     long long work = (long long)ntasks * 4 * a.geo.n;
     reflux_kernel<<<grid_for(work, 128), 128, 0, s>>>(tasks, ntasks, a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_post_stage(const PostArgs& p, cudaStream_t s) {
+    static int max_blocks = 0;
+    if (!max_blocks) {
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_stage_kernel, kPostThreads, 0);
+        if (e != cudaSuccess) return e;
+        max_blocks = (occ < 1 ? 1 : occ) * sm_count();
+    }
+    const int n = p.a.geo.n;
+    long long need = ((long long)p.nr * 4 * n + kPostThreads - 1) / kPostThreads;
+    for (int l = 1; l < p.levels; ++l)
+        need = std::max(need, ((long long)p.nrl[l] * n * n + kPostThreads - 1) / kPostThreads);
+    need = std::max(need, (long long)p.np);
+    const int grid = (int)std::max(1LL, std::min(need, (long long)max_blocks));
+    void* args[] = {const_cast<PostArgs*>(&p)};
+    return cudaLaunchCooperativeKernel((const void*)post_stage_kernel, dim3(grid), dim3(kPostThreads), args, 0, s);
 }
 
 cudaError_t launch_restrict(const RestrictTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s) {
