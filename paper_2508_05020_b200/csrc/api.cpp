@@ -407,7 +407,42 @@ AuxArgs aux(amr_ctx* c, const double* Ur, double* Uw) {
     return a;
 }
 
+// Launch timeline for performance work (AMR_TRACE=<file>, not for capture): an event before and after every
+// launch; written as "name start_us duration_us" lines (relative to the first event) at amr_destroy.
+void trace_pre(amr_ctx* c) {
+    if (!c->trace_on || c->capturing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    c->trace_ev.push_back(e);
+}
+void trace_post(amr_ctx* c, const char* what) {
+    if (!c->trace_on || c->capturing || c->trace_ev.size() % 2 == 0) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    c->trace_ev.push_back(e);
+    c->trace_name.push_back(what);
+}
+void trace_dump(amr_ctx* c) {
+    if (!c->trace_on || c->trace_ev.empty()) return;
+    cudaStreamSynchronize(c->stream);
+    FILE* f = std::fopen(getenv("AMR_TRACE"), "a");
+    if (!f) return;
+    for (size_t k = 0; k + 1 < c->trace_ev.size(); k += 2) {
+        float t0 = 0.f, t1 = 0.f;
+        cudaEventElapsedTime(&t0, c->trace_ev[0], c->trace_ev[k]);
+        cudaEventElapsedTime(&t1, c->trace_ev[k], c->trace_ev[k + 1]);
+        std::fprintf(f, "%s %.2f %.2f\n", c->trace_name[k / 2].c_str(), t0 * 1e3, t1 * 1e3);
+    }
+    std::fclose(f);
+    for (auto e : c->trace_ev) cudaEventDestroy(e);
+    c->trace_ev.clear();
+    c->trace_name.clear();
+}
+
 amr_status count_launch(amr_ctx* c, cudaError_t e, const char* what) {
+    trace_post(c, what);
     if (e != cudaSuccess) return fail(c, AMR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     c->st.launches++;
     return AMR_OK;
@@ -415,6 +450,7 @@ amr_status count_launch(amr_ctx* c, cudaError_t e, const char* what) {
 
 #define LAUNCH(expr, what)                                         \
     do {                                                           \
+        trace_pre(c);                                              \
         amr_status s_ = count_launch(c, (expr), what);             \
         if (s_ != AMR_OK) return s_;                               \
     } while (0)
@@ -983,6 +1019,7 @@ amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
 void amr_destroy(amr_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
+    trace_dump(c);
     c->comm.finalize(c);
     c->d_leaves.release(); c->d_gleaves.release(); c->d_singles.release(); c->d_ptasks.release(); c->d_rtasks.release(); c->d_prolong.release();
     for (auto& d : c->d_rlev) d.release();

@@ -2,6 +2,7 @@
 #pragma once
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -134,6 +135,9 @@ struct amr_ctx {
     uint64_t plan_version = 0;
     int64_t plan_steps = 0;     // steps taken with the current plan
     bool capturing = false;
+    bool trace_on = getenv("AMR_TRACE") != nullptr;   // launch timeline (performance work only)
+    std::vector<cudaEvent_t> trace_ev;
+    std::vector<std::string> trace_name;
     cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
     uint64_t gver[3] = {0, 0, 0};
     int64_t glaunches[3] = {0, 0, 0};

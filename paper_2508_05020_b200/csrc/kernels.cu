@@ -2171,9 +2171,12 @@ __global__ void ghost_kernel(const ProxyTask* __restrict__ tasks, int ntasks, in
 // every fine ghost cell applies prolong_value's arithmetic to them -- bitwise the per-cell kernel's result with
 // ~16x fewer global reads (each coarse value was re-read by up to 20 fine cells x stencil points).
 constexpr int kGhostThreads = 128;
-// One C/F or physical-boundary ghost strip, by a whole thread block (block-uniform pt; cs: shared staging of
-// 4 (g/2 + 2)(n/2 + 2) doubles).  Used by ghost_tile_kernel (one block per strip) and the fused post-stage kernel.
-__device__ __forceinline__ void ghost_strip(const ProxyTask& pt, int g, const AuxArgs& a, double* cs) {
+// One C/F or physical-boundary ghost strip by a group of nth threads (this one: tid; group-uniform pt; cs: shared
+// staging of 4 (g/2 + 2)(n/2 + 2) doubles; sync() orders the group between staging and use).  ghost_tile_kernel:
+// one block per strip; the fused post-stage kernel: one warp per strip.
+template <class Sync>
+__device__ __forceinline__ void ghost_strip(const ProxyTask& pt, int g, const AuxArgs& a, double* cs, int tid, int nth,
+                                            Sync sync) {
     const int n = a.geo.n;
     const size_t nn = (size_t)n * n;
     // ghost cells of the strip, patch-local (li, lj) ranges
@@ -2187,7 +2190,7 @@ __device__ __forceinline__ void ghost_strip(const ProxyTask& pt, int g, const Au
     const int ncell = (li1 - li0 + 1) * (lj1 - lj0 + 1);
     if (pt.kind == 0) {   // physical boundary: a plain copy (A25), as in ghost_kernel
         const int bc = a.geo.bc[pt.side];
-        for (int e = threadIdx.x; e < ncell; e += blockDim.x) {
+        for (int e = tid; e < ncell; e += nth) {
             const int w = li1 - li0 + 1, li = li0 + e % w, lj = lj0 + e / w;
             const int pli = pt.side == kW ? li + n : (pt.side == kE ? li - n : li);
             const int plj = pt.side == kS ? lj + n : (pt.side == kN ? lj - n : lj);
@@ -2211,12 +2214,12 @@ __device__ __forceinline__ void ghost_strip(const ProxyTask& pt, int g, const Au
     const int rx0 = ((pt.P * n + li0) >> 1) - Pp * n - 1, rx1 = ((pt.P * n + li1) >> 1) - Pp * n + 1;
     const int ry0 = ((pt.Q * n + lj0) >> 1) - Qp * n - 1, ry1 = ((pt.Q * n + lj1) >> 1) - Qp * n + 1;
     const int wx = rx1 - rx0 + 1, wy = ry1 - ry0 + 1, plane = wx * wy;
-    for (int e = threadIdx.x; e < 4 * plane; e += blockDim.x) {
+    for (int e = tid; e < 4 * plane; e += nth) {
         const int k = e / plane, r = e - k * plane, ry = ry0 + r / wx, rx = rx0 + r % wx;
         cs[e] = coarse_value(a.Uc, pt.coarse, n, pt.level - 1, Pp, Qp, rx, ry, k, a.geo, a.Uold, a.tfrac);
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < ncell; e += blockDim.x) {
+    sync();
+    for (int e = tid; e < ncell; e += nth) {
         const int w = li1 - li0 + 1, li = li0 + e % w, lj = lj0 + e / w;
         const int pli = pt.side == kW ? li + n : (pt.side == kE ? li - n : li);
         const int plj = pt.side == kS ? lj + n : (pt.side == kN ? lj - n : lj);
@@ -2281,7 +2284,7 @@ __global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntas
 __global__ void __launch_bounds__(kGhostThreads) ghost_tile_kernel(const ProxyTask* __restrict__ tasks, int g,
                                                                   const AuxArgs a) {
     extern __shared__ double cs[];   // [4][ry span][rx span]
-    ghost_strip(tasks[blockIdx.x], g, a, cs);
+    ghost_strip(tasks[blockIdx.x], g, a, cs, threadIdx.x, blockDim.x, [] { __syncthreads(); });
 }
 
 // O12 correction of one coarse boundary cell (work item t of 4 n per reflux task); Lambda (stage 3) into lam
@@ -2356,7 +2359,7 @@ __global__ void reflux_kernel(const RefluxTask* __restrict__ tasks, int ntasks, 
 constexpr int kPostThreads = 256;
 __global__ void __launch_bounds__(kPostThreads) post_stage_kernel(const PostArgs p) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double cs[4 * (kGL / 2 + 2) * (64 / 2 + 2)];   // ghost staging (n <= 64, g = kGL)
+    extern __shared__ double post_cs[];   // ghost staging, one [4][g/2+2][n/2+2] slice per warp
     const int n = p.a.geo.n;
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthr = (long long)gridDim.x * blockDim.x;
@@ -2374,9 +2377,13 @@ __global__ void __launch_bounds__(kPostThreads) post_stage_kernel(const PostArgs
         for (long long t = tid; t < w; t += nthr) restrict_cell(p.rl[l], t, p.a);
         grid.sync();
     }
-    for (int task = blockIdx.x; task < p.np; task += gridDim.x) {
-        ghost_strip(p.ptasks[task], p.g, p.a, cs);
-        __syncthreads();   // cs is reused by the block's next strip
+    // ghost strips: one warp per strip (a strip is g x n cells)
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* cs = post_cs + (size_t)wib * 4 * (p.g / 2 + 2) * (n / 2 + 2);
+    const int nw = gridDim.x * (kPostThreads / 32);
+    for (int task = blockIdx.x * (kPostThreads / 32) + wib; task < p.np; task += nw) {
+        ghost_strip(p.ptasks[task], p.g, p.a, cs, lane, 32, [] { __syncwarp(); });
+        __syncwarp();   // cs is reused by the warp's next strip
     }
 }
 
@@ -2579,21 +2586,26 @@ cudaError_t launch_reflux(const RefluxTask* tasks, int ntasks, const AuxArgs& a,
 }
 
 cudaError_t launch_post_stage(const PostArgs& p, cudaStream_t s) {
-    static int max_blocks = 0;
-    if (!max_blocks) {
-        int occ = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_stage_kernel, kPostThreads, 0);
-        if (e != cudaSuccess) return e;
-        max_blocks = (occ < 1 ? 1 : occ) * sm_count();
-    }
     const int n = p.a.geo.n;
+    const size_t smem = sizeof(double) * (kPostThreads / 32) * 4 * (p.g / 2 + 2) * (n / 2 + 2);
+    static int max_blocks = 0;
+    static size_t for_smem = 0;
+    if (!max_blocks || for_smem != smem) {
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_stage_kernel, kPostThreads, smem);
+        if (e != cudaSuccess) return e;
+        // at most 2 blocks per SM: the grid barriers cost more with more blocks, and the phases are short
+        static const int bps = [] { const char* e = getenv("AMR_POST_BPS"); return e ? atoi(e) : 2; }();   // A/B
+        max_blocks = std::max(1, std::min(occ, bps)) * sm_count();
+        for_smem = smem;
+    }
     long long need = ((long long)p.nr * 4 * n + kPostThreads - 1) / kPostThreads;
     for (int l = 1; l < p.levels; ++l)
         need = std::max(need, ((long long)p.nrl[l] * n * n + kPostThreads - 1) / kPostThreads);
-    need = std::max(need, (long long)p.np);
+    need = std::max(need, ((long long)p.np + kPostThreads / 32 - 1) / (kPostThreads / 32));
     const int grid = (int)std::max(1LL, std::min(need, (long long)max_blocks));
     void* args[] = {const_cast<PostArgs*>(&p)};
-    return cudaLaunchCooperativeKernel((const void*)post_stage_kernel, dim3(grid), dim3(kPostThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel((const void*)post_stage_kernel, dim3(grid), dim3(kPostThreads), args, smem, s);
 }
 
 cudaError_t launch_restrict(const RestrictTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s) {
