@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define AMR_ABI_VERSION 3
+#define AMR_ABI_VERSION 4
 
 typedef struct amr_ctx amr_ctx;   /* opaque */
 
@@ -148,6 +148,8 @@ typedef struct {
     int64_t leaf_cells;           /* current leaf cells owned by this rank                   */
     int64_t leaves, patches;      /* current leaf / active patch counts (whole mesh)         */
     int64_t proxies;              /* ghost strips filled per stage (C/F or physical BC sides) */
+    double  sim_time;             /* simulated time advanced by committed steps since the last reset
+                                     (summed on the device; reading it synchronises the stream) */
 } amr_stats;
 
 /* Library / ABI version; never fails. */

@@ -26,7 +26,7 @@ SCHEME = {"central4": 0, "weno5": 1}
 COARSEN = {"r2_exact": 0, "alg2_literal": 1}
 
 # every symbol include/amr.h declares (checked by tests/test_abi.py)
-ABI_VERSION = 3   # include/amr.h AMR_ABI_VERSION: the amr_config layout below
+ABI_VERSION = 4   # include/amr.h AMR_ABI_VERSION: the amr_config / amr_stats layouts below
 ABI_SYMBOLS = ["amr_abi_version", "amr_default_config", "amr_query_pool_bytes", "amr_create", "amr_destroy",
                "amr_set_state", "amr_set_state_fn", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
                "amr_regrid", "amr_regrid_with_flags", "amr_get_patch_tree", "amr_diagnostics",
@@ -95,7 +95,7 @@ class amr_stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("stage_launches", C.c_int64), ("stage_ms", C.c_double),
                 ("stage_timed", C.c_int64), ("stage_cells", C.c_int64), ("stage_bytes", C.c_double),
                 ("steps", C.c_int64), ("leaf_cells", C.c_int64), ("leaves", C.c_int64), ("patches", C.c_int64),
-                ("proxies", C.c_int64)]
+                ("proxies", C.c_int64), ("sim_time", C.c_double)]
 
 
 _lib = None

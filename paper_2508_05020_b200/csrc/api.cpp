@@ -121,7 +121,7 @@ amr_status build_subcycle_plan(amr_ctx* c) {
         d.level = t.lev[id];
         d.pad = covered ? 1 : 0;
         for (int s = 0; s < 4; ++s) {
-            int nb = t.neighbour(id, dirs[s][0], dirs[s][1]);
+            int nb = c->nb4[(size_t)4 * id + s];
             if (nb >= 0) {
                 d.side[s] = nb;
                 if (!covered && t.has_children(nb)) d.cf |= 1 << s;
@@ -207,19 +207,13 @@ amr_status build_plan(amr_ctx* c) {
     clk.mark("plan: canonical");
     for (size_t e = 0; e < c->canon.size(); ++e) c->canon_pos[c->canon[e]] = (int)e;
 
-    // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos
-    c->leaf_ids.clear();
-    for (int id : c->canon)
-        if (t.is_leaf(id) && c->comm.owns(c, id)) c->leaf_ids.push_back(id);
-    {   // packed (level, Morton key) computed once per leaf, then one radix sort of (key, id) pairs
-        static thread_local std::vector<std::pair<uint64_t, int32_t>> kv;   // scratch kept across plans
-        kv.clear();
-        kv.reserve(c->leaf_ids.size());
-        const int ms = t.morton_shift();   // level above the Morton key of the finest-level coordinate bits
-        for (int id : c->leaf_ids)
-            kv.push_back({(uint64_t(t.lev[id]) << ms) | morton(t.pi[id], t.pj[id]), id});
-        radix_sort_pairs(kv);
-        for (size_t e = 0; e < kv.size(); ++e) c->leaf_ids[e] = kv[e].second;
+    // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos (a depth-first walk
+    // from the roots in Morton order; the planning API checks it against the sort of (level, Morton) keys)
+    {
+        static thread_local std::vector<std::vector<int32_t>> per;   // scratch kept across plans
+        t.leaves_morton(per, [&](int id) { return c->comm.owns(c, id); });
+        c->leaf_ids.clear();
+        for (const auto& lv : per) c->leaf_ids.insert(c->leaf_ids.end(), lv.begin(), lv.end());
     }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
     clk.mark("plan: leaf order");
@@ -234,7 +228,20 @@ amr_status build_plan(amr_ctx* c) {
     }
     clk.mark("plan: canon + leaf order");
 
-    static const int dirs[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
+    // face neighbours of every active patch from the parents' (level-major, no recursion): nb4[4 id + s]
+    t.face_neighbours(c->canon, c->nb4);
+    clk.mark("plan: face neighbours");
+    // a C/F parent's 3 x 3 neighbourhood: faces from nb4, corners through the N / S face neighbour (R2: all 8
+    // exist inside the domain); -2 outside the domain
+    auto nbr = [&](int id, int dx, int dy) -> int {
+        if (dx == 0 && dy == 0) return id;
+        const int32_t* o = &c->nb4[(size_t)4 * id];
+        if (dy == 0) return o[dx < 0 ? kW : kE];
+        const int v = o[dy < 0 ? kS : kN];
+        if (dx == 0 || v < 0) return v;
+        const int r = c->nb4[(size_t)4 * v + (dx < 0 ? kW : kE)];
+        return r == -1 ? t.neighbour(id, dx, dy) : r;   // (-1: R2 violated; neighbour() decides as before)
+    };
     c->leaves.clear();
     c->ptasks.clear();
     c->rtasks.clear();
@@ -250,7 +257,7 @@ amr_status build_plan(amr_ctx* c) {
         rt.level = t.lev[id];
         rt.mask = 0;
         for (int s = 0; s < 4; ++s) {
-            int nb = t.neighbour(id, dirs[s][0], dirs[s][1]);
+            int nb = c->nb4[(size_t)4 * id + s];
             if (nb >= 0) {
                 d.side[s] = nb;
                 if (c->comm.world > 1 && c->comm.halo_mode == 2 && c->comm.owner[nb] != c->comm.rank)
@@ -290,7 +297,7 @@ amr_status build_plan(amr_ctx* c) {
                         cpar = par;
                         for (int dy = -1; dy <= 1; ++dy)
                             for (int dx = -1; dx <= 1; ++dx) {
-                                int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
+                                int q = nbr(par, dx, dy);
                                 if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
                                 cnb[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
                             }
@@ -660,6 +667,7 @@ amr_status finish_step(amr_ctx* c, int prev_un, double* dt_used) {
         if (prev_un >= 0) {
             c->un = prev_un;
             c->st.steps--;
+            c->sim_time_fix -= *hdt;   // the rolled-back step's dt was added on the device
         }
         c->lambda_valid = false;
     c->ghost_valid = false;
@@ -994,7 +1002,8 @@ amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
     }
     for (int b = 0; b < 3; ++b) c->U[b] = (double*)(base + (size_t)b * (need / 3));
     CU(cudaMemsetAsync(base, 0, need, c->stream));
-    CU(cudaMalloc(&c->d_dt, 8 * kMaxLevels));   // dt per level (subcycling); dt[0] otherwise
+    CU(cudaMalloc(&c->d_dt, 8 * (kMaxLevels + 1)));   // dt per level (subcycling; dt[0] otherwise), simulated time
+    CU(cudaMemset(c->d_dt, 0, 8 * (kMaxLevels + 1)));
     CU(cudaMalloc(&c->d_lambda, 8));
     CU(cudaMalloc(&c->d_tmp, 8));
     CU(cudaMalloc(&c->d_err, 16));
@@ -1548,6 +1557,10 @@ amr_status amr_get_stats(amr_ctx* c, amr_stats* out) {
     if (!out) return fail(c, AMR_E_ARG, "get_stats: NULL");
     s = harvest_events(c);
     if (s != AMR_OK) return s;
+    double t = 0.0;
+    CU(cudaMemcpyAsync(&t, c->d_dt + kMaxLevels, 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    c->st.sim_time = t + c->sim_time_fix;
     *out = c->st;
     return AMR_OK;
 }
@@ -1563,6 +1576,8 @@ amr_status amr_reset_stats(amr_ctx* c) {
     c->st.leaves = keep.leaves;
     c->st.patches = keep.patches;
     c->st.proxies = keep.proxies;
+    CU(cudaMemsetAsync(c->d_dt + kMaxLevels, 0, 8, c->stream));
+    c->sim_time_fix = 0.0;
     return AMR_OK;
 }
 

@@ -44,16 +44,6 @@ struct DevArray {
 };
 
 // bit interleave x0 y0 x1 y1 ... (Morton / Z order) by magic-number spreading
-inline uint64_t spread_bits(uint32_t v) {
-    uint64_t x = v;
-    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
-    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
-    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
-    x = (x | (x << 2)) & 0x3333333333333333ull;
-    x = (x | (x << 1)) & 0x5555555555555555ull;
-    return x;
-}
-inline uint64_t morton(uint32_t x, uint32_t y) { return spread_bits(x) | (spread_bits(y) << 1); }
 
 }  // namespace amr
 
@@ -110,7 +100,9 @@ struct amr_ctx {
     unsigned long long* d_tmp = nullptr;
     void* h_pinned = nullptr;   // {int32 err[4]; double dt}
     bool lambda_valid = false;
-    bool ghost_valid = false;      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
+    bool ghost_valid = false;
+    double sim_time_fix = 0.0;     // host correction of the device time sum (rolled-back steps)
+    std::vector<int32_t> nb4;      // face neighbours W, E, S, N of every slot (PatchTree::face_neighbours)      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
     double last_dt = 0.0;
 
     // flags of the last evaluation, per id

@@ -70,6 +70,27 @@ amr_status amr_plan_regrid(amr_plan* p, int32_t n, const int32_t* tree_index, co
     if (!full) return AMR_E_MESH;
     nt.commit();
     p->tree = nt;
+    // the O(active) orders and neighbour table of build_plan against their definitions (sorts, neighbour())
+    const amr::PatchTree& t = p->tree;
+    const std::vector<int32_t> ca = t.canonical(), cs = t.canonical_sorted();
+    if (ca != cs) return AMR_E_STATE;
+    std::vector<std::vector<int32_t>> per;
+    t.leaves_morton(per, [](int) { return true; });
+    std::vector<std::pair<uint64_t, int32_t>> kv;
+    for (int id : ca)
+        if (t.is_leaf(id)) kv.push_back({(uint64_t(t.lev[id]) << t.morton_shift()) | amr::morton(t.pi[id], t.pj[id]), id});
+    amr::radix_sort_pairs(kv);
+    size_t e = 0;
+    for (const auto& lv : per)
+        for (int id : lv)
+            if (e >= kv.size() || kv[e++].second != id) return AMR_E_STATE;
+    if (e != kv.size()) return AMR_E_STATE;
+    std::vector<int32_t> nb4;
+    t.face_neighbours(ca, nb4);
+    static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+    for (int id : ca)
+        for (int s2 = 0; s2 < 4; ++s2)
+            if (nb4[4 * (size_t)id + s2] != t.neighbour(id, d[s2][0], d[s2][1])) return AMR_E_STATE;
     return AMR_OK;
 }
 

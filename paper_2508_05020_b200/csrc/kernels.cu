@@ -2418,6 +2418,7 @@ __device__ __forceinline__ void dt_kernel_body(double* dt, unsigned long long* l
         if (atomicCAS(err, 0, 2) == 0) { err[1] = -1; err[2] = 0; err[3] = -1; }
     }
     *dt = d;
+    dt[kMaxLevels] += d;   // simulated time (amr_stats.sim_time)
     *lambda_bits = 0ull;
 }
 

@@ -47,7 +47,11 @@ void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, 
         for (int i = 0; i < npx; ++i) kv.push_back({morton_key(i, j), j * npx + i});
     radix_sort_pairs(kv);
     root_.assign((size_t)npx * npy, -1);
-    for (const auto& e : kv) root_[e.second] = alloc(0, e.second % npx, e.second / npx);
+    root_morton_.clear();
+    for (const auto& e : kv) {
+        root_[e.second] = alloc(0, e.second % npx, e.second / npx);
+        root_morton_.push_back(root_[e.second]);
+    }
 }
 
 void PatchTree::touch(int id) {
@@ -265,6 +269,59 @@ bool PatchTree::validate_txn(std::string& err) const {
 }
 
 std::vector<int32_t> PatchTree::canonical() const {
+    std::vector<int32_t> ids;
+    ids.reserve((size_t)n_alive);
+    for (int j = 0; j < np0[1]; ++j)
+        for (int i = 0; i < np0[0]; ++i) ids.push_back(root_[(size_t)j * np0[0] + i]);
+    size_t b = 0, e = ids.size();   // [b, e): level l in (j, i) order
+    while (b < e) {
+        for (size_t r = b; r < e;) {   // one row J of level l: rows 2J (children 0, 1) and 2J + 1 (children 2, 3)
+            size_t q = r;
+            while (q < e && node_[ids[q]].pj == node_[ids[r]].pj) ++q;
+            for (int half = 0; half < 2; ++half)
+                for (size_t k = r; k < q; ++k) {
+                    const Node& nd = node_[ids[k]];
+                    if (nd.child[0] < 0) continue;
+                    ids.push_back(nd.child[2 * half]);
+                    ids.push_back(nd.child[2 * half + 1]);
+                }
+            r = q;
+        }
+        b = e;
+        e = ids.size();
+    }
+    return ids;
+}
+
+void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4) const {
+    if (nb4.size() != (size_t)4 * capacity) nb4.assign((size_t)4 * capacity, -1);
+    static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
+    for (int id : canon) {
+        const Node& nd = node_[id];
+        int32_t* o = &nb4[(size_t)4 * id];
+        if (nd.lev == 0) {
+            for (int s = 0; s < 4; ++s) {
+                int i = nd.pi + d[s][0], j = nd.pj + d[s][1];
+                o[s] = wrap(0, i, j) ? root_[(size_t)j * np0[0] + i] : -2;
+            }
+            continue;
+        }
+        const Node& par = node_[nd.parent];
+        const int32_t* pn = &nb4[(size_t)4 * nd.parent];
+        const int a = nd.pi & 1, b = nd.pj & 1;
+        auto across = [&](int side, int cidx) {   // child cidx of the parent's neighbour on `side`, else -1 / -2
+            const int q = pn[side];
+            if (q < 0) return q;
+            return node_[q].child[0] < 0 ? -1 : node_[q].child[cidx];
+        };
+        o[0] = a == 1 ? par.child[0 + 2 * b] : across(0, 1 + 2 * b);
+        o[1] = a == 0 ? par.child[1 + 2 * b] : across(1, 0 + 2 * b);
+        o[2] = b == 1 ? par.child[a] : across(2, a + 2);
+        o[3] = b == 0 ? par.child[a + 2] : across(3, a);
+    }
+}
+
+std::vector<int32_t> PatchTree::canonical_sorted() const {
     static thread_local std::vector<std::pair<uint64_t, int32_t>> kv;   // key (level, j, i) = the map key
     index_.dump(kv);
     for (auto& e : kv) e.first = canon_key(e.first);

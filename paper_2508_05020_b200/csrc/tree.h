@@ -99,6 +99,17 @@ class FlatIndex {
 // passes of digits of at most 8 bits (under 2 k pairs), 12 bits (under 64 k) or 16 bits, split evenly (a compact
 // 22-bit patch key takes two passes).  Keys are unique in every use (patch keys, level-Morton keys), so the order
 // is the plain key order.
+inline uint64_t spread_bits(uint32_t v) {
+    uint64_t x = v;
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+inline uint64_t morton(uint32_t x, uint32_t y) { return spread_bits(x) | (spread_bits(y) << 1); }
+
 inline void radix_sort_pairs(std::vector<std::pair<uint64_t, int32_t>>& v) {
     if (v.size() < 2) return;
     uint64_t diff = 0;   // bits in which some key differs from the first: only that span needs passes
@@ -168,8 +179,33 @@ struct PatchTree {
     // removed positions, released slots with children): equal to validate() when the tree was valid at
     // begin_txn(), in O(changes).
     bool validate_txn(std::string& err) const;
-    // ids of active patches in canonical order (level, j, i)
+    // ids of active patches in canonical order (level, j, i): generated level by level from the parent rows (a
+    // level-(l+1) row 2J / 2J+1 is the SW,SE / NW,NE children of level-l row J, left to right), O(active)
     std::vector<int32_t> canonical() const;
+    // the same order by sorting the packed keys of the index (the definition; the planning API checks the two agree)
+    std::vector<int32_t> canonical_sorted() const;
+    // leaves per level in Morton order of their position (depth-first from the roots in Morton order, children in
+    // Morton order a + 2b): the launch order of build_plan without a sort; keep(id) filters (ownership)
+    template <class Keep>
+    void leaves_morton(std::vector<std::vector<int32_t>>& per_level, Keep keep) const {
+        per_level.assign(levels, {});
+        std::vector<int32_t>& st = dfs_;
+        st.clear();
+        for (auto it = root_morton_.rbegin(); it != root_morton_.rend(); ++it) st.push_back(*it);
+        while (!st.empty()) {
+            const int id = st.back();
+            st.pop_back();
+            const Node& nd = node_[id];
+            if (nd.child[0] < 0) {
+                if (keep(id)) per_level[nd.lev].push_back(id);
+            } else {
+                for (int q = 3; q >= 0; --q) st.push_back(nd.child[q]);
+            }
+        }
+    }
+    // face neighbours W, E, S, N of every active patch (nb4[4 id + s]: id, -1 missing, -2 outside the domain), top
+    // down over `canon` (level-major) from the parents' entries: equal to neighbour(id, +-1 / 0) without recursion
+    void face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4) const;
 
     // Transactions (regrid is atomic): between begin_txn() and commit()/rollback() every modified slot
     // is journaled once with its prior state, so a failed regrid is undone in O(changes) -- no copy of the
@@ -200,6 +236,8 @@ struct PatchTree {
         node_[id] = Node{lev[id], pi[id], pj[id], parent[id], {child[4 * id], child[4 * id + 1], child[4 * id + 2], child[4 * id + 3]}};
     }
     std::vector<int32_t> root_;   // root (i, j) -> slot, row-major (R1: roots are permanent)
+    std::vector<int32_t> root_morton_;   // root slots in Morton order of (i, j)
+    mutable std::vector<int32_t> dfs_;   // leaves_morton's stack
     std::vector<int32_t> free_;   // min-heap of free slots
     int alloc(int l, int i, int j);
     void release(int id);
