@@ -111,6 +111,42 @@ __device__ __forceinline__ double weno5(double v0, double v1, double v2, double 
     return num * fast_rcp(den);
 }
 
+// Both WENO5-JS interpolations at one face from the 6 stencil values w0..w5 (cells i-2 .. i+3): the left-biased
+// value from (w0..w4) and the right-biased one from (w5..w1) (A2), with exact-in-real-arithmetic sharing (A41):
+// the right stencil's second / third smoothness indicators reuse the left's t = v - 2v + v terms (T_c, T_b), its
+// middle candidate is twice the left's third (and the left's middle twice the right's third) once the linear
+// weights 10/16 and 5/16 are folded in, and every indicator is evaluated scaled by 12 -- S = (12 eps + 13 t^2 +
+// 3 u^2)^2 = 144 (eps + beta)^2, a common factor of all weights that cancels in the normalisation.
+__device__ __forceinline__ void weno5_pair(double w0, double w1, double w2, double w3, double w4, double w5,
+                                           double eps12, double& left, double& right) {
+    // candidate stencils (1/8 and the linear weights (1, 10, 5)/16 folded into the coefficients)
+    const double q0 = fma(0.375, w0, fma(-1.25, w1, 1.875 * w2));
+    const double q1 = fma(-1.25, w1, fma(7.5, w2, 3.75 * w3));
+    const double q2 = fma(1.875, w2, fma(3.75, w3, -0.625 * w4));
+    const double r0 = fma(0.375, w5, fma(-1.25, w4, 1.875 * w3));
+    const double r1 = 2.0 * q2, r2 = 0.5 * q1;
+    // second differences T (13 T^2 + 12 eps shared) and the one-sided u terms
+    const double Ta = fma(-2.0, w1, w0 + w2), Tb = fma(-2.0, w2, w1 + w3);
+    const double Tc = fma(-2.0, w3, w2 + w4), Td = fma(-2.0, w4, w3 + w5);
+    const double Aa = fma(13.0 * Ta, Ta, eps12), Ab = fma(13.0 * Tb, Tb, eps12);
+    const double Ac = fma(13.0 * Tc, Tc, eps12), Ad = fma(13.0 * Td, Td, eps12);
+    const double u0 = fma(-4.0, w1, fma(3.0, w2, w0)), u1 = w1 - w3, u2 = fma(3.0, w2, fma(-4.0, w3, w4));
+    const double v0 = fma(-4.0, w4, fma(3.0, w3, w5)), v1 = w4 - w2, v2 = fma(3.0, w3, fma(-4.0, w2, w1));
+    double s0 = fma(3.0 * u0, u0, Aa), s1 = fma(3.0 * u1, u1, Ab), s2 = fma(3.0 * u2, u2, Ac);
+    double z0 = fma(3.0 * v0, v0, Ad), z1 = fma(3.0 * v1, v1, Ac), z2 = fma(3.0 * v2, v2, Ab);
+    s0 *= s0; s1 *= s1; s2 *= s2;
+    z0 *= z0; z1 *= z1; z2 *= z2;
+    // omega_k ~ d_k / S_k: weights prod_{j != k} S_j with d_k folded into the candidates / the denominator
+    {
+        const double a0 = s1 * s2, a1 = s0 * s2, a2 = s0 * s1;
+        left = fma(a0, q0, fma(a1, q1, a2 * q2)) * fast_rcp(fma(10.0, a1, fma(5.0, a2, a0)));
+    }
+    {
+        const double a0 = z1 * z2, a1 = z0 * z2, a2 = z0 * z1;
+        right = fma(a0, r0, fma(a1, r1, a2 * r2)) * fast_rcp(fma(10.0, a1, fma(5.0, a2, a0)));
+    }
+}
+
 // WENO5 + Rusanov flux at one face in the face-normal frame (O10).
 // q points at component 0 of cell i-2 (the first of the 6 stencil cells) in shared memory;
 // cs = cell stride along the face normal, plane = component stride, kn / kt = components of
@@ -120,6 +156,7 @@ template <bool CHAR>
 __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int cs, int plane, int kn, int kt, double g,
                                              double eps, double F[4]) {
     const double gm1 = g - 1.0;
+    const double eps12 = 12.0 * eps;
 #define QV(s, k) q[(k) * plane + (s) * cs]
     double wl[4], wr[4];
     double u = 0.0, v = 0.0, c = 0.0, qk = 0.0, H = 0.0;
@@ -139,7 +176,7 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         c = fast_sqrt(c2);
         double ic = fast_rcp(c);
         qk = 0.5 * (u * u + v * v);
-        H = c2 / gm1 + qk;
+        H = c2 * (1.0 / gm1) + qk;   // (1 / gm1: one division per thread, hoisted by the compiler)
         double b1 = gm1 * (ic * ic);
         double b2 = b1 * qk;
         // rows of L (O10): l1 = 1/2 (b2 + u/c, -b1 u - 1/c, -b1 v, b1), l2, l3 = (-v, 0, 1, 0), l4
@@ -149,26 +186,22 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         double w[6];
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = h1 * QV(s, 0) + h2 * QV(s, kn) + h3 * QV(s, kt) + h4 * QV(s, 3);
-        wl[0] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
-        wr[0] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[0], wr[0]);
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = m1 * QV(s, 0) + m2 * QV(s, kn) + m3 * QV(s, kt) + m4 * QV(s, 3);
-        wl[1] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
-        wr[1] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[1], wr[1]);
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = -v * QV(s, 0) + QV(s, kt);
-        wl[2] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
-        wr[2] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[2], wr[2]);
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = k1 * QV(s, 0) + k2 * QV(s, kn) + h3 * QV(s, kt) + h4 * QV(s, 3);
-        wl[3] = weno5(w[0], w[1], w[2], w[3], w[4], eps);
-        wr[3] = weno5(w[5], w[4], w[3], w[2], w[1], eps);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[3], wr[3]);
     } else {
         const int kk[4] = {0, kn, kt, 3};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            wl[k] = weno5(QV(0, kk[k]), QV(1, kk[k]), QV(2, kk[k]), QV(3, kk[k]), QV(4, kk[k]), eps);
-            wr[k] = weno5(QV(5, kk[k]), QV(4, kk[k]), QV(3, kk[k]), QV(2, kk[k]), QV(1, kk[k]), eps);
+            weno5_pair(QV(0, kk[k]), QV(1, kk[k]), QV(2, kk[k]), QV(3, kk[k]), QV(4, kk[k]), QV(5, kk[k]), eps12, wl[k],
+                       wr[k]);
         }
     }
 #undef QV
