@@ -17,6 +17,23 @@ template <class T>
 struct DevArray {
     T* p = nullptr;
     size_t cap = 0, count = 0;
+    T* host = nullptr;         // pinned mirror of the last upload: the copy is a true async DMA (a pageable source
+    size_t hcap = 0;           // makes every cudaMemcpyAsync a staged, blocking copy of ~10 us)
+    DevArray() = default;
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    DevArray(DevArray&& o) noexcept : p(o.p), cap(o.cap), count(o.count), host(o.host), hcap(o.hcap) {
+        o.p = nullptr; o.host = nullptr; o.cap = o.count = o.hcap = 0;
+    }
+    DevArray& operator=(DevArray&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; cap = o.cap; count = o.count; host = o.host; hcap = o.hcap;
+            o.p = nullptr; o.host = nullptr; o.cap = o.count = o.hcap = 0;
+        }
+        return *this;
+    }
+    ~DevArray() { release(); }   // every device / pinned buffer of a ctx is freed with it
     cudaError_t upload(const std::vector<T>& v, cudaStream_t s) {
         count = v.size();
         if (v.size() > cap) {   // grow with 50 % slack: regrids that add a few patches do not reallocate
@@ -27,7 +44,20 @@ struct DevArray {
             if (e != cudaSuccess) { cap = 0; return e; }
         }
         if (v.empty()) return cudaSuccess;
-        return cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+        if (v.size() > hcap) {
+            if (host) cudaFreeHost(host);
+            host = nullptr;
+            hcap = std::max<size_t>(v.size() + v.size() / 2, 16);
+            cudaError_t e = cudaMallocHost(&host, hcap * sizeof(T));
+            if (e != cudaSuccess) { hcap = 0; return e; }
+        } else {
+            // the previous upload from the mirror must have left it (uploads happen at regrid, which synchronises
+            // the stream at its end; this is a no-op then)
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return e;
+        }
+        std::copy(v.begin(), v.end(), host);
+        return cudaMemcpyAsync(p, host, v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
     }
     // grows with 50 % slack (a proxy count growing by one must not re-allocate); slack = false for arrays sized
     // by the fixed slot capacity
@@ -40,7 +70,13 @@ struct DevArray {
         if (e != cudaSuccess) cap = 0;
         return e;
     }
-    void release() { if (p) cudaFree(p); p = nullptr; cap = count = 0; }
+    void release() {
+        if (p) cudaFree(p);
+        if (host) cudaFreeHost(host);
+        p = nullptr;
+        host = nullptr;
+        cap = count = hcap = 0;
+    }
 };
 
 // bit interleave x0 y0 x1 y1 ... (Morton / Z order) by magic-number spreading

@@ -293,10 +293,11 @@ std::vector<int32_t> PatchTree::canonical() const {
     return ids;
 }
 
-void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4) const {
+void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4,
+                                const std::function<void(int, const std::function<void(int)>&)>& par) const {
     if (nb4.size() != (size_t)4 * capacity) nb4.assign((size_t)4 * capacity, -1);
     static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
-    for (int id : canon) {
+    auto one = [&](int id) {
         const Node& nd = node_[id];
         int32_t* o = &nb4[(size_t)4 * id];
         if (nd.lev == 0) {
@@ -304,9 +305,9 @@ void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<i
                 int i = nd.pi + d[s][0], j = nd.pj + d[s][1];
                 o[s] = wrap(0, i, j) ? root_[(size_t)j * np0[0] + i] : -2;
             }
-            continue;
+            return;
         }
-        const Node& par = node_[nd.parent];
+        const Node& pa = node_[nd.parent];
         const int32_t* pn = &nb4[(size_t)4 * nd.parent];
         const int a = nd.pi & 1, b = nd.pj & 1;
         auto across = [&](int side, int cidx) {   // child cidx of the parent's neighbour on `side`, else -1 / -2
@@ -314,10 +315,27 @@ void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<i
             if (q < 0) return q;
             return node_[q].child[0] < 0 ? -1 : node_[q].child[cidx];
         };
-        o[0] = a == 1 ? par.child[0 + 2 * b] : across(0, 1 + 2 * b);
-        o[1] = a == 0 ? par.child[1 + 2 * b] : across(1, 0 + 2 * b);
-        o[2] = b == 1 ? par.child[a] : across(2, a + 2);
-        o[3] = b == 0 ? par.child[a + 2] : across(3, a);
+        o[0] = a == 1 ? pa.child[0 + 2 * b] : across(0, 1 + 2 * b);
+        o[1] = a == 0 ? pa.child[1 + 2 * b] : across(1, 0 + 2 * b);
+        o[2] = b == 1 ? pa.child[a] : across(2, a + 2);
+        o[3] = b == 0 ? pa.child[a + 2] : across(3, a);
+    };
+    // level by level (a level reads only its parents' entries)
+    for (size_t b0 = 0; b0 < canon.size();) {
+        size_t b1 = b0;
+        const int l = node_[canon[b0]].lev;
+        while (b1 < canon.size() && node_[canon[b1]].lev == l) ++b1;
+        const size_t cnt = b1 - b0;
+        const int nchunk = par ? (int)std::max<size_t>(1, std::min<size_t>(16, cnt / 2048)) : 1;
+        if (nchunk == 1) {
+            for (size_t e = b0; e < b1; ++e) one(canon[e]);
+        } else {
+            par(nchunk, [&](int k) {
+                const size_t e0 = b0 + cnt * k / nchunk, e1 = b0 + cnt * (k + 1) / nchunk;
+                for (size_t e = e0; e < e1; ++e) one(canon[e]);
+            });
+        }
+        b0 = b1;
     }
 }
 
