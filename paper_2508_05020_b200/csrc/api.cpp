@@ -253,8 +253,7 @@ amr_status build_plan(amr_ctx* c) {
     };
     const int nleaf = (int)c->leaf_ids.size();
     const int nchunk = std::max(1, std::min(HostPool::get().threads() * 2, nleaf / 1024));
-    static thread_local std::vector<Chunk> chunks;
-    chunks.resize(nchunk);
+    std::vector<Chunk> chunks(nchunk);   // shared by the workers (a thread_local would be per worker)
     HostPool::get().run(nchunk, [&](int k) {
         Chunk& ch = chunks[k];
         ch.leaves.clear();
