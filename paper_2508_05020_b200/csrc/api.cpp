@@ -14,7 +14,6 @@
 #include <vector>
 
 #include "ctx.h"
-#include "hostpool.h"
 
 using namespace amr;
 
@@ -230,7 +229,7 @@ amr_status build_plan(amr_ctx* c) {
     clk.mark("plan: canon + leaf order");
 
     // face neighbours of every active patch from the parents' (level-major, no recursion): nb4[4 id + s]
-    t.face_neighbours(c->canon, c->nb4, [](int n, const std::function<void(int)>& f) { HostPool::get().run(n, f); });
+    t.face_neighbours(c->canon, c->nb4);
     clk.mark("plan: face neighbours");
     // a C/F parent's 3 x 3 neighbourhood: faces from nb4, corners through the N / S face neighbour (R2: all 8
     // exist inside the domain); -2 outside the domain
@@ -243,112 +242,74 @@ amr_status build_plan(amr_ctx* c) {
         const int r = c->nb4[(size_t)4 * v + (dx < 0 ? kW : kE)];
         return r == -1 ? t.neighbour(id, dx, dy) : r;   // (-1: R2 violated; neighbour() decides as before)
     };
-    // leaf descriptors, proxy (ghost strip) tasks and reflux tasks: chunks of the launch order on the host pool,
-    // each with chunk-local proxy / leaf numbering, then merged in chunk order (the serial loop's numbering)
-    struct Chunk {
-        std::vector<LeafDesc> leaves;
-        std::vector<ProxyTask> ptasks;
-        std::vector<RefluxTask> rtasks;
-        std::string err;
-    };
-    const int nleaf = (int)c->leaf_ids.size();
-    const int nchunk = std::max(1, std::min(HostPool::get().threads() * 2, nleaf / 1024));
-    std::vector<Chunk> chunks(nchunk);   // shared by the workers (a thread_local would be per worker)
-    HostPool::get().run(nchunk, [&](int k) {
-        Chunk& ch = chunks[k];
-        ch.leaves.clear();
-        ch.ptasks.clear();
-        ch.rtasks.clear();
-        ch.err.clear();
-        const int e0 = (int)((int64_t)nleaf * k / nchunk), e1 = (int)((int64_t)nleaf * (k + 1) / nchunk);
-        int cpar = -1, cnb[9];   // the last C/F parent's 3 x 3 neighbourhood
-        for (int e = e0; e < e1 && ch.err.empty(); ++e) {
-            const int id = c->leaf_ids[e];
-            LeafDesc d{};
-            d.slot = id;
-            d.level = t.lev[id];
-            d.cf = 0;
-            RefluxTask rt{};
-            rt.leaf = (int)ch.leaves.size();
-            rt.slot = id;
-            rt.level = t.lev[id];
-            rt.mask = 0;
-            for (int s = 0; s < 4; ++s) {
-                int nb = c->nb4[(size_t)4 * id + s];
-                if (nb >= 0) {
-                    d.side[s] = nb;
-                    if (c->comm.world > 1 && c->comm.halo_mode == 2 && c->comm.owner[nb] != c->comm.rank)
-                        d.pad |= (16 << s) | (c->comm.owner[nb] << (8 + 3 * s));   // strip read from the owner's pool
-                    if (t.has_children(nb)) {
-                        d.cf |= 1 << s;
-                        rt.mask |= 1 << s;
-                        // the two children of nb adjacent to the shared face, ordered along it
-                        int cidx[2];
-                        if (s == kW) { cidx[0] = 1; cidx[1] = 3; }
-                        else if (s == kE) { cidx[0] = 0; cidx[1] = 2; }
-                        else if (s == kS) { cidx[0] = 2; cidx[1] = 3; }
-                        else { cidx[0] = 0; cidx[1] = 1; }
-                        for (int h = 0; h < 2; ++h) {
-                            int chd = t.child[4 * nb + cidx[h]];
-                            if (chd < 0 || !t.is_leaf(chd)) { ch.err = "reflux: fine side is not a leaf"; break; }
-                            rt.fine[s][h] = chd;
-                        }
-                    }
-                } else {
-                    ProxyTask p{};
-                    p.proxy = (int)ch.ptasks.size();
-                    p.slot = id;
-                    p.side = s;
-                    p.level = t.lev[id];
-                    p.P = t.pi[id];
-                    p.Q = t.pj[id];
-                    if (nb == -2) {
-                        p.kind = 0;
-                        for (int q = 0; q < 9; ++q) p.coarse[q] = -1;
-                    } else {
-                        p.kind = 1;
-                        d.cf |= 1 << (4 + s);
-                        int par = t.parent[id];
-                        if (par < 0) { ch.err = "missing same-level neighbour of a root"; break; }
-                        if (par != cpar) {   // siblings are consecutive in Morton order: one 3 x 3 lookup per parent
-                            cpar = par;
-                            for (int dy = -1; dy <= 1; ++dy)
-                                for (int dx = -1; dx <= 1; ++dx) {
-                                    int q = nbr(par, dx, dy);
-                                    if (q == -1) ch.err = "R2 violated: coarse neighbourhood incomplete";
-                                    cnb[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
-                                }
-                            if (!ch.err.empty()) { cpar = -1; break; }
-                        }
-                        for (int q = 0; q < 9; ++q) p.coarse[q] = cnb[q];
-                    }
-                    d.side[s] = -1 - p.proxy;
-                    ch.ptasks.push_back(p);
-                }
-            }
-            ch.leaves.push_back(d);
-            if (rt.mask) ch.rtasks.push_back(rt);
-        }
-    });
     c->leaves.clear();
     c->ptasks.clear();
     c->rtasks.clear();
-    for (Chunk& ch : chunks) {
-        if (!ch.err.empty()) return fail(c, AMR_E_MESH, ch.err);
-        const int loff = (int)c->leaves.size(), poff = (int)c->ptasks.size();
-        for (LeafDesc d : ch.leaves) {
-            for (int s = 0; s < 4; ++s)
-                if (d.side[s] < 0) d.side[s] -= poff;   // -1 - (local + poff)
-            c->leaves.push_back(d);
+    int cpar = -1, cnb[9];   // the last C/F parent's 3 x 3 neighbourhood
+    for (int id : c->leaf_ids) {
+        LeafDesc d{};
+        d.slot = id;
+        d.level = t.lev[id];
+        d.cf = 0;
+        RefluxTask rt{};
+        rt.leaf = (int)c->leaves.size();
+        rt.slot = id;
+        rt.level = t.lev[id];
+        rt.mask = 0;
+        for (int s = 0; s < 4; ++s) {
+            int nb = c->nb4[(size_t)4 * id + s];
+            if (nb >= 0) {
+                d.side[s] = nb;
+                if (c->comm.world > 1 && c->comm.halo_mode == 2 && c->comm.owner[nb] != c->comm.rank)
+                    d.pad |= (16 << s) | (c->comm.owner[nb] << (8 + 3 * s));   // strip read from the owner's pool
+                if (t.has_children(nb)) {
+                    d.cf |= 1 << s;
+                    rt.mask |= 1 << s;
+                    // the two children of nb adjacent to the shared face, ordered along it
+                    int cidx[2];
+                    if (s == kW) { cidx[0] = 1; cidx[1] = 3; }
+                    else if (s == kE) { cidx[0] = 0; cidx[1] = 2; }
+                    else if (s == kS) { cidx[0] = 2; cidx[1] = 3; }
+                    else { cidx[0] = 0; cidx[1] = 1; }
+                    for (int h = 0; h < 2; ++h) {
+                        int ch = t.child[4 * nb + cidx[h]];
+                        if (ch < 0 || !t.is_leaf(ch)) return fail(c, AMR_E_MESH, "reflux: fine side is not a leaf");
+                        rt.fine[s][h] = ch;
+                    }
+                }
+            } else {
+                ProxyTask p{};
+                p.proxy = (int)c->ptasks.size();
+                p.slot = id;
+                p.side = s;
+                p.level = t.lev[id];
+                p.P = t.pi[id];
+                p.Q = t.pj[id];
+                if (nb == -2) {
+                    p.kind = 0;
+                    for (int q = 0; q < 9; ++q) p.coarse[q] = -1;
+                } else {
+                    p.kind = 1;
+                    d.cf |= 1 << (4 + s);
+                    int par = t.parent[id];
+                    if (par < 0) return fail(c, AMR_E_MESH, "missing same-level neighbour of a root");
+                    if (par != cpar) {   // siblings are consecutive in Morton order: one 3 x 3 lookup per parent
+                        cpar = par;
+                        for (int dy = -1; dy <= 1; ++dy)
+                            for (int dx = -1; dx <= 1; ++dx) {
+                                int q = nbr(par, dx, dy);
+                                if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
+                                cnb[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
+                            }
+                    }
+                    for (int q = 0; q < 9; ++q) p.coarse[q] = cnb[q];
+                }
+                d.side[s] = -1 - p.proxy;
+                c->ptasks.push_back(p);
+            }
         }
-        for (ProxyTask p : ch.ptasks) {
-            p.proxy += poff;
-            c->ptasks.push_back(p);
-        }
-        for (RefluxTask r : ch.rtasks) {
-            r.leaf += loff;
-            c->rtasks.push_back(r);
-        }
+        c->leaves.push_back(d);
+        if (rt.mask) c->rtasks.push_back(rt);
     }
     clk.mark("plan: leaf descriptors");
     c->rlev.assign(L, {});

@@ -17,19 +17,17 @@ template <class T>
 struct DevArray {
     T* p = nullptr;
     size_t cap = 0, count = 0;
-    T* host = nullptr;         // pinned mirror of the last upload: the copy is a true async DMA (a pageable source
-    size_t hcap = 0;           // makes every cudaMemcpyAsync a staged, blocking copy of ~10 us)
     DevArray() = default;
     DevArray(const DevArray&) = delete;
     DevArray& operator=(const DevArray&) = delete;
-    DevArray(DevArray&& o) noexcept : p(o.p), cap(o.cap), count(o.count), host(o.host), hcap(o.hcap) {
-        o.p = nullptr; o.host = nullptr; o.cap = o.count = o.hcap = 0;
+    DevArray(DevArray&& o) noexcept : p(o.p), cap(o.cap), count(o.count) {
+        o.p = nullptr; o.cap = o.count = 0;
     }
     DevArray& operator=(DevArray&& o) noexcept {
         if (this != &o) {
             release();
-            p = o.p; cap = o.cap; count = o.count; host = o.host; hcap = o.hcap;
-            o.p = nullptr; o.host = nullptr; o.cap = o.count = o.hcap = 0;
+            p = o.p; cap = o.cap; count = o.count;
+            o.p = nullptr; o.cap = o.count = 0;
         }
         return *this;
     }
@@ -44,20 +42,7 @@ struct DevArray {
             if (e != cudaSuccess) { cap = 0; return e; }
         }
         if (v.empty()) return cudaSuccess;
-        if (v.size() > hcap) {
-            if (host) cudaFreeHost(host);
-            host = nullptr;
-            hcap = std::max<size_t>(v.size() + v.size() / 2, 16);
-            cudaError_t e = cudaMallocHost(&host, hcap * sizeof(T));
-            if (e != cudaSuccess) { hcap = 0; return e; }
-        } else {
-            // the previous upload from the mirror must have left it (uploads happen at regrid, which synchronises
-            // the stream at its end; this is a no-op then)
-            cudaError_t e = cudaStreamSynchronize(s);
-            if (e != cudaSuccess) return e;
-        }
-        std::copy(v.begin(), v.end(), host);
-        return cudaMemcpyAsync(p, host, v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+        return cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
     }
     // grows with 50 % slack (a proxy count growing by one must not re-allocate); slack = false for arrays sized
     // by the fixed slot capacity
@@ -72,10 +57,8 @@ struct DevArray {
     }
     void release() {
         if (p) cudaFree(p);
-        if (host) cudaFreeHost(host);
         p = nullptr;
-        host = nullptr;
-        cap = count = hcap = 0;
+        cap = count = 0;
     }
 };
 
@@ -136,9 +119,9 @@ struct amr_ctx {
     unsigned long long* d_tmp = nullptr;
     void* h_pinned = nullptr;   // {int32 err[4]; double dt}
     bool lambda_valid = false;
-    bool ghost_valid = false;
+    bool ghost_valid = false;      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
     double sim_time_fix = 0.0;     // host correction of the device time sum (rolled-back steps)
-    std::vector<int32_t> nb4;      // face neighbours W, E, S, N of every slot (PatchTree::face_neighbours)      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
+    std::vector<int32_t> nb4;      // face neighbours W, E, S, N of every slot (PatchTree::face_neighbours)
     double last_dt = 0.0;
 
     // flags of the last evaluation, per id

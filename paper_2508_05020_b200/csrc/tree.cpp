@@ -293,8 +293,7 @@ std::vector<int32_t> PatchTree::canonical() const {
     return ids;
 }
 
-void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4,
-                                const std::function<void(int, const std::function<void(int)>&)>& par) const {
+void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4) const {
     if (nb4.size() != (size_t)4 * capacity) nb4.assign((size_t)4 * capacity, -1);
     static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
     auto one = [&](int id) {
@@ -320,23 +319,7 @@ void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<i
         o[2] = b == 1 ? pa.child[a] : across(2, a + 2);
         o[3] = b == 0 ? pa.child[a + 2] : across(3, a);
     };
-    // level by level (a level reads only its parents' entries)
-    for (size_t b0 = 0; b0 < canon.size();) {
-        size_t b1 = b0;
-        const int l = node_[canon[b0]].lev;
-        while (b1 < canon.size() && node_[canon[b1]].lev == l) ++b1;
-        const size_t cnt = b1 - b0;
-        const int nchunk = par ? (int)std::max<size_t>(1, std::min<size_t>(16, cnt / 2048)) : 1;
-        if (nchunk == 1) {
-            for (size_t e = b0; e < b1; ++e) one(canon[e]);
-        } else {
-            par(nchunk, [&](int k) {
-                const size_t e0 = b0 + cnt * k / nchunk, e1 = b0 + cnt * (k + 1) / nchunk;
-                for (size_t e = e0; e < e1; ++e) one(canon[e]);
-            });
-        }
-        b0 = b1;
-    }
+    for (int id : canon) one(id);   // level-major: a patch's parent is done before it
 }
 
 std::vector<int32_t> PatchTree::canonical_sorted() const {

@@ -206,9 +206,7 @@ struct PatchTree {
     }
     // face neighbours W, E, S, N of every active patch (nb4[4 id + s]: id, -1 missing, -2 outside the domain), top
     // down over `canon` (level-major) from the parents' entries: equal to neighbour(id, +-1 / 0) without recursion
-    // par(n, f): optional parallel runner (f(k) for k < n; chunks of one level are independent)
-    void face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4,
-                         const std::function<void(int, const std::function<void(int)>&)>& par = nullptr) const;
+    void face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4) const;
 
     // Transactions (regrid is atomic): between begin_txn() and commit()/rollback() every modified slot
     // is journaled once with its prior state, so a failed regrid is undone in O(changes) -- no copy of the
