@@ -53,11 +53,15 @@ def fp64_peak():
     return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SM x 64 DFMA/clk x 2 x 1.965 GHz)"
 
 
-def fp64_work(kernel):
-    """fp64 SASS work per leaf cell-stage of a stage kernel, counted by ncu (profiles/r1f_fp64_work.json)."""
-    p = os.path.join(ROOT, "profiles", "r1f_fp64_work.json")
+def fp64_work(kernel, n=None):
+    """fp64 SASS work per leaf cell-stage of a stage kernel (kernel "weno5_char" / "central4" at patch size n, whose
+    launch configuration differs), counted by ncu (profiles/r2_fp64_work.json, scripts/profile_r2.sh)."""
+    p = os.path.join(ROOT, "profiles", "r2_fp64_work.json")
     d = json.load(open(p)) if os.path.exists(p) else {}
-    return d.get(kernel, {"fp64_thread_inst_per_cell_stage": float("nan"), "flops_per_cell_stage": float("nan")})
+    nan = {"fp64_thread_inst_per_cell_stage": float("nan"), "flops_per_cell_stage": float("nan")}
+    if n is not None and f"{kernel}_n{min(n, 32)}" in d:
+        return d[f"{kernel}_n{min(n, 32)}"]
+    return d.get(kernel, nan)
 
 
 class Clocks:
@@ -379,7 +383,7 @@ def measure_sweep_table(X, args, hbm_peak):
             row = {"N": N, "n": n, "scheme": scheme if scheme == "central4" else ("weno5_char" if char else "weno5_comp"),
                    "stage_ms": ms, "cell_updates_per_s": cells / (ms / 1e3), "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak}
             if scheme == "weno5" and char:   # fp64-issue bound: SASS instruction count of the WENO5-char kernel
-                row["fp64_issue_frac"] = fp64_work("weno5_char")["fp64_thread_inst_per_cell_stage"] * row["cell_updates_per_s"] / fpk_inst
+                row["fp64_issue_frac"] = fp64_work("weno5_char", n)["fp64_thread_inst_per_cell_stage"] * row["cell_updates_per_s"] / fpk_inst
             rows.append(row)
         del U0
         torch.cuda.empty_cache()
@@ -484,7 +488,7 @@ def main():
         wcfg, _ = sweep_cfg(args, X.world, "weno5", 1)
         wr = measure_sweep(X, args, wcfg, max(3, args.steps // 2), 2, False)
         fpk, fpk_kind = fp64_peak()
-        work = fp64_work("weno5_char")
+        work = fp64_work("weno5_char", args.n)
         rate = wr["cells_per_launch"] / (wr["stage_avg_ms"] / 1e3)          # cell-stages/s of the stage kernel
         inst_peak = 148 * 64 * 1.965e9 / 1e12                                  # T fp64 thread-inst/s (unit counts)
         extra["weno5_char"] = {
@@ -514,8 +518,8 @@ def main():
                 "configs[3] with time subcycling: 8 level-0 steps (each = 8 finest-level steps), 2 regrids")
     if not args.no_sweep_table and X.world == 1:
         extra["sweep_table"] = {"workload": "BASELINE configs[4]: stage kernel per total size and patch size (Central4 at "
-                                            "4096^2..16384^2; WENO5 char / comp at 4096^2; fp64_issue_frac from the "
-                                            "n = 32 WENO5-char SASS count)",
+                                            "4096^2..16384^2; WENO5 char / comp at 4096^2; fp64_issue_frac from each "
+                                            "WENO5-char kernel's own SASS fp64 count, profiles/r2_fp64_work.json)",
                                 "rows": measure_sweep_table(X, args, hbm_peak)}
     if X.rank == 0:
         rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",

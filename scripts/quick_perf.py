@@ -43,7 +43,7 @@ def stage_time(X, n, scheme, char, N=4096, steps=3):
     if scheme == "central4":
         out["hbm_frac"] = round(rate * bench.BYTES_PER_CELL_STAGE / 1e9 / bench.peaks()[0], 4)
     elif char:
-        out["fp64_issue_frac"] = round(bench.fp64_work("weno5_char")["fp64_thread_inst_per_cell_stage"] * rate /
+        out["fp64_issue_frac"] = round(bench.fp64_work("weno5_char", n)["fp64_thread_inst_per_cell_stage"] * rate /
                                        (148 * 64 * 1.965e9), 4)
     return out
 
