@@ -27,7 +27,11 @@ amr_status amr_plan_tree(amr_plan* p, int32_t world_size, amr_patch_desc* out, i
 /* Exchange lists of `rank`: kind 0 halo (per stage), 1 flux registers; subcycling (plan_subcycle) for level l:
  * kind 2 + 3 l face halo of a level-l stage, 3 + 3 l coarse sources of its C/F ghosts, 4 + 3 l accumulated
  * registers of the fine leaves its reflux reads.  counts_*[world] per peer;
- * the index arrays hold the peers' lists back to back (capacity cap each). */
+ * the index arrays hold the peers' lists back to back (capacity cap each).  The halo lists (kind 0 and the
+ * subcycling face lists) move BAND ITEMS -- the 4-wide strip of a face neighbour facing the reader, whole patches
+ * (all row bands) of coarse sources -- and are reported as the distinct tree indices they touch; kind + 1000 reports
+ * the items themselves as tree_index * 32 + code (code < 16: row band 4 code .. 4 code + 3; 16: columns 0..3;
+ * 17: columns n-4..n-1). */
 amr_status amr_plan_exchange(amr_plan* p, int32_t world_size, int32_t rank, int32_t kind, int32_t* send_counts,
                              int32_t* send_index, int32_t* recv_counts, int32_t* recv_index, int32_t cap);
 

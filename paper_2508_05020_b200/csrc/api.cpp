@@ -1217,7 +1217,7 @@ struct SubRun {
     // same sequence of collective exchanges, whether or not it owns patches of the level)
     bool has_level(int l) const { return l < L && l < c->sub_levels; }
     amr_status xchg(const ExchangeLists& x, double* buf, int per, const char* what) {
-        return c->comm.world > 1 ? c->comm.exchange_lists(c, x, buf, per, what) : AMR_OK;
+        return c->comm.world > 1 ? c->comm.exchange_lists(c, x, buf, per, what, true) : AMR_OK;   // (plan lists)
     }
 
     amr_status advance(int l, bool final, int sub_i) {

@@ -78,35 +78,41 @@ std::vector<int32_t> partition_owners(const PatchTree& t, int world) {
     return owner;
 }
 
-void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out, bool faces) {
+void halo_sources(const PatchTree& t, int id, int n, std::vector<int32_t>& out, bool faces) {
     out.clear();
+    const int nb4 = n / 4;
+    auto whole = [&](int q) { for (int b = 0; b < nb4; ++b) out.push_back(q * 32 + b); };
+    // of the neighbour on side s (W, E, S, N of id) the strip facing id: its E columns, W columns, N rows, S rows
+    const int facing[4] = {kBandE, kBandW, nb4 - 1, 0};
     for (int s = 0; s < 4; ++s) {
         int nb = t.neighbour(id, kSideDir[s][0], kSideDir[s][1]);
         if (nb >= 0) {
-            if (faces) out.push_back(nb);
+            if (faces) out.push_back(nb * 32 + facing[s]);
         } else if (nb == -1) {
             int par = t.parent[id];
             if (par < 0) continue;
             for (int dy = -1; dy <= 1; ++dy)
                 for (int dx = -1; dx <= 1; ++dx) {
                     int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
-                    if (q >= 0) out.push_back(q);
+                    if (q >= 0) whole(q);
                 }
         }
     }
 }
 
-ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, bool faces) {
+ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n, bool faces) {
     std::vector<std::map<int, std::set<int32_t>>> need(world);
     std::vector<int32_t> src;
     for (int id = 0; id < t.capacity; ++id) {
         if (!t.is_leaf(id)) continue;
         int o = owner[id];
-        halo_sources(t, id, src, faces);
+        halo_sources(t, id, n, src, faces);
         for (int q : src)
-            if (owner[q] != o) need[o][owner[q]].insert(q);
+            if (owner[q >> 5] != o) need[o][owner[q >> 5]].insert(q);
     }
-    return from_needs(need, world, rank);
+    ExchangeLists L = from_needs(need, world, rank);
+    L.items = true;
+    return L;
 }
 
 ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank) {
@@ -141,7 +147,7 @@ ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_ne
     return from_needs(need, world, rank);
 }
 
-SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank) {
+SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n) {
     static const int cidx[4][2] = {{1, 3}, {0, 2}, {2, 3}, {0, 1}};   // children of a W/E/S/N neighbour on the face
     const int L = t.levels;
     std::vector<std::vector<std::map<int, std::set<int32_t>>>> face(L), coarse(L), facc(L);
@@ -157,7 +163,9 @@ SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, in
         for (int s = 0; s < 4; ++s) {
             const int nb = t.neighbour(id, kSideDir[s][0], kSideDir[s][1]);
             if (nb >= 0) {
-                if (owner[nb] != o) face[l][o][owner[nb]].insert(nb);
+                // the strip of nb facing id (band item, as plan_halo)
+                const int facing[4] = {kBandE, kBandW, n / 4 - 1, 0};
+                if (owner[nb] != o) face[l][o][owner[nb]].insert(nb * 32 + facing[s]);
                 if (leaf && t.has_children(nb))
                     for (int h = 0; h < 2; ++h) {
                         const int f = t.child[4 * nb + cidx[s][h]];
@@ -177,6 +185,7 @@ SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, in
     SubLists out;
     for (int l = 0; l < L; ++l) {
         out.face.push_back(from_needs(face[l], world, rank));
+        out.face.back().items = true;
         out.coarse.push_back(from_needs(coarse[l], world, rank));
         out.facc.push_back(from_needs(facc[l], world, rank));
     }
@@ -556,6 +565,7 @@ Comm::Comm() = default;
 Comm::~Comm() = default;
 
 amr_status Comm::init(amr_ctx* c) {
+    n = c->n;
     world = c->cfg.world_size;
     rank = c->cfg.rank;
     halo_mode = c->cfg.halo_mode;
@@ -620,6 +630,7 @@ amr_status Comm::init(amr_ctx* c) {
 }
 
 void Comm::finalize(amr_ctx*) {
+    free_dev_lists();
     for (PullList* P : {&pull_halo, &pull_flux, &pull_halo_cf})
         if (P->slots) { cudaFree(P->slots); cudaFree(P->peers); P->slots = P->peers = nullptr; }
     if (d_pool_bases) cudaFree(d_pool_bases);
@@ -632,34 +643,67 @@ void Comm::repartition(const PatchTree& t) { owner = partition_owners(t, world);
 
 void Comm::replan(const PatchTree& t) {
     if (world == 1) return;
-    halo = plan_halo(t, owner, world, rank);
+    free_dev_lists();
+    halo = plan_halo(t, owner, world, rank, n);
     flux = plan_flux(t, owner, world, rank);
-    if (halo_mode == 2) halo_cf = plan_halo(t, owner, world, rank, false);
-    if (subcycle) sub = plan_subcycle(t, owner, world, rank);
+    if (halo_mode == 2) halo_cf = plan_halo(t, owner, world, rank, n, false);
+    if (subcycle) sub = plan_subcycle(t, owner, world, rank, n);
     ++lists_version;
 }
 
-amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per, const char* what) {
+void Comm::free_dev_lists() {
+    for (auto& kv : dev_lists) {
+        if (kv.second.send) cudaFree(kv.second.send);
+        if (kv.second.recv) cudaFree(kv.second.recv);
+    }
+    dev_lists.clear();
+}
+
+amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per, const char* what,
+                                bool persistent) {
     if (world == 1) return AMR_OK;
     NvtxRange nv(what);
+    if (L.items) per = 16 * n;   // a band item: 4 variables x 4 n cells
     size_t ns = L.nsend(), nr = L.nrecv();
-    std::vector<int32_t> sidx, ridx;
-    sidx.reserve(ns);
-    ridx.reserve(nr);
-    for (auto& v : L.send) sidx.insert(sidx.end(), v.begin(), v.end());
-    for (auto& v : L.recv) ridx.insert(ridx.end(), v.begin(), v.end());
     cudaStream_t s = c->stream;
-    if (c->x_sidx.upload(sidx, s) != cudaSuccess || c->x_ridx.upload(ridx, s) != cudaSuccess ||
-        c->x_send.reserve(std::max<size_t>(1, ns * per)) != cudaSuccess ||
-        c->x_recv.reserve(std::max<size_t>(1, nr * per)) != cudaSuccess) {
-        c->err = std::string(what) + ": exchange buffers";
-        c->sticky = AMR_E_CUDA;
-        return AMR_E_CUDA;
+    auto bad = [&](amr_status st, const std::string& m) { c->err = std::string(what) + ": " + m; c->sticky = st; return st; };
+    const int32_t *dsidx = nullptr, *dridx = nullptr;
+    DevLists* dl = persistent ? &dev_lists[&L] : nullptr;
+    if (dl && dl->version == lists_version) {   // index lists already on the device (this plan)
+        dsidx = dl->send;
+        dridx = dl->recv;
+    } else {
+        std::vector<int32_t> sidx, ridx;
+        sidx.reserve(ns);
+        ridx.reserve(nr);
+        for (auto& v : L.send) sidx.insert(sidx.end(), v.begin(), v.end());
+        for (auto& v : L.recv) ridx.insert(ridx.end(), v.begin(), v.end());
+        if (dl) {
+            if (dl->send) cudaFree(dl->send);
+            if (dl->recv) cudaFree(dl->recv);
+            dl->send = dl->recv = nullptr;
+            if ((ns && cudaMalloc(&dl->send, ns * 4) != cudaSuccess) || (nr && cudaMalloc(&dl->recv, nr * 4) != cudaSuccess))
+                return bad(AMR_E_CUDA, "index lists");
+            if ((ns && h2d_sync(dl->send, sidx.data(), ns * 4, s) != cudaSuccess) ||
+                (nr && h2d_sync(dl->recv, ridx.data(), nr * 4, s) != cudaSuccess))
+                return bad(AMR_E_CUDA, "index lists upload");
+            dl->version = lists_version;
+            dsidx = dl->send;
+            dridx = dl->recv;
+        } else {
+            if (c->x_sidx.upload(sidx, s) != cudaSuccess || c->x_ridx.upload(ridx, s) != cudaSuccess)
+                return bad(AMR_E_CUDA, "exchange lists");
+            dsidx = c->x_sidx.p;
+            dridx = c->x_ridx.p;
+        }
     }
-    if (ns && launch_gather(U, c->x_sidx.p, (int)ns, c->x_send.p, per, s) != cudaSuccess) {
-        c->err = std::string(what) + ": pack";
-        c->sticky = AMR_E_CUDA;
-        return AMR_E_CUDA;
+    if (c->x_send.reserve(std::max<size_t>(1, ns * per)) != cudaSuccess ||
+        c->x_recv.reserve(std::max<size_t>(1, nr * per)) != cudaSuccess)
+        return bad(AMR_E_CUDA, "exchange buffers");
+    if (ns) {
+        cudaError_t e = L.items ? launch_band_gather(U, dsidx, (int)ns, c->x_send.p, n, s)
+                                : launch_gather(U, dsidx, (int)ns, c->x_send.p, per, s);
+        if (e != cudaSuccess) return bad(AMR_E_CUDA, "pack");
     }
     std::vector<Xfer> sends, recvs;
     size_t so = 0, ro = 0;
@@ -670,16 +714,12 @@ amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, i
         ro += L.recv[p].size();
     }
     std::string e = tr->p2p(sends, recvs, s);
-    if (!e.empty()) {
-        c->err = std::string(what) + ": " + e;
-        c->sticky = AMR_E_COMM;
-        return AMR_E_COMM;
-    }
+    if (!e.empty()) return bad(AMR_E_COMM, e);
     bytes_sent += (int64_t)(ns * per * sizeof(double));
-    if (nr && launch_scatter(c->x_recv.p, c->x_ridx.p, (int)nr, U, per, s) != cudaSuccess) {
-        c->err = std::string(what) + ": unpack";
-        c->sticky = AMR_E_CUDA;
-        return AMR_E_CUDA;
+    if (nr) {
+        cudaError_t e2 = L.items ? launch_band_scatter(c->x_recv.p, dridx, (int)nr, U, n, s)
+                                 : launch_scatter(c->x_recv.p, dridx, (int)nr, U, per, s);
+        if (e2 != cudaSuccess) return bad(AMR_E_CUDA, "unpack");
     }
     c->st.launches += (ns ? 1 : 0) + (nr ? 1 : 0);
     return AMR_OK;
@@ -687,7 +727,7 @@ amr_status Comm::exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, i
 
 amr_status Comm::exchange_halos(amr_ctx* c, double* U) {
     if (world > 1 && halo_mode >= 1) return peer_pull(c, halo, pull_halo, U, false, "halo pull");
-    return exchange_lists(c, halo, U, (int)c->PS, "halo exchange");
+    return exchange_lists(c, halo, U, (int)c->PS, "halo exchange", true);
 }
 
 amr_status Comm::exchange_halos_stage(amr_ctx* c, double* U) {
@@ -697,7 +737,7 @@ amr_status Comm::exchange_halos_stage(amr_ctx* c, double* U) {
 
 amr_status Comm::exchange_fluxes(amr_ctx* c) {
     if (world > 1 && halo_mode >= 1) return peer_pull(c, flux, pull_flux, c->freg.p, true, "flux-register pull");
-    return exchange_lists(c, flux, c->freg.p, 16 * c->n, "flux-register exchange");
+    return exchange_lists(c, flux, c->freg.p, 16 * c->n, "flux-register exchange", true);
 }
 
 amr_status Comm::map_pool(amr_ctx* c, void* base, size_t bytes) {
@@ -744,11 +784,13 @@ amr_status Comm::peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, doub
     }
     std::string e = tr->fence(c->stream);
     if (!e.empty()) return bad(AMR_E_COMM, e);
-    const int per = freg ? 16 * c->n : (int)c->PS;
+    const int per = L.items ? 16 * c->n : (freg ? 16 * c->n : (int)c->PS);
     const size_t off = freg ? 0 : (size_t)(dst - (double*)pool_base);
     if (P.n) {
-        if (launch_peer_pull(P.slots, P.peers, P.n, freg ? d_freg_bases : d_pool_bases, off, dst, per, c->stream) != cudaSuccess)
-            return bad(AMR_E_CUDA, "pull kernel");
+        cudaError_t ce = L.items ? launch_band_pull(P.slots, P.peers, P.n, d_pool_bases, off, dst, c->n, c->stream)
+                                 : launch_peer_pull(P.slots, P.peers, P.n, freg ? d_freg_bases : d_pool_bases, off, dst,
+                                                    per, c->stream);
+        if (ce != cudaSuccess) return bad(AMR_E_CUDA, "pull kernel");
         c->st.launches += 1;
         bytes_sent += (int64_t)P.n * per * (int64_t)sizeof(double);   // bytes moved into this rank
     }

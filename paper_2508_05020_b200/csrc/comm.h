@@ -11,6 +11,7 @@
 // in-process loopback (virtual ranks as host threads on one GPU; test-only).
 #pragma once
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <vector>
 
@@ -21,9 +22,14 @@ struct amr_ctx;
 
 namespace amr {
 
-// per-peer slot lists (sorted); send[r]: my slots that rank r needs; recv[r]: slots owned by r I need
+// per-peer slot lists (sorted); send[r]: my slots that rank r needs; recv[r]: slots owned by r I need.
+// items = true: the entries are BAND ITEMS, slot * 32 + code -- the g-wide strips a halo reader needs instead of whole
+// patches: code < 16 the row band 4 code .. 4 code + 3 (code 0 = the S strip, n/4 - 1 = the N
+// strip), 16 the W strip (columns 0..3), 17 the E strip (columns n-4..n-1); a whole patch is its n/4 row bands
+constexpr int kBandW = 16, kBandE = 17;
 struct ExchangeLists {
     std::vector<std::vector<int32_t>> send, recv;
+    bool items = false;
     void reset(int world) { send.assign(world, {}); recv.assign(world, {}); }
     size_t nsend() const { size_t s = 0; for (auto& v : send) s += v.size(); return s; }
     size_t nrecv() const { size_t s = 0; for (auto& v : recv) s += v.size(); return s; }
@@ -31,10 +37,12 @@ struct ExchangeLists {
 
 // ---- pure host planning (no CUDA): testable on CPU
 std::vector<int32_t> partition_owners(const PatchTree& t, int world);
-// slots read by the stage / flags / ghost kernels of leaf `id` that may live on another rank
-// (faces = false: only the coarse sources of C/F ghost strips -- halo_mode 2 reads face neighbours in the stage kernel)
-void halo_sources(const PatchTree& t, int id, std::vector<int32_t>& out, bool faces = true);
-ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, bool faces = true);
+// band items read by the stage / flags / ghost kernels of leaf `id` that may live on another rank (patch size n): of a
+// face neighbour the strip facing id, of a coarse source of a C/F ghost strip (the parent's 3 x 3 neighbourhood) the
+// whole patch (faces = false: only the coarse sources -- halo_mode 2 reads face strips in the stage kernel)
+void halo_sources(const PatchTree& t, int id, int n, std::vector<int32_t>& out, bool faces = true);
+ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n,
+                        bool faces = true);
 ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
 // coarse sources of new level-l patches prolonged by the (old) owner of their root
 ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_new, int level,
@@ -46,7 +54,7 @@ ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_ne
 struct SubLists {
     std::vector<ExchangeLists> face, coarse, facc;
 };
-SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
+SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n);
 ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& old_owner,
                              const std::vector<int32_t>& new_owner, int world, int rank);
 
@@ -54,6 +62,7 @@ struct Transport;
 
 struct Comm {
     int world = 1, rank = 0;
+    int n = 0;                         // patch size (band items)
     std::unique_ptr<Transport> tr;
     std::vector<int32_t> owner;        // per slot (patch id); -1 for free slots
     ExchangeLists halo, flux, halo_cf;
@@ -90,7 +99,16 @@ struct Comm {
     // before a stage kernel: halo_mode 2 pulls only the C/F coarse sources (face strips are read in the kernel)
     amr_status exchange_halos_stage(amr_ctx* c, double* U);
     amr_status exchange_fluxes(amr_ctx* c);
-    amr_status exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per_slot, const char* what);
+    // persistent = true: L lives until the next replan, so its index lists stay on the device (keyed by &L)
+    amr_status exchange_lists(amr_ctx* c, const ExchangeLists& L, double* U, int per_slot, const char* what,
+                              bool persistent = false);
+    struct DevLists {
+        uint64_t version = ~0ull;
+        int32_t *send = nullptr, *recv = nullptr;
+        size_t ns = 0, nr = 0;
+    };
+    std::map<const ExchangeLists*, DevLists> dev_lists;   // per-plan index lists on the device (freed at replan)
+    void free_dev_lists();
     amr_status exchange_children(amr_ctx*, double*) { return AMR_OK; }   // root-tree ownership: local
     amr_status map_pool(amr_ctx* c, void* base, size_t bytes);   // collective (amr_create)
     amr_status peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, double* dst, bool freg, const char* what);

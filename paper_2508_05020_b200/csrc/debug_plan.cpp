@@ -12,6 +12,7 @@
 struct amr_plan {
     amr::PatchTree tree;
     int levels = 1;
+    int n = 8;
 };
 
 namespace {
@@ -36,6 +37,7 @@ amr_status amr_plan_create(const amr_config* cfg, amr_plan** out) {
     if ((int64_t)npx * npy > c.max_patches) return AMR_E_CAPACITY;
     amr_plan* p = new amr_plan();
     p->levels = c.num_levels;
+    p->n = n;
     p->tree.init(npx, npy, c.num_levels, c.bc[0] == AMR_BC_PERIODIC, c.bc[2] == AMR_BC_PERIODIC, c.max_patches,
                  c.coarsen_rule);
     *out = p;
@@ -129,26 +131,43 @@ amr_status amr_plan_exchange(amr_plan* p, int32_t world, int32_t rank, int32_t k
     std::vector<int32_t> canon;
     std::vector<int32_t> pos = canon_pos_of(p->tree, canon);
     std::vector<int32_t> owner = amr::partition_owners(p->tree, world);
+    const bool raw = kind >= 1000;   // raw band items (tree index * 32 + code) instead of the slots they touch
+    if (raw) kind -= 1000;
     amr::ExchangeLists L;
-    if (kind == 0) L = amr::plan_halo(p->tree, owner, world, rank);
+    if (kind == 0) L = amr::plan_halo(p->tree, owner, world, rank, p->n);
     else if (kind == 1) L = amr::plan_flux(p->tree, owner, world, rank);
     else {
         const int l = (kind - 2) / 3, which = (kind - 2) % 3;
         if (kind < 2 || l >= p->levels) return AMR_E_ARG;
-        amr::SubLists S = amr::plan_subcycle(p->tree, owner, world, rank);
+        amr::SubLists S = amr::plan_subcycle(p->tree, owner, world, rank, p->n);
         L = which == 0 ? S.face[l] : (which == 1 ? S.coarse[l] : S.facc[l]);
     }
+    // entries: slots (tree indices), or for band-item lists the distinct slots they touch (raw: the items)
+    auto listed = [&](const std::vector<int32_t>& v) {
+        std::vector<int32_t> o;
+        for (int x : v) {
+            if (!L.items) o.push_back(pos[x]);
+            else if (raw) o.push_back(pos[x >> 5] * 32 + (x & 31));
+            else if (o.empty() || o.back() != pos[x >> 5]) o.push_back(pos[x >> 5]);
+        }
+        if (L.items && !raw) {
+            std::sort(o.begin(), o.end());
+            o.erase(std::unique(o.begin(), o.end()), o.end());
+        }
+        return o;
+    };
     int ns = 0, nr = 0;
     for (int q = 0; q < world; ++q) {
-        send_counts[q] = (int32_t)L.send[q].size();
-        recv_counts[q] = (int32_t)L.recv[q].size();
-        for (int s : L.send[q]) {
+        std::vector<int32_t> sv = listed(L.send[q]), rv = listed(L.recv[q]);
+        send_counts[q] = (int32_t)sv.size();
+        recv_counts[q] = (int32_t)rv.size();
+        for (int x : sv) {
             if (ns >= cap) return AMR_E_ARG;
-            send_index[ns++] = pos[s];
+            send_index[ns++] = x;
         }
-        for (int s : L.recv[q]) {
+        for (int x : rv) {
             if (nr >= cap) return AMR_E_ARG;
-            recv_index[nr++] = pos[s];
+            recv_index[nr++] = x;
         }
     }
     return AMR_OK;

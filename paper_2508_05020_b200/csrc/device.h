@@ -177,6 +177,14 @@ cudaError_t launch_gather(const double* U, const int32_t* slots, int npatch, dou
 cudaError_t launch_peer_pull(const int32_t* slots, const int32_t* peers, int n, const double* const* bases,
                              size_t off, double* dst, int per, cudaStream_t s);
 
+// band items of the halo exchange (item = slot * 32 + code, comm.h): pack / unpack 16 n doubles per item between a
+// buffer of the pool (U) and a packed array; pull the same bands of the same buffer (offset off in every pool) from
+// each item's owner
+cudaError_t launch_band_scatter(const double* packed, const int32_t* items, int nitem, double* U, int n, cudaStream_t s);
+cudaError_t launch_band_gather(const double* U, const int32_t* items, int nitem, double* packed, int n, cudaStream_t s);
+cudaError_t launch_band_pull(const int32_t* items, const int32_t* peers, int nitem, const double* const* bases,
+                             size_t off, double* dst, int n, cudaStream_t s);
+
 // unfused stage (variant 2): scratch doubles for nleaves patches; kernel launches per stage of a variant
 size_t unfused_scratch_doubles(int n, int nleaves);
 int stage_launches_per_stage(int variant, int nleaves);

@@ -2765,6 +2765,62 @@ cudaError_t launch_peer_pull(const int32_t* slots, const int32_t* peers, int n, 
     return cudaGetLastError();
 }
 
+// Band items of the halo exchange (comm.h): item = slot * 32 + code; code < 16: rows 4 code .. 4 code + 3 (a row
+// band), 16: columns 0..3, 17: columns n-4..n-1; 16 n doubles each (4 variables x 4 n cells), in [var][band cell]
+// order.  The pool offset of element e of an item:
+__device__ __forceinline__ size_t band_offset(int32_t item, int e, int n) {
+    const size_t slot = (size_t)(item >> 5);
+    const int code = item & 31, per_var = 4 * n;
+    const int var = e / per_var, r = e - var * per_var;
+    int i, j;
+    if (code < 16) { j = 4 * code + r / n; i = r % n; }
+    else { j = r >> 2; i = (code == 16 ? 0 : n - 4) + (r & 3); }
+    return ((slot * 4 + var) * n + j) * (size_t)n + i;
+}
+__global__ void band_copy_kernel(const double* __restrict__ packed, const int32_t* __restrict__ items, long long total,
+                                 int n, double* __restrict__ U, int to_pool) {
+    const int per = 16 * n;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long k = t / per;
+        const size_t o = band_offset(items[k], (int)(t - k * per), n);
+        if (to_pool) U[o] = packed[t];
+        else const_cast<double*>(packed)[t] = U[o];
+    }
+}
+__global__ void band_pull_kernel(const int32_t* __restrict__ items, const int32_t* __restrict__ peers,
+                                 const double* const* __restrict__ bases, size_t off, double* __restrict__ dst, int n) {
+    const int32_t item = items[blockIdx.x];
+    const double* src = bases[peers[blockIdx.x]] + off;
+    for (int e = threadIdx.x; e < 16 * n; e += blockDim.x) {
+        const size_t o = band_offset(item, e, n);
+        dst[o] = src[o];   // the same band of the same slot and RK buffer in the owner's pool
+    }
+}
+
+cudaError_t launch_band_scatter(const double* packed, const int32_t* items, int nitem, double* U, int n, cudaStream_t s) {
+    if (nitem <= 0) return cudaSuccess;
+    const long long total = (long long)nitem * 16 * n;
+    unsigned blocks = grid_for(total, 256);
+    if (blocks > 148u * 64u) blocks = 148u * 64u;
+    band_copy_kernel<<<blocks, 256, 0, s>>>(packed, items, total, n, U, 1);
+    return cudaGetLastError();
+}
+cudaError_t launch_band_gather(const double* U, const int32_t* items, int nitem, double* packed, int n, cudaStream_t s) {
+    if (nitem <= 0) return cudaSuccess;
+    const long long total = (long long)nitem * 16 * n;
+    unsigned blocks = grid_for(total, 256);
+    if (blocks > 148u * 64u) blocks = 148u * 64u;
+    band_copy_kernel<<<blocks, 256, 0, s>>>(packed, items, total, n, const_cast<double*>(U), 0);
+    return cudaGetLastError();
+}
+cudaError_t launch_band_pull(const int32_t* items, const int32_t* peers, int nitem, const double* const* bases,
+                             size_t off, double* dst, int n, cudaStream_t s) {
+    if (nitem <= 0) return cudaSuccess;
+    band_pull_kernel<<<nitem, 128, 0, s>>>(items, peers, bases, off, dst, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(const double* packed, const int32_t* slots, int npatch, double* U, int per, cudaStream_t s) {
     if (npatch <= 0) return cudaSuccess;
     long long total = (long long)npatch * per;

@@ -109,6 +109,39 @@ def needed_sources(tree, rank, world_tree):
     return need
 
 
+def needed_bands(tree, rank, world_tree, n=8):
+    """Independent statement of the halo's band items (tree index * 32 + code): of a remote face neighbour the
+    4-wide strip facing the reader (W neighbour: its columns n-4..n-1 = code 17; E: columns 0..3 = 16; S: its top
+    row band n/4 - 1; N: its bottom row band 0), of a remote coarse source of a C/F side every row band (whole)."""
+    key = {(d.level, d.i, d.j): e for e, d in enumerate(world_tree)}
+    npx = {l: (128 // 8) << l for l in range(3)}
+    npy = {l: (64 // 8) << l for l in range(3)}
+    facing = {(-1, 0): 17, (1, 0): 16, (0, -1): n // 4 - 1, (0, 1): 0}
+    need = set()
+
+    def pos(l, i, j):
+        i %= npx[l]
+        if j < 0 or j >= npy[l]:
+            return None
+        return key.get((l, i, j))
+
+    for d in world_tree:
+        if not d.leaf or d.owner != rank:
+            continue
+        for dx, dy in SIDES:
+            q = pos(d.level, d.i + dx, d.j + dy)
+            if q is not None:
+                if world_tree[q].owner != rank:
+                    need.add(q * 32 + facing[(dx, dy)])
+            elif 0 <= d.j + dy < npy[d.level]:
+                for ddy in (-1, 0, 1):
+                    for ddx in (-1, 0, 1):
+                        c = pos(d.level - 1, d.i // 2 + ddx, d.j // 2 + ddy)
+                        if c is not None and world_tree[c].owner != rank:
+                            need.update(c * 32 + b for b in range(n // 4))
+    return need
+
+
 def needed_subcycle(tree, rank, levels=3):
     """Independent statement of the subcycled exchanges of `rank`: per level, remote same-level face
     neighbours of every owned active patch, remote coarse sources of owned leaves' C/F sides, remote fine leaves
@@ -157,13 +190,15 @@ def _worker(rank, world, port, q):
         p = build_plan()
         tr = p.tree(world)
         halo = dict(zip(("send", "recv"), p.exchange(world, rank, 0)))
+        bands = dict(zip(("send", "recv"), p.exchange(world, rank, 1000)))
         flux = dict(zip(("send", "recv"), p.exchange(world, rank, 1)))
         sub = {k: [dict(zip(("send", "recv"), p.exchange(world, rank, 2 + 3 * l + w))) for l in range(3)]
                for w, k in enumerate(("face", "coarse", "facc"))}
         ns = needed_subcycle(tr, rank)
         mine = {"rank": rank, "owner": [d.owner for d in tr], "halo": halo, "flux": flux, "sub": sub,
                 "sub_need": {k: [sorted(x) for x in v] for k, v in zip(("face", "coarse", "facc"), ns)},
-                "need": sorted(needed_sources(tr, rank, tr)),
+                "need": sorted(needed_sources(tr, rank, tr)), "bands": bands,
+                "need_bands": sorted(needed_bands(tr, rank, tr)),
                 "leaves": sum(1 for d in tr if d.leaf and d.owner == rank)}
         allv = [None] * world
         dist.all_gather_object(allv, mine)
@@ -224,6 +259,21 @@ def test_gloo_halo_covers_every_remote_read(gathered):
         assert all(r["owner"][q] == other for q in got)
 
 
+def test_gloo_halo_moves_only_the_strips_read(gathered):
+    """The halo exchange moves band items: exactly the facing 4-wide strip of every remote face neighbour and whole
+    patches only for remote coarse sources of C/F ghost strips; the sender's list is the receiver's."""
+    a, b = gathered
+    assert a["bands"]["send"][1] == b["bands"]["recv"][0] and b["bands"]["send"][0] == a["bands"]["recv"][1]
+    for r in gathered:
+        got = set(r["bands"]["recv"][1 - r["rank"]])
+        assert got == set(r["need_bands"])
+        codes = [x & 31 for x in got]
+        assert any(c >= 16 for c in codes) and any(c < 16 for c in codes)
+    # fewer cells than whole patches: 2 of the 8 x 8 patch's 4 bands-worth per strip
+    whole = 2 * len(a["need"])          # n/4 = 2 row bands per whole patch at n = 8
+    assert len(a["bands"]["recv"][1]) < whole
+
+
 def test_single_rank_has_no_exchange():
     p = build_plan()
     for kind in (0, 1):
@@ -244,6 +294,10 @@ def test_partition_weak_scaling_slabs():
         send, recv = p.exchange(world, 0, 0)
         # the square of rank 0 needs one row of 128 patches from each y-neighbour
         assert sum(len(v) for v in recv.values()) == 256   # two rows of 128 (periodic in y)
+        send, recv = p.exchange(world, 0, 1000)
+        # ... and of each of them only the 4-row strip facing it: 256 bands of 4 x 32 cells (1/8 of the patches)
+        items = [x for v in recv.values() for x in v]
+        assert len(items) == 256 and all((x & 31) in (0, 7) for x in items)
 
 
 @pytest.mark.parametrize("kind", ["face", "coarse", "facc"])
