@@ -117,10 +117,12 @@ typedef struct {
                                      exchange is a stream-ordered cross-rank fence (a one-word NCCL allreduce, or
                                      CUDA events between loopback streams) followed by ONE kernel that loads the
                                      needed slots from the owners' pools over NVLink into the local pool;
-                                     2 (Central4 TMA kernel: central4, patch_cells >= 32, stage_kernel 0, <= 8 ranks)
-                                     as 1, but the stage kernel itself loads the 4-wide face strips of remote
-                                     neighbours by TMA from the owners' pools, so before a stage only the coarse
-                                     sources of C/F ghosts are pulled (the halo transfer overlaps the compute).
+                                     2 (Central4 TMA kernel: central4, patch_cells >= 32, stage_kernel 0; or a WENO5
+                                     stage kernel, stage_kernel 0 / 1; <= 8 ranks) as 1, but the stage kernel itself
+                                     loads the 4-wide face strips of remote neighbours from the owners' pools (TMA /
+                                     cp.async over NVLink), so before a stage only the coarse sources of C/F ghosts
+                                     are pulled (the halo transfer overlaps the compute).  The halo lists of modes
+                                     0 / 1 move band items (the facing 4-wide strips), not whole patches.
                                      Regrid exchanges (coarse sources, migration, flags) use the transport in all
                                      modes */
     const amr_host_comm* host_comm;   /* comm_backend 2: the caller's collectives (kept alive until destroy) */

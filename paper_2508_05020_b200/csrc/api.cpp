@@ -78,9 +78,13 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
     if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }
     if (c.halo_mode < 0 || c.halo_mode > 2) { m = "halo_mode must be 0, 1 or 2"; return AMR_E_CONFIG; }
+    // halo_mode 2: the stage kernels that load remote face strips themselves -- the Central4 TMA kernel (n >= 32) and
+    // the WENO5 kernels (per-tile and n = 8 block tiles); <= 8 ranks (3-bit owner field of LeafDesc.pad)
     if (c.halo_mode == 2 && c.world_size > 1 &&
-        (c.scheme != AMR_CENTRAL4 || c.patch_cells < 32 || c.stage_kernel != 0 || c.world_size > 8)) {
-        m = "halo_mode 2 needs the Central4 TMA kernel (central4, patch_cells >= 32, stage_kernel 0) and <= 8 ranks";
+        (c.world_size > 8 ||
+         (c.scheme == AMR_CENTRAL4 ? (c.patch_cells < 32 || c.stage_kernel != 0) : (c.stage_kernel > 1)))) {
+        m = "halo_mode 2 needs the Central4 TMA kernel (central4, patch_cells >= 32, stage_kernel 0) or a WENO5 stage "
+            "kernel (stage_kernel 0 / 1), and <= 8 ranks";
         return AMR_E_CONFIG;
     }
     return AMR_OK;

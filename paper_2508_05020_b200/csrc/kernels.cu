@@ -284,6 +284,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// The stage-input buffer a same-level side neighbour is read from: the local one, or -- halo_mode 2, neighbour owned
+// by another rank (LeafDesc.pad bits 4 + s, owner in bits 8 + 3 s) -- that rank's pool mapped over NVLink, so the
+// face strip is loaded by this kernel from the owner's memory (no halo exchange before the stage)
+__device__ __forceinline__ const double* side_source(const StageArgs& a, const LeafDesc& d, int side) {
+    if (!(d.pad & (16 << side))) return a.Uin;
+    return a.peer_in[(d.pad >> (8 + 3 * side)) & 7];
+}
+
 // SCHEME 0: Central4; 1: WENO5 characteristic; 2: WENO5 component-wise.
 // One CTA per T x T tile of a leaf patch (T = n, or 32 for n = 64).
 template <int SCHEME, int T>
@@ -319,14 +327,15 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             else if (f < CB + CS) { int h = f - CB; j = h / (T / 2) - G; i = 2 * (h - (j + G) * (T / 2)); }
             else { int h = f - CB - CS; j = h / (T / 2); i = 2 * (h - j * (T / 2)); j += T; }
             int pi = tx * T + i, pj = ty * T + j;
-            int s = 0;
+            int s = 0, sd = -1;
             bool halo = true;
-            if (pi < 0) { s = d.side[kW]; pi += n; }
-            else if (pi >= n) { s = d.side[kE]; pi -= n; }
-            else if (pj < 0) { s = d.side[kS]; pj += n; }
-            else if (pj >= n) { s = d.side[kN]; pj -= n; }
+            if (pi < 0) { sd = kW; pi += n; }
+            else if (pi >= n) { sd = kE; pi -= n; }
+            else if (pj < 0) { sd = kS; pj += n; }
+            else if (pj >= n) { sd = kN; pj -= n; }
             else halo = false;
-            const double* base = !halo ? own : (s >= 0 ? a.Uin + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS);
+            if (halo) s = d.side[sd];
+            const double* base = !halo ? own : (s >= 0 ? side_source(a, d, sd) + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS);
             cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + (i + G)) * 8), base + k * nn + (size_t)pj * n + pi);
         }
         cp_async_wait_all();
@@ -1937,15 +1946,16 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
             else { int h = f - CB - CS; j = h / (T / 2); i = 2 * (h - j * (T / 2)); j += T; }
             const int mx = i < 0 ? 0 : (i >= T ? B - 1 : i / N), my = j < 0 ? 0 : (j >= T ? B - 1 : j / N);
             const LeafDesc& d = sD[mem(mx, my)];
-            int pi = i - mx * N, pj = j - my * N, sl = d.slot;
+            int pi = i - mx * N, pj = j - my * N, sl = d.slot, sd = -1;
             bool halo = true;
-            if (pi < 0) { sl = d.side[kW]; pi += N; }
-            else if (pi >= N) { sl = d.side[kE]; pi -= N; }
-            else if (pj < 0) { sl = d.side[kS]; pj += N; }
-            else if (pj >= N) { sl = d.side[kN]; pj -= N; }
+            if (pi < 0) { sd = kW; pi += N; }
+            else if (pi >= N) { sd = kE; pi -= N; }
+            else if (pj < 0) { sd = kS; pj += N; }
+            else if (pj >= N) { sd = kN; pj -= N; }
             else halo = false;
+            if (halo) sl = d.side[sd];
             const double* base = !halo ? a.Uin + (size_t)sl * PS
-                                       : (sl >= 0 ? a.Uin + (size_t)sl * PS : a.proxy + (size_t)(-1 - sl) * PS);
+                                       : (sl >= 0 ? side_source(a, d, sd) + (size_t)sl * PS : a.proxy + (size_t)(-1 - sl) * PS);
             cp_async16(sb + (uint32_t)((kq * PL + (j + G) * W + (i + G)) * 8), base + kq * NN + pj * N + pi);
         }
         cp_async_wait_all();

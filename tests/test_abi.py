@@ -78,7 +78,8 @@ def _cfg(lib, **kw):
     dict(halo_mode=3),
     dict(comm_backend=3),
     dict(world_size=2, rank=0, comm_backend=2),                      # host collectives missing
-    dict(world_size=2, rank=0, halo_mode=2, scheme=1, nccl_unique_id=1),   # halo_mode 2 is the Central4 TMA path
+    dict(world_size=2, rank=0, halo_mode=2, scheme=1, stage_kernel=2, nccl_unique_id=1),   # unfused: no in-kernel strips
+    dict(world_size=2, rank=0, halo_mode=2, scheme=0, patch_cells=16, nccl_unique_id=1),   # Central4 n < 32
 ])
 def test_invalid_config_rejected_without_device(lib, kw):
     c = _cfg(lib, **kw)

@@ -69,6 +69,7 @@ def _free_port():
 
 @pytest.mark.parametrize("name,halo_mode", [("uniform_c4_n32", 0), ("uniform_c4_n32", 1), ("uniform_c4_n32", 2),
                                             ("implosion_c4_amr_n32", 2), ("quadrant_weno_amr", 1),
+                                            ("quadrant_weno_amr", 2),
                                             ("noise_c4_n32", 0), ("noise_c4_n32", 2)])
 def test_two_processes_bitwise_equal_single_rank(name, halo_mode):
     import torch.multiprocessing as mp

@@ -86,10 +86,11 @@ CASES = {
 @pytest.mark.parametrize("case", list(CASES))
 def test_virtual_ranks_bitwise_equal_single_rank(case, world, halo_mode):
     """halo_mode 0: pack + transport copy + unpack; 1: peer pull (NEXT #3) from the other ranks' mapped pools;
-    2: the Central4 TMA stage kernel loads remote face strips from the owners' pools itself (n >= 32 only)."""
+    2: the stage kernel loads remote face strips from the owners' pools itself (Central4 TMA kernel, n >= 32; WENO5
+    per-tile and n = 8 block-tile kernels)."""
     cfg, steps, regrid = CASES[case]
-    if halo_mode == 2 and not (cfg["scheme"] == "central4" and cfg["n"] >= 32):
-        pytest.skip("halo_mode 2 is the Central4 TMA path")
+    if halo_mode == 2 and cfg["scheme"] == "central4" and cfg["n"] < 32:
+        pytest.skip("halo_mode 2: Central4 only through the TMA kernel (n >= 32); WENO5 kernels at every n")
     ref_state, ref_keys, ref_dts = run_single(cfg, steps, regrid)
     res = run_multi(dict(cfg, halo_mode=halo_mode), world, steps, regrid)
     merged = {}
