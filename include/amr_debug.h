@@ -35,6 +35,12 @@ amr_status amr_plan_tree(amr_plan* p, int32_t world_size, amr_patch_desc* out, i
 amr_status amr_plan_exchange(amr_plan* p, int32_t world_size, int32_t rank, int32_t kind, int32_t* send_counts,
                              int32_t* send_index, int32_t* recv_counts, int32_t* recv_index, int32_t cap);
 
+/* Host plan work of `rank` at a regrid (what every rank computes: partition, its own and boundary roots, leaf launch
+ * order, face-neighbour table, halo and flux-register lists), averaged over reps runs on this CPU.  ms[7]: partition,
+ * roots, leaf order, face neighbours, halo lists, flux lists, total (milliseconds); counts[4]: active patches,
+ * rank's leaves, halo items received, halo items sent.  Host only. */
+amr_status amr_plan_profile(amr_plan* p, int32_t world, int32_t rank, int32_t reps, double* ms, int64_t* counts);
+
 /* NCCL self-test (needs a GPU and torch's libnccl.so.2): a ONE-rank communicator from the 128-byte unique id
  * (amr_nccl_unique_id) drives the data path's NCCL transport -- grouped send/recv to self (the halo / flux /
  * migration exchange call pattern), the four allreduce kinds (Lambda max-u64, max-f64, sum-f64 totals, max-i32

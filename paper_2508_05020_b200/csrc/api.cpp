@@ -107,10 +107,11 @@ struct PhaseClock {
 // (launch order) and then its covered patches (pad bit 0; all same-level neighbours exist by R2) -- with proxies
 // of their own (C/F ghosts prolonged in time per stage, physical BC), the C/F register tasks of the level's
 // leaves, and per-level offsets of the reflux tasks (rtasks are in level-major leaf order).
+void ensure_canon(amr_ctx* c);
+
 amr_status build_subcycle_plan(amr_ctx* c) {
     const PatchTree& t = c->tree;
     const int L = c->cfg.num_levels;
-    static const int dirs[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
     c->sub_descs.clear();
     c->sub_ptasks.clear();
     c->acc_tasks.clear();
@@ -169,6 +170,7 @@ amr_status build_subcycle_plan(amr_ctx* c) {
         return AMR_OK;
     };
     size_t e = 0, r = 0, cp = 0;
+    ensure_canon(c);
     for (int l = 0; l < L; ++l) {
         c->sub_off[l] = (int32_t)c->sub_descs.size();
         c->sub_poff[l] = (int32_t)c->sub_ptasks.size();
@@ -196,44 +198,70 @@ amr_status build_subcycle_plan(amr_ctx* c) {
     return AMR_OK;
 }
 
+// The canonical (level, j, i) order and its inverse, computed on first use after a plan change: the ABI's tree indices
+// need them, the step / regrid path does not (O(active patches) on every rank otherwise)
+void ensure_canon(amr_ctx* c) {
+    if (c->canon_valid) return;
+    const PatchTree& t = c->tree;
+    if ((int)c->canon_pos.size() != t.capacity) c->canon_pos.assign(t.capacity, -1);
+    else for (int id : c->canon) c->canon_pos[id] = -1;
+    c->canon = t.canonical();
+    for (size_t e = 0; e < c->canon.size(); ++e) c->canon_pos[c->canon[e]] = (int)e;
+    c->canon_valid = true;
+}
+
 amr_status build_plan(amr_ctx* c) {
     NvtxRange nv("build_plan");
     PhaseClock clk;
     PatchTree& t = c->tree;
     const int L = c->cfg.num_levels;
+    c->canon_valid = false;   // the canonical order is rebuilt on demand (ensure_canon)
     // id -> position maps sized once; the previous plan's entries are cleared instead of refilling all slots
-    if ((int)c->canon_pos.size() != t.capacity) c->canon_pos.assign(t.capacity, -1);
-    else for (int id : c->canon) c->canon_pos[id] = -1;
     if ((int)c->leaf_pos.size() != t.capacity) c->leaf_pos.assign(t.capacity, -1);
     else for (int id : c->leaf_ids) c->leaf_pos[id] = -1;
     clk.mark("plan: reset maps");
-    c->canon = t.canonical();
-    clk.mark("plan: canonical");
-    for (size_t e = 0; e < c->canon.size(); ++e) c->canon_pos[c->canon[e]] = (int)e;
+    // this rank's roots (all of them on one rank) and the roots its patches read from across the partition
+    // boundary: every loop below is over their subtrees, O(local)
+    const std::vector<int32_t> my_roots = c->comm.owner.roots_of(c->comm.rank);
+    std::vector<int32_t> nb_roots = my_roots;
+    if (c->comm.world > 1) {
+        for (int r : c->comm.owner.boundary_roots(c->comm.rank))
+            if (c->comm.owner.root_rank[(size_t)r] != c->comm.rank) nb_roots.push_back(r);
+    }
 
     // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos (a depth-first walk
-    // from the roots in Morton order; the planning API checks it against the sort of (level, Morton) keys)
+    // from this rank's roots in Morton order; the planning API checks it against the sort of (level, Morton) keys)
     {
         static thread_local std::vector<std::vector<int32_t>> per;   // scratch kept across plans
-        t.leaves_morton(per, [&](int id) { return c->comm.owns(c, id); });
+        t.leaves_morton_roots(per, [](int) { return true; },
+                              [&](int root) { return c->comm.owns(c, root); });
         c->leaf_ids.clear();
         for (const auto& lv : per) c->leaf_ids.insert(c->leaf_ids.end(), lv.begin(), lv.end());
     }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
     clk.mark("plan: leaf order");
-    c->sib.clear();   // owned parents whose 4 children are (owned) leaves: the coarsening candidates of a12
-    for (int id : c->canon) {
-        if (!t.has_children(id)) continue;
-        int q = 0;
-        while (q < 4 && c->leaf_pos[t.child[4 * id + q]] >= 0) ++q;
-        if (q < 4) continue;
-        c->sib.push_back(id);
-        for (q = 0; q < 4; ++q) c->sib.push_back(c->leaf_pos[t.child[4 * id + q]]);
-    }
-    clk.mark("plan: canon + leaf order");
+    // owned parents whose 4 children are leaves: the coarsening candidates of a12; owned covered patches: the
+    // restriction tasks per level (O9)
+    c->sib.clear();
+    c->rlev.assign(L, {});
+    for (int r : my_roots)
+        t.subtree(t.root_slot(r), [&](int id) {
+            if (!t.has_children(id)) return;
+            RestrictTask rt{};
+            rt.parent = id;
+            for (int q = 0; q < 4; ++q) rt.child[q] = t.child[4 * id + q];
+            c->rlev[t.lev[id] + 1].push_back(rt);
+            int q = 0;
+            while (q < 4 && c->leaf_pos[t.child[4 * id + q]] >= 0) ++q;
+            if (q < 4) return;
+            c->sib.push_back(id);
+            for (q = 0; q < 4; ++q) c->sib.push_back(c->leaf_pos[t.child[4 * id + q]]);
+        });
+    clk.mark("plan: sib + restriction");
 
-    // face neighbours of every active patch from the parents' (level-major, no recursion): nb4[4 id + s]
-    t.face_neighbours(c->canon, c->nb4);
+    // face neighbours of the local patches and of those they read across the boundary, from the parents' entries
+    // (subtree pre-order, no recursion): nb4[4 id + s]
+    t.face_neighbours_roots(nb_roots, c->nb4);
     clk.mark("plan: face neighbours");
     // a C/F parent's 3 x 3 neighbourhood: faces from nb4, corners through the N / S face neighbour (R2: all 8
     // exist inside the domain); -2 outside the domain
@@ -316,14 +344,6 @@ amr_status build_plan(amr_ctx* c) {
         if (rt.mask) c->rtasks.push_back(rt);
     }
     clk.mark("plan: leaf descriptors");
-    c->rlev.assign(L, {});
-    for (int id : c->canon) {
-        if (!t.has_children(id) || !c->comm.owns(c, id)) continue;
-        RestrictTask r{};
-        r.parent = id;
-        for (int q = 0; q < 4; ++q) r.child[q] = t.child[4 * id + q];
-        c->rlev[t.lev[id] + 1].push_back(r);
-    }
     c->leaf_cells = (int64_t)c->leaf_ids.size() * c->n * c->n;
     // Central4 with n = 8, 16: complete aligned B x B blocks of same-level leaves (consecutive in level-Morton
     // order, B = 32/n) form the 32 x 32 tiles of the TMA group kernel; the other leaves take the per-tile kernel
@@ -385,9 +405,8 @@ amr_status build_plan(amr_ctx* c) {
     CU(cudaStreamSynchronize(s));   // host vectors may change after return
     clk.mark("plan: uploads");
 
-    c->st.leaves = 0;
-    for (int id : c->canon) c->st.leaves += t.is_leaf(id);
-    c->st.patches = (int64_t)c->canon.size();
+    c->st.leaves = t.n_leaves();
+    c->st.patches = (int64_t)t.n_alive;
     c->st.leaf_cells = c->leaf_cells;
     c->st.proxies = (int64_t)c->ptasks.size();
     if (c->cfg.stage_kernel == 2)
@@ -706,6 +725,7 @@ amr_status evaluate_flags(amr_ctx* c) {
     CU(cudaStreamSynchronize(c->stream));
     PatchTree& t = c->tree;
     // per-id arrays sized once to the slot capacity; only the entries of active patches are (re)written and read
+    ensure_canon(c);
     std::vector<double>& eta = c->fl_eta_raw;
     std::vector<uint8_t>& amb = c->fl_amb_raw;
     if ((int)eta.size() != t.capacity) { eta.assign(t.capacity, std::nan("")); amb.assign(t.capacity, 0); }
@@ -799,7 +819,7 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     // canonical list would act on, in the same order, in O(requests log requests)
     std::vector<std::pair<uint64_t, int32_t>>& order = c->rq_order;
     order.clear();
-    for (int id : req) order.push_back({(uint64_t)c->canon_pos[id], id});
+    for (int id : req) order.push_back({nt.canon_key(PatchTree::key(nt.lev[id], nt.pi[id], nt.pj[id])), id});
     radix_sort_pairs(order);
     order.erase(std::unique(order.begin(), order.end()), order.end());
     nt.begin_txn();
@@ -827,29 +847,17 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     clk.mark("validate");
     int n_new = 0, n_del = 0;
     const int W = c->comm.world, R = c->comm.rank;
-    std::vector<uint8_t>& is_new = c->rq_new;   // kept across regrids; the previous regrid's entries reset
-    if ((int)is_new.size() != nt.capacity) { is_new.assign(nt.capacity, 0); c->rq_new_ids.clear(); }
-    for (int id : c->rq_new_ids) is_new[id] = 0;
     std::vector<int32_t>& new_ids = c->rq_new_ids;
     new_ids.clear();
     for (const auto& sn : nt.journal()) {   // created / deleted slots, from the transaction journal
-        if (nt.alive[sn.id] && !sn.alive) { is_new[sn.id] = 1; new_ids.push_back(sn.id); ++n_new; }
+        if (nt.alive[sn.id] && !sn.alive) { new_ids.push_back(sn.id); ++n_new; }
         if (!nt.alive[sn.id] && sn.alive) ++n_del;
     }
     std::sort(new_ids.begin(), new_ids.end());
     nt.commit();
     // ownership of the new tree under the OLD partition (roots never change): the old owner of a
     // root prolongs the new patches of that root, since it holds their parents' data
-    std::vector<int32_t> old_owner;
-    if (W > 1) {
-        old_owner.assign(nt.capacity, -1);
-        for (int id = 0; id < nt.capacity; ++id) {
-            if (!nt.alive[id]) continue;
-            int l = nt.lev[id];
-            int root = nt.find(0, nt.pi[id] >> l, nt.pj[id] >> l);
-            old_owner[id] = c->comm.owner[root];
-        }
-    }
+    const Owners old_owner = c->comm.owner;   // root ranks of the old partition (valid for the new tree's patches)
     std::vector<std::vector<ProlongTask>> pro(c->cfg.num_levels);
     for (int id : new_ids) {
         if (W > 1 && old_owner[id] != R) continue;
@@ -868,14 +876,13 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
         pro[p.level].push_back(p);
     }
     clk.mark("new patches / owners");
-    if (W > 1) c->comm.owner = old_owner;
     amr_status s = build_plan(c);
     if (s != AMR_OK) return s;
     clk.mark("build_plan");
     double* Un = c->U[c->un];
     for (int l = 1; l < c->cfg.num_levels; ++l) {
         if (W > 1) {
-            ExchangeLists xl = plan_coarse(nt, is_new, l, old_owner, W, R);
+            ExchangeLists xl = plan_coarse(nt, new_ids, l, old_owner, W, R);
             s = c->comm.exchange_lists(c, xl, Un, (int)c->PS, "coarse exchange");
             if (s != AMR_OK) return s;
         }
@@ -890,7 +897,7 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     clk.mark("prolong + restrict");
     if (W > 1) {
         // repartition the new tree and migrate every patch whose owner changed
-        std::vector<int32_t> new_owner = partition_owners(nt, W);
+        Owners new_owner = partition_owners(nt, W);
         ExchangeLists mig = plan_migration(nt, old_owner, new_owner, W, R);
         s = c->comm.exchange_lists(c, mig, Un, (int)c->PS, "migration");
         if (s != AMR_OK) return s;
@@ -901,8 +908,10 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     CU(cudaStreamSynchronize(c->stream));
     c->lambda_valid = false;
     c->ghost_valid = false;
-    if ((int)c->fl_eta.size() == nt.capacity)   // no requests on the new mesh until the next flag evaluation
+    if ((int)c->fl_eta.size() == nt.capacity) {   // no requests on the new mesh until the next flag evaluation
+        ensure_canon(c);
         for (int id : c->canon) { c->fl_eta[id] = std::nan(""); c->fl_ref[id] = c->fl_crs[id] = c->fl_amb[id] = 0; }
+    }
     if (nr) *nr = n_new;
     if (nc) *nc = n_del;
     clk.mark("finish");
@@ -1051,6 +1060,7 @@ void amr_destroy(amr_ctx* c) {
 
 static amr_status select_local(amr_ctx* c, int32_t npatch, const int32_t* tree_index, std::vector<int32_t>& slots,
                                std::vector<int32_t>& which) {
+    ensure_canon(c);
     slots.clear();
     which.clear();
     for (int k = 0; k < npatch; ++k) {
@@ -1072,6 +1082,7 @@ amr_status amr_set_state_fn(amr_ctx* c, amr_ic_fn fn, void* user) {
     const PatchTree& t = c->tree;
     const int n = c->n;
     const size_t PS = c->PS, nn = (size_t)n * n;
+    ensure_canon(c);
     std::vector<int32_t> idx;
     for (size_t e = 0; e < c->canon.size(); ++e)
         if (c->comm.owns(c, c->canon[e])) idx.push_back((int32_t)e);
@@ -1436,6 +1447,7 @@ amr_status amr_sync(amr_ctx* c) {
 amr_status amr_get_flags(amr_ctx* c, int32_t cap, double* maxeta, uint8_t* bits) {
     amr_status s = check(c);
     if (s != AMR_OK) return s;
+    ensure_canon(c);
     if (cap < (int)c->canon.size() || !maxeta || !bits) return fail(c, AMR_E_ARG, "get_flags: capacity");
     s = evaluate_flags(c);
     if (s != AMR_OK) return s;
@@ -1465,6 +1477,7 @@ amr_status amr_regrid_with_flags(amr_ctx* c, int32_t n, const int32_t* tree_inde
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     if (n < 0 || (n > 0 && (!tree_index || !bits))) return fail(c, AMR_E_ARG, "regrid_with_flags: bad arguments");
+    ensure_canon(c);
     std::vector<uint8_t> ref(c->tree.capacity, 0), crs(c->tree.capacity, 0);
     std::vector<int32_t> req(n);
     for (int k = 0; k < n; ++k) {
@@ -1482,6 +1495,7 @@ amr_status amr_get_patch_tree(amr_ctx* c, amr_patch_desc* out, int32_t cap, int3
     amr_status s = check(c);
     if (s != AMR_OK) return s;
     if (!count) return fail(c, AMR_E_ARG, "get_patch_tree: count is NULL");
+    ensure_canon(c);
     *count = (int32_t)c->canon.size();
     if (!out || cap < *count) return fail(c, AMR_E_ARG, "get_patch_tree: capacity smaller than the patch count");
     const PatchTree& t = c->tree;
@@ -1520,6 +1534,7 @@ amr_status amr_diagnostics(amr_ctx* c, double totals[4], double* lambda_max) {
             CU(cudaMemcpyAsync(part.data(), c->d_partial.p, part.size() * 8, cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
         // combine in canonical order (deterministic), long double accumulation
+        ensure_canon(c);
         std::vector<int32_t> order(c->leaves.size());
         for (size_t e = 0; e < order.size(); ++e) order[e] = (int32_t)e;
         std::sort(order.begin(), order.end(),

@@ -41,41 +41,60 @@ ExchangeLists from_needs(const std::vector<std::map<int, std::set<int32_t>>>& ne
 }
 }  // namespace
 
-std::vector<int32_t> partition_owners(const PatchTree& t, int world) {
-    std::vector<int32_t> owner(t.capacity, -1);
-    if (world <= 1) {
-        for (int id = 0; id < t.capacity; ++id)
-            if (t.alive[id]) owner[id] = 0;
-        return owner;
-    }
-    const int npx = t.np0[0], npy = t.np0[1];
-    std::vector<int64_t> weight((size_t)npx * npy, 0);
-    for (int id = 0; id < t.capacity; ++id) {
-        if (!t.is_leaf(id)) continue;
-        int l = t.lev[id];
-        weight[(size_t)(t.pj[id] >> l) * npx + (t.pi[id] >> l)] += 1;
-    }
-    std::vector<int32_t> roots((size_t)npx * npy);
-    for (size_t r = 0; r < roots.size(); ++r) roots[r] = (int32_t)r;
-    std::stable_sort(roots.begin(), roots.end(), [&](int a, int b) {
-        return morton((uint32_t)(a % npx), (uint32_t)(a / npx)) < morton((uint32_t)(b % npx), (uint32_t)(b / npx));
-    });
+Owners partition_owners(const PatchTree& t, int world) {
+    Owners o;
+    o.t = &t;
+    o.world = world;
+    const int nr = t.nroots();
+    o.root_rank.assign((size_t)nr, 0);
+    if (world <= 1) return o;
+    // roots in Morton order, weighted by their (incrementally maintained) leaf counts, cut into world chunks
+    const std::vector<int32_t>& w = t.root_leaves();
     int64_t total = 0;
-    for (auto w : weight) total += w;
-    std::vector<int32_t> root_rank((size_t)npx * npy, 0);
+    for (int r = 0; r < nr; ++r) total += w[(size_t)r];
     int64_t prefix = 0;
-    for (int r : roots) {
-        int64_t w = weight[r];
-        int64_t k = ((2 * prefix + w) * (int64_t)world) / (2 * std::max<int64_t>(total, 1));
-        root_rank[r] = (int32_t)std::min<int64_t>(k, world - 1);
-        prefix += w;
+    for (int slot : t.root_morton()) {
+        const int r = t.root_index(slot);
+        const int64_t wr = w[(size_t)r];
+        const int64_t k = ((2 * prefix + wr) * (int64_t)world) / (2 * std::max<int64_t>(total, 1));
+        o.root_rank[(size_t)r] = (int32_t)std::min<int64_t>(k, world - 1);
+        prefix += wr;
     }
-    for (int id = 0; id < t.capacity; ++id) {
-        if (!t.alive[id]) continue;
-        int l = t.lev[id];
-        owner[id] = root_rank[(size_t)(t.pj[id] >> l) * npx + (t.pi[id] >> l)];
-    }
-    return owner;
+    return o;
+}
+
+std::vector<int32_t> Owners::roots_of(int rank) const {
+    std::vector<int32_t> out;
+    for (size_t r = 0; r < root_rank.size(); ++r)
+        if (world == 1 || root_rank[r] == rank) out.push_back((int32_t)r);
+    return out;
+}
+
+const std::vector<int32_t>& Owners::boundary_roots(int rank) const {
+    if (bnd_rank_ == rank) return bnd_;
+    bnd_.clear();
+    bnd_rank_ = rank;
+    if (world <= 1) return bnd_;
+    // from this rank's roots and their 8 neighbours only: O(local roots)
+    const int npx = t->np0[0], npy = t->np0[1];
+    std::vector<uint8_t> mark;   // (sparse set over the roots touched)
+    std::vector<int32_t> cand;
+    for (int J = 0; J < npy; ++J)
+        for (int I = 0; I < npx; ++I) {
+            if (root_rank[(size_t)J * npx + I] != rank) continue;
+            bool edge = false;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int i = I + dx, j = J + dy;
+                    if (!t->wrap(0, i, j)) continue;
+                    if (root_rank[(size_t)j * npx + i] != rank) { edge = true; cand.push_back(j * npx + i); }
+                }
+            if (edge) cand.push_back(J * npx + I);
+        }
+    std::sort(cand.begin(), cand.end());
+    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+    bnd_.swap(cand);
+    return bnd_;
 }
 
 void halo_sources(const PatchTree& t, int id, int n, std::vector<int32_t>& out, bool faces) {
@@ -100,54 +119,67 @@ void halo_sources(const PatchTree& t, int id, int n, std::vector<int32_t>& out, 
     }
 }
 
-ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n, bool faces) {
+namespace {
+// f(id) for every active patch (leaves_only: every leaf) in the subtrees of `rank`'s boundary roots
+template <class F>
+void for_boundary(const PatchTree& t, const Owners& owner, int rank, bool leaves_only, F f) {
+    for (int r : owner.boundary_roots(rank))
+        t.subtree(t.root_slot(r), [&](int id) {
+            if (!leaves_only || t.is_leaf(id)) f(id);
+        });
+}
+}  // namespace
+
+ExchangeLists plan_halo(const PatchTree& t, const Owners& owner, int world, int rank, int n, bool faces) {
     std::vector<std::map<int, std::set<int32_t>>> need(world);
     std::vector<int32_t> src;
-    for (int id = 0; id < t.capacity; ++id) {
-        if (!t.is_leaf(id)) continue;
-        int o = owner[id];
+    for_boundary(t, owner, rank, true, [&](int id) {
+        const int o = owner[id];
         halo_sources(t, id, n, src, faces);
-        for (int q : src)
-            if (owner[q >> 5] != o) need[o][owner[q >> 5]].insert(q);
-    }
+        for (int q : src) {
+            const int oq = owner[q >> 5];
+            if (oq != o && (o == rank || oq == rank)) need[o][oq].insert(q);
+        }
+    });
     ExchangeLists L = from_needs(need, world, rank);
     L.items = true;
     return L;
 }
 
-ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank) {
+ExchangeLists plan_flux(const PatchTree& t, const Owners& owner, int world, int rank) {
     static const int cidx[4][2] = {{1, 3}, {0, 2}, {2, 3}, {0, 1}};
     std::vector<std::map<int, std::set<int32_t>>> need(world);
-    for (int id = 0; id < t.capacity; ++id) {
-        if (!t.is_leaf(id)) continue;
+    for_boundary(t, owner, rank, true, [&](int id) {
+        const int o = owner[id];
         for (int s = 0; s < 4; ++s) {
             int nb = t.neighbour(id, kSideDir[s][0], kSideDir[s][1]);
             if (nb < 0 || !t.has_children(nb)) continue;
             for (int h = 0; h < 2; ++h) {
-                int f = t.child[4 * nb + cidx[s][h]];
-                if (owner[f] != owner[id]) need[owner[id]][owner[f]].insert(f);
+                const int f = t.child[4 * nb + cidx[s][h]];
+                const int of = owner[f];
+                if (of != o && (o == rank || of == rank)) need[o][of].insert(f);
             }
         }
-    }
+    });
     return from_needs(need, world, rank);
 }
 
-ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_new, int level,
-                          const std::vector<int32_t>& owner, int world, int rank) {
+ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<int32_t>& new_ids, int level, const Owners& owner,
+                          int world, int rank) {
     std::vector<std::map<int, std::set<int32_t>>> need(world);
-    for (int id = 0; id < nt.capacity; ++id) {
-        if (!nt.alive[id] || !is_new[id] || nt.lev[id] != level) continue;
+    for (int id : new_ids) {
+        if (!nt.alive[id] || nt.lev[id] != level) continue;
         int o = owner[id], par = nt.parent[id];
         for (int dy = -1; dy <= 1; ++dy)
             for (int dx = -1; dx <= 1; ++dx) {
                 int q = (dx == 0 && dy == 0) ? par : nt.neighbour(par, dx, dy);
-                if (q >= 0 && owner[q] != o) need[o][owner[q]].insert(q);
+                if (q >= 0 && owner[q] != o && (o == rank || owner[q] == rank)) need[o][owner[q]].insert(q);
             }
     }
     return from_needs(need, world, rank);
 }
 
-SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n) {
+SubLists plan_subcycle(const PatchTree& t, const Owners& owner, int world, int rank, int n) {
     static const int cidx[4][2] = {{1, 3}, {0, 2}, {2, 3}, {0, 1}};   // children of a W/E/S/N neighbour on the face
     const int L = t.levels;
     std::vector<std::vector<std::map<int, std::set<int32_t>>>> face(L), coarse(L), facc(L);
@@ -156,8 +188,8 @@ SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, in
         coarse[l].resize(world);
         facc[l].resize(world);
     }
-    for (int id = 0; id < t.capacity; ++id) {
-        if (!t.alive[id]) continue;   // every active patch is advanced (leaves, and covered patches)
+    auto keep = [&](int o, int q) { return q != o && (o == rank || q == rank); };
+    for_boundary(t, owner, rank, false, [&](int id) {   // every active patch is advanced (leaves and covered ones)
         const int l = t.lev[id], o = owner[id];
         const bool leaf = t.is_leaf(id);
         for (int s = 0; s < 4; ++s) {
@@ -165,11 +197,11 @@ SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, in
             if (nb >= 0) {
                 // the strip of nb facing id (band item, as plan_halo)
                 const int facing[4] = {kBandE, kBandW, n / 4 - 1, 0};
-                if (owner[nb] != o) face[l][o][owner[nb]].insert(nb * 32 + facing[s]);
+                if (keep(o, owner[nb])) face[l][o][owner[nb]].insert(nb * 32 + facing[s]);
                 if (leaf && t.has_children(nb))
                     for (int h = 0; h < 2; ++h) {
                         const int f = t.child[4 * nb + cidx[s][h]];
-                        if (f >= 0 && owner[f] != o) facc[l][o][owner[f]].insert(f);
+                        if (f >= 0 && keep(o, owner[f])) facc[l][o][owner[f]].insert(f);
                     }
             } else if (nb == -1 && leaf) {
                 const int par = t.parent[id];
@@ -177,11 +209,11 @@ SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, in
                 for (int dy = -1; dy <= 1; ++dy)
                     for (int dx = -1; dx <= 1; ++dx) {
                         const int q = (dx == 0 && dy == 0) ? par : t.neighbour(par, dx, dy);
-                        if (q >= 0 && owner[q] != o) coarse[l][o][owner[q]].insert(q);
+                        if (q >= 0 && keep(o, owner[q])) coarse[l][o][owner[q]].insert(q);
                     }
             }
         }
-    }
+    });
     SubLists out;
     for (int l = 0; l < L; ++l) {
         out.face.push_back(from_needs(face[l], world, rank));
@@ -192,11 +224,14 @@ SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, in
     return out;
 }
 
-ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& old_owner,
-                             const std::vector<int32_t>& new_owner, int world, int rank) {
+ExchangeLists plan_migration(const PatchTree& nt, const Owners& old_owner, const Owners& new_owner, int world,
+                             int rank) {
     std::vector<std::map<int, std::set<int32_t>>> need(world);
-    for (int id = 0; id < nt.capacity; ++id)
-        if (nt.alive[id] && old_owner[id] != new_owner[id]) need[new_owner[id]][old_owner[id]].insert(id);
+    for (int r = 0; r < nt.nroots(); ++r) {
+        const int a = old_owner.root_rank[(size_t)r], b = new_owner.root_rank[(size_t)r];
+        if (a == b || (a != rank && b != rank)) continue;
+        nt.subtree(nt.root_slot(r), [&](int id) { need[b][a].insert(id); });
+    }
     return from_needs(need, world, rank);
 }
 

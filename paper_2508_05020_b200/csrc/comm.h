@@ -36,17 +36,34 @@ struct ExchangeLists {
 };
 
 // ---- pure host planning (no CUDA): testable on CPU
-std::vector<int32_t> partition_owners(const PatchTree& t, int world);
+// Ownership by root tree: owner(id) = root_rank[root of id] -- O(1) per query, O(roots) per repartition (no
+// capacity-sized array); the tree must outlive the object
+struct Owners {
+    const PatchTree* t = nullptr;
+    int world = 1;
+    std::vector<int32_t> root_rank;   // per root, row-major
+    int operator[](int id) const { return world == 1 ? 0 : root_rank[(size_t)t->root_index(id)]; }
+    // roots whose subtrees can hold leaves that read from, or are read by, `rank` across a partition boundary: the
+    // roots of `rank` with a Moore-neighbour root of another rank, and the other ranks' roots Moore-adjacent to one of
+    // `rank` (a patch reads only its own root and the 8 around it: face neighbours, parent's 3 x 3 neighbourhood)
+    const std::vector<int32_t>& boundary_roots(int rank) const;   // (cached per rank until the partition changes)
+    std::vector<int32_t> roots_of(int rank) const;   // row-major indices of rank's roots
+
+  private:
+    mutable int bnd_rank_ = -1;
+    mutable std::vector<int32_t> bnd_;
+};
+Owners partition_owners(const PatchTree& t, int world);
 // band items read by the stage / flags / ghost kernels of leaf `id` that may live on another rank (patch size n): of a
 // face neighbour the strip facing id, of a coarse source of a C/F ghost strip (the parent's 3 x 3 neighbourhood) the
 // whole patch (faces = false: only the coarse sources -- halo_mode 2 reads face strips in the stage kernel)
 void halo_sources(const PatchTree& t, int id, int n, std::vector<int32_t>& out, bool faces = true);
-ExchangeLists plan_halo(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n,
-                        bool faces = true);
-ExchangeLists plan_flux(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank);
+// the per-rank lists are built from the leaves of owner.boundary_roots(rank) only: O(partition boundary)
+ExchangeLists plan_halo(const PatchTree& t, const Owners& owner, int world, int rank, int n, bool faces = true);
+ExchangeLists plan_flux(const PatchTree& t, const Owners& owner, int world, int rank);
 // coarse sources of new level-l patches prolonged by the (old) owner of their root
-ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_new, int level,
-                          const std::vector<int32_t>& owner, int world, int rank);
+ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<int32_t>& new_ids, int level, const Owners& owner,
+                          int world, int rank);
 // subcycling (NEXT #4) across ranks, per level l: the remote slots a level-l stage reads (same-level face
 // neighbours of every advanced level-l patch, leaves and covered ones), the remote coarse sources of the level's
 // C/F ghosts (read at two times: the coarse step's start and end buffers), and the remote fine leaves whose
@@ -54,9 +71,9 @@ ExchangeLists plan_coarse(const PatchTree& nt, const std::vector<uint8_t>& is_ne
 struct SubLists {
     std::vector<ExchangeLists> face, coarse, facc;
 };
-SubLists plan_subcycle(const PatchTree& t, const std::vector<int32_t>& owner, int world, int rank, int n);
-ExchangeLists plan_migration(const PatchTree& nt, const std::vector<int32_t>& old_owner,
-                             const std::vector<int32_t>& new_owner, int world, int rank);
+SubLists plan_subcycle(const PatchTree& t, const Owners& owner, int world, int rank, int n);
+// patches of the roots whose owner changed (O(changed subtrees))
+ExchangeLists plan_migration(const PatchTree& nt, const Owners& old_owner, const Owners& new_owner, int world, int rank);
 
 struct Transport;
 
@@ -64,7 +81,7 @@ struct Comm {
     int world = 1, rank = 0;
     int n = 0;                         // patch size (band items)
     std::unique_ptr<Transport> tr;
-    std::vector<int32_t> owner;        // per slot (patch id); -1 for free slots
+    Owners owner;                      // root-tree ownership of every active patch
     ExchangeLists halo, flux, halo_cf;
     bool subcycle = false;
     SubLists sub;                      // subcycle: per-level lists (plan_subcycle)

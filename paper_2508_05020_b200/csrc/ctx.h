@@ -122,6 +122,7 @@ struct amr_ctx {
     bool ghost_valid = false;      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
     double sim_time_fix = 0.0;     // host correction of the device time sum (rolled-back steps)
     std::vector<int32_t> nb4;      // face neighbours W, E, S, N of every slot (PatchTree::face_neighbours)
+    bool canon_valid = false;      // canon / canon_pos match the tree (ensure_canon)
     double last_dt = 0.0;
 
     // flags of the last evaluation, per id

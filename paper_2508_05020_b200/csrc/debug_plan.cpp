@@ -3,6 +3,7 @@
 #include "../../include/amr_debug.h"
 
 #include <algorithm>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -102,7 +103,7 @@ amr_status amr_plan_tree(amr_plan* p, int32_t world, amr_patch_desc* out, int32_
     std::vector<int32_t> pos = canon_pos_of(p->tree, canon);
     *count = (int32_t)canon.size();
     if (!out || cap < *count) return AMR_E_ARG;
-    std::vector<int32_t> owner = amr::partition_owners(p->tree, world);
+    amr::Owners owner = amr::partition_owners(p->tree, world);
     static const int moore[8][2] = {{0, 1}, {1, 0}, {0, -1}, {-1, 0}, {1, 1}, {1, -1}, {-1, -1}, {-1, 1}};
     const amr::PatchTree& t = p->tree;
     for (size_t e = 0; e < canon.size(); ++e) {
@@ -130,7 +131,7 @@ amr_status amr_plan_exchange(amr_plan* p, int32_t world, int32_t rank, int32_t k
         return AMR_E_ARG;
     std::vector<int32_t> canon;
     std::vector<int32_t> pos = canon_pos_of(p->tree, canon);
-    std::vector<int32_t> owner = amr::partition_owners(p->tree, world);
+    amr::Owners owner = amr::partition_owners(p->tree, world);
     const bool raw = kind >= 1000;   // raw band items (tree index * 32 + code) instead of the slots they touch
     if (raw) kind -= 1000;
     amr::ExchangeLists L;
@@ -170,6 +171,49 @@ amr_status amr_plan_exchange(amr_plan* p, int32_t world, int32_t rank, int32_t k
             recv_index[nr++] = x;
         }
     }
+    return AMR_OK;
+}
+
+// Host plan work of one rank at a regrid (the replicated part of build_plan + Comm::replan), timed on this CPU:
+// ms[0] partition, [1] this rank's roots and boundary roots, [2] leaf launch order, [3] face-neighbour table, [4] halo lists, [5] flux
+// lists, [6] total; counts[0] active patches, [1] this rank's leaves, [2] halo items received, [3] sent.
+amr_status amr_plan_profile(amr_plan* p, int32_t world, int32_t rank, int32_t reps, double* ms, int64_t* counts) {
+    if (!p || world < 1 || rank < 0 || rank >= world || reps < 1 || !ms || !counts) return AMR_E_ARG;
+    using clk = std::chrono::steady_clock;
+    const amr::PatchTree& t = p->tree;
+    for (int k = 0; k < 7; ++k) ms[k] = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        auto t0 = clk::now();
+        amr::Owners owner = amr::partition_owners(t, world);
+        auto t1 = clk::now();
+        // (as build_plan: the canonical order is not needed on the regrid path; this rank's roots and their boundary)
+        const std::vector<int32_t> mine = owner.roots_of(rank);
+        std::vector<int32_t> nbr = mine;
+        for (int r2 : owner.boundary_roots(rank))
+            if (owner.root_rank[(size_t)r2] != rank) nbr.push_back(r2);
+        auto t2 = clk::now();
+        std::vector<std::vector<int32_t>> per;
+        t.leaves_morton_roots(per, [](int) { return true; }, [&](int root) { return owner[root] == rank; });
+        auto t3 = clk::now();
+        static std::vector<int32_t> nb4;   // (sized once, as the library's)
+        t.face_neighbours_roots(nbr, nb4);
+        auto t4 = clk::now();
+        amr::ExchangeLists h = amr::plan_halo(t, owner, world, rank, p->n);
+        auto t5 = clk::now();
+        amr::ExchangeLists f = amr::plan_flux(t, owner, world, rank);
+        auto t6 = clk::now();
+        auto d = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        ms[0] += d(t0, t1); ms[1] += d(t1, t2); ms[2] += d(t2, t3); ms[3] += d(t3, t4); ms[4] += d(t4, t5);
+        ms[5] += d(t5, t6); ms[6] += d(t0, t6);
+        int64_t nl = 0;
+        for (auto& v : per) nl += (int64_t)v.size();
+        counts[0] = (int64_t)t.n_alive;
+        counts[1] = nl;
+        counts[2] = (int64_t)h.nrecv();
+        counts[3] = (int64_t)h.nsend();
+        (void)f;
+    }
+    for (int k = 0; k < 7; ++k) ms[k] /= reps;
     return AMR_OK;
 }
 

@@ -52,6 +52,15 @@ void PatchTree::init(int npx, int npy, int nlev, bool perx, bool pery, int cap, 
         root_[e.second] = alloc(0, e.second % npx, e.second / npx);
         root_morton_.push_back(root_[e.second]);
     }
+    root_leaves_.assign((size_t)npx * npy, 1);
+    n_leaves_ = (int64_t)npx * npy;
+}
+
+void PatchTree::recount_leaves() {
+    std::fill(root_leaves_.begin(), root_leaves_.end(), 0);
+    n_leaves_ = 0;
+    for (int id = 0; id < capacity; ++id)
+        if (alive[id] && child[4 * id] < 0) { ++root_leaves_[root_index(id)]; ++n_leaves_; }
 }
 
 void PatchTree::touch(int id) {
@@ -92,6 +101,7 @@ void PatchTree::rollback() {
     for (const auto& sn : journal_) touched_[sn.id] = 0;
     journal_.clear();
     txn_ = false;
+    recount_leaves();   // rare path
 }
 
 int PatchTree::alloc(int l, int i, int j) {
@@ -166,6 +176,8 @@ bool PatchTree::refine(int id, std::string& err) {
     }
     if ((int)free_.size() < 4) { err = "slot capacity exceeded"; return false; }
     touch(id);
+    root_leaves_[root_index(id)] += 3;
+    n_leaves_ += 3;
     for (int c = 0; c < 4; ++c) {
         int a = c & 1, b = c >> 1;
         int k = alloc(l + 1, 2 * pi[id] + a, 2 * pj[id] + b);
@@ -204,6 +216,10 @@ bool PatchTree::coarsen_allowed(int id) const {
 
 void PatchTree::delete_children(int id) {
     touch(id);
+    if (child[4 * id] >= 0) {   // (coarsening: the 4 children are leaves)
+        root_leaves_[root_index(id)] -= 3;
+        n_leaves_ -= 3;
+    }
     for (int c = 0; c < 4; ++c) {
         int k = child[4 * id + c];
         if (k >= 0) release(k);
@@ -320,6 +336,35 @@ void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<i
         o[3] = b == 0 ? pa.child[a + 2] : across(3, a);
     };
     for (int id : canon) one(id);   // level-major: a patch's parent is done before it
+}
+
+void PatchTree::face_neighbours_roots(const std::vector<int32_t>& roots, std::vector<int32_t>& nb4) const {
+    if (nb4.size() != (size_t)4 * capacity) nb4.assign((size_t)4 * capacity, -1);
+    static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
+    for (int r : roots)
+        subtree(root_[(size_t)r], [&](int id) {
+            const Node& nd = node_[id];
+            int32_t* o = &nb4[(size_t)4 * id];
+            if (nd.lev == 0) {
+                for (int s = 0; s < 4; ++s) {
+                    int i = nd.pi + d[s][0], j = nd.pj + d[s][1];
+                    o[s] = wrap(0, i, j) ? root_[(size_t)j * np0[0] + i] : -2;
+                }
+                return;
+            }
+            const Node& pa = node_[nd.parent];
+            const int32_t* pn = &nb4[(size_t)4 * nd.parent];
+            const int a = nd.pi & 1, b = nd.pj & 1;
+            auto across = [&](int side, int cidx) {
+                const int q = pn[side];
+                if (q < 0) return q;
+                return node_[q].child[0] < 0 ? -1 : node_[q].child[cidx];
+            };
+            o[0] = a == 1 ? pa.child[0 + 2 * b] : across(0, 1 + 2 * b);
+            o[1] = a == 0 ? pa.child[1 + 2 * b] : across(1, 0 + 2 * b);
+            o[2] = b == 1 ? pa.child[a] : across(2, a + 2);
+            o[3] = b == 0 ? pa.child[a + 2] : across(3, a);
+        });
 }
 
 std::vector<int32_t> PatchTree::canonical_sorted() const {

@@ -168,6 +168,29 @@ struct PatchTree {
     // the parent's neighbour (roots from a table) -- with no hash probe
     int neighbour(int id, int dx, int dy) const;
     bool has_children(int id) const { return node_[id].child[0] >= 0; }
+    // root (row-major index) of the tree holding slot id
+    int root_index(int id) const { const Node& nd = node_[id]; return (nd.pj >> nd.lev) * np0[0] + (nd.pi >> nd.lev); }
+    int root_slot(int r) const { return root_[(size_t)r]; }
+    int nroots() const { return np0[0] * np0[1]; }
+    const std::vector<int32_t>& root_morton() const { return root_morton_; }   // root slots in Morton order
+    // leaves per root (row-major), maintained by refine / delete_children (+3 / -3), recomputed by rollback
+    const std::vector<int32_t>& root_leaves() const { return root_leaves_; }
+    int64_t n_leaves() const { return n_leaves_; }
+    // pre-order walk of the subtree of a slot (parents before children), f(id)
+    template <class F>
+    void subtree(int top, F f) const {
+        std::vector<int32_t>& st = walk_;
+        st.clear();
+        st.push_back(top);
+        while (!st.empty()) {
+            const int id = st.back();
+            st.pop_back();
+            f(id);
+            const Node& nd = node_[id];
+            if (nd.child[0] >= 0)
+                for (int q = 3; q >= 0; --q) st.push_back(nd.child[q]);
+        }
+    }
     bool is_leaf(int id) const { return node_[id].lev >= 0 && node_[id].child[0] < 0; }   // alive <=> lev >= 0
 
     // Alg. 1 on a copy-on-write basis; returns false (tree unchanged by caller's
@@ -189,10 +212,16 @@ struct PatchTree {
     // Morton order a + 2b): the launch order of build_plan without a sort; keep(id) filters (ownership)
     template <class Keep>
     void leaves_morton(std::vector<std::vector<int32_t>>& per_level, Keep keep) const {
+        leaves_morton_roots(per_level, keep, [](int) { return true; });
+    }
+    // the same walk over the roots with root_ok(root slot) only (a rank's own roots: O(local))
+    template <class Keep, class RootOk>
+    void leaves_morton_roots(std::vector<std::vector<int32_t>>& per_level, Keep keep, RootOk root_ok) const {
         per_level.assign(levels, {});
         std::vector<int32_t>& st = dfs_;
         st.clear();
-        for (auto it = root_morton_.rbegin(); it != root_morton_.rend(); ++it) st.push_back(*it);
+        for (auto it = root_morton_.rbegin(); it != root_morton_.rend(); ++it)
+            if (root_ok(*it)) st.push_back(*it);
         while (!st.empty()) {
             const int id = st.back();
             st.pop_back();
@@ -207,6 +236,9 @@ struct PatchTree {
     // face neighbours W, E, S, N of every active patch (nb4[4 id + s]: id, -1 missing, -2 outside the domain), top
     // down over `canon` (level-major) from the parents' entries: equal to neighbour(id, +-1 / 0) without recursion
     void face_neighbours(const std::vector<int32_t>& canon, std::vector<int32_t>& nb4) const;
+    // the same table for the subtrees of the given roots only (row-major root indices; each subtree pre-order, a patch
+    // needs only its parent's entries); nb4 is sized once to the capacity
+    void face_neighbours_roots(const std::vector<int32_t>& roots, std::vector<int32_t>& nb4) const;
 
     // Transactions (regrid is atomic): between begin_txn() and commit()/rollback() every modified slot
     // is journaled once with its prior state, so a failed regrid is undone in O(changes) -- no copy of the
@@ -239,6 +271,10 @@ struct PatchTree {
     std::vector<int32_t> root_;   // root (i, j) -> slot, row-major (R1: roots are permanent)
     std::vector<int32_t> root_morton_;   // root slots in Morton order of (i, j)
     mutable std::vector<int32_t> dfs_;   // leaves_morton's stack
+    mutable std::vector<int32_t> walk_;  // subtree()'s stack
+    std::vector<int32_t> root_leaves_;   // leaves per root (row-major)
+    int64_t n_leaves_ = 0;
+    void recount_leaves();
     std::vector<int32_t> free_;   // min-heap of free slots
     int alloc(int l, int i, int j);
     void release(int id);
