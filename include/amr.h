@@ -204,10 +204,15 @@ amr_status amr_get_state(amr_ctx* ctx, int32_t npatch, const int32_t* tree_index
  * (U^n unchanged); amr_last_error names level, patch and stage. */
 amr_status amr_step(amr_ctx* ctx, double dt, double cfl, double* dt_used);
 
-/* nsteps steps without host synchronisation in between (same semantics). */
+/* nsteps steps queued without host synchronisation in between: each step is amr_step's arithmetic, but errors are
+ * reported LATE and nothing is rolled back.  A non-physical state (check_positivity) or a non-finite dt detected on
+ * the device in any of the queued steps is returned as AMR_E_NONPHYSICAL by the next amr_sync (or by the next amr_step,
+ * which then does not commit its own step either); the mesh then holds the state advanced by all nsteps steps (the steps
+ * queued after the failing one ran on its non-physical data) -- unlike amr_step, which keeps U^n on failure.  Use
+ * amr_step where a failed step must leave U^n intact. */
 amr_status amr_steps(amr_ctx* ctx, int32_t nsteps, double dt, double cfl);
 
-/* Wait for all queued work; returns a deferred AMR_E_NONPHYSICAL if any. */
+/* Wait for all queued work; returns a deferred AMR_E_NONPHYSICAL (of amr_steps) if any, without rollback. */
 amr_status amr_sync(amr_ctx* ctx);
 
 /* Evaluate the refinement indicator (BJ configs[0]: eta = dx |grad rho| / rho,

@@ -189,6 +189,9 @@ amr_status build_subcycle_plan(amr_ctx* c) {
         }
         while (r < c->rtasks.size() && c->rtasks[r].level == l) ++r;
     }
+    // the one-pass walk above relies on canon being level-major (canon_key): every covered patch must have been seen
+    if (cp != c->canon.size() || e != c->leaf_ids.size())
+        return fail(c, AMR_E_STATE, "subcycle plan: canonical / leaf order not level-major");
     c->sub_levels = 0;
     for (int id : c->canon) c->sub_levels = std::max(c->sub_levels, t.lev[id] + 1);
     c->sub_off[L] = (int32_t)c->sub_descs.size();

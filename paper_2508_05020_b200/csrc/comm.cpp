@@ -260,7 +260,8 @@ struct Transport {
     // in-place allreduce on a device buffer; kind 0: max u64, 1: max f64, 2: sum f64, 3: max i32
     virtual std::string allreduce(void* d, size_t count, int kind, cudaStream_t s) = 0;
     // halo_mode 1: map every rank's device buffer [base, base + bytes) into this process (out[rank] = base)
-    virtual std::string map_peers(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s) = 0;
+    // tag: 0 the state pool, 1 the flux registers -- a re-map of a tag first closes that tag's previous mappings
+    virtual std::string map_peers(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s, int tag = 0) = 0;
     // stream-ordered cross-rank fence: work queued after it on s runs after every rank's work queued before it
     virtual std::string fence(cudaStream_t s) = 0;
 };
@@ -330,10 +331,12 @@ struct NcclTransport : Transport {
     }
     // peer mapping by CUDA IPC: each rank publishes (handle of the allocation holding base, offset of base in it);
     // the W records are combined by a byte-wise sum allreduce (every record is zero except on its owner)
-    std::vector<void*> opened;
+    std::vector<void*> opened[2];   // IPC mappings per tag
     int32_t* d_fence = nullptr;
-    std::string map_peers(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s) override {
+    std::string map_peers(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s, int tag = 0) override {
         (void)bytes;
+        for (void* p : opened[tag]) cudaIpcCloseMemHandle(p);   // the tag's previous buffer (re-allocated)
+        opened[tag].clear();
         using RangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
         static RangeFn range = nullptr;
         if (!range) {
@@ -369,7 +372,7 @@ struct NcclTransport : Transport {
             void* p = nullptr;
             if (cudaIpcOpenMemHandle(&p, recs[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
                 return "cudaIpcOpenMemHandle failed";
-            opened.push_back(p);
+            opened[tag].push_back(p);
             out[q] = (char*)p + recs[q].off;
         }
         return std::string();
@@ -380,7 +383,8 @@ struct NcclTransport : Transport {
         return r == ncclSuccess ? std::string() : err(r);
     }
     ~NcclTransport() override {
-        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        for (auto& v : opened)
+            for (void* p : v) cudaIpcCloseMemHandle(p);
         if (d_fence) cudaFree(d_fence);
         if (comm) nccl_api().CommDestroy(comm);
     }
@@ -392,7 +396,7 @@ struct NcclTransport : Transport {
 struct HostTransport : Transport {
     const amr_host_comm* hc = nullptr;
     int world = 1, rank = 0;
-    std::vector<void*> opened;
+    std::vector<void*> opened[2];   // IPC mappings per tag
     std::string gather(const void* send, size_t bytes, void* recv) {
         return hc->allgather(send, (uint64_t)bytes, recv, hc->user) == 0 ? std::string() : "host allgather failed";
     }
@@ -448,7 +452,9 @@ struct HostTransport : Transport {
             }
         return h2d_sync(d, all.data(), bytes, s) == cudaSuccess ? std::string() : "host allreduce: upload";
     }
-    std::string map_peers(void* base, size_t, std::vector<void*>& out, cudaStream_t) override {
+    std::string map_peers(void* base, size_t, std::vector<void*>& out, cudaStream_t, int tag = 0) override {
+        for (void* p : opened[tag]) cudaIpcCloseMemHandle(p);   // the tag's previous buffer (re-allocated)
+        opened[tag].clear();
         using RangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
         static RangeFn range = nullptr;
         if (!range) {
@@ -473,7 +479,7 @@ struct HostTransport : Transport {
             void* p = nullptr;
             if (cudaIpcOpenMemHandle(&p, recs[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
                 return "cudaIpcOpenMemHandle failed";
-            opened.push_back(p);
+            opened[tag].push_back(p);
             out[q] = (char*)p + recs[q].off;
         }
         return std::string();
@@ -483,7 +489,8 @@ struct HostTransport : Transport {
         return hc->barrier(hc->user) == 0 ? std::string() : "host barrier failed";
     }
     ~HostTransport() override {
-        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        for (auto& v : opened)
+            for (void* p : v) cudaIpcCloseMemHandle(p);
     }
 };
 
@@ -571,7 +578,8 @@ struct LoopTransport : Transport {
         G->barrier();
         return std::string();
     }
-    std::string map_peers(void* base, size_t, std::vector<void*>& out, cudaStream_t) override {
+    std::string map_peers(void* base, size_t, std::vector<void*>& out, cudaStream_t, int tag = 0) override {
+        (void)tag;
         G->bufs[rank] = base;   // virtual ranks share the process: their buffers are directly addressable
         G->barrier();
         for (int q = 0; q < G->world; ++q) out[q] = G->bufs[q];
@@ -795,7 +803,7 @@ amr_status Comm::peer_pull(amr_ctx* c, const ExchangeLists& L, PullList& P, doub
     auto bad = [&](amr_status st, const std::string& m) { c->err = std::string(what) + ": " + m; c->sticky = st; return st; };
     if (freg && mapped_freg != c->freg.p) {   // (re)map the flux-register buffers (identical sizes on every rank)
         std::vector<void*> peers(world, nullptr);
-        std::string e = tr->map_peers(c->freg.p, c->freg.cap * sizeof(double), peers, c->stream);
+        std::string e = tr->map_peers(c->freg.p, c->freg.cap * sizeof(double), peers, c->stream, 1);
         if (!e.empty()) return bad(AMR_E_COMM, e);
         if (!d_freg_bases && cudaMalloc(&d_freg_bases, world * sizeof(double*)) != cudaSuccess) return bad(AMR_E_CUDA, "alloc");
         if (h2d_sync(d_freg_bases, peers.data(), world * sizeof(double*), c->stream) != cudaSuccess)

@@ -2638,8 +2638,9 @@ cudaError_t launch_post_stage(const PostArgs& p, cudaStream_t s) {
         int occ = 0;
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_stage_kernel, kPostThreads, smem);
         if (e != cudaSuccess) return e;
-        // at most 2 blocks per SM: the grid barriers cost more with more blocks, and the phases are short
-        static const int bps = [] { const char* e = getenv("AMR_POST_BPS"); return e ? atoi(e) : 2; }();   // A/B
+        // at most 4 blocks per SM (A/B with AMR_POST_BPS: 2 / 4 / 8 within noise on configs[2], 4 = the separate
+        // launches' time on configs[3]): the grid barriers cost more with more blocks, and the phases are short
+        static const int bps = [] { const char* e = getenv("AMR_POST_BPS"); return e ? atoi(e) : 4; }();   // A/B
         max_blocks = std::max(1, std::min(occ, bps)) * sm_count();
         for_smem = smem;
     }
