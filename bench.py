@@ -521,6 +521,11 @@ def main():
                                             "4096^2..16384^2; WENO5 char / comp at 4096^2; fp64_issue_frac from each "
                                             "WENO5-char kernel's own SASS fp64 count, profiles/r2_fp64_work.json)",
                                 "rows": measure_sweep_table(X, args, hbm_peak)}
+    if "sweep_table" in extra:   # the largest single-GPU configs[4] row beside the 4096^2-per-GPU headline
+        big = [r for r in extra["sweep_table"]["rows"] if r["N"] == 16384 and r["n"] == args.n and r["scheme"] == args.scheme]
+        if big:
+            extra["largest_single_gpu"] = dict(big[0], workload="BASELINE configs[4] at its largest single-GPU size: "
+                                                                 f"16384^2 cells, {args.n}^2 patches (stage kernel only)")
     if X.rank == 0:
         rf = {"bound": "hbm", "achieved": main_res["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
               "frac": main_res["achieved_gbs"] / hbm_peak, "traffic": None, "peak_kind": hbm_kind,

@@ -64,6 +64,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--tag", default="r1")
+    ap.add_argument("--per-patch-max", type=int, default=4096,
+                    help="skip the one-launch-per-patch organisation above this many patches (launch-bound: ~5 us each)")
     a = ap.parse_args()
     from paper_2508_05020_b200 import build as B
     B.build()
@@ -73,6 +75,10 @@ def main():
     for scheme, n in plan:
         for variant in (0, 1, 2, 3):
             for graphs in (0, 1):
+                if variant == 3 and (a.N // n) ** 2 > a.per_patch_max:
+                    rows.append(dict(scheme=scheme, n=n, stage_kernel=variant, use_graphs=graphs, ms_per_step=None,
+                                     skipped=f"{(a.N // n) ** 2} patches > --per-patch-max"))
+                    continue
                 r = time_config(a.N, n, scheme, variant, graphs, a.steps, a.warmup, stream)
                 r.update(scheme=scheme, n=n, stage_kernel=variant, use_graphs=graphs)
                 rows.append(r)
@@ -87,12 +93,14 @@ def main():
     for scheme, n in plan:
         sel = {(r["stage_kernel"], r["use_graphs"]): r["ms_per_step"] for r in rows if r["scheme"] == scheme and r["n"] == n}
         best = min(sel[(0, 0)], sel[(0, 1)])
+        pp = sel[(3, 0)] is not None
         out.setdefault("speedups", []).append({
             "scheme": scheme, "n": n,
             "fused_vs_unfused": sel[(2, 0)] / sel[(0, 0)],
-            "fused_vs_per_patch_launches": sel[(3, 0)] / sel[(0, 0)],
-            "fused_vs_per_patch_graph": sel[(3, 1)] / best,
-            "graphs_on_per_patch": sel[(3, 0)] / sel[(3, 1)]})
+            "fused_vs_unfused_graphs": sel[(2, 1)] / sel[(0, 1)],
+            "fused_vs_per_patch_launches": sel[(3, 0)] / sel[(0, 0)] if pp else None,
+            "fused_vs_per_patch_graph": sel[(3, 1)] / best if pp else None,
+            "graphs_on_per_patch": sel[(3, 0)] / sel[(3, 1)] if pp else None})
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{a.tag}_fusion_study.json"), "w") as f:
         json.dump(out, f, indent=1)
