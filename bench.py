@@ -212,7 +212,9 @@ class Ctx:
             else:
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
         from paper_2508_05020_b200 import build as B
-        if self.rank == 0:   # the library of this source tree (an mtime no-op when it is fresh)
+        # the library of this source tree (an mtime no-op when it is fresh); AMR_NO_BUILD=1 keeps a swapped-in prebuilt
+        # library (A/B of two builds, scripts/ab_so.sh)
+        if self.rank == 0 and os.environ.get("AMR_NO_BUILD", "0") != "1":
             B.build()
         self.barrier()
         import paper_2508_05020_b200 as amr
