@@ -2327,7 +2327,8 @@ __global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntas
 __global__ void __launch_bounds__(kGhostThreads) ghost_tile_kernel(const ProxyTask* __restrict__ tasks, int g,
                                                                   const AuxArgs a) {
     extern __shared__ double cs[];   // [4][ry span][rx span]
-    ghost_strip(tasks[blockIdx.x], g, a, cs, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+    const ProxyTask pt = tasks[blockIdx.x];
+    ghost_strip(pt, g, a, cs, threadIdx.x, blockDim.x, [] { __syncthreads(); });
 }
 
 // O12 correction of one coarse boundary cell (work item t of 4 n per reflux task); Lambda (stage 3) into lam
@@ -2425,7 +2426,8 @@ __global__ void __launch_bounds__(kPostThreads) post_stage_kernel(const PostArgs
     double* cs = post_cs + (size_t)wib * 4 * (p.g / 2 + 2) * (n / 2 + 2);
     const int nw = gridDim.x * (kPostThreads / 32);
     for (int task = blockIdx.x * (kPostThreads / 32) + wib; task < p.np; task += nw) {
-        ghost_strip(p.ptasks[task], p.g, p.a, cs, lane, 32, [] { __syncwarp(); });
+        const ProxyTask pt = p.ptasks[task];   // (a private copy: the strip code re-reads the task's fields)
+        ghost_strip(pt, p.g, p.a, cs, lane, 32, [] { __syncwarp(); });
         __syncwarp();   // cs is reused by the warp's next strip
     }
 }
