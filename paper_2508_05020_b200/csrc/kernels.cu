@@ -939,9 +939,10 @@ constexpr size_t kTmaGroupSmem = kTmaSmem - 96 + 3 * 16 * 32;   // member descri
 // of the normal / tangential velocity), Central4 edge fluxes, and Eq. 9 F-hat at the 5 faces with f(m0-1) and
 // f(m0+5) from the neighbouring segments' lanes, plus F-hat(m0+5) from the next segment (s unused: the values
 // shuffled in across the line ends are garbage and never used).
-template <bool DIV4, int PL = kTmaPL>
+template <bool DIV4>
 __device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs, int kn, int kt, double inv_gm1,
                                            int s, double (&Fh)[6][4]) {
+    constexpr int PL = kTmaPL;
     double p[4], Tt[4], un[4], ut[4];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -1328,317 +1329,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #endif
 }
 
-// ---------------------------------------------------------------- warp-specialised Central4 kernel (round 2)
-// The per-tile kernel above runs its phases one after another on all 16 warps (cons->prim, faces, epilogue: the
-// fp64 pipe idles in the shared-memory-bound phases).  Here two warp groups pipeline them across tiles:
-//   Y (warps 8-15): wait for tile k's TMA landing -> cons->prim into prim[k % 2] (keeping U^(s-1) of its cells in
-//     registers) -> re-issue the landing for tile k+1 -> epilogue of tile k-1 (L[(k-1) % 2], U^n from L2);
-//   X (warps 0-7): x faces of tile k (L = L_x) -> y faces (L += L_y) on prim[k % 2] / L[k % 2].
-// So the face passes of tile k overlap the conversion of tile k+1 and the epilogue of tile k-1.  Named barriers
-// hand buffers between the groups (ids 1-8, two per buffer pair), 9 / 10 are group-internal.  The arithmetic of
-// every cell is the per-tile kernel's (c4_segment, L_x + L_y, U + dt L, the RK combination), so results are
-// bitwise equal.  Shared memory: one landing buffer, two prim planes (rows -3..34), two L planes.
-constexpr int kWsRows = kTmaT + 6;                        // prim rows -3 .. 34 (S / N strips are 3 deep)
-constexpr int kWsPL = kWsRows * kTmaWP;                   // one prim plane
-constexpr int kWsLS = 34;                                 // L plane row stride
-constexpr size_t kWsSmem = sizeof(double) * (kLandSz + 2 * 4 * kWsPL + 2 * 4 * kTmaT * kWsLS) + 16 + 3 * 32 + 128;
-
-__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-template <int N, bool DIV4>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-    stage_c4_ws_kernel(const StageArgs a, const __grid_constant__ C4Maps maps, const int ntiles) {
-    constexpr int T = kTmaT, G = kGL, TILES = N / T, TT = TILES * TILES;
-    constexpr int NN = N * N, PS = 4 * NN;
-    constexpr int WP = kTmaWP, PL = kWsPL, LS = kWsLS;
-    constexpr int B_PREADY = 1, B_PFREE = 3, B_LREADY = 5, B_LFREE = 7, B_X = 9, B_Y = 10;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* const land = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-    double* const prim0 = land + kLandSz;                 // [2][4][PL]: cell (j, i) at (j + 3) * WP + i + G
-    double* const L0 = prim0 + 2 * 4 * PL;                // [2][4][T][LS]: L = L_x + L_y of cell (i, j)
-    uint64_t* const mbar = reinterpret_cast<uint64_t*>(L0 + 2 * 4 * T * LS);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool xg = warp < 8;
-    const double g = a.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
-    const bool rk_un = a.stage > 1;
-    const double ca = a.a, cb = a.b;
-    const double dt = *a.dt;
-    const int cnt = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    auto tile_of = [&](int k) { return (int)blockIdx.x + k * (int)gridDim.x; };
-    auto desc_of = [&](int k) { const int t = tile_of(k); return a.leaves + (TILES == 1 ? t : t / TT); };
-
-    auto issue = [&](int t, const LeafDesc& d) {   // the per-tile kernel's TMA boxes, into the single landing buffer
-        const int tt = TILES == 1 ? 0 : t % TT;
-        const int tx = tt % TILES, ty = tt / TILES;
-        const uint32_t mb = smem_u32(&mbar[0]);
-        const uint32_t dst = smem_u32(land);
-        mbar_expect_tx(mb, (kLandSz - 2 * 4 * T) * 8);
-        tma_load3(dst + kLandI * 8, &maps.in_int, tx * T, ty * T, 4 * d.slot, mb);
-        const CUtensorMap* mw = &maps.in_we;
-        int i0 = tx * T - G, z = 4 * d.slot;
-        auto peer = [&](int side) { return (d.pad >> (8 + 3 * side)) & 7; };
-        if (tx == 0) {
-            i0 = N - G; const int s = d.side[kW];
-            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kW)) mw = &maps.peer_we[peer(kW)]; }
-            else { z = 4 * (-1 - s); mw = &maps.px_we; }
-        }
-        tma_load3(dst + kLandW * 8, mw, i0, ty * T, z, mb);
-        mw = &maps.in_we; i0 = tx * T + T; z = 4 * d.slot;
-        if (tx == TILES - 1) {
-            i0 = 0; const int s = d.side[kE];
-            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kE)) mw = &maps.peer_we[peer(kE)]; }
-            else { z = 4 * (-1 - s); mw = &maps.px_we; }
-        }
-        tma_load3(dst + kLandE * 8, mw, i0, ty * T, z, mb);
-        const CUtensorMap* ms = &maps.in_sn;
-        int j0 = ty * T - (G - 1); z = 4 * d.slot;
-        if (ty == 0) {
-            j0 = N - (G - 1); const int s = d.side[kS];
-            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kS)) ms = &maps.peer_sn[peer(kS)]; }
-            else { z = 4 * (-1 - s); ms = &maps.px_sn; }
-        }
-        tma_load3(dst + kLandS * 8, ms, tx * T, j0, z, mb);
-        ms = &maps.in_sn; j0 = ty * T + T; z = 4 * d.slot;
-        if (ty == TILES - 1) {
-            j0 = 0; const int s = d.side[kN];
-            if (s >= 0) { z = 4 * s; if (d.pad & (16 << kN)) ms = &maps.peer_sn[peer(kN)]; }
-            else { z = 4 * (-1 - s); ms = &maps.px_sn; }
-        }
-        tma_load3(dst + kLandN * 8, ms, tx * T, j0, z, mb);
-        if (rk_un) tma_prefetch3(&maps.un_int, tx * T, ty * T, 4 * d.slot);   // U^n of the tile towards L2
-    };
-
-    if (tid == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_int)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_we)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.in_sn)) : "memory");
-        mbar_init(smem_u32(&mbar[0]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (cnt == 0) return;
-    if (tid == 256) issue(tile_of(0), *desc_of(0));
-
-    if (xg) {
-        // ================= X: face passes
-        const int seg_line = lane & 3, seg = lane < 28 ? lane >> 2 : 6;
-        const bool seg_store = lane < 28;
-        const int m0 = seg * 5 - 1;
-        LeafDesc dn = load_desc_early(desc_of(0));
-        for (int k = 0; k < cnt; ++k) {
-            const int b = k & 1, t = tile_of(k);
-            const LeafDesc d = dn;
-            if (k + 1 < cnt) dn = load_desc_early(desc_of(k + 1));
-            const int tt = TILES == 1 ? 0 : t % TT;
-            const int tx = tt % TILES, ty = tt / TILES;
-            const double* prim = prim0 + b * 4 * PL;
-            double* L = L0 + b * 4 * T * LS;
-            nbar_sync(B_PREADY + b, 512);                 // prim[b] holds tile k
-            if (k >= 2) nbar_sync(B_LFREE + b, 512);      // the epilogue of tile k-2 has read L[b]
-            const int lvl = d.level;
-            const int sm = (d.cf | (d.cf >> 4)) & 15;
-            double Fh[6][4];
-            {   // x faces: row j, faces m0 .. m0+4
-                const int j = 4 * warp + seg_line;
-                const double idx = 0.0625 * a.geo.inv_dx[lvl];   // F-hat arrive scaled by 16 (c4_face16)
-                c4_segment<DIV4, PL>(prim + (j + 3) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
-                if (seg_store) {
-#pragma unroll
-                    for (int e = 0; e < 5; ++e)
-                        if (m0 + e >= 0 && m0 + e < T)
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) L[(q * T + j) * LS + m0 + e] = -(Fh[e + 1][q] - Fh[e][q]) * idx;
-                    if (sm & 3) {   // flux registers of coarse/fine x sides: F-hat at faces 0 and T
-#pragma unroll
-                        for (int e = 0; e < 5; ++e)
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                if (m0 + e == 0 && tx == 0 && (sm & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + j] = 0.0625 * Fh[e][q];
-                                if (m0 + e == T && tx == TILES - 1 && (sm & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + j] = 0.0625 * Fh[e][q];
-                            }
-                    }
-                }
-            }
-            nbar_sync(B_X, 256);                          // L = L_x complete
-            {   // y faces: column i, faces m0 .. m0+4; L += L_y
-                const int i = 4 * warp + seg_line;
-                const double idy = 0.0625 * a.geo.inv_dy[lvl];
-                c4_segment<DIV4, PL>(prim + (m0 + 3) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
-                if (seg_store) {
-#pragma unroll
-                    for (int e = 0; e < 5; ++e)
-                        if (m0 + e >= 0 && m0 + e < T) {
-                            double* o = L + (m0 + e) * LS + i;
-                            o[0 * T * LS] = o[0 * T * LS] + -(Fh[e + 1][0] - Fh[e][0]) * idy;
-                            o[1 * T * LS] = o[1 * T * LS] + -(Fh[e + 1][2] - Fh[e][2]) * idy;
-                            o[2 * T * LS] = o[2 * T * LS] + -(Fh[e + 1][1] - Fh[e][1]) * idy;
-                            o[3 * T * LS] = o[3 * T * LS] + -(Fh[e + 1][3] - Fh[e][3]) * idy;
-                        }
-                    if (sm & 12) {
-#pragma unroll
-                        for (int e = 0; e < 5; ++e) {
-                            const double Fu[4] = {0.0625 * Fh[e][0], 0.0625 * Fh[e][2], 0.0625 * Fh[e][1], 0.0625 * Fh[e][3]};
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                if (m0 + e == 0 && ty == 0 && (sm & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + q) * N + tx * T + i] = Fu[q];
-                                if (m0 + e == T && ty == TILES - 1 && (sm & 8)) a.freg[(((size_t)d.slot * 4 + kN) * 4 + q) * N + tx * T + i] = Fu[q];
-                            }
-                        }
-                    }
-                }
-            }
-            nbar_arrive(B_LREADY + b, 512);                        // L[b] = L_x + L_y of tile k
-            if (k + 2 < cnt) nbar_arrive(B_PFREE + b, 512);        // prim[b] may take tile k+2
-        }
-        return;
-    }
-
-    // ================= Y: conversion, landing re-issue, epilogue
-    const int wy = warp - 8;
-    const int cr = 2 * wy + (lane >> 4), cc = 2 * (lane & 15);   // interior pairs (cr, cc..cc+1), (cr+16, ..)
-    unsigned long long lam = 0ull;
-    auto convert = [&](int k, double (&uc)[2][2][4]) {
-        const int b = k & 1;
-        double* prim = prim0 + b * 4 * PL;
-        if (k >= 2) nbar_sync(B_PFREE + b, 512);          // the faces of tile k-2 are done with prim[b]
-        mbar_wait(smem_u32(&mbar[0]), (uint32_t)(k & 1));
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int r = cr + 16 * h;
-            const double* s0 = land + kLandI + r * T + cc;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double2 v = *reinterpret_cast<const double2*>(s0 + q * T * T);
-                uc[h][0][q] = v.x;
-                uc[h][1][q] = v.y;
-            }
-            double pr[4][2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double ir = fast_rcp(uc[h][e][0]);
-                const double u = uc[h][e][1] * ir, v = uc[h][e][2] * ir;
-                const double p = gm1 * (uc[h][e][3] - 0.5 * (uc[h][e][1] * u + uc[h][e][2] * v));
-                pr[0][e] = p; pr[1][e] = p * ir; pr[2][e] = u; pr[3][e] = v;
-            }
-            const int o = (r + 3) * WP + cc + G;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) *reinterpret_cast<double2*>(prim + q * PL + o) = make_double2(pr[q][0], pr[q][1]);
-        }
-        {   // strips: W/E 2 x 64 and S/N (3 rows) 2 x 48 adjacent cell pairs, one per thread 0-223 of the group
-            const int P = wy * 32 + lane;
-            if (P < 224) {
-                int off, i, j, ps;
-                if (P < 128) {
-                    const int wg = P >> 6, e = P & 63;
-                    j = e >> 1; const int c = (e & 1) * 2;
-                    off = (wg == 0 ? kLandW : kLandE) + j * G + c; i = wg == 0 ? c - G : T + c; ps = G * T;
-                } else {
-                    const int h = P - 128, wg = h >= 48, e = h - 48 * wg, rr = e >> 4;
-                    i = (e & 15) * 2;
-                    off = (wg == 0 ? kLandS : kLandN) + rr * T + i; j = wg == 0 ? rr - (G - 1) : T + rr; ps = (G - 1) * T;
-                }
-                double2 cv[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) cv[q] = *reinterpret_cast<const double2*>(land + off + q * ps);
-                double pr[4][2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const double r = h ? cv[0].y : cv[0].x, m = h ? cv[1].y : cv[1].x;
-                    const double w = h ? cv[2].y : cv[2].x, E = h ? cv[3].y : cv[3].x;
-                    const double ir = fast_rcp(r);
-                    const double u = m * ir, v = w * ir;
-                    const double p = gm1 * (E - 0.5 * (m * u + w * v));
-                    pr[0][h] = p; pr[1][h] = p * ir; pr[2][h] = u; pr[3][h] = v;
-                }
-                if (j >= -3 && j <= T + 2) {   // (row -4 / T+3 of the W/E strips is never read; the rows exist)
-                    const int o = (j + 3) * WP + i + G;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) *reinterpret_cast<double2*>(prim + q * PL + o) = make_double2(pr[q][0], pr[q][1]);
-                }
-            }
-        }
-        nbar_arrive(B_PREADY + b, 512);                   // prim[b] holds tile k
-        nbar_sync(B_Y, 256);                              // every Y thread is done with the landing buffer
-        if (tid == 256 && k + 1 < cnt) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(tile_of(k + 1), *desc_of(k + 1));
-        }
-    };
-    auto epilogue = [&](int k, const double (&uc)[2][2][4]) {
-        const int b = k & 1, t = tile_of(k);
-        const LeafDesc d = *desc_of(k);
-        const int tt = TILES == 1 ? 0 : t % TT;
-        const int tx = tt % TILES, ty = tt / TILES;
-        const double* L = L0 + b * 4 * T * LS;
-        const int lvl = d.level;
-        const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
-        const bool x_lo = tx == 0, x_hi = tx == TILES - 1, y_lo = ty == 0, y_hi = ty == TILES - 1;
-        const int coarse_mask = d.cf & 15;
-        nbar_sync(B_LREADY + b, 512);                     // L[b] = L_x + L_y of tile k
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int r = cr + 16 * h;
-            double2 un[4];
-            if (rk_un)   // U^n from L2 (prefetched towards it by the tile's TMA issue)
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    un[q] = __ldg(reinterpret_cast<const double2*>(a.Un + (size_t)d.slot * PS + ((size_t)q * N + ty * T + r) * N +
-                                                                   tx * T + cc));
-            double out[2][4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double2 l2 = *reinterpret_cast<const double2*>(L + (q * T + r) * LS + cc);
-                double v0 = uc[h][0][q] + dt * l2.x, v1 = uc[h][1][q] + dt * l2.y;
-                if (rk_un) {
-                    v0 = ca * un[q].x + cb * v0;
-                    v1 = ca * un[q].y + cb * v1;
-                }
-                out[0][q] = v0;
-                out[1][q] = v1;
-                *reinterpret_cast<double2*>(a.Uout + (size_t)d.slot * PS + ((size_t)q * N + ty * T + r) * N + tx * T + cc) =
-                    make_double2(v0, v1);
-            }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int j = r, i = cc + e;
-                const bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && i == 0) || ((coarse_mask & 2) && x_hi && i == T - 1) ||
-                                                     ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
-                if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
-                    if (a.check && !physical_state(out[e][0], out[e][1], out[e][2], out[e][3], g))
-                        report_error(a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + i);
-                    if (a.want_lambda) {
-                        double sp = wave_speed(out[e][0], out[e][1], out[e][2], out[e][3], g, idx, idy);
-                        if (a.lam0) sp = ldexp(sp, -d.level);   // subcycling: level-0-normalised (S6)
-                        const unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
-                        lam = bits > lam ? bits : lam;
-                    }
-                }
-            }
-        }
-        if (k + 2 < cnt) nbar_arrive(B_LFREE + b, 512);   // L[b] may take tile k+2
-    };
-    double ucA[2][2][4], ucB[2][2][4];
-    convert(0, ucA);
-    for (int k = 1; k < cnt; k += 2) {
-        convert(k, ucB);
-        epilogue(k - 1, ucA);
-        if (k + 1 < cnt) {
-            convert(k + 1, ucA);
-            epilogue(k, ucB);
-        } else {
-            epilogue(k, ucB);
-            break;
-        }
-    }
-    if (cnt % 2 == 1) epilogue(cnt - 1, ucA);
-    if (a.want_lambda) {
-        lam = warp_max_u64(lam);
-        if (lane == 0 && lam) atomicMax(a.lambda_bits, lam);
-    }
-}
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1680,46 +1370,8 @@ int sm_count() {
     return n;
 }
 
-// A/B switch of the warp-specialised kernel (AMR_C4_WS=1) while it is evaluated
-bool c4_ws_enabled() {
-    static const bool on = [] { const char* e = getenv("AMR_C4_WS"); return e && e[0] == '1'; }();
-    return on;
-}
-
-template <int N, bool DIV4>
-cudaError_t launch_c4_ws_t(const StageArgs& a, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(stage_c4_ws_kernel<N, DIV4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kWsSmem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    const int ntiles = a.nleaves * (N / kTmaT) * (N / kTmaT);
-    if (ntiles == 0) return cudaSuccess;
-    C4Maps m;
-    const double* px = a.proxy ? a.proxy : a.Uin;
-    const int npx = a.proxy && a.nproxy > 0 ? a.nproxy : a.nslots;
-    if (!encode_pool_map(&m.in_int, a.Uin, N, a.nslots, kTmaT, kTmaT) ||
-        !encode_pool_map(&m.in_we, a.Uin, N, a.nslots, kGL, kTmaT) ||
-        !encode_pool_map(&m.in_sn, a.Uin, N, a.nslots, kTmaT, kGL - 1) ||
-        !encode_pool_map(&m.px_we, px, N, npx, kGL, kTmaT) ||
-        !encode_pool_map(&m.px_sn, px, N, npx, kTmaT, kGL - 1) ||
-        !encode_pool_map(&m.un_int, a.Un, N, a.nslots, kTmaT, kTmaT) ||
-        !encode_pool_map(&m.out_int, a.Uout, N, a.nslots, kTmaT, kTmaT))
-        return cudaErrorInvalidValue;
-    for (int q = 0; q < a.npeers && q < 8; ++q)
-        if (!encode_pool_map(&m.peer_we[q], a.peer_in[q], N, a.nslots, kGL, kTmaT) ||
-            !encode_pool_map(&m.peer_sn[q], a.peer_in[q], N, a.nslots, kTmaT, kGL - 1))
-            return cudaErrorInvalidValue;
-    const int grid = ntiles < sm_count() ? ntiles : sm_count();
-    stage_c4_ws_kernel<N, DIV4><<<grid, kTmaThreads, kWsSmem, s>>>(a, m, ntiles);
-    return cudaGetLastError();
-}
-
 template <int N, bool DIV4>
 cudaError_t launch_c4_tma_t(const StageArgs& a, cudaStream_t s) {
-    if (c4_ws_enabled()) return launch_c4_ws_t<N, DIV4>(a, s);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(stage_c4_tma_kernel<N, DIV4>,
