@@ -148,6 +148,23 @@ def test_nonphysical_step_not_committed():
     assert np.array_equal(before, g.get_state(as_dict=False))
 
 
+def test_steps_report_a_nonphysical_state_late_without_rollback():
+    """include/amr.h amr_steps: a non-physical state in a batch is reported by the next amr_sync (AMR_E_NONPHYSICAL),
+    and the mesh keeps the advanced state (no rollback, unlike amr_step)."""
+    cfg = W.sweep(N=64, n=16, scheme="central4", seed=5)
+    g = amr.Mesh(cfg)
+    U0 = W.level0_state(cfg).reshape(-1, 4, 16, 16).copy()
+    U0[5, 0, 3, 3] = -1.0
+    g.set_state(U=U0)
+    before = g.get_state(as_dict=False)
+    g.steps(3, dt=1e-4)              # queued: no error yet
+    with pytest.raises(amr.AmrError) as ei:
+        g.sync()
+    assert ei.value.code == amr.AMR_E_NONPHYSICAL
+    assert not np.array_equal(before, g.get_state(as_dict=False))
+    assert g.stats()["steps"] == 3
+
+
 def test_capacity_error_leaves_mesh_unchanged():
     cfg = dict(W.quadrant(N=64, n=16, levels=3), max_patches=20)
     g = amr.Mesh(cfg)
