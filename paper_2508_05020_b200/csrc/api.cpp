@@ -383,11 +383,40 @@ amr_status build_plan(amr_ctx* c) {
     clk.mark("plan: descriptors");
 
     cudaStream_t s = c->stream;
-    CU(c->d_leaves.upload(c->leaves, s));
-    CU(c->d_gleaves.upload(c->gleaves, s));
-    CU(c->d_singles.upload(c->singles, s));
-    CU(c->d_ptasks.upload(c->ptasks, s));
-    CU(c->d_rtasks.upload(c->rtasks, s));
+    {   // one packed upload of the per-plan descriptor arrays (each 256-byte aligned in the arena)
+        std::vector<char>& H = c->arena_host;
+        H.clear();
+        std::vector<size_t> offs;
+        auto add = [&](const void* src, size_t bytes) {
+            const size_t o = (H.size() + 255) & ~(size_t)255;
+            H.resize(o + bytes);
+            if (bytes) std::memcpy(H.data() + o, src, bytes);
+            offs.push_back(o);
+        };
+        add(c->leaves.data(), c->leaves.size() * sizeof(LeafDesc));
+        add(c->gleaves.data(), c->gleaves.size() * sizeof(LeafDesc));
+        add(c->singles.data(), c->singles.size() * sizeof(LeafDesc));
+        add(c->ptasks.data(), c->ptasks.size() * sizeof(ProxyTask));
+        add(c->rtasks.data(), c->rtasks.size() * sizeof(RefluxTask));
+        for (int l = 0; l < L; ++l) add(c->rlev[l].data(), c->rlev[l].size() * sizeof(RestrictTask));
+        add(c->sib.data(), c->sib.size() * sizeof(int32_t));
+        // the views must not alias the arena while it is re-allocated
+        c->d_leaves.release(); c->d_gleaves.release(); c->d_singles.release(); c->d_ptasks.release();
+        c->d_rtasks.release(); c->d_sib.release();
+        for (auto& d : c->d_rlev) d.release();
+        CU(c->arena_dev.reserve(std::max<size_t>(H.size(), 256)));
+        if (!H.empty()) CU(cudaMemcpyAsync(c->arena_dev.p, H.data(), H.size(), cudaMemcpyHostToDevice, s));
+        char* base = c->arena_dev.p;
+        size_t k = 0;
+        c->d_leaves.view(reinterpret_cast<LeafDesc*>(base + offs[k++]), c->leaves.size());
+        c->d_gleaves.view(reinterpret_cast<LeafDesc*>(base + offs[k++]), c->gleaves.size());
+        c->d_singles.view(reinterpret_cast<LeafDesc*>(base + offs[k++]), c->singles.size());
+        c->d_ptasks.view(reinterpret_cast<ProxyTask*>(base + offs[k++]), c->ptasks.size());
+        c->d_rtasks.view(reinterpret_cast<RefluxTask*>(base + offs[k++]), c->rtasks.size());
+        c->d_rlev.resize(L);
+        for (int l = 0; l < L; ++l) c->d_rlev[l].view(reinterpret_cast<RestrictTask*>(base + offs[k++]), c->rlev[l].size());
+        c->d_sib.view(reinterpret_cast<int32_t*>(base + offs[k++]), c->sib.size());
+    }
     if (c->cfg.subcycle) {
         CU(c->d_sub_descs.upload(c->sub_descs, s));
         CU(c->d_sub_ptasks.upload(c->sub_ptasks, s));
@@ -395,13 +424,11 @@ amr_status build_plan(amr_ctx* c) {
         CU(c->sub_proxy.reserve(std::max<size_t>(1, c->sub_ptasks.size()) * c->PS));
         CU(c->facc.reserve((size_t)t.capacity * 16 * c->n, false));
     }
-    c->d_rlev.resize(L);
-    for (int l = 0; l < L; ++l) CU(c->d_rlev[l].upload(c->rlev[l], s));
+
     CU(c->proxy.reserve(std::max<size_t>(1, c->ptasks.size()) * c->PS));
     CU(c->freg.reserve((size_t)t.capacity * 16 * c->n, false));   // indexed by slot (remote fine leaves arrive by exchange)
     CU(c->d_maxeta.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_amb.reserve(std::max<size_t>(1, c->leaves.size())));
-    CU(c->d_sib.upload(c->sib, c->stream));
     CU(c->d_flist.reserve(2 * (c->leaves.size() + c->sib.size() / 5) + 2));
     CU(c->d_fcount.reserve(1));
     CU(c->d_partial.reserve(4 * std::max<size_t>(1, c->leaves.size())));
@@ -1051,6 +1078,7 @@ void amr_destroy(amr_ctx* c) {
     c->proxy.release(); c->freg.release(); c->staging.release(); c->d_maxeta.release(); c->d_partial.release();
     c->unf_scratch.release();
     c->d_slots.release(); c->d_amb.release(); c->d_sib.release(); c->d_flist.release(); c->d_fcount.release();
+    c->arena_dev.release();
     if (c->own_pool) cudaFree(c->own_pool);
     cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp); cudaFree(c->d_dtp);
     for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);

@@ -17,22 +17,31 @@ template <class T>
 struct DevArray {
     T* p = nullptr;
     size_t cap = 0, count = 0;
+    bool owned = true;         // false: a view into a PlanArena (not freed here)
     DevArray() = default;
     DevArray(const DevArray&) = delete;
     DevArray& operator=(const DevArray&) = delete;
-    DevArray(DevArray&& o) noexcept : p(o.p), cap(o.cap), count(o.count) {
-        o.p = nullptr; o.cap = o.count = 0;
+    DevArray(DevArray&& o) noexcept : p(o.p), cap(o.cap), count(o.count), owned(o.owned) {
+        o.p = nullptr; o.cap = o.count = 0; o.owned = true;
     }
     DevArray& operator=(DevArray&& o) noexcept {
         if (this != &o) {
             release();
-            p = o.p; cap = o.cap; count = o.count;
-            o.p = nullptr; o.cap = o.count = 0;
+            p = o.p; cap = o.cap; count = o.count; owned = o.owned;
+            o.p = nullptr; o.cap = o.count = 0; o.owned = true;
         }
         return *this;
     }
     ~DevArray() { release(); }   // every device / pinned buffer of a ctx is freed with it
+    // point into memory owned elsewhere (the plan arena); drops an owned buffer first
+    void view(T* ptr, size_t n) {
+        release();
+        p = ptr;
+        count = n;
+        owned = false;
+    }
     cudaError_t upload(const std::vector<T>& v, cudaStream_t s) {
+        if (!owned) { p = nullptr; cap = 0; owned = true; }
         count = v.size();
         if (v.size() > cap) {   // grow with 50 % slack: regrids that add a few patches do not reallocate
             if (p) cudaFree(p);
@@ -56,9 +65,10 @@ struct DevArray {
         return e;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p && owned) cudaFree(p);
         p = nullptr;
         cap = count = 0;
+        owned = true;
     }
 };
 
@@ -105,6 +115,10 @@ struct amr_ctx {
     DevArray<ProxyTask> d_ptasks;
     DevArray<RefluxTask> d_rtasks;
     std::vector<DevArray<RestrictTask>> d_rlev;
+    // the per-plan descriptor arrays packed into ONE host buffer and ONE device buffer (one H2D copy per plan; the
+    // DevArrays above are views into it)
+    std::vector<char> arena_host;
+    DevArray<char> arena_dev;
     DevArray<ProlongTask> d_prolong;
     DevArray<double> proxy, freg, staging, d_maxeta, d_partial, unf_scratch;
     DevArray<int32_t> d_slots, d_amb, d_sib, d_flist, d_fcount;

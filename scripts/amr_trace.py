@@ -12,7 +12,9 @@ import workloads as W  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "q"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-cfg = W.shock_bubble(max_patches=100_000) if which == "sb" else W.quadrant(N=512, n=16, levels=3, seed=1)
+cfg = (W.shock_bubble(max_patches=100_000) if which in ("sb", "sbs") else W.quadrant(N=512, n=16, levels=3, seed=1))
+if which == "sbs":   # with Berger-Colella subcycling
+    cfg["subcycle"] = 1
 out = os.environ["AMR_TRACE"]
 if os.path.exists(out):
     os.remove(out)
