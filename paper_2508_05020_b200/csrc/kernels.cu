@@ -53,13 +53,6 @@ __device__ __forceinline__ double fast_sqrt(double x) {
     return fma(r, 0.5 * y, s);
 }
 
-__device__ __forceinline__ bool physical_state(double r, double m, double w, double E, double g) {
-    double u = m / r, v = w / r;
-    double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
-    return r > 0.0 && p > 0.0 && isfinite(r) && isfinite(m) && isfinite(w) && isfinite(E) && isfinite(u) &&
-           isfinite(v) && isfinite(p);
-}
-
 __device__ __forceinline__ double wave_speed(double r, double m, double w, double E, double g, double idx,
                                              double idy) {
     double ir = fast_rcp(r);
@@ -83,6 +76,27 @@ __device__ __forceinline__ void report_error(int32_t* err, int slot, int stage, 
         err[1] = slot;
         err[2] = stage;
         err[3] = cell;
+    }
+}
+
+// S5 positivity check and, at the last stage, the O13 wave speed of a new leaf state from ONE reciprocal of rho
+// (A41: the check's velocities use the <= 1 ulp reciprocal of cons->prim instead of two IEEE divisions with their
+// slow-path calls; the speed is wave_speed()'s arithmetic)
+__device__ __forceinline__ void leaf_check(double r, double m, double w, double E, double g, double idx, double idy,
+                                           bool check, bool want_lambda, int lam_shift, int32_t* err, int slot,
+                                           int stage, int cell, unsigned long long& lam) {
+    const double ir = fast_rcp(r);
+    const double u = m * ir, v = w * ir;
+    const double p = (g - 1.0) * (E - 0.5 * (m * u + w * v));
+    if (check && !(r > 0.0 && p > 0.0 && isfinite(r) && isfinite(m) && isfinite(w) && isfinite(E) && isfinite(u) &&
+                   isfinite(v) && isfinite(p)))
+        report_error(err, slot, stage, cell);
+    if (want_lambda) {
+        const double c = fast_sqrt(g * p * ir);
+        double sp = (fabs(u) + c) * idx + (fabs(v) + c) * idy;
+        if (lam_shift) sp = ldexp(sp, -lam_shift);   // subcycling: level-0-normalised (S6)
+        const unsigned long long b = (unsigned long long)__double_as_longlong(sp);
+        lam = b > lam ? b : lam;
     }
 }
 
@@ -470,14 +484,9 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             bool edge_cf = ((coarse_mask & 1) && x_lo && i == 0) || ((coarse_mask & 2) && x_hi && i == T - 1) ||
                            ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1);
             if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
-                if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], g))
-                    report_error(a.err, d.slot, a.stage, (int)off);
-                if (a.want_lambda) {
-                    double s = wave_speed(o4[0], o4[1], o4[2], o4[3], g, idx, idy);
-                    if (a.lam0) s = ldexp(s, -d.level);
-                    unsigned long long b = (unsigned long long)__double_as_longlong(s);
-                    lam = b > lam ? b : lam;
-                }
+                if (a.check || a.want_lambda)
+                    leaf_check(o4[0], o4[1], o4[2], o4[3], g, idx, idy, a.check, a.want_lambda, a.lam0 ? d.level : 0,
+                               a.err, d.slot, a.stage, (int)off, lam);
             }
         }
     }
@@ -756,14 +765,9 @@ __global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 
         bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && ci == 0) || ((coarse_mask & 2) && x_hi && ci == T - 1) ||
                                        ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
         if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
-            if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
-                report_error(a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + ci);
-            if (a.want_lambda) {
-                double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
-                    if (a.lam0) sp = ldexp(sp, -d.level);   // subcycling: level-0-normalised (S6)
-                unsigned long long b = (unsigned long long)__double_as_longlong(sp);
-                lam = b > lam ? b : lam;
-            }
+            if (a.check || a.want_lambda)
+                leaf_check(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy, a.check, a.want_lambda,
+                           a.lam0 ? d.level : 0, a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + ci, lam);
         }
     }
     if (a.want_lambda) {
@@ -939,6 +943,10 @@ constexpr size_t kTmaGroupSmem = kTmaSmem - 96 + 3 * 16 * 32;   // member descri
 // of the normal / tangential velocity), Central4 edge fluxes, and Eq. 9 F-hat at the 5 faces with f(m0-1) and
 // f(m0+5) from the neighbouring segments' lanes, plus F-hat(m0+5) from the next segment (s unused: the values
 // shuffled in across the line ends are garbage and never used).
+// scale of the F-hat values c4_segment returns: 16 (c4_face16) x 24 (Eq. 9 as 26 f - (f- + f+)) with DIV4, else 16
+template <bool DIV4>
+__host__ __device__ constexpr double c4_fh_scale() { return DIV4 ? 1.0 / 384.0 : 0.0625; }
+
 template <bool DIV4>
 __device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs, int kn, int kt, double inv_gm1,
                                            int s, double (&Fh)[6][4]) {
@@ -963,12 +971,11 @@ __device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs,
         const double lo = __shfl_up_sync(0xffffffffu, f[4][k], 4);
         const double hi = __shfl_down_sync(0xffffffffu, f[0][k], 4);
         (void)s;
-        if (DIV4) {
-            const double c13 = 13.0 / 12.0, c24 = 1.0 / 24.0;
-            Fh[0][k] = c13 * f[0][k] - c24 * (lo + f[1][k]);
+        if (DIV4) {   // 24 F-hat = 26 f - (f- + f+): two operations per component instead of three
+            Fh[0][k] = fma(26.0, f[0][k], -(lo + f[1][k]));
 #pragma unroll
-            for (int e = 1; e < 4; ++e) Fh[e][k] = c13 * f[e][k] - c24 * (f[e - 1][k] + f[e + 1][k]);
-            Fh[4][k] = c13 * f[4][k] - c24 * (f[3][k] + hi);
+            for (int e = 1; e < 4; ++e) Fh[e][k] = fma(26.0, f[e][k], -(f[e - 1][k] + f[e + 1][k]));
+            Fh[4][k] = fma(26.0, f[4][k], -(f[3][k] + hi));
         } else {
 #pragma unroll
             for (int e = 0; e < 5; ++e) Fh[e][k] = f[e][k];
@@ -1198,7 +1205,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             double Fh[6][4];
             if (warp < 8) {
                 const int j = 4 * warp + seg_line;
-                const double idx = 0.0625 * a.geo.inv_dx[lvl];   // F-hat arrive scaled by 16 (c4_face16)
+                const double idx = c4_fh_scale<DIV4>() * a.geo.inv_dx[lvl];   // F-hat arrive scaled (c4_segment)
                 c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
@@ -1212,14 +1219,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         for (int e = 0; e < 5; ++e)
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                if (m0 + e == 0 && tx == 0 && (sm & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + j] = 0.0625 * Fh[e][q];
-                                if (m0 + e == T && tx == TILES - 1 && (sm & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + j] = 0.0625 * Fh[e][q];
+                                if (m0 + e == 0 && tx == 0 && (sm & 1)) a.freg[(((size_t)d.slot * 4 + kW) * 4 + q) * N + ty * T + j] = c4_fh_scale<DIV4>() * Fh[e][q];
+                                if (m0 + e == T && tx == TILES - 1 && (sm & 2)) a.freg[(((size_t)d.slot * 4 + kE) * 4 + q) * N + ty * T + j] = c4_fh_scale<DIV4>() * Fh[e][q];
                             }
                     }
                 }
             } else {
                 const int i = 4 * (warp - 8) + seg_line;
-                const double idy = 0.0625 * a.geo.inv_dy[lvl];
+                const double idy = c4_fh_scale<DIV4>() * a.geo.inv_dy[lvl];
                 c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
@@ -1235,7 +1242,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     if (sm & 12) {
 #pragma unroll
                         for (int e = 0; e < 5; ++e) {
-                            const double Fu[4] = {0.0625 * Fh[e][0], 0.0625 * Fh[e][2], 0.0625 * Fh[e][1], 0.0625 * Fh[e][3]};
+                            constexpr double fs = c4_fh_scale<DIV4>();
+                            const double Fu[4] = {fs * Fh[e][0], fs * Fh[e][2], fs * Fh[e][1], fs * Fh[e][3]};
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 if (m0 + e == 0 && ty == 0 && (sm & 4)) a.freg[(((size_t)d.slot * 4 + kS) * 4 + q) * N + tx * T + i] = Fu[q];
@@ -1299,14 +1307,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const bool edge_cf = coarse_mask && (((coarse_mask & 1) && x_lo && i == 0) || ((coarse_mask & 2) && x_hi && i == T - 1) ||
                                                  ((coarse_mask & 4) && y_lo && j == 0) || ((coarse_mask & 8) && y_hi && j == T - 1));
             if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
-                if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
-                    report_error(a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + i);
-                if (a.want_lambda) {
-                    double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
-                    if (a.lam0) sp = ldexp(sp, -d.level);   // subcycling: level-0-normalised (S6)
-                    const unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
-                    lam = bits > lam ? bits : lam;
-                }
+                if (a.check || a.want_lambda)
+                    leaf_check(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy, a.check, a.want_lambda,
+                               a.lam0 ? d.level : 0, a.err, d.slot, a.stage, (ty * T + j) * N + tx * T + i, lam);
             }
         }
         if (!kC4Stg) {   // (with direct stores, barrier (A) of the next tile orders the Lx / Ly reuse)
@@ -1541,10 +1544,9 @@ __global__ void unf_rk_kernel(const StageArgs a) {
                          ((coarse_mask & 4) && j == 0) || ((coarse_mask & 8) && j == n - 1);
     unsigned long long lam = 0ull;
     if (!edge_cf && !(d.pad & 1)) {   // covered patches (subcycling) are not leaves
-        if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], a.gamma)) report_error(a.err, d.slot, a.stage, c);
-        if (a.want_lambda)
-            lam = (unsigned long long)__double_as_longlong(a.lam0 ? ldexp(wave_speed(o4[0], o4[1], o4[2], o4[3], a.gamma, idx, idy), -d.level)
-                                                                  : wave_speed(o4[0], o4[1], o4[2], o4[3], a.gamma, idx, idy));
+        if (a.check || a.want_lambda)
+            leaf_check(o4[0], o4[1], o4[2], o4[3], a.gamma, idx, idy, a.check, a.want_lambda, a.lam0 ? d.level : 0,
+                       a.err, d.slot, a.stage, c, lam);
     }
     if (a.want_lambda) {
         lam = warp_max_u64(lam);
@@ -1746,7 +1748,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             double Fh[6][4];
             if (warp < 8) {
                 const int j = 4 * warp + seg_line;
-                const double idx = 0.0625 * a.geo.inv_dx[lvl];
+                const double idx = c4_fh_scale<DIV4>() * a.geo.inv_dx[lvl];
                 c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
@@ -1763,14 +1765,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         for (int e = 0; e < 5; ++e)
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                if (m0 + e == 0 && smw) a.freg[(((size_t)dw.slot * 4 + kW) * 4 + q) * N + j - r * N] = 0.0625 * Fh[e][q];
-                                if (m0 + e == T && sme) a.freg[(((size_t)de.slot * 4 + kE) * 4 + q) * N + j - r * N] = 0.0625 * Fh[e][q];
+                                if (m0 + e == 0 && smw) a.freg[(((size_t)dw.slot * 4 + kW) * 4 + q) * N + j - r * N] = c4_fh_scale<DIV4>() * Fh[e][q];
+                                if (m0 + e == T && sme) a.freg[(((size_t)de.slot * 4 + kE) * 4 + q) * N + j - r * N] = c4_fh_scale<DIV4>() * Fh[e][q];
                             }
                     }
                 }
             } else {
                 const int i = 4 * (warp - 8) + seg_line;
-                const double idy = 0.0625 * a.geo.inv_dy[lvl];
+                const double idy = c4_fh_scale<DIV4>() * a.geo.inv_dy[lvl];
                 c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
@@ -1789,7 +1791,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     if (sms | smn) {
 #pragma unroll
                         for (int e = 0; e < 5; ++e) {
-                            const double Fu[4] = {0.0625 * Fh[e][0], 0.0625 * Fh[e][2], 0.0625 * Fh[e][1], 0.0625 * Fh[e][3]};
+                            constexpr double fs = c4_fh_scale<DIV4>();
+                            const double Fu[4] = {fs * Fh[e][0], fs * Fh[e][2], fs * Fh[e][1], fs * Fh[e][3]};
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 if (m0 + e == 0 && sms) a.freg[(((size_t)ds.slot * 4 + kS) * 4 + q) * N + i - r * N] = Fu[q];
@@ -1830,14 +1833,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const bool edge_cf = cmask && (((cmask & 1) && ii == 0) || ((cmask & 2) && ii == N - 1) ||
                                            ((cmask & 4) && jj == 0) || ((cmask & 8) && jj == N - 1));
             if (!edge_cf) {
-                if (a.check && !physical_state(out[r][0], out[r][1], out[r][2], out[r][3], g))
-                    report_error(a.err, dm.slot, a.stage, cw[r]);
-                if (a.want_lambda) {
-                    double sp = wave_speed(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy);
-                    if (a.lam0) sp = ldexp(sp, -dm.level);   // subcycling: level-0-normalised (S6)
-                    const unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
-                    lam = bits > lam ? bits : lam;
-                }
+                if (a.check || a.want_lambda)
+                    leaf_check(out[r][0], out[r][1], out[r][2], out[r][3], g, idx, idy, a.check, a.want_lambda,
+                               a.lam0 ? dm.level : 0, a.err, dm.slot, a.stage, cw[r], lam);
             }
         }
         if (!kC4Stg) {
@@ -2044,13 +2042,9 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
         const bool edge_cf = ((cm & 1) && li == 0) || ((cm & 2) && li == N - 1) || ((cm & 4) && lj == 0) ||
                              ((cm & 8) && lj == N - 1);
         if (!edge_cf) {
-            if (a.check && !physical_state(o4[0], o4[1], o4[2], o4[3], g)) report_error(a.err, dm.slot, a.stage, (int)off);
-            if (a.want_lambda) {
-                double sp = wave_speed(o4[0], o4[1], o4[2], o4[3], g, idx, idy);
-                if (a.lam0) sp = ldexp(sp, -dm.level);
-                unsigned long long bits = (unsigned long long)__double_as_longlong(sp);
-                lam = bits > lam ? bits : lam;
-            }
+            if (a.check || a.want_lambda)
+                leaf_check(o4[0], o4[1], o4[2], o4[3], g, idx, idy, a.check, a.want_lambda, a.lam0 ? dm.level : 0,
+                           a.err, dm.slot, a.stage, (int)off, lam);
         }
     }
     if (a.want_lambda) {
@@ -2376,13 +2370,9 @@ __device__ __forceinline__ void reflux_cell(const RefluxTask* __restrict__ tasks
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) U[k * nn] = u[k];
-        if (a.check && !physical_state(u[0], u[1], u[2], u[3], a.gamma)) report_error(a.err, rt.slot, a.stage, j * n + i);
-        if (a.want_lambda) {
-            double sp = wave_speed(u[0], u[1], u[2], u[3], a.gamma, a.geo.inv_dx[l], a.geo.inv_dy[l]);
-            if (a.lam0) sp = ldexp(sp, -l);
-            const unsigned long long b = (unsigned long long)__double_as_longlong(sp);
-            lam = b > lam ? b : lam;
-        }
+        if (a.check || a.want_lambda)
+            leaf_check(u[0], u[1], u[2], u[3], a.gamma, a.geo.inv_dx[l], a.geo.inv_dy[l], a.check, a.want_lambda,
+                       a.lam0 ? l : 0, a.err, rt.slot, a.stage, j * n + i, lam);
     }
 }
 
