@@ -898,11 +898,6 @@ constexpr bool kC4Vec2 = false;
 #else
 constexpr bool kC4Vec2 = true;
 #endif
-#ifdef AMR_C4_STRIP_SCALAR   // A/B: strip conversion one cell per thread instead of pairs on half the lanes
-constexpr bool kC4StripPairs = false;
-#else
-constexpr bool kC4StripPairs = true;
-#endif
 #ifdef AMR_GHOST_PER_CELL   // A/B: the per-cell ghost kernel (every coarse value re-read by each fine cell)
 constexpr bool kGhostTile = false;
 #else
@@ -1142,36 +1137,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 c2p(uc[r][0], uc[r][1], uc[r][2], uc[r][3], (cj0 + r + G) * WP + ci + G);
             }
         }
-        static_assert(kC4Vec2 && kC4StripPairs, "the per-tile kernel converts cells in pairs");
-        {   // strips: W/E 2 x 64 and S/N (3 rows) 2 x 48 adjacent cell pairs, one per lane 0-15 of warps 0-13
-            const int P = warp * 16 + lane;
-            if (lane < 16 && P < 224) {
+        static_assert(kC4Vec2, "the per-tile kernel converts interior cells in pairs");
+        {   // strips: the 3 W / E columns and 3 S / N rows the faces read (cells -3..-1 and T..T+2; the TMA boxes
+            // land 4 columns, the outermost is never read), one cell per thread of warps 0-11
+            if (tid < 384) {
                 int off, i, j, ps;
-                if (P < 128) {
-                    const int wg = P >> 6, e = P & 63;
-                    j = e >> 1; const int c = (e & 1) * 2;
-                    off = (wg == 0 ? kLandW : kLandE) + j * G + c; i = wg == 0 ? c - G : T + c; ps = G * T;
+                if (tid < 192) {
+                    const int wg = tid >= 96, e = tid - 96 * wg, jj = e / 3, c = e - 3 * jj + (wg == 0 ? 1 : 0);
+                    off = (wg == 0 ? kLandW : kLandE) + jj * G + c; i = wg == 0 ? c - G : T + c; j = jj; ps = G * T;
                 } else {
-                    const int h = P - 128, wg = h >= 48, e = h - 48 * wg, rr = e >> 4;
-                    i = (e & 15) * 2;
+                    const int h = tid - 192, wg = h >= 96, e = h - 96 * wg, rr = e >> 5;
+                    i = e & 31;
                     off = (wg == 0 ? kLandS : kLandN) + rr * T + i; j = wg == 0 ? rr - (G - 1) : T + rr; ps = (G - 1) * T;
                 }
-                double2 cv[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) cv[q] = *reinterpret_cast<const double2*>(L + off + q * ps);
-                double pr[4][2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const double r = h ? cv[0].y : cv[0].x, m = h ? cv[1].y : cv[1].x;
-                    const double w = h ? cv[2].y : cv[2].x, E = h ? cv[3].y : cv[3].x;
-                    const double ir = fast_rcp(r);
-                    const double u = m * ir, v = w * ir;
-                    const double p = gm1 * (E - 0.5 * (m * u + w * v));
-                    pr[0][h] = p; pr[1][h] = p * ir; pr[2][h] = u; pr[3][h] = v;
-                }
-                const int o = (j + G) * WP + i + G;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) *reinterpret_cast<double2*>(prim + q * PL + o) = make_double2(pr[q][0], pr[q][1]);
+                c2p(L[off], L[off + ps], L[off + 2 * ps], L[off + 3 * ps], (j + G) * WP + i + G);
             }
         }
         if (tid == 32) cp_async_wait_all();      // descriptor of tile k+1 in sDesc[dsn] before (A)

@@ -5,6 +5,7 @@
 The csv is `ncu -i rep --page source --csv --print-source sass`; the disassembly comes from the
 locally built cubin of the same source (`cuobjdump -xelf all kernels.cu.o; nvdisasm -g -c ...`)."""
 import csv
+import os
 import re
 import sys
 from collections import defaultdict
@@ -25,9 +26,10 @@ off2line = {}
 for l in lines[start + 1:]:
     if l.startswith("//-----"):
         break
-    m = re.search(r'line (\d+)', l)
+    m = re.search(r'File "([^"]*)", line (\d+)', l)
     if "//##" in l and m:
-        cur = int(m.group(1))
+        f = os.path.basename(m.group(1))
+        cur = int(m.group(2)) if f == "kernels.cu" else f"{f}:{m.group(2)}"
         continue
     m = re.match(r'\s*/\*([0-9a-f]{4,})\*/\s+(.*)', l)
     if m:
@@ -50,6 +52,6 @@ if os.environ.get("REGIONS"):
     for spec in os.environ["REGIONS"].split(","):
         nm, rng = spec.split(":")
         lo, hi = map(int, rng.split("-"))
-        i = sum(v for k, v in inst.items() if k is not None and lo <= k <= hi)
-        s = sum(v for k, v in stall.items() if k is not None and lo <= k <= hi)
+        i = sum(v for k, v in inst.items() if isinstance(k, int) and lo <= k <= hi)
+        s = sum(v for k, v in stall.items() if isinstance(k, int) and lo <= k <= hi)
         print(f"region {nm:10s} {100*i/tot:5.1f}% inst {100*s/max(1,tots):5.1f}% stall")
