@@ -36,9 +36,10 @@ constexpr int kBcPeriodic = 0, kBcTransmissive = 1, kBcReflective = 2;
 __device__ __forceinline__ double fast_rcp(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    // r (1 + e + e^2) with e = 1 - x r: relative error e^3 (the seed's e ~ 2^-23), below half an ulp before the
+    // final rounding -- three DFMA instead of two Newton steps' four
     double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
+    e = fma(e, e, e);
     return fma(r, e, r);
 }
 __device__ __forceinline__ double fast_sqrt(double x) {
@@ -1673,20 +1674,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             for (int q = 0; q < 4; ++q) uc[r][q] = s[q * NN];
             c2p(uc[r][0], uc[r][1], uc[r][2], uc[r][3], (cj[r] + G) * WP + ci[r] + G);
         }
-        {
-            const int wg = warp >> 2, e = ((warp & 3) << 5) + lane;   // 0 W, 1 E, 2 S, 3 N; 128 cells each
+        if (tid < 384) {   // strips: the 3 columns / rows the faces read (cells -3..-1, T..T+2), warps 0-11
             int off, i, j;
-            if (wg < 2) {
-                j = e >> 2;
-                const int c = e & 3, r = j / N;
+            if (tid < 192) {
+                const int wg = tid >= 96, e = tid - 96 * wg;   // 0 W, 1 E
+                j = e / 3;
+                const int c = e - 3 * j + (wg == 0 ? 1 : 0), r = j / N;
                 off = (wg == 0 ? kLandW : kLandE) + r * 16 * N + (j - r * N) * 4 + c;
                 i = wg == 0 ? c - G : T + c;
             } else {
-                const int rr = e >> 5;
+                const int h = tid - 192, wg = h >= 96, e = h - 96 * wg;   // 0 S, 1 N
+                const int rr = (e >> 5) + (wg == 0 ? 1 : 0);
                 i = e & 31;
                 const int r = i / N;
-                off = (wg == 2 ? kLandS : kLandN) + r * 16 * N + rr * N + (i - r * N);
-                j = wg == 2 ? rr - G : T + rr;
+                off = (wg == 0 ? kLandS : kLandN) + r * 16 * N + rr * N + (i - r * N);
+                j = wg == 0 ? rr - G : T + rr;
             }
             const double* s = L + off;
             c2p(s[0], s[4 * N], s[8 * N], s[12 * N], (j + G) * WP + i + G);   // strip plane = 4 N doubles
