@@ -127,38 +127,42 @@ __device__ __forceinline__ double weno5(double v0, double v1, double v2, double 
 }
 
 // Both WENO5-JS interpolations at one face from the 6 stencil values w0..w5 (cells i-2 .. i+3): the left-biased
-// value from (w0..w4) and the right-biased one from (w5..w1) (A2), with exact-in-real-arithmetic sharing (A41):
-// the right stencil's second / third smoothness indicators reuse the left's t = v - 2v + v terms (T_c, T_b), its
-// middle candidate is twice the left's third (and the left's middle twice the right's third) once the linear
-// weights 10/16 and 5/16 are folded in, and every indicator is evaluated scaled by 12 -- S = (12 eps + 13 t^2 +
-// 3 u^2)^2 = 144 (eps + beta)^2, a common factor of all weights that cancels in the normalisation.
+// value from (w0..w4) and the right-biased one from (w5..w1) (A2), rewritten exactly in real arithmetic (A41):
+// - everything from the first differences d_ij = w_i - w_j: the second differences T of the smoothness indicators
+//   (shared by the two sides), their one-sided u terms, and the candidate stencils as corrections to the
+//   face-adjacent cell (w2 left, w3 right) -- the result is w2 + sum_k omega_k (q_k - w2), since sum omega_k = 1;
+// - the linear weights (1, 10, 5)/16 folded into the corrections and the normalisation (the 1/16 cancels);
+// - every indicator evaluated scaled by 12/13: S = (12 eps/13 + T^2 + 3/13 u^2)^2 = (12/13)^2 (eps + beta)^2, a
+//   common factor of all weights that cancels in the normalisation, and one weight product per candidate
+//   (omega_k ~ d_k prod_{j != k} S_j, one reciprocal per side).
 __device__ __forceinline__ void weno5_pair(double w0, double w1, double w2, double w3, double w4, double w5,
-                                           double eps12, double& left, double& right) {
-    // candidate stencils (1/8 and the linear weights (1, 10, 5)/16 folded into the coefficients)
-    const double q0 = fma(0.375, w0, fma(-1.25, w1, 1.875 * w2));
-    const double q1 = fma(-1.25, w1, fma(7.5, w2, 3.75 * w3));
-    const double q2 = fma(1.875, w2, fma(3.75, w3, -0.625 * w4));
-    const double r0 = fma(0.375, w5, fma(-1.25, w4, 1.875 * w3));
-    const double r1 = 2.0 * q2, r2 = 0.5 * q1;
-    // second differences T (13 T^2 + 12 eps shared) and the one-sided u terms
-    const double Ta = fma(-2.0, w1, w0 + w2), Tb = fma(-2.0, w2, w1 + w3);
-    const double Tc = fma(-2.0, w3, w2 + w4), Td = fma(-2.0, w4, w3 + w5);
-    const double Aa = fma(13.0 * Ta, Ta, eps12), Ab = fma(13.0 * Tb, Tb, eps12);
-    const double Ac = fma(13.0 * Tc, Tc, eps12), Ad = fma(13.0 * Td, Td, eps12);
-    const double u0 = fma(-4.0, w1, fma(3.0, w2, w0)), u1 = w1 - w3, u2 = fma(3.0, w2, fma(-4.0, w3, w4));
-    const double v0 = fma(-4.0, w4, fma(3.0, w3, w5)), v1 = w4 - w2, v2 = fma(3.0, w3, fma(-4.0, w2, w1));
-    double s0 = fma(3.0 * u0, u0, Aa), s1 = fma(3.0 * u1, u1, Ab), s2 = fma(3.0 * u2, u2, Ac);
-    double z0 = fma(3.0 * v0, v0, Ad), z1 = fma(3.0 * v1, v1, Ac), z2 = fma(3.0 * v2, v2, Ab);
+                                           double eps12_13, double& left, double& right) {
+    const double d01 = w0 - w1, d12 = w1 - w2, d23 = w2 - w3, d34 = w3 - w4, d45 = w4 - w5;
+    // corrections q_k - w2 (left) / r_k - w3 (right) times the linear weights 1, 10, 5 (x 16):
+    // left (3 d01 - 7 d12)/8, -10 (d12 + 3 d23)/8, 5 (d34 - 5 d23)/8; right (7 d34 - 3 d45)/8, 10 (3 d23 + d34)/8,
+    // 5 (5 d23 - d12)/8
+    const double q0 = fma(0.375, d01, -0.875 * d12), q1 = fma(-1.25, d12, -3.75 * d23);
+    const double q2 = fma(0.625, d34, -3.125 * d23);
+    const double r0 = fma(0.875, d34, -0.375 * d45), r1 = fma(3.75, d23, 1.25 * d34);
+    const double r2 = fma(3.125, d23, -0.625 * d12);
+    // second differences (shared) and one-sided terms: T_a = w0 - 2 w1 + w2 ... T_d = w3 - 2 w4 + w5
+    const double Ta = d01 - d12, Tb = d12 - d23, Tc = d23 - d34, Td = d34 - d45;
+    const double Aa = fma(Ta, Ta, eps12_13), Ab = fma(Tb, Tb, eps12_13);
+    const double Ac = fma(Tc, Tc, eps12_13), Ad = fma(Td, Td, eps12_13);
+    const double u0 = fma(-2.0, d12, Ta), u1 = d12 + d23, u2 = fma(2.0, d23, Tc);   // w0-4w1+3w2, w1-w3, 3w2-4w3+w4
+    const double v0 = fma(2.0, d34, Td), v1 = d23 + d34, v2 = fma(-2.0, d23, Tb);   // 3w3-4w4+w5, w2-w4, w1-4w2+3w3
+    constexpr double c3 = 3.0 / 13.0;
+    double s0 = fma(c3 * u0, u0, Aa), s1 = fma(c3 * u1, u1, Ab), s2 = fma(c3 * u2, u2, Ac);
+    double z0 = fma(c3 * v0, v0, Ad), z1 = fma(c3 * v1, v1, Ac), z2 = fma(c3 * v2, v2, Ab);
     s0 *= s0; s1 *= s1; s2 *= s2;
     z0 *= z0; z1 *= z1; z2 *= z2;
-    // omega_k ~ d_k / S_k: weights prod_{j != k} S_j with d_k folded into the candidates / the denominator
     {
         const double a0 = s1 * s2, a1 = s0 * s2, a2 = s0 * s1;
-        left = fma(a0, q0, fma(a1, q1, a2 * q2)) * fast_rcp(fma(10.0, a1, fma(5.0, a2, a0)));
+        left = fma(fma(a0, q0, fma(a1, q1, a2 * q2)), fast_rcp(fma(10.0, a1, fma(5.0, a2, a0))), w2);
     }
     {
         const double a0 = z1 * z2, a1 = z0 * z2, a2 = z0 * z1;
-        right = fma(a0, r0, fma(a1, r1, a2 * r2)) * fast_rcp(fma(10.0, a1, fma(5.0, a2, a0)));
+        right = fma(fma(a0, r0, fma(a1, r1, a2 * r2)), fast_rcp(fma(10.0, a1, fma(5.0, a2, a0))), w3);
     }
 }
 
@@ -171,7 +175,7 @@ template <bool CHAR>
 __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int cs, int plane, int kn, int kt, double g,
                                              double eps, double F[4]) {
     const double gm1 = g - 1.0;
-    const double eps12 = 12.0 * eps;
+    const double eps12_13 = eps * (12.0 / 13.0);
 #define QV(s, k) q[(k) * plane + (s) * cs]
     double wl[4], wr[4];
     double u = 0.0, v = 0.0, c = 0.0, qk = 0.0, H = 0.0;
@@ -192,45 +196,54 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         double ic = fast_rcp(c);
         qk = 0.5 * (u * u + v * v);
         H = c2 * (1.0 / gm1) + qk;   // (1 / gm1: one division per thread, hoisted by the compiler)
-        double b1 = gm1 * (ic * ic);
-        double b2 = b1 * qk;
-        // rows of L (O10): l1 = 1/2 (b2 + u/c, -b1 u - 1/c, -b1 v, b1), l2, l3 = (-v, 0, 1, 0), l4
-        const double h1 = 0.5 * (b2 + u * ic), h2 = 0.5 * (-b1 * u - ic), h3 = 0.5 * (-b1 * v), h4 = 0.5 * b1;
-        const double m1 = 1.0 - b2, m2 = b1 * u, m3 = b1 * v, m4 = -b1;
-        const double k1 = 0.5 * (b2 - u * ic), k2 = 0.5 * (-b1 * u + ic);
-        double w[6];
+        // rows of L (O10): l1 = 1/2 (b2 + u/c, -b1 u - 1/c, -b1 v, b1), l2 = (1 - b2, b1 u, b1 v, -b1),
+        // l3 = (-v, 0, 1, 0), l4 = 1/2 (b2 - u/c, -b1 u + 1/c, -b1 v, b1), b1 = (g-1)/c^2, b2 = b1 q -- applied
+        // factorised (A41): with X = u Qn + v Qt - Q3, hA = (b2 Q0 - b1 X)/2 and hB = (u Q0 - Qn)/(2c),
+        // l1 Q = hA + hB, l4 Q = hA - hB, l2 Q = Q0 - 2 hA, l3 Q = Qt - v Q0
+        const double hb1 = 0.5 * (gm1 * (ic * ic)), hb2 = hb1 * qk, hic = 0.5 * ic;
+        double hA[6], hB[6], w[6];
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = h1 * QV(s, 0) + h2 * QV(s, kn) + h3 * QV(s, kt) + h4 * QV(s, 3);
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[0], wr[0]);
+        for (int s = 0; s < 6; ++s) {
+            const double q0 = QV(s, 0), qn = QV(s, kn);
+            const double X = fma(u, qn, fma(v, QV(s, kt), -QV(s, 3)));
+            hA[s] = fma(hb2, q0, -hb1 * X);
+            hB[s] = fma(u, q0, -qn) * hic;
+        }
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = m1 * QV(s, 0) + m2 * QV(s, kn) + m3 * QV(s, kt) + m4 * QV(s, 3);
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[1], wr[1]);
+        for (int s = 0; s < 6; ++s) w[s] = hA[s] + hB[s];
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[0], wr[0]);
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = -v * QV(s, 0) + QV(s, kt);
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[2], wr[2]);
+        for (int s = 0; s < 6; ++s) w[s] = hA[s] - hB[s];
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[3], wr[3]);
 #pragma unroll
-        for (int s = 0; s < 6; ++s) w[s] = k1 * QV(s, 0) + k2 * QV(s, kn) + h3 * QV(s, kt) + h4 * QV(s, 3);
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12, wl[3], wr[3]);
+        for (int s = 0; s < 6; ++s) w[s] = fma(-2.0, hA[s], QV(s, 0));
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[1], wr[1]);
+#pragma unroll
+        for (int s = 0; s < 6; ++s) w[s] = fma(-v, QV(s, 0), QV(s, kt));
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[2], wr[2]);
     } else {
         const int kk[4] = {0, kn, kt, 3};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            weno5_pair(QV(0, kk[k]), QV(1, kk[k]), QV(2, kk[k]), QV(3, kk[k]), QV(4, kk[k]), QV(5, kk[k]), eps12, wl[k],
-                       wr[k]);
+            weno5_pair(QV(0, kk[k]), QV(1, kk[k]), QV(2, kk[k]), QV(3, kk[k]), QV(4, kk[k]), QV(5, kk[k]), eps12_13,
+                       wl[k], wr[k]);
         }
     }
 #undef QV
     double UL[4], UR[4];
     if (CHAR) {
-        // U = R w, columns r1 = (1, u-c, v, H-uc), r2 = (1, u, v, q), r3 = (0,0,1,v), r4 = (1, u+c, v, H+uc)
-        UL[0] = wl[0] + wl[1] + wl[3];
-        UL[1] = (u - c) * wl[0] + u * wl[1] + (u + c) * wl[3];
-        UL[2] = v * wl[0] + v * wl[1] + wl[2] + v * wl[3];
-        UL[3] = (H - u * c) * wl[0] + qk * wl[1] + v * wl[2] + (H + u * c) * wl[3];
-        UR[0] = wr[0] + wr[1] + wr[3];
-        UR[1] = (u - c) * wr[0] + u * wr[1] + (u + c) * wr[3];
-        UR[2] = v * wr[0] + v * wr[1] + wr[2] + v * wr[3];
-        UR[3] = (H - u * c) * wr[0] + qk * wr[1] + v * wr[2] + (H + u * c) * wr[3];
+        // U = R w, columns r1 = (1, u-c, v, H-uc), r2 = (1, u, v, q), r3 = (0,0,1,v), r4 = (1, u+c, v, H+uc), as
+        // U0 = w1 + w2 + w4, U1 = u U0 + c (w4 - w1), U2 = v U0 + w3, U3 = H (w1 + w4) + uc (w4 - w1) + q w2 + v w3
+        const double uc = u * c;
+        auto back = [&](const double (&wk)[4], double (&U)[4]) {
+            const double S03 = wk[0] + wk[3], D = wk[3] - wk[0];
+            U[0] = S03 + wk[1];
+            U[1] = fma(u, U[0], c * D);
+            U[2] = fma(v, U[0], wk[2]);
+            U[3] = fma(H, S03, fma(uc, D, fma(qk, wk[1], v * wk[2])));
+        };
+        back(wl, UL);
+        back(wr, UR);
     } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) { UL[k] = wl[k]; UR[k] = wr[k]; }
@@ -383,6 +396,8 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
     const int lvl = d.level;
     const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
     const bool div4 = a.div_order == 4;
+    // Eq. 9 as 24 F-hat = 26 f - (f- + f+): the 1/24 goes into the divergence and the flux registers
+    const double fsc = div4 ? 1.0 / 24.0 : 1.0, idx24 = fsc * idx, idy24 = fsc * idy;
     const int x_lo = tx == 0, x_hi = tx == a.tiles - 1, y_lo = ty == 0, y_hi = ty == a.tiles - 1;
     const int store_mask = (d.cf | (d.cf >> 4)) & 15;
 
@@ -433,13 +448,13 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             for (int k = 0; k < 4; ++k) {
                 const double* fr = sF + (k * T + j) * NF + i + 1;   // fr[0] = f at face i
                 double fl = fr[0], fh = fr[1];
-                double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-1] + fh) : fl;
-                double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2]) : fh;
-                acc[r][k] = -(Fh - Fl) * idx;
+                double Fl = div4 ? fma(26.0, fl, -(fr[-1] + fh)) : fl;   // 24 F-hat
+                double Fh = div4 ? fma(26.0, fh, -(fl + fr[2])) : fh;
+                acc[r][k] = -(Fh - Fl) * idx24;
                 if (i == 0 && x_lo && (store_mask & 1))
-                    a.freg[(((size_t)d.slot * 4 + kW) * 4 + k) * n + ty * T + j] = Fl;
+                    a.freg[(((size_t)d.slot * 4 + kW) * 4 + k) * n + ty * T + j] = fsc * Fl;
                 if (i == T - 1 && x_hi && (store_mask & 2))
-                    a.freg[(((size_t)d.slot * 4 + kE) * 4 + k) * n + ty * T + j] = Fh;
+                    a.freg[(((size_t)d.slot * 4 + kE) * 4 + k) * n + ty * T + j] = fsc * Fh;
             }
         }
     }
@@ -467,13 +482,13 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             for (int k = 0; k < 4; ++k) {
                 const double* fr = sFy + (k * NF + j + 1) * T + i;   // fr[0] = f at face j
                 double fl = fr[0], fh = fr[T];
-                double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-T] + fh) : fl;
-                double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2 * T]) : fh;
-                double L = acc[r][k] - (Fh - Fl) * idy;
+                double Fl = div4 ? fma(26.0, fl, -(fr[-T] + fh)) : fl;   // 24 F-hat
+                double Fh = div4 ? fma(26.0, fh, -(fl + fr[2 * T])) : fh;
+                double L = acc[r][k] - (Fh - Fl) * idy24;
                 if (j == 0 && y_lo && (store_mask & 4))
-                    a.freg[(((size_t)d.slot * 4 + kS) * 4 + k) * n + tx * T + i] = Fl;
+                    a.freg[(((size_t)d.slot * 4 + kS) * 4 + k) * n + tx * T + i] = fsc * Fl;
                 if (j == T - 1 && y_hi && (store_mask & 8))
-                    a.freg[(((size_t)d.slot * 4 + kN) * 4 + k) * n + tx * T + i] = Fh;
+                    a.freg[(((size_t)d.slot * 4 + kN) * 4 + k) * n + tx * T + i] = fsc * Fh;
                 // U^(s-1): the WENO tile holds it in shared memory (Central4 converted its tile to primitives)
                 double v = (SCHEME != 0 ? sQ[k * PL + (j + G) * W + (i + G)] : __ldg(pin + k * nn + off)) + dt * L;
                 if (a.stage > 1) v = a.a * __ldg(pn + k * nn + off) + a.b * v;
@@ -1945,6 +1960,8 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
     const int lvl = sD[0].level;
     const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
     const bool div4 = a.div_order == 4;
+    // Eq. 9 as 24 F-hat = 26 f - (f- + f+): the 1/24 goes into the divergence and the flux registers
+    const double fsc = div4 ? 1.0 / 24.0 : 1.0, idx24 = fsc * idx, idy24 = fsc * idy;
 
     // ---- x faces (a4-a6): face m (left of cell m), row j
     for (int e = tid; e < T * NF; e += NT) {
@@ -1966,13 +1983,13 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
         for (int q = 0; q < 4; ++q) {
             const double* fr = sF + (q * T + j) * NF + i + 1;
             double fl = fr[0], fh = fr[1];
-            double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-1] + fh) : fl;
-            double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2]) : fh;
-            acc[r][q] = -(Fh - Fl) * idx;
+            double Fl = div4 ? fma(26.0, fl, -(fr[-1] + fh)) : fl;   // 24 F-hat
+            double Fh = div4 ? fma(26.0, fh, -(fl + fr[2])) : fh;
+            acc[r][q] = -(Fh - Fl) * idx24;
             if (i == 0 && ((dw.cf | (dw.cf >> 4)) & 1))   // flux registers of C/F sides on the block edge
-                a.freg[(((size_t)dw.slot * 4 + kW) * 4 + q) * N + j % N] = Fl;
+                a.freg[(((size_t)dw.slot * 4 + kW) * 4 + q) * N + j % N] = fsc * Fl;
             if (i == T - 1 && ((de.cf | (de.cf >> 4)) & 2))
-                a.freg[(((size_t)de.slot * 4 + kE) * 4 + q) * N + j % N] = Fh;
+                a.freg[(((size_t)de.slot * 4 + kE) * 4 + q) * N + j % N] = fsc * Fh;
         }
     }
     __syncthreads();
@@ -2008,11 +2025,11 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
         for (int q = 0; q < 4; ++q) {
             const double* fr = sF + (q * NF + j + 1) * T + i;
             double fl = fr[0], fh = fr[T];
-            double Fl = div4 ? (13.0 / 12.0) * fl - (1.0 / 24.0) * (fr[-T] + fh) : fl;
-            double Fh = div4 ? (13.0 / 12.0) * fh - (1.0 / 24.0) * (fl + fr[2 * T]) : fh;
-            double L = acc[r][q] - (Fh - Fl) * idy;
-            if (j == 0 && ((ds.cf | (ds.cf >> 4)) & 4)) a.freg[(((size_t)ds.slot * 4 + kS) * 4 + q) * N + li] = Fl;
-            if (j == T - 1 && ((dn.cf | (dn.cf >> 4)) & 8)) a.freg[(((size_t)dn.slot * 4 + kN) * 4 + q) * N + li] = Fh;
+            double Fl = div4 ? fma(26.0, fl, -(fr[-T] + fh)) : fl;   // 24 F-hat
+            double Fh = div4 ? fma(26.0, fh, -(fl + fr[2 * T])) : fh;
+            double L = acc[r][q] - (Fh - Fl) * idy24;
+            if (j == 0 && ((ds.cf | (ds.cf >> 4)) & 4)) a.freg[(((size_t)ds.slot * 4 + kS) * 4 + q) * N + li] = fsc * Fl;
+            if (j == T - 1 && ((dn.cf | (dn.cf >> 4)) & 8)) a.freg[(((size_t)dn.slot * 4 + kN) * 4 + q) * N + li] = fsc * Fh;
             double v = __ldg(pin + q * NN + off) + dt * L;
             if (a.stage > 1) v = a.a * __ldg(pn + q * NN + off) + a.b * v;
             o4[q] = v;

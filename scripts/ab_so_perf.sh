@@ -7,6 +7,6 @@ cp $SO /tmp/libamr_orig.so
 for r in 1 2; do for v in $NAMES; do
   cp abso/$v.so $SO
   echo "== $v (rep $r)"
-  AMR_NO_BUILD=1 timeout 600 python scripts/quick_perf.py "$@" 2>&1 | tail -6
+  AMR_NO_BUILD=1 timeout 600 python scripts/quick_perf.py "$@" 2>&1 | tail -12
 done; done
 cp /tmp/libamr_orig.so $SO
