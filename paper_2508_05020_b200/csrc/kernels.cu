@@ -53,6 +53,13 @@ __device__ __forceinline__ double fast_sqrt(double x) {
     double r = fma(-s, s, x);
     return fma(r, 0.5 * y, s);
 }
+// 1/sqrt(x): seed y, t = x y^2 - 1, y (1 - t/2 + 3 t^2/8) (relative error O(t^3) below half an ulp, then rounding)
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double t = fma(x * y, y, -1.0);
+    return fma(y, t * fma(0.375, t, -0.5), y);
+}
 
 __device__ __forceinline__ double wave_speed(double r, double m, double w, double E, double g, double idx,
                                              double idy) {
@@ -192,8 +199,8 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         v = 0.5 * (vL + vR);
         double p = 0.5 * (pL + pR);
         double c2 = g * p * fast_rcp(r);
-        c = fast_sqrt(c2);
-        double ic = fast_rcp(c);
+        const double ic = fast_rsqrt(c2);   // 1/c, and c = c2 / c (A41: <= 2 ulp)
+        c = c2 * ic;
         qk = 0.5 * (u * u + v * v);
         H = c2 * (1.0 / gm1) + qk;   // (1 / gm1: one division per thread, hoisted by the compiler)
         // rows of L (O10): l1 = 1/2 (b2 + u/c, -b1 u - 1/c, -b1 v, b1), l2 = (1 - b2, b1 u, b1 v, -b1),
@@ -257,11 +264,14 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
     double sL = fast_sqrt(g * pL * irL) + fabs(unL);
     double sR = fast_sqrt(g * pR * irR) + fabs(unR);
     double S = sR > sL ? sR : sL;   // as the oracle (O10): a NaN wave speed propagates instead of being dropped
-    F[0] = 0.5 * (UR[1] + UL[1]) - 0.5 * S * (UR[0] - UL[0]);
-    F[1] = 0.5 * ((UR[1] * unR + pR) + (UL[1] * unL + pL)) - 0.5 * S * (UR[1] - UL[1]);
-    F[2] = 0.5 * (UR[2] * unR + UL[2] * unL) - 0.5 * S * (UR[2] - UL[2]);
-    F[3] = 0.5 * ((UR[3] + pR) * unR + (UL[3] + pL) * unL) - 0.5 * S * (UR[3] - UL[3]);
+    // returned as 2 F (the 1/2 of Eq. 11 goes into the caller's divergence / flux-register scale, kWenoFluxScale)
+    F[0] = (UR[1] + UL[1]) - S * (UR[0] - UL[0]);
+    F[1] = (fma(UR[1], unR, pR) + fma(UL[1], unL, pL)) - S * (UR[1] - UL[1]);
+    F[2] = fma(UR[2], unR, UL[2] * unL) - S * (UR[2] - UL[2]);
+    F[3] = fma(UR[3] + pR, unR, (UL[3] + pL) * unL) - S * (UR[3] - UL[3]);
 }
+// weno_rusanov returns 2 F
+constexpr double kWenoFluxScale = 0.5;
 
 // Central4 edge flux: Eq. 8 weights (9/16, -1/16) applied edge-from-node (A7)
 // to (p, T = p/rho, u_n, u_t) of cells i-1..i+2; rho_e = p_e / T_e (A6).
@@ -397,7 +407,7 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
     const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
     const bool div4 = a.div_order == 4;
     // Eq. 9 as 24 F-hat = 26 f - (f- + f+): the 1/24 goes into the divergence and the flux registers
-    const double fsc = div4 ? 1.0 / 24.0 : 1.0, idx24 = fsc * idx, idy24 = fsc * idy;
+    const double fsc = (SCHEME == 0 ? 1.0 : kWenoFluxScale) * (div4 ? 1.0 / 24.0 : 1.0), idx24 = fsc * idx, idy24 = fsc * idy;
     const int x_lo = tx == 0, x_hi = tx == a.tiles - 1, y_lo = ty == 0, y_hi = ty == a.tiles - 1;
     const int store_mask = (d.cf | (d.cf >> 4)) & 15;
 
@@ -412,17 +422,29 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
 #pragma unroll
         for (int k = 0; k < 4; ++k) sF[(k * T + j) * NF + m + 1] = f[k];
     };
-    auto y_face = [&](int e) {   // face m (below cell m), column i; normal momentum is component 2
+    auto y_flux = [&](int e, double (&f)[4]) {   // face m (below cell m), column i; normal momentum is component 2
         int m = e / T - 1, i = e - (m + 1) * T;
         int o = (m + G) * W + (i + G);
-        double f[4];
         if (SCHEME == 0) central4_flux(sQ + o - 2 * W, W, PL, 3, 2, inv_gm1, f);
         else weno_rusanov<SCHEME == 1>(sQ + o - 3 * W, W, PL, 2, 1, g, a.eps, f);
+    };
+    auto y_store = [&](int e, const double (&f)[4]) {
+        int m = e / T - 1, i = e - (m + 1) * T;
         sFy[(0 * NF + m + 1) * T + i] = f[0];
         sFy[(1 * NF + m + 1) * T + i] = f[2];
         sFy[(2 * NF + m + 1) * T + i] = f[1];
         sFy[(3 * NF + m + 1) * T + i] = f[3];
     };
+    auto y_face = [&](int e) {
+        double f[4];
+        y_flux(e, f);
+        y_store(e, f);
+    };
+    // one plane (T > 16): the threads left idle by the last x-face pass compute their first y face then and keep
+    // it in registers until the x divergence has read the plane (T = 32: 9 face passes instead of 10)
+    constexpr int NXF = T * NF, KX = (NXF + NT - 1) / NT;
+    int yh_e = -1;
+    double yh[4];
     // ---- faces (a4-a6)
     if (COMB) {   // both directions in one pass; the x range padded to whole warps (no warp straddles x / y)
         constexpr int NX = T * NF, NXP = (NX + 31) / 32 * 32;
@@ -434,7 +456,12 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
             }
         }
     } else {
-        for (int e = tid; e < T * NF; e += NT) x_face(e);
+#pragma unroll 1
+        for (int k = 0; k < KX; ++k) {
+            const int e = tid + k * NT;
+            if (e < NXF) x_face(e);
+            else if (e - NXF < NXF) { yh_e = e - NXF; y_flux(yh_e, yh); }
+        }
     }
     __syncthreads();
     // ---- x divergence (a7, Eq. 9 flux form) into registers
@@ -460,7 +487,8 @@ __global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(con
     }
     if (!COMB) {   // y faces into the same plane once the x divergence has read it
         __syncthreads();
-        for (int e = tid; e < T * NF; e += NT) y_face(e);
+        if (yh_e >= 0) y_store(yh_e, yh);
+        for (int e = tid + KX * NT - NXF; e < NXF; e += NT) y_face(e);
         __syncthreads();
     }
 
@@ -1480,14 +1508,20 @@ __global__ void unf_flux_kernel(const StageArgs a) {
         const int j = e / NF, m = e - j * NF - 1;
         const int o = (j + kUnfG) * Wd + m + kUnfG;
         if (SCHEME == 0) central4_flux(W + o - 2, 1, (int)per, 2, 3, inv_gm1, F);
-        else weno_rusanov<SCHEME == 1>(W + o - 3, 1, (int)per, 1, 2, g, a.eps, F);
+        else {
+            weno_rusanov<SCHEME == 1>(W + o - 3, 1, (int)per, 1, 2, g, a.eps, F);
+            for (int k = 0; k < 4; ++k) F[k] *= kWenoFluxScale;
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) f[((size_t)k * n + j) * NF + m + 1] = F[k];
     } else {          // y faces: column i, face m (below cell m); components stored in U order
         const int m = e / n - 1, i = e - (m + 1) * n;
         const int o = (m + kUnfG) * Wd + i + kUnfG;
         if (SCHEME == 0) central4_flux(W + o - 2 * Wd, Wd, (int)per, 3, 2, inv_gm1, F);
-        else weno_rusanov<SCHEME == 1>(W + o - 3 * Wd, Wd, (int)per, 2, 1, g, a.eps, F);
+        else {
+            weno_rusanov<SCHEME == 1>(W + o - 3 * Wd, Wd, (int)per, 2, 1, g, a.eps, F);
+            for (int k = 0; k < 4; ++k) F[k] *= kWenoFluxScale;
+        }
         f[((size_t)0 * NF + m + 1) * n + i] = F[0];
         f[((size_t)1 * NF + m + 1) * n + i] = F[2];
         f[((size_t)2 * NF + m + 1) * n + i] = F[1];
@@ -1961,9 +1995,10 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
     const double idx = a.geo.inv_dx[lvl], idy = a.geo.inv_dy[lvl];
     const bool div4 = a.div_order == 4;
     // Eq. 9 as 24 F-hat = 26 f - (f- + f+): the 1/24 goes into the divergence and the flux registers
-    const double fsc = div4 ? 1.0 / 24.0 : 1.0, idx24 = fsc * idx, idy24 = fsc * idy;
+    const double fsc = (SCHEME == 0 ? 1.0 : kWenoFluxScale) * (div4 ? 1.0 / 24.0 : 1.0), idx24 = fsc * idx, idy24 = fsc * idy;
 
-    // ---- x faces (a4-a6): face m (left of cell m), row j
+    // ---- x faces (a4-a6): face m (left of cell m), row j (packing the idle threads of the last x pass with y faces,
+    // as stage_kernel<., 32> does, was 1.3 % slower here)
     for (int e = tid; e < T * NF; e += NT) {
         int j = e / NF, m = e - j * NF - 1;
         int o = (j + G) * W + (m + G);
