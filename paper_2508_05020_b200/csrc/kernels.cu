@@ -42,17 +42,6 @@ __device__ __forceinline__ double fast_rcp(double x) {
     e = fma(e, e, e);
     return fma(r, e, r);
 }
-__device__ __forceinline__ double fast_sqrt(double x) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    // two Newton steps on 1/sqrt(x), then one on sqrt(x) itself
-    double h = 0.5 * x;
-    y = y * fma(-h * y, y, 1.5);
-    y = y * fma(-h * y, y, 1.5);
-    double s = x * y;
-    double r = fma(-s, s, x);
-    return fma(r, 0.5 * y, s);
-}
 // 1/sqrt(x): seed y, t = x y^2 - 1, y (1 - t/2 + 3 t^2/8) (relative error O(t^3) below half an ulp, then rounding)
 __device__ __forceinline__ double fast_rsqrt(double x) {
     double y;
@@ -60,6 +49,8 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
     const double t = fma(x * y, y, -1.0);
     return fma(y, t * fma(0.375, t, -0.5), y);
 }
+// sqrt(x) = x / sqrt(x) (A41: <= 2 ulp for positive normal x, scripts/rcp_check.cu; 0, negative and NaN give NaN)
+__device__ __forceinline__ double fast_sqrt(double x) { return x * fast_rsqrt(x); }
 
 __device__ __forceinline__ double wave_speed(double r, double m, double w, double E, double g, double idx,
                                              double idy) {
@@ -192,14 +183,14 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         double iL = fast_rcp(rL), iR = fast_rcp(rR);
         double uL = QV(2, kn) * iL, vL = QV(2, kt) * iL;
         double uR = QV(3, kn) * iR, vR = QV(3, kt) * iR;
-        double pL = gm1 * (QV(2, 3) - 0.5 * (QV(2, kn) * uL + QV(2, kt) * vL));
-        double pR = gm1 * (QV(3, 3) - 0.5 * (QV(3, kn) * uR + QV(3, kt) * vR));
-        double r = 0.5 * (rL + rR);
+        // internal energies per volume e = E - (m u + w v)/2 (p = (g-1) e); at the mean state
+        // c^2 = g p / rho = g (g-1) (e_L + e_R) / (rho_L + rho_R)
+        const double eL = QV(2, 3) - 0.5 * (QV(2, kn) * uL + QV(2, kt) * vL);
+        const double eR = QV(3, 3) - 0.5 * (QV(3, kn) * uR + QV(3, kt) * vR);
         u = 0.5 * (uL + uR);
         v = 0.5 * (vL + vR);
-        double p = 0.5 * (pL + pR);
-        double c2 = g * p * fast_rcp(r);
-        const double ic = fast_rsqrt(c2);   // 1/c, and c = c2 / c (A41: <= 2 ulp)
+        const double c2 = (g * gm1) * (eL + eR) * fast_rcp(rL + rR);
+        const double ic = fast_rsqrt(c2);   // 1/c, and c = c2 / c (A41: <= 3 / 2 ulp, scripts/rcp_check.cu)
         c = c2 * ic;
         qk = 0.5 * (u * u + v * v);
         H = c2 * (1.0 / gm1) + qk;   // (1 / gm1: one division per thread, hoisted by the compiler)
