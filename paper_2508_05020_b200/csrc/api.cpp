@@ -384,13 +384,29 @@ amr_status build_plan(amr_ctx* c) {
 
     cudaStream_t s = c->stream;
     {   // one packed upload of the per-plan descriptor arrays (each 256-byte aligned in the arena)
-        std::vector<char>& H = c->arena_host;
-        H.clear();
+        size_t total = 0;   // the arena layout first (each array 256-byte aligned), then one pinned staging fill
+        auto span = [&](size_t bytes) { total = ((total + 255) & ~(size_t)255) + bytes; };
+        span(c->leaves.size() * sizeof(LeafDesc));
+        span(c->gleaves.size() * sizeof(LeafDesc));
+        span(c->singles.size() * sizeof(LeafDesc));
+        span(c->ptasks.size() * sizeof(ProxyTask));
+        span(c->rtasks.size() * sizeof(RefluxTask));
+        for (int l = 0; l < L; ++l) span(c->rlev[l].size() * sizeof(RestrictTask));
+        span(c->sib.size() * sizeof(int32_t));
+        if (total > c->arena_host_cap) {
+            if (c->arena_host) cudaFreeHost(c->arena_host);
+            c->arena_host = nullptr;
+            c->arena_host_cap = 0;
+            const size_t cap = std::max<size_t>(total + total / 2, 4096);
+            CU(cudaMallocHost(reinterpret_cast<void**>(&c->arena_host), cap));
+            c->arena_host_cap = cap;
+        }
+        size_t used = 0;
         std::vector<size_t> offs;
         auto add = [&](const void* src, size_t bytes) {
-            const size_t o = (H.size() + 255) & ~(size_t)255;
-            H.resize(o + bytes);
-            if (bytes) std::memcpy(H.data() + o, src, bytes);
+            const size_t o = (used + 255) & ~(size_t)255;
+            if (bytes) std::memcpy(c->arena_host + o, src, bytes);
+            used = o + bytes;
             offs.push_back(o);
         };
         add(c->leaves.data(), c->leaves.size() * sizeof(LeafDesc));
@@ -404,8 +420,8 @@ amr_status build_plan(amr_ctx* c) {
         c->d_leaves.release(); c->d_gleaves.release(); c->d_singles.release(); c->d_ptasks.release();
         c->d_rtasks.release(); c->d_sib.release();
         for (auto& d : c->d_rlev) d.release();
-        CU(c->arena_dev.reserve(std::max<size_t>(H.size(), 256)));
-        if (!H.empty()) CU(cudaMemcpyAsync(c->arena_dev.p, H.data(), H.size(), cudaMemcpyHostToDevice, s));
+        CU(c->arena_dev.reserve(std::max<size_t>(used, 256)));
+        if (used) CU(cudaMemcpyAsync(c->arena_dev.p, c->arena_host, used, cudaMemcpyHostToDevice, s));
         char* base = c->arena_dev.p;
         size_t k = 0;
         c->d_leaves.view(reinterpret_cast<LeafDesc*>(base + offs[k++]), c->leaves.size());
@@ -1083,6 +1099,7 @@ void amr_destroy(amr_ctx* c) {
     cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp); cudaFree(c->d_dtp);
     for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    if (c->arena_host) cudaFreeHost(c->arena_host);
     for (auto e : c->ev_free) cudaEventDestroy(e);
     for (auto e : c->ev_pending) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -117,7 +117,10 @@ struct amr_ctx {
     std::vector<DevArray<RestrictTask>> d_rlev;
     // the per-plan descriptor arrays packed into ONE host buffer and ONE device buffer (one H2D copy per plan; the
     // DevArrays above are views into it)
-    std::vector<char> arena_host;
+    // host side of the plan arena: pinned (the packed upload is one DMA, no staging through pageable memory),
+    // grown geometrically, never zero-filled; freed with the ctx
+    char* arena_host = nullptr;
+    size_t arena_host_cap = 0;
     DevArray<char> arena_dev;
     DevArray<ProlongTask> d_prolong;
     DevArray<double> proxy, freg, staging, d_maxeta, d_partial, unf_scratch;

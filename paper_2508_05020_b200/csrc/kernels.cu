@@ -2275,9 +2275,22 @@ __device__ __forceinline__ void ghost_strip(const ProxyTask& pt, int g, const Au
     const int rx0 = ((pt.P * n + li0) >> 1) - Pp * n - 1, rx1 = ((pt.P * n + li1) >> 1) - Pp * n + 1;
     const int ry0 = ((pt.Q * n + lj0) >> 1) - Qp * n - 1, ry1 = ((pt.Q * n + lj1) >> 1) - Qp * n + 1;
     const int wx = rx1 - rx0 + 1, wy = ry1 - ry0 + 1, plane = wx * wy;
-    for (int e = tid; e < 4 * plane; e += nth) {
-        const int k = e / plane, r = e - k * plane, ry = ry0 + r / wx, rx = rx0 + r % wx;
-        cs[e] = coarse_value(a.Uc, pt.coarse, n, pt.level - 1, Pp, Qp, rx, ry, k, a.geo, a.Uold, a.tfrac);
+    // staged in batches of kGhostBatch values per thread: all loads of a batch are issued before the first store
+    // (one dependent global round trip per batch instead of one per value)
+    constexpr int kGhostBatch = 8;
+    for (int e0 = tid; e0 < 4 * plane; e0 += kGhostBatch * nth) {
+        double v[kGhostBatch];
+#pragma unroll
+        for (int b = 0; b < kGhostBatch; ++b) {
+            const int e = e0 + b * nth;
+            if (e < 4 * plane) {
+                const int k = e / plane, r = e - k * plane, ry = ry0 + r / wx, rx = rx0 + r % wx;
+                v[b] = coarse_value(a.Uc, pt.coarse, n, pt.level - 1, Pp, Qp, rx, ry, k, a.geo, a.Uold, a.tfrac);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kGhostBatch; ++b)
+            if (e0 + b * nth < 4 * plane) cs[e0 + b * nth] = v[b];
     }
     sync();
     for (int e = tid; e < ncell; e += nth) {
