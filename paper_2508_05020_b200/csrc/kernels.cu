@@ -582,19 +582,20 @@ __device__ __forceinline__ void c4_face(const double (&p)[4], const double (&Tt)
 // Eq. 8 weights (9/16, -1/16) become fma(9, inner pair, -outer pair), one operation fewer per variable; the
 // ratio p/T is scale-free, and the caller folds 1/16 into the divergence (idx / 16).
 __device__ __forceinline__ void c4_face16(const double (&p)[4], const double (&Tt)[4], const double (&un)[4],
-                                          const double (&ut)[4], double inv_gm1, double F16[4]) {
+                                          const double (&ut)[4], double g_gm1, double F16[4]) {
     const double pe = fma(9.0, p[1] + p[2], -(p[0] + p[3]));      // 16 p_e
     const double Te = fma(9.0, Tt[1] + Tt[2], -(Tt[0] + Tt[3]));  // 16 T_e
     const double U16 = fma(9.0, un[1] + un[2], -(un[0] + un[3]));   // 16 u_e
     const double ue = 0.0625 * U16;
     const double ve = 0.0625 * fma(9.0, ut[1] + ut[2], -(ut[0] + ut[3]));
     const double re = pe * fast_rcp(Te);                          // rho_e (scale-free)
-    const double Ee = fma(pe, inv_gm1, (8.0 * re) * fma(ve, ve, ue * ue));   // 16 E_e
+    // 16 (E_e + p_e) = 16 p_e g/(g-1) + 8 rho_e (u_e^2 + v_e^2) (one operation fewer than E_e, then + p_e)
+    const double He = fma(pe, g_gm1, (8.0 * re) * fma(ve, ve, ue * ue));
     const double mn16 = re * U16;                                 // = 16 (re ue) exactly
     F16[0] = mn16;
     F16[1] = fma(mn16, ue, pe);
     F16[2] = mn16 * ve;
-    F16[3] = (Ee + pe) * ue;
+    F16[3] = He * ue;
 }
 
 template <int N>
@@ -978,7 +979,7 @@ template <bool DIV4>
 __host__ __device__ constexpr double c4_fh_scale() { return DIV4 ? 1.0 / 384.0 : 0.0625; }
 
 template <bool DIV4>
-__device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs, int kn, int kt, double inv_gm1,
+__device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs, int kn, int kt, double g_gm1,
                                            int s, double (&Fh)[6][4]) {
     constexpr int PL = kTmaPL;
     double p[4], Tt[4], un[4], ut[4];
@@ -994,7 +995,7 @@ __device__ __forceinline__ void c4_segment(const double* __restrict__ q, int cs,
         for (int c = 0; c < 3; ++c) { p[c] = p[c + 1]; Tt[c] = Tt[c + 1]; un[c] = un[c + 1]; ut[c] = ut[c + 1]; }
         const int o = (e + 1) * cs;
         p[3] = q[o]; Tt[3] = q[PL + o]; un[3] = q[kn * PL + o]; ut[3] = q[kt * PL + o];
-        c4_face16(p, Tt, un, ut, inv_gm1, f[e]);   // 16 f
+        c4_face16(p, Tt, un, ut, g_gm1, f[e]);   // 16 f
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -1031,7 +1032,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     LeafDesc* const sDesc = reinterpret_cast<LeafDesc*>(mbar + 4);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double g = a.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
+    const double g = a.gamma, gm1 = g - 1.0, g_gm1 = g / gm1;   // g/(g-1): c4_face16
     const bool rk_un = a.stage > 1;
     const double ca = a.a, cb = a.b;
     const double dt = *a.dt;
@@ -1220,7 +1221,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             if (warp < 8) {
                 const int j = 4 * warp + seg_line;
                 const double idx = c4_fh_scale<DIV4>() * a.geo.inv_dx[lvl];   // F-hat arrive scaled (c4_segment)
-                c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
+                c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, g_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
                     for (int e = 0; e < 5; ++e)
@@ -1241,7 +1242,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             } else {
                 const int i = 4 * (warp - 8) + seg_line;
                 const double idy = c4_fh_scale<DIV4>() * a.geo.inv_dy[lvl];
-                c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
+                c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, g_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
                     for (int e = 0; e < 5; ++e)
@@ -1616,7 +1617,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     LeafDesc* const sDesc = reinterpret_cast<LeafDesc*>(mbar + 4);          // [3][K] member descriptor ring
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double g = a.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
+    const double g = a.gamma, gm1 = g - 1.0, g_gm1 = g / gm1;   // g/(g-1): c4_face16
     const bool rk_un = a.stage > 1;
     const double ca = a.a, cb = a.b;
     const double dt = *a.dt;
@@ -1770,7 +1771,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             if (warp < 8) {
                 const int j = 4 * warp + seg_line;
                 const double idx = c4_fh_scale<DIV4>() * a.geo.inv_dx[lvl];
-                c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, inv_gm1, seg, Fh);
+                c4_segment<DIV4>(prim + (j + G) * WP + G + m0, 1, 2, 3, g_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
                     for (int e = 0; e < 5; ++e)
@@ -1794,7 +1795,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             } else {
                 const int i = 4 * (warp - 8) + seg_line;
                 const double idy = c4_fh_scale<DIV4>() * a.geo.inv_dy[lvl];
-                c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, inv_gm1, seg, Fh);
+                c4_segment<DIV4>(prim + (m0 + G) * WP + G + i, WP, 3, 2, g_gm1, seg, Fh);
                 if (seg_store) {
 #pragma unroll
                     for (int e = 0; e < 5; ++e)
