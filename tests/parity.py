@@ -27,6 +27,9 @@ def parity_error(so: dict, sg: dict):
     floor = 1e-3 * mx.max()
     den = np.maximum(mx, floor)
     rel = np.where(den > 0, err / np.where(den > 0, den, 1.0), np.where(err == 0, 0.0, np.inf))
+    # O18: a component that is IDENTICALLY zero in the oracle (every cell exactly 0.0, e.g. rho v of the Sod strip)
+    # must be exactly zero on the GPU too -- the floor above only serves components that are zero up to rounding
+    rel = np.where((mx == 0) & (err != 0), np.inf, rel)
     return float(rel.max()), rel
 
 
