@@ -2461,21 +2461,34 @@ __global__ void __launch_bounds__(kPostThreads) post_stage_kernel(const PostArgs
 }
 
 // ---------------------------------------------------------------- Lambda (O13) over leaves
-__global__ void lambda_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs a) {
-    const LeafDesc d = leaves[blockIdx.x];
+// Lambda over all leaves (after a regrid / set_state): one warp per leaf, grid-stride over the leaves, the maximum
+// reduced over the block before ONE atomic per block (a block per leaf with one atomic per warp queued ~8 same-address
+// atomics per leaf -- 10^5 on the shock-bubble mesh)
+__global__ void __launch_bounds__(256) lambda_kernel(const LeafDesc* __restrict__ leaves, int nleaves, const AuxArgs a) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int n = a.geo.n;
     const size_t nn = (size_t)n * n;
-    const double* U = a.U + (size_t)d.slot * 4 * nn;
     unsigned long long lam = 0ull;
-    for (int e = threadIdx.x; e < (int)nn; e += blockDim.x) {
-        double s = wave_speed(U[e], U[nn + e], U[2 * nn + e], U[3 * nn + e], a.gamma, a.geo.inv_dx[d.level],
-                              a.geo.inv_dy[d.level]);
-        if (a.lam0) s = ldexp(s, -d.level);
-        unsigned long long b = (unsigned long long)__double_as_longlong(s);
-        lam = b > lam ? b : lam;
+    for (int leaf = blockIdx.x * 8 + wib; leaf < nleaves; leaf += gridDim.x * 8) {
+        const LeafDesc d = leaves[leaf];
+        const double* U = a.U + (size_t)d.slot * 4 * nn;
+        const double idx = a.geo.inv_dx[d.level], idy = a.geo.inv_dy[d.level];
+#pragma unroll 4
+        for (int e = lane; e < (int)nn; e += 32) {
+            double s = wave_speed(U[e], U[nn + e], U[2 * nn + e], U[3 * nn + e], a.gamma, idx, idy);
+            if (a.lam0) s = ldexp(s, -d.level);
+            unsigned long long bits = (unsigned long long)__double_as_longlong(s);
+            lam = bits > lam ? bits : lam;
+        }
     }
     lam = warp_max_u64(lam);
-    if ((threadIdx.x & 31) == 0 && lam) atomicMax(a.lambda_bits, lam);
+    __shared__ unsigned long long sl[8];
+    if (lane == 0) sl[wib] = lam;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) lam = sl[w] > lam ? sl[w] : lam;
+        if (lam) atomicMax(a.lambda_bits, lam);
+    }
 }
 
 __global__ void set2_kernel(double* p, double a, double b) {
@@ -2525,12 +2538,18 @@ __global__ void dt_dev_kernel(double* dt, unsigned long long* lambda_bits, int32
 }
 
 // ---------------------------------------------------------------- flags (O6)
-__global__ void flags_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs a, double* maxeta, int32_t* amb) {
-    const LeafDesc d = leaves[blockIdx.x];
+// O6 indicator per leaf: one WARP per leaf (a block-per-leaf version waited on a block reduction and one
+// descriptor -> data load chain per 256 cells); the per-cell arithmetic and the u64 maximum are unchanged
+__global__ void __launch_bounds__(256) flags_kernel(const LeafDesc* __restrict__ leaves, int nleaves, const AuxArgs a,
+                                                   double* maxeta, int32_t* amb) {
+    const int leaf = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (leaf >= nleaves) return;
+    const LeafDesc d = leaves[leaf];
     const int n = a.geo.n;
     const size_t nn = (size_t)n * n, PS = 4 * nn;
     const double* own = a.U + (size_t)d.slot * PS;
     const double dx = a.geo.dx[d.level], dy = a.geo.dy[d.level];
+    const double hix = 0.5 * a.geo.inv_dx[d.level], hiy = 0.5 * a.geo.inv_dy[d.level];
     const double th = a.theta, tc = a.theta * a.coarsen_fraction;
     auto rho = [&](int i, int j) -> double {
         const double* b = own;
@@ -2542,27 +2561,24 @@ __global__ void flags_kernel(const LeafDesc* __restrict__ leaves, const AuxArgs 
     };
     unsigned long long m = 0ull;
     int am = 0;
-    for (int e = threadIdx.x; e < (int)nn; e += blockDim.x) {
+#pragma unroll 4
+    for (int e = lane; e < (int)nn; e += 32) {
         int i = e % n, j = e / n;
-        double gx = (rho(i + 1, j) - rho(i - 1, j)) / (2.0 * dx);
-        double gy = (rho(i, j + 1) - rho(i, j - 1)) / (2.0 * dy);
-        double eta = dx * sqrt(gx * gx + gy * gy) / rho(i, j);
+        // central differences and eta = dx |grad rho| / rho with the reciprocal spacings and the stage path's fast
+        // reciprocal / square root (A41: within a few ulp of the divisions; A32's 1e-9 band covers the flags)
+        double gx = (rho(i + 1, j) - rho(i - 1, j)) * hix;
+        double gy = (rho(i, j + 1) - rho(i, j - 1)) * hiy;
+        const double g2 = fma(gx, gx, gy * gy);
+        double eta = dx * (g2 > 0.0 ? fast_sqrt(g2) : g2) * fast_rcp(rho(i, j));   // (fast_sqrt(0) is NaN)
         unsigned long long b = (unsigned long long)__double_as_longlong(eta);
         m = b > m ? b : m;
         if (fabs(eta - th) <= 1e-9 * th || fabs(eta - tc) <= 1e-9 * tc) am = 1;
     }
     m = warp_max_u64(m);
     am = __any_sync(0xffffffffu, am);
-    __shared__ unsigned long long sm[32];
-    __shared__ int sa[32];
-    if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = m; sa[threadIdx.x >> 5] = am; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long r = 0;
-        int ra = 0;
-        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) { r = sm[w] > r ? sm[w] : r; ra |= sa[w]; }
-        maxeta[blockIdx.x] = __longlong_as_double((long long)r);
-        amb[blockIdx.x] = ra;
+    if (lane == 0) {
+        maxeta[leaf] = __longlong_as_double((long long)m);
+        amb[leaf] = am;
     }
 }
 
@@ -2699,7 +2715,8 @@ cudaError_t launch_prolong(const ProlongTask* tasks, int ntasks, const AuxArgs& 
 
 cudaError_t launch_lambda(const LeafDesc* leaves, int nleaves, const AuxArgs& a, cudaStream_t s) {
     if (nleaves <= 0) return cudaSuccess;
-    lambda_kernel<<<nleaves, 256, 0, s>>>(leaves, a);
+    const int blocks = std::min((nleaves + 7) / 8, 4 * sm_count());
+    lambda_kernel<<<blocks, 256, 0, s>>>(leaves, nleaves, a);
     return cudaGetLastError();
 }
 
@@ -2737,7 +2754,7 @@ cudaError_t launch_dt(double* dt, unsigned long long* lambda_bits, int32_t* err,
 cudaError_t launch_flags(const LeafDesc* leaves, int nleaves, const AuxArgs& a, double* maxeta, int32_t* amb,
                          cudaStream_t s) {
     if (nleaves <= 0) return cudaSuccess;
-    flags_kernel<<<nleaves, 256, 0, s>>>(leaves, a, maxeta, amb);
+    flags_kernel<<<(unsigned)((nleaves + 7) / 8), 256, 0, s>>>(leaves, nleaves, a, maxeta, amb);
     return cudaGetLastError();
 }
 
