@@ -29,7 +29,10 @@ res = {}
 for arg in sys.argv[2:]:
     name, spec = arg.split("=")
     rep, cells = spec.split(":")
-    res[name] = work(rep, float(cells))
+    try:
+        res[name] = work(rep, float(cells))
+    except Exception as e:   # noqa: BLE001 -- a missing capture must not lose the others
+        res[name] = {"error": repr(e), "report": rep}
 res["note"] = ("SASS fp64 op counts per leaf cell-stage from ncu --set full (stage 2 of the 4096^2 sweep); "
                "flops = dadd + dmul + 2 dfma")
 json.dump(res, open(sys.argv[1], "w"), indent=1)

@@ -57,7 +57,11 @@ if __name__ == "__main__":
     if reps:
         with open(f"profiles/{tag}_ncu_summary.jsonl", "w") as f:
             for rep in reps:
-                f.write(json.dumps({os.path.basename(rep).replace(".ncu-rep", ""): raw_metrics(rep)}) + "\n")
+                try:
+                    m = raw_metrics(rep)
+                except Exception as e:   # noqa: BLE001 -- a missing capture must not lose the others
+                    m = {"error": repr(e)}
+                f.write(json.dumps({os.path.basename(rep).replace(".ncu-rep", ""): m}) + "\n")
     lp = f"gpurun_out/launches_{tag}.csv"
     if os.path.exists(lp):
         json.dump(launches(lp), open(f"profiles/{tag}_launches.json", "w"), indent=1)
