@@ -130,11 +130,11 @@ __device__ __forceinline__ double weno5(double v0, double v1, double v2, double 
 //   (shared by the two sides), their one-sided u terms, and the candidate stencils as corrections to the
 //   face-adjacent cell (w2 left, w3 right) -- the result is w2 + sum_k omega_k (q_k - w2), since sum omega_k = 1;
 // - the linear weights (1, 10, 5)/16 folded into the corrections and the normalisation (the 1/16 cancels);
-// - every indicator evaluated scaled by 12/13: S = (12 eps/13 + T^2 + 3/13 u^2)^2 = (12/13)^2 (eps + beta)^2, a
-//   common factor of all weights that cancels in the normalisation, and one weight product per candidate
+// - every indicator evaluated scaled by 4: S = (4 eps + 13/3 T^2 + u^2)^2 = 16 (eps + beta)^2, a common factor of all
+//   weights that cancels in the normalisation (the 13/3 on the four shared T terms), and one weight product per candidate
 //   (omega_k ~ d_k prod_{j != k} S_j, one reciprocal per side).
 __device__ __forceinline__ void weno5_pair(double w0, double w1, double w2, double w3, double w4, double w5,
-                                           double eps12_13, double& left, double& right) {
+                                           double eps4, double& left, double& right) {
     const double d01 = w0 - w1, d12 = w1 - w2, d23 = w2 - w3, d34 = w3 - w4, d45 = w4 - w5;
     // corrections q_k - w2 (left) / r_k - w3 (right) times the linear weights 1, 10, 5 (x 16):
     // left (3 d01 - 7 d12)/8, -10 (d12 + 3 d23)/8, 5 (d34 - 5 d23)/8; right (7 d34 - 3 d45)/8, 10 (3 d23 + d34)/8,
@@ -145,13 +145,13 @@ __device__ __forceinline__ void weno5_pair(double w0, double w1, double w2, doub
     const double r2 = fma(3.125, d23, -0.625 * d12);
     // second differences (shared) and one-sided terms: T_a = w0 - 2 w1 + w2 ... T_d = w3 - 2 w4 + w5
     const double Ta = d01 - d12, Tb = d12 - d23, Tc = d23 - d34, Td = d34 - d45;
-    const double Aa = fma(Ta, Ta, eps12_13), Ab = fma(Tb, Tb, eps12_13);
-    const double Ac = fma(Tc, Tc, eps12_13), Ad = fma(Td, Td, eps12_13);
+    constexpr double c13 = 13.0 / 3.0;   // (13/3) T^2 on the four shared terms, u^2 unscaled on the six one-sided ones
+    const double Aa = fma(c13 * Ta, Ta, eps4), Ab = fma(c13 * Tb, Tb, eps4);
+    const double Ac = fma(c13 * Tc, Tc, eps4), Ad = fma(c13 * Td, Td, eps4);
     const double u0 = fma(-2.0, d12, Ta), u1 = d12 + d23, u2 = fma(2.0, d23, Tc);   // w0-4w1+3w2, w1-w3, 3w2-4w3+w4
     const double v0 = fma(2.0, d34, Td), v1 = d23 + d34, v2 = fma(-2.0, d23, Tb);   // 3w3-4w4+w5, w2-w4, w1-4w2+3w3
-    constexpr double c3 = 3.0 / 13.0;
-    double s0 = fma(c3 * u0, u0, Aa), s1 = fma(c3 * u1, u1, Ab), s2 = fma(c3 * u2, u2, Ac);
-    double z0 = fma(c3 * v0, v0, Ad), z1 = fma(c3 * v1, v1, Ac), z2 = fma(c3 * v2, v2, Ab);
+    double s0 = fma(u0, u0, Aa), s1 = fma(u1, u1, Ab), s2 = fma(u2, u2, Ac);
+    double z0 = fma(v0, v0, Ad), z1 = fma(v1, v1, Ac), z2 = fma(v2, v2, Ab);
     s0 *= s0; s1 *= s1; s2 *= s2;
     z0 *= z0; z1 *= z1; z2 *= z2;
     {
@@ -173,7 +173,7 @@ template <bool CHAR>
 __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int cs, int plane, int kn, int kt, double g,
                                              double eps, double F[4]) {
     const double gm1 = g - 1.0;
-    const double eps12_13 = eps * (12.0 / 13.0);
+    const double eps4 = 4.0 * eps;
 #define QV(s, k) q[(k) * plane + (s) * cs]
     double wl[4], wr[4];
     double u = 0.0, v = 0.0, c = 0.0, qk = 0.0, H = 0.0;
@@ -209,21 +209,21 @@ __device__ __forceinline__ void weno_rusanov(const double* __restrict__ q, int c
         }
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = hA[s] + hB[s];
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[0], wr[0]);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps4, wl[0], wr[0]);
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = hA[s] - hB[s];
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[3], wr[3]);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps4, wl[3], wr[3]);
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = fma(-2.0, hA[s], QV(s, 0));
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[1], wr[1]);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps4, wl[1], wr[1]);
 #pragma unroll
         for (int s = 0; s < 6; ++s) w[s] = fma(-v, QV(s, 0), QV(s, kt));
-        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps12_13, wl[2], wr[2]);
+        weno5_pair(w[0], w[1], w[2], w[3], w[4], w[5], eps4, wl[2], wr[2]);
     } else {
         const int kk[4] = {0, kn, kt, 3};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            weno5_pair(QV(0, kk[k]), QV(1, kk[k]), QV(2, kk[k]), QV(3, kk[k]), QV(4, kk[k]), QV(5, kk[k]), eps12_13,
+            weno5_pair(QV(0, kk[k]), QV(1, kk[k]), QV(2, kk[k]), QV(3, kk[k]), QV(4, kk[k]), QV(5, kk[k]), eps4,
                        wl[k], wr[k]);
         }
     }
