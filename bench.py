@@ -113,6 +113,7 @@ def sweep_cfg(args, world, scheme, characteristic=1):
     cfg["check_positivity"] = 0
     cfg["stage_kernel"] = args.stage_kernel
     cfg["halo_mode"] = args.halo_mode
+    cfg["peer_map"] = args.peer_map
     name = (f"BASELINE configs[4] uniform-patch sweep: {args.N}x{args.N * world} cells ({args.N}^2 per GPU, "
             f"D5w weak scaling), {args.n}^2 patches, periodic, noise seed 7")
     return cfg, name
@@ -468,6 +469,8 @@ def main():
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--cfl", type=float, default=0.3)
     ap.add_argument("--stage-kernel", type=int, default=0, help="amr_config.stage_kernel (0 default, 1 per-tile)")
+    ap.add_argument("--peer-map", type=int, default=0, choices=[0, 1],
+                    help="halo_mode 1/2 peer mapping: 0 CUDA IPC, 1 NCCL symmetric windows (ncclMemAlloc pool)")
     ap.add_argument("--halo-mode", type=int, default=0, choices=[0, 1, 2],
                     help="N > 1 halo exchange: 0 pack + NCCL send/recv + unpack, 1 peer pull over CUDA IPC, "
                          "2 remote face strips loaded by the stage kernel from the peers' pools (NEXT #3)")

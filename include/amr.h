@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define AMR_ABI_VERSION 4
+#define AMR_ABI_VERSION 5
 
 typedef struct amr_ctx amr_ctx;   /* opaque */
 
@@ -126,6 +126,13 @@ typedef struct {
                                      Regrid exchanges (coarse sources, migration, flags) use the transport in all
                                      modes */
     const amr_host_comm* host_comm;   /* comm_backend 2: the caller's collectives (kept alive until destroy) */
+    int32_t peer_map;             /* halo_mode 1 / 2 over NCCL (comm_backend 0): how every rank's state pool and
+                                     flux-register buffer are mapped into this process.  0 CUDA IPC handles exchanged
+                                     by an NCCL byte-sum allreduce; 1 NCCL symmetric memory windows: both buffers are
+                                     allocated by the library with ncclMemAlloc (cfg.pool must be NULL), registered
+                                     with ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC), and every peer's address
+                                     is taken on the device from the window with ncclGetPeerPointer (NCCL's
+                                     load/store-accessible device API, nccl_device.h); ABI 5 */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none

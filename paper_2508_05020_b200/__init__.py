@@ -26,7 +26,7 @@ SCHEME = {"central4": 0, "weno5": 1}
 COARSEN = {"r2_exact": 0, "alg2_literal": 1}
 
 # every symbol include/amr.h declares (checked by tests/test_abi.py)
-ABI_VERSION = 4   # include/amr.h AMR_ABI_VERSION: the amr_config / amr_stats layouts below
+ABI_VERSION = 5   # include/amr.h AMR_ABI_VERSION: the amr_config / amr_stats layouts below
 ABI_SYMBOLS = ["amr_abi_version", "amr_default_config", "amr_query_pool_bytes", "amr_create", "amr_destroy",
                "amr_set_state", "amr_set_state_fn", "amr_get_state", "amr_set_state_device", "amr_get_state_device", "amr_step", "amr_steps", "amr_sync", "amr_get_flags",
                "amr_regrid", "amr_regrid_with_flags", "amr_get_patch_tree", "amr_diagnostics",
@@ -44,7 +44,7 @@ class amr_config(C.Structure):
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("world_size", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("check_positivity", C.c_int32),
                 ("use_graphs", C.c_int32), ("comm_backend", C.c_int32), ("stage_kernel", C.c_int32), ("subcycle", C.c_int32),
-                ("halo_mode", C.c_int32), ("host_comm", C.c_void_p)]
+                ("halo_mode", C.c_int32), ("host_comm", C.c_void_p), ("peer_map", C.c_int32)]
 
 
 HOST_ALLGATHER = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p)
@@ -191,6 +191,7 @@ def make_config(cfg: dict, **over) -> amr_config:
     c.use_graphs = int(cfg.get("use_graphs", 0))
     c.subcycle = int(cfg.get("subcycle", 0))
     c.halo_mode = int(cfg.get("halo_mode", 0))
+    c.peer_map = int(cfg.get("peer_map", 0))
     c.world_size = 1
     c.rank = 0
     c.device = -1

@@ -78,6 +78,8 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.max_patches < 1) { m = "max_patches must be positive"; return AMR_E_CONFIG; }
     if (c.stage_kernel < 0 || c.stage_kernel > 3) { m = "stage_kernel must be 0..3"; return AMR_E_CONFIG; }
     if (c.halo_mode < 0 || c.halo_mode > 2) { m = "halo_mode must be 0, 1 or 2"; return AMR_E_CONFIG; }
+    if (c.peer_map < 0 || c.peer_map > 1) { m = "peer_map must be 0 or 1"; return AMR_E_CONFIG; }
+    if (c.peer_map == 1 && c.pool) { m = "peer_map 1 allocates the pool with ncclMemAlloc: cfg.pool must be NULL"; return AMR_E_CONFIG; }
     // halo_mode 2: the stage kernels that load remote face strips themselves -- the Central4 TMA kernel (n >= 32) and
     // the WENO5 kernels (per-tile and n = 8 block tiles); <= 8 ranks (3-bit owner field of LeafDesc.pad)
     if (c.halo_mode == 2 && c.world_size > 1 &&
@@ -211,6 +213,11 @@ void ensure_canon(amr_ctx* c) {
     c->canon = t.canonical();
     for (size_t e = 0; e < c->canon.size(); ++e) c->canon_pos[c->canon[e]] = (int)e;
     c->canon_valid = true;
+}
+
+// peer_map 1: the state pool and the flux registers are NCCL symmetric-window memory, mapped by window registration
+bool nccl_windows(const amr_ctx* c) {
+    return c->cfg.peer_map == 1 && c->cfg.world_size > 1 && c->cfg.comm_backend == 0 && c->cfg.halo_mode >= 1;
 }
 
 amr_status build_plan(amr_ctx* c) {
@@ -442,6 +449,14 @@ amr_status build_plan(amr_ctx* c) {
     }
 
     CU(c->proxy.reserve(std::max<size_t>(1, c->ptasks.size()) * c->PS));
+    if (nccl_windows(c) && !c->freg_nccl) {   // peer_map 1: the flux registers are NCCL window memory too (fixed size)
+        const size_t cnt = (size_t)t.capacity * 16 * c->n;
+        std::string e;
+        c->freg_nccl = comm_nccl_mem_alloc(cnt * sizeof(double), e);
+        if (!c->freg_nccl) return fail(c, AMR_E_COMM, "flux registers: " + e);
+        c->freg.view(reinterpret_cast<double*>(c->freg_nccl), cnt);
+        c->freg.cap = cnt;
+    }
     CU(c->freg.reserve((size_t)t.capacity * 16 * c->n, false));   // indexed by slot (remote fine leaves arrive by exchange)
     CU(c->d_maxeta.reserve(std::max<size_t>(1, c->leaves.size())));
     CU(c->d_amb.reserve(std::max<size_t>(1, c->leaves.size())));
@@ -1055,6 +1070,12 @@ amr_status amr_create(const amr_config* cfg, amr_ctx** out) {
             return AMR_E_ARG;
         }
         base = (char*)cfg->pool;
+    } else if (nccl_windows(c)) {   // symmetric NCCL window memory (peer_map 1)
+        std::string e;
+        c->own_pool = comm_nccl_mem_alloc(need, e);
+        if (!c->own_pool) { std::fprintf(stderr, "amr_create: %s\n", e.c_str()); return AMR_E_COMM; }
+        c->own_pool_nccl = true;
+        base = (char*)c->own_pool;
     } else {
         CU(cudaMalloc(&c->own_pool, need));
         base = (char*)c->own_pool;
@@ -1095,7 +1116,8 @@ void amr_destroy(amr_ctx* c) {
     c->unf_scratch.release();
     c->d_slots.release(); c->d_amb.release(); c->d_sib.release(); c->d_flist.release(); c->d_fcount.release();
     c->arena_dev.release();
-    if (c->own_pool) cudaFree(c->own_pool);
+    if (c->freg_nccl) { c->freg.release(); comm_nccl_mem_free(c->freg_nccl); }
+    if (c->own_pool) { if (c->own_pool_nccl) comm_nccl_mem_free(c->own_pool); else cudaFree(c->own_pool); }
     cudaFree(c->d_dt); cudaFree(c->d_lambda); cudaFree(c->d_err); cudaFree(c->d_tmp); cudaFree(c->d_dtp);
     for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);

@@ -280,6 +280,11 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    // symmetric memory windows (NCCL >= 2.27; optional: only peer_map 1 needs them)
+    ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+    ncclResult_t (*MemFree)(void*) = nullptr;
+    ncclResult_t (*CommWindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+    ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
     bool load(std::string& err) {
         if (h) return true;
         const char* env = getenv("AMR_NCCL_LIB");
@@ -301,6 +306,10 @@ struct NcclApi {
         SYM(GetErrorString, "ncclGetErrorString");
         SYM(CommUserRank, "ncclCommUserRank");
 #undef SYM
+        MemAlloc = reinterpret_cast<decltype(MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+        MemFree = reinterpret_cast<decltype(MemFree)>(dlsym(h, "ncclMemFree"));
+        CommWindowRegister = reinterpret_cast<decltype(CommWindowRegister)>(dlsym(h, "ncclCommWindowRegister"));
+        CommWindowDeregister = reinterpret_cast<decltype(CommWindowDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
         return true;
     }
 };
@@ -311,6 +320,9 @@ NcclApi& nccl_api() {
 
 struct NcclTransport : Transport {
     ncclComm_t comm = nullptr;
+    bool windows = false;           // peer_map 1: map_peers registers NCCL symmetric windows instead of CUDA IPC
+    ncclWindow_t win[2] = {nullptr, nullptr};   // per tag
+    void** d_ptrs = nullptr;        // device scratch for the peer addresses read from a window
     std::string err(ncclResult_t r) { return std::string("NCCL: ") + nccl_api().GetErrorString(r); }
     std::string p2p(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
         NcclApi& A = nccl_api();
@@ -333,7 +345,32 @@ struct NcclTransport : Transport {
     // the W records are combined by a byte-wise sum allreduce (every record is zero except on its owner)
     std::vector<void*> opened[2];   // IPC mappings per tag
     int32_t* d_fence = nullptr;
+    // peer mapping by an NCCL symmetric window (peer_map 1; base from ncclMemAlloc, the same size on every rank):
+    // ncclCommWindowRegister maps every rank's buffer into one load/store-accessible range, and the peers' addresses
+    // are read on the device with ncclGetPeerPointer (launch_window_peer_ptrs); this rank keeps its own base
+    std::string map_peers_window(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s, int tag,
+                                 std::vector<void*>* aliases = nullptr) {
+        NcclApi& A = nccl_api();
+        if (!A.CommWindowRegister || !A.CommWindowDeregister) return "NCCL without ncclCommWindowRegister (need >= 2.27)";
+        if (win[tag]) { A.CommWindowDeregister(comm, win[tag]); win[tag] = nullptr; }
+        ncclResult_t r = A.CommWindowRegister(comm, base, bytes, &win[tag], NCCL_WIN_COLL_SYMMETRIC);
+        if (r != ncclSuccess) { win[tag] = nullptr; return "ncclCommWindowRegister: " + std::string(A.GetErrorString(r)); }
+        const int world = (int)out.size();
+        if (!d_ptrs && cudaMalloc(&d_ptrs, 64 * sizeof(void*)) != cudaSuccess) return "window: cudaMalloc";
+        if (world > 64) return "window: more than 64 ranks";
+        if (launch_window_peer_ptrs(win[tag], world, d_ptrs, s) != cudaSuccess) return "window: peer-pointer kernel";
+        std::vector<void*> h(world, nullptr);
+        if (cudaMemcpyAsync(h.data(), d_ptrs, world * sizeof(void*), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return "window: peer pointers";
+        int me = 0;
+        A.CommUserRank(comm, &me);
+        for (int q = 0; q < world; ++q) out[q] = q == me ? base : h[q];
+        if (aliases) *aliases = h;
+        return std::string();
+    }
     std::string map_peers(void* base, size_t bytes, std::vector<void*>& out, cudaStream_t s, int tag = 0) override {
+        if (windows) return map_peers_window(base, bytes, out, s, tag);
         (void)bytes;
         for (void* p : opened[tag]) cudaIpcCloseMemHandle(p);   // the tag's previous buffer (re-allocated)
         opened[tag].clear();
@@ -385,7 +422,10 @@ struct NcclTransport : Transport {
     ~NcclTransport() override {
         for (auto& v : opened)
             for (void* p : v) cudaIpcCloseMemHandle(p);
+        for (auto& w : win)
+            if (w && comm) nccl_api().CommWindowDeregister(comm, w);
         if (d_fence) cudaFree(d_fence);
+        if (d_ptrs) cudaFree(d_ptrs);
         if (comm) nccl_api().CommDestroy(comm);
     }
 };
@@ -664,6 +704,7 @@ amr_status Comm::init(amr_ctx* c) {
         delete T;
         return AMR_E_COMM;
     }
+    T->windows = c->cfg.peer_map == 1;
     tr.reset(T);
     return AMR_OK;
 #else
@@ -946,6 +987,29 @@ amr_status Comm::allgather_requests(amr_ctx* c, std::vector<int32_t>& lst) {
 
 amr_status Comm::agree_error(amr_ctx*, int32_t*) { return AMR_OK; }
 
+void* comm_nccl_mem_alloc(size_t bytes, std::string& err) {
+#ifdef AMR_HAVE_NCCL_H
+    if (!nccl_api().load(err)) return nullptr;
+    if (!nccl_api().MemAlloc) { err = "NCCL without ncclMemAlloc (need >= 2.19)"; return nullptr; }
+    void* p = nullptr;
+    ncclResult_t r = nccl_api().MemAlloc(&p, bytes);
+    if (r != ncclSuccess) { err = std::string("ncclMemAlloc: ") + nccl_api().GetErrorString(r); return nullptr; }
+    return p;
+#else
+    (void)bytes;
+    err = "library built without nccl.h";
+    return nullptr;
+#endif
+}
+
+void comm_nccl_mem_free(void* p) {
+#ifdef AMR_HAVE_NCCL_H
+    if (p && nccl_api().MemFree) nccl_api().MemFree(p);
+#else
+    (void)p;
+#endif
+}
+
 }  // namespace amr
 
 // ====================================================================================  C ABI pieces
@@ -1020,6 +1084,31 @@ extern "C" amr_status amr_debug_nccl_selftest(const void* uid128, char* msg, int
         else if (!(x = T->fence(s)).empty()) fail(AMR_E_COMM, x);
         else if (cudaStreamSynchronize(s) != cudaSuccess) fail(AMR_E_CUDA, "sync");
     }
+    std::string win_note = "windows not exercised";
+    if (st == AMR_OK && A.MemAlloc && A.CommWindowRegister) {   // peer_map 1: ncclMemAlloc + symmetric window
+        std::string e2;
+        const size_t wb = 1 << 20;
+        void* wbuf = amr::comm_nccl_mem_alloc(wb, e2);
+        if (!wbuf) fail(AMR_E_COMM, e2);
+        else {
+            T->windows = true;
+            std::vector<void*> peers(1, nullptr), alias;
+            std::string x = T->map_peers_window(wbuf, wb, peers, s, 0, &alias);
+            if (!x.empty()) fail(AMR_E_COMM, x);
+            else if (peers[0] != wbuf || !alias[0]) fail(AMR_E_COMM, "window: own base / alias not returned");
+            else {   // rank 0's window address aliases the buffer: write through the alias, read through the base
+                std::vector<double> got(n);
+                if (cudaMemcpyAsync(alias[0], h.data(), n * 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                    amr::d2h_sync(got.data(), wbuf, n * 8, s) != cudaSuccess)
+                    fail(AMR_E_CUDA, "window: copy");
+                else if (std::memcmp(got.data(), h.data(), n * 8) != 0) fail(AMR_E_COMM, "window: alias does not map the buffer");
+                else win_note = "window ok";
+            }
+            if (T->win[0]) { A.CommWindowDeregister(T->comm, T->win[0]); T->win[0] = nullptr; }
+            amr::comm_nccl_mem_free(wbuf);
+        }
+    }
+    if (st == AMR_OK) say(std::string("ok: ") + A.GetErrorString(ncclSuccess) + "; " + win_note);
     cudaFree(src);
     cudaFree(dst);
     T.reset();   // ncclCommDestroy

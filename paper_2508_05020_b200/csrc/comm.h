@@ -138,4 +138,9 @@ struct Comm {
     amr_status agree_error(amr_ctx* c, int32_t* h_err4);
 };
 
+// NCCL symmetric-window memory (peer_map 1): ncclMemAlloc / ncclMemFree through the dlopen'ed library (nullptr and
+// a message when NCCL or the symbol is unavailable)
+void* comm_nccl_mem_alloc(size_t bytes, std::string& err);
+void comm_nccl_mem_free(void* p);
+
 }  // namespace amr

@@ -135,6 +135,8 @@ struct amr_ctx {
     int32_t* d_err = nullptr;
     unsigned long long* d_tmp = nullptr;
     void* h_pinned = nullptr;   // {int32 err[4]; double dt}
+    bool own_pool_nccl = false;  // own_pool from ncclMemAlloc (peer_map 1)
+    void* freg_nccl = nullptr;   // flux registers from ncclMemAlloc (peer_map 1; c->freg is a view of it)
     bool lambda_valid = false;
     bool ghost_valid = false;      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
     double sim_time_fix = 0.0;     // host correction of the device time sum (rolled-back steps)

@@ -22,6 +22,10 @@
 #include <algorithm>
 
 #include "device.h"
+#ifdef AMR_HAVE_NCCL_H
+#include <nccl.h>
+#include <nccl_device.h>   // ncclGetPeerPointer (symmetric memory windows, peer_map 1)
+#endif
 
 namespace amr {
 namespace cg = cooperative_groups;
@@ -2673,6 +2677,24 @@ cudaError_t launch_reflux(const RefluxTask* tasks, int ntasks, const AuxArgs& a,
     long long work = (long long)ntasks * 4 * a.geo.n;
     reflux_kernel<<<grid_for(work, 128), 128, 0, s>>>(tasks, ntasks, a);
     return cudaGetLastError();
+}
+
+#ifdef AMR_HAVE_NCCL_H
+__global__ void window_peer_ptrs_kernel(ncclWindow_t w, int world, void** out) {
+    const int q = threadIdx.x;
+    if (q < world) out[q] = ncclGetPeerPointer(w, 0, q);
+}
+#endif
+
+cudaError_t launch_window_peer_ptrs(const void* win, int world, void** d_out, cudaStream_t s) {
+#ifdef AMR_HAVE_NCCL_H
+    if (!win || world < 1 || world > 64) return cudaErrorInvalidValue;
+    window_peer_ptrs_kernel<<<1, 64, 0, s>>>(reinterpret_cast<ncclWindow_t>(const_cast<void*>(win)), world, d_out);
+    return cudaGetLastError();
+#else
+    (void)win; (void)world; (void)d_out; (void)s;
+    return cudaErrorNotSupported;
+#endif
 }
 
 cudaError_t launch_post_stage(const PostArgs& p, cudaStream_t s) {

@@ -46,7 +46,7 @@ def test_struct_sizes_match_header(lib):
     assert tail == b"\xab" * 64
     c = C.cast(buf, C.POINTER(amr.amr_config)).contents
     assert c.dim == 2 and c.ratio == 2 and c.gamma == 1.4 and c.div_order == 4 and c.weno_eps == 1e-6
-    assert lib.amr_abi_version() == amr.ABI_VERSION == 4
+    assert lib.amr_abi_version() == amr.ABI_VERSION == 5
 
 
 def _cfg(lib, **kw):
