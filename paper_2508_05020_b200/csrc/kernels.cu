@@ -1633,7 +1633,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #endif
 
     // warp 0: arm the landing barrier, then one box per lane (interior of member `lane`, or one edge strip)
-    auto issue = [&](int b, const LeafDesc* D) {
+    // landing of a tile, split so that several warps can issue it: the arrival with the byte count and the member
+    // interiors (lanes < K), and the 4B block-edge strips (strip e = 0 .. 4B-1 per lane); the strips may complete
+    // before the count is armed (the mbarrier's tx-count goes transiently negative)
+    auto issue_interior = [&](int b, const LeafDesc* D) {
         const uint32_t mb = smem_u32(&mbar[b]);
         const uint32_t dst = smem_u32(land + b * kLandSz);
         if (lane == 0) mbar_expect_tx(mb, kLandSz * 8);
@@ -1644,8 +1647,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             } else {
                 tma_load3(dst + (kLandI + lane * 4 * NN) * 8, &maps.in_int, 0, 0, 4 * D[lane].slot, mb);
             }
-        } else if (lane < K + 4 * B) {
-            const int e = lane - K, side = e / B, r = e - side * B;
+        }
+    };
+    auto issue_strip = [&](int b, const LeafDesc* D, int e) {
+        const uint32_t mb = smem_u32(&mbar[b]);
+        const uint32_t dst = smem_u32(land + b * kLandSz);
+        {
+            const int side = e / B, r = e - side * B;
             const int m = side == kW ? gm_of(0, r) : side == kE ? gm_of(B - 1, r) : side == kS ? gm_of(r, 0) : gm_of(r, B - 1);
             const int s = D[m].side[side];
             const int z = s >= 0 ? 4 * s : 4 * (-1 - s);
@@ -1657,6 +1665,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 tma_load3(dst + ((side == kS ? kLandS : kLandN) + r * 16 * N) * 8, mp, 0, side == kS ? N - G : 0, z, mb);
             }
         }
+    };
+    auto issue = [&](int b, const LeafDesc* D) {   // the whole landing from warp 0 (first tile)
+        issue_interior(b, D);
+        if (lane >= K && lane < K + 4 * B) issue_strip(b, D, lane - K);
     };
     auto fetch_desc = [&](int t, int slotbuf) {   // warp 1: member descriptors of tile t -> sDesc[slotbuf]
         // the compiler predicates this copy in every warp; lanes that copy nothing keep one common address (ncu
@@ -1742,21 +1754,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         PH_MARK(2);
         __syncthreads();   // (A)
         PH_MARK(3);
-        if (warp == 0) {
+        // the TMA work of this point spread over three warps (on warp 0 alone it delayed that warp's face pass, and
+        // every other warp waited for it at barrier (B))
+        const bool more = t + stride < ntiles;
+        const LeafDesc* Dn = sDesc + dsn * K;
+        if (warp == 0) {                         // tile k+1: the arrival and the member interiors
             if (lane < K) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 bulk_wait_read0();               // this lane's store of tile k-1 has read landing[b^1]
             }
             __syncwarp();
-            if (t + stride < ntiles) {
-                issue(b ^ 1, sDesc + dsn * K);
-                const LeafDesc* Dn = sDesc + dsn * K;
-                if (rk_un && lane < K) {
-                    if (kBulk1D && (Dn[0].pad & 2)) { if (lane == 0) bulk_prefetch(a.Un + (size_t)Dn[0].slot * 4 * NN, K * 4 * NN * 8); }
-                    else tma_prefetch3(&maps.un_int, 0, 0, 4 * Dn[lane].slot);
-                }
+            if (more) issue_interior(b ^ 1, Dn);
+        } else if (warp == kTmaThreads / 32 - 1) {   // tile k+1: the block-edge strips
+            if (more && lane < 4 * B) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_strip(b ^ 1, Dn, lane);
             }
-            if (rk_un) {                         // U^n of tile k into the converted landing[b] interior
+        } else if (warp == kTmaThreads / 64 - 1) {   // U^n of tile k into the converted landing[b]; tile k+1's to L2
+            if (rk_un) {
+                if (lane < K) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 const uint32_t mb = smem_u32(&mbar[2 + b]);
                 if (lane == 0) mbar_expect_tx(mb, 4 * T * T * 8);
                 __syncwarp();
@@ -1764,6 +1780,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     if (lane == 0) bulk_load(smem_u32(land + b * kLandSz + kLandI), a.Un + (size_t)D[0].slot * 4 * NN, K * 4 * NN * 8, mb);
                 } else if (lane < K) {
                     tma_load3(smem_u32(land + b * kLandSz + kLandI + lane * 4 * NN), &maps.un_int, 0, 0, 4 * D[lane].slot, mb);
+                }
+                if (more && lane < K) {
+                    if (kBulk1D && (Dn[0].pad & 2)) { if (lane == 0) bulk_prefetch(a.Un + (size_t)Dn[0].slot * 4 * NN, K * 4 * NN * 8); }
+                    else tma_prefetch3(&maps.un_int, 0, 0, 4 * Dn[lane].slot);
                 }
             }
         }
