@@ -327,8 +327,14 @@ __device__ __forceinline__ const double* side_source(const StageArgs& a, const L
 
 // SCHEME 0: Central4; 1: WENO5 characteristic; 2: WENO5 component-wise.
 // One CTA per T x T tile of a leaf patch (T = n, or 32 for n = 64).
+// CTAs per SM the stage kernel is compiled for: component-wise WENO5 at T = 16 fits 96 registers without spills at
+// 5 (shared memory admits 5 x 38 KB), 1.22 -> 1.16 ms on the 4096^2 sweep; the characteristic kernel was 1.2 % slower
+// there (1.51 -> 1.53 ms) and keeps 4
 template <int SCHEME, int T>
-__global__ void __launch_bounds__(Block<T>::NT, Block<T>::MINB) stage_kernel(const StageArgs a) {
+struct StageMinB { static constexpr int v = (SCHEME == 2 && T == 16) ? 5 : Block<T>::MINB; };
+
+template <int SCHEME, int T>
+__global__ void __launch_bounds__(Block<T>::NT, StageMinB<SCHEME, T>::v) stage_kernel(const StageArgs a) {
     constexpr int G = kGL;
     constexpr int NT = Block<T>::NT;
     constexpr int W = T + 2 * G;       // tile row width in shared memory (doubles)
