@@ -104,30 +104,6 @@ __device__ __forceinline__ void leaf_check(double r, double m, double w, double 
 }
 
 // ---------------------------------------------------------------- reconstruction + flux
-// WENO5-JS point-value interpolation to the face between v2 and v3 (A2), with the
-// three nonlinear weights normalised through one division (A41):
-// alpha_k ~ d_k / s_k, s_k = (eps + beta_k)^2  =>  omega_k ~ d_k prod_{j != k} s_j.
-__device__ __forceinline__ double weno5(double v0, double v1, double v2, double v3, double v4, double eps) {
-    const double c13_12 = 13.0 / 12.0;
-    // candidate stencils with the 1/8 and the linear weights' 10 and 5 folded into the coefficients:
-    // q0 = (3 v0 - 10 v1 + 15 v2)/8, q1' = 10 (-v1 + 6 v2 + 3 v3)/8, q2' = 5 (3 v2 + 6 v3 - v4)/8
-    const double q0 = fma(0.375, v0, fma(-1.25, v1, 1.875 * v2));
-    const double q1 = fma(-1.25, v1, fma(7.5, v2, 3.75 * v3));
-    const double q2 = fma(1.875, v2, fma(3.75, v3, -0.625 * v4));
-    const double t0 = fma(-2.0, v1, v0 + v2), u0 = fma(-4.0, v1, fma(3.0, v2, v0));
-    const double t1 = fma(-2.0, v2, v1 + v3), u1 = v1 - v3;
-    const double t2 = fma(-2.0, v3, v2 + v4), u2 = fma(3.0, v2, fma(-4.0, v3, v4));
-    double s0 = eps + fma(c13_12 * t0, t0, (0.25 * u0) * u0);
-    double s1 = eps + fma(c13_12 * t1, t1, (0.25 * u1) * u1);
-    double s2 = eps + fma(c13_12 * t2, t2, (0.25 * u2) * u2);
-    s0 *= s0; s1 *= s1; s2 *= s2;
-    // omega_k ~ d_k / s_k with d = (1, 10, 5)/16: weights w_k = prod_{j != k} s_j, the d_k folded into q1, q2
-    const double w0 = s1 * s2, w1 = s0 * s2, w2 = s0 * s1;
-    const double num = fma(w0, q0, fma(w1, q1, w2 * q2));
-    const double den = fma(10.0, w1, fma(5.0, w2, w0));
-    return num * fast_rcp(den);
-}
-
 // Both WENO5-JS interpolations at one face from the 6 stencil values w0..w5 (cells i-2 .. i+3): the left-biased
 // value from (w0..w4) and the right-biased one from (w5..w1) (A2), rewritten exactly in real arithmetic (A41):
 // - everything from the first differences d_ij = w_i - w_j: the second differences T of the smoothness indicators
