@@ -80,6 +80,8 @@ def _cfg(lib, **kw):
     dict(world_size=2, rank=0, comm_backend=2),                      # host collectives missing
     dict(world_size=2, rank=0, halo_mode=2, scheme=1, stage_kernel=2, nccl_unique_id=1),   # unfused: no in-kernel strips
     dict(world_size=2, rank=0, halo_mode=2, scheme=0, patch_cells=16, nccl_unique_id=1),   # Central4 n < 32
+    dict(peer_map=2),
+    dict(world_size=2, rank=0, halo_mode=1, peer_map=1, nccl_unique_id=1, pool=1, pool_bytes=1 << 40),   # window pool
 ])
 def test_invalid_config_rejected_without_device(lib, kw):
     c = _cfg(lib, **kw)
