@@ -336,8 +336,9 @@ __global__ void __launch_bounds__(Block<T>::NT, StageMinB<SCHEME, T>::v) stage_k
     {
         constexpr int CR = W / 2, CB = T * CR, CS = G * T / 2, CV = CB + 2 * CS;
         const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sQ);
-        for (int e = tid; e < 4 * CV; e += NT) {
-            int k = e / CV, f = e - k * CV, i, j;
+        // 16-byte chunk f of one component plane -> (shared offset, source address of component 0)
+        auto chunk = [&](int f, uint32_t& dst, const double*& src) {
+            int i, j;
             if (f < CB) { j = f / CR; i = 2 * (f - j * CR) - G; }
             else if (f < CB + CS) { int h = f - CB; j = h / (T / 2) - G; i = 2 * (h - (j + G) * (T / 2)); }
             else { int h = f - CB - CS; j = h / (T / 2); i = 2 * (h - j * (T / 2)); j += T; }
@@ -351,7 +352,26 @@ __global__ void __launch_bounds__(Block<T>::NT, StageMinB<SCHEME, T>::v) stage_k
             else halo = false;
             if (halo) s = d.side[sd];
             const double* base = !halo ? own : (s >= 0 ? side_source(a, d, sd) + (size_t)s * PS : a.proxy + (size_t)(-1 - s) * PS);
-            cp_async16(sb + (uint32_t)((k * PL + (j + G) * W + (i + G)) * 8), base + k * nn + (size_t)pj * n + pi);
+            dst = sb + (uint32_t)(((j + G) * W + (i + G)) * 8);
+            src = base + (size_t)pj * n + pi;
+        };
+        if (CV % NT == 0) {   // a thread's chunks are the same CV / NT positions in each of the 4 planes: map once
+#pragma unroll
+            for (int r = 0; r < CV / NT; ++r) {
+                uint32_t dst;
+                const double* src;
+                chunk(tid + r * NT, dst, src);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) cp_async16(dst + (uint32_t)(k * PL * 8), src + k * nn);
+            }
+        } else {
+            for (int e = tid; e < 4 * CV; e += NT) {
+                const int k = e / CV;
+                uint32_t dst;
+                const double* src;
+                chunk(e - k * CV, dst, src);
+                cp_async16(dst + (uint32_t)(k * PL * 8), src + k * nn);
+            }
         }
         cp_async_wait_all();
     }
@@ -1964,9 +1984,12 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
     // ---- halo gather (a1): plus-shaped block tile in 16-byte chunks; a chunk never straddles two members
     {
         constexpr int CR = W / 2, CB = T * CR, CS = G * T / 2, CV = CB + 2 * CS;
+        static_assert(CV % NT == 0, "a thread's chunks sit at the same positions of the 4 planes");
         const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sQ);
-        for (int e = tid; e < 4 * CV; e += NT) {
-            int kq = e / CV, f = e - kq * CV, i, j;
+#pragma unroll
+        for (int r = 0; r < CV / NT; ++r) {   // each chunk position mapped once, then its 4 component planes
+            const int f = tid + r * NT;
+            int i, j;
             if (f < CB) { j = f / CR; i = 2 * (f - j * CR) - G; }
             else if (f < CB + CS) { int h = f - CB; j = h / (T / 2) - G; i = 2 * (h - (j + G) * (T / 2)); }
             else { int h = f - CB - CS; j = h / (T / 2); i = 2 * (h - j * (T / 2)); j += T; }
@@ -1982,7 +2005,10 @@ __global__ void __launch_bounds__(Block<32>::NT, Block<32>::MINB) stage_group_ke
             if (halo) sl = d.side[sd];
             const double* base = !halo ? a.Uin + (size_t)sl * PS
                                        : (sl >= 0 ? side_source(a, d, sd) + (size_t)sl * PS : a.proxy + (size_t)(-1 - sl) * PS);
-            cp_async16(sb + (uint32_t)((kq * PL + (j + G) * W + (i + G)) * 8), base + kq * NN + pj * N + pi);
+            const uint32_t dst = sb + (uint32_t)(((j + G) * W + (i + G)) * 8);
+            const double* src = base + pj * N + pi;
+#pragma unroll
+            for (int kq = 0; kq < 4; ++kq) cp_async16(dst + (uint32_t)(kq * PL * 8), src + kq * NN);
         }
         cp_async_wait_all();
     }
