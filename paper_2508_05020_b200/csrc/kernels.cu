@@ -281,9 +281,14 @@ struct Block<32> { static constexpr int NT = 256; static constexpr int MINB = 2;
 template <int T>
 constexpr bool kCombFaces = T <= 16;
 
+// WENO tiles of T <= 16 also stage U^n of the tile in shared memory (cp.async issued with the halo gather, waited
+// for before the divergence), instead of a dependent global load in the update
+template <int SCHEME, int T>
+constexpr bool kUnSmem = SCHEME == 1 && T <= 16;   // (component-wise WENO runs 5 CTAs/SM at T = 16: no room)
 template <int SCHEME, int T>
 constexpr size_t stage_smem() {
-    return sizeof(double) * (4 * (T + 2 * kGL) * (T + 2 * kGL) + (kCombFaces<T> ? 2 : 1) * 4 * T * (T + 3));
+    return sizeof(double) * (4 * (T + 2 * kGL) * (T + 2 * kGL) + (kCombFaces<T> ? 2 : 1) * 4 * T * (T + 3) +
+                             (kUnSmem<SCHEME, T> ? 4 * T * T : 0));
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
@@ -292,6 +297,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // The stage-input buffer a same-level side neighbour is read from: the local one, or -- halo_mode 2, neighbour owned
 // by another rank (LeafDesc.pad bits 4 + s, owner in bits 8 + 3 s) -- that rank's pool mapped over NVLink, so the
@@ -320,6 +328,7 @@ __global__ void __launch_bounds__(Block<T>::NT, StageMinB<SCHEME, T>::v) stage_k
     extern __shared__ __align__(16) double smem[];
     double* sQ = smem;                 // [4][W][W]: conserved (WENO) / (p, T, u, v) (Central4)
     double* sF = smem + 4 * PL;        // [4][T][NF] x-fluxes, then [4][NF][T] y-fluxes
+    double* const sUn = sF + (kCombFaces<T> ? 2 : 1) * 4 * T * (T + 3);   // [4][T][T] U^n (kUnSmem)
 
     const int tid = threadIdx.x;
     const int tiles2 = a.tiles * a.tiles;
@@ -373,7 +382,20 @@ __global__ void __launch_bounds__(Block<T>::NT, StageMinB<SCHEME, T>::v) stage_k
                 cp_async16(dst + (uint32_t)(k * PL * 8), src + k * nn);
             }
         }
-        cp_async_wait_all();
+        if (kUnSmem<SCHEME, T> && a.stage > 1) {   // U^n of the tile: a second group, waited for before the divergence
+            cp_async_commit();
+            const uint32_t su = (uint32_t)__cvta_generic_to_shared(sUn);
+            const double* pn0 = a.Un + (size_t)d.slot * PS;
+            constexpr int CH = T * T / 2;   // 16-byte chunks per component
+            for (int e = tid; e < 4 * CH; e += NT) {
+                const int k = e / CH, r = e - k * CH, jj = r / (T / 2), ii = 2 * (r - jj * (T / 2));
+                cp_async16(su + (uint32_t)((k * T * T + jj * T + ii) * 8), pn0 + k * nn + (size_t)(ty * T + jj) * n + tx * T + ii);
+            }
+            cp_async_commit();
+            cp_async_wait1();
+        } else {
+            cp_async_wait_all();
+        }
     }
     __syncthreads();
 
@@ -460,6 +482,7 @@ __global__ void __launch_bounds__(Block<T>::NT, StageMinB<SCHEME, T>::v) stage_k
             else if (e - NXF < NXF) { yh_e = e - NXF; y_flux(yh_e, yh); }
         }
     }
+    if (kUnSmem<SCHEME, T> && a.stage > 1) cp_async_wait0();   // this thread's U^n chunks; the barrier shows all
     __syncthreads();
     // ---- x divergence (a7, Eq. 9 flux form) into registers
     double acc[CPT][4];
@@ -516,7 +539,7 @@ __global__ void __launch_bounds__(Block<T>::NT, StageMinB<SCHEME, T>::v) stage_k
                     a.freg[(((size_t)d.slot * 4 + kN) * 4 + k) * n + tx * T + i] = fsc * Fh;
                 // U^(s-1): the WENO tile holds it in shared memory (Central4 converted its tile to primitives)
                 double v = (SCHEME != 0 ? sQ[k * PL + (j + G) * W + (i + G)] : __ldg(pin + k * nn + off)) + dt * L;
-                if (a.stage > 1) v = a.a * __ldg(pn + k * nn + off) + a.b * v;
+                if (a.stage > 1) v = a.a * (kUnSmem<SCHEME, T> ? sUn[(k * T + j) * T + i] : __ldg(pn + k * nn + off)) + a.b * v;
                 o4[k] = v;
             }
 #pragma unroll
