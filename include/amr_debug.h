@@ -41,6 +41,14 @@ amr_status amr_plan_exchange(amr_plan* p, int32_t world_size, int32_t rank, int3
  * rank's leaves, halo items received, halo items sent.  Host only. */
 amr_status amr_plan_profile(amr_plan* p, int32_t world, int32_t rank, int32_t reps, double* ms, int64_t* counts);
 
+/* The plan phases of a regrid's build_plan (leaf launch order, face-neighbour table, leaf descriptors with their proxy
+ * strip and reflux tasks) of `rank` under a world_size partition, computed serially and in parts on the library's armed
+ * host thread pool (AMR_HOST_THREADS), reps times each.  ms[6]: serial leaf order, neighbours, descriptors, then the
+ * same pooled (milliseconds per run, this CPU); counts[4]: leaves, proxy tasks, reflux tasks, pool threads; *equal = 1
+ * iff the two plans agree byte for byte.  AMR_E_MESH if the tree fails the descriptor checks.  Host only. */
+amr_status amr_plan_build_check(amr_plan* p, int32_t world, int32_t rank, int32_t halo_mode, int32_t reps, double* ms,
+                                int64_t* counts, int32_t* equal);
+
 /* NCCL self-test (needs a GPU and torch's libnccl.so.2): a ONE-rank communicator from the 128-byte unique id
  * (amr_nccl_unique_id) drives the data path's NCCL transport -- grouped send/recv to self (the halo / flux /
  * migration exchange call pattern), the four allreduce kinds (Lambda max-u64, max-f64, sum-f64 totals, max-i32

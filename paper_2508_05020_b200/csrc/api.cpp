@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "ctx.h"
+#include "plan.h"
 
 using namespace amr;
 
@@ -225,6 +226,9 @@ amr_status build_plan(amr_ctx* c) {
     PhaseClock clk;
     PatchTree& t = c->tree;
     const int L = c->cfg.num_levels;
+    // the plan phases run in parts on the host pool for large trees (its workers spin while armed; below ~8 k leaves
+    // the parts' fixed cost and the spinning threads' competition for the cores cost more than they save: configs[2])
+    std::unique_ptr<PoolArm> arm(t.n_leaves() >= kPoolMinLeaves ? new PoolArm() : nullptr);
     c->canon_valid = false;   // the canonical order is rebuilt on demand (ensure_canon)
     // id -> position maps sized once; the previous plan's entries are cleared instead of refilling all slots
     if ((int)c->leaf_pos.size() != t.capacity) c->leaf_pos.assign(t.capacity, -1);
@@ -240,14 +244,9 @@ amr_status build_plan(amr_ctx* c) {
     }
 
     // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos (a depth-first walk
-    // from this rank's roots in Morton order; the planning API checks it against the sort of (level, Morton) keys)
-    {
-        static thread_local std::vector<std::vector<int32_t>> per;   // scratch kept across plans
-        t.leaves_morton_roots(per, [](int) { return true; },
-                              [&](int root) { return c->comm.owns(c, root); });
-        c->leaf_ids.clear();
-        for (const auto& lv : per) c->leaf_ids.insert(c->leaf_ids.end(), lv.begin(), lv.end());
-    }
+    // from this rank's roots in Morton order, in parts over root ranges merged level by level -- plan.h; the planning
+    // API checks it against the sort of (level, Morton) keys)
+    plan_leaf_order(t, [&](int root) { return c->comm.owns(c, root); }, c->leaf_ids);
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
     clk.mark("plan: leaf order");
     // owned parents whose 4 children are leaves: the coarsening candidates of a12; owned covered patches: the
@@ -270,88 +269,19 @@ amr_status build_plan(amr_ctx* c) {
     clk.mark("plan: sib + restriction");
 
     // face neighbours of the local patches and of those they read across the boundary, from the parents' entries
-    // (subtree pre-order, no recursion): nb4[4 id + s]
-    t.face_neighbours_roots(nb_roots, c->nb4);
+    // (subtree pre-order, no recursion; independent root subtrees in parts): nb4[4 id + s]
+    plan_face_neighbours(t, nb_roots, c->nb4);
     clk.mark("plan: face neighbours");
-    // a C/F parent's 3 x 3 neighbourhood: faces from nb4, corners through the N / S face neighbour (R2: all 8
-    // exist inside the domain); -2 outside the domain
-    auto nbr = [&](int id, int dx, int dy) -> int {
-        if (dx == 0 && dy == 0) return id;
-        const int32_t* o = &c->nb4[(size_t)4 * id];
-        if (dy == 0) return o[dx < 0 ? kW : kE];
-        const int v = o[dy < 0 ? kS : kN];
-        if (dx == 0 || v < 0) return v;
-        const int r = c->nb4[(size_t)4 * v + (dx < 0 ? kW : kE)];
-        return r == -1 ? t.neighbour(id, dx, dy) : r;   // (-1: R2 violated; neighbour() decides as before)
-    };
-    c->leaves.clear();
-    c->ptasks.clear();
-    c->rtasks.clear();
-    int cpar = -1, cnb[9];   // the last C/F parent's 3 x 3 neighbourhood
-    for (int id : c->leaf_ids) {
-        LeafDesc d{};
-        d.slot = id;
-        d.level = t.lev[id];
-        d.cf = 0;
-        RefluxTask rt{};
-        rt.leaf = (int)c->leaves.size();
-        rt.slot = id;
-        rt.level = t.lev[id];
-        rt.mask = 0;
-        for (int s = 0; s < 4; ++s) {
-            int nb = c->nb4[(size_t)4 * id + s];
-            if (nb >= 0) {
-                d.side[s] = nb;
-                if (c->comm.world > 1 && c->comm.halo_mode == 2 && c->comm.owner[nb] != c->comm.rank)
-                    d.pad |= (16 << s) | (c->comm.owner[nb] << (8 + 3 * s));   // strip read from the owner's pool
-                if (t.has_children(nb)) {
-                    d.cf |= 1 << s;
-                    rt.mask |= 1 << s;
-                    // the two children of nb adjacent to the shared face, ordered along it
-                    int cidx[2];
-                    if (s == kW) { cidx[0] = 1; cidx[1] = 3; }
-                    else if (s == kE) { cidx[0] = 0; cidx[1] = 2; }
-                    else if (s == kS) { cidx[0] = 2; cidx[1] = 3; }
-                    else { cidx[0] = 0; cidx[1] = 1; }
-                    for (int h = 0; h < 2; ++h) {
-                        int ch = t.child[4 * nb + cidx[h]];
-                        if (ch < 0 || !t.is_leaf(ch)) return fail(c, AMR_E_MESH, "reflux: fine side is not a leaf");
-                        rt.fine[s][h] = ch;
-                    }
-                }
-            } else {
-                ProxyTask p{};
-                p.proxy = (int)c->ptasks.size();
-                p.slot = id;
-                p.side = s;
-                p.level = t.lev[id];
-                p.P = t.pi[id];
-                p.Q = t.pj[id];
-                if (nb == -2) {
-                    p.kind = 0;
-                    for (int q = 0; q < 9; ++q) p.coarse[q] = -1;
-                } else {
-                    p.kind = 1;
-                    d.cf |= 1 << (4 + s);
-                    int par = t.parent[id];
-                    if (par < 0) return fail(c, AMR_E_MESH, "missing same-level neighbour of a root");
-                    if (par != cpar) {   // siblings are consecutive in Morton order: one 3 x 3 lookup per parent
-                        cpar = par;
-                        for (int dy = -1; dy <= 1; ++dy)
-                            for (int dx = -1; dx <= 1; ++dx) {
-                                int q = nbr(par, dx, dy);
-                                if (q == -1) return fail(c, AMR_E_MESH, "R2 violated: coarse neighbourhood incomplete");
-                                cnb[(dy + 1) * 3 + (dx + 1)] = q < 0 ? -1 : q;
-                            }
-                    }
-                    for (int q = 0; q < 9; ++q) p.coarse[q] = cnb[q];
-                }
-                d.side[s] = -1 - p.proxy;
-                c->ptasks.push_back(p);
-            }
-        }
-        c->leaves.push_back(d);
-        if (rt.mask) c->rtasks.push_back(rt);
+    {   // leaf descriptors, proxy strips (numbered in leaf order) and reflux tasks, in parts of the leaf order
+        static thread_local DescOut dout;
+        DescOut& D = dout;
+        std::string m;
+        if (!plan_descriptors(t, c->nb4, c->leaf_ids, c->comm.owner, c->comm.world, c->comm.rank, c->comm.halo_mode,
+                              D, m))
+            return fail(c, AMR_E_MESH, m);
+        c->leaves.swap(D.leaves);
+        c->ptasks.swap(D.ptasks);
+        c->rtasks.swap(D.rtasks);
     }
     clk.mark("plan: leaf descriptors");
     c->leaf_cells = (int64_t)c->leaf_ids.size() * c->n * c->n;
@@ -400,6 +330,9 @@ amr_status build_plan(amr_ctx* c) {
         span(c->rtasks.size() * sizeof(RefluxTask));
         for (int l = 0; l < L; ++l) span(c->rlev[l].size() * sizeof(RestrictTask));
         span(c->sib.size() * sizeof(int32_t));
+        // the previous plan's DMA out of the pinned arena must be done before it is refilled (build_plan does not
+        // wait for its own upload: the host goes on to the prolongation launches while it runs)
+        if (c->arena_ev) CU(cudaEventSynchronize(c->arena_ev));
         if (total > c->arena_host_cap) {
             if (c->arena_host) cudaFreeHost(c->arena_host);
             c->arena_host = nullptr;
@@ -429,6 +362,8 @@ amr_status build_plan(amr_ctx* c) {
         for (auto& d : c->d_rlev) d.release();
         CU(c->arena_dev.reserve(std::max<size_t>(used, 256)));
         if (used) CU(cudaMemcpyAsync(c->arena_dev.p, c->arena_host, used, cudaMemcpyHostToDevice, s));
+        if (!c->arena_ev) CU(cudaEventCreateWithFlags(&c->arena_ev, cudaEventDisableTiming));
+        CU(cudaEventRecord(c->arena_ev, s));
         char* base = c->arena_dev.p;
         size_t k = 0;
         c->d_leaves.view(reinterpret_cast<LeafDesc*>(base + offs[k++]), c->leaves.size());
@@ -463,7 +398,8 @@ amr_status build_plan(amr_ctx* c) {
     CU(c->d_flist.reserve(2 * (c->leaves.size() + c->sib.size() / 5) + 2));
     CU(c->d_fcount.reserve(1));
     CU(c->d_partial.reserve(4 * std::max<size_t>(1, c->leaves.size())));
-    CU(cudaStreamSynchronize(s));   // host vectors may change after return
+    // no stream synchronisation: the descriptors travel from the pinned arena (guarded by arena_ev) and the
+    // subcycling lists' pageable copies are staged by the driver before cudaMemcpyAsync returns
     clk.mark("plan: uploads");
 
     c->st.leaves = t.n_leaves();
@@ -951,7 +887,8 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
         CU(c->d_prolong.upload(pro[l], c->stream));
         AuxArgs a = aux(c, Un, Un);
         LAUNCH(launch_prolong(c->d_prolong.p, (int)pro[l].size(), a, c->stream), "prolong");
-        CU(cudaStreamSynchronize(c->stream));
+        // (no synchronisation per level: the next level's upload into d_prolong is stream-ordered after this launch;
+        // a growing d_prolong is freed by cudaFree, which waits for the device)
     }
     s = restrict_all(c, Un);
     if (s != AMR_OK) return s;
@@ -1122,6 +1059,7 @@ void amr_destroy(amr_ctx* c) {
     for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->arena_host) cudaFreeHost(c->arena_host);
+    if (c->arena_ev) cudaEventDestroy(c->arena_ev);
     for (auto e : c->ev_free) cudaEventDestroy(e);
     for (auto e : c->ev_pending) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);

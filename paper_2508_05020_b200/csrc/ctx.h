@@ -121,6 +121,7 @@ struct amr_ctx {
     // grown geometrically, never zero-filled; freed with the ctx
     char* arena_host = nullptr;
     size_t arena_host_cap = 0;
+    cudaEvent_t arena_ev = nullptr;   // recorded after the arena's upload: the next fill waits for it
     DevArray<char> arena_dev;
     DevArray<ProlongTask> d_prolong;
     DevArray<double> proxy, freg, staging, d_maxeta, d_partial, unf_scratch;

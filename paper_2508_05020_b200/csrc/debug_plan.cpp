@@ -4,10 +4,12 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <string>
 #include <vector>
 
 #include "comm.h"
+#include "plan.h"
 #include "tree.h"
 
 struct amr_plan {
@@ -215,6 +217,61 @@ amr_status amr_plan_profile(amr_plan* p, int32_t world, int32_t rank, int32_t re
     }
     for (int k = 0; k < 7; ++k) ms[k] /= reps;
     return AMR_OK;
+}
+
+
+// The plan phases of build_plan (leaf order, face-neighbour table, leaf descriptors: plan.h) of `rank` under a
+// `world` partition, serially and on the armed host pool, reps times each; ms[0..2] serial, ms[3..5] pooled
+// (milliseconds per run), *equal = 1 iff both give the same leaf order, nb4 entries of the planned patches and
+// descriptor / proxy / reflux arrays byte for byte.  counts[0..2]: leaves, proxy tasks, reflux tasks; counts[3]:
+// threads of the pool.
+amr_status amr_plan_build_check(amr_plan* p, int32_t world, int32_t rank, int32_t halo_mode, int32_t reps, double* ms,
+                                int64_t* counts, int32_t* equal) {
+    if (!p || world < 1 || rank < 0 || rank >= world || reps < 1 || !ms || !counts || !equal) return AMR_E_ARG;
+    using clk = std::chrono::steady_clock;
+    const amr::PatchTree& t = p->tree;
+    amr::Owners owner = amr::partition_owners(t, world);
+    std::vector<int32_t> nb_roots = owner.roots_of(rank);
+    for (int r2 : owner.boundary_roots(rank))
+        if (owner.root_rank[(size_t)r2] != rank) nb_roots.push_back(r2);
+    struct Out {
+        std::vector<int32_t> ids, nb4;
+        amr::DescOut d;
+        std::string err;
+        bool ok = true;
+    } o[2];
+    amr::HostPool& pool = amr::HostPool::get();
+    auto d = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    for (int v = 0; v < 2; ++v) {
+        pool.set_serial(v == 0);
+        amr::PoolArm arm;
+        double a0 = 0, a1 = 0, a2 = 0;
+        for (int r = 0; r < reps; ++r) {
+            auto t0 = clk::now();
+            amr::plan_leaf_order(t, [&](int root) { return owner[root] == rank; }, o[v].ids);
+            auto t1 = clk::now();
+            amr::plan_face_neighbours(t, nb_roots, o[v].nb4);
+            auto t2 = clk::now();
+            o[v].ok = amr::plan_descriptors(t, o[v].nb4, o[v].ids, owner, world, rank, halo_mode, o[v].d, o[v].err);
+            auto t3 = clk::now();
+            a0 += d(t0, t1); a1 += d(t1, t2); a2 += d(t2, t3);
+        }
+        ms[3 * v] = a0 / reps; ms[3 * v + 1] = a1 / reps; ms[3 * v + 2] = a2 / reps;
+    }
+    pool.set_serial(false);
+    auto same = [](const auto& a, const auto& b) {
+        return a.size() == b.size() && (a.empty() || std::memcmp(a.data(), b.data(), a.size() * sizeof(a[0])) == 0);
+    };
+    bool eq = o[0].ok == o[1].ok && o[0].err == o[1].err && same(o[0].ids, o[1].ids) && same(o[0].d.leaves, o[1].d.leaves) &&
+              same(o[0].d.ptasks, o[1].d.ptasks) && same(o[0].d.rtasks, o[1].d.rtasks);
+    for (int id : o[0].ids)   // the planned leaves' neighbour entries (the rest of the table is scratch)
+        for (int s2 = 0; s2 < 4; ++s2) eq = eq && o[0].nb4[(size_t)4 * id + s2] == o[1].nb4[(size_t)4 * id + s2];
+    *equal = eq ? 1 : 0;
+    counts[0] = (int64_t)o[1].ids.size();
+    counts[1] = (int64_t)o[1].d.ptasks.size();
+    counts[2] = (int64_t)o[1].d.rtasks.size();
+    counts[3] = pool.threads();
+    return o[0].ok ? AMR_OK : AMR_E_MESH;
 }
 
 }  // extern "C"

@@ -340,17 +340,28 @@ void PatchTree::face_neighbours(const std::vector<int32_t>& canon, std::vector<i
 
 void PatchTree::face_neighbours_roots(const std::vector<int32_t>& roots, std::vector<int32_t>& nb4) const {
     if (nb4.size() != (size_t)4 * capacity) nb4.assign((size_t)4 * capacity, -1);
+    face_neighbours_span(roots.data(), roots.size(), nb4, walk_);
+}
+
+void PatchTree::face_neighbours_span(const int32_t* roots, size_t nr, std::vector<int32_t>& nb4,
+                                     std::vector<int32_t>& st) const {
     static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
-    for (int r : roots)
-        subtree(root_[(size_t)r], [&](int id) {
+    for (size_t k = 0; k < nr; ++k) {
+        st.clear();
+        st.push_back(root_[(size_t)roots[k]]);
+        while (!st.empty()) {   // pre-order: a patch's parent is done before it
+            const int id = st.back();
+            st.pop_back();
             const Node& nd = node_[id];
+            if (nd.child[0] >= 0)
+                for (int q = 3; q >= 0; --q) st.push_back(nd.child[q]);
             int32_t* o = &nb4[(size_t)4 * id];
             if (nd.lev == 0) {
                 for (int s = 0; s < 4; ++s) {
                     int i = nd.pi + d[s][0], j = nd.pj + d[s][1];
                     o[s] = wrap(0, i, j) ? root_[(size_t)j * np0[0] + i] : -2;
                 }
-                return;
+                continue;
             }
             const Node& pa = node_[nd.parent];
             const int32_t* pn = &nb4[(size_t)4 * nd.parent];
@@ -364,7 +375,8 @@ void PatchTree::face_neighbours_roots(const std::vector<int32_t>& roots, std::ve
             o[1] = a == 0 ? pa.child[1 + 2 * b] : across(1, 0 + 2 * b);
             o[2] = b == 1 ? pa.child[a] : across(2, a + 2);
             o[3] = b == 0 ? pa.child[a + 2] : across(3, a);
-        });
+        }
+    }
 }
 
 std::vector<int32_t> PatchTree::canonical_sorted() const {

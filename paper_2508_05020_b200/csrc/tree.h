@@ -217,11 +217,17 @@ struct PatchTree {
     // the same walk over the roots with root_ok(root slot) only (a rank's own roots: O(local))
     template <class Keep, class RootOk>
     void leaves_morton_roots(std::vector<std::vector<int32_t>>& per_level, Keep keep, RootOk root_ok) const {
-        per_level.assign(levels, {});
-        std::vector<int32_t>& st = dfs_;
+        leaves_morton_span(0, root_morton_.size(), per_level, keep, root_ok, dfs_);
+    }
+    // the same walk over the roots root_morton()[r0, r1) with a caller-owned stack (parts of a parallel plan)
+    template <class Keep, class RootOk>
+    void leaves_morton_span(size_t r0, size_t r1, std::vector<std::vector<int32_t>>& per_level, Keep keep,
+                            RootOk root_ok, std::vector<int32_t>& st) const {
+        per_level.resize(levels);
+        for (auto& v : per_level) v.clear();
         st.clear();
-        for (auto it = root_morton_.rbegin(); it != root_morton_.rend(); ++it)
-            if (root_ok(*it)) st.push_back(*it);
+        for (size_t r = r1; r-- > r0;)
+            if (root_ok(root_morton_[r])) st.push_back(root_morton_[r]);
         while (!st.empty()) {
             const int id = st.back();
             st.pop_back();
@@ -239,6 +245,9 @@ struct PatchTree {
     // the same table for the subtrees of the given roots only (row-major root indices; each subtree pre-order, a patch
     // needs only its parent's entries); nb4 is sized once to the capacity
     void face_neighbours_roots(const std::vector<int32_t>& roots, std::vector<int32_t>& nb4) const;
+    // the same for roots[0, nr) with a caller-owned stack, into an nb4 already sized to 4 x capacity (parts of a
+    // parallel plan: a patch's entries depend only on its parent's, so root subtrees are independent)
+    void face_neighbours_span(const int32_t* roots, size_t nr, std::vector<int32_t>& nb4, std::vector<int32_t>& st) const;
 
     // Transactions (regrid is atomic): between begin_txn() and commit()/rollback() every modified slot
     // is journaled once with its prior state, so a failed regrid is undone in O(changes) -- no copy of the
