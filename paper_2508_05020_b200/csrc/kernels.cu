@@ -2497,8 +2497,17 @@ __global__ void __launch_bounds__(kPostThreads) post_stage_kernel(const PostArgs
         lam = warp_max_u64(lam);
         if ((threadIdx.x & 31) == 0 && lam) atomicMax(p.a.lambda_bits, lam);
     }
+    // the restriction of the finest level present shares the reflux phase: its children are leaves with nothing
+    // finer, which the reflux never touches, and it writes covered patches, which the reflux never reads (disjoint
+    // data: the result is bitwise the phase-by-phase one; one grid barrier and one dependent round trip fewer)
+    int lf = p.levels - 1;
+    while (lf >= 1 && p.nrl[lf] == 0) --lf;
+    if (lf >= 1) {
+        const long long w = (long long)p.nrl[lf] * n * n;
+        for (long long t = tid; t < w; t += nthr) restrict_cell(p.rl[lf], t, p.a);
+    }
     grid.sync();
-    for (int l = p.levels - 1; l >= 1; --l) {
+    for (int l = lf - 1; l >= 1; --l) {
         if (p.nrl[l] == 0) continue;
         const long long w = (long long)p.nrl[l] * n * n;
         for (long long t = tid; t < w; t += nthr) restrict_cell(p.rl[l], t, p.a);
