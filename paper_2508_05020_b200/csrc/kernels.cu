@@ -2396,11 +2396,17 @@ __device__ __forceinline__ void restrict_cell(const RestrictTask* __restrict__ t
     const int fi = 2 * i - ca * n, fj = 2 * j - cb * n;
     const double* f = a.U + (size_t)rt.child[ca + 2 * cb] * 4 * nn + (size_t)fj * n + fi;   // children (read)
     double* dst = a.Uw + (size_t)rt.parent * 4 * nn + e;
+    // every child value loaded before the first store (the stores may alias the loads as far as the compiler knows,
+    // so a load-store sequence per component would be four dependent round trips); fi even: 16-byte pairs
+    double2 v[4][2];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const double* fk = f + k * nn;
-        dst[k * nn] = ((fk[0] + fk[1]) + (fk[n] + fk[n + 1])) * 0.25;
+        v[k][0] = *reinterpret_cast<const double2*>(fk);
+        v[k][1] = *reinterpret_cast<const double2*>(fk + n);
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[k * nn] = ((v[k][0].x + v[k][0].y) + (v[k][1].x + v[k][1].y)) * 0.25;
 }
 
 __global__ void restrict_kernel(const RestrictTask* __restrict__ tasks, int ntasks, const AuxArgs a) {
