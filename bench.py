@@ -55,8 +55,8 @@ def fp64_peak():
 
 def fp64_work(kernel, n=None):
     """fp64 SASS work per leaf cell-stage of a stage kernel (kernel "weno5_char" / "central4" at patch size n, whose
-    launch configuration differs), counted by ncu on the current kernels (profiles/r2g_fp64_work.json, scripts/profile_round.sh)."""
-    p = os.path.join(ROOT, "profiles", "r2g_fp64_work.json")
+    launch configuration differs), counted by ncu on the current kernels (profiles/r2i_fp64_work.json, scripts/profile_round.sh)."""
+    p = os.path.join(ROOT, "profiles", "r2i_fp64_work.json")
     d = json.load(open(p)) if os.path.exists(p) else {}
     nan = {"fp64_thread_inst_per_cell_stage": float("nan"), "flops_per_cell_stage": float("nan")}
     if n is not None and f"{kernel}_n{min(n, 32)}" in d:
@@ -552,7 +552,7 @@ def main():
     if not args.no_sweep_table and X.world == 1:
         extra["sweep_table"] = {"workload": "BASELINE configs[4]: stage kernel per total size and patch size (Central4 at "
                                             "4096^2..16384^2; WENO5 char / comp at 4096^2; fp64_issue_frac from each "
-                                            "WENO5-char kernel's own SASS fp64 count, profiles/r2g_fp64_work.json)",
+                                            "WENO5-char kernel's own SASS fp64 count, profiles/r2i_fp64_work.json)",
                                 "rows": measure_sweep_table(X, args, hbm_peak)}
     if "sweep_table" in extra:   # the largest single-GPU configs[4] row beside the 4096^2-per-GPU headline
         big = [r for r in extra["sweep_table"]["rows"] if r["N"] == 16384 and r["n"] == args.n and r["scheme"] == args.scheme]
