@@ -821,9 +821,11 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     order.erase(std::unique(order.begin(), order.end()), order.end());
     nt.begin_txn();
     std::string m;
+    int n_rq_ref = 0, n_rq_crs = 0, n_crs_done = 0;   // (AMR_REGRID_PROF: request statistics)
     for (const auto& o : order) {
         const int id = o.second;
         if (!ref[id] || !nt.is_leaf(id) || nt.lev[id] >= c->cfg.num_levels - 1) continue;
+        ++n_rq_ref;
         if (!nt.refine(id, m)) {
             nt.rollback();
             amr_status s = m.find("capacity") != std::string::npos ? AMR_E_CAPACITY : AMR_E_MESH;
@@ -834,9 +836,13 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
         for (const auto& o : order) {
             const int id = o.second;
             if (nt.lev[id] != l || !crs[id] || !nt.alive[id]) continue;
-            if (nt.coarsen_allowed(id)) nt.delete_children(id);
+            ++n_rq_crs;
+            if (nt.coarsen_allowed(id)) { nt.delete_children(id); ++n_crs_done; }
         }
     clk.mark("refine + coarsen");
+    if (clk.on)
+        std::fprintf(stderr, "  [regrid] requests %zu: refine %d, coarsen %d (%d done), patches %d\n", order.size(),
+                     n_rq_ref, n_rq_crs, n_crs_done, nt.n_alive);
     if (!nt.validate_txn(m)) {   // O(changes); amr_plan_regrid checks it against the full validate()
         nt.rollback();
         return fail(c, AMR_E_MESH, "regrid produced an invalid mesh: " + m);

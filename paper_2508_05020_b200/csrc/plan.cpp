@@ -214,7 +214,7 @@ bool plan_descriptors(const PatchTree& t, const std::vector<int32_t>& nb4, const
     HostPool& pool = HostPool::get();
     const size_t nl = leaf_ids.size();
     // parts of at least ~1k leaves (a part's fixed cost is a few vector clears and the merge offsets)
-    const int parts = (int)std::max<size_t>(1, std::min<size_t>(4 * (size_t)pool.threads(), nl / 1024));
+    const int parts = pool.active() ? (int)std::max<size_t>(1, std::min<size_t>(4 * (size_t)pool.threads(), nl / 1024)) : 1;
     if (parts == 1) return describe_part(t, nb4, leaf_ids, 0, nl, owner, world, rank, halo_mode, out, err);
     static thread_local std::vector<DescOut> part_out;
     static thread_local std::vector<std::string> part_err;

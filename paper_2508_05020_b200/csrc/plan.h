@@ -27,6 +27,8 @@ class HostPool {
   public:
     static HostPool& get();
     int threads() const { return nworkers_ + 1; }
+    // whether run() would use the workers (armed, with workers): parts are only worth splitting then
+    bool active() const { return nworkers_ > 0 && !serial_ && armed_.load(std::memory_order_relaxed) > 0; }
     void arm();
     void disarm();
     template <class F>
@@ -98,7 +100,7 @@ template <class RootOk>
 void plan_leaf_order(const PatchTree& t, RootOk root_ok, std::vector<int32_t>& leaf_ids) {
     HostPool& pool = HostPool::get();
     const std::vector<int32_t>& rm = t.root_morton();
-    const int parts = std::max(1, std::min<int>(16 * pool.threads(), (int)rm.size()));   // (refinement is clustered)
+    const int parts = pool.active() ? std::max(1, std::min<int>(16 * pool.threads(), (int)rm.size())) : 1;   // (refinement is clustered)
     // per-part, per-level scratch kept across plans (thread_local: loopback virtual ranks plan concurrently)
     static thread_local std::vector<std::vector<std::vector<int32_t>>> per;
     static thread_local std::vector<std::vector<int32_t>> stacks;

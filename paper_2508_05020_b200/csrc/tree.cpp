@@ -204,11 +204,20 @@ bool PatchTree::coarsen_allowed(int id) const {
         }
         return true;
     }
-    for (int c = 0; c < 4; ++c) {
-        int k = child[4 * id + c];
-        for (int d = 0; d < 8; ++d) {
-            int q = neighbour(k, kMoore[d][0], kMoore[d][1]);
-            if (q >= 0 && parent[q] != id && has_children(q)) return false;
+    // R2-exact rule: no Moore neighbour q of a child (same level, parent[q] != id) may have children.  Those q are the
+    // 12 level-(l+1) cells around the 2 x 2 block: the children of id's 8 Moore neighbours that touch it, so they are
+    // found from 8 neighbour() calls at level l instead of 20 at level l+1 (each of which recursed to level l anyway)
+    for (int d = 0; d < 8; ++d) {
+        const int DX = kMoore[d][0], DY = kMoore[d][1];
+        const int pn = neighbour(id, DX, DY);
+        if (pn < 0 || pn == id || node_[pn].child[0] < 0) continue;   // (pn == id: periodic self-wrap, q are siblings)
+        const Node& p = node_[pn];
+        for (int qb = 0; qb < 2; ++qb) {
+            if ((DY == 1 && qb != 0) || (DY == -1 && qb != 1)) continue;   // the row of pn's children facing id
+            for (int qa = 0; qa < 2; ++qa) {
+                if ((DX == 1 && qa != 0) || (DX == -1 && qa != 1)) continue;
+                if (has_children(p.child[qa + 2 * qb])) return false;
+            }
         }
     }
     return true;
