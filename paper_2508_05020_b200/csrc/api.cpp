@@ -269,8 +269,24 @@ amr_status build_plan(amr_ctx* c) {
     clk.mark("plan: sib + restriction");
 
     // face neighbours of the local patches and of those they read across the boundary, from the parents' entries
-    // (subtree pre-order, no recursion; independent root subtrees in parts): nb4[4 id + s]
-    plan_face_neighbours(t, nb_roots, c->nb4);
+    // (subtree pre-order, no recursion): nb4[4 id + s]; after a regrid on one rank only the created / deleted slots
+    // and their neighbours are updated (O(changes))
+    if (c->comm.world == 1 && c->nb4_incr && c->nb4_full) {
+        update_face_neighbours(t, c->nb4_created, c->nb4_deleted, c->nb4);
+        static const bool check = getenv("AMR_CHECK_NB4") != nullptr;   // (tests: against the full table)
+        if (check) {
+            std::vector<int32_t> full;
+            plan_face_neighbours(t, nb_roots, full);
+            for (int id : c->canon_valid ? c->canon : t.canonical())
+                for (int s = 0; s < 4; ++s)
+                    if (full[(size_t)4 * id + s] != c->nb4[(size_t)4 * id + s])
+                        return fail(c, AMR_E_STATE, "incremental face-neighbour table differs from the full one");
+        }
+    } else {
+        plan_face_neighbours(t, nb_roots, c->nb4);
+        c->nb4_full = c->comm.world == 1;
+    }
+    c->nb4_incr = false;
     clk.mark("plan: face neighbours");
     {   // leaf descriptors, proxy strips (numbered in leaf order) and reflux tasks, in parts of the leaf order
         static thread_local DescOut dout;
@@ -857,6 +873,13 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
         if (!nt.alive[sn.id] && sn.alive) ++n_del;
     }
     std::sort(new_ids.begin(), new_ids.end());
+    // created / deleted slots for the incremental face-neighbour table (created in level order)
+    c->nb4_created = new_ids;
+    std::stable_sort(c->nb4_created.begin(), c->nb4_created.end(), [&](int a, int b) { return nt.lev[a] < nt.lev[b]; });
+    c->nb4_deleted.clear();
+    for (const auto& sn : nt.journal())
+        if (!nt.alive[sn.id] && sn.alive) c->nb4_deleted.push_back(sn.id);
+    c->nb4_incr = W == 1;
     nt.commit();
     // ownership of the new tree under the OLD partition (roots never change): the old owner of a
     // root prolongs the new patches of that root, since it holds their parents' data

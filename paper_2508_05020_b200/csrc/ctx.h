@@ -142,6 +142,9 @@ struct amr_ctx {
     bool ghost_valid = false;      // proxies hold the ghost strips of U^n under the current plan (post-stage fill)
     double sim_time_fix = 0.0;     // host correction of the device time sum (rolled-back steps)
     std::vector<int32_t> nb4;      // face neighbours W, E, S, N of every slot (PatchTree::face_neighbours)
+    bool nb4_full = false;         // nb4 holds every active patch's entries (one rank, since the last full build)
+    bool nb4_incr = false;         // the next build_plan may update nb4 from the regrid's created / deleted slots
+    std::vector<int32_t> nb4_created, nb4_deleted;
     bool canon_valid = false;      // canon / canon_pos match the tree (ensure_canon)
     double last_dt = 0.0;
 

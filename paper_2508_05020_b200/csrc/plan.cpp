@@ -118,6 +118,22 @@ void plan_face_neighbours(const PatchTree& t, const std::vector<int32_t>& roots,
     });
 }
 
+void update_face_neighbours(const PatchTree& t, const std::vector<int32_t>& created, const std::vector<int32_t>& deleted,
+                            std::vector<int32_t>& nb4) {
+    for (int d : deleted)
+        for (int s = 0; s < 4; ++s) {
+            const int q = nb4[(size_t)4 * d + s];   // (the deleted slot's entries are those of the previous tree)
+            if (q >= 0 && t.alive[q] && nb4[(size_t)4 * q + (s ^ 1)] == d) nb4[(size_t)4 * q + (s ^ 1)] = -1;
+        }
+    for (int id : created) {
+        t.face_neighbours_one(id, nb4);
+        for (int s = 0; s < 4; ++s) {
+            const int q = nb4[(size_t)4 * id + s];
+            if (q >= 0) nb4[(size_t)4 * q + (s ^ 1)] = id;
+        }
+    }
+}
+
 namespace {
 // The descriptors of leaf_ids[e0, e1): proxies and reflux tasks numbered from 0 within the part (the merge shifts
 // them); the first inconsistency sets err and stops the part.

@@ -83,6 +83,12 @@ template <class RootOk>
 void plan_leaf_order(const PatchTree& t, RootOk root_ok, std::vector<int32_t>& leaf_ids);
 // nb4 of the subtrees of `roots` (PatchTree::face_neighbours_roots)
 void plan_face_neighbours(const PatchTree& t, const std::vector<int32_t>& roots, std::vector<int32_t>& nb4);
+// nb4 after a regrid, in O(changes) (one rank, the previous table complete): the same-level neighbours of every
+// deleted slot lose it (-1, missing), then every created patch -- in level order, so that its parent's entries are
+// final -- gets its entries from its parent's and its neighbours point back to it.  Equal to plan_face_neighbours
+// over all roots on every active patch (AMR_CHECK_NB4=1 compares them in build_plan).
+void update_face_neighbours(const PatchTree& t, const std::vector<int32_t>& created, const std::vector<int32_t>& deleted,
+                            std::vector<int32_t>& nb4);
 
 // Leaf descriptors (LeafDesc), proxy-strip tasks (ProxyTask, numbered in leaf order) and reflux tasks of the leaves
 // in leaf_ids order, from the face-neighbour table nb4.  halo_mode 2 with world > 1 marks remote face neighbours

@@ -354,7 +354,6 @@ void PatchTree::face_neighbours_roots(const std::vector<int32_t>& roots, std::ve
 
 void PatchTree::face_neighbours_span(const int32_t* roots, size_t nr, std::vector<int32_t>& nb4,
                                      std::vector<int32_t>& st) const {
-    static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
     for (size_t k = 0; k < nr; ++k) {
         st.clear();
         st.push_back(root_[(size_t)roots[k]]);
@@ -364,28 +363,34 @@ void PatchTree::face_neighbours_span(const int32_t* roots, size_t nr, std::vecto
             const Node& nd = node_[id];
             if (nd.child[0] >= 0)
                 for (int q = 3; q >= 0; --q) st.push_back(nd.child[q]);
-            int32_t* o = &nb4[(size_t)4 * id];
-            if (nd.lev == 0) {
-                for (int s = 0; s < 4; ++s) {
-                    int i = nd.pi + d[s][0], j = nd.pj + d[s][1];
-                    o[s] = wrap(0, i, j) ? root_[(size_t)j * np0[0] + i] : -2;
-                }
-                continue;
-            }
-            const Node& pa = node_[nd.parent];
-            const int32_t* pn = &nb4[(size_t)4 * nd.parent];
-            const int a = nd.pi & 1, b = nd.pj & 1;
-            auto across = [&](int side, int cidx) {
-                const int q = pn[side];
-                if (q < 0) return q;
-                return node_[q].child[0] < 0 ? -1 : node_[q].child[cidx];
-            };
-            o[0] = a == 1 ? pa.child[0 + 2 * b] : across(0, 1 + 2 * b);
-            o[1] = a == 0 ? pa.child[1 + 2 * b] : across(1, 0 + 2 * b);
-            o[2] = b == 1 ? pa.child[a] : across(2, a + 2);
-            o[3] = b == 0 ? pa.child[a + 2] : across(3, a);
+            face_neighbours_one(id, nb4);
         }
     }
+}
+
+void PatchTree::face_neighbours_one(int id, std::vector<int32_t>& nb4) const {
+    static const int d[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};   // W, E, S, N
+    const Node& nd = node_[id];
+    int32_t* o = &nb4[(size_t)4 * id];
+    if (nd.lev == 0) {
+        for (int s = 0; s < 4; ++s) {
+            int i = nd.pi + d[s][0], j = nd.pj + d[s][1];
+            o[s] = wrap(0, i, j) ? root_[(size_t)j * np0[0] + i] : -2;
+        }
+        return;
+    }
+    const Node& pa = node_[nd.parent];
+    const int32_t* pn = &nb4[(size_t)4 * nd.parent];
+    const int a = nd.pi & 1, b = nd.pj & 1;
+    auto across = [&](int side, int cidx) {
+        const int q = pn[side];
+        if (q < 0) return q;
+        return node_[q].child[0] < 0 ? -1 : node_[q].child[cidx];
+    };
+    o[0] = a == 1 ? pa.child[0 + 2 * b] : across(0, 1 + 2 * b);
+    o[1] = a == 0 ? pa.child[1 + 2 * b] : across(1, 0 + 2 * b);
+    o[2] = b == 1 ? pa.child[a] : across(2, a + 2);
+    o[3] = b == 0 ? pa.child[a + 2] : across(3, a);
 }
 
 std::vector<int32_t> PatchTree::canonical_sorted() const {

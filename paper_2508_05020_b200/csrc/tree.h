@@ -248,6 +248,8 @@ struct PatchTree {
     // the same for roots[0, nr) with a caller-owned stack, into an nb4 already sized to 4 x capacity (parts of a
     // parallel plan: a patch's entries depend only on its parent's, so root subtrees are independent)
     void face_neighbours_span(const int32_t* roots, size_t nr, std::vector<int32_t>& nb4, std::vector<int32_t>& st) const;
+    // the entries of one patch from its parent's (level 0: the root table); nb4 sized to 4 x capacity
+    void face_neighbours_one(int id, std::vector<int32_t>& nb4) const;
 
     // Transactions (regrid is atomic): between begin_txn() and commit()/rollback() every modified slot
     // is journaled once with its prior state, so a failed regrid is undone in O(changes) -- no copy of the
