@@ -246,7 +246,44 @@ amr_status build_plan(amr_ctx* c) {
     // leaves in launch order: level, then Morton order of (i, j) for L2 locality of halos (a depth-first walk
     // from this rank's roots in Morton order, in parts over root ranges merged level by level -- plan.h; the planning
     // API checks it against the sort of (level, Morton) keys)
-    plan_leaf_order(t, [&](int root) { return c->comm.owns(c, root); }, c->leaf_ids);
+    static const bool check_incr = getenv("AMR_CHECK_INCR") != nullptr;   // (tests: incremental tables vs full ones)
+    if (c->comm.world == 1 && c->nb4_incr && c->lo_full) {
+        // one rank after a regrid: per level, drop the leaves it removed and merge in the ones it added (by key)
+        if ((int)c->lo_mark.size() != t.capacity) c->lo_mark.assign(t.capacity, 0);
+        for (const auto& r : c->lo_rm) c->lo_mark[r.second.second] = 1;
+        std::sort(c->lo_add.begin(), c->lo_add.end());
+        std::vector<std::pair<uint64_t, int32_t>> merged;
+        size_t ia = 0;
+        for (int l = 0; l < L; ++l) {
+            auto& lst = c->lo_lvl[l];
+            merged.clear();
+            merged.reserve(lst.size() + 16);
+            for (const auto& e : lst) {
+                if (c->lo_mark[e.second]) continue;
+                while (ia < c->lo_add.size() && c->lo_add[ia].first == l && c->lo_add[ia].second.first < e.first)
+                    merged.push_back(c->lo_add[ia++].second);
+                merged.push_back(e);
+            }
+            while (ia < c->lo_add.size() && c->lo_add[ia].first == l) merged.push_back(c->lo_add[ia++].second);
+            lst.swap(merged);
+        }
+        for (const auto& r : c->lo_rm) c->lo_mark[r.second.second] = 0;
+        c->leaf_ids.clear();
+        for (int l = 0; l < L; ++l)
+            for (const auto& e : c->lo_lvl[l]) c->leaf_ids.push_back(e.second);
+        if (check_incr) {
+            std::vector<int32_t> full;
+            plan_leaf_order(t, [&](int root) { return c->comm.owns(c, root); }, full);
+            if (full != c->leaf_ids) return fail(c, AMR_E_STATE, "incremental leaf order differs from the full walk");
+        }
+    } else {
+        plan_leaf_order(t, [&](int root) { return c->comm.owns(c, root); }, c->leaf_ids);
+        c->lo_full = c->comm.world == 1;
+        if (c->lo_full) {
+            c->lo_lvl.assign(L, {});
+            for (int id : c->leaf_ids) c->lo_lvl[t.lev[id]].push_back({morton((uint32_t)t.pi[id], (uint32_t)t.pj[id]), id});
+        }
+    }
     for (size_t e = 0; e < c->leaf_ids.size(); ++e) c->leaf_pos[c->leaf_ids[e]] = (int)e;
     clk.mark("plan: leaf order");
     // owned parents whose 4 children are leaves: the coarsening candidates of a12; owned covered patches: the
@@ -273,8 +310,7 @@ amr_status build_plan(amr_ctx* c) {
     // and their neighbours are updated (O(changes))
     if (c->comm.world == 1 && c->nb4_incr && c->nb4_full) {
         update_face_neighbours(t, c->nb4_created, c->nb4_deleted, c->nb4);
-        static const bool check = getenv("AMR_CHECK_NB4") != nullptr;   // (tests: against the full table)
-        if (check) {
+        if (check_incr) {
             std::vector<int32_t> full;
             plan_face_neighbours(t, nb_roots, full);
             for (int id : c->canon_valid ? c->canon : t.canonical())
@@ -877,8 +913,17 @@ amr_status apply_regrid(amr_ctx* c, const std::vector<uint8_t>& ref, const std::
     c->nb4_created = new_ids;
     std::stable_sort(c->nb4_created.begin(), c->nb4_created.end(), [&](int a, int b) { return nt.lev[a] < nt.lev[b]; });
     c->nb4_deleted.clear();
-    for (const auto& sn : nt.journal())
+    c->lo_rm.clear();
+    c->lo_add.clear();
+    for (const auto& sn : nt.journal()) {
         if (!nt.alive[sn.id] && sn.alive) c->nb4_deleted.push_back(sn.id);
+        // leaves removed (refined or deleted) / added (created leaves, coarsened parents): every change of a slot's
+        // leaf status is journaled (refine, alloc, release and delete_children touch the slot)
+        const bool was = sn.alive && sn.child[0] < 0, now = nt.is_leaf(sn.id);
+        if (was && !now) c->lo_rm.push_back({sn.lev, {morton((uint32_t)sn.pi, (uint32_t)sn.pj), sn.id}});
+        if (now && !was)
+            c->lo_add.push_back({nt.lev[sn.id], {morton((uint32_t)nt.pi[sn.id], (uint32_t)nt.pj[sn.id]), sn.id}});
+    }
     c->nb4_incr = W == 1;
     nt.commit();
     // ownership of the new tree under the OLD partition (roots never change): the old owner of a

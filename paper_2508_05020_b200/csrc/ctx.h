@@ -145,6 +145,13 @@ struct amr_ctx {
     bool nb4_full = false;         // nb4 holds every active patch's entries (one rank, since the last full build)
     bool nb4_incr = false;         // the next build_plan may update nb4 from the regrid's created / deleted slots
     std::vector<int32_t> nb4_created, nb4_deleted;
+    // the leaf launch order kept per level as (Morton key of (i, j), slot), sorted -- the depth-first order from the
+    // roots in Morton order (one rank) -- and updated at a regrid from the leaves it removed / added (O(leaves) merge
+    // instead of a tree walk)
+    std::vector<std::vector<std::pair<uint64_t, int32_t>>> lo_lvl;
+    bool lo_full = false;
+    std::vector<std::pair<int32_t, std::pair<uint64_t, int32_t>>> lo_rm, lo_add;   // (level, (key, slot))
+    std::vector<uint8_t> lo_mark;
     bool canon_valid = false;      // canon / canon_pos match the tree (ensure_canon)
     double last_dt = 0.0;
 

@@ -86,7 +86,7 @@ void plan_face_neighbours(const PatchTree& t, const std::vector<int32_t>& roots,
 // nb4 after a regrid, in O(changes) (one rank, the previous table complete): the same-level neighbours of every
 // deleted slot lose it (-1, missing), then every created patch -- in level order, so that its parent's entries are
 // final -- gets its entries from its parent's and its neighbours point back to it.  Equal to plan_face_neighbours
-// over all roots on every active patch (AMR_CHECK_NB4=1 compares them in build_plan).
+// over all roots on every active patch (AMR_CHECK_INCR=1 compares them in build_plan).
 void update_face_neighbours(const PatchTree& t, const std::vector<int32_t>& created, const std::vector<int32_t>& deleted,
                             std::vector<int32_t>& nb4);
 
