@@ -822,8 +822,10 @@ amr_status flag_requests(amr_ctx* c, std::vector<uint8_t>& ref, std::vector<uint
     double* Un = c->U[c->un];
     amr_status s = c->comm.exchange_halos(c, Un);   // the indicator reads neighbours (remote ones on N > 1)
     if (s != AMR_OK) return s;
-    s = fill_ghosts(c, Un);
-    if (s != AMR_OK) return s;
+    if (!c->ghost_valid) {   // (the last step's post-stage kernel already filled U^n's strips: ghost_valid)
+        s = fill_ghosts(c, Un);
+        if (s != AMR_OK) return s;
+    }
     AuxArgs a = aux(c, Un, nullptr);
     const int nl = (int)c->leaves.size(), ns = (int)c->sib.size() / 5;
     LAUNCH(launch_flags(c->d_leaves.p, nl, a, c->d_maxeta.p, c->d_amb.p, c->stream), "flags");
