@@ -221,6 +221,85 @@ bool nccl_windows(const amr_ctx* c) {
     return c->cfg.peer_map == 1 && c->cfg.world_size > 1 && c->cfg.comm_backend == 0 && c->cfg.halo_mode >= 1;
 }
 
+// AMR_CHECK_PLAN=1 (tests; compute-sanitizer is closed on this GPU pool): every index a kernel dereferences through
+// the plan's descriptors is checked against the tree and the buffer extents before the upload -- leaf slots alive
+// leaves below the slot capacity, same-level side sources alive patches of the leaf's level at the face position,
+// proxy numbers inside the proxy list, C/F parents' 3 x 3 sources alive level-(l-1) patches or -1, reflux fine
+// slots alive level-(l+1) leaves, restriction parents / children alive with the parent-child links, sibling groups'
+// leaf positions inside the leaf list and the children of their parent.  The kernels' addressing inside a patch is
+// fixed by n and the tile shape; with these checks every global address they form is inside the pools.
+bool plan_checks_on() {
+    static const bool on = getenv("AMR_CHECK_PLAN") != nullptr;
+    return on;
+}
+amr_status validate_plan(amr_ctx* c) {
+    const PatchTree& t = c->tree;
+    const int cap = t.capacity, L = c->cfg.num_levels;
+    auto live = [&](int id) { return id >= 0 && id < cap && t.alive[id]; };
+    auto bad = [&](const std::string& m) { return fail(c, AMR_E_STATE, "plan check: " + m); };
+    static const int dx[4] = {-1, 1, 0, 0}, dy[4] = {0, 0, -1, 1};
+    const int np = (int)c->ptasks.size();
+    auto check_leaf = [&](const LeafDesc& d, bool covered_ok) -> bool {
+        if (!live(d.slot) || d.level != t.lev[d.slot]) return false;
+        if (!covered_ok && !t.is_leaf(d.slot)) return false;
+        for (int s = 0; s < 4; ++s) {
+            const int v = d.side[s];
+            if (v >= 0) {
+                if (!live(v) || t.lev[v] != d.level) return false;
+                int i = t.pi[d.slot] + dx[s], j = t.pj[d.slot] + dy[s];
+                if (!t.wrap(d.level, i, j) || t.pi[v] != i || t.pj[v] != j) return false;
+            } else if (-1 - v >= np) {
+                return false;
+            }
+        }
+        return true;
+    };
+    for (const LeafDesc& d : c->leaves)
+        if (!check_leaf(d, false)) return bad("leaf descriptor of slot " + std::to_string(d.slot));
+    for (const LeafDesc& d : c->gleaves)
+        if (!check_leaf(d, false)) return bad("block-tile member of slot " + std::to_string(d.slot));
+    for (const LeafDesc& d : c->singles)
+        if (!check_leaf(d, false)) return bad("single leaf of slot " + std::to_string(d.slot));
+    for (int k = 0; k < np; ++k) {
+        const ProxyTask& p = c->ptasks[k];
+        if (p.proxy != k || !live(p.slot) || p.side < 0 || p.side > 3 || p.level != t.lev[p.slot])
+            return bad("proxy task " + std::to_string(k));
+        for (int q = 0; q < 9; ++q) {
+            const int v = p.coarse[q];
+            if (p.kind == 0 ? v != -1 : !(v == -1 || (live(v) && t.lev[v] == p.level - 1)))
+                return bad("coarse source of proxy " + std::to_string(k));
+        }
+        if (p.kind == 1 && p.coarse[4] != t.parent[p.slot]) return bad("proxy parent " + std::to_string(k));
+    }
+    for (const RefluxTask& r : c->rtasks) {
+        if (r.leaf < 0 || r.leaf >= (int)c->leaves.size() || c->leaves[r.leaf].slot != r.slot || !live(r.slot))
+            return bad("reflux task of slot " + std::to_string(r.slot));
+        for (int s = 0; s < 4; ++s)
+            if (r.mask & (1 << s))
+                for (int h = 0; h < 2; ++h)
+                    if (!live(r.fine[s][h]) || !t.is_leaf(r.fine[s][h]) || t.lev[r.fine[s][h]] != r.level + 1)
+                        return bad("reflux fine slot of " + std::to_string(r.slot));
+    }
+    for (int l = 1; l < L && l < (int)c->rlev.size(); ++l)
+        for (const RestrictTask& r : c->rlev[l]) {
+            if (!live(r.parent) || t.lev[r.parent] != l - 1) return bad("restriction parent");
+            for (int q = 0; q < 4; ++q)
+                if (!live(r.child[q]) || t.parent[r.child[q]] != r.parent || t.child[4 * r.parent + q] != r.child[q])
+                    return bad("restriction child");
+        }
+    const int nl = (int)c->leaves.size();
+    for (size_t g = 0; g + 4 < c->sib.size(); g += 5) {
+        const int par = c->sib[g];
+        if (!live(par)) return bad("sibling group parent");
+        for (int q = 0; q < 4; ++q) {
+            const int e = c->sib[g + 1 + q];
+            if (e < 0 || e >= nl || c->leaves[e].slot != t.child[4 * par + q]) return bad("sibling group leaf position");
+        }
+    }
+    if ((int64_t)c->proxy.cap < (int64_t)std::max(1, np) * (int64_t)c->PS) return bad("proxy buffer smaller than the proxy list");
+    return AMR_OK;
+}
+
 amr_status build_plan(amr_ctx* c) {
     NvtxRange nv("build_plan");
     PhaseClock clk;
@@ -465,6 +544,7 @@ amr_status build_plan(amr_ctx* c) {
     c->plan_version++;
     c->plan_steps = 0;
     c->comm.replan(t);
+    if (plan_checks_on()) return validate_plan(c);
     return AMR_OK;
 }
 
