@@ -2390,12 +2390,13 @@ __device__ __forceinline__ void restrict_cell(const RestrictTask* __restrict__ t
     const int n = a.geo.n;
     const size_t nn = (size_t)n * n;
     const int task = (int)(t / (long long)nn), e = (int)(t - (long long)task * nn);
-    const RestrictTask rt = tasks[task];
     const int i = e % n, j = e / n;
     const int ca = (2 * i) / n, cb = (2 * j) / n;
     const int fi = 2 * i - ca * n, fj = 2 * j - cb * n;
-    const double* f = a.U + (size_t)rt.child[ca + 2 * cb] * 4 * nn + (size_t)fj * n + fi;   // children (read)
-    double* dst = a.Uw + (size_t)rt.parent * 4 * nn + e;
+    // the two fields this cell needs, loaded directly (a copy of the task indexed by ca + 2 cb went through local memory)
+    const int child = tasks[task].child[ca + 2 * cb], parent = tasks[task].parent;
+    const double* f = a.U + (size_t)child * 4 * nn + (size_t)fj * n + fi;   // children (read)
+    double* dst = a.Uw + (size_t)parent * 4 * nn + e;
     // every child value loaded before the first store (the stores may alias the loads as far as the compiler knows,
     // so a load-store sequence per component would be four dependent round trips); fi even: 16-byte pairs
     double2 v[4][2];
