@@ -2443,7 +2443,8 @@ __device__ __forceinline__ void reflux_cell(const RefluxTask* __restrict__ tasks
         act = ok ? touch & tasks[task].mask : 0;
     }
     if (act) {
-        const RefluxTask rt = tasks[task];
+        // the task's fields read where needed (a copy of the task indexed by side / half went through local memory)
+        const RefluxTask& rt = tasks[task];
         const double coef = a.b * (*a.dt);
         double* U = a.Uw + (size_t)rt.slot * 4 * nn + (size_t)j * n + i;
         double u[4];
