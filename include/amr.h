@@ -117,8 +117,8 @@ typedef struct {
                                      exchange is a stream-ordered cross-rank fence (a one-word NCCL allreduce, or
                                      CUDA events between loopback streams) followed by ONE kernel that loads the
                                      needed slots from the owners' pools over NVLink into the local pool;
-                                     2 (Central4 TMA kernel: central4, patch_cells >= 32, stage_kernel 0; or a WENO5
-                                     stage kernel, stage_kernel 0 / 1; <= 8 ranks) as 1, but the stage kernel itself
+                                     2 (stage_kernel 0 / 1; Central4 with patch_cells < 32 needs stage_kernel 1, the
+                                     per-tile kernel; <= 8 ranks; else AMR_E_CONFIG) as 1, but the stage kernel itself
                                      loads the 4-wide face strips of remote neighbours from the owners' pools (TMA /
                                      cp.async over NVLink), so before a stage only the coarse sources of C/F ghosts
                                      are pulled (the halo transfer overlaps the compute).  The halo lists of modes

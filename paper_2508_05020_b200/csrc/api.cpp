@@ -81,13 +81,15 @@ amr_status validate_config(const amr_config* cfg, std::string& m) {
     if (c.halo_mode < 0 || c.halo_mode > 2) { m = "halo_mode must be 0, 1 or 2"; return AMR_E_CONFIG; }
     if (c.peer_map < 0 || c.peer_map > 1) { m = "peer_map must be 0 or 1"; return AMR_E_CONFIG; }
     if (c.peer_map == 1 && c.pool) { m = "peer_map 1 allocates the pool with ncclMemAlloc: cfg.pool must be NULL"; return AMR_E_CONFIG; }
-    // halo_mode 2: the stage kernels that load remote face strips themselves -- the Central4 TMA kernel (n >= 32) and
-    // the WENO5 kernels (per-tile and n = 8 block tiles); <= 8 ranks (3-bit owner field of LeafDesc.pad)
+    // halo_mode 2: the stage kernels that load remote face strips themselves -- the Central4 TMA kernel (n >= 32,
+    // stage_kernel 0), the Central4 per-tile kernel (stage_kernel 1, every n; the n = 8 / 16 block-tile kernels of
+    // stage_kernel 0 take their block-edge strips by TMA from the local pool only) and the WENO5 kernels (per-tile and
+    // n = 8 block tiles); <= 8 ranks (3-bit owner field of LeafDesc.pad)
     if (c.halo_mode == 2 && c.world_size > 1 &&
-        (c.world_size > 8 ||
-         (c.scheme == AMR_CENTRAL4 ? (c.patch_cells < 32 || c.stage_kernel != 0) : (c.stage_kernel > 1)))) {
-        m = "halo_mode 2 needs the Central4 TMA kernel (central4, patch_cells >= 32, stage_kernel 0) or a WENO5 stage "
-            "kernel (stage_kernel 0 / 1), and <= 8 ranks";
+        (c.world_size > 8 || c.stage_kernel > 1 ||
+         (c.scheme == AMR_CENTRAL4 && c.patch_cells < 32 && c.stage_kernel != 1))) {
+        m = "halo_mode 2 needs stage_kernel 0 / 1 (Central4 with patch_cells < 32: stage_kernel 1, the per-tile "
+            "kernel), and <= 8 ranks";
         return AMR_E_CONFIG;
     }
     return AMR_OK;

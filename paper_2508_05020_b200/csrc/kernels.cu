@@ -657,7 +657,8 @@ __global__ void __launch_bounds__(C4Cfg<(N > 32 ? 32 : N)>::NT, C4Cfg<(N > 32 ? 
     const double* src[4];
 #pragma unroll
     for (int s = 0; s < 4; ++s)
-        src[s] = d.side[s] >= 0 ? a.Uin + (size_t)d.side[s] * PS : a.proxy + (size_t)(-1 - d.side[s]) * PS;
+        src[s] = d.side[s] >= 0 ? side_source(a, d, s) + (size_t)d.side[s] * PS   // halo_mode 2: maybe a peer's pool
+                                : a.proxy + (size_t)(-1 - d.side[s]) * PS;
 
     // ---- (a1) halo gather: one warp per (component, row); lanes move 16-byte chunks
     {

@@ -77,6 +77,7 @@ CASES = {
     "quadrant_amr_weno": (W.quadrant(N=64, n=16, levels=3, seed=2), 8, 4),
     "shock_bubble_reflective": (W.shock_bubble(Nx=128, Ny=64, n=16, levels=3), 8, 4),
     "shock_bubble_subcycled": (dict(W.shock_bubble(Nx=128, Ny=64, n=16, levels=3), subcycle=1), 4, 2),
+    "implosion_c4_amr_n16": (W.implosion(N=128, n=16, scheme="central4", levels=2), 6, 3),
     "implosion_c4_subcycled_n32": (W.implosion(N=256, n=32, scheme="central4", levels=3, subcycle=1), 4, 2),
 }
 
@@ -86,11 +87,13 @@ CASES = {
 @pytest.mark.parametrize("case", list(CASES))
 def test_virtual_ranks_bitwise_equal_single_rank(case, world, halo_mode):
     """halo_mode 0: pack + transport copy + unpack; 1: peer pull (NEXT #3) from the other ranks' mapped pools;
-    2: the stage kernel loads remote face strips from the owners' pools itself (Central4 TMA kernel, n >= 32; WENO5
-    per-tile and n = 8 block-tile kernels)."""
+    2: the stage kernel loads remote face strips from the owners' pools itself (Central4 TMA kernel, n >= 32, and
+    per-tile kernel, every n; WENO5 per-tile and n = 8 block-tile kernels)."""
     cfg, steps, regrid = CASES[case]
     if halo_mode == 2 and cfg["scheme"] == "central4" and cfg["n"] < 32:
-        pytest.skip("halo_mode 2: Central4 only through the TMA kernel (n >= 32); WENO5 kernels at every n")
+        # the n = 8 / 16 block-tile kernels read block-edge strips from the local pool only: halo_mode 2 runs Central4
+        # there on the per-tile kernel (stage_kernel 1), and so does the single-rank reference
+        cfg = dict(cfg, stage_kernel=1)
     ref_state, ref_keys, ref_dts = run_single(cfg, steps, regrid)
     res = run_multi(dict(cfg, halo_mode=halo_mode), world, steps, regrid)
     merged = {}
