@@ -132,7 +132,11 @@ typedef struct {
                                      allocated by the library with ncclMemAlloc (cfg.pool must be NULL), registered
                                      with ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC), and every peer's address
                                      is taken on the device from the window with ncclGetPeerPointer (NCCL's
-                                     load/store-accessible device API, nccl_device.h); ABI 5 */
+                                     load/store-accessible device API, nccl_device.h); with NCCL's device
+                                     communicator (ncclDevCommCreate, one LSA barrier) and every rank in one LSA
+                                     team, the stage fence is an ncclLsaBarrierSession kernel instead of the
+                                     one-word allreduce (ncclDevCommCreate failing -> AMR_E_COMM at amr_create);
+                                     ABI 5 */
 } amr_config;
 
 /* Patch metadata as in Fig. 2; links are tree indices, -1 = none

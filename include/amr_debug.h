@@ -54,8 +54,9 @@ amr_status amr_plan_build_check(amr_plan* p, int32_t world, int32_t rank, int32_
  * migration exchange call pattern), the four allreduce kinds (Lambda max-u64, max-f64, sum-f64 totals, max-i32
  * errors), the peer-table byte-sum allreduce and the one-word fence -- and checks the results (bytes received =
  * bytes sent; 1-rank reductions are the identity); then the symmetric-window mapping of peer_map 1 (ncclMemAlloc,
- * ncclCommWindowRegister, the device-side ncclGetPeerPointer, whose address must alias the buffer; msg ends in
- * "window ok").  Returns AMR_OK, AMR_E_COMM (message in msg, NUL-terminated,
+ * ncclCommWindowRegister, the device-side ncclGetPeerPointer, whose address must alias the buffer; msg then holds
+ * "window ok"), and with ncclDevCommCreate present three peer_map 1 fences as ncclLsaBarrierSession kernels ("lsa
+ * barrier fence ok").  Returns AMR_OK, AMR_E_COMM (message in msg, NUL-terminated,
  * at most msg_cap bytes) or AMR_E_CUDA. */
 amr_status amr_debug_nccl_selftest(const void* nccl_unique_id, char* msg, int32_t msg_cap);
 

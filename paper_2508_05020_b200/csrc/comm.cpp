@@ -17,6 +17,7 @@
 
 #ifdef AMR_HAVE_NCCL_H
 #include <nccl.h>
+#include <nccl_device.h>   // ncclDevComm / ncclDevCommRequirements (the LSA-barrier fence of peer_map 1)
 #endif
 
 namespace amr {
@@ -285,6 +286,9 @@ struct NcclApi {
     ncclResult_t (*MemFree)(void*) = nullptr;
     ncclResult_t (*CommWindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
     ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+    // device communicator (NCCL >= 2.28; optional: the LSA-barrier fence of peer_map 1)
+    ncclResult_t (*DevCommCreate)(ncclComm_t, const ncclDevCommRequirements_t*, ncclDevComm_t*) = nullptr;
+    ncclResult_t (*DevCommDestroy)(ncclComm_t, const ncclDevComm_t*) = nullptr;
     bool load(std::string& err) {
         if (h) return true;
         const char* env = getenv("AMR_NCCL_LIB");
@@ -310,6 +314,8 @@ struct NcclApi {
         MemFree = reinterpret_cast<decltype(MemFree)>(dlsym(h, "ncclMemFree"));
         CommWindowRegister = reinterpret_cast<decltype(CommWindowRegister)>(dlsym(h, "ncclCommWindowRegister"));
         CommWindowDeregister = reinterpret_cast<decltype(CommWindowDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
+        DevCommCreate = reinterpret_cast<decltype(DevCommCreate)>(dlsym(h, "ncclDevCommCreate"));
+        DevCommDestroy = reinterpret_cast<decltype(DevCommDestroy)>(dlsym(h, "ncclDevCommDestroy"));
         return true;
     }
 };
@@ -323,6 +329,12 @@ struct NcclTransport : Transport {
     bool windows = false;           // peer_map 1: map_peers registers NCCL symmetric windows instead of CUDA IPC
     ncclWindow_t win[2] = {nullptr, nullptr};   // per tag
     void** d_ptrs = nullptr;        // device scratch for the peer addresses read from a window
+    // peer_map 1: a device communicator with one LSA barrier, made (collectively) with the first window; when its LSA
+    // team is the whole world (one NVLink domain) the stage fence is an in-kernel LSA barrier session instead of the
+    // one-word allreduce
+    ncclDevComm dc{};
+    bool have_dc = false, lsa_fence = false;
+    long long lsa_fences = 0;       // fences issued as LSA barrier kernels (the self-test reports it)
     std::string err(ncclResult_t r) { return std::string("NCCL: ") + nccl_api().GetErrorString(r); }
     std::string p2p(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
         NcclApi& A = nccl_api();
@@ -355,6 +367,14 @@ struct NcclTransport : Transport {
         if (win[tag]) { A.CommWindowDeregister(comm, win[tag]); win[tag] = nullptr; }
         ncclResult_t r = A.CommWindowRegister(comm, base, bytes, &win[tag], NCCL_WIN_COLL_SYMMETRIC);
         if (r != ncclSuccess) { win[tag] = nullptr; return "ncclCommWindowRegister: " + std::string(A.GetErrorString(r)); }
+        if (!have_dc && A.DevCommCreate && A.DevCommDestroy) {   // collective, like the registration (same lib on all ranks)
+            ncclDevCommRequirements req{};
+            req.lsaBarrierCount = 1;
+            r = A.DevCommCreate(comm, &req, &dc);
+            if (r != ncclSuccess) return "ncclDevCommCreate: " + std::string(A.GetErrorString(r));
+            have_dc = true;
+            lsa_fence = dc.lsaSize == dc.nRanks;
+        }
         const int world = (int)out.size();
         if (!d_ptrs && cudaMalloc(&d_ptrs, 64 * sizeof(void*)) != cudaSuccess) return "window: cudaMalloc";
         if (world > 64) return "window: more than 64 ranks";
@@ -415,6 +435,11 @@ struct NcclTransport : Transport {
         return std::string();
     }
     std::string fence(cudaStream_t s) override {   // a one-word allreduce completes only after every rank reached it
+        if (windows && lsa_fence) {   // peer_map 1 in one NVLink domain: the LSA barrier session, in-kernel
+            if (launch_lsa_fence(&dc, s) != cudaSuccess) return "fence: LSA barrier kernel";
+            ++lsa_fences;
+            return std::string();
+        }
         if (!d_fence && cudaMalloc(&d_fence, sizeof(int32_t)) != cudaSuccess) return "fence: cudaMalloc";
         ncclResult_t r = nccl_api().AllReduce(d_fence, d_fence, 1, ncclInt32, ncclMax, comm, s);
         return r == ncclSuccess ? std::string() : err(r);
@@ -422,6 +447,7 @@ struct NcclTransport : Transport {
     ~NcclTransport() override {
         for (auto& v : opened)
             for (void* p : v) cudaIpcCloseMemHandle(p);
+        if (have_dc && comm) nccl_api().DevCommDestroy(comm, &dc);
         for (auto& w : win)
             if (w && comm) nccl_api().CommWindowDeregister(comm, w);
         if (d_fence) cudaFree(d_fence);
@@ -1103,6 +1129,16 @@ extern "C" amr_status amr_debug_nccl_selftest(const void* uid128, char* msg, int
                     fail(AMR_E_CUDA, "window: copy");
                 else if (std::memcmp(got.data(), h.data(), n * 8) != 0) fail(AMR_E_COMM, "window: alias does not map the buffer");
                 else win_note = "window ok";
+                // the peer_map 1 fence: an LSA barrier session in a kernel when the device communicator exists
+                if (st == AMR_OK && T->lsa_fence) {
+                    const long long f0 = T->lsa_fences;
+                    for (int k = 0; k < 3 && st == AMR_OK; ++k)
+                        if (!(x = T->fence(s)).empty()) fail(AMR_E_COMM, x);
+                    if (st == AMR_OK && cudaStreamSynchronize(s) != cudaSuccess) fail(AMR_E_CUDA, "LSA fence: sync");
+                    else if (st == AMR_OK && T->lsa_fences == f0 + 3) win_note += "; lsa barrier fence ok";
+                } else if (st == AMR_OK) {
+                    win_note += T->have_dc ? "; devcomm LSA team is not the world" : "; no ncclDevCommCreate";
+                }
             }
             if (T->win[0]) { A.CommWindowDeregister(T->comm, T->win[0]); T->win[0] = nullptr; }
             amr::comm_nccl_mem_free(wbuf);

@@ -150,6 +150,9 @@ cudaError_t launch_post_stage(const PostArgs& p, cudaStream_t s);
 // peer_map 1: every world rank's address of offset 0 of an NCCL symmetric window (win: an ncclWindow_t), read on the
 // device with ncclGetPeerPointer, into d_out[0 .. world)
 cudaError_t launch_window_peer_ptrs(const void* win, int world, void** d_out, cudaStream_t s);
+// peer_map 1: the stream-ordered cross-rank fence as an NCCL LSA barrier session in one CTA (devcomm: the host copy of
+// an ncclDevComm made by ncclDevCommCreate with lsaBarrierCount >= 1; passed to the kernel by value)
+cudaError_t launch_lsa_fence(const void* devcomm, cudaStream_t s);
 cudaError_t launch_stage(int scheme, const StageArgs& a, cudaStream_t s);
 cudaError_t launch_ghost(const ProxyTask* tasks, int ntasks, int g, const AuxArgs& a, cudaStream_t s);
 cudaError_t launch_reflux(const RefluxTask* tasks, int ntasks, const AuxArgs& a, cudaStream_t s);

@@ -2757,6 +2757,29 @@ __global__ void window_peer_ptrs_kernel(ncclWindow_t w, int world, void** out) {
 }
 #endif
 
+#ifdef AMR_HAVE_NCCL_H
+// peer_map 1 stage fence (NEXT #3: "synchronise stages with ncclLsaBarrierSession"): one CTA opens a
+// session on barrier 0 of the device communicator's LSA team and syncs -- arrive stores epoch + 1 into every peer's
+// inbox with release semantics (system scope), wait spins on this rank's inboxes with acquire -- so work queued
+// after this kernel on the stream runs after every rank's work queued before its own fence kernel, with the peers'
+// pool writes visible to this rank's loads over NVLink.  No host round trip and no NCCL collective kernel.
+__global__ void __launch_bounds__(32) lsa_fence_kernel(const ncclDevComm dc) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+#endif
+
+cudaError_t launch_lsa_fence(const void* devcomm, cudaStream_t s) {
+#ifdef AMR_HAVE_NCCL_H
+    if (!devcomm) return cudaErrorInvalidValue;
+    lsa_fence_kernel<<<1, 32, 0, s>>>(*reinterpret_cast<const ncclDevComm*>(devcomm));
+    return cudaGetLastError();
+#else
+    (void)devcomm; (void)s;
+    return cudaErrorNotSupported;
+#endif
+}
+
 cudaError_t launch_window_peer_ptrs(const void* win, int world, void** d_out, cudaStream_t s) {
 #ifdef AMR_HAVE_NCCL_H
     if (!win || world < 1 || world > 64) return cudaErrorInvalidValue;

@@ -25,3 +25,6 @@ def test_nccl_transport_selftest_one_rank():
     # peer_map 1: ncclMemAlloc + ncclCommWindowRegister + ncclGetPeerPointer (device) map the buffer
     assert "window ok" in msg.value.decode(), msg.value.decode()
 
+    # peer_map 1 fence (NEXT #3): ncclDevCommCreate with one LSA barrier, and the stage fence as an
+    # ncclLsaBarrierSession kernel (three fences issued and completed on the stream)
+    assert "lsa barrier fence ok" in msg.value.decode(), msg.value.decode()
