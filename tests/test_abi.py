@@ -110,3 +110,23 @@ def test_sass_is_sm100a(lib):
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", amr.LIB_PATH], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+@pytest.mark.parametrize("kw", [
+    dict(world_size=2, rank=0, halo_mode=2, scheme=0, patch_cells=16, stage_kernel=1, nccl_unique_id=1),  # per-tile C4
+    dict(world_size=2, rank=0, halo_mode=2, scheme=0, patch_cells=8, stage_kernel=1, nccl_unique_id=1),
+    dict(world_size=2, rank=0, halo_mode=2, scheme=0, patch_cells=32, stage_kernel=0, nccl_unique_id=1),  # TMA kernel
+    dict(world_size=2, rank=0, halo_mode=2, scheme=1, patch_cells=16, stage_kernel=0, nccl_unique_id=1),  # WENO5
+])
+def test_halo_mode2_configs_pass_validation(lib, kw):
+    """halo_mode 2 needs a stage kernel that loads remote face strips itself: these pass the config check (on a
+    CPU-only box amr_create then fails later, at the device / communicator, never with AMR_E_CONFIG)."""
+    import torch
+    if torch.cuda.is_available():   # a GPU box would go on to a 2-rank NCCL init that waits for the missing rank
+        pytest.skip("CPU-only check")
+    c = _cfg(lib, **kw)
+    h = C.c_void_p()
+    rc = lib.amr_create(C.byref(c), C.byref(h))
+    if h.value:
+        lib.amr_destroy(h)
+    assert rc not in (amr.AMR_E_CONFIG, amr.AMR_E_ARG), (rc, lib.amr_last_error(None))
