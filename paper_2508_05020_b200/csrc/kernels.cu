@@ -1719,15 +1719,36 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 
     const int seg_line = lane & 3, seg = lane < 28 ? lane >> 2 : 6;
     const bool seg_store = lane < 28;
+    // N = 8: the L_x / L_y planes are column-swizzled (odd tile rows: column ^ 8), see the cell mapping below
+    constexpr int SWZ = N == 8 ? 8 : 0;
     // interior / epilogue cells c = tid + 512 r: member m, in-member index w, tile position (ci[r], cj[r])
     int cm[2], cw[2], ci[2], cj[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         const int c = tid + 512 * r;
-        cm[r] = c / NN;
-        cw[r] = c - cm[r] * NN;
-        ci[r] = gm_x(cm[r]) * N + cw[r] % N;
-        cj[r] = gm_y(cm[r]) * N + cw[r] / N;
+        if (N == 8) {
+            // a half-warp (16 cells, 8-byte accesses) takes four 4-cell chunks of two x-neighbour members P, Q at rows
+            // r0, r0 + 1 (r0 even): P r0 [0,4), P r0 [4,8), P r0+1 [0,4), Q r0+1 [4,8) -- the other half-warp of the
+            // warp the same with P, Q swapped -- so that its accesses hit 16 distinct bank pairs on the member-major
+            // landing (member stride = 0 mod 16 doubles: 8 row + col), on the prim planes (stride 44: 12 row + 8 X
+            // + col) and on the swizzled L planes (stride 36: 4 row + 8 X + col, + 8 on odd rows); the member-major
+            // mapping (two rows of one member) had 2-way conflicts on the latter two
+            const int H = c >> 4, l = c & 15, unit = H >> 1, second = H & 1;
+            const int pr = unit >> 2, r0 = 2 * (unit & 3);
+            const int XA = 2 * (pr & 1), Y = pr >> 1;
+            const int XP = XA + second, XQ = XA + 1 - second;
+            const int ch = l >> 2, e = l & 3;
+            const int X = ch == 3 ? XQ : XP, row = r0 + (ch >> 1), col = (ch == 1 || ch == 3 ? 4 : 0) + e;
+            cm[r] = gm_of(X, Y);
+            cw[r] = row * N + col;
+            ci[r] = X * N + col;
+            cj[r] = Y * N + row;
+        } else {
+            cm[r] = c / NN;
+            cw[r] = c - cm[r] * NN;
+            ci[r] = gm_x(cm[r]) * N + cw[r] % N;
+            cj[r] = gm_y(cm[r]) * N + cw[r] / N;
+        }
     }
     unsigned long long lam = 0ull;
     int k = 0;
@@ -1827,7 +1848,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     for (int e = 0; e < 5; ++e)
                         if (m0 + e >= 0 && m0 + e < T)
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) dUx[(q * T + j) * FXS + m0 + e] = -(Fh[e + 1][q] - Fh[e][q]) * idx;
+                            for (int q = 0; q < 4; ++q)
+                                dUx[(q * T + j) * FXS + ((m0 + e) ^ ((j & 1) * SWZ))] = -(Fh[e + 1][q] - Fh[e][q]) * idx;
                     const int r = j / N;
                     const LeafDesc& dw = D[gm_of(0, r)];
                     const LeafDesc& de = D[gm_of(B - 1, r)];
@@ -1850,7 +1872,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #pragma unroll
                     for (int e = 0; e < 5; ++e)
                         if (m0 + e >= 0 && m0 + e < T) {
-                            double* o = dUy + (m0 + e) * FYS + i;
+                            double* o = dUy + (m0 + e) * FYS + (i ^ (((m0 + e) & 1) * SWZ));
                             o[0 * T * FYS] = -(Fh[e + 1][0] - Fh[e][0]) * idy;
                             o[1 * T * FYS] = -(Fh[e + 1][2] - Fh[e][2]) * idy;
                             o[2 * T * FYS] = -(Fh[e + 1][1] - Fh[e][1]) * idy;
@@ -1887,7 +1909,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         for (int r = 0; r < 2; ++r) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const int o = (q * T + cj[r]) * FXS + ci[r];
+                const int o = (q * T + cj[r]) * FXS + (ci[r] ^ ((cj[r] & 1) * SWZ));
                 const double Lr = dUx[o] + dUy[o];
                 double v = uc[r][q] + dt * Lr;
                 double* su = sU + cm[r] * 4 * NN + q * NN + cw[r];
